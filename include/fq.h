@@ -1,0 +1,148 @@
+/*
+ * fq.h — C ABI of the B200 (sm_100a) FineQuant hot path.
+ *
+ * FineQuant (arXiv 2308.09723): weight-only, symmetric, linear-absmax, group-wise quantization
+ * of a weight matrix to int4 / int8 codes with per-group scales in the activation dtype, the
+ * paper's adaptive group-size heuristic, and a fused "dequantize on the fly" GEMM of fp16/bf16
+ * activations with those codes.  Citations "P:<line> §x" point into the paper text.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  Shapes.  The paper's weight matrix W has K rows (reduction dim) and N columns (outputs);
+ *    "each contiguous block of B elements in a given column has its own scaling factor"
+ *    (§4.1).  W is STORED like torch nn.Linear.weight: [N, K] row-major, so paper column n
+ *    is the contiguous row n.  G = K / group.
+ *  Canonical packed layout (bit-exact contract):
+ *    codes  [N, K*bits/8] bytes, K contiguous per column n.
+ *           int4: byte (n, k/2) = (q[n,k] & 0xF) | (q[n,k+1] & 0xF) << 4  (k even; two's complement)
+ *           int8: byte (n, k)   = (uint8_t) q[n,k]
+ *    scales [G, N] row-major, dtype = scale_dtype (the activation dtype, §4.1).
+ *  Memory.  Every tensor argument is a caller-owned DEVICE pointer unless documented as host.
+ *    The library never allocates device memory; scratch is the caller's `ws`.
+ *  Streams.  `stream` is a cudaStream_t passed as void*; all work is enqueued on it
+ *    asynchronously.  NULL = legacy default stream.
+ *  Errors.  Argument/shape validation is synchronous and happens before any launch, so a call
+ *    that returns != FQ_OK has written nothing.  Launch failures return FQ_ERR_CUDA.  Data-
+ *    dependent conditions the host cannot see (non-finite W, fp16 scale overflow) are reported
+ *    through the optional device status word (bit 0: non-finite input in a group, bit 1: scale
+ *    overflow); affected groups get scale 0 and codes 0.  No C++ exception crosses the ABI.
+ *  Thread safety.  All functions are re-entrant; the only global state is a lazily cached
+ *    device-properties struct.
+ */
+#ifndef FQ_H_
+#define FQ_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FQ_OK = 0,
+  FQ_ERR_INVALID_ARG = 1, /* null pointer, alpha out of range, bad dtype enum */
+  FQ_ERR_SHAPE = 2,       /* K/N/M/group inconsistent or misaligned */
+  FQ_ERR_UNSUPPORTED = 3, /* bits not in {4,8}; dtype combination without a kernel */
+  FQ_ERR_WORKSPACE = 4,   /* ws too small (see fq_gemm_workspace_bytes) */
+  FQ_ERR_CUDA = 5         /* a CUDA launch / runtime call failed */
+} fq_status;
+
+typedef enum { FQ_BF16 = 0, FQ_FP16 = 1, FQ_FP32 = 2 } fq_dtype;
+
+/* Description of one quantized weight matrix. */
+typedef struct {
+  int64_t K;           /* reduction dim (paper rows); K % 32 == 0 */
+  int64_t N;           /* outputs (paper columns); N % 8 == 0 */
+  int32_t bits;        /* 4 or 8 ("int8 or int4 weights") */
+  int32_t group;       /* group size along K; group % 16 == 0 and K % group == 0; group == K is
+                          per-column (§3.2.1, App. B) */
+  int32_t scale_dtype; /* fq_dtype of the scales: FQ_BF16 or FQ_FP16 (activation dtype) */
+  int32_t reserved;    /* must be 0 */
+} fq_wdesc;
+
+/* Library version string. */
+const char* fq_version(void);
+/* Human-readable name of a status code (static storage). */
+const char* fq_status_str(fq_status s);
+
+/* Byte sizes of the canonical buffers (0 on invalid arguments).
+ * fq_codes_bytes = N*K*bits/8 ; fq_scales_bytes = (K/group)*N*sizeof(scale dtype). */
+size_t fq_codes_bytes(int64_t K, int64_t N, int32_t bits);
+size_t fq_scales_bytes(int64_t K, int64_t N, int32_t group, int32_t scale_dtype);
+
+/* ---------------------------------------------------------------------------------------------
+ * Adaptive fine-grained group size (§3.3).  "we start from the column-wise quantization
+ * and compute the range ... We then halve the quantization group size and compute the range of
+ * each group.  If for any group [the ratio test fires] we halve the quantization group size
+ * again."  Reading (R6): level L >= 1 fires iff some group has
+ *   1000 * max|child| < alpha_milli * max|parent|,
+ * levels are accepted while they fire; the result is the group of the last accepted level.
+ * Ladder (R9): g_0 = K, g_{L+1} = g_L/2 while g_L is even, g_L/2 >= min_group, g_L/2 % 16 == 0.
+ * The decision is split in two so that tensor-parallel callers can OR the flags of all shards
+ * (all-reduce MAX) between the device pass and the host decision.
+ * ------------------------------------------------------------------------------------------- */
+
+/* Number of ladder levels including level 0 (= K); flags arrays have fq_adapt_levels()-1 ints.
+ * Returns 0 on invalid arguments. */
+int32_t fq_adapt_levels(int64_t K, int32_t min_group);
+/* Group size of ladder level `level` (0 = K); 0 on invalid arguments. */
+int32_t fq_adapt_group_at(int64_t K, int32_t min_group, int32_t level);
+
+/* Device pass (kernel A1): for W [N, K] (dtype wdt in {BF16, FP16, FP32}), OR-accumulates into
+ * flags_dev[L-1] (L = 1 .. levels-1) whether level L fires.  flags_dev must be zeroed by the
+ * caller before the first contributing call (several calls on row blocks / shards may
+ * accumulate into the same flags).  alpha_milli in [1, 1000].  status_dev (nullable) gets bit 0
+ * if W holds a non-finite value. */
+fq_status fq_adapt_flags(const void* W, int32_t wdt, int64_t K, int64_t N, uint32_t alpha_milli,
+                         int32_t min_group, int32_t* flags_dev, int32_t* status_dev, void* stream);
+
+/* Host decision (A2): flags_host = the (levels-1) flags copied back from the device. */
+int32_t fq_adapt_decide(int64_t K, int32_t min_group, const int32_t* flags_host);
+
+/* ---------------------------------------------------------------------------------------------
+ * Quantize + pack (kernel A3), App. A with groups:
+ *   s[j,n] = RNE_scale_dtype( 2 * max_{k in group j} |W[n,k]| / (2^bits - 1) )   (one rounding)
+ *   q[n,k] = clamp( round_half_away( W[n,k] / s[k/group, n] ), -2^(bits-1), 2^(bits-1)-1 ),
+ *            q = 0 where s == 0.
+ * W: [N, K] device, dtype wdt.  codes/scales: device outputs in the canonical layout.
+ * status_dev: nullable device int32, OR-ed with bit 0 (non-finite W) / bit 1 (scale overflow).
+ * ------------------------------------------------------------------------------------------- */
+fq_status fq_quantize(const void* W, int32_t wdt, const fq_wdesc* d, void* codes, void* scales,
+                      int32_t* status_dev, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * Fused dequantize + GEMM (kernels A4/A5 for M <= 16, A6 for large M), §4.1:
+ *   C[m,n] = sum_k A[m,k] * q[n,k] * s[k/group, n]
+ * A: [M, K] row-major, dtype adt in {BF16, FP16}; the scales must have dtype adt.
+ * C: [M, N] row-major, dtype cdt in {adt, FP32} (FP32 is a diagnostic mode).
+ * ws/ws_bytes: device scratch of at least fq_gemm_workspace_bytes(M, d) bytes.  The workspace
+ *   holds split-K partials and arrival counters: it must be ZERO-FILLED once before its first
+ *   use; every call leaves the counters zeroed again, so it can be reused (and graph-captured)
+ *   without re-clearing.  Calls sharing one ws must be stream-ordered.
+ * Accumulation is fp32; results are deterministic (fixed-order split-K reduction).
+ * ------------------------------------------------------------------------------------------- */
+size_t fq_gemm_workspace_bytes(int64_t M, const fq_wdesc* d);
+fq_status fq_gemm(const void* A, int32_t adt, int64_t M, const fq_wdesc* d, const void* codes,
+                  const void* scales, void* C, int32_t cdt, void* ws, size_t ws_bytes,
+                  void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * MoE expert batch (kernel A7).  E experts share K, N, bits and scale dtype (d->group ignored);
+ * each expert has its own group size (adaptive per expert, "different model weight
+ * matrices"; MoE experts P:166-167).  Tokens are sorted by expert:
+ *   rows offsets[e] .. offsets[e+1]-1 of A ([T, K]) use expert e; C is [T, N].
+ * offsets_host: HOST array of E+1 int64 (non-decreasing, offsets[0] = 0, offsets[E] = T).
+ * codes_dev / scales_dev: DEVICE arrays of E device pointers; groups_host: HOST array of E group
+ * sizes (each valid for K).  ws: fq_gemm_grouped_workspace_bytes(...) bytes, zero-filled once.
+ * ------------------------------------------------------------------------------------------- */
+size_t fq_gemm_grouped_workspace_bytes(int64_t T, int32_t E, const fq_wdesc* d);
+fq_status fq_gemm_grouped(const void* A, int32_t adt, int64_t T, const int64_t* offsets_host,
+                          int32_t E, const fq_wdesc* d, const int32_t* groups_host,
+                          const void* const* codes_dev, const void* const* scales_dev, void* C,
+                          int32_t cdt, void* ws, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FQ_H_ */

@@ -1,0 +1,160 @@
+// fq_api.cu — the C ABI (include/fq.h): argument validation, sizing, dispatch to the kernels.
+// No compute happens here; every step of the hot path runs in the sm_100a kernels.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+
+#include "../../include/fq.h"
+#include "fq_internal.h"
+
+namespace fq {
+
+int num_sms() {
+  static std::atomic<int> cached{0};
+  int v = cached.load();
+  if (v) return v;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+  cached.store(v);
+  return v;
+}
+
+static bool valid_dtype(int d) { return d == FQ_BF16 || d == FQ_FP16 || d == FQ_FP32; }
+static bool valid_half(int d) { return d == FQ_BF16 || d == FQ_FP16; }
+
+static fq_status check_wdesc(const fq_wdesc* d) {
+  if (!d) return FQ_ERR_INVALID_ARG;
+  if (d->reserved != 0 || !valid_half(d->scale_dtype)) return FQ_ERR_INVALID_ARG;
+  if (d->bits != 4 && d->bits != 8) return FQ_ERR_UNSUPPORTED;
+  if (d->K <= 0 || d->N <= 0 || d->K % 32 || d->N % 8) return FQ_ERR_SHAPE;
+  if (d->K > (int64_t)1 << 20 || d->N > (int64_t)1 << 24) return FQ_ERR_SHAPE;
+  if (d->group <= 0 || d->group % 16 || d->K % d->group) return FQ_ERR_SHAPE;
+  return FQ_OK;
+}
+
+static cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+static fq_status from_cuda(cudaError_t e) { return e == cudaSuccess ? FQ_OK : FQ_ERR_CUDA; }
+
+}  // namespace fq
+
+using namespace fq;
+
+extern "C" {
+
+const char* fq_version(void) { return "fq 0.1.0 (sm_100a)"; }
+
+const char* fq_status_str(fq_status s) {
+  switch (s) {
+    case FQ_OK: return "FQ_OK";
+    case FQ_ERR_INVALID_ARG: return "FQ_ERR_INVALID_ARG";
+    case FQ_ERR_SHAPE: return "FQ_ERR_SHAPE";
+    case FQ_ERR_UNSUPPORTED: return "FQ_ERR_UNSUPPORTED";
+    case FQ_ERR_WORKSPACE: return "FQ_ERR_WORKSPACE";
+    case FQ_ERR_CUDA: return "FQ_ERR_CUDA";
+  }
+  return "FQ_ERR_UNKNOWN";
+}
+
+size_t fq_codes_bytes(int64_t K, int64_t N, int32_t bits) {
+  if (K <= 0 || N <= 0 || (bits != 4 && bits != 8) || (K * bits) % 8) return 0;
+  return (size_t)(N * (K * bits / 8));
+}
+
+size_t fq_scales_bytes(int64_t K, int64_t N, int32_t group, int32_t sdt) {
+  if (K <= 0 || N <= 0 || group <= 0 || K % group || !valid_half(sdt)) return 0;
+  return (size_t)((K / group) * N * 2);
+}
+
+int32_t fq_adapt_levels(int64_t K, int32_t min_group) {
+  if (K <= 0 || min_group <= 0 || K % 16) return 0;
+  int32_t n = 1;
+  int64_t g = K;
+  while (g % 2 == 0 && g / 2 >= min_group && (g / 2) % 16 == 0) {
+    g /= 2;
+    ++n;
+  }
+  return n;
+}
+
+int32_t fq_adapt_group_at(int64_t K, int32_t min_group, int32_t level) {
+  const int32_t n = fq_adapt_levels(K, min_group);
+  if (n == 0 || level < 0 || level >= n) return 0;
+  return (int32_t)(K >> level);
+}
+
+int32_t fq_adapt_decide(int64_t K, int32_t min_group, const int32_t* flags_host) {
+  const int32_t n = fq_adapt_levels(K, min_group);
+  if (n == 0) return 0;
+  int64_t g = K;
+  for (int32_t L = 1; L < n; ++L) {
+    if (!flags_host || !flags_host[L - 1]) break;
+    g = K >> L;
+  }
+  return (int32_t)g;
+}
+
+fq_status fq_adapt_flags(const void* W, int32_t wdt, int64_t K, int64_t N, uint32_t alpha_milli,
+                         int32_t min_group, int32_t* flags_dev, int32_t* status_dev,
+                         void* stream) {
+  if (!W || !flags_dev || !valid_dtype(wdt)) return FQ_ERR_INVALID_ARG;
+  if (alpha_milli < 1 || alpha_milli > 1000 || min_group < 16) return FQ_ERR_INVALID_ARG;
+  if (K <= 0 || N <= 0 || K % 32 || K > (1 << 20) || N > (1 << 24)) return FQ_ERR_SHAPE;
+  const int32_t nlev = fq_adapt_levels(K, min_group);
+  if (nlev <= 0 || nlev > 16) return FQ_ERR_SHAPE;
+  const int gfin = (int)(K >> (nlev - 1));
+  if (gfin % 8) return FQ_ERR_SHAPE;
+  if (nlev == 1) return FQ_OK;  // nothing to test
+  return from_cuda(run_adapt_flags(wdt, W, (int)K, (int)N, nlev, gfin, alpha_milli, flags_dev,
+                                   status_dev, as_stream(stream)));
+}
+
+fq_status fq_quantize(const void* W, int32_t wdt, const fq_wdesc* d, void* codes, void* scales,
+                      int32_t* status_dev, void* stream) {
+  fq_status s = check_wdesc(d);
+  if (s != FQ_OK) return s;
+  if (!W || !codes || !scales || !valid_dtype(wdt)) return FQ_ERR_INVALID_ARG;
+  return from_cuda(run_quantize(wdt, d->scale_dtype, d->bits, W, (int)d->K, (int)d->N, d->group,
+                                codes, scales, status_dev, as_stream(stream)));
+}
+
+size_t fq_gemm_workspace_bytes(int64_t M, const fq_wdesc* d) {
+  if (check_wdesc(d) != FQ_OK || M <= 0) return 0;
+  const GemvPlan p = plan_gemv((int)M, (int)d->K, (int)d->N, d->bits, d->group, num_sms());
+  return gemv_workspace_bytes(p, (int)M, (int)d->N);
+}
+
+fq_status fq_gemm(const void* A, int32_t adt, int64_t M, const fq_wdesc* d, const void* codes,
+                  const void* scales, void* C, int32_t cdt, void* ws, size_t ws_bytes,
+                  void* stream) {
+  fq_status s = check_wdesc(d);
+  if (s != FQ_OK) return s;
+  if (!A || !codes || !scales || !C || !valid_half(adt)) return FQ_ERR_INVALID_ARG;
+  if (d->scale_dtype != adt) return FQ_ERR_UNSUPPORTED;
+  if (cdt != adt && cdt != FQ_FP32) return FQ_ERR_UNSUPPORTED;
+  if (M <= 0 || M > (1 << 20)) return FQ_ERR_SHAPE;
+  const GemvPlan p = plan_gemv((int)M, (int)d->K, (int)d->N, d->bits, d->group, num_sms());
+  if (p.splits > 1 && (!ws || ws_bytes < gemv_workspace_bytes(p, (int)M, (int)d->N)))
+    return FQ_ERR_WORKSPACE;
+  return from_cuda(run_gemv(p, adt, cdt, d->bits, A, (int)M, (int)d->K, (int)d->N, codes, scales,
+                            d->group, C, ws, as_stream(stream)));
+}
+
+size_t fq_gemm_grouped_workspace_bytes(int64_t T, int32_t E, const fq_wdesc* d) {
+  (void)T; (void)E; (void)d;
+  return 0;
+}
+
+fq_status fq_gemm_grouped(const void* A, int32_t adt, int64_t T, const int64_t* offsets_host,
+                          int32_t E, const fq_wdesc* d, const int32_t* groups_host,
+                          const void* const* codes_dev, const void* const* scales_dev, void* C,
+                          int32_t cdt, void* ws, size_t ws_bytes, void* stream) {
+  (void)A; (void)adt; (void)T; (void)offsets_host; (void)E; (void)d; (void)groups_host;
+  (void)codes_dev; (void)scales_dev; (void)C; (void)cdt; (void)ws; (void)ws_bytes; (void)stream;
+  return FQ_ERR_UNSUPPORTED;
+}
+
+}  // extern "C"

@@ -1,0 +1,31 @@
+// fq_internal.h — launchers exported by the kernel translation units to the C-ABI layer.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fq {
+
+cudaError_t run_quantize(int wdt, int sdt, int bits, const void* W, int K, int N, int group,
+                         void* codes, void* scales, int32_t* status, cudaStream_t st);
+cudaError_t run_adapt_flags(int wdt, const void* W, int K, int N, int nlev, int gfin,
+                            uint32_t alpha, int32_t* flags, int32_t* status, cudaStream_t st);
+
+// Decode / tensor-core-fallback GEMM (mma.sync, kernels A4/A5).
+struct GemvPlan {
+  int rows_per_cta;   // 128 * RT
+  int rt;             // row tiles (16 rows) per warp
+  int splits;         // split-K factor S
+  int kchunk;         // K elements per chunk (128 int4, 64 int8)
+  int ktiles;         // token tiles of 16 (gridDim.z)
+  int mt;             // 8-token MMA tiles per token tile (1 or 2)
+  int klen;           // K elements per split (multiple of kchunk)
+};
+GemvPlan plan_gemv(int M, int K, int N, int bits, int group, int num_sms);
+size_t gemv_workspace_bytes(const GemvPlan& p, int M, int N);
+cudaError_t run_gemv(const GemvPlan& p, int adt, int cdt, int bits, const void* A, int M, int K,
+                     int N, const void* codes, const void* scales, int group, void* C, void* ws,
+                     cudaStream_t st);
+
+int num_sms();
+
+}  // namespace fq

@@ -1,0 +1,292 @@
+// fq_quant.cu — kernels A1 (adaptive range pyramid + level flags) and A3 (scale, quantize, pack).
+//
+// A3 follows App. A: s = 2*max|A_group|/(2^b-1), Q = integer(A/s), with groups of
+// `group` contiguous elements along K of each paper column (§4.1), scales stored in the
+// activation dtype.  Arithmetic contract (bit-exact with the oracle):
+//   * amax is exact;  s = RNE_dtype((double)(2*amax) / (2^b-1)) — the double quotient can never sit
+//     on a bf16/fp16 tie, so this equals one rounding of the exact rational (R4);
+//   * q = roundf(__fdiv_rn(x, s)) for bf16/fp16 inputs (exact decision: x has <= 11 significant
+//     bits), round((double)x/(double)s) for fp32 inputs; clamp to [-2^(b-1), 2^(b-1)-1].
+// A1 follows P:147-149 §3.3 under reading R6: level L fires iff some child group range is below
+// alpha * its parent's range, compared exactly as 1000*child < alpha_milli*parent in fp64.
+//
+// Layout: one CTA per paper column n (= row n of the stored [N, K] matrix).  Pass 1 streams the
+// row once from HBM with 16-byte loads and writes one max|.| per 8-element chunk to shared memory;
+// pass 2 reduces chunks to groups; pass 3 re-reads the row (L2-resident: the CTA just read it),
+// computes codes and writes them coalesced.  HBM traffic = read W once + write codes/scales.
+#include "fq_common.cuh"
+#include "fq_internal.h"
+
+namespace fq {
+
+template <typename TIn>
+struct Chunk8 {
+  float v[8];
+  __device__ __forceinline__ void load(const TIn* p);
+};
+template <>
+__device__ __forceinline__ void Chunk8<__nv_bfloat16>::load(const __nv_bfloat16* p) {
+  uint4 r = ldg_keep(p);
+  uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    v[2 * i] = __uint_as_float(w[i] << 16);
+    v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+  }
+}
+template <>
+__device__ __forceinline__ void Chunk8<__half>::load(const __half* p) {
+  uint4 r = ldg_keep(p);
+  const __half2* h = reinterpret_cast<const __half2*>(&r);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 f = __half22float2(h[i]);
+    v[2 * i] = f.x;
+    v[2 * i + 1] = f.y;
+  }
+}
+template <>
+__device__ __forceinline__ void Chunk8<float>::load(const float* p) {
+  uint4 a = ldg_keep(p), b = ldg_keep(p + 4);
+  v[0] = __uint_as_float(a.x); v[1] = __uint_as_float(a.y);
+  v[2] = __uint_as_float(a.z); v[3] = __uint_as_float(a.w);
+  v[4] = __uint_as_float(b.x); v[5] = __uint_as_float(b.y);
+  v[6] = __uint_as_float(b.z); v[7] = __uint_as_float(b.w);
+}
+
+// max|x| over a chunk; +inf if any element is non-finite (the group is then flagged).
+__device__ __forceinline__ float chunk_amax(const float (&v)[8]) {
+  float m = 0.f;
+  bool fin = true;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    fin &= isfinite(v[i]);
+    m = fmaxf(m, fabsf(v[i]));
+  }
+  return fin ? m : __int_as_float(0x7f800000);
+}
+
+constexpr int kQThreads = 256;
+
+// ------------------------------------------------------------------------------------- A3
+template <typename TIn, typename TS, int BITS>
+__global__ void __launch_bounds__(kQThreads) quantize_kernel(const TIn* __restrict__ W, int K,
+                                                             int N, int group,
+                                                             uint8_t* __restrict__ codes,
+                                                             TS* __restrict__ scales,
+                                                             int32_t* __restrict__ status) {
+  extern __shared__ float smem[];
+  const int nchunk = K >> 3;
+  const int G = K / group;
+  const int cpg = group >> 3;  // chunks per group
+  float* pm = smem;            // [nchunk]
+  float* sc = smem + nchunk;   // [G] scale as float (0 => codes 0)
+  __shared__ int s_status;
+  const int n = blockIdx.x;
+  const TIn* row = W + (size_t)n * K;
+  if (threadIdx.x == 0) s_status = 0;
+
+  // pass 1: chunk maxima
+  for (int c = threadIdx.x; c < nchunk; c += kQThreads) {
+    Chunk8<TIn> ch;
+    ch.load(row + (size_t)c * 8);
+    pm[c] = chunk_amax(ch.v);
+  }
+  __syncthreads();
+
+  // pass 2: group maxima -> scales
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto finish_group = [&](int j, float amax) {
+    int st = 0;
+    float s = 0.f;
+    TS s_t;
+    if (!isfinite(amax)) {
+      st |= 1;
+      s_t = Dt<TS>::from_f(0.f);
+    } else {
+      s_t = Dt<TS>::from_d(2.0 * (double)amax / (double)((1 << BITS) - 1));
+      s = Dt<TS>::to_f(s_t);
+      if (!isfinite(s)) {
+        st |= 2;
+        s = 0.f;
+        s_t = Dt<TS>::from_f(0.f);
+      }
+    }
+    sc[j] = s;
+    scales[(size_t)j * N + n] = s_t;
+    if (st) atomicOr(&s_status, st);
+  };
+  if (cpg <= 32) {
+    for (int j = threadIdx.x; j < G; j += kQThreads) {
+      float m = 0.f;
+      for (int i = 0; i < cpg; ++i) m = fmaxf(m, pm[j * cpg + i]);  // fmaxf keeps +inf
+      finish_group(j, m);
+    }
+  } else {
+    for (int j = warp; j < G; j += kQThreads / 32) {
+      float m = 0.f;
+      for (int i = lane; i < cpg; i += 32) m = fmaxf(m, pm[j * cpg + i]);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (lane == 0) finish_group(j, m);
+    }
+  }
+  __syncthreads();
+
+  // pass 3: codes
+  constexpr int lo = -(1 << (BITS - 1)), hi = (1 << (BITS - 1)) - 1;
+  for (int c = threadIdx.x; c < nchunk; c += kQThreads) {
+    Chunk8<TIn> ch;
+    ch.load(row + (size_t)c * 8);
+    const float s = sc[c / cpg];
+    int q[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float r;
+      if (s == 0.f) {
+        r = 0.f;
+      } else if (Dt<TIn>::id == FQ_FP32) {
+        r = (float)round((double)ch.v[i] / (double)s);
+      } else {
+        r = roundf(__fdiv_rn(ch.v[i], s));
+      }
+      r = fminf(fmaxf(r, (float)lo), (float)hi);
+      q[i] = (int)r;
+    }
+    if (BITS == 4) {
+      uint32_t w = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) w |= (uint32_t)(q[i] & 0xF) << (4 * i);
+      reinterpret_cast<uint32_t*>(codes + (size_t)n * (K / 2))[c] = w;
+    } else {
+      uint2 w;
+      w.x = (q[0] & 0xFF) | (q[1] & 0xFF) << 8 | (q[2] & 0xFF) << 16 | (uint32_t)(q[3] & 0xFF) << 24;
+      w.y = (q[4] & 0xFF) | (q[5] & 0xFF) << 8 | (q[6] & 0xFF) << 16 | (uint32_t)(q[7] & 0xFF) << 24;
+      reinterpret_cast<uint2*>(codes + (size_t)n * K)[c] = w;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && s_status && status) atomicOr(status, s_status);
+}
+
+// ------------------------------------------------------------------------------------- A1
+// Per column: chunk maxima -> finest-level group maxima -> pairwise up the ladder (each level is
+// an exact halving of the one above, so parent(j) = j/2) -> OR of the level flags.
+constexpr int kMaxLevels = 16;
+
+template <typename TIn>
+__global__ void __launch_bounds__(kQThreads) adapt_flags_kernel(const TIn* __restrict__ W, int K,
+                                                                int N, int nlev, int gfin,
+                                                                uint32_t alpha_milli,
+                                                                int32_t* __restrict__ flags,
+                                                                int32_t* __restrict__ status) {
+  extern __shared__ float smem[];
+  const int nchunk = K >> 3;
+  const int Gf = K / gfin;
+  float* pm = smem;               // [nchunk]
+  float* lev = smem + nchunk;     // levels finest..0 packed: offsets below
+  __shared__ int s_flag[kMaxLevels];
+  __shared__ int s_status;
+  if (threadIdx.x < kMaxLevels) s_flag[threadIdx.x] = 0;
+  if (threadIdx.x == 0) s_status = 0;
+  const int n = blockIdx.x;
+  const TIn* row = W + (size_t)n * K;
+  for (int c = threadIdx.x; c < nchunk; c += kQThreads) {
+    Chunk8<TIn> ch;
+    ch.load(row + (size_t)c * 8);
+    pm[c] = chunk_amax(ch.v);
+  }
+  __syncthreads();
+  // finest level L = nlev-1 stored at lev[0 .. Gf)
+  const int cpg = gfin >> 3;
+  for (int j = threadIdx.x; j < Gf; j += kQThreads) {
+    float m = 0.f;
+    for (int i = 0; i < cpg; ++i) m = fmaxf(m, pm[j * cpg + i]);
+    lev[j] = m;
+  }
+  __syncthreads();
+  // coarser levels: level L has Gf >> (nlev-1-L) groups; offset off(L) accumulates.
+  int off_child = 0, cnt_child = Gf;
+  for (int L = nlev - 2; L >= 0; --L) {
+    const int off_par = off_child + cnt_child, cnt_par = cnt_child >> 1;
+    for (int j = threadIdx.x; j < cnt_par; j += kQThreads)
+      lev[off_par + j] = fmaxf(lev[off_child + 2 * j], lev[off_child + 2 * j + 1]);
+    __syncthreads();
+    // flag for child level L+1 against parent level L
+    bool fire = false;
+    for (int j = threadIdx.x; j < cnt_child; j += kQThreads) {
+      const double ch = lev[off_child + j], pa = lev[off_par + (j >> 1)];
+      fire |= (1000.0 * ch < (double)alpha_milli * pa);
+    }
+    if (__syncthreads_or(fire) && threadIdx.x == 0) s_flag[L + 1] = 1;
+    off_child = off_par;
+    cnt_child = cnt_par;
+  }
+  if (threadIdx.x == 0 && !isfinite(lev[off_child])) s_status = 1;
+  __syncthreads();
+  if (threadIdx.x >= 1 && threadIdx.x < nlev && s_flag[threadIdx.x]) atomicOr(&flags[threadIdx.x - 1], 1);
+  if (threadIdx.x == 0 && s_status && status) atomicOr(status, 1);
+}
+
+// ------------------------------------------------------------------------------------- launchers
+template <typename TIn, typename TS, int BITS>
+static cudaError_t launch_quant(const void* W, int K, int N, int group, void* codes, void* scales,
+                                int32_t* status, cudaStream_t st) {
+  const size_t smem = (size_t)(K / 8 + K / group) * sizeof(float);
+  auto kern = quantize_kernel<TIn, TS, BITS>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  kern<<<N, kQThreads, smem, st>>>((const TIn*)W, K, N, group, (uint8_t*)codes, (TS*)scales, status);
+  return cudaGetLastError();
+}
+
+template <typename TIn, typename TS>
+static cudaError_t launch_quant_b(int bits, const void* W, int K, int N, int group, void* codes,
+                                  void* scales, int32_t* status, cudaStream_t st) {
+  return bits == 4 ? launch_quant<TIn, TS, 4>(W, K, N, group, codes, scales, status, st)
+                   : launch_quant<TIn, TS, 8>(W, K, N, group, codes, scales, status, st);
+}
+
+template <typename TIn>
+static cudaError_t launch_quant_s(int sdt, int bits, const void* W, int K, int N, int group,
+                                  void* codes, void* scales, int32_t* status, cudaStream_t st) {
+  return sdt == FQ_BF16
+             ? launch_quant_b<TIn, __nv_bfloat16>(bits, W, K, N, group, codes, scales, status, st)
+             : launch_quant_b<TIn, __half>(bits, W, K, N, group, codes, scales, status, st);
+}
+
+cudaError_t run_quantize(int wdt, int sdt, int bits, const void* W, int K, int N, int group,
+                         void* codes, void* scales, int32_t* status, cudaStream_t st) {
+  switch (wdt) {
+    case FQ_BF16: return launch_quant_s<__nv_bfloat16>(sdt, bits, W, K, N, group, codes, scales, status, st);
+    case FQ_FP16: return launch_quant_s<__half>(sdt, bits, W, K, N, group, codes, scales, status, st);
+    default: return launch_quant_s<float>(sdt, bits, W, K, N, group, codes, scales, status, st);
+  }
+}
+
+template <typename TIn>
+static cudaError_t launch_adapt(const void* W, int K, int N, int nlev, int gfin, uint32_t alpha,
+                                int32_t* flags, int32_t* status, cudaStream_t st) {
+  const int Gf = K / gfin;
+  const size_t smem = (size_t)(K / 8 + 2 * Gf) * sizeof(float);
+  auto kern = adapt_flags_kernel<TIn>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  kern<<<N, kQThreads, smem, st>>>((const TIn*)W, K, N, nlev, gfin, alpha, flags, status);
+  return cudaGetLastError();
+}
+
+cudaError_t run_adapt_flags(int wdt, const void* W, int K, int N, int nlev, int gfin,
+                            uint32_t alpha, int32_t* flags, int32_t* status, cudaStream_t st) {
+  switch (wdt) {
+    case FQ_BF16: return launch_adapt<__nv_bfloat16>(W, K, N, nlev, gfin, alpha, flags, status, st);
+    case FQ_FP16: return launch_adapt<__half>(W, K, N, nlev, gfin, alpha, flags, status, st);
+    default: return launch_adapt<float>(W, K, N, nlev, gfin, alpha, flags, status, st);
+  }
+}
+
+}  // namespace fq

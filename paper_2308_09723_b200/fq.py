@@ -1,0 +1,233 @@
+"""Thin Python binding of libfq.so (include/fq.h).  Argument marshalling only.
+
+The `fq_*` functions mirror the C ABI one to one (same names, same arguments, torch tensors in
+place of device pointers).  `quantize()` / `gemm()` / `gemm_grouped()` are the user-facing
+conveniences built from them.  Every step of the hot path runs in the CUDA kernels of libfq.so;
+there is no CPU or PyTorch fallback: if the library is missing or fails to load, importing this
+module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libfq.so")
+
+FQ_OK, FQ_ERR_INVALID_ARG, FQ_ERR_SHAPE, FQ_ERR_UNSUPPORTED, FQ_ERR_WORKSPACE, FQ_ERR_CUDA = range(6)
+FQ_BF16, FQ_FP16, FQ_FP32 = 0, 1, 2
+_DT = {torch.bfloat16: FQ_BF16, torch.float16: FQ_FP16, torch.float32: FQ_FP32}
+_TD = {v: k for k, v in _DT.items()}
+
+
+class FQError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        self.status = status
+        super().__init__(f"{what}: {fq_status_str(status)}")
+
+
+class fq_wdesc(ctypes.Structure):
+    _fields_ = [("K", ctypes.c_int64), ("N", ctypes.c_int64), ("bits", ctypes.c_int32),
+                ("group", ctypes.c_int32), ("scale_dtype", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libfq.so not built ({LIB_PATH}); run __graft_entry__.build() "
+                          "or python -m paper_2308_09723_b200.build")
+    lib = ctypes.CDLL(LIB_PATH)
+    c = ctypes
+    P, I32, I64, U32, SZ = c.c_void_p, c.c_int32, c.c_int64, c.c_uint32, c.c_size_t
+    WD = c.POINTER(fq_wdesc)
+    sig = {
+        "fq_version": (c.c_char_p, []),
+        "fq_status_str": (c.c_char_p, [c.c_int]),
+        "fq_codes_bytes": (SZ, [I64, I64, I32]),
+        "fq_scales_bytes": (SZ, [I64, I64, I32, I32]),
+        "fq_adapt_levels": (I32, [I64, I32]),
+        "fq_adapt_group_at": (I32, [I64, I32, I32]),
+        "fq_adapt_flags": (c.c_int, [P, I32, I64, I64, U32, I32, P, P, P]),
+        "fq_adapt_decide": (I32, [I64, I32, c.POINTER(I32)]),
+        "fq_quantize": (c.c_int, [P, I32, WD, P, P, P, P]),
+        "fq_gemm_workspace_bytes": (SZ, [I64, WD]),
+        "fq_gemm": (c.c_int, [P, I32, I64, WD, P, P, P, I32, P, SZ, P]),
+        "fq_gemm_grouped_workspace_bytes": (SZ, [I64, I32, WD]),
+        "fq_gemm_grouped": (c.c_int, [P, I32, I64, c.POINTER(I64), I32, WD, c.POINTER(I32),
+                                      c.POINTER(P), c.POINTER(P), P, I32, P, SZ, P]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype, f.argtypes = res, args
+    return lib
+
+
+_lib = _load()
+EXPORTED = ("fq_version", "fq_status_str", "fq_codes_bytes", "fq_scales_bytes", "fq_adapt_levels",
+            "fq_adapt_group_at", "fq_adapt_flags", "fq_adapt_decide", "fq_quantize",
+            "fq_gemm_workspace_bytes", "fq_gemm", "fq_gemm_grouped_workspace_bytes", "fq_gemm_grouped")
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _check(st: int, what: str):
+    if st != FQ_OK:
+        raise FQError(st, what)
+
+
+# ------------------------------------------------------------------------------ 1:1 ABI wrappers
+def fq_version() -> str:
+    return _lib.fq_version().decode()
+
+
+def fq_status_str(s: int) -> str:
+    return _lib.fq_status_str(s).decode()
+
+
+def fq_codes_bytes(K: int, N: int, bits: int) -> int:
+    return _lib.fq_codes_bytes(K, N, bits)
+
+
+def fq_scales_bytes(K: int, N: int, group: int, scale_dtype: int) -> int:
+    return _lib.fq_scales_bytes(K, N, group, scale_dtype)
+
+
+def fq_adapt_levels(K: int, min_group: int) -> int:
+    return _lib.fq_adapt_levels(K, min_group)
+
+
+def fq_adapt_group_at(K: int, min_group: int, level: int) -> int:
+    return _lib.fq_adapt_group_at(K, min_group, level)
+
+
+def fq_adapt_flags(W: torch.Tensor, alpha_milli: int, min_group: int, flags: torch.Tensor,
+                   status: torch.Tensor | None = None, stream=None) -> None:
+    N, K = W.shape
+    _check(_lib.fq_adapt_flags(_ptr(W), _DT[W.dtype], K, N, alpha_milli, min_group, _ptr(flags),
+                               _ptr(status), _stream(stream)), "fq_adapt_flags")
+
+
+def fq_adapt_decide(K: int, min_group: int, flags_host) -> int:
+    arr = (ctypes.c_int32 * max(1, len(flags_host)))(*[int(f) for f in flags_host])
+    return _lib.fq_adapt_decide(K, min_group, arr)
+
+
+def make_wdesc(K: int, N: int, bits: int, group: int, scale_dtype: int) -> fq_wdesc:
+    return fq_wdesc(K, N, bits, group, scale_dtype, 0)
+
+
+def fq_quantize(W: torch.Tensor, d: fq_wdesc, codes: torch.Tensor, scales: torch.Tensor,
+                status: torch.Tensor | None = None, stream=None) -> None:
+    _check(_lib.fq_quantize(_ptr(W), _DT[W.dtype], ctypes.byref(d), _ptr(codes), _ptr(scales),
+                            _ptr(status), _stream(stream)), "fq_quantize")
+
+
+def fq_gemm_workspace_bytes(M: int, d: fq_wdesc) -> int:
+    return _lib.fq_gemm_workspace_bytes(M, ctypes.byref(d))
+
+
+def fq_gemm(A: torch.Tensor, M: int, d: fq_wdesc, codes: torch.Tensor, scales: torch.Tensor,
+            C: torch.Tensor, ws: torch.Tensor | None, stream=None) -> None:
+    _check(_lib.fq_gemm(_ptr(A), _DT[A.dtype], M, ctypes.byref(d), _ptr(codes), _ptr(scales),
+                        _ptr(C), _DT[C.dtype], _ptr(ws), 0 if ws is None else ws.numel() * ws.element_size(),
+                        _stream(stream)), "fq_gemm")
+
+
+def fq_gemm_grouped_workspace_bytes(T: int, E: int, d: fq_wdesc) -> int:
+    return _lib.fq_gemm_grouped_workspace_bytes(T, E, ctypes.byref(d))
+
+
+def fq_gemm_grouped(A, T, offsets_host, E, d, groups_host, codes_ptrs, scales_ptrs, C, ws, stream=None):
+    offs = (ctypes.c_int64 * (E + 1))(*[int(x) for x in offsets_host])
+    grps = (ctypes.c_int32 * E)(*[int(x) for x in groups_host])
+    cps = (ctypes.c_void_p * E)(*[int(x) for x in codes_ptrs])
+    sps = (ctypes.c_void_p * E)(*[int(x) for x in scales_ptrs])
+    _check(_lib.fq_gemm_grouped(_ptr(A), _DT[A.dtype], T, offs, E, ctypes.byref(d), grps, cps, sps,
+                                _ptr(C), _DT[C.dtype], _ptr(ws),
+                                0 if ws is None else ws.numel() * ws.element_size(), _stream(stream)),
+           "fq_gemm_grouped")
+
+
+# ------------------------------------------------------------------------------ conveniences
+_WS: dict = {}
+
+
+def workspace(nbytes: int, device) -> torch.Tensor:
+    """Zero-filled scratch reused across calls (the kernels leave their counters zeroed)."""
+    dev = torch.device(device)
+    key = (dev.type, dev.index)
+    ws = _WS.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=dev)
+        _WS[key] = ws
+    return ws
+
+
+@dataclass
+class QuantizedWeight:
+    """Packed weights of one matrix in the canonical layout (include/fq.h)."""
+    codes: torch.Tensor       # uint8 [N, K*bits/8]
+    scales: torch.Tensor      # [K/group, N], activation dtype
+    K: int
+    N: int
+    bits: int
+    group: int
+
+    @property
+    def desc(self) -> fq_wdesc:
+        return make_wdesc(self.K, self.N, self.bits, self.group, _DT[self.scales.dtype])
+
+    @property
+    def nbytes(self) -> int:
+        return self.codes.numel() + self.scales.numel() * self.scales.element_size()
+
+
+def adapt_group(W: torch.Tensor, alpha_milli: int = 500, min_group: int = 16, process_group=None) -> int:
+    """Adaptive group size (§3.3): device flags (A1), optional OR across a process group
+    (tensor-parallel shards of one matrix), host decision (A2)."""
+    N, K = W.shape
+    nlev = fq_adapt_levels(K, min_group)
+    flags = torch.zeros(max(1, nlev - 1), dtype=torch.int32, device=W.device)
+    fq_adapt_flags(W, alpha_milli, min_group, flags)
+    if process_group is not None:
+        import torch.distributed as dist
+        dist.all_reduce(flags, op=dist.ReduceOp.MAX, group=process_group)
+    return fq_adapt_decide(K, min_group, flags.cpu().tolist()[: nlev - 1])
+
+
+def quantize(W: torch.Tensor, bits: int = 4, group: int | None = 128, scale_dtype=torch.bfloat16,
+             alpha_milli: int = 500, min_group: int = 16, status: torch.Tensor | None = None) -> QuantizedWeight:
+    """fq_quantize(W, bits, group | adaptive): W is [N, K] (nn.Linear layout) on a CUDA device.
+    group=None selects the adaptive group size."""
+    assert W.is_cuda and W.dim() == 2 and W.is_contiguous()
+    N, K = W.shape
+    if group is None:
+        group = adapt_group(W, alpha_milli, min_group)
+    d = make_wdesc(K, N, bits, group, _DT[scale_dtype])
+    codes = torch.empty((N, K * bits // 8), dtype=torch.uint8, device=W.device)
+    scales = torch.empty((K // group, N), dtype=scale_dtype, device=W.device)
+    fq_quantize(W, d, codes, scales, status)
+    return QuantizedWeight(codes, scales, K, N, bits, group)
+
+
+def gemm(A: torch.Tensor, qw: QuantizedWeight, out: torch.Tensor | None = None,
+         out_dtype=None, stream=None) -> torch.Tensor:
+    """C[M, N] = A[M, K] . dequant(qw)^T  (fused, on the GPU)."""
+    assert A.is_cuda and A.dim() == 2 and A.is_contiguous() and A.shape[1] == qw.K
+    M = A.shape[0]
+    d = qw.desc
+    if out is None:
+        out = torch.empty((M, qw.N), dtype=out_dtype or A.dtype, device=A.device)
+    nb = fq_gemm_workspace_bytes(M, d)
+    ws = workspace(nb, A.device)
+    fq_gemm(A, M, d, qw.codes, qw.scales, out, ws, stream)
+    return out

@@ -101,3 +101,13 @@ def zipf_routing(E: int, total_tokens: int, seed: int = 3000, s: float = 1.0) ->
     off = np.zeros(E + 1, dtype=np.int64)
     off[1:] = np.cumsum(counts)
     return off
+
+
+def gaussian_torch(shape, std: float, seed: int, device="cuda", dtype=None):
+    """Large-input generator (full-size configs): N(0, std^2) drawn on `device` with a seeded
+    torch.Generator (Philox), rounded to `dtype` (default bf16).  Used where numpy generation of
+    ~6e8 values would dominate test time; the oracle consumes the same bytes copied back."""
+    import torch
+    g = torch.Generator(device=device).manual_seed(int(seed))
+    x = torch.randn(*shape, generator=g, device=device, dtype=torch.float32) * float(std)
+    return x.to(dtype or torch.bfloat16)

@@ -1,0 +1,72 @@
+"""CPU-only checks of the C-ABI library: it loads, exports every symbol fq.h declares, and its
+host-side logic (sizes, ladder, decision, validation) behaves as documented.  No compute calls."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "fq.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(fq_[a-z_0-9]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def fq():
+    from paper_2308_09723_b200 import fq as m
+    return m
+
+
+def test_library_exports_every_declared_symbol(fq):
+    lib = ctypes.CDLL(fq.LIB_PATH)
+    names = header_functions()
+    assert len(names) >= 13
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(fq.EXPORTED)
+
+
+def test_sizes_and_ladder(fq):
+    assert fq.fq_codes_bytes(12288, 49152, 4) == 12288 * 49152 // 2
+    assert fq.fq_codes_bytes(12288, 49152, 8) == 12288 * 49152
+    assert fq.fq_codes_bytes(12288, 49152, 3) == 0
+    assert fq.fq_scales_bytes(12288, 49152, 128, fq.FQ_BF16) == 96 * 49152 * 2
+    assert fq.fq_scales_bytes(12288, 49152, 100, fq.FQ_BF16) == 0
+    from oracle import fq_oracle as O
+    for K in (128, 4096, 12288, 49152, 7168, 96):
+        lad = O.adapt_ladder(K, 16)
+        assert fq.fq_adapt_levels(K, 16) == len(lad)
+        assert [fq.fq_adapt_group_at(K, 16, L) for L in range(len(lad))] == lad
+    assert fq.fq_adapt_decide(12288, 16, [1, 1, 0, 1]) == 3072
+    assert fq.fq_adapt_decide(12288, 16, [0, 1]) == 12288
+    assert fq.fq_adapt_decide(4096, 16, [1] * 8) == 16
+
+
+def test_decide_matches_oracle_decide(fq):
+    from oracle import fq_oracle as O
+    import itertools
+    for flags in itertools.product([0, 1], repeat=4):
+        assert fq.fq_adapt_decide(4096, 256, list(flags)) == O.adapt_decide([bool(f) for f in flags], 4096, 256)
+
+
+def test_validation_is_synchronous_and_launch_free(fq):
+    """Invalid descriptors are rejected before any device work (pointers are dummies)."""
+    d = fq.make_wdesc(256, 256, 3, 64, fq.FQ_BF16)
+    dummy = ctypes.c_void_p(16)
+    st = fq._lib.fq_gemm(dummy, fq.FQ_BF16, 1, ctypes.byref(d), dummy, dummy, dummy, fq.FQ_BF16,
+                         None, 0, None)
+    assert st == fq.FQ_ERR_UNSUPPORTED
+    for bad in (fq.make_wdesc(250, 256, 4, 64, 0), fq.make_wdesc(256, 252, 4, 64, 0),
+                fq.make_wdesc(256, 256, 4, 48, 0), fq.make_wdesc(256, 256, 4, 24, 0)):
+        assert fq._lib.fq_quantize(dummy, 0, ctypes.byref(bad), dummy, dummy, None, None) == fq.FQ_ERR_SHAPE
+    d = fq.make_wdesc(256, 256, 4, 64, fq.FQ_BF16)
+    assert fq._lib.fq_gemm(dummy, fq.FQ_FP16, 1, ctypes.byref(d), dummy, dummy, dummy, fq.FQ_FP16,
+                           None, 0, None) == fq.FQ_ERR_UNSUPPORTED  # scale dtype != activation dtype
+    assert fq._lib.fq_gemm(None, 0, 1, ctypes.byref(d), dummy, dummy, dummy, 0, None, 0, None) == fq.FQ_ERR_INVALID_ARG
+    assert fq._lib.fq_adapt_flags(dummy, 0, 256, 8, 0, 16, dummy, None, None) == fq.FQ_ERR_INVALID_ARG
+    assert fq._lib.fq_adapt_flags(dummy, 0, 256, 8, 1001, 16, dummy, None, None) == fq.FQ_ERR_INVALID_ARG
+    assert fq.fq_status_str(fq.FQ_ERR_SHAPE) == "FQ_ERR_SHAPE"

@@ -1,0 +1,179 @@
+"""GPU parity of the fused dequant-GEMM (kernels A4/A5, and the large-M path) against the fp64
+oracle.  Tolerance (BASELINE.json north_star): max |C - C_ref| / sum|a*w| <= 2e-3."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import fq_oracle as O
+from synth import activations_bits, gaussian_bits, gaussian_with_outliers_bits
+from helpers import bits_to_torch, torch_to_f64
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-3
+
+
+@pytest.fixture(scope="module")
+def fq():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2308_09723_b200 import fq as m
+    return m
+
+
+@pytest.fixture
+def env():
+    saved = {}
+
+    def set_(k, v):
+        saved.setdefault(k, os.environ.get(k))
+        os.environ[k] = str(v)
+    yield set_
+    for k, v in saved.items():
+        if v is None:
+            os.environ.pop(k, None)
+        else:
+            os.environ[k] = v
+
+
+def make_case(M, K, N, bits, group, adt="bf16", seed=0, outliers=0):
+    if outliers:
+        Wb = gaussian_with_outliers_bits((N, K), 0.02, 1000 + seed, outliers, 0.5, "bf16")
+    else:
+        Wb = gaussian_bits((N, K), 0.02, 1000 + seed, "bf16")
+    Ab = activations_bits(M, K, 2000 + seed, adt)
+    return Wb, Ab
+
+
+def run_case(fq, Wb, Ab, bits, group, adt="bf16", cdt=None):
+    W = bits_to_torch(Wb, "bf16")
+    A = bits_to_torch(Ab, adt)
+    sdt = {"bf16": torch.bfloat16, "fp16": torch.float16}[adt]
+    qw = fq.quantize(W, bits, group, scale_dtype=sdt)
+    C = fq.gemm(A, qw, out_dtype={"fp32": torch.float32, None: None}[cdt])
+    torch.cuda.synchronize()
+    return qw, C
+
+
+def oracle_ref(Wb, Ab, bits, group, adt, cols=None):
+    sf = O.FORMATS[adt]
+    r = O.quantize(O.decode_bits(Wb, "bf16"), bits, group, sf)
+    return O.gemm(O.decode_bits(Ab, adt), r.q, r.s, group, cols)
+
+
+@pytest.mark.parametrize("M", [1, 2, 3, 8, 9, 16])
+@pytest.mark.parametrize("bits", [4, 8])
+def test_tiny_config_parity(fq, M, bits):
+    # configs[0]: K=256, N=256, group 64 (+ M sweep of the decode regime)
+    Wb, Ab = make_case(M, 256, 256, bits, 64, seed=M)
+    _, C = run_case(fq, Wb, Ab, bits, 64)
+    Cr, D = oracle_ref(Wb, Ab, bits, 64, "bf16")
+    assert O.rel_err(torch_to_f64(C), Cr, D) <= TOL
+
+
+@pytest.mark.parametrize("group", [16, 32, 48, 64, 96, 128, 256, 1536])
+@pytest.mark.parametrize("bits", [4, 8])
+def test_group_sizes_multi_tile_ragged(fq, bits, group):
+    # several CTA tiles, ragged N tail (N not a multiple of the 256-row CTA tile)
+    M, K, N = 5, 1536, 776
+    Wb, Ab = make_case(M, K, N, bits, group, seed=group, outliers=2)
+    _, C = run_case(fq, Wb, Ab, bits, group)
+    Cr, D = oracle_ref(Wb, Ab, bits, group, "bf16")
+    assert O.rel_err(torch_to_f64(C), Cr, D) <= TOL
+
+
+@pytest.mark.parametrize("adt", ["bf16", "fp16"])
+@pytest.mark.parametrize("bits", [4, 8])
+@pytest.mark.parametrize("cdt", [None, "fp32"])
+def test_dtypes(fq, adt, bits, cdt):
+    M, K, N = 7, 1024, 512
+    Wb, Ab = make_case(M, K, N, bits, 128, adt, seed=3)
+    _, C = run_case(fq, Wb, Ab, bits, 128, adt, cdt)
+    Cr, D = oracle_ref(Wb, Ab, bits, 128, adt)
+    assert O.rel_err(torch_to_f64(C), Cr, D) <= TOL
+
+
+@pytest.mark.parametrize("splits", [1, 2, 3, 7])
+@pytest.mark.parametrize("M", [1, 12])
+def test_split_k_paths(fq, env, splits, M):
+    env("FQ_GEMV_SPLITS", splits)
+    Wb, Ab = make_case(M, 4096, 512, 4, 128, seed=11)
+    for _ in range(2):  # second call checks the self-resetting counters
+        _, C = run_case(fq, Wb, Ab, 4, 128)
+        Cr, D = oracle_ref(Wb, Ab, 4, 128, "bf16")
+        assert O.rel_err(torch_to_f64(C), Cr, D) <= TOL
+
+
+def test_identity_exact_fp32_out(fq):
+    """A = I (M = K = 256): C[k, n] = q[n,k] * s[k/g, n] exactly in fp32-output mode — catches any
+    nibble-order / k-permutation / scale-index bug with zero tolerance."""
+    K = N = 256
+    Wb = gaussian_bits((N, K), 0.02, 5)
+    # groups that are a multiple of the K chunk (128 int4 / 64 int8) apply the scale in fp32 on
+    # exact integer partials -> exact; smaller groups dequantize q*s to the activation dtype
+    # first (one bf16 rounding, the paper's own "dequantize to the activation dtype").
+    for bits, group, exact in ((4, 128, True), (8, 64, True), (4, 256, True), (8, 256, True),
+                               (4, 64, False), (4, 16, False), (8, 16, False)):
+        W = bits_to_torch(Wb, "bf16")
+        qw = fq.quantize(W, bits, group)
+        A = torch.eye(K, dtype=torch.bfloat16, device="cuda")
+        C = fq.gemm(A, qw, out_dtype=torch.float32)
+        r = O.quantize(O.decode_bits(Wb, "bf16"), bits, group, O.BF16)
+        ref = O.dequantize(r.q, r.s, group).T
+        if exact:
+            assert np.array_equal(torch_to_f64(C), ref)
+        else:
+            assert np.all(np.abs(torch_to_f64(C) - ref) <= np.abs(ref) * 2.0**-8)
+
+
+def test_integer_exact_special_case(fq):
+    """Small-integer A and weights built by the exact round-trip construction with s = 2^e:
+    C is exactly representable, so the fused kernel must return it with zero error."""
+    rng = np.random.default_rng(17)
+    M, K, N, g = 16, 512, 64, 64
+    A = rng.integers(-2, 3, size=(M, K)).astype(np.float32)
+    q = rng.integers(-7, 8, size=(N, K))
+    s = 2.0 ** -6
+    Wv = (q * s).astype(np.float32)
+    for n in range(N):
+        for j in range(K // g):
+            Wv[n, j * g] = np.float32(7.5 * s)  # anchor: makes the group scale exactly s
+    from synth import f32_to_bf16_bits
+    W = bits_to_torch(f32_to_bf16_bits(Wv), "bf16")
+    qw = fq.quantize(W, 4, g)
+    Ct = fq.gemm(bits_to_torch(f32_to_bf16_bits(A), "bf16"), qw, out_dtype=torch.float32)
+    qx = q.copy()
+    qx[:, ::g] = 7
+    exact = (A.astype(np.int64) @ qx.T.astype(np.int64)) * s
+    assert np.array_equal(torch_to_f64(Ct), exact.astype(np.float64))
+
+
+@pytest.mark.parametrize("M", [17, 64, 200])
+def test_large_m(fq, M):
+    Wb, Ab = make_case(M, 1024, 384, 4, 128, seed=M)
+    _, C = run_case(fq, Wb, Ab, 4, 128)
+    Cr, D = oracle_ref(Wb, Ab, 4, 128, "bf16")
+    assert O.rel_err(torch_to_f64(C), Cr, D) <= TOL
+
+
+@pytest.mark.parametrize("shape", [(12288, 49152), (49152, 12288)])
+@pytest.mark.parametrize("bits", [4, 8])
+@pytest.mark.parametrize("M", [1, 16])
+def test_opt175b_full_size_sampled(fq, shape, bits, M):
+    """configs[1] at full size in the bench's launch configuration; parity on 64 sampled columns
+    computed by the oracle one by one (scales/codes of those columns only)."""
+    K, N = shape
+    from synth import gaussian_torch
+    W = gaussian_torch((N, K), 0.02, 1000 + K)
+    A = gaussian_torch((M, K), 1.0, 2000 + K)
+    qw = fq.quantize(W, bits, 128)
+    C = fq.gemm(A, qw)
+    torch.cuda.synchronize()
+    cols = np.random.default_rng(0).choice(N, 64, replace=False)
+    Wc = W[torch.from_numpy(cols).cuda()].float().cpu().double().numpy()
+    r = O.quantize(Wc, bits, 128, O.BF16)
+    Cr, D = O.gemm(A.float().cpu().double().numpy(), r.q, r.s, 128)
+    assert O.rel_err(torch_to_f64(C)[:, cols], Cr, D) <= TOL
+    # the sampled columns' codes/scales are bit-exact as well
+    assert np.array_equal(qw.codes[torch.from_numpy(cols).cuda()].cpu().numpy(), O.pack_codes(r.q, bits))

@@ -1,0 +1,117 @@
+"""GPU parity of kernels A1/A3 (adaptive flags, quantize+pack) against the oracle: bit-exact."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import fq_oracle as O
+from synth import gaussian_bits, gaussian_with_outliers_bits
+from helpers import bits_to_torch, torch_to_bits
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fq():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2308_09723_b200 import fq as m
+    return m
+
+
+def run_quant(fq, bits_W, wdt, bits, group, sdt):
+    W = bits_to_torch(bits_W, wdt)
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    qw = fq.quantize(W, bits, group, scale_dtype={"bf16": torch.bfloat16, "fp16": torch.float16}[sdt], status=st)
+    torch.cuda.synchronize()
+    return qw, int(st.item())
+
+
+def check_exact(fq, bits_W, wdt, bits, group, sdt):
+    qw, st = run_quant(fq, bits_W, wdt, bits, group, sdt)
+    ref = O.quantize(O.decode_bits(bits_W, wdt), bits, group, O.FORMATS[sdt])
+    assert st == ref.status
+    got_s = torch_to_bits(qw.scales)
+    assert np.array_equal(got_s, ref.s_bits), f"scale mismatch at {np.argwhere(got_s != ref.s_bits)[:5]}"
+    got_c = qw.codes.cpu().numpy()
+    exp_c = O.pack_codes(ref.q, bits)
+    if not np.array_equal(got_c, exp_c):
+        bad = np.argwhere(got_c != exp_c)[:5]
+        raise AssertionError(f"codes mismatch at {bad}")
+
+
+@pytest.mark.parametrize("sdt", ["bf16", "fp16"])
+def test_hand_example_gpu(fq, golden, sdt):
+    g = golden("quant_hand.txt")
+    col = np.array([float(v) for v in g["column"]], dtype=np.float32)
+    W = np.zeros((8, 64), dtype=np.float32)
+    W[0, :4] = col
+    from synth import f32_to_bf16_bits
+    qw, st = run_quant(fq, f32_to_bf16_bits(W), "bf16", 4, 64, sdt)
+    assert st == 0
+    assert int(torch_to_bits(qw.scales)[0, 0]) == int(g[f"{sdt}.scale_bits"][0], 16)
+    assert qw.codes[0, :2].cpu().tolist() == [int(v, 16) for v in g[f"{sdt}.bytes"]]
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+@pytest.mark.parametrize("group", [16, 32, 48, 64, 96, 128, 256, 768])
+def test_quantize_exact_groups(fq, bits, group):
+    W = gaussian_with_outliers_bits((40, 1536), 0.02, 1000 + group, 3, 0.5)
+    check_exact(fq, W, "bf16", bits, group, "bf16")
+
+
+@pytest.mark.parametrize("wdt", ["bf16", "fp16", "fp32"])
+@pytest.mark.parametrize("sdt", ["bf16", "fp16"])
+def test_quantize_exact_dtypes(fq, wdt, sdt):
+    W = gaussian_bits((24, 512), 0.02, 7, wdt)
+    check_exact(fq, W, wdt, 4, 64, sdt)
+    check_exact(fq, W, wdt, 8, 512, sdt)  # per-column
+
+
+def test_quantize_exact_tiny_config(fq):
+    # configs[0]: M=1, K=256, N=256, int4 group=64, bf16
+    W = gaussian_bits((256, 256), 0.02, 1001)
+    check_exact(fq, W, "bf16", 4, 64, "bf16")
+
+
+def test_quantize_ties_all_bf16_patterns(fq):
+    """Every finite bf16 value appears in a group whose scale is fixed by a planted anchor; codes
+    must match the oracle bit for bit (covers the +-7.5 / 127.5 tie cases)."""
+    allb = np.arange(65536, dtype=np.uint32).astype(np.uint16)
+    vals = O.decode_bits(allb, "bf16")
+    allb = allb[np.isfinite(vals)]
+    K = 256
+    n = (allb.size + K - 1) // K
+    buf = np.zeros(n * K, dtype=np.uint16)
+    buf[: allb.size] = allb
+    W = buf.reshape(n, K)
+    for bits in (4, 8):
+        check_exact(fq, W, "bf16", bits, 32, "bf16")
+
+
+def test_zero_and_nonfinite_status(fq):
+    from synth import f32_to_bf16_bits
+    W = np.zeros((8, 64), dtype=np.float32)
+    W[1, 3] = np.inf
+    W[2, 40] = np.nan
+    W[3, 5] = 0.25
+    check_exact(fq, f32_to_bf16_bits(W), "bf16", 4, 32, "bf16")
+    W2 = np.full((8, 64), 1e6, dtype=np.float32)
+    check_exact(fq, W2.view(np.uint32), "fp32", 4, 32, "fp16")  # fp16 scale overflow -> status 2
+
+
+@pytest.mark.parametrize("K,N,alpha,outliers", [(128, 8, 500, 0), (128, 8, 500, 1), (4096, 64, 500, 2),
+                                                (12288, 32, 300, 1), (7168, 16, 800, 3)])
+def test_adapt_flags_match_oracle(fq, K, N, alpha, outliers):
+    if outliers:
+        Wb = gaussian_with_outliers_bits((N, K), 0.01, K + N, outliers, 1.0)
+    else:
+        Wb = gaussian_bits((N, K), 1.0, K + N)
+    Wd = O.decode_bits(Wb, "bf16")
+    exp_flags = O.adapt_flags(Wd, alpha, 16)
+    W = bits_to_torch(Wb, "bf16")
+    nlev = fq.fq_adapt_levels(K, 16)
+    flags = torch.zeros(nlev - 1, dtype=torch.int32, device="cuda")
+    fq.fq_adapt_flags(W, alpha, 16, flags)
+    got = [bool(f) for f in flags.cpu().tolist()]
+    assert got == exp_flags
+    assert fq.adapt_group(W, alpha, 16) == O.adapt_group_size(Wd, alpha, 16)
