@@ -117,6 +117,8 @@ fq_status fq_quantize(const void* W, int32_t wdt, const fq_wdesc* d, void* codes
   fq_status s = check_wdesc(d);
   if (s != FQ_OK) return s;
   if (!W || !codes || !scales || !valid_dtype(wdt)) return FQ_ERR_INVALID_ARG;
+  // one CTA per column holds the whole column in registers: K <= 65536 (16-bit W), 32768 (fp32 W)
+  if (d->K > (wdt == FQ_FP32 ? 32768 : 65536)) return FQ_ERR_SHAPE;
   return from_cuda(run_quantize(wdt, d->scale_dtype, d->bits, W, (int)d->K, (int)d->N, d->group,
                                 codes, scales, status_dev, as_stream(stream)));
 }

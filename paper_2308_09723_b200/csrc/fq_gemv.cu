@@ -1,116 +1,131 @@
-// fq_gemv.cu — kernels A4 (decode GEMM, weights streamed from HBM, dequantized in registers,
-// multiplied on the tensor cores with mma.sync in swap-AB form) and A5 (deterministic split-K
-// fixup, fused: the last-arriving CTA of a tile reduces the partials in split order).
+// fq_gemv.cu — kernels A4 (decode GEMM) and A5 (deterministic split-K fixup, fused).
 //
 // Computes C[m,n] = sum_k A[m,k] * q[n,k] * s[k/g, n]  (§4.1: "dequantize the weights to
 // match the data type of the activation and perform floating-point tensor core math").  Decode is
 // "bottlenecked by memory bandwidth ... weights typically dominate the memory traffic": the
-// design goal is to stream each packed weight byte exactly once at HBM speed.
+// kernel's job is to stream every packed weight byte exactly once at HBM speed.
 //
-// Mapping (swap-AB): the MMA's M=16 rows are 16 output columns n, its N=8 are tokens, K=16.
-//   lane = 4*gq + t.  Thread (gq,t) owns rows n0+gq and n0+gq+8 and, inside a K chunk, the
-//   contiguous K segment [kc + t*SEG, kc + (t+1)*SEG) of both rows, loaded with one 16-byte
-//   streaming load per row (SEG = 32 for int4, 16 for int8).  The four lanes of a quad read 64
-//   contiguous bytes of a row.
-//   int4: LOP3 of a 32-bit word w (nibbles n0..n7 = k..k+7) with mask 0x000F000F yields the bf16x2
-//   pair (k, k+4) as 128+(n^8) [fp16: 1024+(n^8)]; one subtract gives the exact signed code.  The
-//   MMA k-slots are therefore filled with the permutation (0,4),(1,5),(2,6),(3,7) of each 8-k word;
-//   the activations are loaded in natural order and permuted identically with PRMT (the sum over k
-//   is invariant under a common permutation of both operands).
-//   int8: bytes -> fp32 magic (bf16) or fp16 magic, natural (k, k+1) pairs.
-// Scales: if group % KCHUNK == 0 every MMA of a chunk lies in one group; the chunk is accumulated
-//   in a fresh fp32 fragment and folded into the accumulator with one FFMA by s[j, n] (exact codes,
-//   fp32 scale application).  Otherwise (group 16..112, 48, 96, ...) the codes are scaled in the
-//   activation dtype before the MMA (the paper's "dequantize to the activation dtype").
-// Split-K: grid.y splits K; partials go to ws[S][M][N] fp32 and the last CTA of each output tile
-//   (arrival counter, self-resetting) sums them in split order -> deterministic results.
+// Warp-specialised, TMA-pipelined (B200 design):
+//   warp 0 (producer): per pipeline stage, one 2-D TMA load of the packed weight tile
+//     [256 columns n x 128 bytes of K] (SWIZZLE_128B) into shared memory, plus the activation slice
+//     of the stage, copied with 16-byte loads and written to shared memory already in the
+//     per-thread MMA fragment order (so consumers need no shuffles).  mbarrier full/empty ring.
+//   warps 1..8 (consumers): each owns 32 output columns (2 tiles of 16).  Swap-AB mma.sync
+//     m16n8k16: the MMA's 16 "rows" are output columns n, its 8 "columns" are tokens.  Codes are
+//     unpacked in registers: int4 with one LOP3 per bf16x2 pair (mask 0x000F000F yields the pair
+//     (k, k+4) as 128+(n^8)) and one subtract; the activations were stored by the producer with the
+//     same (0,4),(1,5),(2,6),(3,7) permutation of each 8-k word.  int8: bytes -> exact bf16/fp16.
+//   Scales: if group % KCHUNK == 0 every MMA of a K chunk lies in one group: the chunk accumulates
+//     exact integer-weight partials in a fresh fp32 fragment, folded in with one FFMA by s[j,n].
+//     Otherwise (small/odd groups) q*s is formed in the activation dtype before the MMA.
+//   Split-K (grid.y): fp32 partials ws[S][M][N]; the last CTA of each column tile (self-resetting
+//     arrival counter) reduces them in split order -> deterministic output.
+//   Token tiles (grid.z): 16 tokens per tile (M > 16 re-streams the weights per tile; the
+//     tensor-core prefill kernel A6 is the large-M path).
+#include <cuda.h>
+
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
-#include <cstdio>
 
 #include "fq_common.cuh"
 #include "fq_internal.h"
 
 namespace fq {
 
-constexpr int kGemvThreads = 256;  // 8 warps; each warp owns 16*RT output columns
+constexpr int kConsumerWarps = 8;
+constexpr int kDecThreads = 32 * (1 + kConsumerWarps);
+constexpr int kRowsPerCta = 256;      // 8 consumer warps x 2 tiles x 16 columns
+constexpr int kWBytesPerRow = 128;    // packed bytes of one column per stage (one SW128 line)
+constexpr int kStageW = kRowsPerCta * kWBytesPerRow;  // 32 KB
+constexpr int kDecStages = 2;
 
-struct GemvParams {
+template <int BITS>
+struct DecGeom {
+  static constexpr int KS = kWBytesPerRow * 8 / BITS;  // K per stage: 256 (int4) / 128 (int8)
+  static constexpr int SEG = BITS == 4 ? 32 : 16;      // K per thread per column per chunk
+  static constexpr int KCH = 4 * SEG;                  // K per chunk (one quad): 128 / 64
+  static constexpr int CHUNKS = KS / KCH;              // 2
+  static constexpr int PIECES = SEG / 8;               // 16-byte activation pieces per thread/chunk
+  static constexpr int TOK_BYTES = KS * 2 + 64;        // token row stride in smem, = 64 mod 128
+};
+
+struct DecodeParams {
   const void* A;
-  const uint8_t* codes;
   const void* scales;
   void* C;
-  float* ws;       // [S][M][N] partials
-  int* counters;   // [gridDim.z][gridDim.x]
+  float* ws;
+  int* counters;
   int M, K, N, group, klen, cdt;
 };
 
 template <typename T>
 __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
-                                         uint32_t b1, const float (&c)[4]);
+                                         uint32_t b1);
 template <>
 __device__ __forceinline__ void mma16816<__nv_bfloat16>(float (&d)[4], const uint32_t (&a)[4],
-                                                        uint32_t b0, uint32_t b1,
-                                                        const float (&c)[4]) {
+                                                        uint32_t b0, uint32_t b1) {
   asm volatile(
       "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-      "{%8,%9}, {%10,%11,%12,%13};"
-      : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "f"(c[0]), "f"(c[1]),
-        "f"(c[2]), "f"(c[3]));
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 template <>
-__device__ __forceinline__ void mma16816<__half>(float (&d)[4], const uint32_t (&a)[4],
-                                                 uint32_t b0, uint32_t b1, const float (&c)[4]) {
+__device__ __forceinline__ void mma16816<__half>(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
+                                                 uint32_t b1) {
   asm volatile(
       "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-      "{%8,%9}, {%10,%11,%12,%13};"
-      : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "f"(c[0]), "f"(c[1]),
-        "f"(c[2]), "f"(c[3]));
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
 template <typename T>
 __device__ __forceinline__ uint32_t sub2(uint32_t a, uint32_t b);
 template <>
 __device__ __forceinline__ uint32_t sub2<__nv_bfloat16>(uint32_t a, uint32_t b) {
-  __nv_bfloat162 r = __hsub2(*reinterpret_cast<__nv_bfloat162*>(&a), *reinterpret_cast<__nv_bfloat162*>(&b));
-  return *reinterpret_cast<uint32_t*>(&r);
+  uint32_t d;
+  asm("sub.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
 }
 template <>
 __device__ __forceinline__ uint32_t sub2<__half>(uint32_t a, uint32_t b) {
-  __half2 r = __hsub2(*reinterpret_cast<__half2*>(&a), *reinterpret_cast<__half2*>(&b));
-  return *reinterpret_cast<uint32_t*>(&r);
+  uint32_t d;
+  asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
 }
 template <typename T>
 __device__ __forceinline__ uint32_t mul2(uint32_t a, uint32_t b);
 template <>
 __device__ __forceinline__ uint32_t mul2<__nv_bfloat16>(uint32_t a, uint32_t b) {
-  __nv_bfloat162 r = __hmul2(*reinterpret_cast<__nv_bfloat162*>(&a), *reinterpret_cast<__nv_bfloat162*>(&b));
-  return *reinterpret_cast<uint32_t*>(&r);
+  uint32_t d;
+  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
 }
 template <>
 __device__ __forceinline__ uint32_t mul2<__half>(uint32_t a, uint32_t b) {
-  __half2 r = __hmul2(*reinterpret_cast<__half2*>(&a), *reinterpret_cast<__half2*>(&b));
-  return *reinterpret_cast<uint32_t*>(&r);
+  uint32_t d;
+  asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
 }
 
-// int4 word (k..k+7) -> 4 packed pairs (k,k+4),(k+1,k+5),(k+2,k+6),(k+3,k+7), exact codes.
+// int4 word (k..k+7) -> pairs (k,k+4),(k+1,k+5),(k+2,k+6),(k+3,k+7) holding the exact codes.
 template <typename T>
 __device__ __forceinline__ void i4_pairs(uint32_t w, uint32_t (&q)[4]) {
   constexpr uint32_t mask = 0x000F000Fu;
   q[0] = sub2<T>(lop3_and_xor(w, mask, Dt<T>::kMagic4), Dt<T>::kBias4);
-  q[1] = sub2<T>(lop3_and_xor(w >> 4, mask, Dt<T>::kMagic4), Dt<T>::kBias4);
+  q[1] = sub2<T>(lop3_and_xor(__umulhi(w, 1u << 28), mask, Dt<T>::kMagic4), Dt<T>::kBias4);  // w >> 4
   q[2] = sub2<T>(lop3_and_xor(w >> 8, mask, Dt<T>::kMagic4), Dt<T>::kBias4);
-  q[3] = sub2<T>(lop3_and_xor(w >> 12, mask, Dt<T>::kMagic4), Dt<T>::kBias4);
+  q[3] = sub2<T>(lop3_and_xor(__umulhi(w, 1u << 20), mask, Dt<T>::kMagic4), Dt<T>::kBias4);  // w >> 12
 }
 
-// int8 word (k..k+3) -> 2 natural pairs (k,k+1),(k+2,k+3), exact codes.
+// int8 word (k..k+3) -> natural pairs (k,k+1),(k+2,k+3) holding the exact codes.
 template <typename T>
 __device__ __forceinline__ void i8_pairs(uint32_t w, uint32_t (&q)[2]);
 template <>
 __device__ __forceinline__ void i8_pairs<__half>(uint32_t w, uint32_t (&q)[2]) {
-  const uint32_t u = w ^ 0x80808080u;  // offset binary: u = q + 128
+  const uint32_t u = w ^ 0x80808080u;                                 // u = q + 128
   q[0] = sub2<__half>(prmt(u, 0x64646464u, 0x4140u), 0x64806480u);  // (1024+u) - 1152
   q[1] = sub2<__half>(prmt(u, 0x64646464u, 0x4342u), 0x64806480u);
 }
@@ -120,7 +135,7 @@ __device__ __forceinline__ void i8_pairs<__nv_bfloat16>(uint32_t w, uint32_t (&q
   float f[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
-    f[i] = __uint_as_float(prmt(u, 0x4B000000u, 0x7440u + i)) - 8388736.0f;  // 2^23 + 128
+    f[i] = __uint_as_float(prmt(u, 0x4B000000u, 0x7440u + i)) - 8388736.0f;  // (2^23+u) - (2^23+128)
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
     uint32_t r;
@@ -134,176 +149,207 @@ __device__ __forceinline__ uint32_t splat_scale(const T* scales, size_t idx) {
   const unsigned short s = __ldg(reinterpret_cast<const unsigned short*>(scales) + idx);
   return (uint32_t)s | ((uint32_t)s << 16);
 }
-template <typename T>
-__device__ __forceinline__ float load_scale_f(const T* scales, size_t idx) {
-  return Dt<T>::to_f(__ldg(scales + idx));
-}
 
-template <typename T, int BITS, int MT, bool SACC, int RT>
-__global__ void __launch_bounds__(kGemvThreads, 2) gemv_kernel(const GemvParams p) {
-  constexpr int SEG = (BITS == 4) ? 32 : 16;   // K elements per thread per row per chunk
-  constexpr int KCH = 4 * SEG;                 // K per chunk (quad)
-  constexpr int WORDS = 4;                     // 32-bit words per 16-byte load
-  constexpr int KPW = SEG / WORDS;             // K per word: 8 (int4) / 4 (int8)
-  const T* __restrict__ A = reinterpret_cast<const T*>(p.A);
-  const T* __restrict__ S = reinterpret_cast<const T*>(p.scales);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int gq = lane >> 2, t = lane & 3;
+// MMA row m (0..7) of a 16-column tile -> tile row; odd m land 4 rows away so the two columns a
+// 128-bit shared-memory phase touches sit in different SW128 bank groups (conflict-free).
+__device__ __forceinline__ int prow(int m) { return ((m & 1) << 2) | (m >> 1); }
+
+template <typename T, int BITS, int MT, bool SACC>
+__global__ void __launch_bounds__(kDecThreads, 2)
+    decode_kernel(const __grid_constant__ CUtensorMap tmW, const DecodeParams p) {
+  using G = DecGeom<BITS>;
+  constexpr int KS = G::KS, SEG = G::SEG, KCH = G::KCH, CHUNKS = G::CHUNKS, PIECES = G::PIECES;
+  constexpr int TOK = G::TOK_BYTES;
+  constexpr int ACT_BYTES = MT * 8 * TOK;
+  constexpr int STAGE_BYTES = kStageW + ((ACT_BYTES + 1023) / 1024) * 1024;
+
+  extern __shared__ __align__(1024) uint8_t dsmem[];
+  __shared__ __align__(8) uint64_t full_bar[kDecStages], empty_bar[kDecStages];
+  __shared__ int s_last;
+  uint8_t* sbase = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsmem) + 1023) & ~uintptr_t(1023));
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int N = p.N, K = p.K, M = p.M;
-  const size_t row_bytes = (size_t)K * BITS / 8;
-  const int rowbase = blockIdx.x * (128 * RT) + warp * 16 * RT;
+  const int n0 = blockIdx.x * kRowsPerCta;
   const int kbeg = blockIdx.y * p.klen;
   const int kend = min(K, kbeg + p.klen);
+  const int nst = (kend - kbeg + KS - 1) / KS;
   const int tok0 = blockIdx.z * 16;
 
-  // row pointers (clamped for the ragged N tail; stores are masked)
-  const uint8_t* wrow[RT][2];
-#pragma unroll
-  for (int r = 0; r < RT; ++r)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int n = min(rowbase + r * 16 + h * 8 + gq, N - 1);
-      wrow[r][h] = p.codes + (size_t)n * row_bytes;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kDecStages; ++s) {
+      mbar_init(&full_bar[s], 32);
+      mbar_init(&empty_bar[s], kConsumerWarps);
     }
-  const T* arow[MT];
-  bool tok_ok[MT];
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt) {
-    const int tok = tok0 + mt * 8 + gq;
-    tok_ok[mt] = tok < M;
-    arow[mt] = A + (size_t)min(tok, M - 1) * K;
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) prefetch_tmap(&tmW);
+  __syncthreads();
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------------- producer
+    const T* __restrict__ A = reinterpret_cast<const T*>(p.A);
+    const uint64_t pol = policy_evict_first();
+    constexpr int NPIECE = MT * 8 * (KS / 8);
+    for (int i = 0; i < nst; ++i) {
+      const int s = i % kDecStages;
+      const uint32_t ph = (i / kDecStages) & 1;
+      mbar_wait(&empty_bar[s], ph ^ 1);
+      uint8_t* st = sbase + s * STAGE_BYTES;
+      const int k0 = kbeg + i * KS;
+      if (lane == 0) {
+        mbar_expect_tx(&full_bar[s], kStageW);
+        tma_load_2d(st, &tmW, &full_bar[s], k0 * BITS / 8, n0, pol);
+      }
+      const uint32_t act = smem_u32(st + kStageW);
+#pragma unroll 4
+      for (int pc = lane; pc < NPIECE; pc += 32) {
+        const int tl = pc / (KS / 8);          // local token
+        const int kl = (pc % (KS / 8)) * 8;    // local k of this 8-element piece
+        const int tok = tok0 + tl;
+        const int kk = kl / KCH, r = kl % KCH, t = r / SEG, w16 = (r % SEG) / 8;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (tok < M && k0 + kl < kend) v = ldg_keep(A + (size_t)tok * K + k0 + kl);
+        if (BITS == 4) {
+          v = make_uint4(prmt(v.x, v.z, 0x5410u), prmt(v.x, v.z, 0x7632u), prmt(v.y, v.w, 0x5410u),
+                         prmt(v.y, v.w, 0x7632u));
+        }
+        sts128(act + tl * TOK + kk * (KCH * 2) + (w16 * 4 + t) * 16, v);
+      }
+      mbar_arrive(&full_bar[s]);
+    }
+    return;
   }
 
-  float acc[RT][MT][4];
+  // --------------------------------------------------------------------------- consumers
+  const T* __restrict__ S = reinterpret_cast<const T*>(p.scales);
+  const int cw = warp - 1;
+  const int gq = lane >> 2, t = lane & 3;
+  int Rg[2], Rh[2], ng[2], nh[2];
 #pragma unroll
-  for (int r = 0; r < RT; ++r)
+  for (int rt = 0; rt < 2; ++rt) {
+    Rg[rt] = cw * 32 + rt * 16 + prow(gq);
+    Rh[rt] = Rg[rt] + 8;
+    ng[rt] = min(n0 + Rg[rt], N - 1);
+    nh[rt] = min(n0 + Rh[rt], N - 1);
+  }
+  float acc[2][MT][4];
+#pragma unroll
+  for (int rt = 0; rt < 2; ++rt)
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) acc[r][mt][i] = 0.f;
+      for (int i = 0; i < 4; ++i) acc[rt][mt][i] = 0.f;
 
-  auto load_w = [&](uint4 (&wr)[RT][2], int kc) {
-    const int k = kc + t * SEG;
-    const bool ok = k < kend;
+  for (int i = 0; i < nst; ++i) {
+    const int s = i % kDecStages;
+    const uint32_t ph = (i / kDecStages) & 1;
+    const int k0 = kbeg + i * KS;
+    // scales of this stage's chunks (issued before the wait to hide their latency)
+    float sg[CHUNKS][2], sh[CHUNKS][2];
+    if (SACC) {
 #pragma unroll
-    for (int r = 0; r < RT; ++r)
+      for (int kk = 0; kk < CHUNKS; ++kk) {
+        const size_t j = (size_t)min((k0 + kk * KCH) / p.group, K / p.group - 1) * N;
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
-        wr[r][h] = ok ? ldg_stream(wrow[r][h] + (size_t)k * BITS / 8) : make_uint4(0, 0, 0, 0);
-  };
-
-  uint4 wcur[RT][2], wnxt[RT][2];
-  load_w(wcur, kbeg);
-  for (int kc = kbeg; kc < kend; kc += KCH) {
-    if (kc + KCH < kend) load_w(wnxt, kc + KCH);
-    const int k = kc + t * SEG;
-    const bool kok = k < kend;
-    // activation fragments for this thread's K segment: per word 2 regs (b0,b1) per step
-    uint32_t bfr[MT][WORDS][4];
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-      const bool ok = kok && tok_ok[mt];
-      if (BITS == 4) {
-#pragma unroll
-        for (int w = 0; w < WORDS; ++w) {
-          const uint4 r = ok ? ldg_keep(arow[mt] + k + w * 8) : make_uint4(0, 0, 0, 0);
-          bfr[mt][w][0] = prmt(r.x, r.z, 0x5410u);  // (o0,o4)
-          bfr[mt][w][1] = prmt(r.x, r.z, 0x7632u);  // (o1,o5)
-          bfr[mt][w][2] = prmt(r.y, r.w, 0x5410u);  // (o2,o6)
-          bfr[mt][w][3] = prmt(r.y, r.w, 0x7632u);  // (o3,o7)
-        }
-      } else {
-#pragma unroll
-        for (int w2 = 0; w2 < 2; ++w2) {
-          const uint4 r = ok ? ldg_keep(arow[mt] + k + w2 * 8) : make_uint4(0, 0, 0, 0);
-          bfr[mt][2 * w2][0] = r.x; bfr[mt][2 * w2][1] = r.y;
-          bfr[mt][2 * w2 + 1][0] = r.z; bfr[mt][2 * w2 + 1][1] = r.w;
+        for (int rt = 0; rt < 2; ++rt) {
+          sg[kk][rt] = Dt<T>::to_f(__ldg(S + j + ng[rt]));
+          sh[kk][rt] = Dt<T>::to_f(__ldg(S + j + nh[rt]));
         }
       }
     }
-    float part[RT][MT][4];
-    if (SACC) {
+    mbar_wait(&full_bar[s], ph);
+    const uint32_t wst = smem_u32(sbase + s * STAGE_BYTES);
+    const uint32_t act = wst + kStageW;
 #pragma unroll
-      for (int r = 0; r < RT; ++r)
+    for (int kk = 0; kk < CHUNKS; ++kk) {
+      uint4 b[MT][PIECES];
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
+      for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-          for (int i = 0; i < 4; ++i) part[r][mt][i] = 0.f;
-    }
+        for (int w16 = 0; w16 < PIECES; ++w16)
+          b[mt][w16] = lds128(act + (mt * 8 + gq) * TOK + kk * (KCH * 2) + (w16 * 4 + t) * 16);
+      const int cell = kk * 4 + t;
 #pragma unroll
-    for (int r = 0; r < RT; ++r) {
-      const uint32_t wg[4] = {wcur[r][0].x, wcur[r][0].y, wcur[r][0].z, wcur[r][0].w};
-      const uint32_t wh[4] = {wcur[r][1].x, wcur[r][1].y, wcur[r][1].z, wcur[r][1].w};
+      for (int rt = 0; rt < 2; ++rt) {
+        const uint4 wg = lds128(wst + Rg[rt] * kWBytesPerRow + ((cell ^ (Rg[rt] & 7)) << 4));
+        const uint4 wh = lds128(wst + Rh[rt] * kWBytesPerRow + ((cell ^ (Rh[rt] & 7)) << 4));
+        const uint32_t wgw[4] = {wg.x, wg.y, wg.z, wg.w};
+        const uint32_t whw[4] = {wh.x, wh.y, wh.z, wh.w};
+        float part[MT][4];
+        if (SACC) {
 #pragma unroll
-      for (int w = 0; w < WORDS; ++w) {
-        uint32_t sg = 0, sh = 0;
-        if (!SACC) {
-          const int j = (k + w * KPW) / p.group;
-          const int ng = min(rowbase + r * 16 + gq, N - 1), nh = min(ng + 8, N - 1);
-          sg = splat_scale<T>(S, (size_t)j * N + ng);
-          sh = splat_scale<T>(S, (size_t)j * N + nh);
+          for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) part[mt][q] = 0.f;
         }
-        if (BITS == 4) {
-          uint32_t qg[4], qh[4];
-          i4_pairs<T>(wg[w], qg);
-          i4_pairs<T>(wh[w], qh);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          uint32_t sgs = 0, shs = 0;
           if (!SACC) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i) { qg[i] = mul2<T>(qg[i], sg); qh[i] = mul2<T>(qh[i], sh); }
+            const int kw = k0 + kk * KCH + t * SEG + w * (SEG / 4);
+            const size_t j = (size_t)min(kw / p.group, K / p.group - 1) * N;
+            sgs = splat_scale<T>(S, j + ng[rt]);
+            shs = splat_scale<T>(S, j + nh[rt]);
           }
+          if (BITS == 4) {
+            uint32_t qg[4], qh[4];
+            i4_pairs<T>(wgw[w], qg);
+            i4_pairs<T>(whw[w], qh);
+            if (!SACC) {
 #pragma unroll
-          for (int pp = 0; pp < 2; ++pp) {
-            const uint32_t a[4] = {qg[2 * pp], qh[2 * pp], qg[2 * pp + 1], qh[2 * pp + 1]};
+              for (int q = 0; q < 4; ++q) { qg[q] = mul2<T>(qg[q], sgs); qh[q] = mul2<T>(qh[q], shs); }
+            }
+#pragma unroll
+            for (int pp = 0; pp < 2; ++pp) {
+              const uint32_t a[4] = {qg[2 * pp], qh[2 * pp], qg[2 * pp + 1], qh[2 * pp + 1]};
+#pragma unroll
+              for (int mt = 0; mt < MT; ++mt) {
+                const uint32_t b0 = pp ? b[mt][w].z : b[mt][w].x;
+                const uint32_t b1 = pp ? b[mt][w].w : b[mt][w].y;
+                if (SACC) mma16816<T>(part[mt], a, b0, b1);
+                else mma16816<T>(acc[rt][mt], a, b0, b1);
+              }
+            }
+          } else {
+            uint32_t qg[2], qh[2];
+            i8_pairs<T>(wgw[w], qg);
+            i8_pairs<T>(whw[w], qh);
+            if (!SACC) {
+#pragma unroll
+              for (int q = 0; q < 2; ++q) { qg[q] = mul2<T>(qg[q], sgs); qh[q] = mul2<T>(qh[q], shs); }
+            }
+            const uint32_t a[4] = {qg[0], qh[0], qg[1], qh[1]};
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt) {
-              if (SACC)
-                mma16816<T>(part[r][mt], a, bfr[mt][w][2 * pp], bfr[mt][w][2 * pp + 1], part[r][mt]);
-              else
-                mma16816<T>(acc[r][mt], a, bfr[mt][w][2 * pp], bfr[mt][w][2 * pp + 1], acc[r][mt]);
+              const uint4 bb = b[mt][w >> 1];
+              const uint32_t b0 = (w & 1) ? bb.z : bb.x;
+              const uint32_t b1 = (w & 1) ? bb.w : bb.y;
+              if (SACC) mma16816<T>(part[mt], a, b0, b1);
+              else mma16816<T>(acc[rt][mt], a, b0, b1);
             }
           }
-        } else {
-          uint32_t qg[2], qh[2];
-          i8_pairs<T>(wg[w], qg);
-          i8_pairs<T>(wh[w], qh);
-          if (!SACC) {
-#pragma unroll
-            for (int i = 0; i < 2; ++i) { qg[i] = mul2<T>(qg[i], sg); qh[i] = mul2<T>(qh[i], sh); }
-          }
-          const uint32_t a[4] = {qg[0], qh[0], qg[1], qh[1]};
+        }
+        if (SACC) {
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt) {
-            if (SACC)
-              mma16816<T>(part[r][mt], a, bfr[mt][w][0], bfr[mt][w][1], part[r][mt]);
-            else
-              mma16816<T>(acc[r][mt], a, bfr[mt][w][0], bfr[mt][w][1], acc[r][mt]);
+            acc[rt][mt][0] = fmaf(sg[kk][rt], part[mt][0], acc[rt][mt][0]);
+            acc[rt][mt][1] = fmaf(sg[kk][rt], part[mt][1], acc[rt][mt][1]);
+            acc[rt][mt][2] = fmaf(sh[kk][rt], part[mt][2], acc[rt][mt][2]);
+            acc[rt][mt][3] = fmaf(sh[kk][rt], part[mt][3], acc[rt][mt][3]);
           }
         }
       }
     }
-    if (SACC) {
-      const int j = kc / p.group;
-#pragma unroll
-      for (int r = 0; r < RT; ++r) {
-        const int ng = min(rowbase + r * 16 + gq, N - 1), nh = min(ng + 8, N - 1);
-        const float s_g = load_scale_f<T>(S, (size_t)j * N + ng);
-        const float s_h = load_scale_f<T>(S, (size_t)j * N + nh);
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-          acc[r][mt][0] = fmaf(s_g, part[r][mt][0], acc[r][mt][0]);
-          acc[r][mt][1] = fmaf(s_g, part[r][mt][1], acc[r][mt][1]);
-          acc[r][mt][2] = fmaf(s_h, part[r][mt][2], acc[r][mt][2]);
-          acc[r][mt][3] = fmaf(s_h, part[r][mt][3], acc[r][mt][3]);
-        }
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < RT; ++r)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) wcur[r][h] = wnxt[r][h];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[s]);
   }
 
-  // ---------------------------------------------------------------- epilogue (+ fused A5 fixup)
+  // ------------------------------------------------------------- epilogue (+ fused A5 fixup)
+  auto out_idx = [&](int rt, int mt, int i, int& n, int& tok) {
+    n = n0 + ((i >> 1) ? Rh[rt] : Rg[rt]);
+    tok = tok0 + mt * 8 + 2 * t + (i & 1);
+  };
   auto store_out = [&](int tok, int n, float v) {
     const size_t o = (size_t)tok * N + n;
     if (p.cdt == FQ_FP32) reinterpret_cast<float*>(p.C)[o] = v;
@@ -312,54 +358,50 @@ __global__ void __launch_bounds__(kGemvThreads, 2) gemv_kernel(const GemvParams 
   const int S_ = gridDim.y;
   if (S_ == 1) {
 #pragma unroll
-    for (int r = 0; r < RT; ++r)
+    for (int rt = 0; rt < 2; ++rt)
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const int n = rowbase + r * 16 + gq + (i >> 1) * 8;
-          const int tok = tok0 + mt * 8 + 2 * t + (i & 1);
-          if (n < N && tok < M) store_out(tok, n, acc[r][mt][i]);
+          int n, tok;
+          out_idx(rt, mt, i, n, tok);
+          if (n < N && tok < M) store_out(tok, n, acc[rt][mt][i]);
         }
     return;
   }
   float* part_out = p.ws + (size_t)blockIdx.y * M * N;
 #pragma unroll
-  for (int r = 0; r < RT; ++r)
+  for (int rt = 0; rt < 2; ++rt)
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const int n = rowbase + r * 16 + gq + (i >> 1) * 8;
-        const int tok = tok0 + mt * 8 + 2 * t + (i & 1);
-        if (n < N && tok < M) __stcg(part_out + (size_t)tok * N + n, acc[r][mt][i]);
+        int n, tok;
+        out_idx(rt, mt, i, n, tok);
+        if (n < N && tok < M) __stcg(part_out + (size_t)tok * N + n, acc[rt][mt][i]);
       }
   __threadfence();
-  __shared__ int s_last;
-  __syncthreads();
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * kConsumerWarps));
   int* ctr = p.counters + blockIdx.z * gridDim.x + blockIdx.x;
-  if (threadIdx.x == 0) {
-    const int prev = atomicAdd(ctr, 1);
-    s_last = (prev == S_ - 1);
-  }
-  __syncthreads();
+  if (threadIdx.x == 32) s_last = (atomicAdd(ctr, 1) == S_ - 1);
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * kConsumerWarps));
   if (!s_last) return;
   __threadfence();
 #pragma unroll
-  for (int r = 0; r < RT; ++r)
+  for (int rt = 0; rt < 2; ++rt)
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const int n = rowbase + r * 16 + gq + (i >> 1) * 8;
-        const int tok = tok0 + mt * 8 + 2 * t + (i & 1);
+        int n, tok;
+        out_idx(rt, mt, i, n, tok);
         if (n < N && tok < M) {
           float v = 0.f;
           for (int s = 0; s < S_; ++s) v += __ldcg(p.ws + ((size_t)s * M + tok) * N + n);
           store_out(tok, n, v);
         }
       }
-  if (threadIdx.x == 0) *ctr = 0;  // self-reset for the next call / graph replay
+  if (threadIdx.x == 32) *ctr = 0;  // self-reset for the next call / graph replay
 }
 
 // ------------------------------------------------------------------------------------- host side
@@ -368,29 +410,34 @@ static int env_int(const char* name, int dflt) {
   return v ? std::atoi(v) : dflt;
 }
 
+template <int BITS, int MT>
+static constexpr int dec_smem_bytes() {
+  using G = DecGeom<BITS>;
+  return kDecStages * (kStageW + ((MT * 8 * G::TOK_BYTES + 1023) / 1024) * 1024) + 1024;
+}
+
 GemvPlan plan_gemv(int M, int K, int N, int bits, int group, int nsm) {
+  (void)group;
   GemvPlan p{};
-  p.kchunk = bits == 4 ? 128 : 64;
+  p.kchunk = bits == 4 ? 256 : 128;  // K per pipeline stage (splits are multiples of it)
   p.mt = M <= 8 ? 1 : 2;
   p.ktiles = (M + 15) / 16;
-  p.rt = env_int("FQ_GEMV_RT", N >= 128 * 2 * 64 ? 2 : 1);
-  if (p.rt != 1 && p.rt != 2) p.rt = 2;
-  p.rows_per_cta = 128 * p.rt;
+  p.rt = 2;
+  p.rows_per_cta = kRowsPerCta;
   const int gx = (N + p.rows_per_cta - 1) / p.rows_per_cta;
   const int nchunks = (K + p.kchunk - 1) / p.kchunk;
-  const int slots = 2 * nsm;  // 2 CTAs per SM (launch bounds)
+  const int slots = 2 * nsm;  // 2 CTAs per SM (launch bounds + smem)
   int best_s = 1;
-  double best = -1.0;
+  double best = -1e30;
   const int smax = std::min(nchunks, 64);
   for (int s = 1; s <= smax; ++s) {
     const int klen = ((nchunks + s - 1) / s) * p.kchunk;
-    const int s_eff = (K + klen - 1) / klen;
-    if (s_eff != s) continue;
+    if ((K + klen - 1) / klen != s) continue;
     const double ctas = (double)gx * s * p.ktiles;
     const double waves = ctas / slots;
     const double eff = waves / std::ceil(waves);
-    // prefer full waves; among near-equal efficiencies prefer fewer splits (partial traffic)
-    const double score = eff - 0.004 * s - (waves < 0.9 ? 1.0 : 0.0) * (1.0 - waves);
+    // full waves first; a few waves smooth per-SM imbalance; fewer splits = less partial traffic
+    const double score = eff + 0.02 * std::min(waves, 4.0) - 0.003 * s * (M > 4 ? 2 : 1);
     if (score > best + 1e-9) { best = score; best_s = s; }
   }
   int s = env_int("FQ_GEMV_SPLITS", best_s);
@@ -408,39 +455,49 @@ size_t gemv_workspace_bytes(const GemvPlan& p, int M, int N) {
   return align256((size_t)p.splits * M * N * sizeof(float)) + align256((size_t)gx * p.ktiles * sizeof(int));
 }
 
-template <typename T, int BITS, int MT, bool SACC, int RT>
-static cudaError_t launch_gemv(const GemvPlan& pl, const GemvParams& prm, cudaStream_t st) {
+template <typename T, int BITS, int MT, bool SACC>
+static cudaError_t launch_dec(const GemvPlan& pl, const CUtensorMap& tm, const DecodeParams& prm,
+                              cudaStream_t st) {
+  constexpr int smem = dec_smem_bytes<BITS, MT>();
+  auto kern = decode_kernel<T, BITS, MT, SACC>;
+  static bool attr_set = false;  // benign race: idempotent attribute call
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
   const int gx = (prm.N + pl.rows_per_cta - 1) / pl.rows_per_cta;
   dim3 grid(gx, pl.splits, pl.ktiles);
-  gemv_kernel<T, BITS, MT, SACC, RT><<<grid, kGemvThreads, 0, st>>>(prm);
+  kern<<<grid, kDecThreads, smem, st>>>(tm, prm);
   return cudaGetLastError();
 }
 
-template <typename T, int BITS, int MT, bool SACC>
-static cudaError_t dispatch_rt(const GemvPlan& pl, const GemvParams& prm, cudaStream_t st) {
-  return pl.rt == 1 ? launch_gemv<T, BITS, MT, SACC, 1>(pl, prm, st)
-                    : launch_gemv<T, BITS, MT, SACC, 2>(pl, prm, st);
-}
 template <typename T, int BITS, int MT>
-static cudaError_t dispatch_sacc(bool sacc, const GemvPlan& pl, const GemvParams& prm, cudaStream_t st) {
-  return sacc ? dispatch_rt<T, BITS, MT, true>(pl, prm, st) : dispatch_rt<T, BITS, MT, false>(pl, prm, st);
+static cudaError_t dispatch_sacc(bool sacc, const GemvPlan& pl, const CUtensorMap& tm,
+                                 const DecodeParams& prm, cudaStream_t st) {
+  return sacc ? launch_dec<T, BITS, MT, true>(pl, tm, prm, st) : launch_dec<T, BITS, MT, false>(pl, tm, prm, st);
 }
 template <typename T, int BITS>
-static cudaError_t dispatch_mt(bool sacc, const GemvPlan& pl, const GemvParams& prm, cudaStream_t st) {
-  return pl.mt == 1 ? dispatch_sacc<T, BITS, 1>(sacc, pl, prm, st) : dispatch_sacc<T, BITS, 2>(sacc, pl, prm, st);
+static cudaError_t dispatch_mt(bool sacc, const GemvPlan& pl, const CUtensorMap& tm,
+                               const DecodeParams& prm, cudaStream_t st) {
+  return pl.mt == 1 ? dispatch_sacc<T, BITS, 1>(sacc, pl, tm, prm, st)
+                    : dispatch_sacc<T, BITS, 2>(sacc, pl, tm, prm, st);
 }
 template <typename T>
-static cudaError_t dispatch_bits(int bits, bool sacc, const GemvPlan& pl, const GemvParams& prm,
-                                 cudaStream_t st) {
-  return bits == 4 ? dispatch_mt<T, 4>(sacc, pl, prm, st) : dispatch_mt<T, 8>(sacc, pl, prm, st);
+static cudaError_t dispatch_bits(int bits, bool sacc, const GemvPlan& pl, const CUtensorMap& tm,
+                                 const DecodeParams& prm, cudaStream_t st) {
+  return bits == 4 ? dispatch_mt<T, 4>(sacc, pl, tm, prm, st) : dispatch_mt<T, 8>(sacc, pl, tm, prm, st);
 }
 
 cudaError_t run_gemv(const GemvPlan& pl, int adt, int cdt, int bits, const void* A, int M, int K,
                      int N, const void* codes, const void* scales, int group, void* C, void* ws,
                      cudaStream_t st) {
-  GemvParams prm{};
+  CUtensorMap tm;
+  const uint64_t row_bytes = (uint64_t)K * bits / 8;
+  if (!make_tmap_2d(&tm, codes, 1, row_bytes, (uint64_t)N, row_bytes, kWBytesPerRow, kRowsPerCta, 1))
+    return cudaErrorInvalidValue;
+  DecodeParams prm{};
   prm.A = A;
-  prm.codes = reinterpret_cast<const uint8_t*>(codes);
   prm.scales = scales;
   prm.C = C;
   prm.M = M; prm.K = K; prm.N = N; prm.group = group; prm.cdt = cdt;
@@ -448,9 +505,10 @@ cudaError_t run_gemv(const GemvPlan& pl, int adt, int cdt, int bits, const void*
   prm.ws = reinterpret_cast<float*>(ws);
   const size_t part = align256((size_t)pl.splits * M * N * sizeof(float));
   prm.counters = reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + (pl.splits > 1 ? part : 0));
-  const bool sacc = (group % pl.kchunk) == 0;
-  return adt == FQ_BF16 ? dispatch_bits<__nv_bfloat16>(bits, sacc, pl, prm, st)
-                        : dispatch_bits<__half>(bits, sacc, pl, prm, st);
+  const int chunk = bits == 4 ? 128 : 64;  // K per MMA chunk (one scale per chunk if SACC)
+  const bool sacc = (group % chunk) == 0;
+  return adt == FQ_BF16 ? dispatch_bits<__nv_bfloat16>(bits, sacc, pl, tm, prm, st)
+                        : dispatch_bits<__half>(bits, sacc, pl, tm, prm, st);
 }
 
 }  // namespace fq

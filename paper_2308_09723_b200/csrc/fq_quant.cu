@@ -10,24 +10,30 @@
 // A1 follows P:147-149 §3.3 under reading R6: level L fires iff some child group range is below
 // alpha * its parent's range, compared exactly as 1000*child < alpha_milli*parent in fp64.
 //
-// Layout: one CTA per paper column n (= row n of the stored [N, K] matrix).  Pass 1 streams the
-// row once from HBM with 16-byte loads and writes one max|.| per 8-element chunk to shared memory;
-// pass 2 reduces chunks to groups; pass 3 re-reads the row (L2-resident: the CTA just read it),
-// computes codes and writes them coalesced.  HBM traffic = read W once + write codes/scales.
+// Layout: one CTA per paper column n (= row n of the stored [N, K] matrix), sized so each thread
+// holds <= 8 chunks of 8 elements.  Pass 1 streams the row once from HBM with 16-byte loads, keeps
+// the raw chunks in registers and writes one max|.| per chunk to shared memory; pass 2 reduces
+// chunks to groups and writes the scales; pass 3 turns the register-resident chunks into codes,
+// written coalesced.  HBM traffic = read W once + write codes/scales (the algorithmic minimum).
 #include "fq_common.cuh"
 #include "fq_internal.h"
 
 namespace fq {
 
+// One 8-element chunk of a weight row kept in its raw storage format (16 B bf16/fp16, 32 B fp32).
 template <typename TIn>
 struct Chunk8 {
-  float v[8];
-  __device__ __forceinline__ void load(const TIn* p);
+  static constexpr int NV = sizeof(TIn) / 2;  // uint4 words
+  uint4 r[NV];
+  __device__ __forceinline__ void load(const TIn* p) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) r[i] = ldg_keep(reinterpret_cast<const uint4*>(p) + i);
+  }
+  __device__ __forceinline__ void decode(float (&v)[8]) const;
 };
 template <>
-__device__ __forceinline__ void Chunk8<__nv_bfloat16>::load(const __nv_bfloat16* p) {
-  uint4 r = ldg_keep(p);
-  uint32_t w[4] = {r.x, r.y, r.z, r.w};
+__device__ __forceinline__ void Chunk8<__nv_bfloat16>::decode(float (&v)[8]) const {
+  const uint32_t w[4] = {r[0].x, r[0].y, r[0].z, r[0].w};
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     v[2 * i] = __uint_as_float(w[i] << 16);
@@ -35,9 +41,8 @@ __device__ __forceinline__ void Chunk8<__nv_bfloat16>::load(const __nv_bfloat16*
   }
 }
 template <>
-__device__ __forceinline__ void Chunk8<__half>::load(const __half* p) {
-  uint4 r = ldg_keep(p);
-  const __half2* h = reinterpret_cast<const __half2*>(&r);
+__device__ __forceinline__ void Chunk8<__half>::decode(float (&v)[8]) const {
+  const __half2* h = reinterpret_cast<const __half2*>(&r[0]);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     float2 f = __half22float2(h[i]);
@@ -46,12 +51,11 @@ __device__ __forceinline__ void Chunk8<__half>::load(const __half* p) {
   }
 }
 template <>
-__device__ __forceinline__ void Chunk8<float>::load(const float* p) {
-  uint4 a = ldg_keep(p), b = ldg_keep(p + 4);
-  v[0] = __uint_as_float(a.x); v[1] = __uint_as_float(a.y);
-  v[2] = __uint_as_float(a.z); v[3] = __uint_as_float(a.w);
-  v[4] = __uint_as_float(b.x); v[5] = __uint_as_float(b.y);
-  v[6] = __uint_as_float(b.z); v[7] = __uint_as_float(b.w);
+__device__ __forceinline__ void Chunk8<float>::decode(float (&v)[8]) const {
+  v[0] = __uint_as_float(r[0].x); v[1] = __uint_as_float(r[0].y);
+  v[2] = __uint_as_float(r[0].z); v[3] = __uint_as_float(r[0].w);
+  v[4] = __uint_as_float(r[1].x); v[5] = __uint_as_float(r[1].y);
+  v[6] = __uint_as_float(r[1].z); v[7] = __uint_as_float(r[1].w);
 }
 
 // max|x| over a chunk; +inf if any element is non-finite (the group is then flagged).
@@ -69,8 +73,10 @@ __device__ __forceinline__ float chunk_amax(const float (&v)[8]) {
 constexpr int kQThreads = 256;
 
 // ------------------------------------------------------------------------------------- A3
-template <typename TIn, typename TS, int BITS>
-__global__ void __launch_bounds__(kQThreads) quantize_kernel(const TIn* __restrict__ W, int K,
+constexpr int kQCpt = 8;  // chunks per thread cached in registers by the quantizer
+
+template <typename TIn, typename TS, int BITS, int CPT = kQCpt>
+__global__ void __launch_bounds__(sizeof(TIn) == 4 ? 512 : 1024) quantize_kernel(const TIn* __restrict__ W, int K,
                                                              int N, int group,
                                                              uint8_t* __restrict__ codes,
                                                              TS* __restrict__ scales,
@@ -86,11 +92,19 @@ __global__ void __launch_bounds__(kQThreads) quantize_kernel(const TIn* __restri
   const TIn* row = W + (size_t)n * K;
   if (threadIdx.x == 0) s_status = 0;
 
-  // pass 1: chunk maxima
-  for (int c = threadIdx.x; c < nchunk; c += kQThreads) {
-    Chunk8<TIn> ch;
-    ch.load(row + (size_t)c * 8);
-    pm[c] = chunk_amax(ch.v);
+  // pass 1: chunk maxima; the raw chunks stay in registers for pass 3 (CPT chunks per thread,
+  // the launcher sizes the CTA so that K <= 8 * CPT * blockDim.x) — W is read from HBM once.
+  const int T = blockDim.x;
+  Chunk8<TIn> raw[CPT];
+#pragma unroll
+  for (int i = 0; i < CPT; ++i) {
+    const int c = threadIdx.x + i * T;
+    if (c < nchunk) {
+      raw[i].load(row + (size_t)c * 8);
+      float v[8];
+      raw[i].decode(v);
+      pm[c] = chunk_amax(v);
+    }
   }
   __syncthreads();
 
@@ -117,13 +131,13 @@ __global__ void __launch_bounds__(kQThreads) quantize_kernel(const TIn* __restri
     if (st) atomicOr(&s_status, st);
   };
   if (cpg <= 32) {
-    for (int j = threadIdx.x; j < G; j += kQThreads) {
+    for (int j = threadIdx.x; j < G; j += T) {
       float m = 0.f;
       for (int i = 0; i < cpg; ++i) m = fmaxf(m, pm[j * cpg + i]);  // fmaxf keeps +inf
       finish_group(j, m);
     }
   } else {
-    for (int j = warp; j < G; j += kQThreads / 32) {
+    for (int j = warp; j < G; j += T / 32) {
       float m = 0.f;
       for (int i = lane; i < cpg; i += 32) m = fmaxf(m, pm[j * cpg + i]);
 #pragma unroll
@@ -135,9 +149,12 @@ __global__ void __launch_bounds__(kQThreads) quantize_kernel(const TIn* __restri
 
   // pass 3: codes
   constexpr int lo = -(1 << (BITS - 1)), hi = (1 << (BITS - 1)) - 1;
-  for (int c = threadIdx.x; c < nchunk; c += kQThreads) {
-    Chunk8<TIn> ch;
-    ch.load(row + (size_t)c * 8);
+#pragma unroll
+  for (int ci = 0; ci < CPT; ++ci) {
+    const int c = threadIdx.x + ci * T;
+    if (c >= nchunk) break;
+    float v[8];
+    raw[ci].decode(v);
     const float s = sc[c / cpg];
     int q[8];
 #pragma unroll
@@ -146,9 +163,9 @@ __global__ void __launch_bounds__(kQThreads) quantize_kernel(const TIn* __restri
       if (s == 0.f) {
         r = 0.f;
       } else if (Dt<TIn>::id == FQ_FP32) {
-        r = (float)round((double)ch.v[i] / (double)s);
+        r = (float)round((double)v[i] / (double)s);
       } else {
-        r = roundf(__fdiv_rn(ch.v[i], s));
+        r = roundf(__fdiv_rn(v[i], s));
       }
       r = fminf(fmaxf(r, (float)lo), (float)hi);
       q[i] = (int)r;
@@ -191,10 +208,13 @@ __global__ void __launch_bounds__(kQThreads) adapt_flags_kernel(const TIn* __res
   if (threadIdx.x == 0) s_status = 0;
   const int n = blockIdx.x;
   const TIn* row = W + (size_t)n * K;
+#pragma unroll 4
   for (int c = threadIdx.x; c < nchunk; c += kQThreads) {
     Chunk8<TIn> ch;
     ch.load(row + (size_t)c * 8);
-    pm[c] = chunk_amax(ch.v);
+    float v[8];
+    ch.decode(v);
+    pm[c] = chunk_amax(v);
   }
   __syncthreads();
   // finest level L = nlev-1 stored at lev[0 .. Gf)
@@ -238,7 +258,12 @@ static cudaError_t launch_quant(const void* W, int K, int N, int group, void* co
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  kern<<<N, kQThreads, smem, st>>>((const TIn*)W, K, N, group, (uint8_t*)codes, (TS*)scales, status);
+  // threads: enough that every 8-element chunk is cached in registers (<= kQCpt per thread)
+  const int nchunk = K / 8;
+  int threads = ((nchunk + kQCpt - 1) / kQCpt + 31) / 32 * 32;
+  threads = threads < 128 ? 128 : threads;
+  if (threads > (sizeof(TIn) == 4 ? 512 : 1024)) return cudaErrorInvalidValue;  // rejected by the API
+  kern<<<N, threads, smem, st>>>((const TIn*)W, K, N, group, (uint8_t*)codes, (TS*)scales, status);
   return cudaGetLastError();
 }
 
