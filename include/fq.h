@@ -101,7 +101,8 @@ fq_status fq_adapt_flags(const void* W, int32_t wdt, int64_t K, int64_t N, uint3
 int32_t fq_adapt_decide(int64_t K, int32_t min_group, const int32_t* flags_host);
 
 /* ---------------------------------------------------------------------------------------------
- * Quantize + pack (kernel A3), App. A with groups:
+ * Quantize + pack (kernel A3), App. A with groups.  K <= 65536 for 16-bit W,
+ * K <= 32768 for fp32 W (one CTA holds a whole column in registers), else FQ_ERR_SHAPE.
  *   s[j,n] = RNE_scale_dtype( 2 * max_{k in group j} |W[n,k]| / (2^bits - 1) )   (one rounding)
  *   q[n,k] = clamp( round_half_away( W[n,k] / s[k/group, n] ), -2^(bits-1), 2^(bits-1)-1 ),
  *            q = 0 where s == 0.
@@ -116,9 +117,10 @@ fq_status fq_quantize(const void* W, int32_t wdt, const fq_wdesc* d, void* codes
  *   C[m,n] = sum_k A[m,k] * q[n,k] * s[k/group, n]
  * A: [M, K] row-major, dtype adt in {BF16, FP16}; the scales must have dtype adt.
  * C: [M, N] row-major, dtype cdt in {adt, FP32} (FP32 is a diagnostic mode).
- * ws/ws_bytes: device scratch of at least fq_gemm_workspace_bytes(M, d) bytes.  The workspace
- *   holds split-K partials and arrival counters: it must be ZERO-FILLED once before its first
- *   use; every call leaves the counters zeroed again, so it can be reused (and graph-captured)
+ * ws/ws_bytes: device scratch of at least fq_gemm_workspace_bytes(M, d) bytes.  Layout: a fixed
+ *   64 KiB region of arrival counters at offset 0, then split-K fp32 partials.  The buffer must be
+ *   ZERO-FILLED once before its first use; every call leaves the counters zeroed again, so one
+ *   buffer (sized for the largest call) can be shared by calls of any shape and graph-captured
  *   without re-clearing.  Calls sharing one ws must be stream-ordered.
  * Accumulation is fp32; results are deterministic (fixed-order split-K reduction).
  * ------------------------------------------------------------------------------------------- */

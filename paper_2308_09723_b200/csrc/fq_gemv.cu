@@ -405,6 +405,10 @@ __global__ void __launch_bounds__(kDecThreads, 2)
 }
 
 // ------------------------------------------------------------------------------------- host side
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+constexpr int kMaxCounters = 16384;
+constexpr size_t kCounterBytes = kMaxCounters * sizeof(int);
+
 static int env_int(const char* name, int dflt) {
   const char* v = std::getenv(name);
   return v ? std::atoi(v) : dflt;
@@ -442,17 +446,19 @@ GemvPlan plan_gemv(int M, int K, int N, int bits, int group, int nsm) {
   }
   int s = env_int("FQ_GEMV_SPLITS", best_s);
   s = std::max(1, std::min(s, nchunks));
+  if ((long long)gx * p.ktiles > kMaxCounters) s = 1;  // counter region is fixed-size
   p.klen = ((nchunks + s - 1) / s) * p.kchunk;
   p.splits = (K + p.klen - 1) / p.klen;
   return p;
 }
 
-static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// Workspace layout (fixed, so buffers can be shared by calls of different shapes):
+//   [0, kCounterBytes)  arrival counters (zeroed once by the caller, self-resetting)
+//   [kCounterBytes, ..) split-K fp32 partials [S][M][N] (fully overwritten by every call)
 size_t gemv_workspace_bytes(const GemvPlan& p, int M, int N) {
-  if (p.splits <= 1) return 256;
-  const int gx = (N + p.rows_per_cta - 1) / p.rows_per_cta;
-  return align256((size_t)p.splits * M * N * sizeof(float)) + align256((size_t)gx * p.ktiles * sizeof(int));
+  if (p.splits <= 1) return kCounterBytes;
+  return kCounterBytes + align256((size_t)p.splits * M * N * sizeof(float));
 }
 
 template <typename T, int BITS, int MT, bool SACC>
@@ -502,9 +508,8 @@ cudaError_t run_gemv(const GemvPlan& pl, int adt, int cdt, int bits, const void*
   prm.C = C;
   prm.M = M; prm.K = K; prm.N = N; prm.group = group; prm.cdt = cdt;
   prm.klen = pl.klen;
-  prm.ws = reinterpret_cast<float*>(ws);
-  const size_t part = align256((size_t)pl.splits * M * N * sizeof(float));
-  prm.counters = reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + (pl.splits > 1 ? part : 0));
+  prm.counters = reinterpret_cast<int*>(ws);
+  prm.ws = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + kCounterBytes);
   const int chunk = bits == 4 ? 128 : 64;  // K per MMA chunk (one scale per chunk if SACC)
   const bool sacc = (group % chunk) == 0;
   return adt == FQ_BF16 ? dispatch_bits<__nv_bfloat16>(bits, sacc, pl, tm, prm, st)

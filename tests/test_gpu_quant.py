@@ -80,7 +80,7 @@ def test_quantize_ties_all_bf16_patterns(fq):
     vals = O.decode_bits(allb, "bf16")
     allb = allb[np.isfinite(vals)]
     K = 256
-    n = (allb.size + K - 1) // K
+    n = ((allb.size + K - 1) // K + 7) // 8 * 8
     buf = np.zeros(n * K, dtype=np.uint16)
     buf[: allb.size] = allb
     W = buf.reshape(n, K)
