@@ -120,6 +120,22 @@ __device__ __forceinline__ void i4_pairs(uint32_t w, uint32_t (&q)[4]) {
   q[3] = sub2<T>(lop3_and_xor(__umulhi(w, 1u << 20), mask, Dt<T>::kMagic4), Dt<T>::kBias4);  // w >> 12
 }
 
+// Same pairs WITHOUT the subtract: the values are q + OFF exactly (OFF = 136 bf16, 1032 fp16).
+// The scale-on-accumulator path uses these and removes OFF * sum(a) per chunk afterwards (the
+// activation sums are produced once per CTA by the producer warp), saving one HADD2 per pair.
+template <typename T>
+__device__ __forceinline__ void i4_pairs_off(uint32_t w, uint32_t (&q)[4]) {
+  constexpr uint32_t mask = 0x000F000Fu;
+  q[0] = lop3_and_xor(w, mask, Dt<T>::kMagic4);
+  q[1] = lop3_and_xor(__umulhi(w, 1u << 28), mask, Dt<T>::kMagic4);  // w >> 4
+  q[2] = lop3_and_xor(w >> 8, mask, Dt<T>::kMagic4);
+  q[3] = lop3_and_xor(__umulhi(w, 1u << 20), mask, Dt<T>::kMagic4);  // w >> 12
+}
+template <typename T, int BITS> struct CodeOffset { static constexpr float v = 0.f; };
+template <> struct CodeOffset<__nv_bfloat16, 4> { static constexpr float v = 136.f; };
+template <> struct CodeOffset<__half, 4> { static constexpr float v = 1032.f; };
+template <> struct CodeOffset<__half, 8> { static constexpr float v = 1152.f; };
+
 // int8 word (k..k+3) -> natural pairs (k,k+1),(k+2,k+3) holding the exact codes.
 template <typename T>
 __device__ __forceinline__ void i8_pairs(uint32_t w, uint32_t (&q)[2]);
@@ -144,6 +160,12 @@ __device__ __forceinline__ void i8_pairs<__nv_bfloat16>(uint32_t w, uint32_t (&q
   }
 }
 
+__device__ __forceinline__ void i8_pairs_off_half(uint32_t w, uint32_t (&q)[2]) {
+  const uint32_t u = w ^ 0x80808080u;         // values 1024 + u = q + 1152
+  q[0] = prmt(u, 0x64646464u, 0x4140u);
+  q[1] = prmt(u, 0x64646464u, 0x4342u);
+}
+
 template <typename T>
 __device__ __forceinline__ uint32_t splat_scale(const T* scales, size_t idx) {
   const unsigned short s = __ldg(reinterpret_cast<const unsigned short*>(scales) + idx);
@@ -161,7 +183,10 @@ __global__ void __launch_bounds__(kDecThreads, 2)
   constexpr int KS = G::KS, SEG = G::SEG, KCH = G::KCH, CHUNKS = G::CHUNKS, PIECES = G::PIECES;
   constexpr int TOK = G::TOK_BYTES;
   constexpr int ACT_BYTES = MT * 8 * TOK;
-  constexpr int STAGE_BYTES = kStageW + ((ACT_BYTES + 1023) / 1024) * 1024;
+  constexpr int SA_BYTES = MT * 8 * CHUNKS * 4;  // fp32 activation sums [token][chunk]
+  constexpr int STAGE_BYTES = kStageW + ((ACT_BYTES + SA_BYTES + 1023) / 1024) * 1024;
+  constexpr float OFF = SACC ? CodeOffset<T, BITS>::v : 0.f;
+  constexpr int PPC = KCH / 8;  // 8-element pieces per chunk (16 int4, 8 int8): divides 32
 
   extern __shared__ __align__(1024) uint8_t dsmem[];
   __shared__ __align__(8) uint64_t full_bar[kDecStages], empty_bar[kDecStages];
@@ -202,6 +227,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
         tma_load_2d(st, &tmW, &full_bar[s], k0 * BITS / 8, n0, pol);
       }
       const uint32_t act = smem_u32(st + kStageW);
+      static_assert(NPIECE % 32 == 0, "pieces per stage must be a multiple of the warp size");
 #pragma unroll 4
       for (int pc = lane; pc < NPIECE; pc += 32) {
         const int tl = pc / (KS / 8);          // local token
@@ -210,6 +236,24 @@ __global__ void __launch_bounds__(kDecThreads, 2)
         const int kk = kl / KCH, r = kl % KCH, t = r / SEG, w16 = (r % SEG) / 8;
         uint4 v = make_uint4(0, 0, 0, 0);
         if (tok < M && k0 + kl < kend) v = ldg_keep(A + (size_t)tok * K + k0 + kl);
+        if (OFF != 0.f) {
+          // sum of the 8 activations, reduced over the PPC lanes of this chunk (aligned groups)
+          float sum = 0.f;
+          const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if (Dt<T>::id == FQ_BF16) {
+              sum += __uint_as_float(vv[e] << 16) + __uint_as_float(vv[e] & 0xFFFF0000u);
+            } else {
+              const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&vv[e]));
+              sum += f.x + f.y;
+            }
+          }
+#pragma unroll
+          for (int o = PPC / 2; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+          if ((lane % PPC) == 0)
+            reinterpret_cast<float*>(st + kStageW + ACT_BYTES)[kk * (MT * 8) + tl] = sum;
+        }
         if (BITS == 4) {
           v = make_uint4(prmt(v.x, v.z, 0x5410u), prmt(v.x, v.z, 0x7632u), prmt(v.y, v.w, 0x5410u),
                          prmt(v.y, v.w, 0x7632u));
@@ -294,8 +338,13 @@ __global__ void __launch_bounds__(kDecThreads, 2)
           }
           if (BITS == 4) {
             uint32_t qg[4], qh[4];
-            i4_pairs<T>(wgw[w], qg);
-            i4_pairs<T>(whw[w], qh);
+            if (OFF != 0.f) {
+              i4_pairs_off<T>(wgw[w], qg);
+              i4_pairs_off<T>(whw[w], qh);
+            } else {
+              i4_pairs<T>(wgw[w], qg);
+              i4_pairs<T>(whw[w], qh);
+            }
             if (!SACC) {
 #pragma unroll
               for (int q = 0; q < 4; ++q) { qg[q] = mul2<T>(qg[q], sgs); qh[q] = mul2<T>(qh[q], shs); }
@@ -313,8 +362,13 @@ __global__ void __launch_bounds__(kDecThreads, 2)
             }
           } else {
             uint32_t qg[2], qh[2];
-            i8_pairs<T>(wgw[w], qg);
-            i8_pairs<T>(whw[w], qh);
+            if (OFF != 0.f && Dt<T>::id == FQ_FP16) {
+              i8_pairs_off_half(wgw[w], qg);
+              i8_pairs_off_half(whw[w], qh);
+            } else {
+              i8_pairs<T>(wgw[w], qg);
+              i8_pairs<T>(whw[w], qh);
+            }
             if (!SACC) {
 #pragma unroll
               for (int q = 0; q < 2; ++q) { qg[q] = mul2<T>(qg[q], sgs); qh[q] = mul2<T>(qh[q], shs); }
@@ -333,6 +387,14 @@ __global__ void __launch_bounds__(kDecThreads, 2)
         if (SACC) {
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt) {
+            if (OFF != 0.f) {  // remove OFF * sum_k a[tok, k] (tokens 2t, 2t+1 of this MMA tile)
+              const float2 sa = *reinterpret_cast<const float2*>(
+                  sbase + s * STAGE_BYTES + kStageW + ACT_BYTES + (kk * (MT * 8) + mt * 8 + 2 * t) * 4);
+              part[mt][0] = fmaf(-OFF, sa.x, part[mt][0]);
+              part[mt][1] = fmaf(-OFF, sa.y, part[mt][1]);
+              part[mt][2] = fmaf(-OFF, sa.x, part[mt][2]);
+              part[mt][3] = fmaf(-OFF, sa.y, part[mt][3]);
+            }
             acc[rt][mt][0] = fmaf(sg[kk][rt], part[mt][0], acc[rt][mt][0]);
             acc[rt][mt][1] = fmaf(sg[kk][rt], part[mt][1], acc[rt][mt][1]);
             acc[rt][mt][2] = fmaf(sh[kk][rt], part[mt][2], acc[rt][mt][2]);
@@ -417,7 +479,7 @@ static int env_int(const char* name, int dflt) {
 template <int BITS, int MT>
 static constexpr int dec_smem_bytes() {
   using G = DecGeom<BITS>;
-  return kDecStages * (kStageW + ((MT * 8 * G::TOK_BYTES + 1023) / 1024) * 1024) + 1024;
+  return kDecStages * (kStageW + ((MT * 8 * G::TOK_BYTES + MT * 8 * G::CHUNKS * 4 + 1023) / 1024) * 1024) + 1024;
 }
 
 GemvPlan plan_gemv(int M, int K, int N, int bits, int group, int nsm) {
