@@ -216,6 +216,21 @@ __global__ void __launch_bounds__(kDecThreads, 2)
     const T* __restrict__ A = reinterpret_cast<const T*>(p.A);
     const uint64_t pol = policy_evict_first();
     constexpr int NPIECE = MT * 8 * (KS / 8);
+    static_assert(NPIECE % 32 == 0, "pieces per stage must be a multiple of the warp size");
+    constexpr int NPW = NPIECE / 32;  // 16-byte activation pieces per lane per stage
+    // Activation loads are software-pipelined one stage ahead (their L2 latency overlaps the wait
+    // for a free stage), all NPW loads of a stage in flight at once.
+    uint4 va[NPW];
+    auto load_act = [&](int k0) {
+#pragma unroll
+      for (int j = 0; j < NPW; ++j) {
+        const int pc = lane + 32 * j;
+        const int tok = tok0 + pc / (KS / 8);
+        const int kl = (pc % (KS / 8)) * 8;
+        va[j] = (tok < M && k0 + kl < kend) ? ldg_keep(A + (size_t)tok * K + k0 + kl) : make_uint4(0, 0, 0, 0);
+      }
+    };
+    load_act(kbeg);
     for (int i = 0; i < nst; ++i) {
       const int s = i % kDecStages;
       const uint32_t ph = (i / kDecStages) & 1;
@@ -227,15 +242,13 @@ __global__ void __launch_bounds__(kDecThreads, 2)
         tma_load_2d(st, &tmW, &full_bar[s], k0 * BITS / 8, n0, pol);
       }
       const uint32_t act = smem_u32(st + kStageW);
-      static_assert(NPIECE % 32 == 0, "pieces per stage must be a multiple of the warp size");
-#pragma unroll 4
-      for (int pc = lane; pc < NPIECE; pc += 32) {
+#pragma unroll
+      for (int j = 0; j < NPW; ++j) {
+        const int pc = lane + 32 * j;
         const int tl = pc / (KS / 8);          // local token
         const int kl = (pc % (KS / 8)) * 8;    // local k of this 8-element piece
-        const int tok = tok0 + tl;
         const int kk = kl / KCH, r = kl % KCH, t = r / SEG, w16 = (r % SEG) / 8;
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (tok < M && k0 + kl < kend) v = ldg_keep(A + (size_t)tok * K + k0 + kl);
+        uint4 v = va[j];
         if (OFF != 0.f) {
           // sum of the 8 activations, reduced over the PPC lanes of this chunk (aligned groups)
           float sum = 0.f;
@@ -261,6 +274,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
         sts128(act + tl * TOK + kk * (KCH * 2) + (w16 * 4 + t) * 16, v);
       }
       mbar_arrive(&full_bar[s]);
+      if (i + 1 < nst) load_act(k0 + KS);
     }
     return;
   }
