@@ -36,9 +36,9 @@ namespace fq {
 constexpr int kConsumerWarps = 8;
 constexpr int kDecThreads = 32 * (1 + kConsumerWarps);
 constexpr int kRowsPerCta = 256;      // 8 consumer warps x 2 tiles x 16 columns
-constexpr int kWBytesPerRow = 128;    // packed bytes of one column per stage (one SW128 line)
+constexpr int kWBytesPerRow = 64;     // packed bytes of one column per stage (SWIZZLE_64B rows)
 constexpr int kStageW = kRowsPerCta * kWBytesPerRow;  // 32 KB
-constexpr int kDecStages = 2;
+constexpr int kDecStages = 4;
 
 template <int BITS>
 struct DecGeom {
@@ -172,9 +172,12 @@ __device__ __forceinline__ uint32_t splat_scale(const T* scales, size_t idx) {
   return (uint32_t)s | ((uint32_t)s << 16);
 }
 
-// MMA row m (0..7) of a 16-column tile -> tile row; odd m land 4 rows away so the two columns a
-// 128-bit shared-memory phase touches sit in different SW128 bank groups (conflict-free).
-__device__ __forceinline__ int prow(int m) { return ((m & 1) << 2) | (m >> 1); }
+// MMA row m of a 16-column tile -> tile row.  With 64-byte rows the two columns a 128-bit
+// shared-memory phase touches (m = 2i, 2i+1) sit in different bank halves, and SWIZZLE_64B spreads
+// the four 16-byte cells of a row: conflict-free.
+__device__ __forceinline__ int prow(int m) { return m; }
+// physical 16-byte cell of logical cell c in tile row R under CU_TENSOR_MAP_SWIZZLE_64B
+__device__ __forceinline__ int swz64(int c, int R) { return c ^ ((R >> 1) & 3); }
 
 template <typename T, int BITS, int MT, bool SACC>
 __global__ void __launch_bounds__(kDecThreads, 2)
@@ -299,6 +302,9 @@ __global__ void __launch_bounds__(kDecThreads, 2)
 #pragma unroll
       for (int i = 0; i < 4; ++i) acc[rt][mt][i] = 0.f;
 
+  const int ngroups = K / p.group;
+  const int gm = SACC ? p.group / KCH : 1;  // chunks per group
+  int gj = SACC ? (kbeg / KCH) / gm : 0, grem = SACC ? (kbeg / KCH) % gm : 0;
   for (int i = 0; i < nst; ++i) {
     const int s = i % kDecStages;
     const uint32_t ph = (i / kDecStages) & 1;
@@ -308,7 +314,8 @@ __global__ void __launch_bounds__(kDecThreads, 2)
     if (SACC) {
 #pragma unroll
       for (int kk = 0; kk < CHUNKS; ++kk) {
-        const size_t j = (size_t)min((k0 + kk * KCH) / p.group, K / p.group - 1) * N;
+        // chunk c = k0/KCH + kk runs consecutively: group index tracked without divisions
+        const size_t j = (size_t)min(gj + (grem + kk >= gm ? 1 : 0), ngroups - 1) * N;
 #pragma unroll
         for (int rt = 0; rt < 2; ++rt) {
           sg[kk][rt] = Dt<T>::to_f(__ldg(S + j + ng[rt]));
@@ -330,16 +337,16 @@ __global__ void __launch_bounds__(kDecThreads, 2)
       const int cell = kk * 4 + t;
 #pragma unroll
       for (int rt = 0; rt < 2; ++rt) {
-        const uint4 wg = lds128(wst + Rg[rt] * kWBytesPerRow + ((cell ^ (Rg[rt] & 7)) << 4));
-        const uint4 wh = lds128(wst + Rh[rt] * kWBytesPerRow + ((cell ^ (Rh[rt] & 7)) << 4));
+        const uint4 wg = lds128(wst + Rg[rt] * kWBytesPerRow + (swz64(cell, Rg[rt]) << 4));
+        const uint4 wh = lds128(wst + Rh[rt] * kWBytesPerRow + (swz64(cell, Rh[rt]) << 4));
         const uint32_t wgw[4] = {wg.x, wg.y, wg.z, wg.w};
         const uint32_t whw[4] = {wh.x, wh.y, wh.z, wh.w};
-        float part[MT][4];
+        float part[MT][4], part2[MT][4];  // two MMA chains per tile (latency)
         if (SACC) {
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-            for (int q = 0; q < 4; ++q) part[mt][q] = 0.f;
+            for (int q = 0; q < 4; ++q) part[mt][q] = part2[mt][q] = 0.f;
         }
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
@@ -370,7 +377,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
               for (int mt = 0; mt < MT; ++mt) {
                 const uint32_t b0 = pp ? b[mt][w].z : b[mt][w].x;
                 const uint32_t b1 = pp ? b[mt][w].w : b[mt][w].y;
-                if (SACC) mma16816<T>(part[mt], a, b0, b1);
+                if (SACC) mma16816<T>(w < 2 ? part[mt] : part2[mt], a, b0, b1);
                 else mma16816<T>(acc[rt][mt], a, b0, b1);
               }
             }
@@ -393,7 +400,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
               const uint4 bb = b[mt][w >> 1];
               const uint32_t b0 = (w & 1) ? bb.z : bb.x;
               const uint32_t b1 = (w & 1) ? bb.w : bb.y;
-              if (SACC) mma16816<T>(part[mt], a, b0, b1);
+              if (SACC) mma16816<T>(w < 2 ? part[mt] : part2[mt], a, b0, b1);
               else mma16816<T>(acc[rt][mt], a, b0, b1);
             }
           }
@@ -401,6 +408,8 @@ __global__ void __launch_bounds__(kDecThreads, 2)
         if (SACC) {
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) part[mt][q] += part2[mt][q];
             if (OFF != 0.f) {  // remove OFF * sum_k a[tok, k] (tokens 2t, 2t+1 of this MMA tile)
               const float2 sa = *reinterpret_cast<const float2*>(
                   sbase + s * STAGE_BYTES + kStageW + ACT_BYTES + (kk * (MT * 8) + mt * 8 + 2 * t) * 4);
@@ -419,6 +428,10 @@ __global__ void __launch_bounds__(kDecThreads, 2)
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[s]);
+    if (SACC) {
+      grem += CHUNKS;
+      while (grem >= gm) { grem -= gm; ++gj; }
+    }
   }
 
   // ------------------------------------------------------------- epilogue (+ fused A5 fixup)
@@ -576,7 +589,7 @@ cudaError_t run_gemv(const GemvPlan& pl, int adt, int cdt, int bits, const void*
                      cudaStream_t st) {
   CUtensorMap tm;
   const uint64_t row_bytes = (uint64_t)K * bits / 8;
-  if (!make_tmap_2d(&tm, codes, 1, row_bytes, (uint64_t)N, row_bytes, kWBytesPerRow, kRowsPerCta, 1))
+  if (!make_tmap_2d(&tm, codes, 1, row_bytes, (uint64_t)N, row_bytes, kWBytesPerRow, kRowsPerCta, 64))
     return cudaErrorInvalidValue;
   DecodeParams prm{};
   prm.A = A;

@@ -30,6 +30,6 @@ int num_sms();
 
 // 2-D TMA descriptor (CUtensorMap, 128 bytes, written to `tmap`).  elem_bytes 1/2/4 -> u8/bf16/f32.
 bool make_tmap_2d(void* tmap, const void* base, int elem_bytes, uint64_t inner, uint64_t outer,
-                  uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, int swizzle128);
+                  uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, int swizzle_bytes);
 
 }  // namespace fq
