@@ -179,7 +179,9 @@ __device__ __forceinline__ int prow(int m) { return m; }
 // physical 16-byte cell of logical cell c in tile row R under CU_TENSOR_MAP_SWIZZLE_64B
 __device__ __forceinline__ int swz64(int c, int R) { return c ^ ((R >> 1) & 3); }
 
-template <typename T, int BITS, int MT, bool SACC>
+// DBG (diagnostics only, selected by FQ_DEC_DEBUG for bf16/int4/M<=8): 1 = no MMA (fake FADD
+// accumulate), 2 = no dequant (raw code words as MMA operands), 3 = consumers skip all compute.
+template <typename T, int BITS, int MT, bool SACC, int DBG = 0>
 __global__ void __launch_bounds__(kDecThreads, 2)
     decode_kernel(const __grid_constant__ CUtensorMap tmW, const DecodeParams p) {
   using G = DecGeom<BITS>;
@@ -324,6 +326,11 @@ __global__ void __launch_bounds__(kDecThreads, 2)
       }
     }
     mbar_wait(&full_bar[s], ph);
+    if (DBG == 3) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[s]);
+      continue;
+    }
     const uint32_t wst = smem_u32(sbase + s * STAGE_BYTES);
     const uint32_t act = wst + kStageW;
 #pragma unroll
@@ -359,7 +366,10 @@ __global__ void __launch_bounds__(kDecThreads, 2)
           }
           if (BITS == 4) {
             uint32_t qg[4], qh[4];
-            if (OFF != 0.f) {
+            if (DBG == 2) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) { qg[q] = wgw[w] + q; qh[q] = whw[w] + q; }
+            } else if (OFF != 0.f) {
               i4_pairs_off<T>(wgw[w], qg);
               i4_pairs_off<T>(whw[w], qh);
             } else {
@@ -377,7 +387,11 @@ __global__ void __launch_bounds__(kDecThreads, 2)
               for (int mt = 0; mt < MT; ++mt) {
                 const uint32_t b0 = pp ? b[mt][w].z : b[mt][w].x;
                 const uint32_t b1 = pp ? b[mt][w].w : b[mt][w].y;
-                if (SACC) mma16816<T>(w < 2 ? part[mt] : part2[mt], a, b0, b1);
+                if (DBG == 1) {
+                  float* d = w < 2 ? part[mt] : part2[mt];
+#pragma unroll
+                  for (int q = 0; q < 4; ++q) d[q] += __uint_as_float(a[q] ^ b0);
+                } else if (SACC) mma16816<T>(w < 2 ? part[mt] : part2[mt], a, b0, b1);
                 else mma16816<T>(acc[rt][mt], a, b0, b1);
               }
             }
@@ -550,11 +564,11 @@ size_t gemv_workspace_bytes(const GemvPlan& p, int M, int N) {
   return kCounterBytes + align256((size_t)p.splits * M * N * sizeof(float));
 }
 
-template <typename T, int BITS, int MT, bool SACC>
+template <typename T, int BITS, int MT, bool SACC, int DBG = 0>
 static cudaError_t launch_dec(const GemvPlan& pl, const CUtensorMap& tm, const DecodeParams& prm,
                               cudaStream_t st) {
   constexpr int smem = dec_smem_bytes<BITS, MT>();
-  auto kern = decode_kernel<T, BITS, MT, SACC>;
+  auto kern = decode_kernel<T, BITS, MT, SACC, DBG>;
   static bool attr_set = false;  // benign race: idempotent attribute call
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -601,6 +615,12 @@ cudaError_t run_gemv(const GemvPlan& pl, int adt, int cdt, int bits, const void*
   prm.ws = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + kCounterBytes);
   const int chunk = bits == 4 ? 128 : 64;  // K per MMA chunk (one scale per chunk if SACC)
   const bool sacc = (group % chunk) == 0;
+  const int dbg = env_int("FQ_DEC_DEBUG", 0);
+  if (dbg && adt == FQ_BF16 && bits == 4 && pl.mt == 1 && sacc) {
+    if (dbg == 1) return launch_dec<__nv_bfloat16, 4, 1, true, 1>(pl, tm, prm, st);
+    if (dbg == 2) return launch_dec<__nv_bfloat16, 4, 1, true, 2>(pl, tm, prm, st);
+    if (dbg == 3) return launch_dec<__nv_bfloat16, 4, 1, true, 3>(pl, tm, prm, st);
+  }
   return adt == FQ_BF16 ? dispatch_bits<__nv_bfloat16>(bits, sacc, pl, tm, prm, st)
                         : dispatch_bits<__half>(bits, sacc, pl, tm, prm, st);
 }
