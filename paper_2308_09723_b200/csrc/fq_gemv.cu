@@ -285,17 +285,27 @@ __global__ void __launch_bounds__(kDecThreads, 2)
   }
 
   // --------------------------------------------------------------------------- consumers
+  static_assert(CHUNKS == 1, "one MMA chunk (one scale) per stage");
   const T* __restrict__ S = reinterpret_cast<const T*>(p.scales);
   const int cw = warp - 1;
   const int gq = lane >> 2, t = lane & 3;
   int Rg[2], Rh[2], ng[2], nh[2];
+  uint32_t wofs_g[2], wofs_h[2];  // per-thread byte offsets inside a stage (swizzled cells)
 #pragma unroll
   for (int rt = 0; rt < 2; ++rt) {
     Rg[rt] = cw * 32 + rt * 16 + prow(gq);
     Rh[rt] = Rg[rt] + 8;
     ng[rt] = min(n0 + Rg[rt], N - 1);
     nh[rt] = min(n0 + Rh[rt], N - 1);
+    wofs_g[rt] = Rg[rt] * kWBytesPerRow + (swz64(t, Rg[rt]) << 4);
+    wofs_h[rt] = Rh[rt] * kWBytesPerRow + (swz64(t, Rh[rt]) << 4);
   }
+  uint32_t aofs[MT][PIECES];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int w16 = 0; w16 < PIECES; ++w16) aofs[mt][w16] = kStageW + (mt * 8 + gq) * TOK + (w16 * 4 + t) * 16;
+  const uint32_t saofs = kStageW + ACT_BYTES + 2 * t * 4;
   float acc[2][MT][4];
 #pragma unroll
   for (int rt = 0; rt < 2; ++rt)
@@ -304,66 +314,59 @@ __global__ void __launch_bounds__(kDecThreads, 2)
 #pragma unroll
       for (int i = 0; i < 4; ++i) acc[rt][mt][i] = 0.f;
 
-  const int ngroups = K / p.group;
-  const int gm = SACC ? p.group / KCH : 1;  // chunks per group
-  int gj = SACC ? (kbeg / KCH) / gm : 0, grem = SACC ? (kbeg / KCH) % gm : 0;
+  // scale rows: chunk c = kbeg/KCH + i runs consecutively, group j = c / gm tracked incrementally
+  const int gm = SACC ? p.group / KCH : 1;
+  int grem = SACC ? (kbeg / KCH) % gm : 0;
+  size_t jN = SACC ? (size_t)((kbeg / KCH) / gm) * N : 0;
+  const uint32_t sb = smem_u32(sbase);
+  int s = 0;
+  uint32_t ph = 0;
   for (int i = 0; i < nst; ++i) {
-    const int s = i % kDecStages;
-    const uint32_t ph = (i / kDecStages) & 1;
     const int k0 = kbeg + i * KS;
-    // scales of this stage's chunks (issued before the wait to hide their latency)
-    float sg[CHUNKS][2], sh[CHUNKS][2];
+    float sg[2], sh[2];  // issued before the wait to hide their latency
     if (SACC) {
 #pragma unroll
-      for (int kk = 0; kk < CHUNKS; ++kk) {
-        // chunk c = k0/KCH + kk runs consecutively: group index tracked without divisions
-        const size_t j = (size_t)min(gj + (grem + kk >= gm ? 1 : 0), ngroups - 1) * N;
-#pragma unroll
-        for (int rt = 0; rt < 2; ++rt) {
-          sg[kk][rt] = Dt<T>::to_f(__ldg(S + j + ng[rt]));
-          sh[kk][rt] = Dt<T>::to_f(__ldg(S + j + nh[rt]));
-        }
+      for (int rt = 0; rt < 2; ++rt) {
+        sg[rt] = Dt<T>::to_f(__ldg(S + jN + ng[rt]));
+        sh[rt] = Dt<T>::to_f(__ldg(S + jN + nh[rt]));
       }
     }
     mbar_wait(&full_bar[s], ph);
-    if (DBG == 3) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_bar[s]);
-      continue;
-    }
-    const uint32_t wst = smem_u32(sbase + s * STAGE_BYTES);
-    const uint32_t act = wst + kStageW;
-#pragma unroll
-    for (int kk = 0; kk < CHUNKS; ++kk) {
+    const uint32_t wst = sb + s * STAGE_BYTES;
+    if (DBG != 3) {
       uint4 b[MT][PIECES];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-        for (int w16 = 0; w16 < PIECES; ++w16)
-          b[mt][w16] = lds128(act + (mt * 8 + gq) * TOK + kk * (KCH * 2) + (w16 * 4 + t) * 16);
-      const int cell = kk * 4 + t;
+        for (int w16 = 0; w16 < PIECES; ++w16) b[mt][w16] = lds128(wst + aofs[mt][w16]);
+      float2 sa[MT];
+      if (OFF != 0.f) {
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) sa[mt] = lds64f(wst + saofs + mt * 32);
+      }
 #pragma unroll
       for (int rt = 0; rt < 2; ++rt) {
-        const uint4 wg = lds128(wst + Rg[rt] * kWBytesPerRow + (swz64(cell, Rg[rt]) << 4));
-        const uint4 wh = lds128(wst + Rh[rt] * kWBytesPerRow + (swz64(cell, Rh[rt]) << 4));
+        const uint4 wg = lds128(wst + wofs_g[rt]);
+        const uint4 wh = lds128(wst + wofs_h[rt]);
         const uint32_t wgw[4] = {wg.x, wg.y, wg.z, wg.w};
         const uint32_t whw[4] = {wh.x, wh.y, wh.z, wh.w};
-        float part[MT][4], part2[MT][4];  // two MMA chains per tile (latency)
+        float part[MT][4];
         if (SACC) {
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-            for (int q = 0; q < 4; ++q) part[mt][q] = part2[mt][q] = 0.f;
+            for (int q = 0; q < 4; ++q) part[mt][q] = 0.f;
         }
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
           uint32_t sgs = 0, shs = 0;
-          if (!SACC) {
-            const int kw = k0 + kk * KCH + t * SEG + w * (SEG / 4);
-            const size_t j = (size_t)min(kw / p.group, K / p.group - 1) * N;
+          if (!SACC) {  // small / odd groups: q*s in the activation dtype before the MMA
+            const int kw = k0 + t * SEG + w * (SEG / 4);
+            const size_t j = (size_t)(kw / p.group) * N;
             sgs = splat_scale<T>(S, j + ng[rt]);
             shs = splat_scale<T>(S, j + nh[rt]);
           }
+          float(*dst)[4] = SACC ? part : acc[rt];
           if (BITS == 4) {
             uint32_t qg[4], qh[4];
             if (DBG == 2) {
@@ -388,11 +391,11 @@ __global__ void __launch_bounds__(kDecThreads, 2)
                 const uint32_t b0 = pp ? b[mt][w].z : b[mt][w].x;
                 const uint32_t b1 = pp ? b[mt][w].w : b[mt][w].y;
                 if (DBG == 1) {
-                  float* d = w < 2 ? part[mt] : part2[mt];
 #pragma unroll
-                  for (int q = 0; q < 4; ++q) d[q] += __uint_as_float(a[q] ^ b0);
-                } else if (SACC) mma16816<T>(w < 2 ? part[mt] : part2[mt], a, b0, b1);
-                else mma16816<T>(acc[rt][mt], a, b0, b1);
+                  for (int q = 0; q < 4; ++q) dst[mt][q] += __uint_as_float(a[q] ^ b0);
+                } else {
+                  mma16816<T>(dst[mt], a, b0, b1);
+                }
               }
             }
           } else {
@@ -412,40 +415,31 @@ __global__ void __launch_bounds__(kDecThreads, 2)
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt) {
               const uint4 bb = b[mt][w >> 1];
-              const uint32_t b0 = (w & 1) ? bb.z : bb.x;
-              const uint32_t b1 = (w & 1) ? bb.w : bb.y;
-              if (SACC) mma16816<T>(w < 2 ? part[mt] : part2[mt], a, b0, b1);
-              else mma16816<T>(acc[rt][mt], a, b0, b1);
+              mma16816<T>(dst[mt], a, (w & 1) ? bb.z : bb.x, (w & 1) ? bb.w : bb.y);
             }
           }
         }
         if (SACC) {
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) part[mt][q] += part2[mt][q];
             if (OFF != 0.f) {  // remove OFF * sum_k a[tok, k] (tokens 2t, 2t+1 of this MMA tile)
-              const float2 sa = *reinterpret_cast<const float2*>(
-                  sbase + s * STAGE_BYTES + kStageW + ACT_BYTES + (kk * (MT * 8) + mt * 8 + 2 * t) * 4);
-              part[mt][0] = fmaf(-OFF, sa.x, part[mt][0]);
-              part[mt][1] = fmaf(-OFF, sa.y, part[mt][1]);
-              part[mt][2] = fmaf(-OFF, sa.x, part[mt][2]);
-              part[mt][3] = fmaf(-OFF, sa.y, part[mt][3]);
+              part[mt][0] = fmaf(-OFF, sa[mt].x, part[mt][0]);
+              part[mt][1] = fmaf(-OFF, sa[mt].y, part[mt][1]);
+              part[mt][2] = fmaf(-OFF, sa[mt].x, part[mt][2]);
+              part[mt][3] = fmaf(-OFF, sa[mt].y, part[mt][3]);
             }
-            acc[rt][mt][0] = fmaf(sg[kk][rt], part[mt][0], acc[rt][mt][0]);
-            acc[rt][mt][1] = fmaf(sg[kk][rt], part[mt][1], acc[rt][mt][1]);
-            acc[rt][mt][2] = fmaf(sh[kk][rt], part[mt][2], acc[rt][mt][2]);
-            acc[rt][mt][3] = fmaf(sh[kk][rt], part[mt][3], acc[rt][mt][3]);
+            acc[rt][mt][0] = fmaf(sg[rt], part[mt][0], acc[rt][mt][0]);
+            acc[rt][mt][1] = fmaf(sg[rt], part[mt][1], acc[rt][mt][1]);
+            acc[rt][mt][2] = fmaf(sh[rt], part[mt][2], acc[rt][mt][2]);
+            acc[rt][mt][3] = fmaf(sh[rt], part[mt][3], acc[rt][mt][3]);
           }
         }
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[s]);
-    if (SACC) {
-      grem += CHUNKS;
-      while (grem >= gm) { grem -= gm; ++gj; }
-    }
+    if (++s == kDecStages) { s = 0; ph ^= 1; }
+    if (SACC && ++grem == gm) { grem = 0; jN += N; }
   }
 
   // ------------------------------------------------------------- epilogue (+ fused A5 fixup)
