@@ -34,7 +34,7 @@
 namespace fq {
 
 constexpr int kConsumerWarps = 8;
-constexpr int kDecThreads = 32 * (1 + kConsumerWarps);
+constexpr int kDecThreads = 32 * (2 + kConsumerWarps);  // TMA warp + consumers + activation stager
 constexpr int kRowsPerCta = 256;      // 8 consumer warps x 2 tiles x 16 columns
 constexpr int kWBytesPerRow = 64;     // packed bytes of one column per stage (SWIZZLE_64B rows)
 constexpr int kStageW = kRowsPerCta * kWBytesPerRow;  // 32 KB
@@ -48,6 +48,11 @@ struct DecGeom {
   static constexpr int CHUNKS = KS / KCH;              // 2
   static constexpr int PIECES = SEG / 8;               // 16-byte activation pieces per thread/chunk
   static constexpr int TOK_BYTES = KS * 2 + 64;        // token row stride in smem, = 64 mod 128
+};
+
+struct DecMaps {
+  CUtensorMap w;  // packed codes [N][K*bits/8] u8, box [256 rows][64 B], SWIZZLE_64B
+  CUtensorMap a;  // activations [M][K] 16-bit, box [MT*8 rows][K per stage]
 };
 
 struct DecodeParams {
@@ -183,18 +188,21 @@ __device__ __forceinline__ int swz64(int c, int R) { return c ^ ((R >> 1) & 3); 
 // accumulate), 2 = no dequant (raw code words as MMA operands), 3 = consumers skip all compute.
 template <typename T, int BITS, int MT, bool SACC, int DBG = 0>
 __global__ void __launch_bounds__(kDecThreads, 2)
-    decode_kernel(const __grid_constant__ CUtensorMap tmW, const DecodeParams p) {
+    decode_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA,
+                  const DecodeParams p) {
   using G = DecGeom<BITS>;
   constexpr int KS = G::KS, SEG = G::SEG, KCH = G::KCH, CHUNKS = G::CHUNKS, PIECES = G::PIECES;
   constexpr int TOK = G::TOK_BYTES;
   constexpr int ACT_BYTES = MT * 8 * TOK;
   constexpr int SA_BYTES = MT * 8 * CHUNKS * 4;  // fp32 activation sums [token][chunk]
-  constexpr int STAGE_BYTES = kStageW + ((ACT_BYTES + SA_BYTES + 1023) / 1024) * 1024;
+  constexpr int RAW_BYTES = MT * 8 * KS * 2;     // TMA-staged activations, natural order
+  constexpr int RAW_OFS = kStageW + ((ACT_BYTES + SA_BYTES + 127) / 128) * 128;
+  constexpr int STAGE_BYTES = ((RAW_OFS + RAW_BYTES + 1023) / 1024) * 1024;
   constexpr float OFF = SACC ? CodeOffset<T, BITS>::v : 0.f;
   constexpr int PPC = KCH / 8;  // 8-element pieces per chunk (16 int4, 8 int8): divides 32
 
   extern __shared__ __align__(1024) uint8_t dsmem[];
-  __shared__ __align__(8) uint64_t full_bar[kDecStages], empty_bar[kDecStages];
+  __shared__ __align__(8) uint64_t full_bar[kDecStages], empty_bar[kDecStages], raw_bar[kDecStages];
   __shared__ int s_last;
   uint8_t* sbase = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsmem) + 1023) & ~uintptr_t(1023));
 
@@ -208,51 +216,60 @@ __global__ void __launch_bounds__(kDecThreads, 2)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kDecStages; ++s) {
-      mbar_init(&full_bar[s], 32);
+      mbar_init(&full_bar[s], 1 + 32);  // weight TMA (expect_tx arrival) + 32 stager lanes
+      mbar_init(&raw_bar[s], 1);        // activation TMA
       mbar_init(&empty_bar[s], kConsumerWarps);
     }
     fence_mbar_init();
   }
-  if (warp == 0 && lane == 0) prefetch_tmap(&tmW);
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmW);
+    prefetch_tmap(&tmA);
+  }
   __syncthreads();
 
   if (warp == 0) {
-    // ------------------------------------------------------------------------- producer
-    const T* __restrict__ A = reinterpret_cast<const T*>(p.A);
-    const uint64_t pol = policy_evict_first();
+    // ------------------------------------------------------------ TMA producer (one lane)
+    if (lane == 0) {
+      const uint64_t polw = policy_evict_first();
+      const uint64_t pola = policy_evict_last();
+      int s = 0;
+      uint32_t ph = 0;
+      for (int i = 0; i < nst; ++i) {
+        mbar_wait(&empty_bar[s], ph ^ 1);
+        uint8_t* st = sbase + s * STAGE_BYTES;
+        const int k0 = kbeg + i * KS;
+        mbar_arrive_expect_tx(&full_bar[s], kStageW);
+        tma_load_2d(st, &tmW, &full_bar[s], k0 * BITS / 8, n0, polw);
+        mbar_arrive_expect_tx(&raw_bar[s], RAW_BYTES);
+        tma_load_2d(st + RAW_OFS, &tmA, &raw_bar[s], k0, tok0, pola);
+        if (++s == kDecStages) { s = 0; ph ^= 1; }
+      }
+    }
+    return;
+  }
+  if (warp == kConsumerWarps + 1) {
+    // ------------------------------------------------------------ activation stager
+    // raw [MT*8 tokens][KS] (TMA, natural order, OOB zero) -> per-thread MMA fragment order
+    // (+ the per-token sums used by the code-offset correction).
     constexpr int NPIECE = MT * 8 * (KS / 8);
     static_assert(NPIECE % 32 == 0, "pieces per stage must be a multiple of the warp size");
-    constexpr int NPW = NPIECE / 32;  // 16-byte activation pieces per lane per stage
-    // Activation loads are software-pipelined one stage ahead (their L2 latency overlaps the wait
-    // for a free stage), all NPW loads of a stage in flight at once.
-    uint4 va[NPW];
-    auto load_act = [&](int k0) {
-#pragma unroll
-      for (int j = 0; j < NPW; ++j) {
-        const int pc = lane + 32 * j;
-        const int tok = tok0 + pc / (KS / 8);
-        const int kl = (pc % (KS / 8)) * 8;
-        va[j] = (tok < M && k0 + kl < kend) ? ldg_keep(A + (size_t)tok * K + k0 + kl) : make_uint4(0, 0, 0, 0);
-      }
-    };
-    load_act(kbeg);
+    constexpr int NPW = NPIECE / 32;
+    int s = 0;
+    uint32_t ph = 0;
     for (int i = 0; i < nst; ++i) {
-      const int s = i % kDecStages;
-      const uint32_t ph = (i / kDecStages) & 1;
-      mbar_wait(&empty_bar[s], ph ^ 1);
+      mbar_wait(&raw_bar[s], ph);
       uint8_t* st = sbase + s * STAGE_BYTES;
-      const int k0 = kbeg + i * KS;
-      if (lane == 0) {
-        mbar_expect_tx(&full_bar[s], kStageW);
-        tma_load_2d(st, &tmW, &full_bar[s], k0 * BITS / 8, n0, pol);
-      }
-      const uint32_t act = smem_u32(st + kStageW);
+      const uint32_t stu = smem_u32(st);
+      uint4 va[NPW];
+#pragma unroll
+      for (int j = 0; j < NPW; ++j) va[j] = lds128(stu + RAW_OFS + (lane + 32 * j) * 16);
 #pragma unroll
       for (int j = 0; j < NPW; ++j) {
         const int pc = lane + 32 * j;
         const int tl = pc / (KS / 8);          // local token
         const int kl = (pc % (KS / 8)) * 8;    // local k of this 8-element piece
-        const int kk = kl / KCH, r = kl % KCH, t = r / SEG, w16 = (r % SEG) / 8;
+        const int r = kl % KCH, t = r / SEG, w16 = (r % SEG) / 8;
         uint4 v = va[j];
         if (OFF != 0.f) {
           // sum of the 8 activations, reduced over the PPC lanes of this chunk (aligned groups)
@@ -269,17 +286,16 @@ __global__ void __launch_bounds__(kDecThreads, 2)
           }
 #pragma unroll
           for (int o = PPC / 2; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-          if ((lane % PPC) == 0)
-            reinterpret_cast<float*>(st + kStageW + ACT_BYTES)[kk * (MT * 8) + tl] = sum;
+          if ((lane % PPC) == 0) reinterpret_cast<float*>(st + kStageW + ACT_BYTES)[tl] = sum;
         }
         if (BITS == 4) {
           v = make_uint4(prmt(v.x, v.z, 0x5410u), prmt(v.x, v.z, 0x7632u), prmt(v.y, v.w, 0x5410u),
                          prmt(v.y, v.w, 0x7632u));
         }
-        sts128(act + tl * TOK + kk * (KCH * 2) + (w16 * 4 + t) * 16, v);
+        sts128(stu + kStageW + tl * TOK + (w16 * 4 + t) * 16, v);
       }
       mbar_arrive(&full_bar[s]);
-      if (i + 1 < nst) load_act(k0 + KS);
+      if (++s == kDecStages) { s = 0; ph ^= 1; }
     }
     return;
   }
@@ -514,7 +530,8 @@ static int env_int(const char* name, int dflt) {
 template <int BITS, int MT>
 static constexpr int dec_smem_bytes() {
   using G = DecGeom<BITS>;
-  return kDecStages * (kStageW + ((MT * 8 * G::TOK_BYTES + MT * 8 * G::CHUNKS * 4 + 1023) / 1024) * 1024) + 1024;
+  constexpr int raw_ofs = kStageW + ((MT * 8 * G::TOK_BYTES + MT * 8 * G::CHUNKS * 4 + 127) / 128) * 128;
+  return kDecStages * (((raw_ofs + MT * 8 * G::KS * 2) + 1023) / 1024 * 1024) + 1024;
 }
 
 GemvPlan plan_gemv(int M, int K, int N, int bits, int group, int nsm) {
@@ -559,7 +576,7 @@ size_t gemv_workspace_bytes(const GemvPlan& p, int M, int N) {
 }
 
 template <typename T, int BITS, int MT, bool SACC, int DBG = 0>
-static cudaError_t launch_dec(const GemvPlan& pl, const CUtensorMap& tm, const DecodeParams& prm,
+static cudaError_t launch_dec(const GemvPlan& pl, const DecMaps& tm, const DecodeParams& prm,
                               cudaStream_t st) {
   constexpr int smem = dec_smem_bytes<BITS, MT>();
   auto kern = decode_kernel<T, BITS, MT, SACC, DBG>;
@@ -571,23 +588,23 @@ static cudaError_t launch_dec(const GemvPlan& pl, const CUtensorMap& tm, const D
   }
   const int gx = (prm.N + pl.rows_per_cta - 1) / pl.rows_per_cta;
   dim3 grid(gx, pl.splits, pl.ktiles);
-  kern<<<grid, kDecThreads, smem, st>>>(tm, prm);
+  kern<<<grid, kDecThreads, smem, st>>>(tm.w, tm.a, prm);
   return cudaGetLastError();
 }
 
 template <typename T, int BITS, int MT>
-static cudaError_t dispatch_sacc(bool sacc, const GemvPlan& pl, const CUtensorMap& tm,
+static cudaError_t dispatch_sacc(bool sacc, const GemvPlan& pl, const DecMaps& tm,
                                  const DecodeParams& prm, cudaStream_t st) {
   return sacc ? launch_dec<T, BITS, MT, true>(pl, tm, prm, st) : launch_dec<T, BITS, MT, false>(pl, tm, prm, st);
 }
 template <typename T, int BITS>
-static cudaError_t dispatch_mt(bool sacc, const GemvPlan& pl, const CUtensorMap& tm,
+static cudaError_t dispatch_mt(bool sacc, const GemvPlan& pl, const DecMaps& tm,
                                const DecodeParams& prm, cudaStream_t st) {
   return pl.mt == 1 ? dispatch_sacc<T, BITS, 1>(sacc, pl, tm, prm, st)
                     : dispatch_sacc<T, BITS, 2>(sacc, pl, tm, prm, st);
 }
 template <typename T>
-static cudaError_t dispatch_bits(int bits, bool sacc, const GemvPlan& pl, const CUtensorMap& tm,
+static cudaError_t dispatch_bits(int bits, bool sacc, const GemvPlan& pl, const DecMaps& tm,
                                  const DecodeParams& prm, cudaStream_t st) {
   return bits == 4 ? dispatch_mt<T, 4>(sacc, pl, tm, prm, st) : dispatch_mt<T, 8>(sacc, pl, tm, prm, st);
 }
@@ -595,9 +612,12 @@ static cudaError_t dispatch_bits(int bits, bool sacc, const GemvPlan& pl, const 
 cudaError_t run_gemv(const GemvPlan& pl, int adt, int cdt, int bits, const void* A, int M, int K,
                      int N, const void* codes, const void* scales, int group, void* C, void* ws,
                      cudaStream_t st) {
-  CUtensorMap tm;
+  DecMaps tm;
   const uint64_t row_bytes = (uint64_t)K * bits / 8;
-  if (!make_tmap_2d(&tm, codes, 1, row_bytes, (uint64_t)N, row_bytes, kWBytesPerRow, kRowsPerCta, 64))
+  if (!make_tmap_2d(&tm.w, codes, 1, row_bytes, (uint64_t)N, row_bytes, kWBytesPerRow, kRowsPerCta, 64))
+    return cudaErrorInvalidValue;
+  const int ks = kWBytesPerRow * 8 / bits;  // K per stage
+  if (!make_tmap_2d(&tm.a, A, 2, (uint64_t)K, (uint64_t)M, (uint64_t)K * 2, ks, pl.mt * 8, 0))
     return cudaErrorInvalidValue;
   DecodeParams prm{};
   prm.A = A;
