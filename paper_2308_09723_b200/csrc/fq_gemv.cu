@@ -53,6 +53,7 @@ struct DecGeom {
 struct DecMaps {
   CUtensorMap w;  // packed codes [N][K*bits/8] u8, box [256 rows][64 B], SWIZZLE_64B
   CUtensorMap a;  // activations [M][K] 16-bit, box [MT*8 rows][K per stage]
+  CUtensorMap s;  // scales [G][N] 16-bit, box [1 row][256 columns]
 };
 
 struct DecodeParams {
@@ -172,6 +173,13 @@ __device__ __forceinline__ void i8_pairs_off_half(uint32_t w, uint32_t (&q)[2]) 
 }
 
 template <typename T>
+__device__ __forceinline__ float lds_scale(uint32_t addr) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+  return Dt<T>::to_f(*reinterpret_cast<T*>(&v));
+}
+
+template <typename T>
 __device__ __forceinline__ uint32_t splat_scale(const T* scales, size_t idx) {
   const unsigned short s = __ldg(reinterpret_cast<const unsigned short*>(scales) + idx);
   return (uint32_t)s | ((uint32_t)s << 16);
@@ -189,7 +197,7 @@ __device__ __forceinline__ int swz64(int c, int R) { return c ^ ((R >> 1) & 3); 
 template <typename T, int BITS, int MT, bool SACC, int DBG = 0>
 __global__ void __launch_bounds__(kDecThreads, 2)
     decode_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA,
-                  const DecodeParams p) {
+                  const __grid_constant__ CUtensorMap tmS, const DecodeParams p) {
   using G = DecGeom<BITS>;
   constexpr int KS = G::KS, SEG = G::SEG, KCH = G::KCH, CHUNKS = G::CHUNKS, PIECES = G::PIECES;
   constexpr int TOK = G::TOK_BYTES;
@@ -197,7 +205,9 @@ __global__ void __launch_bounds__(kDecThreads, 2)
   constexpr int SA_BYTES = MT * 8 * CHUNKS * 4;  // fp32 activation sums [token][chunk]
   constexpr int RAW_BYTES = MT * 8 * KS * 2;     // TMA-staged activations, natural order
   constexpr int RAW_OFS = kStageW + ((ACT_BYTES + SA_BYTES + 127) / 128) * 128;
-  constexpr int STAGE_BYTES = ((RAW_OFS + RAW_BYTES + 1023) / 1024) * 1024;
+  constexpr int SC_BYTES = kRowsPerCta * 2;       // TMA-staged scale row segment s[j][n0..n0+255]
+  constexpr int SC_OFS = RAW_OFS + RAW_BYTES;
+  constexpr int STAGE_BYTES = ((SC_OFS + SC_BYTES + 1023) / 1024) * 1024;
   constexpr float OFF = SACC ? CodeOffset<T, BITS>::v : 0.f;
   constexpr int PPC = KCH / 8;  // 8-element pieces per chunk (16 int4, 8 int8): divides 32
 
@@ -225,6 +235,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmW);
     prefetch_tmap(&tmA);
+    if (SACC) prefetch_tmap(&tmS);
   }
   __syncthreads();
 
@@ -235,12 +246,19 @@ __global__ void __launch_bounds__(kDecThreads, 2)
       const uint64_t pola = policy_evict_last();
       int s = 0;
       uint32_t ph = 0;
+      // chunk c = kbeg/KCH + i (one chunk per stage) lies in scale group c / gm
+      const int gm = SACC ? p.group / KCH : 1;
+      int grem = SACC ? (kbeg / KCH) % gm : 0, gj = SACC ? (kbeg / KCH) / gm : 0;
       for (int i = 0; i < nst; ++i) {
         mbar_wait(&empty_bar[s], ph ^ 1);
         uint8_t* st = sbase + s * STAGE_BYTES;
         const int k0 = kbeg + i * KS;
-        mbar_arrive_expect_tx(&full_bar[s], kStageW);
+        mbar_arrive_expect_tx(&full_bar[s], kStageW + (SACC ? SC_BYTES : 0));
         tma_load_2d(st, &tmW, &full_bar[s], k0 * BITS / 8, n0, polw);
+        if (SACC) {
+          tma_load_2d(st + SC_OFS, &tmS, &full_bar[s], n0, gj, polw);
+          if (++grem == gm) { grem = 0; ++gj; }
+        }
         mbar_arrive_expect_tx(&raw_bar[s], RAW_BYTES);
         tma_load_2d(st + RAW_OFS, &tmA, &raw_bar[s], k0, tok0, pola);
         if (++s == kDecStages) { s = 0; ph ^= 1; }
@@ -330,25 +348,21 @@ __global__ void __launch_bounds__(kDecThreads, 2)
 #pragma unroll
       for (int i = 0; i < 4; ++i) acc[rt][mt][i] = 0.f;
 
-  // scale rows: chunk c = kbeg/KCH + i runs consecutively, group j = c / gm tracked incrementally
-  const int gm = SACC ? p.group / KCH : 1;
-  int grem = SACC ? (kbeg / KCH) % gm : 0;
-  size_t jN = SACC ? (size_t)((kbeg / KCH) / gm) * N : 0;
   const uint32_t sb = smem_u32(sbase);
   int s = 0;
   uint32_t ph = 0;
   for (int i = 0; i < nst; ++i) {
     const int k0 = kbeg + i * KS;
-    float sg[2], sh[2];  // issued before the wait to hide their latency
+    mbar_wait(&full_bar[s], ph);
+    const uint32_t wst = sb + s * STAGE_BYTES;
+    float sg[2], sh[2];  // this stage's scales (TMA-staged with the weights)
     if (SACC) {
 #pragma unroll
       for (int rt = 0; rt < 2; ++rt) {
-        sg[rt] = Dt<T>::to_f(__ldg(S + jN + ng[rt]));
-        sh[rt] = Dt<T>::to_f(__ldg(S + jN + nh[rt]));
+        sg[rt] = lds_scale<T>(wst + SC_OFS + Rg[rt] * 2);
+        sh[rt] = lds_scale<T>(wst + SC_OFS + Rh[rt] * 2);
       }
     }
-    mbar_wait(&full_bar[s], ph);
-    const uint32_t wst = sb + s * STAGE_BYTES;
     if (DBG != 3) {
       uint4 b[MT][PIECES];
 #pragma unroll
@@ -455,7 +469,6 @@ __global__ void __launch_bounds__(kDecThreads, 2)
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[s]);
     if (++s == kDecStages) { s = 0; ph ^= 1; }
-    if (SACC && ++grem == gm) { grem = 0; jN += N; }
   }
 
   // ------------------------------------------------------------- epilogue (+ fused A5 fixup)
@@ -531,7 +544,7 @@ template <int BITS, int MT>
 static constexpr int dec_smem_bytes() {
   using G = DecGeom<BITS>;
   constexpr int raw_ofs = kStageW + ((MT * 8 * G::TOK_BYTES + MT * 8 * G::CHUNKS * 4 + 127) / 128) * 128;
-  return kDecStages * (((raw_ofs + MT * 8 * G::KS * 2) + 1023) / 1024 * 1024) + 1024;
+  return kDecStages * (((raw_ofs + MT * 8 * G::KS * 2 + kRowsPerCta * 2) + 1023) / 1024 * 1024) + 1024;
 }
 
 GemvPlan plan_gemv(int M, int K, int N, int bits, int group, int nsm) {
@@ -588,7 +601,7 @@ static cudaError_t launch_dec(const GemvPlan& pl, const DecMaps& tm, const Decod
   }
   const int gx = (prm.N + pl.rows_per_cta - 1) / pl.rows_per_cta;
   dim3 grid(gx, pl.splits, pl.ktiles);
-  kern<<<grid, kDecThreads, smem, st>>>(tm.w, tm.a, prm);
+  kern<<<grid, kDecThreads, smem, st>>>(tm.w, tm.a, tm.s, prm);
   return cudaGetLastError();
 }
 
@@ -618,6 +631,8 @@ cudaError_t run_gemv(const GemvPlan& pl, int adt, int cdt, int bits, const void*
     return cudaErrorInvalidValue;
   const int ks = kWBytesPerRow * 8 / bits;  // K per stage
   if (!make_tmap_2d(&tm.a, A, 2, (uint64_t)K, (uint64_t)M, (uint64_t)K * 2, ks, pl.mt * 8, 0))
+    return cudaErrorInvalidValue;
+  if (!make_tmap_2d(&tm.s, scales, 2, (uint64_t)N, (uint64_t)(K / group), (uint64_t)N * 2, kRowsPerCta, 1, 0))
     return cudaErrorInvalidValue;
   DecodeParams prm{};
   prm.A = A;
