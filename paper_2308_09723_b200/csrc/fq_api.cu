@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/fq.h"
@@ -38,6 +39,15 @@ static fq_status check_wdesc(const fq_wdesc* d) {
 static cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 static fq_status from_cuda(cudaError_t e) { return e == cudaSuccess ? FQ_OK : FQ_ERR_CUDA; }
+
+// M <= 16: memory-bound decode kernel (A4/A5); larger M: tcgen05 tensor-core kernel (A6).
+// FQ_GEMM_PATH=decode|tc forces a path (tests and A/B measurements).
+static bool use_tc_path(int64_t M) {
+  const char* e = std::getenv("FQ_GEMM_PATH");
+  if (e && std::strcmp(e, "decode") == 0) return false;
+  if (e && std::strcmp(e, "tc") == 0) return true;
+  return M > 16;
+}
 
 }  // namespace fq
 
@@ -138,6 +148,9 @@ fq_status fq_gemm(const void* A, int32_t adt, int64_t M, const fq_wdesc* d, cons
   if (d->scale_dtype != adt) return FQ_ERR_UNSUPPORTED;
   if (cdt != adt && cdt != FQ_FP32) return FQ_ERR_UNSUPPORTED;
   if (M <= 0 || M > (1 << 20)) return FQ_ERR_SHAPE;
+  if (use_tc_path(M))
+    return from_cuda(run_gemm_tc(adt, cdt, d->bits, A, (int)M, (int)d->K, (int)d->N, codes, scales,
+                                 d->group, C, as_stream(stream)));
   const GemvPlan p = plan_gemv((int)M, (int)d->K, (int)d->N, d->bits, d->group, num_sms());
   if (p.splits > 1 && (!ws || ws_bytes < gemv_workspace_bytes(p, (int)M, (int)d->N)))
     return FQ_ERR_WORKSPACE;

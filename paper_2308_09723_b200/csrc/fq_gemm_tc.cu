@@ -1,0 +1,381 @@
+// fq_gemm_tc.cu — kernel A6: large-M (prefill) fused dequant GEMM on the 5th-gen tensor cores.
+//
+// Same math as A4 (§4.1): C[m,n] = sum_k A[m,k] * (q[n,k] * s[k/g, n]), weights
+// dequantized to the activation dtype before the tensor-core MMA ("dequantize the weights to match
+// the data type of the activation and perform floating-point tensor core math"), fp32
+// accumulation.  The paper notes that in this compute-bound regime "the conversions from integer
+// to float bottleneck our kernels, rather than tensor core math"; the B200 design keeps the
+// conversion off the tensor core's critical path by warp specialisation and by writing the
+// dequantized weights straight into tensor memory (no shared-memory round trip):
+//
+//   tile = 128 weight rows (output columns n) x 256 tokens, K block = 64, persistent CTAs.
+//   warp 0      TMA producer: activations [256 tokens x 64 k] (SWIZZLE_128B, the UMMA K-major
+//               canonical layout) + packed codes [128 rows x 64 k] (SWIZZLE_32B) per stage.
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer:
+//                 D[n, tok] (fp32, TMEM, 256 columns) += A[n, k] (bf16, TMEM) * B[k, tok] (smem)
+//               "kind::f16", M=128, N=256, K=16; tcgen05.commit releases the stage.
+//   warps 2..9  dequant: thread = one weight row (its TMEM lane) x 32 k; codes -> exact bf16 codes
+//               (PRMT/IMAD/LOP3 magic-number unpack, natural (k,k+1) pairs) -> * scale ->
+//               tcgen05.st into the stage's A slot.  After the last K block of a tile the same
+//               warps drain the accumulator (tcgen05.ld) and store C.
+//   TMEM: 256 accumulator columns + 4 stages x 32 columns of A.
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "fq_common.cuh"
+#include "fq_internal.h"
+
+namespace fq {
+namespace tc {
+
+constexpr int BM = 128;        // weight rows per tile (UMMA M)
+constexpr int BN = 256;        // tokens per tile (UMMA N)
+constexpr int BK = 64;         // K per stage (one SWIZZLE_128B atom of bf16)
+constexpr int STAGES = 4;
+constexpr int kDqWarps = 8;
+constexpr int kThreads = 32 * (2 + kDqWarps);
+constexpr int kActBytes = BN * BK * 2;     // 32 KB
+constexpr int kTmemCols = 512;
+constexpr int kAccCol = 0;                 // accumulator columns [0, 256)
+constexpr int kACol = 256;                 // A stages: [256 + 32 s, 256 + 32 s + 32)
+
+template <int BITS>
+struct Geo {
+  static constexpr int CODE_BYTES_ROW = BK * BITS / 8;        // 32 (int4) / 64 (int8)
+  static constexpr int CODE_BYTES = BM * CODE_BYTES_ROW;      // 4 KB / 8 KB
+  static constexpr int STAGE = kActBytes + CODE_BYTES;
+  static constexpr int SMEM = STAGES * STAGE + 1024;
+};
+
+// ---- tcgen05 wrappers ------------------------------------------------------------------------
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t cols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "r"(cols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t cols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols));
+}
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]));
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row core-matrix groups 1024 B apart.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);        // start address
+  d |= (uint64_t)1 << 16;                         // leading byte offset (unused for SW128 K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;               // stride byte offset
+  d |= (uint64_t)1 << 46;                         // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                         // SWIZZLE_128B
+  return d;
+}
+// Instruction descriptor for kind::f16: fp32 accumulate, K-major A and B, M=128, N=256.
+template <typename T>
+__host__ __device__ constexpr uint32_t idesc_f16() {
+  return (1u << 4)                                      // D format f32
+         | ((Dt<T>::id == FQ_BF16 ? 1u : 0u) << 7)      // A format bf16 / f16
+         | ((Dt<T>::id == FQ_BF16 ? 1u : 0u) << 10)     // B format
+         | ((uint32_t)(BN >> 3) << 17)                  // N >> 3
+         | ((uint32_t)(BM >> 4) << 24);                 // M >> 4
+}
+
+// Natural (k, k+1) pairs of an int4 word (k..k+7) as exact codes in T: byte i holds (k+2i, k+2i+1).
+template <typename T>
+__device__ __forceinline__ void i4_nat_pairs(uint32_t w, uint32_t (&q)[4]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t x = prmt(w, 0u, 0x4440u + i);  // byte i, zero extended
+    const uint32_t y = x * 0x1001u;                // lo nibble at bits 0-3, hi nibble at 16-19
+    const uint32_t v = lop3_and_xor(y, 0x000F000Fu, Dt<T>::kMagic4);
+    if (Dt<T>::id == FQ_BF16) asm("sub.rn.bf16x2 %0, %1, %2;" : "=r"(q[i]) : "r"(v), "r"(Dt<T>::kBias4));
+    else asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(q[i]) : "r"(v), "r"(Dt<T>::kBias4));
+  }
+}
+// Natural pairs of an int8 word (k..k+3): exact codes.
+template <typename T>
+__device__ __forceinline__ void i8_nat_pairs(uint32_t w, uint32_t (&q)[2]) {
+  const uint32_t u = w ^ 0x80808080u;
+  if (Dt<T>::id == FQ_FP16) {
+    asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(q[0]) : "r"(prmt(u, 0x64646464u, 0x4140u)), "r"(0x64806480u));
+    asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(q[1]) : "r"(prmt(u, 0x64646464u, 0x4342u)), "r"(0x64806480u));
+  } else {
+    float f[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) f[i] = __uint_as_float(prmt(u, 0x4B000000u, 0x7440u + i)) - 8388736.0f;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(q[0]) : "f"(f[1]), "f"(f[0]));
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(q[1]) : "f"(f[3]), "f"(f[2]));
+  }
+}
+template <typename T>
+__device__ __forceinline__ uint32_t mul2x(uint32_t a, uint32_t b) {
+  uint32_t d;
+  if (Dt<T>::id == FQ_BF16) asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  else asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+
+struct TcParams {
+  const void* scales;
+  void* C;
+  int M, K, N, group, cdt;
+  int m_tiles, n_tiles;
+};
+
+template <typename T, int BITS>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmQ,
+                   const TcParams p) {
+  using Gm = Geo<BITS>;
+  extern __shared__ __align__(1024) uint8_t dsmem[];
+  __shared__ __align__(8) uint64_t full_bar[STAGES], afull_bar[STAGES], empty_bar[STAGES];
+  __shared__ __align__(8) uint64_t acc_full, acc_empty;
+  __shared__ uint32_t tmem_base_sh;
+  uint8_t* sbase = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsmem) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int K = p.K, N = p.N, M = p.M;
+  const int kblocks = (K + BK - 1) / BK;
+  const int ntiles = p.m_tiles * p.n_tiles;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&afull_bar[s], 32 * kDqWarps);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(&acc_full, 1);
+    mbar_init(&acc_empty, 32 * kDqWarps);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(&tmem_base_sh, kTmemCols);
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmQ);
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = tmem_base_sh;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const uint64_t pol_a = policy_evict_last();
+      const uint64_t pol_q = policy_evict_first();
+      int s = 0;
+      uint32_t ph = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty_bar[s], ph ^ 1);
+          uint8_t* st = sbase + s * Gm::STAGE;
+          mbar_arrive_expect_tx(&full_bar[s], Gm::STAGE);
+          tma_load_2d(st, &tmA, &full_bar[s], kb * BK, mt * BN, pol_a);
+          tma_load_2d(st + kActBytes, &tmQ, &full_bar[s], kb * Gm::CODE_BYTES_ROW, nt * BM, pol_q);
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_f16<T>();
+      const uint32_t sb = smem_u32(sbase);
+      int s = 0;
+      uint32_t ph = 0, acc_ph = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        mbar_wait(&acc_empty, acc_ph ^ 1);  // epilogue drained the accumulator
+        fence_after();
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full_bar[s], ph);
+          mbar_wait(&afull_bar[s], ph);
+          fence_after();
+          const uint64_t bdesc = sw128_desc(sb + s * Gm::STAGE);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk)
+            mma_ts(tmem + kAccCol, tmem + kACol + s * 32 + kk * 8, bdesc + (uint64_t)(kk * 2), idesc,
+                   (kb | kk) != 0);
+          mma_commit(&empty_bar[s]);
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+        mma_commit(&acc_full);
+        acc_ph ^= 1;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ dequant + epilogue
+    const int dq = warp - 2;
+    const int quarter = warp & 3;            // TMEM lane quarter this warp may access
+    const int half = dq >> 2;                // which 32 k of the 64-k block
+    const int row = quarter * 32 + lane;     // weight row within the tile == TMEM lane
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    const T* __restrict__ S = reinterpret_cast<const T*>(p.scales);
+    const int G = K / p.group;
+    const uint32_t sb = smem_u32(sbase);
+    int s = 0;
+    uint32_t ph = 0, acc_ph = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+      const int n = nt * BM + row;
+      const int nc = min(n, N - 1);
+      for (int kb = 0; kb < kblocks; ++kb) {
+        const int k0 = kb * BK + half * 32;  // this thread's 32 k
+        // scale(s) for this thread's k range (group % 32 == 0: one scale; else per 8-k word)
+        uint32_t sc[4];
+        if (p.group % 32 == 0) {
+          const int j = min(k0 / p.group, G - 1);
+          const unsigned short v = __ldg(reinterpret_cast<const unsigned short*>(S) + (size_t)j * N + nc);
+          sc[0] = sc[1] = sc[2] = sc[3] = (uint32_t)v | ((uint32_t)v << 16);
+        } else {
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            const int j = min((k0 + 8 * w) / p.group, G - 1);
+            const unsigned short v = __ldg(reinterpret_cast<const unsigned short*>(S) + (size_t)j * N + nc);
+            sc[w] = (uint32_t)v | ((uint32_t)v << 16);
+          }
+        }
+        mbar_wait(&full_bar[s], ph);
+        const uint32_t qbase = sb + s * Gm::STAGE + kActBytes + row * Gm::CODE_BYTES_ROW;
+        uint32_t out[16];
+        if (BITS == 4) {
+          // 16 bytes = 32 codes; SWIZZLE_32B: 16-byte chunk c of row r sits at c ^ ((r >> 2) & 1)
+          const uint4 c = lds128(qbase + ((half ^ ((row >> 2) & 1)) << 4));
+          const uint32_t words[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            uint32_t q[4];
+            i4_nat_pairs<T>(words[w], q);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) out[4 * w + i] = mul2x<T>(q[i], sc[w]);
+          }
+        } else {
+          // 32 bytes = 32 codes; SWIZZLE_64B: chunk c of row r sits at c ^ ((r >> 1) & 3)
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int cidx = half * 2 + hh;
+            const uint4 c = lds128(qbase + ((cidx ^ ((row >> 1) & 3)) << 4));
+            const uint32_t words[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+              uint32_t q[2];
+              i8_nat_pairs<T>(words[w], q);
+              const uint32_t scw = sc[hh * 2 + (w >> 1)];
+              out[8 * hh + 2 * w] = mul2x<T>(q[0], scw);
+              out[8 * hh + 2 * w + 1] = mul2x<T>(q[1], scw);
+            }
+          }
+        }
+        tmem_st16(tmem + lane_base + kACol + s * 32 + half * 16, out);
+        tmem_wait_st();
+        fence_before();
+        mbar_arrive(&afull_bar[s]);
+        if (++s == STAGES) { s = 0; ph ^= 1; }
+      }
+      // ---- epilogue: accumulator row `row` (weight n), tokens [half*128, half*128+128)
+      mbar_wait(&acc_full, acc_ph);
+      acc_ph ^= 1;
+      fence_after();
+      const int tok_base = mt * BN + half * 128;
+#pragma unroll 1
+      for (int c0 = 0; c0 < 128; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld32(tmem + lane_base + kAccCol + half * 128 + c0, v);
+        tmem_wait_ld();
+        if (n < N) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int tok = tok_base + c0 + i;
+            if (tok < M) {
+              const float f = __uint_as_float(v[i]);
+              if (p.cdt == FQ_FP32) reinterpret_cast<float*>(p.C)[(size_t)tok * N + n] = f;
+              else reinterpret_cast<T*>(p.C)[(size_t)tok * N + n] = Dt<T>::from_f(f);
+            }
+          }
+        }
+      }
+      fence_before();
+      mbar_arrive(&acc_empty);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    tmem_dealloc(tmem, kTmemCols);
+  }
+}
+
+}  // namespace tc
+
+// ------------------------------------------------------------------------------------- host side
+template <typename T, int BITS>
+static cudaError_t launch_tc(const void* A, int M, int K, int N, const void* codes, const void* scales,
+                             int group, void* C, int cdt, cudaStream_t st) {
+  using Gm = tc::Geo<BITS>;
+  CUtensorMap tmA, tmQ;
+  if (!make_tmap_2d(&tmA, A, 2, (uint64_t)K, (uint64_t)M, (uint64_t)K * 2, tc::BK, tc::BN, 128))
+    return cudaErrorInvalidValue;
+  const uint64_t row_bytes = (uint64_t)K * BITS / 8;
+  if (!make_tmap_2d(&tmQ, codes, 1, row_bytes, (uint64_t)N, row_bytes, Gm::CODE_BYTES_ROW, tc::BM,
+                    BITS == 4 ? 32 : 64))
+    return cudaErrorInvalidValue;
+  tc::TcParams prm{};
+  prm.scales = scales;
+  prm.C = C;
+  prm.M = M; prm.K = K; prm.N = N; prm.group = group; prm.cdt = cdt;
+  prm.m_tiles = (M + tc::BN - 1) / tc::BN;
+  prm.n_tiles = (N + tc::BM - 1) / tc::BM;
+  auto kern = tc::gemm_tc_kernel<T, BITS>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Gm::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int tiles = prm.m_tiles * prm.n_tiles;
+  const int grid = std::min(tiles, num_sms());
+  kern<<<grid, tc::kThreads, Gm::SMEM, st>>>(tmA, tmQ, prm);
+  return cudaGetLastError();
+}
+
+cudaError_t run_gemm_tc(int adt, int cdt, int bits, const void* A, int M, int K, int N, const void* codes,
+                        const void* scales, int group, void* C, cudaStream_t st) {
+  if (adt == FQ_BF16)
+    return bits == 4 ? launch_tc<__nv_bfloat16, 4>(A, M, K, N, codes, scales, group, C, cdt, st)
+                     : launch_tc<__nv_bfloat16, 8>(A, M, K, N, codes, scales, group, C, cdt, st);
+  return bits == 4 ? launch_tc<__half, 4>(A, M, K, N, codes, scales, group, C, cdt, st)
+                   : launch_tc<__half, 8>(A, M, K, N, codes, scales, group, C, cdt, st);
+}
+
+}  // namespace fq

@@ -134,7 +134,7 @@ __device__ __forceinline__ void i4_pairs_off(uint32_t w, uint32_t (&q)[4]) {
   constexpr uint32_t mask = 0x000F000Fu;
   q[0] = lop3_and_xor(w, mask, Dt<T>::kMagic4);
   q[1] = lop3_and_xor(__umulhi(w, 1u << 28), mask, Dt<T>::kMagic4);  // w >> 4
-  q[2] = lop3_and_xor(__umulhi(w, 1u << 24), mask, Dt<T>::kMagic4);  // w >> 8 on the FMA pipe
+  q[2] = lop3_and_xor(w >> 8, mask, Dt<T>::kMagic4);  // (SHF; an IMAD.HI here measured slower)
   q[3] = lop3_and_xor(__umulhi(w, 1u << 20), mask, Dt<T>::kMagic4);  // w >> 12
 }
 template <typename T, int BITS> struct CodeOffset { static constexpr float v = 0.f; };

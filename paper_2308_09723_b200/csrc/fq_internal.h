@@ -26,6 +26,10 @@ cudaError_t run_gemv(const GemvPlan& p, int adt, int cdt, int bits, const void* 
                      int N, const void* codes, const void* scales, int group, void* C, void* ws,
                      cudaStream_t st);
 
+// Large-M tensor-core GEMM (tcgen05 + TMEM, kernel A6).
+cudaError_t run_gemm_tc(int adt, int cdt, int bits, const void* A, int M, int K, int N, const void* codes,
+                        const void* scales, int group, void* C, cudaStream_t st);
+
 int num_sms();
 
 // 2-D TMA descriptor (CUtensorMap, 128 bytes, written to `tmap`).  elem_bytes 1/2/4 -> u8/bf16/f32.
