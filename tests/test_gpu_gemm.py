@@ -105,16 +105,21 @@ def test_split_k_paths(fq, env, splits, M):
         assert O.rel_err(torch_to_f64(C), Cr, D) <= TOL
 
 
-def test_identity_exact_fp32_out(fq):
+@pytest.mark.parametrize("path", ["decode", "tc"])
+def test_identity_exact_fp32_out(fq, env, path):
     """A = I (M = K = 256): C[k, n] = q[n,k] * s[k/g, n] exactly in fp32-output mode — catches any
-    nibble-order / k-permutation / scale-index bug with zero tolerance."""
+    nibble-order / k-permutation / scale-index bug with zero tolerance.
+    decode path: run as 16 token tiles of the M<=16 kernel (FQ_GEMM_PATH=decode)."""
+    env("FQ_GEMM_PATH", path)
     K = N = 256
     Wb = gaussian_bits((N, K), 0.02, 5)
-    # groups that are a multiple of the K chunk (128 int4 / 64 int8) apply the scale in fp32 on
-    # exact integer partials -> exact; smaller groups dequantize q*s to the activation dtype
-    # first (one bf16 rounding, the paper's own "dequantize to the activation dtype", P:170).
+    # decode kernel: groups that are a multiple of its K chunk (128 int4 / 64 int8) apply the scale
+    # in fp32 on exact integer partials -> exact.  Smaller groups, and the tcgen05 kernel always,
+    # dequantize q*s to the activation dtype first (one bf16 rounding: the paper's own "dequantize
+    # the weights to match the data type of the activation", P:170).
     for bits, group, exact in ((4, 128, True), (8, 64, True), (4, 256, True), (8, 256, True),
                                (4, 64, False), (4, 16, False), (8, 16, False)):
+        exact = exact and path == "decode"
         W = bits_to_torch(Wb, "bf16")
         qw = fq.quantize(W, bits, group)
         A = torch.eye(K, dtype=torch.bfloat16, device="cuda")
@@ -177,3 +182,43 @@ def test_opt175b_full_size_sampled(fq, shape, bits, M):
     assert O.rel_err(torch_to_f64(C)[:, cols], Cr, D) <= TOL
     # the sampled columns' codes/scales are bit-exact as well
     assert np.array_equal(qw.codes[torch.from_numpy(cols).cuda()].cpu().numpy(), O.pack_codes(r.q, bits))
+
+
+@pytest.mark.parametrize("M,K,N,bits,group,adt", [
+    (256, 256, 256, 4, 64, "bf16"),        # one tile
+    (300, 1024, 392, 4, 128, "bf16"),      # ragged M and N tails, several K blocks
+    (520, 2048, 640, 8, 128, "bf16"),
+    (257, 1536, 264, 4, 48, "bf16"),       # non-power-of-two group (adaptive ladder of 12288)
+    (512, 2048, 1024, 4, 32, "fp16"),
+    (384, 1024, 512, 8, 1024, "fp16"),     # per-column
+    (17, 512, 256, 4, 16, "bf16"),         # smallest M routed to the tcgen05 kernel
+])
+def test_tc_path_parity(fq, env, M, K, N, bits, group, adt):
+    """Large-M tcgen05 kernel (A6) vs the fp64 oracle on full outputs."""
+    env("FQ_GEMM_PATH", "tc")
+    Wb, Ab = make_case(M, K, N, bits, group, adt, seed=M + K, outliers=1)
+    _, C = run_case(fq, Wb, Ab, bits, group, adt)
+    Cr, D = oracle_ref(Wb, Ab, bits, group, adt)
+    assert O.rel_err(torch_to_f64(C), Cr, D) <= TOL
+
+
+@pytest.mark.parametrize("shape", [(12288, 49152), (49152, 12288)])
+@pytest.mark.parametrize("bits", [4, 8])
+def test_opt175b_prefill_sampled(fq, shape, bits):
+    """configs[2]: OPT-175B prefill GEMM at M=2048 through the tcgen05 kernel, parity on sampled
+    outputs (64 columns x 48 token rows) computed by the oracle."""
+    K, N = shape
+    M = 2048
+    from synth import gaussian_torch
+    W = gaussian_torch((N, K), 0.02, 3000 + K)
+    A = gaussian_torch((M, K), 1.0, 4000 + K)
+    qw = fq.quantize(W, bits, 128)
+    C = fq.gemm(A, qw)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(1)
+    cols = rng.choice(N, 64, replace=False)
+    rows = rng.choice(M, 48, replace=False)
+    Wc = W[torch.from_numpy(cols).cuda()].float().cpu().double().numpy()
+    r = O.quantize(Wc, bits, 128, O.BF16)
+    Cr, D = O.gemm(A[torch.from_numpy(rows).cuda()].float().cpu().double().numpy(), r.q, r.s, 128)
+    assert O.rel_err(torch_to_f64(C)[np.ix_(rows, cols)], Cr, D) <= TOL
