@@ -5,8 +5,9 @@
 // activation dtype.  Arithmetic contract (bit-exact with the oracle):
 //   * amax is exact;  s = RNE_dtype((double)(2*amax) / (2^b-1)) — the double quotient can never sit
 //     on a bf16/fp16 tie, so this equals one rounding of the exact rational (R4);
-//   * q = roundf(__fdiv_rn(x, s)) for bf16/fp16 inputs (exact decision: x has <= 11 significant
-//     bits), round((double)x/(double)s) for fp32 inputs; clamp to [-2^(b-1), 2^(b-1)-1].
+//   * q = clamp(round_half_away(x / s)): estimated with the reciprocal, then decided exactly by
+//     comparing |x| with the exact fp32 products (m +- 1/2) * s (any input dtype); clamp to
+//     [-2^(b-1), 2^(b-1)-1].
 // A1 follows P:147-149 §3.3 under reading R6: level L fires iff some child group range is below
 // alpha * its parent's range, compared exactly as 1000*child < alpha_milli*parent in fp64.
 //
@@ -87,6 +88,7 @@ __global__ void __launch_bounds__(sizeof(TIn) == 4 ? 512 : 1024) quantize_kernel
   const int cpg = group >> 3;  // chunks per group
   float* pm = smem;            // [nchunk]
   float* sc = smem + nchunk;   // [G] scale as float (0 => codes 0)
+  float* sr = sc + G;          // [G] rcp(scale) (0 when the scale is 0)
   __shared__ int s_status;
   const int n = blockIdx.x;
   const TIn* row = W + (size_t)n * K;
@@ -127,6 +129,7 @@ __global__ void __launch_bounds__(sizeof(TIn) == 4 ? 512 : 1024) quantize_kernel
       }
     }
     sc[j] = s;
+    sr[j] = s == 0.f ? 0.f : __frcp_rn(s);
     scales[(size_t)j * N + n] = s_t;
     if (st) atomicOr(&s_status, st);
   };
@@ -156,19 +159,21 @@ __global__ void __launch_bounds__(sizeof(TIn) == 4 ? 512 : 1024) quantize_kernel
     float v[8];
     raw[ci].decode(v);
     const float s = sc[c / cpg];
+    const float rs = sr[c / cpg];  // rcp(s), 0 when s == 0
     int q[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      float r;
-      if (s == 0.f) {
-        r = 0.f;
-      } else if (Dt<TIn>::id == FQ_FP32) {
-        r = (float)round((double)v[i] / (double)s);
-      } else {
-        r = roundf(__fdiv_rn(v[i], s));
-      }
-      r = fminf(fmaxf(r, (float)lo), (float)hi);
-      q[i] = (int)r;
+      // q = clamp(round_half_away(x / s)) without a division: m ~ floor(|x|/s + 1/2) from the
+      // reciprocal, then made exact by comparing |x| with the exact products (m +- 1/2) * s
+      // ((m +- 1/2) has <= 9 significant bits, s <= 11, so the products are exact in fp32).
+      const float ax = fabsf(v[i]);
+      int m = __float2int_rd(fmaf(ax, rs, 0.5f));
+      if (__fmul_rn((float)m + 0.5f, s) <= ax) ++m;
+      else if (m > 0 && __fmul_rn((float)m - 0.5f, s) > ax) --m;
+      if (s == 0.f) m = 0;
+      const bool neg = v[i] < 0.f;
+      m = min(m, neg ? -lo : hi);
+      q[i] = neg ? -m : m;
     }
     if (BITS == 4) {
       uint32_t w = 0;
@@ -252,7 +257,7 @@ __global__ void __launch_bounds__(kQThreads) adapt_flags_kernel(const TIn* __res
 template <typename TIn, typename TS, int BITS>
 static cudaError_t launch_quant(const void* W, int K, int N, int group, void* codes, void* scales,
                                 int32_t* status, cudaStream_t st) {
-  const size_t smem = (size_t)(K / 8 + K / group) * sizeof(float);
+  const size_t smem = (size_t)(K / 8 + 2 * (K / group)) * sizeof(float);
   auto kern = quantize_kernel<TIn, TS, BITS>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
