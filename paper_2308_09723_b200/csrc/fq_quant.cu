@@ -167,10 +167,14 @@ __global__ void __launch_bounds__(sizeof(TIn) == 4 ? 512 : 1024) quantize_kernel
       // reciprocal, then made exact by comparing |x| with the exact products (m +- 1/2) * s
       // ((m +- 1/2) has <= 9 significant bits, s <= 11, so the products are exact in fp32).
       const float ax = fabsf(v[i]);
-      int m = __float2int_rd(fmaf(ax, rs, 0.5f));
-      if (__fmul_rn((float)m + 0.5f, s) <= ax) ++m;
-      else if (m > 0 && __fmul_rn((float)m - 0.5f, s) > ax) --m;
-      if (s == 0.f) m = 0;
+      int m;
+      if (s >= 1e-30f) {
+        m = __float2int_rd(fmaf(ax, rs, 0.5f));
+        if (__fmul_rn((float)m + 0.5f, s) <= ax) ++m;
+        else if (m > 0 && __fmul_rn((float)m - 0.5f, s) > ax) --m;
+      } else {  // tiny / subnormal scales: rcp overflows and products lose exactness -> IEEE divide
+        m = s == 0.f ? 0 : (int)fminf(roundf(__fdiv_rn(ax, s)), 256.f);
+      }
       const bool neg = v[i] < 0.f;
       m = min(m, neg ? -lo : hi);
       q[i] = neg ? -m : m;
