@@ -160,34 +160,47 @@ __global__ void __launch_bounds__(sizeof(TIn) == 4 ? 512 : 1024) quantize_kernel
     raw[ci].decode(v);
     const float s = sc[c / cpg];
     const float rs = sr[c / cpg];  // rcp(s), 0 when s == 0
-    int q[8];
+    const float hs = 0.5f * s;     // exact
+    // offset-binary code u = q + 2^(b-1) in [0, 2^b - 1]; the stored two's complement field is
+    // u ^ 2^(b-1).  Kept in float until the final pack (all values are small exact integers).
+    uint32_t u[8];
+    if (Dt<TIn>::id != FQ_FP32 && s >= 1e-30f) {
+      // 16-bit W: m = floor(|x| * rcp(s) + 1/2) is exact except possibly at an exact tie
+      // |x| = (m + 1/2) s, where the estimate may fall one short; the tie is detected exactly
+      // because (m + 1/2) s = fma(m, s, s/2) is an exact fp32 value (<= 20 significant bits).
+      // Off-tie quotients are >= 2^-13 (absolute) away from a half-integer (x, s have <= 11
+      // significant bits), far beyond the ~2^-16 error of the estimate.
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      // q = clamp(round_half_away(x / s)) without a division: m ~ floor(|x|/s + 1/2) from the
-      // reciprocal, then made exact by comparing |x| with the exact products (m +- 1/2) * s
-      // ((m +- 1/2) has <= 9 significant bits, s <= 11, so the products are exact in fp32).
-      const float ax = fabsf(v[i]);
-      int m;
-      if (s >= 1e-30f) {
-        m = __float2int_rd(fmaf(ax, rs, 0.5f));
-        if (__fmul_rn((float)m + 0.5f, s) <= ax) ++m;
-        else if (m > 0 && __fmul_rn((float)m - 0.5f, s) > ax) --m;
-      } else {  // tiny / subnormal scales: rcp overflows and products lose exactness -> IEEE divide
-        m = s == 0.f ? 0 : (int)fminf(roundf(__fdiv_rn(ax, s)), 256.f);
+      for (int i = 0; i < 8; ++i) {
+        const float ax = fabsf(v[i]);
+        float m = floorf(fmaf(ax, rs, 0.5f));
+        m = (fmaf(m, s, hs) == ax) ? m + 1.f : m;
+        const bool neg = v[i] < 0.f;
+        m = fminf(m, neg ? (float)-lo : (float)hi);
+        u[i] = (uint32_t)(int)((neg ? -m : m) + (float)-lo);
       }
-      const bool neg = v[i] < 0.f;
-      m = min(m, neg ? -lo : hi);
-      q[i] = neg ? -m : m;
+    } else {
+      // fp32 W (no tie-distance guarantee) and tiny/subnormal scales: IEEE division decides.
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float m = 0.f;
+        if (s != 0.f) m = fminf(roundf(__fdiv_rn(fabsf(v[i]), s)), 256.f);
+        const bool neg = v[i] < 0.f;
+        m = fminf(m, neg ? (float)-lo : (float)hi);
+        u[i] = (uint32_t)(int)((neg ? -m : m) + (float)-lo);
+      }
     }
     if (BITS == 4) {
-      uint32_t w = 0;
+      uint32_t w = u[7];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) w |= (uint32_t)(q[i] & 0xF) << (4 * i);
-      reinterpret_cast<uint32_t*>(codes + (size_t)n * (K / 2))[c] = w;
+      for (int i = 6; i >= 0; --i) w = w * 16u + u[i];
+      reinterpret_cast<uint32_t*>(codes + (size_t)n * (K / 2))[c] = w ^ 0x88888888u;
     } else {
       uint2 w;
-      w.x = (q[0] & 0xFF) | (q[1] & 0xFF) << 8 | (q[2] & 0xFF) << 16 | (uint32_t)(q[3] & 0xFF) << 24;
-      w.y = (q[4] & 0xFF) | (q[5] & 0xFF) << 8 | (q[6] & 0xFF) << 16 | (uint32_t)(q[7] & 0xFF) << 24;
+      w.x = ((u[3] * 256u + u[2]) * 256u + u[1]) * 256u + u[0];
+      w.y = ((u[7] * 256u + u[6]) * 256u + u[5]) * 256u + u[4];
+      w.x ^= 0x80808080u;
+      w.y ^= 0x80808080u;
       reinterpret_cast<uint2*>(codes + (size_t)n * K)[c] = w;
     }
   }
