@@ -28,7 +28,7 @@ struct Chunk8 {
   uint4 r[NV];
   __device__ __forceinline__ void load(const TIn* p) {
 #pragma unroll
-    for (int i = 0; i < NV; ++i) r[i] = ldg_keep(reinterpret_cast<const uint4*>(p) + i);
+    for (int i = 0; i < NV; ++i) r[i] = __ldg(reinterpret_cast<const uint4*>(p) + i);
   }
   __device__ __forceinline__ void decode(float (&v)[8]) const;
 };
@@ -98,11 +98,16 @@ __global__ void __launch_bounds__(sizeof(TIn) == 4 ? 512 : 1024) quantize_kernel
   // the launcher sizes the CTA so that K <= 8 * CPT * blockDim.x) — W is read from HBM once.
   const int T = blockDim.x;
   Chunk8<TIn> raw[CPT];
+  // all loads first (CPT x 16 B in flight per thread), then the maxima
+#pragma unroll
+  for (int i = 0; i < CPT; ++i) {
+    const int c = threadIdx.x + i * T;
+    if (c < nchunk) raw[i].load(row + (size_t)c * 8);
+  }
 #pragma unroll
   for (int i = 0; i < CPT; ++i) {
     const int c = threadIdx.x + i * T;
     if (c < nchunk) {
-      raw[i].load(row + (size_t)c * 8);
       float v[8];
       raw[i].decode(v);
       pm[c] = chunk_amax(v);
