@@ -135,13 +135,15 @@ fq_status fq_gemm(const void* A, int32_t adt, int64_t M, const fq_wdesc* d, cons
  * matrices"; MoE experts P:166-167).  Tokens are sorted by expert:
  *   rows offsets[e] .. offsets[e+1]-1 of A ([T, K]) use expert e; C is [T, N].
  * offsets_host: HOST array of E+1 int64 (non-decreasing, offsets[0] = 0, offsets[E] = T).
- * codes_dev / scales_dev: DEVICE arrays of E device pointers; groups_host: HOST array of E group
- * sizes (each valid for K).  ws: fq_gemm_grouped_workspace_bytes(...) bytes, zero-filled once.
+ * codes_host / scales_host: HOST arrays of E DEVICE pointers (canonical layout per expert);
+ * groups_host: HOST array of E group sizes (each valid for K).  Experts with 1 <= M_e <= 16 run
+ * in one launch per kernel class of the decode kernel (A4, batched); larger experts run the
+ * tcgen05 kernel (A6).  ws: fq_gemm_grouped_workspace_bytes(...) bytes (may be NULL today).
  * ------------------------------------------------------------------------------------------- */
 size_t fq_gemm_grouped_workspace_bytes(int64_t T, int32_t E, const fq_wdesc* d);
 fq_status fq_gemm_grouped(const void* A, int32_t adt, int64_t T, const int64_t* offsets_host,
                           int32_t E, const fq_wdesc* d, const int32_t* groups_host,
-                          const void* const* codes_dev, const void* const* scales_dev, void* C,
+                          const void* const* codes_host, const void* const* scales_host, void* C,
                           int32_t cdt, void* ws, size_t ws_bytes, void* stream);
 
 #ifdef __cplusplus

@@ -6,6 +6,7 @@
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "../../include/fq.h"
 #include "fq_internal.h"
@@ -159,17 +160,49 @@ fq_status fq_gemm(const void* A, int32_t adt, int64_t M, const fq_wdesc* d, cons
 }
 
 size_t fq_gemm_grouped_workspace_bytes(int64_t T, int32_t E, const fq_wdesc* d) {
-  (void)T; (void)E; (void)d;
-  return 0;
+  (void)T; (void)E;
+  if (check_wdesc(d) != FQ_OK) return 0;
+  return 256;  // the grouped kernels need no split-K scratch (the batch fills the machine)
 }
 
 fq_status fq_gemm_grouped(const void* A, int32_t adt, int64_t T, const int64_t* offsets_host,
                           int32_t E, const fq_wdesc* d, const int32_t* groups_host,
-                          const void* const* codes_dev, const void* const* scales_dev, void* C,
+                          const void* const* codes_host, const void* const* scales_host, void* C,
                           int32_t cdt, void* ws, size_t ws_bytes, void* stream) {
-  (void)A; (void)adt; (void)T; (void)offsets_host; (void)E; (void)d; (void)groups_host;
-  (void)codes_dev; (void)scales_dev; (void)C; (void)cdt; (void)ws; (void)ws_bytes; (void)stream;
-  return FQ_ERR_UNSUPPORTED;
+  (void)ws_bytes;
+  if (!d || !offsets_host || !groups_host || !codes_host || !scales_host || !A || !C || E <= 0)
+    return FQ_ERR_INVALID_ARG;
+  if (!valid_half(adt) || d->scale_dtype != adt || (cdt != adt && cdt != FQ_FP32)) return FQ_ERR_UNSUPPORTED;
+  if (offsets_host[0] != 0 || offsets_host[E] != T || T < 0) return FQ_ERR_SHAPE;
+  std::vector<int> small;
+  small.reserve(E);
+  for (int32_t e = 0; e < E; ++e) {
+    fq_wdesc de = *d;
+    de.group = groups_host[e];
+    const fq_status s = check_wdesc(&de);
+    if (s != FQ_OK) return s;
+    if (offsets_host[e + 1] < offsets_host[e]) return FQ_ERR_SHAPE;
+    if (!codes_host[e] || !scales_host[e]) return FQ_ERR_INVALID_ARG;
+  }
+  const cudaStream_t st = as_stream(stream);
+  const size_t cbytes = cdt == FQ_FP32 ? 4 : 2;
+  for (int32_t e = 0; e < E; ++e) {
+    const int64_t Me = offsets_host[e + 1] - offsets_host[e];
+    if (Me == 0) continue;
+    if (Me <= 16 && !use_tc_path(Me)) {
+      small.push_back(e);
+    } else {  // large expert batch: the tcgen05 kernel
+      const char* Ae = reinterpret_cast<const char*>(A) + (size_t)offsets_host[e] * d->K * 2;
+      char* Ce = reinterpret_cast<char*>(C) + (size_t)offsets_host[e] * d->N * cbytes;
+      cudaError_t r = run_gemm_tc(adt, cdt, d->bits, Ae, (int)Me, (int)d->K, (int)d->N, codes_host[e],
+                                  scales_host[e], groups_host[e], Ce, st);
+      if (r != cudaSuccess) return FQ_ERR_CUDA;
+    }
+  }
+  if (!small.empty())
+    return from_cuda(run_gemv_grouped(adt, cdt, d->bits, A, (int)d->K, (int)d->N, offsets_host, groups_host,
+                                      codes_host, scales_host, C, ws, 0, small.data(), (int)small.size(), st));
+  return FQ_OK;
 }
 
 }  // extern "C"

@@ -50,19 +50,25 @@ struct DecGeom {
   static constexpr int TOK_BYTES = KS * 2 + 64;        // token row stride in smem, = 64 mod 128
 };
 
-struct DecMaps {
+// One decode problem (a matrix, its activation slice and output slice) of a batch.  A single
+// launch can cover several problems (MoE experts): CTAs are numbered consecutively across the
+// problems and each CTA finds its problem from `cta_begin`.  The TMA descriptors live in the
+// __grid_constant__ parameter block (TMA accepts param-space descriptors).
+struct DecProb {
   CUtensorMap w;  // packed codes [N][K*bits/8] u8, box [256 rows][64 B], SWIZZLE_64B
   CUtensorMap a;  // activations [M][K] 16-bit, box [MT*8 rows][K per stage]
   CUtensorMap s;  // scales [G][N] 16-bit, box [1 row][256 columns]
-};
-
-struct DecodeParams {
-  const void* A;
   const void* scales;
   void* C;
-  float* ws;
-  int* counters;
+  float* ws;      // split-K partials [splits][M][N]
+  int* counters;  // [ktiles][gx]
   int M, K, N, group, klen, cdt;
+  int gx, splits, ktiles, cta_begin;
+};
+template <int MAXP>
+struct DecBatch {
+  DecProb p[MAXP];
+  int nprob;
 };
 
 template <typename T>
@@ -194,10 +200,8 @@ __device__ __forceinline__ int swz64(int c, int R) { return c ^ ((R >> 1) & 3); 
 
 // DBG (diagnostics only, selected by FQ_DEC_DEBUG for bf16/int4/M<=8): 1 = no MMA (fake FADD
 // accumulate), 2 = no dequant (raw code words as MMA operands), 3 = consumers skip all compute.
-template <typename T, int BITS, int MT, bool SACC, int DBG = 0>
-__global__ void __launch_bounds__(kDecThreads, 2)
-    decode_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA,
-                  const __grid_constant__ CUtensorMap tmS, const DecodeParams p) {
+template <typename T, int BITS, int MT, bool SACC, int DBG, int MAXP>
+__global__ void __launch_bounds__(kDecThreads, 2) decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
   using G = DecGeom<BITS>;
   constexpr int KS = G::KS, SEG = G::SEG, KCH = G::KCH, CHUNKS = G::CHUNKS, PIECES = G::PIECES;
   constexpr int TOK = G::TOK_BYTES;
@@ -217,12 +221,17 @@ __global__ void __launch_bounds__(kDecThreads, 2)
   uint8_t* sbase = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsmem) + 1023) & ~uintptr_t(1023));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int pi = 0;
+  while (pi + 1 < batch.nprob && (int)blockIdx.x >= batch.p[pi + 1].cta_begin) ++pi;
+  const DecProb& p = batch.p[pi];
+  const int local = (int)blockIdx.x - p.cta_begin;
+  const int bx = local % p.gx, by = (local / p.gx) % p.splits, bz = local / (p.gx * p.splits);
   const int N = p.N, K = p.K, M = p.M;
-  const int n0 = blockIdx.x * kRowsPerCta;
-  const int kbeg = blockIdx.y * p.klen;
+  const int n0 = bx * kRowsPerCta;
+  const int kbeg = by * p.klen;
   const int kend = min(K, kbeg + p.klen);
   const int nst = (kend - kbeg + KS - 1) / KS;
-  const int tok0 = blockIdx.z * 16;
+  const int tok0 = bz * 16;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kDecStages; ++s) {
@@ -233,9 +242,9 @@ __global__ void __launch_bounds__(kDecThreads, 2)
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
-    prefetch_tmap(&tmW);
-    prefetch_tmap(&tmA);
-    if (SACC) prefetch_tmap(&tmS);
+    prefetch_tmap(&p.w);
+    prefetch_tmap(&p.a);
+    if (SACC) prefetch_tmap(&p.s);
   }
   __syncthreads();
 
@@ -254,13 +263,13 @@ __global__ void __launch_bounds__(kDecThreads, 2)
         uint8_t* st = sbase + s * STAGE_BYTES;
         const int k0 = kbeg + i * KS;
         mbar_arrive_expect_tx(&full_bar[s], kStageW + (SACC ? SC_BYTES : 0));
-        tma_load_2d(st, &tmW, &full_bar[s], k0 * BITS / 8, n0, polw);
+        tma_load_2d(st, &p.w, &full_bar[s], k0 * BITS / 8, n0, polw);
         if (SACC) {
-          tma_load_2d(st + SC_OFS, &tmS, &full_bar[s], n0, gj, polw);
+          tma_load_2d(st + SC_OFS, &p.s, &full_bar[s], n0, gj, polw);
           if (++grem == gm) { grem = 0; ++gj; }
         }
         mbar_arrive_expect_tx(&raw_bar[s], RAW_BYTES);
-        tma_load_2d(st + RAW_OFS, &tmA, &raw_bar[s], k0, tok0, pola);
+        tma_load_2d(st + RAW_OFS, &p.a, &raw_bar[s], k0, tok0, pola);
         if (++s == kDecStages) { s = 0; ph ^= 1; }
       }
     }
@@ -481,7 +490,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
     if (p.cdt == FQ_FP32) reinterpret_cast<float*>(p.C)[o] = v;
     else reinterpret_cast<T*>(p.C)[o] = Dt<T>::from_f(v);
   };
-  const int S_ = gridDim.y;
+  const int S_ = p.splits;
   if (S_ == 1) {
 #pragma unroll
     for (int rt = 0; rt < 2; ++rt)
@@ -495,7 +504,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
         }
     return;
   }
-  float* part_out = p.ws + (size_t)blockIdx.y * M * N;
+  float* part_out = p.ws + (size_t)by * M * N;
 #pragma unroll
   for (int rt = 0; rt < 2; ++rt)
 #pragma unroll
@@ -508,7 +517,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
       }
   __threadfence();
   asm volatile("bar.sync 1, %0;" ::"n"(32 * kConsumerWarps));
-  int* ctr = p.counters + blockIdx.z * gridDim.x + blockIdx.x;
+  int* ctr = p.counters + bz * p.gx + bx;
   if (threadIdx.x == 32) s_last = (atomicAdd(ctr, 1) == S_ - 1);
   asm volatile("bar.sync 1, %0;" ::"n"(32 * kConsumerWarps));
   if (!s_last) return;
@@ -588,70 +597,126 @@ size_t gemv_workspace_bytes(const GemvPlan& p, int M, int N) {
   return kCounterBytes + align256((size_t)p.splits * M * N * sizeof(float));
 }
 
-template <typename T, int BITS, int MT, bool SACC, int DBG = 0>
-static cudaError_t launch_dec(const GemvPlan& pl, const DecMaps& tm, const DecodeParams& prm,
-                              cudaStream_t st) {
+template <typename T, int BITS, int MT, bool SACC, int DBG, int MAXP>
+static cudaError_t launch_dec(const DecBatch<MAXP>& b, int ctas, cudaStream_t st) {
   constexpr int smem = dec_smem_bytes<BITS, MT>();
-  auto kern = decode_kernel<T, BITS, MT, SACC, DBG>;
+  auto kern = decode_kernel<T, BITS, MT, SACC, DBG, MAXP>;
   static bool attr_set = false;  // benign race: idempotent attribute call
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int gx = (prm.N + pl.rows_per_cta - 1) / pl.rows_per_cta;
-  dim3 grid(gx, pl.splits, pl.ktiles);
-  kern<<<grid, kDecThreads, smem, st>>>(tm.w, tm.a, tm.s, prm);
+  kern<<<ctas, kDecThreads, smem, st>>>(b);
   return cudaGetLastError();
 }
 
-template <typename T, int BITS, int MT>
-static cudaError_t dispatch_sacc(bool sacc, const GemvPlan& pl, const DecMaps& tm,
-                                 const DecodeParams& prm, cudaStream_t st) {
-  return sacc ? launch_dec<T, BITS, MT, true>(pl, tm, prm, st) : launch_dec<T, BITS, MT, false>(pl, tm, prm, st);
+template <int MAXP>
+static cudaError_t dispatch_dec(int adt, int bits, int mt, bool sacc, int dbg, const DecBatch<MAXP>& b,
+                                int ctas, cudaStream_t st) {
+  if (dbg && adt == FQ_BF16 && bits == 4 && mt == 1 && sacc && MAXP == 1) {
+    if (dbg == 1) return launch_dec<__nv_bfloat16, 4, 1, true, 1, MAXP>(b, ctas, st);
+    if (dbg == 2) return launch_dec<__nv_bfloat16, 4, 1, true, 2, MAXP>(b, ctas, st);
+    if (dbg == 3) return launch_dec<__nv_bfloat16, 4, 1, true, 3, MAXP>(b, ctas, st);
+  }
+#define FQ_DEC_CASE(TT, BB, MM, SS) \
+  if (bits == BB && mt == MM && sacc == SS) return launch_dec<TT, BB, MM, SS, 0, MAXP>(b, ctas, st);
+  if (adt == FQ_BF16) {
+    FQ_DEC_CASE(__nv_bfloat16, 4, 1, true) FQ_DEC_CASE(__nv_bfloat16, 4, 1, false)
+    FQ_DEC_CASE(__nv_bfloat16, 4, 2, true) FQ_DEC_CASE(__nv_bfloat16, 4, 2, false)
+    FQ_DEC_CASE(__nv_bfloat16, 8, 1, true) FQ_DEC_CASE(__nv_bfloat16, 8, 1, false)
+    FQ_DEC_CASE(__nv_bfloat16, 8, 2, true) FQ_DEC_CASE(__nv_bfloat16, 8, 2, false)
+  } else {
+    FQ_DEC_CASE(__half, 4, 1, true) FQ_DEC_CASE(__half, 4, 1, false)
+    FQ_DEC_CASE(__half, 4, 2, true) FQ_DEC_CASE(__half, 4, 2, false)
+    FQ_DEC_CASE(__half, 8, 1, true) FQ_DEC_CASE(__half, 8, 1, false)
+    FQ_DEC_CASE(__half, 8, 2, true) FQ_DEC_CASE(__half, 8, 2, false)
+  }
+#undef FQ_DEC_CASE
+  return cudaErrorInvalidValue;
 }
-template <typename T, int BITS>
-static cudaError_t dispatch_mt(bool sacc, const GemvPlan& pl, const DecMaps& tm,
-                               const DecodeParams& prm, cudaStream_t st) {
-  return pl.mt == 1 ? dispatch_sacc<T, BITS, 1>(sacc, pl, tm, prm, st)
-                    : dispatch_sacc<T, BITS, 2>(sacc, pl, tm, prm, st);
+
+// Fill one batch entry (tensor maps + sizes) for one matrix under plan `pl`.  ws: that problem's
+// workspace (counters at offset 0, partials after kCounterBytes).
+static bool make_dec_prob(DecProb& d, const GemvPlan& pl, int bits, int cdt, const void* A, int M, int K,
+                          int N, const void* codes, const void* scales, int group, void* C, void* ws) {
+  const uint64_t row_bytes = (uint64_t)K * bits / 8;
+  if (!make_tmap_2d(&d.w, codes, 1, row_bytes, (uint64_t)N, row_bytes, kWBytesPerRow, kRowsPerCta, 64))
+    return false;
+  const int ks = kWBytesPerRow * 8 / bits;  // K per stage
+  if (!make_tmap_2d(&d.a, A, 2, (uint64_t)K, (uint64_t)M, (uint64_t)K * 2, ks, pl.mt * 8, 0)) return false;
+  if (!make_tmap_2d(&d.s, scales, 2, (uint64_t)N, (uint64_t)(K / group), (uint64_t)N * 2, kRowsPerCta, 1, 0))
+    return false;
+  d.scales = scales;
+  d.C = C;
+  d.M = M; d.K = K; d.N = N; d.group = group; d.cdt = cdt;
+  d.klen = pl.klen;
+  d.splits = pl.splits;
+  d.ktiles = pl.ktiles;
+  d.gx = (N + pl.rows_per_cta - 1) / pl.rows_per_cta;
+  d.counters = reinterpret_cast<int*>(ws);
+  d.ws = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + kCounterBytes);
+  return true;
 }
-template <typename T>
-static cudaError_t dispatch_bits(int bits, bool sacc, const GemvPlan& pl, const DecMaps& tm,
-                                 const DecodeParams& prm, cudaStream_t st) {
-  return bits == 4 ? dispatch_mt<T, 4>(sacc, pl, tm, prm, st) : dispatch_mt<T, 8>(sacc, pl, tm, prm, st);
-}
+
+static bool sacc_of(int bits, int group) { return group % (bits == 4 ? 128 : 64) == 0; }
 
 cudaError_t run_gemv(const GemvPlan& pl, int adt, int cdt, int bits, const void* A, int M, int K,
                      int N, const void* codes, const void* scales, int group, void* C, void* ws,
                      cudaStream_t st) {
-  DecMaps tm;
-  const uint64_t row_bytes = (uint64_t)K * bits / 8;
-  if (!make_tmap_2d(&tm.w, codes, 1, row_bytes, (uint64_t)N, row_bytes, kWBytesPerRow, kRowsPerCta, 64))
+  DecBatch<1> b{};
+  if (!make_dec_prob(b.p[0], pl, bits, cdt, A, M, K, N, codes, scales, group, C, ws))
     return cudaErrorInvalidValue;
-  const int ks = kWBytesPerRow * 8 / bits;  // K per stage
-  if (!make_tmap_2d(&tm.a, A, 2, (uint64_t)K, (uint64_t)M, (uint64_t)K * 2, ks, pl.mt * 8, 0))
-    return cudaErrorInvalidValue;
-  if (!make_tmap_2d(&tm.s, scales, 2, (uint64_t)N, (uint64_t)(K / group), (uint64_t)N * 2, kRowsPerCta, 1, 0))
-    return cudaErrorInvalidValue;
-  DecodeParams prm{};
-  prm.A = A;
-  prm.scales = scales;
-  prm.C = C;
-  prm.M = M; prm.K = K; prm.N = N; prm.group = group; prm.cdt = cdt;
-  prm.klen = pl.klen;
-  prm.counters = reinterpret_cast<int*>(ws);
-  prm.ws = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + kCounterBytes);
-  const int chunk = bits == 4 ? 128 : 64;  // K per MMA chunk (one scale per chunk if SACC)
-  const bool sacc = (group % chunk) == 0;
-  const int dbg = env_int("FQ_DEC_DEBUG", 0);
-  if (dbg && adt == FQ_BF16 && bits == 4 && pl.mt == 1 && sacc) {
-    if (dbg == 1) return launch_dec<__nv_bfloat16, 4, 1, true, 1>(pl, tm, prm, st);
-    if (dbg == 2) return launch_dec<__nv_bfloat16, 4, 1, true, 2>(pl, tm, prm, st);
-    if (dbg == 3) return launch_dec<__nv_bfloat16, 4, 1, true, 3>(pl, tm, prm, st);
+  b.p[0].cta_begin = 0;
+  b.nprob = 1;
+  const int ctas = b.p[0].gx * pl.splits * pl.ktiles;
+  return dispatch_dec<1>(adt, bits, pl.mt, sacc_of(bits, group), env_int("FQ_DEC_DEBUG", 0), b, ctas, st);
+}
+
+// ---- MoE batch (kernel A7, decode side): experts listed in `experts` (each with 1 <= M_e <= 16)
+// are grouped by (MMA token tiles, scale path) and each group runs as ONE launch over all of its
+// experts (<= kMaxBatch per launch; the descriptors travel in the kernel parameter block).
+constexpr int kMaxBatch = 48;
+
+cudaError_t run_gemv_grouped(int adt, int cdt, int bits, const void* A, int K, int N,
+                             const int64_t* offsets, const int32_t* groups, const void* const* codes,
+                             const void* const* scales, void* C, void* ws, size_t ws_per_expert,
+                             const int* experts, int nexp, cudaStream_t st) {
+  static_assert(sizeof(DecBatch<kMaxBatch>) < 32000, "kernel parameter block limit");
+  for (int cls = 0; cls < 4; ++cls) {
+    const int mt = 1 + (cls >> 1);
+    const bool sacc = cls & 1;
+    DecBatch<kMaxBatch> b{};
+    int ctas = 0;
+    for (int ii = 0; ii < nexp; ++ii) {
+      const int e = experts[ii];
+      const int Me = (int)(offsets[e + 1] - offsets[e]);
+      GemvPlan pl = plan_gemv(Me, K, N, bits, groups[e], num_sms());
+      // the batch fills the machine by itself: no split-K, so no workspace
+      pl.splits = 1;
+      pl.klen = ((K + pl.kchunk - 1) / pl.kchunk) * pl.kchunk;
+      if (pl.mt != mt || sacc_of(bits, groups[e]) != sacc) continue;
+      DecProb& d = b.p[b.nprob];
+      const char* Ae = reinterpret_cast<const char*>(A) + (size_t)offsets[e] * K * 2;
+      char* Ce = reinterpret_cast<char*>(C) + (size_t)offsets[e] * N * (cdt == FQ_FP32 ? 4 : 2);
+      void* wse = reinterpret_cast<char*>(ws) + (size_t)e * ws_per_expert;
+      if (!make_dec_prob(d, pl, bits, cdt, Ae, Me, K, N, codes[e], scales[e], groups[e], Ce, wse))
+        return cudaErrorInvalidValue;
+      d.cta_begin = ctas;
+      ctas += d.gx * d.splits * d.ktiles;
+      if (++b.nprob == kMaxBatch) {
+        cudaError_t r = dispatch_dec<kMaxBatch>(adt, bits, mt, sacc, 0, b, ctas, st);
+        if (r != cudaSuccess) return r;
+        b.nprob = 0;
+        ctas = 0;
+      }
+    }
+    if (b.nprob) {
+      cudaError_t r = dispatch_dec<kMaxBatch>(adt, bits, mt, sacc, 0, b, ctas, st);
+      if (r != cudaSuccess) return r;
+    }
   }
-  return adt == FQ_BF16 ? dispatch_bits<__nv_bfloat16>(bits, sacc, pl, tm, prm, st)
-                        : dispatch_bits<__half>(bits, sacc, pl, tm, prm, st);
+  return cudaSuccess;
 }
 
 }  // namespace fq

@@ -26,6 +26,12 @@ cudaError_t run_gemv(const GemvPlan& p, int adt, int cdt, int bits, const void* 
                      int N, const void* codes, const void* scales, int group, void* C, void* ws,
                      cudaStream_t st);
 
+// MoE batch of decode problems (experts with 1 <= M_e <= 16), one launch per kernel class.
+cudaError_t run_gemv_grouped(int adt, int cdt, int bits, const void* A, int K, int N,
+                             const int64_t* offsets, const int32_t* groups, const void* const* codes,
+                             const void* const* scales, void* C, void* ws, size_t ws_per_expert,
+                             const int* experts, int nexp, cudaStream_t st);
+
 // Large-M tensor-core GEMM (tcgen05 + TMEM, kernel A6).
 cudaError_t run_gemm_tc(int adt, int cdt, int bits, const void* A, int M, int K, int N, const void* codes,
                         const void* scales, int group, void* C, cudaStream_t st);

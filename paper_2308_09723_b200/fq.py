@@ -219,6 +219,26 @@ def quantize(W: torch.Tensor, bits: int = 4, group: int | None = 128, scale_dtyp
     return QuantizedWeight(codes, scales, K, N, bits, group)
 
 
+def gemm_grouped(A: torch.Tensor, offsets, experts: list, out: torch.Tensor | None = None,
+                 out_dtype=None, stream=None) -> torch.Tensor:
+    """MoE expert batch: rows offsets[e]:offsets[e+1] of A (sorted by expert) times expert e.
+    All experts share K, N, bits and scale dtype; each has its own group size (adaptive)."""
+    assert A.is_cuda and A.dim() == 2 and A.is_contiguous()
+    E = len(experts)
+    offs = [int(x) for x in offsets]
+    assert len(offs) == E + 1
+    q0 = experts[0]
+    T = A.shape[0]
+    if out is None:
+        out = torch.empty((T, q0.N), dtype=out_dtype or A.dtype, device=A.device)
+    d = q0.desc
+    nb = fq_gemm_grouped_workspace_bytes(T, E, d)
+    ws = workspace(nb, A.device)
+    fq_gemm_grouped(A, T, offs, E, d, [q.group for q in experts], [q.codes.data_ptr() for q in experts],
+                    [q.scales.data_ptr() for q in experts], out, ws, stream)
+    return out
+
+
 def gemm(A: torch.Tensor, qw: QuantizedWeight, out: torch.Tensor | None = None,
          out_dtype=None, stream=None) -> torch.Tensor:
     """C[M, N] = A[M, K] . dequant(qw)^T  (fused, on the GPU)."""
