@@ -3,14 +3,16 @@
 
 Workload (BASELINE.json configs[1]): OPT-175B decode-layer GEMMs, int4 group 128, bf16
 activations: FC1 W[N=49152, K=12288] and FC2 W[N=12288, K=49152].  One STEP = the config's whole
-decode sweep: for each M in {1, 2, 4, 8, 16}, C = A[M,K] . dequant(Wq)^T for FC1 and FC2 (10 fused
-GEMM launches, kernels A4/A5).  metric = effective weight bytes (codes + scales, the bytes the
+decode sweep: for each M in {1, 2, 4, 8, 16}: Y = X[M,K] . dequant(Wq_FC1)^T, Z = Y . dequant(Wq_FC2)^T
+(10 fused GEMM launches, kernels A4/A5).  metric = effective weight bytes (codes + scales, the bytes the
 method must move) per second, whole job.  Weights are 2 x 311 MB (> 126 MB L2), so
 no L2 flush is needed between launches.
 
-N > 1 (torchrun): every rank runs the same sweep on its own weights (independent replicas, the
-paper's per-node replication model P:194, "scaling": "weak"); the decode GEMM itself has no
-data-path collective.  Time = max over ranks of the CUDA-event time of the K timed steps.
+N > 1 (torchrun, configs[4]): the same two matrices are tensor-parallel over the N ranks - FC1
+column-parallel (N sharded), FC2 row-parallel (K sharded) with an NCCL all-reduce of its fp32
+partial output, the exchange the paper names (P:40).  Total work is fixed ("scaling": "strong");
+value = the whole job's effective weight bytes per second.  Time = max over ranks of the
+CUDA-event time of the K timed steps.
 
 --impl reference: the CPU oracle (oracle/) timed on a bounded sample of the same workload.
 """
@@ -189,134 +191,170 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     from paper_2308_09723_b200 import fq
+    from paper_2308_09723_b200.tp import shard_bounds, check_row_group
     from synth import gaussian_torch
 
     peaks = load_peaks()
-    # ---- weights (quantized once, outside the timed region: the quantizer is offline)
-    mats = []
-    for (K, N), mid in ((FC1, 1), (FC2, 2)):
-        W = gaussian_torch((N, K), 0.02, 1000 + mid + 100 * rank, device=dev)
-        qw = fq.quantize(W, BITS, GROUP)
-        del W
-        mats.append(qw)
+    t = world
+    # ---- weights: every rank derives its shard from the same global matrices (seeded), then
+    # quantizes it (offline, outside the timed region).  FC1 column-parallel (N sharded),
+    # FC2 row-parallel (K sharded, group | K/t) -> partial outputs all-reduced over NCCL.
+    c0, c1 = shard_bounds(FC1[1], t, rank)
+    r0, r1 = shard_bounds(FC2[0], t, rank, 32)
+    check_row_group(FC2[0], t, GROUP)
+    W1 = gaussian_torch((FC1[1], FC1[0]), 0.02, 1001, device=dev)
+    q1 = fq.quantize(W1[c0:c1].contiguous(), BITS, GROUP)
+    del W1
+    W2 = gaussian_torch((FC2[1], FC2[0]), 0.02, 1002, device=dev)
+    q2 = fq.quantize(W2[:, r0:r1].contiguous(), BITS, GROUP)
+    del W2
     torch.cuda.synchronize()
-    acts = {}
-    for (K, N), qw in zip((FC1, FC2), mats):
+    xs = {M: gaussian_torch((M, FC1[0]), 1.0, 2000 + M, device=dev) for M in M_SWEEP}
+    ys = {M: torch.empty((M, q1.N), dtype=torch.bfloat16, device=dev) for M in M_SWEEP}
+    zs = {M: torch.empty((M, q2.N), dtype=torch.float32 if t > 1 else torch.bfloat16, device=dev)
+          for M in M_SWEEP}
+    ws = {}
+    for q in (q1, q2):
         for M in M_SWEEP:
-            acts[(K, M)] = gaussian_torch((M, K), 1.0, 2000 + M, device=dev)
-    outs = {(qw.K, M): torch.empty((M, qw.N), dtype=torch.bfloat16, device=dev) for qw in mats for M in M_SWEEP}
-    wss = {}
-    for qw in mats:
-        for M in M_SWEEP:
-            nb = fq.fq_gemm_workspace_bytes(M, qw.desc)
-            wss[(qw.K, M)] = torch.zeros(max(nb, 256), dtype=torch.uint8, device=dev)
-    launches = [(qw, M) for qw in mats for M in M_SWEEP]
-    step_bytes = sum(eff_bytes(qw.K, qw.N, BITS, GROUP) for qw, M in launches)
+            ws[(q.K, M)] = torch.zeros(max(fq.fq_gemm_workspace_bytes(M, q.desc), 256), dtype=torch.uint8,
+                                       device=dev)
+    # algorithmic bytes: full FC1 + full FC2 per M (sum over ranks' shards)
+    step_bytes_total = len(M_SWEEP) * (eff_bytes(*FC1, BITS, GROUP) + eff_bytes(*FC2, BITS, GROUP))
+    step_bytes_rank = len(M_SWEEP) * (q1.nbytes + q2.nbytes)
     stream = torch.cuda.current_stream()
 
-    def launch(qw, M):
-        fq.fq_gemm(acts[(qw.K, M)], M, qw.desc, qw.codes, qw.scales, outs[(qw.K, M)], wss[(qw.K, M)], stream)
+    def gemm1(M):
+        fq.fq_gemm(xs[M], M, q1.desc, q1.codes, q1.scales, ys[M], ws[(q1.K, M)], stream)
+
+    def gemm2(M):
+        fq.fq_gemm(ys[M], M, q2.desc, q2.codes, q2.scales, zs[M], ws[(q2.K, M)], stream)
+
+    def reduce(M):
+        if t > 1:
+            dist.all_reduce(zs[M], op=dist.ReduceOp.SUM)
 
     def step():
-        for qw, M in launches:
-            launch(qw, M)
+        for M in M_SWEEP:
+            gemm1(M)
+            gemm2(M)
+            reduce(M)
 
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
 
-    # ---- timed region (device time, CUDA events on the launching stream)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in launches]
-    per_launch_ms = np.zeros(len(launches))
+    # ---- timed region: CUDA events on the launching stream, barrier + sync on both sides
     with ClockSampler(local) as clk:
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        t0 = torch.cuda.Event(enable_timing=True)
-        t1 = torch.cuda.Event(enable_timing=True)
-        t0.record(stream)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
         for _ in range(args.steps):
             step()
-        t1.record(stream)
+        e1.record(stream)
         torch.cuda.synchronize()
-        total_ms = t0.elapsed_time(t1)
-        # per-launch durations (same launches, bracketed individually) for the roofline
-        for _ in range(max(1, args.steps // 10)):
-            for i, (qw, M) in enumerate(launches):
-                ev[i][0].record(stream)
-                launch(qw, M)
-                ev[i][1].record(stream)
+        total_ms = e0.elapsed_time(e1)
+        if world > 1:
+            dist.barrier()
+        # per-launch durations of the same launches, bracketed individually (roofline + comm share)
+        names = [f"FC1_M{M}" for M in M_SWEEP] + [f"FC2_M{M}" for M in M_SWEEP]
+        per = {n: 0.0 for n in names}
+        comm = 0.0
+        reps = max(1, args.steps // 10)
+        for _ in range(reps):
+            evs = []
+            for M in M_SWEEP:
+                for n, fn in ((f"FC1_M{M}", gemm1), (f"FC2_M{M}", gemm2), (f"AR_M{M}", reduce)):
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(stream)
+                    fn(M)
+                    b.record(stream)
+                    evs.append((n, a, b))
             torch.cuda.synchronize()
-            per_launch_ms += np.array([a.elapsed_time(b) for a, b in ev])
-        per_launch_ms /= max(1, args.steps // 10)
+            for n, a, b in evs:
+                if n.startswith("AR"):
+                    comm += a.elapsed_time(b)
+                else:
+                    per[n] += a.elapsed_time(b)
+        per = {n: v / reps for n, v in per.items()}
+        comm /= reps
         if world > 1:
             dist.barrier()
     clocks = clk.summary()
-    t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+    tt = torch.tensor([total_ms], device=dev, dtype=torch.float64)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    total_ms = float(tt.item())
     ms_per_step = total_ms / args.steps
-    value = world * step_bytes * args.steps / (total_ms / 1e3) / 1e12
+    value = step_bytes_total * args.steps / (total_ms / 1e3) / 1e12
 
-    # ---- e2e through the public API: pinned host A -> device, fused GEMM, C -> pinned host
-    h_acts = {k: v.cpu().pin_memory() for k, v in acts.items()}
-    h_outs = {k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in outs.items()}
-    d_acts = {k: torch.empty_like(v) for k, v in acts.items()}
-    h2d = sum(v.numel() * 2 for v in h_acts.values())
-    d2h = sum(v.numel() * 2 for v in h_outs.values())
+    # ---- e2e through the public API: pinned host x -> device, FC1 -> FC2 (-> all-reduce),
+    # result -> pinned host, every step.
+    h_x = {M: xs[M].cpu().pin_memory() for M in M_SWEEP}
+    h_z = {M: torch.empty(zs[M].shape, dtype=zs[M].dtype).pin_memory() for M in M_SWEEP}
+    d_x = {M: torch.empty_like(xs[M]) for M in M_SWEEP}
+    h2d = sum(v.numel() * v.element_size() for v in h_x.values())
+    d2h = sum(v.numel() * v.element_size() for v in h_z.values())
 
     def e2e_step():
-        for qw, M in launches:
-            k = (qw.K, M)
-            d_acts[k].copy_(h_acts[k], non_blocking=True)
-            fq.gemm(d_acts[k], qw, out=outs[k])
-            h_outs[k].copy_(outs[k], non_blocking=True)
+        for M in M_SWEEP:
+            d_x[M].copy_(h_x[M], non_blocking=True)
+            y = fq.gemm(d_x[M], q1, out=ys[M])
+            fq.gemm(y, q2, out=zs[M])
+            reduce(M)
+            h_z[M].copy_(zs[M], non_blocking=True)
 
     for _ in range(3):
         e2e_step()
     torch.cuda.synchronize()
     e_steps = max(10, args.steps // 3)
-    t0.record(stream)
+    if world > 1:
+        dist.barrier()
+    e0.record(stream)
     for _ in range(e_steps):
         e2e_step()
-    t1.record(stream)
+    e1.record(stream)
     torch.cuda.synchronize()
-    e_ms = t0.elapsed_time(t1)
-    te = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+    te = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = world * step_bytes * e_steps / (float(te.item()) / 1e3) / 1e12
+    e2e_value = step_bytes_total * e_steps / (float(te.item()) / 1e3) / 1e12
 
-    # ---- roofline of the dominant kernel (the A4 decode GEMM; it is every launch of the step)
-    gemv_s = per_launch_ms.sum() / 1e3
-    achieved_gbs = step_bytes / gemv_s / 1e9
+    # ---- roofline of the dominant kernel (A4 decode GEMM = every GEMM launch of the step)
+    gemv_s = sum(per.values()) / 1e3
+    achieved_gbs = step_bytes_rank / gemv_s / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get("decode_bytes_per_step")
+            traffic = json.load(f).get("decode_dram_bytes_per_step")
     roof = {"bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": round(achieved_gbs / peaks["hbm_gbs"], 4), "traffic": traffic,
-            "peak_source": peaks["source"], "kernel": "fq::gemv_kernel (A4/A5)",
-            "per_launch_us": {f"{'FC1' if qw.K == FC1[0] else 'FC2'}_M{M}": round(x * 1e3, 2)
-                              for (qw, M), x in zip(launches, per_launch_ms)}}
+            "peak_source": peaks["source"], "kernel": "fq::decode_kernel (A4/A5)",
+            "algorithmic_bytes_per_step_per_rank": step_bytes_rank,
+            "per_launch_us": {n: round(v * 1e3, 2) for n, v in per.items()},
+            "allreduce_us_per_step": round(comm * 1e3, 2)}
 
     extras = {}
-    if rank == 0 and not args.no_extras:
+    if rank == 0 and world == 1 and not args.no_extras:
+        del xs, ys, zs
+        q1 = q2 = None
+        torch.cuda.empty_cache()
         extras = measure_extras(fq, dev, peaks)
 
     line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": "opt175b_decode_fc1_fc2_int4_g128_sweep_M1-16",
                        "shapes": {"FC1": {"K": FC1[0], "N": FC1[1]}, "FC2": {"K": FC2[0], "N": FC2[1]}},
                        "M": list(M_SWEEP), "bits": BITS, "group": GROUP,
-                       "l2": "inputs larger than L2 (2 x 311 MB packed weights), no flush",
-                       "parallelism": f"replicas x{world}"},
+                       "l2": "inputs larger than L2 (2 x 311 MB packed weights at N=1), no flush",
+                       "parallelism": f"tp{world} (FC1 column-parallel, FC2 row-parallel + NCCL all-reduce)"},
             "clocks": clocks, "e2e": {"value": round(e2e_value, 4), "unit": UNIT,
                                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-            "gpu_launches": len(launches) * args.steps, "roofline": roof}
+            "gpu_launches": 2 * len(M_SWEEP) * args.steps, "roofline": roof}
     if extras:
         line["extras"] = extras
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -331,9 +369,11 @@ def main():
 
 
 def measure_extras(fq, dev, peaks):
-    """Secondary paths reported next to the headline: int8 decode, the large-M GEMM, the quantizer."""
+    """Secondary paths reported next to the headline (rank 0, N=1): int8 decode, the tcgen05
+    prefill GEMM (configs[2]) against torch.matmul bf16, the quantizer and adaptive pass, and the
+    MoE expert batch (configs[3])."""
     import torch
-    from synth import gaussian_torch
+    from synth import gaussian_torch, gaussian_with_outliers_bits
     out = {}
 
     def timeit(fn, reps=20):
@@ -348,33 +388,67 @@ def measure_extras(fq, dev, peaks):
         torch.cuda.synchronize()
         return s.elapsed_time(e) / reps / 1e3
 
-    K, N = FC1
-    W = gaussian_torch((N, K), 0.02, 1001, device=dev)
-    # quantizer (A3), bf16 W -> int4 g128: bytes = read 2B/w + write codes+scales
-    t = timeit(lambda: fq.quantize(W, 4, 128), 5)
-    qb = K * N * 2 + eff_bytes(K, N, 4, 128)
-    out["quantize_int4_g128_FC1"] = {"us": round(t * 1e6, 1), "GB_s": round(qb / t / 1e9, 1),
-                                     "frac_hbm": round(qb / t / 1e9 / peaks["hbm_gbs"], 3)}
-    t = timeit(lambda: fq.adapt_group(W, 500, 16), 3)
-    out["adapt_flags_FC1"] = {"us": round(t * 1e6, 1), "GB_s": round(K * N * 2 / t / 1e9, 1)}
-    q8 = fq.quantize(W, 8, 128)
-    for M in (1, 16):
-        A = gaussian_torch((M, K), 1.0, 7, device=dev)
-        t = timeit(lambda: fq.gemm(A, q8))
-        b = eff_bytes(K, N, 8, 128)
-        out[f"decode_int8_FC1_M{M}"] = {"us": round(t * 1e6, 1), "TB_s": round(b / t / 1e12, 3)}
-    q4 = fq.quantize(W, 4, 128)
-    del W
-    for M in (2048,):
-        A = gaussian_torch((M, K), 1.0, 8, device=dev)
-        t = timeit(lambda: fq.gemm(A, q4), 3)
-        fl = 2.0 * M * K * N
-        out[f"prefill_int4_FC1_M{M}"] = {"ms": round(t * 1e3, 3), "TFLOP_s": round(fl / t / 1e12, 1),
-                                         "frac_bf16_peak": round(fl / t / 1e12 / peaks["bf16_tflops"], 3)}
-        Wb = gaussian_torch((N, K), 0.02, 1001, device=dev)
-        tb = timeit(lambda: torch.matmul(A, Wb.t()), 3)
-        out[f"torch_matmul_bf16_FC1_M{M}"] = {"ms": round(tb * 1e3, 3), "TFLOP_s": round(fl / tb / 1e12, 1)}
-        del Wb
+    for name, (K, N) in (("FC1", FC1), ("FC2", FC2)):
+        W = gaussian_torch((N, K), 0.02, 1001, device=dev)
+        if name == "FC1":
+            # quantizer (A3): read 2 B/weight + write codes/scales; adaptive flags (A1): read 2 B/w
+            tq = timeit(lambda: fq.quantize(W, 4, 128), 5)
+            qb = K * N * 2 + eff_bytes(K, N, 4, 128)
+            out["quantize_int4_g128_FC1"] = {"us": round(tq * 1e6, 1), "GB_s": round(qb / tq / 1e9, 1),
+                                             "frac_hbm": round(qb / tq / 1e9 / peaks["hbm_gbs"], 3)}
+            ta = timeit(lambda: fq.adapt_group(W, 500, 16), 3)
+            out["adapt_flags_FC1"] = {"us": round(ta * 1e6, 1), "GB_s": round(K * N * 2 / ta / 1e9, 1),
+                                      "frac_hbm": round(K * N * 2 / ta / 1e9 / peaks["hbm_gbs"], 3)}
+        q8 = fq.quantize(W, 8, 128)
+        for M in (1, 16):
+            A = gaussian_torch((M, K), 1.0, 7, device=dev)
+            tt = timeit(lambda: fq.gemm(A, q8))
+            b = eff_bytes(K, N, 8, 128)
+            out[f"decode_int8_{name}_M{M}"] = {"us": round(tt * 1e6, 1), "TB_s": round(b / tt / 1e12, 3),
+                                               "frac_hbm": round(b / tt / 1e9 / peaks["hbm_gbs"], 3)}
+        q4 = fq.quantize(W, 4, 128)
+        for M in (2048, 4096, 8192):
+            A = gaussian_torch((M, K), 1.0, 8, device=dev)
+            fl = 2.0 * M * K * N
+            for bits, q in ((4, q4), (8, q8)):
+                tt = timeit(lambda: fq.gemm(A, q), 3)
+                out[f"prefill_int{bits}_{name}_M{M}"] = {
+                    "ms": round(tt * 1e3, 3), "TFLOP_s": round(fl / tt / 1e12, 1),
+                    "frac_bf16_peak": round(fl / tt / 1e12 / peaks["bf16_tflops"], 3)}
+            if M == 2048:
+                tb = timeit(lambda: torch.matmul(A, W.t()), 3)
+                out[f"torch_matmul_bf16_{name}_M{M}"] = {"ms": round(tb * 1e3, 3),
+                                                         "TFLOP_s": round(fl / tb / 1e12, 1)}
+            del A
+        del W, q4, q8
+        torch.cuda.empty_cache()
+
+    # MoE expert batch (configs[3]): 64 experts [16384, 4096], int4 adaptive (alpha 0.5, min 16),
+    # outliers planted in experts e % 4 == 0 -> g_e in {16, 4096}; uniform M_e sweep.
+    E, K, N = 64, 4096, 16384
+    experts = []
+    for e in range(E):
+        W = gaussian_torch((N, K), 0.01 if e % 4 == 0 else 0.02, 7000 + e, device=dev)
+        if e % 4 == 0:
+            W[e % N, (37 * e) % K] = 1.0
+        experts.append(fq.quantize(W, 4, None, alpha_milli=500, min_group=16))
+        del W
+    torch.cuda.empty_cache()
+    gh = {}
+    for q in experts:
+        gh[q.group] = gh.get(q.group, 0) + 1
+    wbytes = sum(q.nbytes for q in experts)
+    moe = {"group_histogram": {str(k): v for k, v in sorted(gh.items())}, "weight_bytes": wbytes}
+    for me in (1, 4, 16, 64, 256):
+        off = [e * me for e in range(E + 1)]
+        A = gaussian_torch((E * me, K), 1.0, 3000 + me, device=dev)
+        tt = timeit(lambda: fq.gemm_grouped(A, off, experts), 5)
+        fl = 2.0 * E * me * K * N
+        moe[f"M_e={me}"] = {"us": round(tt * 1e6, 1), "TB_s": round(wbytes / tt / 1e12, 3),
+                            "frac_hbm": round(wbytes / tt / 1e9 / peaks["hbm_gbs"], 3),
+                            "TFLOP_s": round(fl / tt / 1e12, 1)}
+        del A
+    out["moe_64x16384x4096_int4_adaptive"] = moe
     return out
 
 

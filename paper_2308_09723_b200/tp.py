@@ -1,0 +1,123 @@
+"""Tensor-parallel FineQuant layers (kernel A8 plumbing): one process per GPU, torch.distributed.
+
+The paper serves OPT-175B with tensor parallelism and notes "We must issue an all reduce after
+each attention and FFN block ... it is desirable to use as few GPUs as possible" (§2.1).
+Megatron-style partitioning of a transformer layer:
+
+  * column-parallel (QKV, FC1): output columns n are sharded, A is replicated, no communication.
+    Groups run along K, so a column shard never splits a group; each rank's codes/scales are the
+    column slice of the unsharded ones (bit-exact).
+  * row-parallel (out-proj, FC2): the reduction dim K is sharded (requires group | K/t); each rank
+    produces a partial C over its K slice, then an all-reduce(SUM) over NCCL (NVLink/NVSwitch).
+  * adaptive group size: the level flags of all shards of one matrix are OR-ed (all-reduce MAX)
+    before the host decision, so every shard uses the same g (reading R11: one g per matrix).
+
+The GEMM and quantizer are the libfq kernels; this module only shards, calls and reduces.
+The shard arithmetic is kept in pure functions (`shard_bounds`, `tp_forward`) so the multi-process
+logic can be tested with the gloo backend on CPU by injecting a reference GEMM.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable
+
+import torch
+import torch.distributed as dist
+
+
+def shard_bounds(n: int, world: int, rank: int, align: int = 8) -> tuple[int, int]:
+    """Contiguous, equal shard [lo, hi) of a dimension of size n (n % (world*align) == 0)."""
+    if n % (world * align):
+        raise ValueError(f"dimension {n} does not split into {world} shards aligned to {align}")
+    sz = n // world
+    return rank * sz, (rank + 1) * sz
+
+
+def check_row_group(K: int, world: int, group: int) -> None:
+    """Row-parallel shards need whole groups on every rank (group | K/world)."""
+    if (K // world) % group:
+        raise ValueError(f"row-parallel shard K/t={K // world} is not a multiple of group {group}")
+
+
+@dataclass
+class ShardSpec:
+    kind: str      # "col" or "row"
+    K: int         # full reduction dim
+    N: int         # full output dim
+    world: int
+    rank: int
+
+    @property
+    def bounds(self) -> tuple[int, int]:
+        return shard_bounds(self.N if self.kind == "col" else self.K, self.world, self.rank,
+                            8 if self.kind == "col" else 32)
+
+
+def tp_forward(x: torch.Tensor, shards: list, gemm_fn: Callable, allreduce_fn: Callable | None,
+               kinds: list[str], world: int, rank: int) -> torch.Tensor:
+    """Run a chain of TP linears: column layers produce a column shard of their output; a row layer
+    consumes the column shard produced before it and all-reduces its partial output.
+
+    gemm_fn(x, shard) -> x @ W_shard^T ; allreduce_fn(t) sums t over the TP group in place."""
+    h = x
+    for shard, kind in zip(shards, kinds):
+        if kind == "col":
+            h = gemm_fn(h, shard)
+        elif kind == "row":
+            h = gemm_fn(h, shard)
+            if allreduce_fn is not None and world > 1:
+                allreduce_fn(h)
+        else:
+            raise ValueError(kind)
+    return h
+
+
+class TPLinearFQ:
+    """A quantized linear shard on this rank (canonical libfq layout)."""
+
+    def __init__(self, W_shard: torch.Tensor, spec: ShardSpec, bits: int = 4, group: int | None = 128,
+                 alpha_milli: int = 500, min_group: int = 16, process_group=None):
+        from . import fq
+        self.spec = spec
+        if group is None:  # adaptive: agree on g across the shards of this matrix
+            group = fq.adapt_group(W_shard, alpha_milli, min_group,
+                                   process_group=process_group if spec.world > 1 else None)
+        if spec.kind == "row":
+            check_row_group(spec.K, spec.world, group)
+        self.qw = fq.quantize(W_shard.contiguous(), bits, group)
+
+    def __call__(self, x: torch.Tensor, out_dtype=None) -> torch.Tensor:
+        from . import fq
+        return fq.gemm(x.contiguous(), self.qw, out_dtype=out_dtype)
+
+
+class TPOptLayer:
+    """The GEMM chain of one OPT decoder layer under TP (configs[4]):
+        QKV (col) -> [attention stand-in: the first h/t columns of this rank's QKV shard]
+        -> out-proj (row) -> all-reduce -> FC1 (col) -> FC2 (row) -> all-reduce.
+    Attention, layer norms, residuals and the activation function are outside the FineQuant hot
+    path and are not modelled; the communication pattern (two all-reduces per
+    layer) and every weight byte are."""
+
+    def __init__(self, qkv: TPLinearFQ, out: TPLinearFQ, fc1: TPLinearFQ, fc2: TPLinearFQ,
+                 process_group=None):
+        self.qkv, self.out, self.fc1, self.fc2 = qkv, out, fc1, fc2
+        self.pg = process_group
+        self.world = qkv.spec.world
+
+    def _row(self, lin: TPLinearFQ, h: torch.Tensor, dtype) -> torch.Tensor:
+        part = lin(h, out_dtype=torch.float32)  # fp32 partials, summed across ranks
+        if self.world > 1:
+            dist.all_reduce(part, op=dist.ReduceOp.SUM, group=self.pg)
+        return part.to(dtype)
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        hs = self.out.qw.K  # h / t: the K shard of the out-projection
+        q = self.qkv(x)
+        y = self._row(self.out, q[:, :hs].contiguous(), x.dtype)
+        f = self.fc1(y)
+        return self._row(self.fc2, f, x.dtype)
+
+    @property
+    def weight_bytes(self) -> int:
+        return sum(l.qw.nbytes for l in (self.qkv, self.out, self.fc1, self.fc2))
