@@ -282,6 +282,14 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode_kernel(const __grid_con
     constexpr int NPIECE = MT * 8 * (KS / 8);
     static_assert(NPIECE % 32 == 0, "pieces per stage must be a multiple of the warp size");
     constexpr int NPW = NPIECE / 32;
+    // tokens >= M stay zero: written once here, skipped in the loop (M = 1 stages 1/8 of the data)
+    const int mloc = min(M - tok0, MT * 8);
+    for (int s0 = 0; s0 < kDecStages; ++s0) {
+      const uint32_t stu = smem_u32(sbase + s0 * STAGE_BYTES);
+      for (int o = mloc * TOK + lane * 16; o < ACT_BYTES; o += 32 * 16) sts128(stu + kStageW + o, make_uint4(0, 0, 0, 0));
+      if (lane < MT * 8 * CHUNKS) reinterpret_cast<float*>(sbase + s0 * STAGE_BYTES + kStageW + ACT_BYTES)[lane] = 0.f;
+    }
+    __syncwarp();
     int s = 0;
     uint32_t ph = 0;
     for (int i = 0; i < nst; ++i) {
@@ -290,9 +298,11 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode_kernel(const __grid_con
       const uint32_t stu = smem_u32(st);
       uint4 va[NPW];
 #pragma unroll
-      for (int j = 0; j < NPW; ++j) va[j] = lds128(stu + RAW_OFS + (lane + 32 * j) * 16);
+      for (int j = 0; j < NPW; ++j)
+        if ((32 * j) / (KS / 8) < mloc) va[j] = lds128(stu + RAW_OFS + (lane + 32 * j) * 16);
 #pragma unroll
       for (int j = 0; j < NPW; ++j) {
+        if ((32 * j) / (KS / 8) >= mloc) continue;  // warp-uniform: whole piece group is zero tokens
         const int pc = lane + 32 * j;
         const int tl = pc / (KS / 8);          // local token
         const int kl = (pc % (KS / 8)) * 8;    // local k of this 8-element piece
