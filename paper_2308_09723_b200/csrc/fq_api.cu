@@ -136,6 +136,9 @@ fq_status fq_quantize(const void* W, int32_t wdt, const fq_wdesc* d, void* codes
 
 size_t fq_gemm_workspace_bytes(int64_t M, const fq_wdesc* d) {
   if (check_wdesc(d) != FQ_OK || M <= 0) return 0;
+  if (use_tc_path(M)) return 256;
+  if (decode_tc_supported(d->bits, d->group, (int)M))
+    return dtc_workspace_bytes((int)M, (int)d->K, (int)d->N, d->bits, num_sms());
   const GemvPlan p = plan_gemv((int)M, (int)d->K, (int)d->N, d->bits, d->group, num_sms());
   return gemv_workspace_bytes(p, (int)M, (int)d->N);
 }
@@ -152,6 +155,12 @@ fq_status fq_gemm(const void* A, int32_t adt, int64_t M, const fq_wdesc* d, cons
   if (use_tc_path(M))
     return from_cuda(run_gemm_tc(adt, cdt, d->bits, A, (int)M, (int)d->K, (int)d->N, codes, scales,
                                  d->group, C, as_stream(stream)));
+  if (decode_tc_supported(d->bits, d->group, (int)M)) {
+    const size_t need = dtc_workspace_bytes((int)M, (int)d->K, (int)d->N, d->bits, num_sms());
+    if (need > 65536 && (!ws || ws_bytes < need)) return FQ_ERR_WORKSPACE;
+    return from_cuda(run_decode_tc(adt, cdt, d->bits, A, (int)M, (int)d->K, (int)d->N, codes, scales,
+                                   d->group, C, ws, as_stream(stream)));
+  }
   const GemvPlan p = plan_gemv((int)M, (int)d->K, (int)d->N, d->bits, d->group, num_sms());
   if (p.splits > 1 && (!ws || ws_bytes < gemv_workspace_bytes(p, (int)M, (int)d->N)))
     return FQ_ERR_WORKSPACE;
@@ -199,9 +208,21 @@ fq_status fq_gemm_grouped(const void* A, int32_t adt, int64_t T, const int64_t* 
       if (r != cudaSuccess) return FQ_ERR_CUDA;
     }
   }
-  if (!small.empty())
+  // small experts: tcgen05 decode kernel where the group allows, mma.sync kernel otherwise
+  std::vector<int> small_tc, small_mma;
+  for (int e : small)
+    (decode_tc_supported(d->bits, groups_host[e], (int)(offsets_host[e + 1] - offsets_host[e])) ? small_tc
+                                                                                                 : small_mma)
+        .push_back(e);
+  if (!small_tc.empty()) {
+    cudaError_t r = run_decode_tc_grouped(adt, cdt, d->bits, A, (int)d->K, (int)d->N, offsets_host, groups_host,
+                                          codes_host, scales_host, C, small_tc.data(), (int)small_tc.size(), st);
+    if (r != cudaSuccess) return FQ_ERR_CUDA;
+  }
+  if (!small_mma.empty())
     return from_cuda(run_gemv_grouped(adt, cdt, d->bits, A, (int)d->K, (int)d->N, offsets_host, groups_host,
-                                      codes_host, scales_host, C, ws, 0, small.data(), (int)small.size(), st));
+                                      codes_host, scales_host, C, ws, 0, small_mma.data(), (int)small_mma.size(),
+                                      st));
   return FQ_OK;
 }
 

@@ -32,6 +32,15 @@ cudaError_t run_gemv_grouped(int adt, int cdt, int bits, const void* A, int K, i
                              const void* const* scales, void* C, void* ws, size_t ws_per_expert,
                              const int* experts, int nexp, cudaStream_t st);
 
+// Decode GEMM on tcgen05 (A4, M <= 16, group % 128 (int4) / 64 (int8) == 0).
+bool decode_tc_supported(int bits, int group, int M);
+size_t dtc_workspace_bytes(int M, int K, int N, int bits, int nsm);
+cudaError_t run_decode_tc(int adt, int cdt, int bits, const void* A, int M, int K, int N, const void* codes,
+                          const void* scales, int group, void* C, void* ws, cudaStream_t st);
+cudaError_t run_decode_tc_grouped(int adt, int cdt, int bits, const void* A, int K, int N, const int64_t* offsets,
+                                  const int32_t* groups, const void* const* codes, const void* const* scales,
+                                  void* C, const int* experts, int nexp, cudaStream_t st);
+
 // Large-M tensor-core GEMM (tcgen05 + TMEM, kernel A6).
 cudaError_t run_gemm_tc(int adt, int cdt, int bits, const void* A, int M, int K, int N, const void* codes,
                         const void* scales, int group, void* C, cudaStream_t st);

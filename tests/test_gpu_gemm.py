@@ -222,3 +222,24 @@ def test_opt175b_prefill_sampled(fq, shape, bits):
     r = O.quantize(Wc, bits, 128, O.BF16)
     Cr, D = O.gemm(A[torch.from_numpy(rows).cuda()].float().cpu().double().numpy(), r.q, r.s, 128)
     assert O.rel_err(torch_to_f64(C)[np.ix_(rows, cols)], Cr, D) <= TOL
+
+
+@pytest.mark.parametrize("impl", ["tcgen05", "mma_sync"])
+@pytest.mark.parametrize("M,K,N,bits,group,adt,splits", [
+    (1, 256, 256, 4, 128, "bf16", None),
+    (3, 1536, 776, 4, 128, "bf16", None),    # ragged N tail
+    (16, 4096, 512, 4, 256, "bf16", 3),      # split-K, deterministic fixup
+    (9, 2048, 640, 8, 64, "bf16", None),
+    (5, 2048, 384, 8, 128, "fp16", 2),
+    (12, 1024, 512, 4, 1024, "fp16", None),  # per-column
+])
+def test_decode_kernels(fq, env, impl, M, K, N, bits, group, adt, splits):
+    """Both decode kernels (tcgen05 A4 and the mma.sync A4) against the oracle."""
+    env("FQ_DECODE_TC", "1" if impl == "tcgen05" else "0")
+    if splits:
+        env("FQ_GEMV_SPLITS", splits)
+    Wb, Ab = make_case(M, K, N, bits, group, adt, seed=M * 7 + K, outliers=1)
+    for _ in range(2):
+        _, C = run_case(fq, Wb, Ab, bits, group, adt)
+        Cr, D = oracle_ref(Wb, Ab, bits, group, adt)
+        assert O.rel_err(torch_to_f64(C), Cr, D) <= TOL
