@@ -52,7 +52,9 @@ struct G {
   static constexpr int SC_BYTES = ROWS * 2;
   static constexpr int SA_OFS = SC_OFS + SC_BYTES;
   static constexpr int SA_BYTES = NT * 4;
-  static constexpr int STAGE = ((SA_OFS + SA_BYTES + 1023) / 1024) * 1024;
+  static constexpr int SF_OFS = SA_OFS + SA_BYTES;  // scales as fp32 (written by the stager)
+  static constexpr int SF_BYTES = ROWS * 4;
+  static constexpr int STAGE = ((SF_OFS + SF_BYTES + 1023) / 1024) * 1024;
   static constexpr int SMEM = SSTAGES * STAGE + 1024;
   static constexpr int A_COLS = KS / 2;            // TMEM columns per A stage
   static constexpr int ACC_COL = ASTAGES * A_COLS; // accumulator slices after the A ring
@@ -109,8 +111,9 @@ template <> struct Off<__nv_bfloat16, 4> { static constexpr float v = 136.f; };
 template <> struct Off<__half, 4> { static constexpr float v = 1032.f; };
 template <> struct Off<__half, 8> { static constexpr float v = 1152.f; };
 
-template <typename T, int BITS, int MAXP>
+template <typename T, int BITS, int MAXP, int NTF>
 __global__ void __launch_bounds__(kThreads, 2) decode_tc_kernel(const __grid_constant__ DtcBatch<MAXP> batch) {
+  // NTF: tokens folded per chunk (compile-time bucket >= M; rows beyond M are zero)
   using Gm = G<BITS>;
   constexpr int KS = Gm::KS;
   constexpr float OFF = Off<T, BITS>::v;
@@ -253,6 +256,18 @@ __global__ void __launch_bounds__(kThreads, 2) decode_tc_kernel(const __grid_con
         const int atom = kl >> 6, chunk = (kl & 63) >> 3;
         sts128(st + Gm::B_OFS + atom * 2048 + tok * 128 + ((chunk ^ (tok & 7)) << 4), v);
       }
+      {  // the stage's 128 scales -> fp32 for the fold warps
+        const uint2 sv = lds64(st + Gm::SC_OFS + lane * 8);
+        const uint32_t h[4] = {sv.x & 0xFFFFu, sv.x >> 16, sv.y & 0xFFFFu, sv.y >> 16};
+        float f[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const unsigned short hv = (unsigned short)h[e];
+          f[e] = Dt<T>::to_f(*reinterpret_cast<const T*>(&hv));
+        }
+        sts128(st + Gm::SF_OFS + lane * 16, make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]),
+                                                       __float_as_uint(f[2]), __float_as_uint(f[3])));
+      }
       fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core
       mbar_arrive(&bready[s]);
       if (++s == SSTAGES) { s = 0; ph ^= 1; }
@@ -295,9 +310,9 @@ __global__ void __launch_bounds__(kThreads, 2) decode_tc_kernel(const __grid_con
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-    float acc[NT];
+    float acc[NTF];
 #pragma unroll
-    for (int t = 0; t < NT; ++t) acc[t] = 0.f;
+    for (int t = 0; t < NTF; ++t) acc[t] = 0.f;
     int s = 0, c = 0;
     uint32_t ph = 0, cph = 0;
     for (int i = 0; i < nst; ++i) {
@@ -308,19 +323,14 @@ __global__ void __launch_bounds__(kThreads, 2) decode_tc_kernel(const __grid_con
       tmem_wait_ld();
       fence_before();
       mbar_arrive(&accfree[c]);
-      // direct acquires of the producers of the scale row (TMA) and token sums (stager)
-      mbar_wait(&full_bar[s], ph);
-      mbar_wait(&bready[s], ph);
-      const uint8_t* st = sbase + s * Gm::STAGE;
-      const float sc = Dt<T>::to_f(reinterpret_cast<const T*>(st + Gm::SC_OFS)[row]);
-      const float* sa = reinterpret_cast<const float*>(st + Gm::SA_OFS);
+      mbar_wait(&bready[s], ph);  // direct acquire of the stager's fp32 scales and token sums
+      const uint32_t st = sb + s * Gm::STAGE;
+      const float sc = lds_f32(st + Gm::SF_OFS + row * 4);
 #pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        if (t < mloc) {
-          float part = __uint_as_float(v[t]);
-          if (OFF != 0.f) part = fmaf(-OFF, sa[t], part);
-          acc[t] = fmaf(sc, part, acc[t]);
-        }
+      for (int t = 0; t < NTF; ++t) {
+        float part = __uint_as_float(v[t]);
+        if (OFF != 0.f) part = fmaf(-OFF, lds_f32(st + Gm::SA_OFS + t * 4), part);
+        acc[t] = fmaf(sc, part, acc[t]);
       }
       mbar_arrive(&sfree[s]);  // scale row + token sums consumed: the stage may be refilled
       if (++s == SSTAGES) { s = 0; ph ^= 1; }
@@ -336,14 +346,14 @@ __global__ void __launch_bounds__(kThreads, 2) decode_tc_kernel(const __grid_con
     if (p.splits == 1) {
       if (n < N) {
 #pragma unroll
-        for (int t = 0; t < NT; ++t)
+        for (int t = 0; t < NTF; ++t)
           if (t < mloc) store_out(t, acc[t]);
       }
     } else {
       float* part_out = p.ws + (size_t)by * M * N;
       if (n < N) {
 #pragma unroll
-        for (int t = 0; t < NT; ++t)
+        for (int t = 0; t < NTF; ++t)
           if (t < mloc) __stcg(part_out + (size_t)t * N + n, acc[t]);
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -358,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, 2) decode_tc_kernel(const __grid_con
         __threadfence();
         if (n < N) {
 #pragma unroll
-          for (int t = 0; t < NT; ++t) {
+          for (int t = 0; t < NTF; ++t) {
             if (t < mloc) {
               float val = 0.f;
               for (int sp = 0; sp < p.splits; ++sp) val += __ldcg(p.ws + ((size_t)sp * M + t) * N + n);
@@ -386,10 +396,10 @@ bool decode_tc_supported(int bits, int group, int M) {
   return M >= 1 && M <= dtc::NT && group % (bits == 4 ? 128 : 64) == 0;
 }
 
-template <typename T, int BITS, int MAXP>
+template <typename T, int BITS, int MAXP, int NTF>
 static cudaError_t launch_dtc(const dtc::DtcBatch<MAXP>& b, int ctas, cudaStream_t st) {
   constexpr int smem = dtc::G<BITS>::SMEM;
-  auto kern = dtc::decode_tc_kernel<T, BITS, MAXP>;
+  auto kern = dtc::decode_tc_kernel<T, BITS, MAXP, NTF>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -400,11 +410,19 @@ static cudaError_t launch_dtc(const dtc::DtcBatch<MAXP>& b, int ctas, cudaStream
   return cudaGetLastError();
 }
 
-template <int MAXP>
-static cudaError_t dispatch_dtc(int adt, int bits, const dtc::DtcBatch<MAXP>& b, int ctas, cudaStream_t st) {
+template <int MAXP, int NTF>
+static cudaError_t dispatch_dtc_t(int adt, int bits, const dtc::DtcBatch<MAXP>& b, int ctas, cudaStream_t st) {
   if (adt == FQ_BF16)
-    return bits == 4 ? launch_dtc<__nv_bfloat16, 4, MAXP>(b, ctas, st) : launch_dtc<__nv_bfloat16, 8, MAXP>(b, ctas, st);
-  return bits == 4 ? launch_dtc<__half, 4, MAXP>(b, ctas, st) : launch_dtc<__half, 8, MAXP>(b, ctas, st);
+    return bits == 4 ? launch_dtc<__nv_bfloat16, 4, MAXP, NTF>(b, ctas, st)
+                     : launch_dtc<__nv_bfloat16, 8, MAXP, NTF>(b, ctas, st);
+  return bits == 4 ? launch_dtc<__half, 4, MAXP, NTF>(b, ctas, st) : launch_dtc<__half, 8, MAXP, NTF>(b, ctas, st);
+}
+template <int MAXP>
+static cudaError_t dispatch_dtc(int adt, int bits, const dtc::DtcBatch<MAXP>& b, int ctas, cudaStream_t st,
+                                int maxm) {
+  if (maxm <= 1) return dispatch_dtc_t<MAXP, 1>(adt, bits, b, ctas, st);
+  if (maxm <= 4) return dispatch_dtc_t<MAXP, 4>(adt, bits, b, ctas, st);
+  return dispatch_dtc_t<MAXP, 16>(adt, bits, b, ctas, st);
 }
 
 static bool make_dtc_prob(dtc::DtcProb& d, int splits, int klen, int bits, int cdt, const void* A, int M, int K,
@@ -462,7 +480,7 @@ cudaError_t run_decode_tc(int adt, int cdt, int bits, const void* A, int M, int 
     return cudaErrorInvalidValue;
   b.p[0].cta_begin = 0;
   b.nprob = 1;
-  return dispatch_dtc<1>(adt, bits, b, b.p[0].gx * splits, st);
+  return dispatch_dtc<1>(adt, bits, b, b.p[0].gx * splits, st, M);
 }
 
 // MoE batch on the tcgen05 decode kernel: experts (1 <= M_e <= 16, group % KS == 0), one launch per
@@ -473,7 +491,7 @@ cudaError_t run_decode_tc_grouped(int adt, int cdt, int bits, const void* A, int
   constexpr int MAXP = 40;
   static_assert(sizeof(dtc::DtcBatch<MAXP>) < 32000, "kernel parameter block limit");
   dtc::DtcBatch<MAXP> b{};
-  int ctas = 0;
+  int ctas = 0, maxm = 0;
   const int ks = 64 * 8 / bits;
   for (int ii = 0; ii < nexp; ++ii) {
     const int e = experts[ii];
@@ -486,14 +504,16 @@ cudaError_t run_decode_tc_grouped(int adt, int cdt, int bits, const void* A, int
       return cudaErrorInvalidValue;
     d.cta_begin = ctas;
     ctas += d.gx;
+    maxm = std::max(maxm, Me);
     if (++b.nprob == MAXP) {
-      cudaError_t r = dispatch_dtc<MAXP>(adt, bits, b, ctas, st);
+      cudaError_t r = dispatch_dtc<MAXP>(adt, bits, b, ctas, st, maxm);
       if (r != cudaSuccess) return r;
       b.nprob = 0;
       ctas = 0;
+      maxm = 0;
     }
   }
-  if (b.nprob) return dispatch_dtc<MAXP>(adt, bits, b, ctas, st);
+  if (b.nprob) return dispatch_dtc<MAXP>(adt, bits, b, ctas, st, maxm);
   return cudaSuccess;
 }
 
