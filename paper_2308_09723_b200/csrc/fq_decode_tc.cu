@@ -33,11 +33,15 @@ using namespace tc5;
 
 constexpr int ROWS = 128;
 constexpr int NT = 16;
-constexpr int SSTAGES = 6;
-constexpr int ASTAGES = 3;
-constexpr int ACC = 4;
+#ifndef FQ_DTC_CTAS
+#define FQ_DTC_CTAS 1
+#endif
+constexpr int CTAS_PER_SM = FQ_DTC_CTAS;
+constexpr int SSTAGES = CTAS_PER_SM == 1 ? 12 : 6;
+constexpr int ASTAGES = CTAS_PER_SM == 1 ? 6 : 3;
+constexpr int ACC = CTAS_PER_SM == 1 ? 8 : 4;
 constexpr int kThreads = 32 * 11;
-constexpr int kTmemCols = 256;
+constexpr int kTmemCols = CTAS_PER_SM == 1 ? 512 : 256;
 
 template <int BITS>
 struct G {
@@ -112,7 +116,7 @@ template <> struct Off<__half, 4> { static constexpr float v = 1032.f; };
 template <> struct Off<__half, 8> { static constexpr float v = 1152.f; };
 
 template <typename T, int BITS, int MAXP, int NTF>
-__global__ void __launch_bounds__(kThreads, 2) decode_tc_kernel(const __grid_constant__ DtcBatch<MAXP> batch) {
+__global__ void __launch_bounds__(kThreads, CTAS_PER_SM) decode_tc_kernel(const __grid_constant__ DtcBatch<MAXP> batch) {
   // NTF: tokens folded per chunk (compile-time bucket >= M; rows beyond M are zero)
   using Gm = G<BITS>;
   constexpr int KS = Gm::KS;
@@ -448,7 +452,7 @@ void plan_dtc(int M, int K, int N, int bits, int nsm, int* splits, int* klen) {
   const int ks = 64 * 8 / bits;
   const int gx = (N + dtc::ROWS - 1) / dtc::ROWS;
   const int nchunks = (K + ks - 1) / ks;
-  const int slots = 2 * nsm;
+  const int slots = dtc::CTAS_PER_SM * nsm;
   int best_s = 1;
   double best = -1e30;
   for (int s = 1; s <= std::min(nchunks, 32); ++s) {
