@@ -34,7 +34,7 @@ using namespace tc5;
 constexpr int ROWS = 128;
 constexpr int NT = 16;
 #ifndef FQ_DTC_CTAS
-#define FQ_DTC_CTAS 1
+#define FQ_DTC_CTAS 2
 #endif
 constexpr int CTAS_PER_SM = FQ_DTC_CTAS;
 constexpr int SSTAGES = CTAS_PER_SM == 1 ? 12 : 6;
@@ -71,6 +71,7 @@ struct DtcProb {
   int* counters;
   int M, K, N, group, klen, cdt;
   int gx, splits, cta_begin;
+  int dbg_nofence;  // diagnostics only (FQ_DTC_NOFENCE): skip the proxy fence
 };
 template <int MAXP>
 struct DtcBatch {
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(kThreads, CTAS_PER_SM) decode_tc_kernel(const 
         sts128(st + Gm::SF_OFS + lane * 16, make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]),
                                                        __float_as_uint(f[2]), __float_as_uint(f[3])));
       }
-      fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core
+      if (!p.dbg_nofence) fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core
       mbar_arrive(&bready[s]);
       if (++s == SSTAGES) { s = 0; ph ^= 1; }
     }
@@ -444,6 +445,8 @@ static bool make_dtc_prob(dtc::DtcProb& d, int splits, int klen, int bits, int c
   d.gx = (N + dtc::ROWS - 1) / dtc::ROWS;
   d.counters = reinterpret_cast<int*>(ws);
   d.ws = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + 65536);
+  const char* nf = std::getenv("FQ_DTC_NOFENCE");
+  d.dbg_nofence = nf && nf[0] == '1';
   return true;
 }
 
