@@ -148,15 +148,15 @@ __global__ void __launch_bounds__(kThreads, CTAS_PER_SM) decode_tc_kernel(const 
     for (int s = 0; s < SSTAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&bready[s], 32);
-      mbar_init(&sfree[s], 128);
+      mbar_init(&sfree[s], 4);   // one arrival per fold warp
     }
     for (int a = 0; a < ASTAGES; ++a) {
-      mbar_init(&aready[a], 128);
+      mbar_init(&aready[a], 4);  // one arrival per dequant warp
       mbar_init(&afree[a], 1);
     }
     for (int c = 0; c < ACC; ++c) {
       mbar_init(&accfull[c], 1);
-      mbar_init(&accfree[c], 128);
+      mbar_init(&accfree[c], 4);
     }
     fence_mbar_init();
   }
@@ -306,7 +306,8 @@ __global__ void __launch_bounds__(kThreads, CTAS_PER_SM) decode_tc_kernel(const 
       }
       tmem_wait_st();
       fence_before();
-      mbar_arrive(&aready[a]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&aready[a]);
       if (++s == SSTAGES) { s = 0; ph ^= 1; }
       if (++a == ASTAGES) { a = 0; aph ^= 1; }
     }
@@ -327,7 +328,8 @@ __global__ void __launch_bounds__(kThreads, CTAS_PER_SM) decode_tc_kernel(const 
       tmem_ld16(tmem + lane_base + Gm::ACC_COL + c * NT, v);
       tmem_wait_ld();
       fence_before();
-      mbar_arrive(&accfree[c]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&accfree[c]);
       mbar_wait(&bready[s], ph);  // direct acquire of the stager's fp32 scales and token sums
       const uint32_t st = sb + s * Gm::STAGE;
       const float sc = lds_f32(st + Gm::SF_OFS + row * 4);
@@ -337,7 +339,8 @@ __global__ void __launch_bounds__(kThreads, CTAS_PER_SM) decode_tc_kernel(const 
         if (OFF != 0.f) part = fmaf(-OFF, lds_f32(st + Gm::SA_OFS + t * 4), part);
         acc[t] = fmaf(sc, part, acc[t]);
       }
-      mbar_arrive(&sfree[s]);  // scale row + token sums consumed: the stage may be refilled
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sfree[s]);  // scales + token sums consumed: refill allowed
       if (++s == SSTAGES) { s = 0; ph ^= 1; }
       if (++c == ACC) { c = 0; cph ^= 1; }
     }

@@ -112,11 +112,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&afull_bar[s], 32 * kDqWarps);
+      mbar_init(&afull_bar[s], kDqWarps);  // one arrival per dequant warp
       mbar_init(&empty_bar[s], 1);
     }
     mbar_init(&acc_full, 1);
-    mbar_init(&acc_empty, 32 * kDqWarps);
+    mbar_init(&acc_empty, kDqWarps);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(&tmem_base_sh, kTmemCols);
@@ -240,7 +240,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_st16(tmem + lane_base + kACol + s * 32 + half * 16, out);
         tmem_wait_st();
         fence_before();
-        mbar_arrive(&afull_bar[s]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&afull_bar[s]);
         if (++s == STAGES) { s = 0; ph ^= 1; }
       }
       // ---- epilogue: accumulator row `row` (weight n), tokens [half*128, half*128+128)
@@ -266,7 +267,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       fence_before();
-      mbar_arrive(&acc_empty);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty);
     }
   }
   __syncthreads();

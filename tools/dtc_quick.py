@@ -18,3 +18,8 @@ for M in (1, 16):
         for k in ("FQ_DECODE_TC", "FQ_DTC_NOFENCE"): os.environ.pop(k, None)
         os.environ.update(env)
         print(M, env, f"{bench(lambda: fq.gemm(A, q, out=C)):.1f} us", flush=True)
+os.environ["FQ_GEMM_PATH"] = "tc"
+for M in (2048,):
+    A = gaussian_torch((M, K), 1.0, 2); C = fq.gemm(A, q)
+    t = bench(lambda: fq.gemm(A, q, out=C), 5)
+    print("prefill", M, f"{t:.1f} us {2*M*K*N/t/1e6:.1f} TFLOP/s", flush=True)
