@@ -72,6 +72,7 @@ struct DtcProb {
   int M, K, N, group, klen, cdt;
   int gx, splits, cta_begin;
   int dbg_nofence;  // diagnostics only (FQ_DTC_NOFENCE): skip the proxy fence
+  int dbg;          // diagnostics only (FQ_DTC_DBG bits): 1 dequant, 2 fold, 4 stager, 8 mma skipped
 };
 template <int MAXP>
 struct DtcBatch {
@@ -212,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, CTAS_PER_SM) decode_tc_kernel(const 
         fence_after();
         const uint64_t bdesc = sw128_desc(sb + s * Gm::STAGE + Gm::B_OFS);
 #pragma unroll
-        for (int kk = 0; kk < KS / 16; ++kk)
+        for (int kk = 0; kk < ((p.dbg & 8) ? 1 : KS / 16); ++kk)
           mma_ts(tmem + Gm::ACC_COL + c * NT, tmem + a * Gm::A_COLS + kk * 8,
                  bdesc + (uint64_t)((((kk >> 2) * 2048) + (kk & 3) * 32) >> 4), idesc, kk != 0);
         mma_commit(&afree[a]);
@@ -234,7 +235,7 @@ __global__ void __launch_bounds__(kThreads, CTAS_PER_SM) decode_tc_kernel(const 
       mbar_wait(&full_bar[s], ph);
       const uint32_t st = sb + s * Gm::STAGE;
 #pragma unroll
-      for (int j = 0; j < NPW; ++j) {
+      for (int j = 0; j < ((p.dbg & 4) ? 0 : NPW); ++j) {
         if ((32 * j) / PPT >= mloc) continue;      // warp-uniform: all-zero token group
         const int pc = lane + 32 * j;
         const int tok = pc / PPT, kl = (pc % PPT) * 8;
@@ -301,7 +302,8 @@ __global__ void __launch_bounds__(kThreads, CTAS_PER_SM) decode_tc_kernel(const 
         uint32_t q[32];
 #pragma unroll
         for (int w = 0; w < 32 / PAIRS_PER_WORD; ++w)
-          unpack_word<T, BITS>(words[half * (32 / PAIRS_PER_WORD) + w], &q[w * PAIRS_PER_WORD]);
+          if (p.dbg & 1) { for (int u = 0; u < PAIRS_PER_WORD; ++u) q[w * PAIRS_PER_WORD + u] = words[half * (32 / PAIRS_PER_WORD) + w]; }
+          else unpack_word<T, BITS>(words[half * (32 / PAIRS_PER_WORD) + w], &q[w * PAIRS_PER_WORD]);
         tmem_st32(tmem + lane_base + a * Gm::A_COLS + half * 32, q);
       }
       tmem_wait_st();
@@ -333,6 +335,8 @@ __global__ void __launch_bounds__(kThreads, CTAS_PER_SM) decode_tc_kernel(const 
       mbar_wait(&bready[s], ph);  // direct acquire of the stager's fp32 scales and token sums
       const uint32_t st = sb + s * Gm::STAGE;
       const float sc = lds_f32(st + Gm::SF_OFS + row * 4);
+#pragma unroll
+      if (!(p.dbg & 2))
 #pragma unroll
       for (int t = 0; t < NTF; ++t) {
         float part = __uint_as_float(v[t]);
@@ -450,6 +454,8 @@ static bool make_dtc_prob(dtc::DtcProb& d, int splits, int klen, int bits, int c
   d.ws = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + 65536);
   const char* nf = std::getenv("FQ_DTC_NOFENCE");
   d.dbg_nofence = nf && nf[0] == '1';
+  const char* db = std::getenv("FQ_DTC_DBG");
+  d.dbg = db ? std::atoi(db) : 0;
   return true;
 }
 
