@@ -403,8 +403,11 @@ __global__ void __launch_bounds__(kThreads, CTAS_PER_SM) decode_tc_kernel(const 
 
 // ------------------------------------------------------------------------------------- host side
 bool decode_tc_supported(int bits, int group, int M) {
+  // Opt-in (FQ_DECODE_TC=1): correct, but its 8 KB-stage pipeline skeleton streams at only
+  // ~3.6 TB/s even with all compute removed (round-1 diagnostics, profiles/r01), so the mma.sync
+  // decode kernel (16 KB stages, 5.7 TB/s skeleton) remains the default A4.
   const char* e = std::getenv("FQ_DECODE_TC");
-  if (e && e[0] == '0') return false;
+  if (!e || e[0] != '1') return false;
   return M >= 1 && M <= dtc::NT && group % (bits == 4 ? 128 : 64) == 0;
 }
 
