@@ -87,6 +87,19 @@ __device__ __forceinline__ uint32_t mul2x(uint32_t a, uint32_t b) {
   return d;
 }
 
+// Tile raster: groups of up to 8 token tiles; inside a group the token tile varies fastest, so the
+// ~148 concurrently running tiles cover <= 8 activation row-blocks and ~18 weight row-blocks and
+// their K slices are shared through L2 (plain m-fastest order re-streams the activations of every
+// weight tile from HBM once M exceeds ~2048 tokens).
+__device__ __forceinline__ void tile_coords(int tile, int m_tiles, int n_tiles, int& mt, int& nt) {
+  constexpr int GM = 8;
+  const int group = tile / (GM * n_tiles);
+  const int gm = min(GM, m_tiles - group * GM);
+  const int local = tile - group * GM * n_tiles;
+  mt = group * GM + local % gm;
+  nt = local / gm;
+}
+
 struct TcParams {
   const void* scales;
   void* C;
@@ -137,7 +150,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+        int mt, nt;
+        tile_coords(tile, p.m_tiles, p.n_tiles, mt, nt);
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty_bar[s], ph ^ 1);
           uint8_t* st = sbase + s * Gm::STAGE;
@@ -187,7 +201,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     int s = 0;
     uint32_t ph = 0, acc_ph = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+      int mt, nt;
+      tile_coords(tile, p.m_tiles, p.n_tiles, mt, nt);
       const int n = nt * BM + row;
       const int nc = min(n, N - 1);
       for (int kb = 0; kb < kblocks; ++kb) {
