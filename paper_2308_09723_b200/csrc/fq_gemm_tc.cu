@@ -91,8 +91,7 @@ __device__ __forceinline__ uint32_t mul2x(uint32_t a, uint32_t b) {
 // ~148 concurrently running tiles cover <= 8 activation row-blocks and ~18 weight row-blocks and
 // their K slices are shared through L2 (plain m-fastest order re-streams the activations of every
 // weight tile from HBM once M exceeds ~2048 tokens).
-__device__ __forceinline__ void tile_coords(int tile, int m_tiles, int n_tiles, int& mt, int& nt) {
-  constexpr int GM = 8;
+__device__ __forceinline__ void tile_coords(int tile, int m_tiles, int n_tiles, int GM, int& mt, int& nt) {
   const int group = tile / (GM * n_tiles);
   const int gm = min(GM, m_tiles - group * GM);
   const int local = tile - group * GM * n_tiles;
@@ -105,6 +104,7 @@ struct TcParams {
   void* C;
   int M, K, N, group, cdt;
   int m_tiles, n_tiles;
+  int gm;  // token tiles per raster group
 };
 
 template <typename T, int BITS>
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t ph = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         int mt, nt;
-        tile_coords(tile, p.m_tiles, p.n_tiles, mt, nt);
+        tile_coords(tile, p.m_tiles, p.n_tiles, p.gm, mt, nt);
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty_bar[s], ph ^ 1);
           uint8_t* st = sbase + s * Gm::STAGE;
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t ph = 0, acc_ph = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       int mt, nt;
-      tile_coords(tile, p.m_tiles, p.n_tiles, mt, nt);
+      tile_coords(tile, p.m_tiles, p.n_tiles, p.gm, mt, nt);
       const int n = nt * BM + row;
       const int nc = min(n, N - 1);
       for (int kb = 0; kb < kblocks; ++kb) {
@@ -313,6 +313,8 @@ static cudaError_t launch_tc(const void* A, int M, int K, int N, const void* cod
   prm.M = M; prm.K = K; prm.N = N; prm.group = group; prm.cdt = cdt;
   prm.m_tiles = (M + tc::BN - 1) / tc::BN;
   prm.n_tiles = (N + tc::BM - 1) / tc::BM;
+  const char* gme = std::getenv("FQ_TC_GM");
+  prm.gm = gme ? std::max(1, std::atoi(gme)) : 8;
   auto kern = tc::gemm_tc_kernel<T, BITS>;
   static bool attr = false;
   if (!attr) {
