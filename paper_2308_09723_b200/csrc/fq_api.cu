@@ -194,19 +194,16 @@ fq_status fq_gemm_grouped(const void* A, int32_t adt, int64_t T, const int64_t* 
     if (!codes_host[e] || !scales_host[e]) return FQ_ERR_INVALID_ARG;
   }
   const cudaStream_t st = as_stream(stream);
-  const size_t cbytes = cdt == FQ_FP32 ? 4 : 2;
+  std::vector<int> large;
   for (int32_t e = 0; e < E; ++e) {
     const int64_t Me = offsets_host[e + 1] - offsets_host[e];
     if (Me == 0) continue;
-    if (Me <= 16 && !use_tc_path(Me)) {
-      small.push_back(e);
-    } else {  // large expert batch: the tcgen05 kernel
-      const char* Ae = reinterpret_cast<const char*>(A) + (size_t)offsets_host[e] * d->K * 2;
-      char* Ce = reinterpret_cast<char*>(C) + (size_t)offsets_host[e] * d->N * cbytes;
-      cudaError_t r = run_gemm_tc(adt, cdt, d->bits, Ae, (int)Me, (int)d->K, (int)d->N, codes_host[e],
-                                  scales_host[e], groups_host[e], Ce, st);
-      if (r != cudaSuccess) return FQ_ERR_CUDA;
-    }
+    (Me <= 16 && !use_tc_path(Me) ? small : large).push_back(e);
+  }
+  if (!large.empty()) {  // every large expert in one persistent tcgen05 launch (per <= 48 experts)
+    cudaError_t r = run_gemm_tc_grouped(adt, cdt, d->bits, A, (int)d->K, (int)d->N, offsets_host, groups_host,
+                                        codes_host, scales_host, C, large.data(), (int)large.size(), st);
+    if (r != cudaSuccess) return FQ_ERR_CUDA;
   }
   // small experts: tcgen05 decode kernel where the group allows, mma.sync kernel otherwise
   std::vector<int> small_tc, small_mma;

@@ -99,18 +99,32 @@ __device__ __forceinline__ void tile_coords(int tile, int m_tiles, int n_tiles, 
   nt = local / gm;
 }
 
-struct TcParams {
+// One GEMM of a batch (MoE experts: one launch covers every large expert; tiles are numbered
+// consecutively across problems and the persistent CTAs walk the global tile list).
+struct TcProb {
+  CUtensorMap a, q;  // activations [M][K] (box 256 x 64, SWIZZLE_128B); codes [N][K*b/8]
   const void* scales;
   void* C;
   int M, K, N, group, cdt;
   int m_tiles, n_tiles;
-  int gm;  // token tiles per raster group
+  int gm;            // token tiles per raster group
+  int tile_begin;
+};
+template <int MAXP>
+struct TcBatch {
+  TcProb p[MAXP];
+  int nprob, total_tiles;
 };
 
-template <typename T, int BITS>
-__global__ void __launch_bounds__(kThreads, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmQ,
-                   const TcParams p) {
+template <int MAXP>
+__device__ __forceinline__ const TcProb& find_prob(const TcBatch<MAXP>& b, int tile) {
+  int pi = 0;
+  while (pi + 1 < b.nprob && tile >= b.p[pi + 1].tile_begin) ++pi;
+  return b.p[pi];
+}
+
+template <typename T, int BITS, int MAXP>
+__global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_constant__ TcBatch<MAXP> batch) {
   using Gm = Geo<BITS>;
   extern __shared__ __align__(1024) uint8_t dsmem[];
   __shared__ __align__(8) uint64_t full_bar[STAGES], afull_bar[STAGES], empty_bar[STAGES];
@@ -118,9 +132,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint32_t tmem_base_sh;
   uint8_t* sbase = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsmem) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int K = p.K, N = p.N, M = p.M;
-  const int kblocks = (K + BK - 1) / BK;
-  const int ntiles = p.m_tiles * p.n_tiles;
+  const int ntiles = batch.total_tiles;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -134,8 +146,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp == 1) tmem_alloc(&tmem_base_sh, kTmemCols);
   if (warp == 0 && lane == 0) {
-    prefetch_tmap(&tmA);
-    prefetch_tmap(&tmQ);
+    for (int i = 0; i < batch.nprob; ++i) {
+      prefetch_tmap(&batch.p[i].a);
+      prefetch_tmap(&batch.p[i].q);
+    }
   }
   fence_before();
   __syncthreads();
@@ -150,14 +164,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const TcProb& p = find_prob(batch, tile);
+        const int kblocks = (p.K + BK - 1) / BK;
         int mt, nt;
-        tile_coords(tile, p.m_tiles, p.n_tiles, p.gm, mt, nt);
+        tile_coords(tile - p.tile_begin, p.m_tiles, p.n_tiles, p.gm, mt, nt);
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty_bar[s], ph ^ 1);
           uint8_t* st = sbase + s * Gm::STAGE;
           mbar_arrive_expect_tx(&full_bar[s], Gm::STAGE);
-          tma_load_2d(st, &tmA, &full_bar[s], kb * BK, mt * BN, pol_a);
-          tma_load_2d(st + kActBytes, &tmQ, &full_bar[s], kb * Gm::CODE_BYTES_ROW, nt * BM, pol_q);
+          tma_load_2d(st, &p.a, &full_bar[s], kb * BK, mt * BN, pol_a);
+          tma_load_2d(st + kActBytes, &p.q, &full_bar[s], kb * Gm::CODE_BYTES_ROW, nt * BM, pol_q);
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
       }
@@ -170,6 +186,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int s = 0;
       uint32_t ph = 0, acc_ph = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int kblocks = (find_prob(batch, tile).K + BK - 1) / BK;
         mbar_wait(&acc_empty, acc_ph ^ 1);  // epilogue drained the accumulator
         fence_after();
         for (int kb = 0; kb < kblocks; ++kb) {
@@ -195,14 +212,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int half = dq >> 2;                // which 32 k of the 64-k block
     const int row = quarter * 32 + lane;     // weight row within the tile == TMEM lane
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-    const T* __restrict__ S = reinterpret_cast<const T*>(p.scales);
-    const int G = K / p.group;
     const uint32_t sb = smem_u32(sbase);
     int s = 0;
     uint32_t ph = 0, acc_ph = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const TcProb& p = find_prob(batch, tile);
+      const int K = p.K, N = p.N, M = p.M;
+      const int kblocks = (K + BK - 1) / BK;
+      const T* __restrict__ S = reinterpret_cast<const T*>(p.scales);
+      const int G = K / p.group;
       int mt, nt;
-      tile_coords(tile, p.m_tiles, p.n_tiles, p.gm, mt, nt);
+      tile_coords(tile - p.tile_begin, p.m_tiles, p.n_tiles, p.gm, mt, nt);
       const int n = nt * BM + row;
       const int nc = min(n, N - 1);
       for (int kb = 0; kb < kblocks; ++kb) {
@@ -296,45 +316,80 @@ __global__ void __launch_bounds__(kThreads, 1)
 }  // namespace tc
 
 // ------------------------------------------------------------------------------------- host side
-template <typename T, int BITS>
-static cudaError_t launch_tc(const void* A, int M, int K, int N, const void* codes, const void* scales,
-                             int group, void* C, int cdt, cudaStream_t st) {
-  using Gm = tc::Geo<BITS>;
-  CUtensorMap tmA, tmQ;
-  if (!make_tmap_2d(&tmA, A, 2, (uint64_t)K, (uint64_t)M, (uint64_t)K * 2, tc::BK, tc::BN, 128))
-    return cudaErrorInvalidValue;
-  const uint64_t row_bytes = (uint64_t)K * BITS / 8;
-  if (!make_tmap_2d(&tmQ, codes, 1, row_bytes, (uint64_t)N, row_bytes, Gm::CODE_BYTES_ROW, tc::BM,
-                    BITS == 4 ? 32 : 64))
-    return cudaErrorInvalidValue;
-  tc::TcParams prm{};
-  prm.scales = scales;
-  prm.C = C;
-  prm.M = M; prm.K = K; prm.N = N; prm.group = group; prm.cdt = cdt;
-  prm.m_tiles = (M + tc::BN - 1) / tc::BN;
-  prm.n_tiles = (N + tc::BM - 1) / tc::BM;
+static bool make_tc_prob(tc::TcProb& d, int bits, const void* A, int M, int K, int N, const void* codes,
+                         const void* scales, int group, void* C, int cdt) {
+  if (!make_tmap_2d(&d.a, A, 2, (uint64_t)K, (uint64_t)M, (uint64_t)K * 2, tc::BK, tc::BN, 128)) return false;
+  const uint64_t row_bytes = (uint64_t)K * bits / 8;
+  if (!make_tmap_2d(&d.q, codes, 1, row_bytes, (uint64_t)N, row_bytes, tc::BK * bits / 8, tc::BM,
+                    bits == 4 ? 32 : 64))
+    return false;
+  d.scales = scales;
+  d.C = C;
+  d.M = M; d.K = K; d.N = N; d.group = group; d.cdt = cdt;
+  d.m_tiles = (M + tc::BN - 1) / tc::BN;
+  d.n_tiles = (N + tc::BM - 1) / tc::BM;
   const char* gme = std::getenv("FQ_TC_GM");
-  prm.gm = gme ? std::max(1, std::atoi(gme)) : 8;
-  auto kern = tc::gemm_tc_kernel<T, BITS>;
+  d.gm = gme ? std::max(1, std::atoi(gme)) : 8;
+  return true;
+}
+
+template <typename T, int BITS, int MAXP>
+static cudaError_t launch_tc(const tc::TcBatch<MAXP>& b, cudaStream_t st) {
+  using Gm = tc::Geo<BITS>;
+  auto kern = tc::gemm_tc_kernel<T, BITS, MAXP>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Gm::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int tiles = prm.m_tiles * prm.n_tiles;
-  const int grid = std::min(tiles, num_sms());
-  kern<<<grid, tc::kThreads, Gm::SMEM, st>>>(tmA, tmQ, prm);
+  const int grid = std::min(b.total_tiles, num_sms());
+  kern<<<grid, tc::kThreads, Gm::SMEM, st>>>(b);
   return cudaGetLastError();
+}
+
+template <int MAXP>
+static cudaError_t dispatch_tc(int adt, int bits, const tc::TcBatch<MAXP>& b, cudaStream_t st) {
+  if (adt == FQ_BF16)
+    return bits == 4 ? launch_tc<__nv_bfloat16, 4, MAXP>(b, st) : launch_tc<__nv_bfloat16, 8, MAXP>(b, st);
+  return bits == 4 ? launch_tc<__half, 4, MAXP>(b, st) : launch_tc<__half, 8, MAXP>(b, st);
 }
 
 cudaError_t run_gemm_tc(int adt, int cdt, int bits, const void* A, int M, int K, int N, const void* codes,
                         const void* scales, int group, void* C, cudaStream_t st) {
-  if (adt == FQ_BF16)
-    return bits == 4 ? launch_tc<__nv_bfloat16, 4>(A, M, K, N, codes, scales, group, C, cdt, st)
-                     : launch_tc<__nv_bfloat16, 8>(A, M, K, N, codes, scales, group, C, cdt, st);
-  return bits == 4 ? launch_tc<__half, 4>(A, M, K, N, codes, scales, group, C, cdt, st)
-                   : launch_tc<__half, 8>(A, M, K, N, codes, scales, group, C, cdt, st);
+  tc::TcBatch<1> b{};
+  if (!make_tc_prob(b.p[0], bits, A, M, K, N, codes, scales, group, C, cdt)) return cudaErrorInvalidValue;
+  b.p[0].tile_begin = 0;
+  b.nprob = 1;
+  b.total_tiles = b.p[0].m_tiles * b.p[0].n_tiles;
+  return dispatch_tc<1>(adt, bits, b, st);
+}
+
+// MoE: every listed expert (M_e > 16) in one persistent launch per <= 48 experts.
+cudaError_t run_gemm_tc_grouped(int adt, int cdt, int bits, const void* A, int K, int N, const int64_t* offsets,
+                                const int32_t* groups, const void* const* codes, const void* const* scales,
+                                void* C, const int* experts, int nexp, cudaStream_t st) {
+  constexpr int MAXP = 48;
+  static_assert(sizeof(tc::TcBatch<MAXP>) < 32000, "kernel parameter block limit");
+  tc::TcBatch<MAXP> b{};
+  for (int ii = 0; ii < nexp; ++ii) {
+    const int e = experts[ii];
+    const int Me = (int)(offsets[e + 1] - offsets[e]);
+    const char* Ae = reinterpret_cast<const char*>(A) + (size_t)offsets[e] * K * 2;
+    char* Ce = reinterpret_cast<char*>(C) + (size_t)offsets[e] * N * (cdt == FQ_FP32 ? 4 : 2);
+    tc::TcProb& d = b.p[b.nprob];
+    if (!make_tc_prob(d, bits, Ae, Me, K, N, codes[e], scales[e], groups[e], Ce, cdt)) return cudaErrorInvalidValue;
+    d.tile_begin = b.total_tiles;
+    b.total_tiles += d.m_tiles * d.n_tiles;
+    if (++b.nprob == MAXP) {
+      cudaError_t r = dispatch_tc<MAXP>(adt, bits, b, st);
+      if (r != cudaSuccess) return r;
+      b.nprob = 0;
+      b.total_tiles = 0;
+    }
+  }
+  if (b.nprob) return dispatch_tc<MAXP>(adt, bits, b, st);
+  return cudaSuccess;
 }
 
 }  // namespace fq

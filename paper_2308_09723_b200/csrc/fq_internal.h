@@ -44,6 +44,9 @@ cudaError_t run_decode_tc_grouped(int adt, int cdt, int bits, const void* A, int
 // Large-M tensor-core GEMM (tcgen05 + TMEM, kernel A6).
 cudaError_t run_gemm_tc(int adt, int cdt, int bits, const void* A, int M, int K, int N, const void* codes,
                         const void* scales, int group, void* C, cudaStream_t st);
+cudaError_t run_gemm_tc_grouped(int adt, int cdt, int bits, const void* A, int K, int N, const int64_t* offsets,
+                                const int32_t* groups, const void* const* codes, const void* const* scales,
+                                void* C, const int* experts, int nexp, cudaStream_t st);
 
 int num_sms();
 
