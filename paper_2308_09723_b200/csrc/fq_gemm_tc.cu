@@ -225,10 +225,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       tile_coords(tile - p.tile_begin, p.m_tiles, p.n_tiles, p.gm, mt, nt);
       const int n = nt * BM + row;
       const int nc = min(n, N - 1);
-      // Software-pipelined: the scales of block kb+1 are fetched one block ahead and block kb+1 is
-      // converted while the tensor-memory stores of block kb drain (tcgen05.wait::st comes last).
-      auto load_scales = [&](int kb, uint32_t (&sc)[4]) {
+      for (int kb = 0; kb < kblocks; ++kb) {
         const int k0 = kb * BK + half * 32;  // this thread's 32 k
+        // scale(s) for this thread's k range (group % 32 == 0: one scale; else per 8-k word)
+        uint32_t sc[4];
         if (p.group % 32 == 0) {
           const int j = min(k0 / p.group, G - 1);
           const unsigned short v = __ldg(reinterpret_cast<const unsigned short*>(S) + (size_t)j * N + nc);
@@ -241,9 +241,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
             sc[w] = (uint32_t)v | ((uint32_t)v << 16);
           }
         }
-      };
-      auto convert = [&](int st, const uint32_t (&sc)[4], uint32_t (&out)[16]) {
-        const uint32_t qbase = sb + st * Gm::STAGE + kActBytes + row * Gm::CODE_BYTES_ROW;
+        mbar_wait(&full_bar[s], ph);
+        const uint32_t qbase = sb + s * Gm::STAGE + kActBytes + row * Gm::CODE_BYTES_ROW;
+        uint32_t out[16];
         if (BITS == 4) {
           // 16 bytes = 32 codes; SWIZZLE_32B: 16-byte chunk c of row r sits at c ^ ((r >> 2) & 1)
           const uint4 c = lds128(qbase + ((half ^ ((row >> 2) & 1)) << 4));
@@ -272,32 +272,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
             }
           }
         }
-      };
-      uint32_t sc_cur[4], sc_nxt[4], out[16], out_nxt[16];
-      load_scales(0, sc_cur);
-      if (kblocks > 1) load_scales(1, sc_nxt);
-      mbar_wait(&full_bar[s], ph);
-      convert(s, sc_cur, out);
-      for (int kb = 0; kb < kblocks; ++kb) {
         tmem_st16(tmem + lane_base + kACol + s * 32 + half * 16, out);
-        int s2 = s + 1;
-        uint32_t ph2 = ph;
-        if (s2 == STAGES) { s2 = 0; ph2 ^= 1; }
-        if (kb + 1 < kblocks) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) sc_cur[i] = sc_nxt[i];
-          if (kb + 2 < kblocks) load_scales(kb + 2, sc_nxt);
-          mbar_wait(&full_bar[s2], ph2);
-          convert(s2, sc_cur, out_nxt);
-        }
         tmem_wait_st();
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&afull_bar[s]);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) out[i] = out_nxt[i];
-        s = s2;
-        ph = ph2;
+        if (++s == STAGES) { s = 0; ph ^= 1; }
       }
       // ---- epilogue: accumulator row `row` (weight n), tokens [half*128, half*128+128)
       mbar_wait(&acc_full, acc_ph);
