@@ -41,12 +41,15 @@ constexpr int kActBytes = BN * BK * 2;     // 32 KB
 constexpr int kTmemCols = 512;
 constexpr int kAccCol = 0;                 // accumulator columns [0, 256)
 constexpr int kACol = 256;                 // A stages: [256 + 32 s, 256 + 32 s + 32)
+constexpr int kScRows = 5;                 // scale rows staged per K block (>= ceil(63/g) + 1, g >= 16)
 
 template <int BITS>
 struct Geo {
   static constexpr int CODE_BYTES_ROW = BK * BITS / 8;        // 32 (int4) / 64 (int8)
   static constexpr int CODE_BYTES = BM * CODE_BYTES_ROW;      // 4 KB / 8 KB
-  static constexpr int STAGE = kActBytes + CODE_BYTES;
+  static constexpr int SC_OFS = kActBytes + CODE_BYTES;       // scale rows of the K block
+  static constexpr int SC_BYTES = kScRows * BM * 2;
+  static constexpr int STAGE = ((SC_OFS + SC_BYTES + 1023) / 1024) * 1024;
   static constexpr int SMEM = STAGES * STAGE + 1024;
 };
 
@@ -103,6 +106,8 @@ __device__ __forceinline__ void tile_coords(int tile, int m_tiles, int n_tiles, 
 // consecutively across problems and the persistent CTAs walk the global tile list).
 struct TcProb {
   CUtensorMap a, q;  // activations [M][K] (box 256 x 64, SWIZZLE_128B); codes [N][K*b/8]
+  CUtensorMap s;     // scales [G][N] (box 5 rows x 128 columns, OOB rows zero)
+  int sc_rows;       // scale rows actually needed per K block (ceil(63/g) + 1, <= kScRows)
   const void* scales;
   void* C;
   int M, K, N, group, cdt;
@@ -149,6 +154,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     for (int i = 0; i < batch.nprob; ++i) {
       prefetch_tmap(&batch.p[i].a);
       prefetch_tmap(&batch.p[i].q);
+      prefetch_tmap(&batch.p[i].s);
     }
   }
   fence_before();
@@ -168,10 +174,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
         const int kblocks = (p.K + BK - 1) / BK;
         int mt, nt;
         tile_coords(tile - p.tile_begin, p.m_tiles, p.n_tiles, p.gm, mt, nt);
-        for (int kb = 0; kb < kblocks; ++kb) {
+        int j0 = 0, r0 = 0;  // first scale row of the K block = floor(64 kb / g), division-free
+        for (int kb = 0; kb < kblocks; ++kb, r0 += BK) {
+          while (r0 >= p.group) { r0 -= p.group; ++j0; }
           mbar_wait(&empty_bar[s], ph ^ 1);
           uint8_t* st = sbase + s * Gm::STAGE;
-          mbar_arrive_expect_tx(&full_bar[s], Gm::STAGE);
+          mbar_arrive_expect_tx(&full_bar[s], kActBytes + Gm::CODE_BYTES + kScRows * BM * 2);
+          tma_load_2d(st + Gm::SC_OFS, &p.s, &full_bar[s], nt * BM, j0, pol_q);
           tma_load_2d(st, &p.a, &full_bar[s], kb * BK, mt * BN, pol_a);
           tma_load_2d(st + kActBytes, &p.q, &full_bar[s], kb * Gm::CODE_BYTES_ROW, nt * BM, pol_q);
           if (++s == STAGES) { s = 0; ph ^= 1; }
@@ -219,29 +228,25 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       const TcProb& p = find_prob(batch, tile);
       const int K = p.K, N = p.N, M = p.M;
       const int kblocks = (K + BK - 1) / BK;
-      const T* __restrict__ S = reinterpret_cast<const T*>(p.scales);
-      const int G = K / p.group;
       int mt, nt;
       tile_coords(tile - p.tile_begin, p.m_tiles, p.n_tiles, p.gm, mt, nt);
       const int n = nt * BM + row;
       const int nc = min(n, N - 1);
+      int j0 = 0, r0 = 0;            // first staged scale row = floor(64 kb / g)
+      int jb = 0, gk = half * 32;     // group of this thread's first k (kb*64 + half*32) and offset
+      while (gk >= p.group) { gk -= p.group; ++jb; }
       for (int kb = 0; kb < kblocks; ++kb) {
-        const int k0 = kb * BK + half * 32;  // this thread's 32 k
-        // scale(s) for this thread's k range (group % 32 == 0: one scale; else per 8-k word)
-        uint32_t sc[4];
-        if (p.group % 32 == 0) {
-          const int j = min(k0 / p.group, G - 1);
-          const unsigned short v = __ldg(reinterpret_cast<const unsigned short*>(S) + (size_t)j * N + nc);
-          sc[0] = sc[1] = sc[2] = sc[3] = (uint32_t)v | ((uint32_t)v << 16);
-        } else {
-#pragma unroll
-          for (int w = 0; w < 4; ++w) {
-            const int j = min((k0 + 8 * w) / p.group, G - 1);
-            const unsigned short v = __ldg(reinterpret_cast<const unsigned short*>(S) + (size_t)j * N + nc);
-            sc[w] = (uint32_t)v | ((uint32_t)v << 16);
-          }
-        }
+        // scales of this thread's 8-k words from the TMA-staged rows: word w lies in group
+        // jb + t, t = [gk + 8w >= g] + [gk + 8w >= 2g]; row index in smem = group - j0.
         mbar_wait(&full_bar[s], ph);
+        uint32_t sc[4];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const int o = gk + 8 * w;
+          const int jr = jb - j0 + (o >= p.group) + (o >= 2 * p.group);
+          const uint32_t v = lds_u16(sb + s * Gm::STAGE + Gm::SC_OFS + (jr * BM + row) * 2);
+          sc[w] = v | (v << 16);
+        }
         const uint32_t qbase = sb + s * Gm::STAGE + kActBytes + row * Gm::CODE_BYTES_ROW;
         uint32_t out[16];
         if (BITS == 4) {
@@ -278,6 +283,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
         __syncwarp();
         if (lane == 0) mbar_arrive(&afull_bar[s]);
         if (++s == STAGES) { s = 0; ph ^= 1; }
+        r0 += BK;
+        while (r0 >= p.group) { r0 -= p.group; ++j0; }
+        gk += BK;
+        while (gk >= p.group) { gk -= p.group; ++jb; }
       }
       // ---- epilogue: accumulator row `row` (weight n), tokens [half*128, half*128+128)
       mbar_wait(&acc_full, acc_ph);
@@ -323,6 +332,9 @@ static bool make_tc_prob(tc::TcProb& d, int bits, const void* A, int M, int K, i
   if (!make_tmap_2d(&d.q, codes, 1, row_bytes, (uint64_t)N, row_bytes, tc::BK * bits / 8, tc::BM,
                     bits == 4 ? 32 : 64))
     return false;
+  if (!make_tmap_2d(&d.s, scales, 2, (uint64_t)N, (uint64_t)(K / group), (uint64_t)N * 2, tc::BM, tc::kScRows, 0))
+    return false;
+  d.sc_rows = (63 + group - 1) / group + 1;
   d.scales = scales;
   d.C = C;
   d.M = M; d.K = K; d.N = N; d.group = group; d.cdt = cdt;
