@@ -138,7 +138,8 @@ fq_status fq_gemm(const void* A, int32_t adt, int64_t M, const fq_wdesc* d, cons
  * codes_host / scales_host: HOST arrays of E DEVICE pointers (canonical layout per expert);
  * groups_host: HOST array of E group sizes (each valid for K).  Experts with 1 <= M_e <= 16 run
  * in one launch per kernel class of the decode kernel (A4, batched); larger experts run the
- * tcgen05 kernel (A6).  ws: fq_gemm_grouped_workspace_bytes(...) bytes (may be NULL today).
+ * tcgen05 kernel (A6).  ws: fq_gemm_grouped_workspace_bytes(...) bytes, zero-filled once (same
+ * contract as fq_gemm's ws); FQ_ERR_WORKSPACE if too small while decode experts are present.
  * ------------------------------------------------------------------------------------------- */
 size_t fq_gemm_grouped_workspace_bytes(int64_t T, int32_t E, const fq_wdesc* d);
 fq_status fq_gemm_grouped(const void* A, int32_t adt, int64_t T, const int64_t* offsets_host,

@@ -88,5 +88,34 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(name: str, defines: list[str]) -> str:
+    """Diagnostics only: a copy of the library compiled with extra -D flags, written to
+    _variants/libfq_<name>.so (load it with FQ_LIB_PATH) so kernel design variants can be timed
+    side by side in one GPU session."""
+    srcs, _ = _sources()
+    out_dir = os.path.join(PKG, "_variants")
+    obj_dir = os.path.join(out_dir, name)
+    os.makedirs(obj_dir, exist_ok=True)
+    cc = nvcc()
+    dflags = [f"-D{d}" for d in defines]
+
+    def compile_one(src):
+        obj = os.path.join(obj_dir, src.replace(".cu", ".o"))
+        r = subprocess.run([cc, *ARCH, *FLAGS, *dflags, "-c", os.path.join(CSRC, src), "-o", obj],
+                           capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
+        return obj
+
+    with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
+        objs = list(ex.map(compile_one, srcs))
+    lib = os.path.join(out_dir, f"libfq_{name}.so")
+    r = subprocess.run([cc, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", lib, *objs],
+                       capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"link failed:\n{r.stderr}")
+    return lib
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

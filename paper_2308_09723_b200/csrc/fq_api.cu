@@ -140,7 +140,7 @@ size_t fq_gemm_workspace_bytes(int64_t M, const fq_wdesc* d) {
   if (decode_tc_supported(d->bits, d->group, (int)M))
     return dtc_workspace_bytes((int)M, (int)d->K, (int)d->N, d->bits, num_sms());
   const GemvPlan p = plan_gemv((int)M, (int)d->K, (int)d->N, d->bits, d->group, num_sms());
-  return gemv_workspace_bytes(p, (int)M, (int)d->N);
+  return gemv_workspace_bytes(p, (int)M, (int)d->K, (int)d->N, d->bits, d->group);
 }
 
 fq_status fq_gemm(const void* A, int32_t adt, int64_t M, const fq_wdesc* d, const void* codes,
@@ -162,23 +162,25 @@ fq_status fq_gemm(const void* A, int32_t adt, int64_t M, const fq_wdesc* d, cons
                                    d->group, C, ws, as_stream(stream)));
   }
   const GemvPlan p = plan_gemv((int)M, (int)d->K, (int)d->N, d->bits, d->group, num_sms());
-  if (p.splits > 1 && (!ws || ws_bytes < gemv_workspace_bytes(p, (int)M, (int)d->N)))
-    return FQ_ERR_WORKSPACE;
+  const size_t need = gemv_workspace_bytes(p, (int)M, (int)d->K, (int)d->N, d->bits, d->group);
+  if (need > 65536 && (!ws || ws_bytes < need)) return FQ_ERR_WORKSPACE;  // counters-only: may be NULL
   return from_cuda(run_gemv(p, adt, cdt, d->bits, A, (int)M, (int)d->K, (int)d->N, codes, scales,
                             d->group, C, ws, as_stream(stream)));
 }
 
 size_t fq_gemm_grouped_workspace_bytes(int64_t T, int32_t E, const fq_wdesc* d) {
-  (void)T; (void)E;
-  if (check_wdesc(d) != FQ_OK) return 0;
-  return 256;  // the grouped kernels need no split-K scratch (the batch fills the machine)
+  (void)E;
+  if (check_wdesc(d) != FQ_OK || T < 0) return 0;
+  // tcgen05 decode experts: counters + per-CTA stream-K partials; mma.sync decode experts:
+  // counters + the pre-converted activations of all T tokens (shared region, stream-ordered)
+  return std::max(dtc_workspace_bytes(16, (int)d->K, (int)d->N, d->bits, num_sms()),
+                  gemv_grouped_workspace_bytes(T, (int)d->K, d->bits));
 }
 
 fq_status fq_gemm_grouped(const void* A, int32_t adt, int64_t T, const int64_t* offsets_host,
                           int32_t E, const fq_wdesc* d, const int32_t* groups_host,
                           const void* const* codes_host, const void* const* scales_host, void* C,
                           int32_t cdt, void* ws, size_t ws_bytes, void* stream) {
-  (void)ws_bytes;
   if (!d || !offsets_host || !groups_host || !codes_host || !scales_host || !A || !C || E <= 0)
     return FQ_ERR_INVALID_ARG;
   if (!valid_half(adt) || d->scale_dtype != adt || (cdt != adt && cdt != FQ_FP32)) return FQ_ERR_UNSUPPORTED;
@@ -212,13 +214,17 @@ fq_status fq_gemm_grouped(const void* A, int32_t adt, int64_t T, const int64_t* 
                                                                                                  : small_mma)
         .push_back(e);
   if (!small_tc.empty()) {
+    if (!ws || ws_bytes < dtc_workspace_bytes(16, (int)d->K, (int)d->N, d->bits, num_sms()))
+      return FQ_ERR_WORKSPACE;
     cudaError_t r = run_decode_tc_grouped(adt, cdt, d->bits, A, (int)d->K, (int)d->N, offsets_host, groups_host,
-                                          codes_host, scales_host, C, small_tc.data(), (int)small_tc.size(), st);
+                                          codes_host, scales_host, C, ws, small_tc.data(), (int)small_tc.size(), st);
     if (r != cudaSuccess) return FQ_ERR_CUDA;
   }
+  if (!small_mma.empty() && (!ws || ws_bytes < gemv_grouped_workspace_bytes(T, (int)d->K, d->bits)))
+    return FQ_ERR_WORKSPACE;
   if (!small_mma.empty())
     return from_cuda(run_gemv_grouped(adt, cdt, d->bits, A, (int)d->K, (int)d->N, offsets_host, groups_host,
-                                      codes_host, scales_host, C, ws, 0, small_mma.data(), (int)small_mma.size(),
+                                      codes_host, scales_host, C, ws, T, small_mma.data(), (int)small_mma.size(),
                                       st));
   return FQ_OK;
 }

@@ -27,18 +27,29 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <type_traits>
 
 #include "fq_common.cuh"
 #include "fq_internal.h"
 
 namespace fq {
 
-constexpr int kConsumerWarps = 8;
-constexpr int kDecThreads = 32 * (2 + kConsumerWarps);  // TMA warp + consumers + activation stager
-constexpr int kRowsPerCta = 256;      // 8 consumer warps x 2 tiles x 16 columns
+#ifndef FQ_DEC_CW
+#define FQ_DEC_CW 8
+#endif
+#ifndef FQ_DEC_EARLY
+#define FQ_DEC_EARLY 1  // consumers release a stage as soon as its data is in registers
+#endif
+constexpr int kConsumerWarps = FQ_DEC_CW;
+// TMA warp + consumers (+ one activation-stager warp unless the activations were pre-converted)
+template <bool PRE> constexpr int dec_threads() { return 32 * (1 + kConsumerWarps + (PRE ? 0 : 1)); }
+constexpr int kRowsPerCta = 32 * kConsumerWarps;      // consumer warp = 2 tiles x 16 columns
+constexpr int kWBoxes = (kRowsPerCta + 255) / 256;    // TMA boxes are at most 256 rows
+constexpr int kWBoxRows = kRowsPerCta / kWBoxes;
+static_assert(kWBoxRows * kWBoxes == kRowsPerCta && kWBoxRows % 8 == 0, "weight box split");
 constexpr int kWBytesPerRow = 64;     // packed bytes of one column per stage (SWIZZLE_64B rows)
-constexpr int kStageW = kRowsPerCta * kWBytesPerRow;  // 32 KB
-constexpr int kDecStages = 4;
+constexpr int kStageW = kRowsPerCta * kWBytesPerRow;
+constexpr int kMaxDecStages = 6;
 
 template <int BITS>
 struct DecGeom {
@@ -47,7 +58,25 @@ struct DecGeom {
   static constexpr int KCH = 4 * SEG;                  // K per chunk (one quad): 128 / 64
   static constexpr int CHUNKS = KS / KCH;              // 2
   static constexpr int PIECES = SEG / 8;               // 16-byte activation pieces per thread/chunk
-  static constexpr int TOK_BYTES = KS * 2 + 64;        // token row stride in smem, = 64 mod 128
+  static constexpr int ROWB = KS * 2;                  // token row stride of the staged activations
+};
+
+// Stage = [packed weights 256 x 64 B][activations MT*8 x KS (TMA, then permuted in place by the
+// stager)][256 scales][per-token activation sums].  As many stages as fit two CTAs per SM.
+template <int BITS, int MT>
+struct DecStage {
+  using G = DecGeom<BITS>;
+  static constexpr int ACT_OFS = kStageW;
+  static constexpr int ACT_BYTES = MT * 8 * G::ROWB;
+  static constexpr int SC_OFS = ACT_OFS + ACT_BYTES;  // TMA destinations: 128-byte aligned
+  static constexpr int SC_BYTES = kRowsPerCta * 2;
+  static constexpr int SUM_OFS = SC_OFS + SC_BYTES;
+  static constexpr int SUM_BYTES = MT * 8 * 16;  // per token: offset correction, inverse scale (+pad)
+  static constexpr int BYTES = ((SUM_OFS + SUM_BYTES + 1023) / 1024) * 1024;
+  static_assert(ACT_OFS % 128 == 0 && SC_OFS % 128 == 0, "TMA smem alignment");
+  static constexpr int kBudget = 115712 - 1024 - 256;  // per CTA at 2 CTAs/SM, minus alignment + static
+  static constexpr int N = kBudget / BYTES < kMaxDecStages ? kBudget / BYTES : kMaxDecStages;
+  static constexpr int SMEM = N * BYTES + 1024;
 };
 
 // One decode problem (a matrix, its activation slice and output slice) of a batch.  A single
@@ -58,12 +87,14 @@ struct DecProb {
   CUtensorMap w;  // packed codes [N][K*bits/8] u8, box [256 rows][64 B], SWIZZLE_64B
   CUtensorMap a;  // activations [M][K] 16-bit, box [MT*8 rows][K per stage]
   CUtensorMap s;  // scales [G][N] 16-bit, box [1 row][256 columns]
+  CUtensorMap sm; // nibble path: per-(chunk, token) {correction, 2^-e, 0, 0} fp32, box [1][MT*8*4]
   const void* scales;
   void* C;
   float* ws;      // split-K partials [splits][M][N]
   int* counters;  // [ktiles][gx]
   int M, K, N, group, klen, cdt;
   int gx, splits, ktiles, cta_begin;
+  int tok_base;   // nibble path: global token index of row 0 (parity of the pre-converted layout)
 };
 template <int MAXP>
 struct DecBatch {
@@ -143,6 +174,39 @@ __device__ __forceinline__ void i4_pairs_off(uint32_t w, uint32_t (&q)[4]) {
   q[2] = lop3_and_xor(w >> 8, mask, Dt<T>::kMagic4);  // (SHF; an IMAD.HI here measured slower)
   q[3] = lop3_and_xor(__umulhi(w, 1u << 20), mask, Dt<T>::kMagic4);  // w >> 12
 }
+// "Nibble" unpack (FQ_NIB, int4 scale-on-accumulator path): the odd codes of a word are taken
+// straight from bits 4..7 of each 16-bit half, which the magic makes worth 16x their value
+// (exponent of 128/1024, mantissa bits 4..7), so one shift serves four pairs:
+//   even pairs (k,k+4),(k+2,k+6): 128 + (n^8) = q + 136   (fp16: q + 1032)
+//   odd  pairs (k+1,k+5),(k+3,k+7): 16 * (q + 16)        (fp16: 16 * (q + 72))
+// The trick needs >= 8 mantissa bits, so the MMA runs in fp16 (10 bits) for bf16 inputs too:
+// the stager re-encodes each token's activations of a chunk as fp16 after scaling them by a power
+// of two 2^e that puts the chunk's max |a| in [2^14, 2^15) -- exact for every element within
+// 2^31 of that max (bf16 has 8 significant bits, fp16 normals 11) -- and the fold multiplies the
+// chunk's partial by 2^-e.  The stager also divides the odd activations by 16 (exact) and stores
+// the per-token correction 1032 * sum_even(a') + 72 * sum_odd(a') (a' the scaled activations),
+// removed once per chunk.
+#ifndef FQ_NIB
+#define FQ_NIB 1
+#endif
+template <typename T> struct Nib;
+template <> struct Nib<__nv_bfloat16> {
+  static constexpr uint32_t lo = 0x43084308u, hi = 0x43804380u, sixteenth = 0x3D803D80u;
+  static constexpr float off_even = 136.f, off_odd = 16.f;
+};
+template <> struct Nib<__half> {
+  static constexpr uint32_t lo = 0x64086408u, hi = 0x64806480u, sixteenth = 0x2C002C00u;
+  static constexpr float off_even = 1032.f, off_odd = 72.f;
+};
+template <typename T>
+__device__ __forceinline__ void i4_pairs_nib(uint32_t w, uint32_t (&q)[4]) {
+  const uint32_t w8 = w >> 8;
+  q[0] = lop3_and_xor(w, 0x000F000Fu, Nib<T>::lo);
+  q[1] = lop3_and_xor(w, 0x00F000F0u, Nib<T>::hi);
+  q[2] = lop3_and_xor(w8, 0x000F000Fu, Nib<T>::lo);
+  q[3] = lop3_and_xor(w8, 0x00F000F0u, Nib<T>::hi);
+}
+
 template <typename T, int BITS> struct CodeOffset { static constexpr float v = 0.f; };
 template <> struct CodeOffset<__nv_bfloat16, 4> { static constexpr float v = 136.f; };
 template <> struct CodeOffset<__half, 4> { static constexpr float v = 1032.f; };
@@ -201,22 +265,25 @@ __device__ __forceinline__ int swz64(int c, int R) { return c ^ ((R >> 1) & 3); 
 // DBG (diagnostics only, selected by FQ_DEC_DEBUG for bf16/int4/M<=8): 1 = no MMA (fake FADD
 // accumulate), 2 = no dequant (raw code words as MMA operands), 3 = consumers skip all compute.
 template <typename T, int BITS, int MT, bool SACC, int DBG, int MAXP>
-__global__ void __launch_bounds__(kDecThreads, 2) decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
+__global__ void __launch_bounds__(dec_threads<FQ_NIB && BITS == 4 && SACC>(), 2) decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
   using G = DecGeom<BITS>;
+  using SG = DecStage<BITS, MT>;
   constexpr int KS = G::KS, SEG = G::SEG, KCH = G::KCH, CHUNKS = G::CHUNKS, PIECES = G::PIECES;
-  constexpr int TOK = G::TOK_BYTES;
-  constexpr int ACT_BYTES = MT * 8 * TOK;
-  constexpr int SA_BYTES = MT * 8 * CHUNKS * 4;  // fp32 activation sums [token][chunk]
-  constexpr int RAW_BYTES = MT * 8 * KS * 2;     // TMA-staged activations, natural order
-  constexpr int RAW_OFS = kStageW + ((ACT_BYTES + SA_BYTES + 127) / 128) * 128;
-  constexpr int SC_BYTES = kRowsPerCta * 2;       // TMA-staged scale row segment s[j][n0..n0+255]
-  constexpr int SC_OFS = RAW_OFS + RAW_BYTES;
-  constexpr int STAGE_BYTES = ((SC_OFS + SC_BYTES + 1023) / 1024) * 1024;
-  constexpr float OFF = SACC ? CodeOffset<T, BITS>::v : 0.f;
+  constexpr int ROWB = G::ROWB;
+  constexpr int NSTG = SG::N;
+  constexpr int ACT_OFS = SG::ACT_OFS, SUM_OFS = SG::SUM_OFS, SC_OFS = SG::SC_OFS;
+  constexpr int STAGE_BYTES = SG::BYTES;
+  constexpr int SC_BYTES = SG::SC_BYTES;
+  constexpr int RAW_BYTES = SG::ACT_BYTES;
+  // Nibble path: activations were pre-converted by prep_acts_kernel (fp16, fragment order) and
+  // arrive by TMA with their per-chunk {correction, 2^-e}; there is no stager warp.
+  constexpr bool NIB = FQ_NIB && BITS == 4 && SACC;
+  using TC = typename std::conditional<NIB, __half, T>::type;  // MMA operand type
+  constexpr float OFF = NIB ? 1.f : (SACC ? CodeOffset<T, BITS>::v : 0.f);  // NIB: sums hold the correction
   constexpr int PPC = KCH / 8;  // 8-element pieces per chunk (16 int4, 8 int8): divides 32
 
   extern __shared__ __align__(1024) uint8_t dsmem[];
-  __shared__ __align__(8) uint64_t full_bar[kDecStages], empty_bar[kDecStages], raw_bar[kDecStages];
+  __shared__ __align__(8) uint64_t full_bar[kMaxDecStages], empty_bar[kMaxDecStages], raw_bar[kMaxDecStages];
   __shared__ int s_last;
   uint8_t* sbase = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsmem) + 1023) & ~uintptr_t(1023));
 
@@ -234,9 +301,9 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode_kernel(const __grid_con
   const int tok0 = bz * 16;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kDecStages; ++s) {
-      mbar_init(&full_bar[s], 1 + 32);  // weight TMA (expect_tx arrival) + 32 stager lanes
-      mbar_init(&raw_bar[s], 1);        // activation TMA
+    for (int s = 0; s < NSTG; ++s) {
+      mbar_init(&full_bar[s], NIB ? 1 : 1 + 32);  // TMA expect_tx arrival (+ 32 stager lanes)
+      mbar_init(&raw_bar[s], 1);                   // activation TMA (stager path)
       mbar_init(&empty_bar[s], kConsumerWarps);
     }
     fence_mbar_init();
@@ -245,6 +312,7 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode_kernel(const __grid_con
     prefetch_tmap(&p.w);
     prefetch_tmap(&p.a);
     if (SACC) prefetch_tmap(&p.s);
+    if (NIB) prefetch_tmap(&p.sm);
   }
   __syncthreads();
 
@@ -262,77 +330,88 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode_kernel(const __grid_con
         mbar_wait(&empty_bar[s], ph ^ 1);
         uint8_t* st = sbase + s * STAGE_BYTES;
         const int k0 = kbeg + i * KS;
-        mbar_arrive_expect_tx(&full_bar[s], kStageW + (SACC ? SC_BYTES : 0));
-        tma_load_2d(st, &p.w, &full_bar[s], k0 * BITS / 8, n0, polw);
+        mbar_arrive_expect_tx(&full_bar[s], kStageW + (SACC ? SC_BYTES : 0) + (NIB ? RAW_BYTES + MT * 8 * 16 : 0));
+#pragma unroll
+        for (int bx2 = 0; bx2 < kWBoxes; ++bx2)
+          tma_load_2d(st + bx2 * kWBoxRows * kWBytesPerRow, &p.w, &full_bar[s], k0 * BITS / 8,
+                      n0 + bx2 * kWBoxRows, polw);
         if (SACC) {
-          tma_load_2d(st + SC_OFS, &p.s, &full_bar[s], n0, gj, polw);
+#pragma unroll
+          for (int bx2 = 0; bx2 < kWBoxes; ++bx2)
+            tma_load_2d(st + SC_OFS + bx2 * kWBoxRows * 2, &p.s, &full_bar[s], n0 + bx2 * kWBoxRows, gj, polw);
           if (++grem == gm) { grem = 0; ++gj; }
         }
-        mbar_arrive_expect_tx(&raw_bar[s], RAW_BYTES);
-        tma_load_2d(st + RAW_OFS, &p.a, &raw_bar[s], k0, tok0, pola);
-        if (++s == kDecStages) { s = 0; ph ^= 1; }
+        if (NIB) {
+          tma_load_2d(st + ACT_OFS, &p.a, &full_bar[s], k0, tok0, pola);
+          tma_load_2d(st + SUM_OFS, &p.sm, &full_bar[s], tok0 * 4, k0 / KCH, pola);
+        } else {
+          mbar_arrive_expect_tx(&raw_bar[s], RAW_BYTES);
+          tma_load_2d(st + ACT_OFS, &p.a, &raw_bar[s], k0, tok0, pola);
+        }
+        if (++s == NSTG) { s = 0; ph ^= 1; }
       }
     }
     return;
   }
-  if (warp == kConsumerWarps + 1) {
-    // ------------------------------------------------------------ activation stager
-    // raw [MT*8 tokens][KS] (TMA, natural order, OOB zero) -> per-thread MMA fragment order
-    // (+ the per-token sums used by the code-offset correction).
-    constexpr int NPIECE = MT * 8 * (KS / 8);
-    static_assert(NPIECE % 32 == 0, "pieces per stage must be a multiple of the warp size");
+  if (!NIB && warp > kConsumerWarps) {
+    // ------------------------------------------------------------ activation stagers
+    // The TMA leaves [MT*8 tokens][KS] in natural order (rows >= M zero-filled).  Each 8-element
+    // piece is permuted in place into the consumers' fragment order: words (0,4),(1,5),(2,6),(3,7)
+    // (int4), cell c -> (c % PIECES) * 4 + c / PIECES, XOR (token & 1) * 4 (puts the two tokens of
+    // a 128-bit shared-memory phase in different bank halves); plus the per-token sums and, on
+    // the nibble path, the fp16 re-encoding.
+    constexpr int CELLS = KS / 8;  // 16-byte pieces per token row
+    constexpr int NPIECE = MT * 8 * CELLS;
+    static_assert(NPIECE % 32 == 0 && 32 % CELLS == 0, "piece groups of whole tokens");
     constexpr int NPW = NPIECE / 32;
-    // tokens >= M stay zero: written once here, skipped in the loop (M = 1 stages 1/8 of the data)
-    const int mloc = min(M - tok0, MT * 8);
-    for (int s0 = 0; s0 < kDecStages; ++s0) {
-      const uint32_t stu = smem_u32(sbase + s0 * STAGE_BYTES);
-      for (int o = mloc * TOK + lane * 16; o < ACT_BYTES; o += 32 * 16) sts128(stu + kStageW + o, make_uint4(0, 0, 0, 0));
-      if (lane < MT * 8 * CHUNKS) reinterpret_cast<float*>(sbase + s0 * STAGE_BYTES + kStageW + ACT_BYTES)[lane] = 0.f;
-    }
-    __syncwarp();
+    const int mloc = min(M - tok0, MT * 8);  // tokens >= mloc are TMA zero fill: left alone
     int s = 0;
     uint32_t ph = 0;
     for (int i = 0; i < nst; ++i) {
       mbar_wait(&raw_bar[s], ph);
       uint8_t* st = sbase + s * STAGE_BYTES;
       const uint32_t stu = smem_u32(st);
-      uint4 va[NPW];
+      uint4 vj[NPW];
 #pragma unroll
       for (int j = 0; j < NPW; ++j)
-        if ((32 * j) / (KS / 8) < mloc) va[j] = lds128(stu + RAW_OFS + (lane + 32 * j) * 16);
+        if ((32 * j) / CELLS < mloc) vj[j] = lds128(stu + ACT_OFS + (lane + 32 * j) * 16);
+      __syncwarp();  // every read of this warp's tokens precedes the in-place writes
 #pragma unroll
       for (int j = 0; j < NPW; ++j) {
-        if ((32 * j) / (KS / 8) >= mloc) continue;  // warp-uniform: whole piece group is zero tokens
+        if ((32 * j) / CELLS >= mloc) continue;  // warp-uniform
         const int pc = lane + 32 * j;
-        const int tl = pc / (KS / 8);          // local token
-        const int kl = (pc % (KS / 8)) * 8;    // local k of this 8-element piece
-        const int r = kl % KCH, t = r / SEG, w16 = (r % SEG) / 8;
-        uint4 v = va[j];
-        if (OFF != 0.f) {
-          // sum of the 8 activations, reduced over the PPC lanes of this chunk (aligned groups)
-          float sum = 0.f;
-          const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+        const int tl = pc / CELLS;           // local token
+        const int kl = (pc % CELLS) * 8;     // local k of this 8-element piece
+        const int r = kl % KCH, tq = r / SEG, w16 = (r % SEG) / 8;
+        const uint4 va = vj[j];
+        uint4 v = va;
+        {
+          if (OFF != 0.f) {
+            // sum of the 8 activations, reduced over the PPC lanes of this chunk (aligned groups)
+            float sum = 0.f;
+            const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            if (Dt<T>::id == FQ_BF16) {
-              sum += __uint_as_float(vv[e] << 16) + __uint_as_float(vv[e] & 0xFFFF0000u);
-            } else {
-              const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&vv[e]));
-              sum += f.x + f.y;
+            for (int e = 0; e < 4; ++e) {
+              if (Dt<T>::id == FQ_BF16) {
+                sum += __uint_as_float(vv[e] << 16) + __uint_as_float(vv[e] & 0xFFFF0000u);
+              } else {
+                const float2 ff = __half22float2(*reinterpret_cast<const __half2*>(&vv[e]));
+                sum += ff.x + ff.y;
+              }
             }
-          }
 #pragma unroll
-          for (int o = PPC / 2; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-          if ((lane % PPC) == 0) reinterpret_cast<float*>(st + kStageW + ACT_BYTES)[tl] = sum;
+            for (int o = PPC / 2; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            if ((lane % PPC) == 0) reinterpret_cast<float*>(st + SUM_OFS)[tl] = sum;
+          }
+          if (BITS == 4) {
+            v = make_uint4(prmt(v.x, v.z, 0x5410u), prmt(v.x, v.z, 0x7632u), prmt(v.y, v.w, 0x5410u),
+                           prmt(v.y, v.w, 0x7632u));
+          }
         }
-        if (BITS == 4) {
-          v = make_uint4(prmt(v.x, v.z, 0x5410u), prmt(v.x, v.z, 0x7632u), prmt(v.y, v.w, 0x5410u),
-                         prmt(v.y, v.w, 0x7632u));
-        }
-        sts128(stu + kStageW + tl * TOK + (w16 * 4 + t) * 16, v);
+        sts128(stu + ACT_OFS + tl * ROWB + (((w16 * 4 + tq) ^ ((tl & 1) << 2)) << 4), v);
       }
       mbar_arrive(&full_bar[s]);
-      if (++s == kDecStages) { s = 0; ph ^= 1; }
+      if (++s == NSTG) { s = 0; ph ^= 1; }
     }
     return;
   }
@@ -357,8 +436,10 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode_kernel(const __grid_con
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-    for (int w16 = 0; w16 < PIECES; ++w16) aofs[mt][w16] = kStageW + (mt * 8 + gq) * TOK + (w16 * 4 + t) * 16;
-  const uint32_t saofs = kStageW + ACT_BYTES + 2 * t * 4;
+    for (int w16 = 0; w16 < PIECES; ++w16)
+      aofs[mt][w16] = ACT_OFS + (mt * 8 + gq) * ROWB +
+                      (((w16 * 4 + t) ^ (((NIB ? p.tok_base + tok0 + gq : gq) & 1) << 2)) << 4);
+  const uint32_t saofs = NIB ? SUM_OFS + 2 * t * 16 : SUM_OFS + 2 * t * 4;
   float acc[2][MT][4];
 #pragma unroll
   for (int rt = 0; rt < 2; ++rt)
@@ -388,15 +469,34 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode_kernel(const __grid_con
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
         for (int w16 = 0; w16 < PIECES; ++w16) b[mt][w16] = lds128(wst + aofs[mt][w16]);
-      float2 sa[MT];
-      if (OFF != 0.f) {
+      float2 sa[MT], iv[MT];
+      if (NIB) {  // {corr, 2^-e} of tokens 2t and 2t+1
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const float2 x0 = lds64f(wst + saofs + mt * 128), x1 = lds64f(wst + saofs + mt * 128 + 16);
+          sa[mt] = make_float2(x0.x, x1.x);
+          iv[mt] = make_float2(x0.y, x1.y);
+        }
+      } else if (OFF != 0.f) {
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) sa[mt] = lds64f(wst + saofs + mt * 32);
       }
+      uint4 wgv[2], whv[2];
 #pragma unroll
       for (int rt = 0; rt < 2; ++rt) {
-        const uint4 wg = lds128(wst + wofs_g[rt]);
-        const uint4 wh = lds128(wst + wofs_h[rt]);
+        wgv[rt] = lds128(wst + wofs_g[rt]);
+        whv[rt] = lds128(wst + wofs_h[rt]);
+      }
+      if (FQ_DEC_EARLY) {
+        // everything this warp needs from the stage is in registers: hand the slot back to the TMA
+        // producer now, so the next loads overlap this warp's dequant + MMA work
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[s]);
+      }
+#pragma unroll
+      for (int rt = 0; rt < 2; ++rt) {
+        const uint4 wg = wgv[rt];
+        const uint4 wh = whv[rt];
         const uint32_t wgw[4] = {wg.x, wg.y, wg.z, wg.w};
         const uint32_t whw[4] = {wh.x, wh.y, wh.z, wh.w};
         float part[MT][4];
@@ -421,6 +521,9 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode_kernel(const __grid_con
             if (DBG == 2) {
 #pragma unroll
               for (int q = 0; q < 4; ++q) { qg[q] = wgw[w] + q; qh[q] = whw[w] + q; }
+            } else if (NIB) {
+              i4_pairs_nib<TC>(wgw[w], qg);
+              i4_pairs_nib<TC>(whw[w], qh);
             } else if (OFF != 0.f) {
               i4_pairs_off<T>(wgw[w], qg);
               i4_pairs_off<T>(whw[w], qh);
@@ -443,7 +546,7 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode_kernel(const __grid_con
 #pragma unroll
                   for (int q = 0; q < 4; ++q) dst[mt][q] += __uint_as_float(a[q] ^ b0);
                 } else {
-                  mma16816<T>(dst[mt], a, b0, b1);
+                  mma16816<TC>(dst[mt], a, b0, b1);
                 }
               }
             }
@@ -477,17 +580,26 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode_kernel(const __grid_con
               part[mt][2] = fmaf(-OFF, sa[mt].x, part[mt][2]);
               part[mt][3] = fmaf(-OFF, sa[mt].y, part[mt][3]);
             }
-            acc[rt][mt][0] = fmaf(sg[rt], part[mt][0], acc[rt][mt][0]);
-            acc[rt][mt][1] = fmaf(sg[rt], part[mt][1], acc[rt][mt][1]);
-            acc[rt][mt][2] = fmaf(sh[rt], part[mt][2], acc[rt][mt][2]);
-            acc[rt][mt][3] = fmaf(sh[rt], part[mt][3], acc[rt][mt][3]);
+            if (NIB) {  // undo the chunk's power-of-two activation scale
+              acc[rt][mt][0] = fmaf(sg[rt] * iv[mt].x, part[mt][0], acc[rt][mt][0]);
+              acc[rt][mt][1] = fmaf(sg[rt] * iv[mt].y, part[mt][1], acc[rt][mt][1]);
+              acc[rt][mt][2] = fmaf(sh[rt] * iv[mt].x, part[mt][2], acc[rt][mt][2]);
+              acc[rt][mt][3] = fmaf(sh[rt] * iv[mt].y, part[mt][3], acc[rt][mt][3]);
+            } else {
+              acc[rt][mt][0] = fmaf(sg[rt], part[mt][0], acc[rt][mt][0]);
+              acc[rt][mt][1] = fmaf(sg[rt], part[mt][1], acc[rt][mt][1]);
+              acc[rt][mt][2] = fmaf(sh[rt], part[mt][2], acc[rt][mt][2]);
+              acc[rt][mt][3] = fmaf(sh[rt], part[mt][3], acc[rt][mt][3]);
+            }
           }
         }
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_bar[s]);
-    if (++s == kDecStages) { s = 0; ph ^= 1; }
+    if (!FQ_DEC_EARLY || DBG == 3) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[s]);
+    }
+    if (++s == NSTG) { s = 0; ph ^= 1; }
   }
 
   // ------------------------------------------------------------- epilogue (+ fused A5 fixup)
@@ -525,13 +637,18 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode_kernel(const __grid_con
         out_idx(rt, mt, i, n, tok);
         if (n < N && tok < M) __stcg(part_out + (size_t)tok * N + n, acc[rt][mt][i]);
       }
-  __threadfence();
+  // bar.sync orders every consumer's partial stores before the counting thread's release fence
+  // (cumulativity); its acquire fence + the second bar.sync order the reads of the last CTA.
   asm volatile("bar.sync 1, %0;" ::"n"(32 * kConsumerWarps));
   int* ctr = p.counters + bz * p.gx + bx;
-  if (threadIdx.x == 32) s_last = (atomicAdd(ctr, 1) == S_ - 1);
+  if (threadIdx.x == 32) {
+    __threadfence();
+    const int last = (atomicAdd(ctr, 1) == S_ - 1);
+    if (last) __threadfence();
+    s_last = last;
+  }
   asm volatile("bar.sync 1, %0;" ::"n"(32 * kConsumerWarps));
   if (!s_last) return;
-  __threadfence();
 #pragma unroll
   for (int rt = 0; rt < 2; ++rt)
 #pragma unroll
@@ -549,6 +666,67 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode_kernel(const __grid_con
   if (threadIdx.x == 32) *ctr = 0;  // self-reset for the next call / graph replay
 }
 
+// ---- activation pre-conversion for the nibble path (one launch per GEMM call, M x K elements) --
+// Half-warp = one (token, 128-k chunk): 16 lanes x 8 activations.  Output A'[tok][k]: fp16, each
+// chunk's 8-element pieces permuted into the decode consumers' fragment order (words (a0,a4),
+// (a1,a5)/16, (a2,a6), (a3,a7)/16; cell c -> (c % 4) * 4 + c / 4, XOR (tok & 1) * 4), values
+// scaled by 2^e (bf16 input: the chunk max |a| lands in [2^14, 2^15); fp16 input: e = 0).
+// S'[chunk][tok] = {1032 * sum_even(a') + 72 * sum_odd(a'), 2^-e, 0, 0}.
+template <typename T>
+__global__ void __launch_bounds__(128) prep_acts_kernel(const T* __restrict__ A, int ntok, int K,
+                                                        __half* __restrict__ Ap, float* __restrict__ Sp) {
+  const int chunks = K >> 7;
+  const int hw = blockIdx.x * 8 + (threadIdx.x >> 4);
+  const int l = threadIdx.x & 15;
+  if (hw >= ntok * chunks) return;  // whole half-warps exit together
+  const unsigned hmask = 0xFFFFu << (threadIdx.x & 16);
+  const int tok = hw / chunks, ch = hw - tok * chunks;
+  const size_t base = (size_t)tok * K + (size_t)ch * 128;
+  const uint4 v = ldg_keep(A + base + l * 8);
+  const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+  float f[8];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    if (Dt<T>::id == FQ_BF16) {
+      f[2 * e] = __uint_as_float(vv[e] << 16);
+      f[2 * e + 1] = __uint_as_float(vv[e] & 0xFFFF0000u);
+    } else {
+      const float2 h = __half22float2(*reinterpret_cast<const __half2*>(&vv[e]));
+      f[2 * e] = h.x;
+      f[2 * e + 1] = h.y;
+    }
+  }
+  float inv = 1.f;
+  if (Dt<T>::id == FQ_BF16) {
+    float mx = 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) mx = fmaxf(mx, fabsf(f[e]));
+#pragma unroll
+    for (int o = 8; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(hmask, mx, o));
+    const int E = (int)((__float_as_uint(mx) >> 23) & 0xFF);
+    const int F = min(268 - E, 253);  // biased exponent of 2^e, e = 14 - (E - 127)
+    const float sc = __uint_as_float((uint32_t)F << 23);
+    inv = __uint_as_float((uint32_t)(254 - F) << 23);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) f[e] *= sc;
+  }
+  float sum = fmaf(Nib<__half>::off_even, (f[0] + f[2]) + (f[4] + f[6]),
+                   Nib<__half>::off_odd * ((f[1] + f[3]) + (f[5] + f[7])));
+#pragma unroll
+  for (int o = 8; o; o >>= 1) sum += __shfl_xor_sync(hmask, sum, o);
+  auto h2 = [](float lo, float hi) {
+    uint32_t hw2;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hw2) : "f"(hi), "f"(lo));
+    return hw2;
+  };
+  const uint4 o = make_uint4(h2(f[0], f[4]), h2(f[1] * 0.0625f, f[5] * 0.0625f), h2(f[2], f[6]),
+                             h2(f[3] * 0.0625f, f[7] * 0.0625f));
+  const int kl = l * 8, tq = kl >> 5, w16 = (kl & 31) >> 3;
+  const int cell = (w16 * 4 + tq) ^ ((tok & 1) << 2);
+  *reinterpret_cast<uint4*>(Ap + base + cell * 8) = o;
+  if (l == 0) *reinterpret_cast<float4*>(Sp + ((size_t)ch * ntok + tok) * 4) = make_float4(sum, inv, 0.f, 0.f);
+}
+
 // ------------------------------------------------------------------------------------- host side
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 constexpr int kMaxCounters = 16384;
@@ -557,13 +735,6 @@ constexpr size_t kCounterBytes = kMaxCounters * sizeof(int);
 static int env_int(const char* name, int dflt) {
   const char* v = std::getenv(name);
   return v ? std::atoi(v) : dflt;
-}
-
-template <int BITS, int MT>
-static constexpr int dec_smem_bytes() {
-  using G = DecGeom<BITS>;
-  constexpr int raw_ofs = kStageW + ((MT * 8 * G::TOK_BYTES + MT * 8 * G::CHUNKS * 4 + 127) / 128) * 128;
-  return kDecStages * (((raw_ofs + MT * 8 * G::KS * 2 + kRowsPerCta * 2) + 1023) / 1024 * 1024) + 1024;
 }
 
 GemvPlan plan_gemv(int M, int K, int N, int bits, int group, int nsm) {
@@ -601,15 +772,36 @@ GemvPlan plan_gemv(int M, int K, int N, int bits, int group, int nsm) {
 
 // Workspace layout (fixed, so buffers can be shared by calls of different shapes):
 //   [0, kCounterBytes)  arrival counters (zeroed once by the caller, self-resetting)
-//   [kCounterBytes, ..) split-K fp32 partials [S][M][N] (fully overwritten by every call)
-size_t gemv_workspace_bytes(const GemvPlan& p, int M, int N) {
-  if (p.splits <= 1) return kCounterBytes;
-  return kCounterBytes + align256((size_t)p.splits * M * N * sizeof(float));
+//   then split-K fp32 partials [S][M][N] (fully overwritten by every call)
+//   then, on the nibble path, the pre-converted activations A' [M][K] fp16 and S' [K/128][M][4].
+static bool nib_of(int bits, int group) { return FQ_NIB && bits == 4 && group % 128 == 0; }
+static size_t prep_bytes(int M, int K) {
+  return align256((size_t)M * K * 2) + align256((size_t)(K / 128) * M * 16);
+}
+size_t gemv_workspace_bytes(const GemvPlan& p, int M, int K, int N, int bits, int group) {
+  size_t b = kCounterBytes;
+  if (p.splits > 1) b += align256((size_t)p.splits * M * N * sizeof(float));
+  if (nib_of(bits, group)) b += prep_bytes(M, K);
+  return b;
+}
+size_t gemv_grouped_workspace_bytes(int64_t T, int K, int bits) {
+  return kCounterBytes + (bits == 4 ? prep_bytes((int)T, K) : 0);
+}
+static cudaError_t launch_prep(int adt, const void* A, int ntok, int K, void* Ap, void* Sp, cudaStream_t st) {
+  const int blocks = (int)(((long long)ntok * (K / 128) + 7) / 8);
+  if (blocks == 0) return cudaSuccess;
+  if (adt == FQ_BF16)
+    prep_acts_kernel<__nv_bfloat16><<<blocks, 128, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(A), ntok, K,
+                                                            reinterpret_cast<__half*>(Ap), reinterpret_cast<float*>(Sp));
+  else
+    prep_acts_kernel<__half><<<blocks, 128, 0, st>>>(reinterpret_cast<const __half*>(A), ntok, K,
+                                                     reinterpret_cast<__half*>(Ap), reinterpret_cast<float*>(Sp));
+  return cudaGetLastError();
 }
 
 template <typename T, int BITS, int MT, bool SACC, int DBG, int MAXP>
 static cudaError_t launch_dec(const DecBatch<MAXP>& b, int ctas, cudaStream_t st) {
-  constexpr int smem = dec_smem_bytes<BITS, MT>();
+  constexpr int smem = DecStage<BITS, MT>::SMEM;
   auto kern = decode_kernel<T, BITS, MT, SACC, DBG, MAXP>;
   static bool attr_set = false;  // benign race: idempotent attribute call
   if (!attr_set) {
@@ -617,7 +809,7 @@ static cudaError_t launch_dec(const DecBatch<MAXP>& b, int ctas, cudaStream_t st
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  kern<<<ctas, kDecThreads, smem, st>>>(b);
+  kern<<<ctas, dec_threads<FQ_NIB && BITS == 4 && SACC>(), smem, st>>>(b);
   return cudaGetLastError();
 }
 
@@ -648,14 +840,21 @@ static cudaError_t dispatch_dec(int adt, int bits, int mt, bool sacc, int dbg, c
 
 // Fill one batch entry (tensor maps + sizes) for one matrix under plan `pl`.  ws: that problem's
 // workspace (counters at offset 0, partials after kCounterBytes).
+// nib: A points at the pre-converted A' rows of this problem, Sp at S' column tok_base of a
+// [K/128][ntok_all][4] array.
 static bool make_dec_prob(DecProb& d, const GemvPlan& pl, int bits, int cdt, const void* A, int M, int K,
-                          int N, const void* codes, const void* scales, int group, void* C, void* ws) {
+                          int N, const void* codes, const void* scales, int group, void* C, void* ws,
+                          const void* Sp = nullptr, int ntok_all = 0, int tok_base = 0) {
   const uint64_t row_bytes = (uint64_t)K * bits / 8;
-  if (!make_tmap_2d(&d.w, codes, 1, row_bytes, (uint64_t)N, row_bytes, kWBytesPerRow, kRowsPerCta, 64))
+  if (!make_tmap_2d(&d.w, codes, 1, row_bytes, (uint64_t)N, row_bytes, kWBytesPerRow, kWBoxRows, 64))
     return false;
   const int ks = kWBytesPerRow * 8 / bits;  // K per stage
   if (!make_tmap_2d(&d.a, A, 2, (uint64_t)K, (uint64_t)M, (uint64_t)K * 2, ks, pl.mt * 8, 0)) return false;
-  if (!make_tmap_2d(&d.s, scales, 2, (uint64_t)N, (uint64_t)(K / group), (uint64_t)N * 2, kRowsPerCta, 1, 0))
+  d.tok_base = tok_base;
+  if (Sp && !make_tmap_2d(&d.sm, reinterpret_cast<const char*>(Sp) + (size_t)tok_base * 16, 4, (uint64_t)M * 4,
+                          (uint64_t)(K / 128), (uint64_t)ntok_all * 16, pl.mt * 8 * 4, 1, 0))
+    return false;
+  if (!make_tmap_2d(&d.s, scales, 2, (uint64_t)N, (uint64_t)(K / group), (uint64_t)N * 2, kWBoxRows, 1, 0))
     return false;
   d.scales = scales;
   d.C = C;
@@ -675,8 +874,17 @@ cudaError_t run_gemv(const GemvPlan& pl, int adt, int cdt, int bits, const void*
                      int N, const void* codes, const void* scales, int group, void* C, void* ws,
                      cudaStream_t st) {
   DecBatch<1> b{};
-  if (!make_dec_prob(b.p[0], pl, bits, cdt, A, M, K, N, codes, scales, group, C, ws))
+  if (nib_of(bits, group)) {
+    char* pre = reinterpret_cast<char*>(ws) + kCounterBytes +
+                (pl.splits > 1 ? align256((size_t)pl.splits * M * N * sizeof(float)) : 0);
+    char* Sp = pre + align256((size_t)M * K * 2);
+    cudaError_t r = launch_prep(adt, A, M, K, pre, Sp, st);
+    if (r != cudaSuccess) return r;
+    if (!make_dec_prob(b.p[0], pl, bits, cdt, pre, M, K, N, codes, scales, group, C, ws, Sp, M, 0))
+      return cudaErrorInvalidValue;
+  } else if (!make_dec_prob(b.p[0], pl, bits, cdt, A, M, K, N, codes, scales, group, C, ws)) {
     return cudaErrorInvalidValue;
+  }
   b.p[0].cta_begin = 0;
   b.nprob = 1;
   const int ctas = b.p[0].gx * pl.splits * pl.ktiles;
@@ -690,9 +898,18 @@ constexpr int kMaxBatch = 48;
 
 cudaError_t run_gemv_grouped(int adt, int cdt, int bits, const void* A, int K, int N,
                              const int64_t* offsets, const int32_t* groups, const void* const* codes,
-                             const void* const* scales, void* C, void* ws, size_t ws_per_expert,
+                             const void* const* scales, void* C, void* ws, int64_t T,
                              const int* experts, int nexp, cudaStream_t st) {
   static_assert(sizeof(DecBatch<kMaxBatch>) < 32000, "kernel parameter block limit");
+  // nibble-path experts read A'/S' pre-converted once for all T tokens
+  char* pre = reinterpret_cast<char*>(ws) + kCounterBytes;
+  char* Sp = pre + align256((size_t)T * K * 2);
+  bool any_nib = false;
+  for (int ii = 0; ii < nexp; ++ii) any_nib |= nib_of(bits, groups[experts[ii]]);
+  if (any_nib) {
+    cudaError_t r = launch_prep(adt, A, (int)T, K, pre, Sp, st);
+    if (r != cudaSuccess) return r;
+  }
   for (int cls = 0; cls < 4; ++cls) {
     const int mt = 1 + (cls >> 1);
     const bool sacc = cls & 1;
@@ -709,8 +926,10 @@ cudaError_t run_gemv_grouped(int adt, int cdt, int bits, const void* A, int K, i
       DecProb& d = b.p[b.nprob];
       const char* Ae = reinterpret_cast<const char*>(A) + (size_t)offsets[e] * K * 2;
       char* Ce = reinterpret_cast<char*>(C) + (size_t)offsets[e] * N * (cdt == FQ_FP32 ? 4 : 2);
-      void* wse = reinterpret_cast<char*>(ws) + (size_t)e * ws_per_expert;
-      if (!make_dec_prob(d, pl, bits, cdt, Ae, Me, K, N, codes[e], scales[e], groups[e], Ce, wse))
+      const bool nib = nib_of(bits, groups[e]);
+      const void* Ause = nib ? static_cast<const void*>(pre + (size_t)offsets[e] * K * 2) : static_cast<const void*>(Ae);
+      if (!make_dec_prob(d, pl, bits, cdt, Ause, Me, K, N, codes[e], scales[e], groups[e], Ce, ws,
+                         nib ? Sp : nullptr, (int)T, (int)offsets[e]))
         return cudaErrorInvalidValue;
       d.cta_begin = ctas;
       ctas += d.gx * d.splits * d.ktiles;

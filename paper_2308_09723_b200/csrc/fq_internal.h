@@ -21,7 +21,8 @@ struct GemvPlan {
   int klen;           // K elements per split (multiple of kchunk)
 };
 GemvPlan plan_gemv(int M, int K, int N, int bits, int group, int num_sms);
-size_t gemv_workspace_bytes(const GemvPlan& p, int M, int N);
+size_t gemv_workspace_bytes(const GemvPlan& p, int M, int K, int N, int bits, int group);
+size_t gemv_grouped_workspace_bytes(int64_t T, int K, int bits);
 cudaError_t run_gemv(const GemvPlan& p, int adt, int cdt, int bits, const void* A, int M, int K,
                      int N, const void* codes, const void* scales, int group, void* C, void* ws,
                      cudaStream_t st);
@@ -29,17 +30,18 @@ cudaError_t run_gemv(const GemvPlan& p, int adt, int cdt, int bits, const void* 
 // MoE batch of decode problems (experts with 1 <= M_e <= 16), one launch per kernel class.
 cudaError_t run_gemv_grouped(int adt, int cdt, int bits, const void* A, int K, int N,
                              const int64_t* offsets, const int32_t* groups, const void* const* codes,
-                             const void* const* scales, void* C, void* ws, size_t ws_per_expert,
+                             const void* const* scales, void* C, void* ws, int64_t T,
                              const int* experts, int nexp, cudaStream_t st);
 
-// Decode GEMM on tcgen05 (A4, M <= 16, group % 128 (int4) / 64 (int8) == 0).
+// Decode GEMM on tcgen05 (A4, M <= 16, group % 128 (int4) / 64 (int8) == 0); workspace = 64 KiB
+// counters + per-CTA split partials (dtc_workspace_bytes), zero-filled once.
 bool decode_tc_supported(int bits, int group, int M);
 size_t dtc_workspace_bytes(int M, int K, int N, int bits, int nsm);
 cudaError_t run_decode_tc(int adt, int cdt, int bits, const void* A, int M, int K, int N, const void* codes,
                           const void* scales, int group, void* C, void* ws, cudaStream_t st);
 cudaError_t run_decode_tc_grouped(int adt, int cdt, int bits, const void* A, int K, int N, const int64_t* offsets,
                                   const int32_t* groups, const void* const* codes, const void* const* scales,
-                                  void* C, const int* experts, int nexp, cudaStream_t st);
+                                  void* C, void* ws, const int* experts, int nexp, cudaStream_t st);
 
 // Large-M tensor-core GEMM (tcgen05 + TMEM, kernel A6).
 cudaError_t run_gemm_tc(int adt, int cdt, int bits, const void* A, int M, int K, int N, const void* codes,

@@ -15,7 +15,8 @@ from dataclasses import dataclass
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libfq.so")
+# FQ_LIB_PATH: diagnostics only (a variant built by build.build_variant, still in-tree)
+LIB_PATH = os.environ.get("FQ_LIB_PATH") or os.path.join(_PKG, "libfq.so")
 
 FQ_OK, FQ_ERR_INVALID_ARG, FQ_ERR_SHAPE, FQ_ERR_UNSUPPORTED, FQ_ERR_WORKSPACE, FQ_ERR_CUDA = range(6)
 FQ_BF16, FQ_FP16, FQ_FP32 = 0, 1, 2

@@ -82,6 +82,24 @@ def activations_bits(M: int, K: int, seed: int, dtype: str = "bf16", std: float 
     return gaussian_bits((M, K), std, seed, dtype)
 
 
+def wide_range_activations_bits(M: int, K: int, seed: int, dtype: str = "bf16",
+                                log2_lo: float = -60.0, log2_hi: float = 60.0,
+                                token_shift: int = 30) -> np.ndarray:
+    """A[M, K] with log-uniform magnitudes 2^U(log2_lo, log2_hi), random signs, and per-token
+    structure: token m's magnitudes are additionally shifted by a per-token power of two, every
+    4th token has one all-zero 128-column chunk, and one token is entirely zero."""
+    rng = np.random.default_rng(seed)
+    e = rng.uniform(log2_lo, log2_hi, size=(M, K))
+    e += rng.integers(-token_shift, token_shift + 1, size=(M, 1))
+    x = np.sign(rng.standard_normal((M, K))) * np.exp2(e)
+    for m in range(0, M, 4):
+        c = int(rng.integers(0, max(1, K // 128)))
+        x[m, c * 128:(c + 1) * 128] = 0.0
+    if M > 2:
+        x[M // 2] = 0.0
+    return _to_bits(x.astype(np.float32), dtype)
+
+
 def uniform_routing(E: int, tokens_per_expert: int) -> np.ndarray:
     """Expert offsets [E+1] for a uniform routing with `tokens_per_expert` tokens each."""
     return np.arange(E + 1, dtype=np.int64) * int(tokens_per_expert)

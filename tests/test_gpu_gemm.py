@@ -7,7 +7,7 @@ import pytest
 import torch
 
 from oracle import fq_oracle as O
-from synth import activations_bits, gaussian_bits, gaussian_with_outliers_bits
+from synth import activations_bits, gaussian_bits, gaussian_with_outliers_bits, wide_range_activations_bits
 from helpers import bits_to_torch, torch_to_f64
 
 pytestmark = pytest.mark.gpu
@@ -92,6 +92,21 @@ def test_dtypes(fq, adt, bits, cdt):
     _, C = run_case(fq, Wb, Ab, bits, 128, adt, cdt)
     Cr, D = oracle_ref(Wb, Ab, bits, 128, adt)
     assert O.rel_err(torch_to_f64(C), Cr, D) <= TOL
+
+
+@pytest.mark.parametrize("adt", ["bf16", "fp16"])
+@pytest.mark.parametrize("M", [1, 5, 16])
+def test_decode_activation_dynamic_range(fq, M, adt):
+    """Activations spanning ~2^-90..2^90 (bf16; fp16: its own range) with zero chunks and a zero
+    token: the decode kernel's internal fp16 re-encoding of bf16 activations (per-token, per-chunk
+    power-of-two scale) must stay within the tolerance of the exact result."""
+    lo, hi, shift = (-60.0, 60.0, 30) if adt == "bf16" else (-8.0, 6.0, 4)
+    K, N = 1024, 512
+    Wb = gaussian_bits((N, K), 0.02, 1234, "bf16")
+    Ab = wide_range_activations_bits(M, K, 4321 + M, adt, lo, hi, shift)
+    _, C = run_case(fq, Wb, Ab, 4, 128, adt, "fp32")
+    Cr, D = oracle_ref(Wb, Ab, 4, 128, adt)
+    assert O.rel_err(torch_to_f64(C), Cr, D) <= TOL  # D == 0 (zero token) requires C == 0 exactly
 
 
 @pytest.mark.parametrize("splits", [1, 2, 3, 7])
