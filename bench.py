@@ -28,6 +28,10 @@ import time
 
 import numpy as np
 
+# fq_gemm on the decode path launches fq::prep_acts_kernel (activation pre-conversion, M x K
+# elements) + fq::decode_kernel (A4/A5, split-K fixup fused)
+LAUNCHES_PER_GEMM = 2
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -258,26 +262,27 @@ def main():
         total_ms = e0.elapsed_time(e1)
         if world > 1:
             dist.barrier()
-        # per-launch durations of the same launches, bracketed individually (roofline + comm share)
+        # per-launch durations: each launch of the step repeated R times back to back between one
+        # pair of CUDA events on the launching stream (steady state, PDL overlap included)
         names = [f"FC1_M{M}" for M in M_SWEEP] + [f"FC2_M{M}" for M in M_SWEEP]
         per = {n: 0.0 for n in names}
         comm = 0.0
-        reps = max(1, args.steps // 10)
-        for _ in range(reps):
-            evs = []
-            for M in M_SWEEP:
-                for n, fn in ((f"FC1_M{M}", gemm1), (f"FC2_M{M}", gemm2), (f"AR_M{M}", reduce)):
-                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    a.record(stream)
+        reps = 20
+        evs = []
+        for M in M_SWEEP:
+            for n, fn in ((f"FC1_M{M}", gemm1), (f"FC2_M{M}", gemm2), (f"AR_M{M}", reduce)):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                for _ in range(reps):
                     fn(M)
-                    b.record(stream)
-                    evs.append((n, a, b))
-            torch.cuda.synchronize()
-            for n, a, b in evs:
-                if n.startswith("AR"):
-                    comm += a.elapsed_time(b)
-                else:
-                    per[n] += a.elapsed_time(b)
+                b.record(stream)
+                evs.append((n, a, b))
+        torch.cuda.synchronize()
+        for n, a, b in evs:
+            if n.startswith("AR"):
+                comm += a.elapsed_time(b)
+            else:
+                per[n] += a.elapsed_time(b)
         per = {n: v / reps for n, v in per.items()}
         comm /= reps
         if world > 1:
@@ -332,7 +337,7 @@ def main():
             traffic = json.load(f).get("decode_dram_bytes_per_step")
     roof = {"bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": round(achieved_gbs / peaks["hbm_gbs"], 4), "traffic": traffic,
-            "peak_source": peaks["source"], "kernel": "fq::decode_kernel (A4/A5)",
+            "peak_source": peaks["source"], "kernel": "fq::decode_kernel (A4/A5) + its fq::prep_acts_kernel (bracketed together)",
             "algorithmic_bytes_per_step_per_rank": step_bytes_rank,
             "per_launch_us": {n: round(v * 1e3, 2) for n, v in per.items()},
             "allreduce_us_per_step": round(comm * 1e3, 2)}
@@ -354,7 +359,7 @@ def main():
                        "parallelism": f"tp{world} (FC1 column-parallel, FC2 row-parallel + NCCL all-reduce)"},
             "clocks": clocks, "e2e": {"value": round(e2e_value, 4), "unit": UNIT,
                                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-            "gpu_launches": 2 * len(M_SWEEP) * args.steps, "roofline": roof}
+            "gpu_launches": LAUNCHES_PER_GEMM * 2 * len(M_SWEEP) * args.steps, "roofline": roof}
     if extras:
         line["extras"] = extras
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -24,6 +24,11 @@ int num_sms() {
   return v;
 }
 
+bool pdl_enabled() {
+  const char* e = std::getenv("FQ_PDL");
+  return !(e && e[0] == '0');
+}
+
 static bool valid_dtype(int d) { return d == FQ_BF16 || d == FQ_FP16 || d == FQ_FP32; }
 static bool valid_half(int d) { return d == FQ_BF16 || d == FQ_FP16; }
 

@@ -165,4 +165,13 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
                : "memory");
 }
 
+// ---- programmatic dependent launch (PDL) -----------------------------------------------------
+// griddep_wait: block until the grids this launch depends on have completed and their writes
+// are visible (no-op when launched without the PDL attribute).  griddep_launch_dependents: allow
+// the next kernel in the stream to be scheduled early (it still waits in its own griddep_wait).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 }  // namespace fq

@@ -265,7 +265,12 @@ __device__ __forceinline__ int swz64(int c, int R) { return c ^ ((R >> 1) & 3); 
 // DBG (diagnostics only, selected by FQ_DEC_DEBUG for bf16/int4/M<=8): 1 = no MMA (fake FADD
 // accumulate), 2 = no dequant (raw code words as MMA operands), 3 = consumers skip all compute.
 template <typename T, int BITS, int MT, bool SACC, int DBG, int MAXP>
-__global__ void __launch_bounds__(dec_threads<FQ_NIB && BITS == 4 && SACC>(), 2) decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
+// Register caps (two CTAs per SM fit up to 112 / 96 registers at 288 / 320 threads), set without
+// ptxas's launch_bounds heuristic.
+#ifndef FQ_DEC_NIB_MAXREG
+#define FQ_DEC_NIB_MAXREG 96  // measured: faster than 104 or 112 (which ptxas schedules worse)
+#endif
+__global__ void __maxnreg__((FQ_NIB && BITS == 4 && SACC) ? FQ_DEC_NIB_MAXREG : 96) decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
   using G = DecGeom<BITS>;
   using SG = DecStage<BITS, MT>;
   constexpr int KS = G::KS, SEG = G::SEG, KCH = G::KCH, CHUNKS = G::CHUNKS, PIECES = G::PIECES;
@@ -321,13 +326,10 @@ __global__ void __launch_bounds__(dec_threads<FQ_NIB && BITS == 4 && SACC>(), 2)
     if (lane == 0) {
       const uint64_t polw = policy_evict_first();
       const uint64_t pola = policy_evict_last();
-      int s = 0;
-      uint32_t ph = 0;
       // chunk c = kbeg/KCH + i (one chunk per stage) lies in scale group c / gm
       const int gm = SACC ? p.group / KCH : 1;
       int grem = SACC ? (kbeg / KCH) % gm : 0, gj = SACC ? (kbeg / KCH) / gm : 0;
-      for (int i = 0; i < nst; ++i) {
-        mbar_wait(&empty_bar[s], ph ^ 1);
+      auto issue_w = [&](int i, int s) {  // the stage's packed weights + scales (+ expect_tx)
         uint8_t* st = sbase + s * STAGE_BYTES;
         const int k0 = kbeg + i * KS;
         mbar_arrive_expect_tx(&full_bar[s], kStageW + (SACC ? SC_BYTES : 0) + (NIB ? RAW_BYTES + MT * 8 * 16 : 0));
@@ -341,6 +343,10 @@ __global__ void __launch_bounds__(dec_threads<FQ_NIB && BITS == 4 && SACC>(), 2)
             tma_load_2d(st + SC_OFS + bx2 * kWBoxRows * 2, &p.s, &full_bar[s], n0 + bx2 * kWBoxRows, gj, polw);
           if (++grem == gm) { grem = 0; ++gj; }
         }
+      };
+      auto issue_a = [&](int i, int s) {  // the stage's activations (+ per-chunk sums)
+        uint8_t* st = sbase + s * STAGE_BYTES;
+        const int k0 = kbeg + i * KS;
         if (NIB) {
           tma_load_2d(st + ACT_OFS, &p.a, &full_bar[s], k0, tok0, pola);
           tma_load_2d(st + SUM_OFS, &p.sm, &full_bar[s], tok0 * 4, k0 / KCH, pola);
@@ -348,8 +354,23 @@ __global__ void __launch_bounds__(dec_threads<FQ_NIB && BITS == 4 && SACC>(), 2)
           mbar_arrive_expect_tx(&raw_bar[s], RAW_BYTES);
           tma_load_2d(st + ACT_OFS, &p.a, &raw_bar[s], k0, tok0, pola);
         }
+      };
+      // Weights are constants: the first NSTG stages are requested before waiting for the grid
+      // this launch depends on (programmatic dependent launch: the activations may still be in
+      // flight from the previous kernel in the stream).
+      const int npre = min(nst, NSTG);
+      for (int i = 0; i < npre; ++i) issue_w(i, i);
+      griddep_wait();
+      for (int i = 0; i < npre; ++i) issue_a(i, i);
+      int s = npre % NSTG;
+      uint32_t ph = npre == NSTG ? 1u : 0u;
+      for (int i = npre; i < nst; ++i) {
+        mbar_wait(&empty_bar[s], ph ^ 1);
+        issue_w(i, s);
+        issue_a(i, s);
         if (++s == NSTG) { s = 0; ph ^= 1; }
       }
+      griddep_launch_dependents();
     }
     return;
   }
@@ -675,6 +696,8 @@ __global__ void __launch_bounds__(dec_threads<FQ_NIB && BITS == 4 && SACC>(), 2)
 template <typename T>
 __global__ void __launch_bounds__(128) prep_acts_kernel(const T* __restrict__ A, int ntok, int K,
                                                         __half* __restrict__ Ap, float* __restrict__ Sp) {
+  griddep_wait();  // A may be the output of the previous kernel in the stream
+  griddep_launch_dependents();
   const int chunks = K >> 7;
   const int hw = blockIdx.x * 8 + (threadIdx.x >> 4);
   const int l = threadIdx.x & 15;
@@ -757,8 +780,9 @@ GemvPlan plan_gemv(int M, int K, int N, int bits, int group, int nsm) {
     const double ctas = (double)gx * s * p.ktiles;
     const double waves = ctas / slots;
     const double eff = waves / std::ceil(waves);
-    // full waves first; a few waves smooth per-SM imbalance; fewer splits = less partial traffic
-    const double score = eff + 0.02 * std::min(waves, 4.0) - 0.003 * s * (M > 4 ? 2 : 1);
+    // full last wave first; then as few waves as possible (each CTA pays a pipeline fill) and
+    // few splits (partials + fixup).  Measured on B200 (OPT FC1/FC2): 1-2 full waves are best.
+    const double score = eff - 0.01 * waves - 0.002 * s;
     if (score > best + 1e-9) { best = score; best_s = s; }
   }
   int s = env_int("FQ_GEMV_SPLITS", best_s);
@@ -791,12 +815,11 @@ static cudaError_t launch_prep(int adt, const void* A, int ntok, int K, void* Ap
   const int blocks = (int)(((long long)ntok * (K / 128) + 7) / 8);
   if (blocks == 0) return cudaSuccess;
   if (adt == FQ_BF16)
-    prep_acts_kernel<__nv_bfloat16><<<blocks, 128, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(A), ntok, K,
-                                                            reinterpret_cast<__half*>(Ap), reinterpret_cast<float*>(Sp));
-  else
-    prep_acts_kernel<__half><<<blocks, 128, 0, st>>>(reinterpret_cast<const __half*>(A), ntok, K,
-                                                     reinterpret_cast<__half*>(Ap), reinterpret_cast<float*>(Sp));
-  return cudaGetLastError();
+    return launch_pdl(prep_acts_kernel<__nv_bfloat16>, blocks, 128, 0, st,
+                      reinterpret_cast<const __nv_bfloat16*>(A), ntok, K, reinterpret_cast<__half*>(Ap),
+                      reinterpret_cast<float*>(Sp));
+  return launch_pdl(prep_acts_kernel<__half>, blocks, 128, 0, st, reinterpret_cast<const __half*>(A), ntok, K,
+                    reinterpret_cast<__half*>(Ap), reinterpret_cast<float*>(Sp));
 }
 
 template <typename T, int BITS, int MT, bool SACC, int DBG, int MAXP>
@@ -809,8 +832,7 @@ static cudaError_t launch_dec(const DecBatch<MAXP>& b, int ctas, cudaStream_t st
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  kern<<<ctas, dec_threads<FQ_NIB && BITS == 4 && SACC>(), smem, st>>>(b);
-  return cudaGetLastError();
+  return launch_pdl(kern, ctas, dec_threads<FQ_NIB && BITS == 4 && SACC>(), smem, st, b);
 }
 
 template <int MAXP>

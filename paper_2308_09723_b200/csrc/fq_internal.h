@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 namespace fq {
 
 cudaError_t run_quantize(int wdt, int sdt, int bits, const void* W, int K, int N, int group,
@@ -51,6 +53,25 @@ cudaError_t run_gemm_tc_grouped(int adt, int cdt, int bits, const void* A, int K
                                 void* C, const int* experts, int nexp, cudaStream_t st);
 
 int num_sms();
+
+// Launch with the programmatic-stream-serialization attribute (PDL) unless FQ_PDL=0; the kernel
+// must call griddep_wait() before touching memory written by earlier kernels in the stream.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // 2-D TMA descriptor (CUtensorMap, 128 bytes, written to `tmap`).  elem_bytes 1/2/4 -> u8/bf16/f32.
 bool make_tmap_2d(void* tmap, const void* base, int elem_bytes, uint64_t inner, uint64_t outer,
