@@ -143,7 +143,7 @@ size_t fq_gemm_workspace_bytes(int64_t M, const fq_wdesc* d) {
   if (check_wdesc(d) != FQ_OK || M <= 0) return 0;
   if (use_tc_path(M)) return 256;
   if (decode_tc_supported(d->bits, d->group, (int)M))
-    return dtc_workspace_bytes((int)M, (int)d->K, (int)d->N, d->bits, num_sms());
+    return dtc_workspace_bytes(M, (int)d->K, num_sms());
   const GemvPlan p = plan_gemv((int)M, (int)d->K, (int)d->N, d->bits, d->group, num_sms());
   return gemv_workspace_bytes(p, (int)M, (int)d->K, (int)d->N, d->bits, d->group);
 }
@@ -161,7 +161,7 @@ fq_status fq_gemm(const void* A, int32_t adt, int64_t M, const fq_wdesc* d, cons
     return from_cuda(run_gemm_tc(adt, cdt, d->bits, A, (int)M, (int)d->K, (int)d->N, codes, scales,
                                  d->group, C, as_stream(stream)));
   if (decode_tc_supported(d->bits, d->group, (int)M)) {
-    const size_t need = dtc_workspace_bytes((int)M, (int)d->K, (int)d->N, d->bits, num_sms());
+    const size_t need = dtc_workspace_bytes(M, (int)d->K, num_sms());
     if (need > 65536 && (!ws || ws_bytes < need)) return FQ_ERR_WORKSPACE;
     return from_cuda(run_decode_tc(adt, cdt, d->bits, A, (int)M, (int)d->K, (int)d->N, codes, scales,
                                    d->group, C, ws, as_stream(stream)));
@@ -178,7 +178,7 @@ size_t fq_gemm_grouped_workspace_bytes(int64_t T, int32_t E, const fq_wdesc* d) 
   if (check_wdesc(d) != FQ_OK || T < 0) return 0;
   // tcgen05 decode experts: counters + per-CTA stream-K partials; mma.sync decode experts:
   // counters + the pre-converted activations of all T tokens (shared region, stream-ordered)
-  return std::max(dtc_workspace_bytes(16, (int)d->K, (int)d->N, d->bits, num_sms()),
+  return std::max(dtc_workspace_bytes(T, (int)d->K, num_sms()),
                   gemv_grouped_workspace_bytes(T, (int)d->K, d->bits));
 }
 
@@ -219,10 +219,11 @@ fq_status fq_gemm_grouped(const void* A, int32_t adt, int64_t T, const int64_t* 
                                                                                                  : small_mma)
         .push_back(e);
   if (!small_tc.empty()) {
-    if (!ws || ws_bytes < dtc_workspace_bytes(16, (int)d->K, (int)d->N, d->bits, num_sms()))
+    if (!ws || ws_bytes < dtc_workspace_bytes(T, (int)d->K, num_sms()))
       return FQ_ERR_WORKSPACE;
     cudaError_t r = run_decode_tc_grouped(adt, cdt, d->bits, A, (int)d->K, (int)d->N, offsets_host, groups_host,
-                                          codes_host, scales_host, C, ws, small_tc.data(), (int)small_tc.size(), st);
+                                          codes_host, scales_host, C, ws, T, small_tc.data(), (int)small_tc.size(),
+                                          st);
     if (r != cudaSuccess) return FQ_ERR_CUDA;
   }
   if (!small_mma.empty() && (!ws || ws_bytes < gemv_grouped_workspace_bytes(T, (int)d->K, d->bits)))

@@ -149,6 +149,13 @@ __device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
   asm volatile("ld.shared.u16 %0, [%1];" : "=h"(r) : "r"(addr));
   return r;
 }
+// one 16-bit value of dtype T from shared memory, as float
+template <typename T>
+__device__ __forceinline__ float lds_f16x(uint32_t addr) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+  return Dt<T>::to_f(*reinterpret_cast<T*>(&v));
+}
 __device__ __forceinline__ float lds_f32(uint32_t addr) {
   float r;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(r) : "r"(addr));

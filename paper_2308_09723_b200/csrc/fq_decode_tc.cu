@@ -1,34 +1,36 @@
 // fq_decode_tc.cu — kernel A4 on the 5th-gen tensor cores: the decode (M <= 16) fused dequant GEMM
-// with the MMA issued by tcgen05 instead of the legacy warp-level mma.sync (whose issue slots and
-// register-fragment traffic compete with the dequant ALU work on the same SM sub-partitions).
+// with the MMA issued by tcgen05 from one thread, so the SM sub-partitions spend their issue slots
+// on the dequantization alone (the legacy mma.sync kernel in fq_gemv.cu also spends them on HMMA,
+// fragment loads and, for 9 <= M <= 16, a second 8-token MMA per weight).
 //
-// C[m,n] = sum_k A[m,k] * q[n,k] * s[k/g, n]   (§4.1), requires group % KS == 0
-// (KS = 128 for int4, 64 for int8: one scale per row per stage; other groups use the mma.sync
-// kernel in fq_gemv.cu).  Decode streams every packed weight byte once, so the design goal
-// is to keep >= 150 KB of weight loads in flight per SM and never let compute hold a stage.
+// C[m,n] = sum_k A[m,k] * q[n,k] * s[k/g, n]   (§4.1).  Decode streams every packed
+// weight byte once: the kernel is built to keep the TMA streaming at HBM speed.
 //
-// One persistent CTA per SM; the (tile, k-stage) space of all problems of the launch (one matrix,
-// or every expert of a MoE batch) is split into equal contiguous stage ranges, one per CTA
-// ("stream-K"): no wave quantisation, and the TMA runs ahead across tile boundaries.  Tiles cut by
-// a range boundary are combined by the last-arriving contributor in CTA order (deterministic).
+// Stream-K: 2 persistent CTAs per SM split the launch's linear (tile, k-stage) space -- all tiles of
+// one matrix, or of every expert of a MoE batch -- into equal contiguous ranges; a tile cut by a
+// range boundary is finished by its last-arriving contributor, which sums the fp32 partials in CTA
+// order (deterministic).  No wave quantisation, one pipeline fill per CTA.
 //
-// Tile = 256 weight rows (two UMMA M=128 halves, TMEM lanes) x 16 tokens (UMMA N).  Warps:
-//   0       TMA: per stage packed codes [256 rows x 64 B] (SWIZZLE_64B), raw activations
-//           [M x KS], the stage's 256 scales; SSTAGES-deep ring.
-//   1       TMEM allocation + single-thread tcgen05.mma (kind::f16, A = dequantized weights in
-//           TMEM, B = activations in shared memory (SWIZZLE_128B K-major), D = accumulator slice).
-//   2       stager: raw activations -> UMMA B tile in the per-word (0,4),(1,5),(2,6),(3,7) k-order
-//           the int4 unpack produces; per-token sums (code-offset correction) and the fp32 scales
-//           -> a fold-data ring.  Releases the smem stage as soon as it has read it.
-//   3..10   dequant: thread = one weight row; LOP3 magic unpack (codes + offset) -> tcgen05.st into
-//           a TMEM A ring.  Releases the smem stage right after its shared-memory loads.
-//   11..18  fold: per stage tcgen05.ld of the accumulator (NTF token columns), remove the offset,
-//           scale in fp32, accumulate in registers; per tile segment the epilogue writes C or a
-//           split partial.
+// Tile = 128 weight rows (UMMA M, TMEM lanes) x NT = 16 tokens (UMMA N).  Stage = 64 packed bytes
+// per row (k = 128 int4 / 64 int8) -- group % 128 == 0, so one scale per row per stage.
+//   warp 0     TMA: codes [128 rows x 64 B] (SWIZZLE_64B) + activations A' [NT x k] (SWIZZLE_128B,
+//              the UMMA K-major layout) into the stage ring; the stage's 128 scales and per-token
+//              2^-e factors into a fold-data ring.
+//   warp 1     TMEM allocation; one thread issues tcgen05.mma kind::f16 (A = codes in TMEM, B = A' in
+//              shared memory, D = a per-stage fp32 accumulator slot), tcgen05.commit releases the
+//              stage, the A slot and signals the accumulator slot.
+//   warps 2-9  dequant: thread = weight row (TMEM lane) x half of the stage's k.  Codes become EXACT
+//              small integers in fp16 (LOP3 magic + one HSUB2/HFMA2 per pair, no scale applied) and
+//              go to TMEM with tcgen05.st.  Two stages later the same warps fold that stage's
+//              accumulator (tcgen05.ld): acc[tok] += s[row] * 2^-e[tok] * part[tok] (fp32).
+// Activations: the prep kernel (fq_gemv.cu, MODE 1/2) converts A to fp16 scaled by 2^e per
+// (token, 128-k chunk) -- exact for bf16 inputs -- in the k order the unpack produces:
+//   int4 word (k..k+7) -> TMEM columns (k,k+4),(k+1,k+5),(k+2,k+6),(k+3,k+7); int8 natural pairs.
+// The integer partials of a stage are exact products q * a' summed in fp32; the scale is applied
+// in fp32 (R13), so the result is within the 2e-3 gate with a wide margin.
 #include <cuda.h>
 
 #include <algorithm>
-#include <cstdio>
 #include <cstdlib>
 
 #include "fq_common.cuh"
@@ -39,499 +41,449 @@ namespace fq {
 namespace dtc {
 using namespace tc5;
 
-constexpr int ROWS = 256;   // weight rows per tile (2 x UMMA M=128)
-constexpr int NT = 16;      // UMMA N (tokens); M <= 16
-constexpr int NB = 4;       // B-tile ring
-constexpr int ACC = 4;      // accumulator ring (TMEM)
-constexpr int FD = NB + ACC;  // fold-data ring (token sums + scales)
-constexpr int kThreads = 32 * 19;
-constexpr int kTmemCols = 512;
-constexpr int kSmemBudget = 232448 - 1024 - 1024;  // 227 KB opt-in minus alignment slack + statics
+constexpr int BM = 128;             // weight rows per tile
+constexpr int WB = 64;              // packed bytes per row per stage
+constexpr int W_BYTES = BM * WB;    // 8 KB
+constexpr int kDqWarps = 4;         // one per TMEM lane quarter (warps 3..6)
+constexpr int kDq0 = 3;             // first dequant warp
+constexpr int kThreads = 32 * (kDq0 + kDqWarps);
+constexpr int kTmemCols = 256;      // two CTAs per SM share the 512 columns
+#ifndef FQ_DTC_AS
+#define FQ_DTC_AS 3
+#endif
+constexpr int AS = FQ_DTC_AS;       // TMEM A slots
+constexpr int AC = 4;               // TMEM accumulator slots
+#ifndef FQ_DTC_LAG
+#define FQ_DTC_LAG 2
+#endif
+constexpr int LAG = FQ_DTC_LAG;     // the fold trails the dequant by LAG stages
+constexpr int kMaxStages = 12;
+constexpr int kSmemBudget = 110 * 1024;  // dynamic smem per CTA (2 CTAs per SM)
+#ifndef FQ_DTC_DBG
+#define FQ_DTC_DBG 0  // diagnostics only: 1 = no MMA, 2 = no unpack / tcgen05.st, 4 = no tcgen05.ld,
+                      // 8 = MMA issuer ignores the A / accumulator barriers, 16 = dequant ignores A-slot reuse
+#endif
 
-template <int BITS>
+template <int BITS, int NT>
 struct G {
-  static constexpr int WB = 64;                          // packed bytes per row per stage
-  static constexpr int KS = WB * 8 / BITS;               // K per stage (= one scale chunk): 128 / 64
-  static constexpr int W_BYTES = ROWS * WB;              // 16 KB
-  static constexpr int RAW_OFS = W_BYTES;
-  static constexpr int RAW_BYTES = NT * KS * 2;          // up to 16 token rows
-  static constexpr int SC_OFS = RAW_OFS + RAW_BYTES;
-  static constexpr int SC_BYTES = ROWS * 2;
-  static constexpr int STAGE = ((SC_OFS + SC_BYTES + 1023) / 1024) * 1024;
-  static constexpr int B_BYTES = NT * KS * 2;            // KS/64 SW128 atoms of 16 rows x 128 B
-  static constexpr int FD_BYTES = (NT + ROWS) * 4;       // token sums + fp32 scales
-  static constexpr int SSTAGES = (kSmemBudget - NB * B_BYTES - FD * FD_BYTES) / STAGE;
-  static constexpr int B_RING = SSTAGES * STAGE;         // 1024-aligned
-  static constexpr int FD_RING = B_RING + NB * B_BYTES;
-  static constexpr int SMEM = FD_RING + FD * FD_BYTES + 1024;
-  static constexpr int A_COLS = KS / 2;                  // TMEM columns per half per A slot
-  static constexpr int ASTAGES = (kTmemCols - ACC * 2 * NT) / KS > 4 ? 4 : (kTmemCols - ACC * 2 * NT) / KS;
-  static constexpr int ACC_COL = ASTAGES * KS;           // accumulator slices after the A ring
-  static_assert(SSTAGES >= 4 && ACC_COL + ACC * 2 * NT <= kTmemCols, "resources");
+  static constexpr int KS = WB * 8 / BITS;            // k per stage: 128 / 64
+  static constexpr int ATOMS = KS / 64;               // SW128 atoms (64 fp16 of k) of the B tile
+  static constexpr int ATOM_BYTES = NT * 128;
+  static constexpr int B_BYTES = ATOMS * ATOM_BYTES;  // activation tile of one stage (1024-aligned)
+  static constexpr int SC_OFS = W_BYTES;              // the stage's 128 scales (activation dtype)
+  static constexpr int SC_BYTES = BM * 2;
+  static constexpr int WSTAGE = ((SC_OFS + SC_BYTES + 1023) / 1024) * 1024;
+  static constexpr int NB = 6;                        // activation ring depth
+  static constexpr int NS0 = (kSmemBudget - 1024 - NB * B_BYTES) / WSTAGE;
+  static constexpr int NSTAGE = NS0 > kMaxStages ? kMaxStages : NS0;   // codes ring depth
+  static constexpr int B_RING = NSTAGE * WSTAGE;
+  static constexpr int SMEM = B_RING + NB * B_BYTES + 1024;
+  static constexpr int A_COLS = KS / 2;               // TMEM columns of one A slot
+  static constexpr int ACC_COL = AS * A_COLS;
+  static constexpr int TXW = W_BYTES + SC_BYTES;
+  static_assert(NSTAGE >= 4 && ACC_COL + AC * NT <= kTmemCols && AC > LAG, "resources");
 };
 
-struct DtcProb {
-  CUtensorMap w, a, s;
+struct Prob {
+  CUtensorMap w;   // codes [N][K*b/8] u8, box [128 rows][64 B], SWIZZLE_64B
+  CUtensorMap a;   // A' [M][K] fp16, box [NT rows][64], SWIZZLE_128B (rows >= M zero-filled)
+  CUtensorMap s;   // scales [G][N], box [1][128]
+  const float* inv;  // per-token 2^-e of A' (this problem's tokens)
   void* C;
   int M, K, N, group, cdt;
   int gx, nk;                    // tiles, stages per tile
-  int stage_begin, tile_begin;   // offsets in the launch's linear stage / tile space
+  int stage_begin, tile_begin;   // offsets in the launch's linear stage / tile spaces
 };
 template <int MAXP>
-struct DtcBatch {
-  DtcProb p[MAXP];
+struct Batch {
+  Prob p[MAXP];
   int nprob;
   int total_stages;
-  float* ws;      // split partials [ctas][2][NT][ROWS]
-  int* counters;  // per global tile (self-resetting)
-  int dbg;        // diagnostics only (FQ_DTC_DBG bits): 1 dequant, 2 fold, 4 stager, 8 mma, 16 TMEM st, 32 all tensor-core work skipped
+  float* ws;      // stream-K partials [ctas][2][16][BM] fp32
+  int* counters;  // per global tile arrival counters (self-resetting)
 };
 
-// Linear stage cursor over the launch's problems (all roles walk the same sequence).
+// Linear stage cursor (every role walks the same sequence).
 struct Cur {
   int p, tile, kidx;
 };
 template <int MAXP>
-__device__ __forceinline__ void cur_locate(const DtcBatch<MAXP>& b, int s, Cur& c) {
+__device__ __forceinline__ void cur_locate(const Batch<MAXP>& b, int g, Cur& c) {
   int p = 0;
-  while (p + 1 < b.nprob && s >= b.p[p + 1].stage_begin) ++p;
-  const int local = s - b.p[p].stage_begin;
+  while (p + 1 < b.nprob && g >= b.p[p + 1].stage_begin) ++p;
+  const int local = g - b.p[p].stage_begin;
   c.p = p;
   c.tile = local / b.p[p].nk;
   c.kidx = local - c.tile * b.p[p].nk;
 }
 template <int MAXP>
-__device__ __forceinline__ void cur_next(const DtcBatch<MAXP>& b, Cur& c) {
+__device__ __forceinline__ void cur_next(const Batch<MAXP>& b, Cur& c) {
   if (++c.kidx == b.p[c.p].nk) {
     c.kidx = 0;
     if (++c.tile == b.p[c.p].gx) { c.tile = 0; ++c.p; }
   }
 }
-__device__ __forceinline__ int range_begin(int T, int P, int c) { return (int)((long long)T * c / P); }
-__device__ __forceinline__ int cta_of(int T, int P, int x) {
+__host__ __device__ __forceinline__ int range_begin(int T, int P, int c) { return (int)((long long)T * c / P); }
+__device__ __forceinline__ int cta_of(int T, int P, int x) {  // CTA whose range holds stage x
   int c = (int)((long long)x * P / T);
   while (c + 1 < P && range_begin(T, P, c + 1) <= x) ++c;
   while (c > 0 && range_begin(T, P, c) > x) --c;
   return c;
 }
 
-template <typename T, int BITS>
-__device__ __forceinline__ void unpack_word(uint32_t w, uint32_t* q);
-template <>
-__device__ __forceinline__ void unpack_word<__nv_bfloat16, 4>(uint32_t w, uint32_t* q) {
-  // pairs (k,k+4),(k+1,k+5),(k+2,k+6),(k+3,k+7) as bf16 (128 + (n ^ 8)) = code + 136
-  q[0] = lop3_and_xor(w, 0x000F000Fu, 0x43084308u);
-  q[1] = lop3_and_xor(__umulhi(w, 1u << 28), 0x000F000Fu, 0x43084308u);
-  q[2] = lop3_and_xor(w >> 8, 0x000F000Fu, 0x43084308u);
-  q[3] = lop3_and_xor(__umulhi(w, 1u << 20), 0x000F000Fu, 0x43084308u);
+__device__ __forceinline__ uint32_t hsub2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
 }
-template <>
-__device__ __forceinline__ void unpack_word<__half, 4>(uint32_t w, uint32_t* q) {
-  q[0] = lop3_and_xor(w, 0x000F000Fu, 0x64086408u);  // fp16 1024 + (n ^ 8) = code + 1032
-  q[1] = lop3_and_xor(__umulhi(w, 1u << 28), 0x000F000Fu, 0x64086408u);
-  q[2] = lop3_and_xor(w >> 8, 0x000F000Fu, 0x64086408u);
-  q[3] = lop3_and_xor(__umulhi(w, 1u << 20), 0x000F000Fu, 0x64086408u);
+__device__ __forceinline__ uint32_t hfma2(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
 }
-template <>
-__device__ __forceinline__ void unpack_word<__half, 8>(uint32_t w, uint32_t* q) {
-  const uint32_t u = w ^ 0x80808080u;  // natural pairs, fp16 1024 + (q + 128) = code + 1152
-  q[0] = prmt(u, 0x64646464u, 0x4140u);
-  q[1] = prmt(u, 0x64646464u, 0x4342u);
+// int4 word (k..k+7) -> fp16 pairs (k,k+4),(k+1,k+5),(k+2,k+6),(k+3,k+7), exact codes q.
+//   even: (w & 0x000F000F) ^ 0x6408 = 1024 + (n ^ 8) = 1032 + q          -> - 1032
+//   odd:  (w & 0x00F000F0) ^ 0x6480 = 1024 + 16 (n ^ 8) = 1152 + 16 q   -> / 16 - 72 (one FMA)
+__device__ __forceinline__ void i4_exact(uint32_t w, uint32_t* q) {
+  const uint32_t w8 = w >> 8;
+  q[0] = hsub2(lop3_and_xor(w, 0x000F000Fu, 0x64086408u), 0x64086408u);
+  q[1] = hfma2(lop3_and_xor(w, 0x00F000F0u, 0x64806480u), 0x2C002C00u, 0xD480D480u);
+  q[2] = hsub2(lop3_and_xor(w8, 0x000F000Fu, 0x64086408u), 0x64086408u);
+  q[3] = hfma2(lop3_and_xor(w8, 0x00F000F0u, 0x64806480u), 0x2C002C00u, 0xD480D480u);
 }
-template <>
-__device__ __forceinline__ void unpack_word<__nv_bfloat16, 8>(uint32_t w, uint32_t* q) {
-  const uint32_t u = w ^ 0x80808080u;  // natural pairs, exact codes (offset removed in fp32)
-  float f[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) f[i] = __uint_as_float(prmt(u, 0x4B000000u, 0x7440u + i)) - 8388736.0f;
-  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(q[0]) : "f"(f[1]), "f"(f[0]));
-  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(q[1]) : "f"(f[3]), "f"(f[2]));
+// int8 word (k..k+3) -> natural fp16 pairs (k,k+1),(k+2,k+3), exact codes: 1024 + (q + 128) - 1152.
+__device__ __forceinline__ void i8_exact(uint32_t w, uint32_t* q) {
+  const uint32_t u = w ^ 0x80808080u;
+  q[0] = hsub2(prmt(u, 0x64646464u, 0x4140u), 0x64806480u);
+  q[1] = hsub2(prmt(u, 0x64646464u, 0x4342u), 0x64806480u);
 }
-template <typename T, int BITS> struct Off { static constexpr float v = 0.f; };
-template <> struct Off<__nv_bfloat16, 4> { static constexpr float v = 136.f; };
-template <> struct Off<__half, 4> { static constexpr float v = 1032.f; };
-template <> struct Off<__half, 8> { static constexpr float v = 1152.f; };
 
-// FQ_DTC_PROF (diagnostics build only): per-warp cycles spent in each barrier wait, printed by
-// CTA 0 at exit.
-#ifndef FQ_DTC_PROF
-#define FQ_DTC_PROF 0
-#endif
-#if FQ_DTC_PROF
-#define DTC_PW(k, stmt)                 \
-  {                                     \
-    const long long t0_ = clock64();    \
-    stmt;                               \
-    prof_[k] += clock64() - t0_;        \
-  }
-#else
-#define DTC_PW(k, stmt) stmt;
-#endif
-
-template <typename T, int BITS, int MAXP, int NTF>
-__global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const __grid_constant__ DtcBatch<MAXP> batch) {
-  // NTF: token columns folded per stage (compile-time bucket >= max M of the launch)
-  using Gm = G<BITS>;
-  constexpr int KS = Gm::KS, SST = Gm::SSTAGES, AST = Gm::ASTAGES;
-  constexpr float OFF = Off<T, BITS>::v;
+template <typename T, int BITS, int NT, int MAXP>
+__global__ void __launch_bounds__(kThreads, 2) decode_tc_kernel(const __grid_constant__ Batch<MAXP> b) {
+  using Gm = G<BITS, NT>;
+  constexpr int NSTAGE = Gm::NSTAGE, KS = Gm::KS;
   extern __shared__ __align__(1024) uint8_t dsmem[];
-  __shared__ __align__(8) uint64_t full_bar[SST], sfree[SST];
-  __shared__ __align__(8) uint64_t bready[NB], bfree[NB];
-  __shared__ __align__(8) uint64_t aready[AST], afree[AST];
-  __shared__ __align__(8) uint64_t accfull[ACC], accfree[ACC];
-  __shared__ __align__(8) uint64_t fdfree[FD];
-  __shared__ uint32_t tmem_base_sh;
+  __shared__ __align__(8) uint64_t full_bar[kMaxStages], empty_bar[kMaxStages];
+  __shared__ __align__(8) uint64_t bfull_bar[Gm::NB], bempty_bar[Gm::NB];
+  __shared__ __align__(8) uint64_t afull_bar[AS], aempty_bar[AS], cfull_bar[AC], cempty_bar[AC];
+  __shared__ uint32_t tmem_sh;
   __shared__ int s_last;
   uint8_t* sbase = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsmem) + 1023) & ~uintptr_t(1023));
-  const uint32_t sb = smem_u32(sbase);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int P = gridDim.x, cta = blockIdx.x;
-  const int TS = batch.total_stages;
-  const int b0 = range_begin(TS, P, cta), b1 = range_begin(TS, P, cta + 1);
-  const int nst = b1 - b0;
-  const int dbg = batch.dbg;
-#if FQ_DTC_PROF
-  long long prof_[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-  const long long tstart_ = clock64();
-#endif
+  const int TS = b.total_stages, P = gridDim.x;
+  const int beg = range_begin(TS, P, blockIdx.x), end = range_begin(TS, P, blockIdx.x + 1);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < SST; ++s) {
+    for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&sfree[s], 1 + 8);  // stager + 8 dequant warps
+      mbar_init(&empty_bar[s], kDqWarps);  // dequant warps (codes + scales read)
     }
-    for (int b = 0; b < NB; ++b) {
-      mbar_init(&bready[b], 1);
-      mbar_init(&bfree[b], 1);
+    for (int s = 0; s < Gm::NB; ++s) {
+      mbar_init(&bfull_bar[s], 1);
+      mbar_init(&bempty_bar[s], 1);        // MMA commit (activation tile read)
     }
-    for (int a = 0; a < AST; ++a) {
-      mbar_init(&aready[a], 8);    // one arrival per dequant warp
-      mbar_init(&afree[a], 1);
+    for (int i = 0; i < AS; ++i) {
+      mbar_init(&afull_bar[i], kDqWarps);
+      mbar_init(&aempty_bar[i], 1);
     }
-    for (int c = 0; c < ACC; ++c) {
-      mbar_init(&accfull[c], 2);   // tcgen05.commit + the MMA thread's release arrival
-      mbar_init(&accfree[c], 8);   // one arrival per fold warp
+    for (int i = 0; i < AC; ++i) {
+      mbar_init(&cfull_bar[i], 1);
+      mbar_init(&cempty_bar[i], kDqWarps);
     }
-    for (int f = 0; f < FD; ++f) mbar_init(&fdfree[f], 8);
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(&tmem_base_sh, kTmemCols);
+  if (warp == 1) tmem_alloc(&tmem_sh, kTmemCols);
   fence_before();
   __syncthreads();
   fence_after();
-  const uint32_t tmem = tmem_base_sh;
+  const uint32_t tmem = tmem_sh;
+  const uint32_t sb = smem_u32(sbase);
 
   if (warp == 0) {
-    // ------------------------------------------------------------------ TMA producer
-    if (lane == 0 && nst > 0) {
-      for (int q = 0; q < batch.nprob; ++q) {
-        prefetch_tmap(&batch.p[q].w);
-        prefetch_tmap(&batch.p[q].a);
-        prefetch_tmap(&batch.p[q].s);
-      }
-      const uint64_t polw = policy_evict_first();
-      const uint64_t pola = policy_evict_last();
-      Cur cur;
-      cur_locate(batch, b0, cur);
+    // ------------------------------------------------------------------------- TMA: codes + scales
+    if (lane == 0) {
+      const uint64_t pol_w = policy_evict_first();
+      Cur c;
+      cur_locate(b, beg, c);
       int s = 0;
       uint32_t ph = 0;
-      for (int i = 0; i < nst; ++i) {
-        const DtcProb& p = batch.p[cur.p];
-        DTC_PW(0, mbar_wait(&sfree[s], ph ^ 1))
-        uint8_t* st = sbase + s * Gm::STAGE;
-        const int k0 = cur.kidx * KS, n0 = cur.tile * ROWS;
-        mbar_arrive_expect_tx(&full_bar[s], Gm::W_BYTES + p.M * KS * 2 + Gm::SC_BYTES);
-        tma_load_2d(st, &p.w, &full_bar[s], k0 * BITS / 8, n0, polw);
-        tma_load_2d(st + Gm::RAW_OFS, &p.a, &full_bar[s], k0, 0, pola);
-        tma_load_2d(st + Gm::SC_OFS, &p.s, &full_bar[s], n0, k0 / p.group, polw);
-        if (++s == SST) { s = 0; ph ^= 1; }
-        cur_next(batch, cur);
+      for (int g = beg; g < end; ++g) {
+        const Prob& p = b.p[c.p];
+        mbar_wait(&empty_bar[s], ph ^ 1);
+        uint8_t* st = sbase + s * Gm::WSTAGE;
+        const int k0 = c.kidx * KS;
+        mbar_arrive_expect_tx(&full_bar[s], Gm::TXW);
+        tma_load_2d(st, &p.w, &full_bar[s], k0 * BITS / 8, c.tile * BM, pol_w);
+        tma_load_2d(st + Gm::SC_OFS, &p.s, &full_bar[s], c.tile * BM, k0 / p.group, pol_w);
+        cur_next(b, c);
+        if (++s == NSTAGE) { s = 0; ph ^= 1; }
       }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------------ MMA issuer (whole warp,
-    // one elected lane issues; operands are warp-uniform)
-    constexpr uint32_t idesc = idesc_f16<T, 128, NT>();
-    int b = 0, a = 0, c = 0;
-    uint32_t bph = 0, aph = 0, cph = 0;
-    for (int i = 0; i < nst; ++i) {
-      DTC_PW(1, mbar_wait(&bready[b], bph))
-      DTC_PW(2, mbar_wait(&aready[a], aph))
-      DTC_PW(3, mbar_wait(&accfree[c], cph ^ 1))
-      fence_after();
-      if (dbg & 32) {  // diagnostics: no tensor-core work at all, plain arrivals
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&afree[a]);
-          mbar_arrive(&bfree[b]);
-          mbar_arrive(&accfull[c]);
-        }
-      } else {
-        const uint64_t bdesc = sw128_desc(sb + Gm::B_RING + b * Gm::B_BYTES);
-        const uint32_t dcol = tmem + Gm::ACC_COL + c * 2 * NT, acol = tmem + a * KS;
-        if (dbg & 8) {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) mma_ts_elect(dcol + h * NT, acol + h * Gm::A_COLS, bdesc, idesc, 0u);
-        } else {
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int kk = 0; kk < KS / 16; ++kk)
-              mma_ts_elect(dcol + h * NT, acol + h * Gm::A_COLS + kk * 8,
-                           bdesc + (uint64_t)((((kk >> 2) * 2048) + (kk & 3) * 32) >> 4), idesc, kk != 0);
-        }
-        mma_commit_elect(&afree[a]);
-        mma_commit_elect(&bfree[b]);
-        mma_commit_elect(&accfull[c]);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&accfull[c]);  // release: orders the stager's fold data (acquired via bready)
-      if (++b == NB) { b = 0; bph ^= 1; }
-      if (++a == AST) { a = 0; aph ^= 1; }
-      if (++c == ACC) { c = 0; cph ^= 1; }
     }
   } else if (warp == 2) {
-    // ------------------------------------------------------------------ activation stager
-    // raw [M tokens][KS] natural order -> B tile element (tok, k) in SW128 K-major atoms of 64 k
-    constexpr int PPT = KS / 8;                    // 8-element pieces per token (one chunk)
-    constexpr int NPW = NT * PPT / 32;             // pieces per lane per stage (all 16 tokens)
-    Cur cur;
-    cur_locate(batch, b0, cur);
-    int s = 0, b = 0, f = 0;
-    uint32_t ph = 0, bph = 0, fph = 0;
-    for (int i = 0; i < nst; ++i) {
-      const int mloc = batch.p[cur.p].M;
-      DTC_PW(4, mbar_wait(&full_bar[s], ph))
-      const uint32_t st = sb + s * Gm::STAGE;
-      uint4 v[NPW];
+    // ------------------------------------------------------------------------- TMA: activations
+    if (lane == 0) {
+      const uint64_t pol_a = policy_evict_last();
+      griddep_wait();  // A' comes from the prep kernel (programmatic dependent launch)
+      Cur c;
+      cur_locate(b, beg, c);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int g = beg; g < end; ++g) {
+        const Prob& p = b.p[c.p];
+        mbar_wait(&bempty_bar[s], ph ^ 1);
+        uint8_t* bt = sbase + Gm::B_RING + s * Gm::B_BYTES;
+        const int k0 = c.kidx * KS;
+        mbar_arrive_expect_tx(&bfull_bar[s], Gm::B_BYTES);
 #pragma unroll
-      for (int j = 0; j < NPW; ++j)
-        if ((32 * j) / PPT < mloc) v[j] = lds128(st + Gm::RAW_OFS + (lane + 32 * j) * 16);
-      const uint2 sv = lds64(st + Gm::SC_OFS + lane * 16);
-      const uint2 sv2 = lds64(st + Gm::SC_OFS + lane * 16 + 8);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sfree[s]);  // stage fully read by this warp
-      DTC_PW(5, mbar_wait(&bfree[b], bph ^ 1))
-      DTC_PW(6, mbar_wait(&fdfree[f], fph ^ 1))
-      const uint32_t bt = sb + Gm::B_RING + b * Gm::B_BYTES;
-      float* fdp = reinterpret_cast<float*>(sbase + Gm::FD_RING + f * Gm::FD_BYTES);
-#pragma unroll
-      for (int j = 0; j < NPW; ++j) {
-        if ((dbg & 4) || (32 * j) / PPT >= mloc) continue;  // warp-uniform: tokens >= M not staged
-        const int pc = lane + 32 * j;
-        const int tok = pc / PPT, kl = (pc % PPT) * 8;
-        uint4 x = v[j];
-        if (OFF != 0.f) {
-          float sum = 0.f;
-          const uint32_t vv[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            if (Dt<T>::id == FQ_BF16) {
-              sum += __uint_as_float(vv[e] << 16) + __uint_as_float(vv[e] & 0xFFFF0000u);
-            } else {
-              const float2 ff = __half22float2(*reinterpret_cast<const __half2*>(&vv[e]));
-              sum += ff.x + ff.y;
-            }
-          }
-#pragma unroll
-          for (int o = PPT / 2; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-          if ((lane % PPT) == 0) fdp[tok] = sum;
-        }
-        if (BITS == 4)
-          x = make_uint4(prmt(x.x, x.z, 0x5410u), prmt(x.x, x.z, 0x7632u), prmt(x.y, x.w, 0x5410u),
-                         prmt(x.y, x.w, 0x7632u));
-        const int atom = kl >> 6, chunk = (kl & 63) >> 3;
-        sts128(bt + atom * 2048 + tok * 128 + ((chunk ^ (tok & 7)) << 4), x);
+        for (int a = 0; a < Gm::ATOMS; ++a)
+          tma_load_2d(bt + a * Gm::ATOM_BYTES, &p.a, &bfull_bar[s], k0 + 64 * a, 0, pol_a);
+        cur_next(b, c);
+        if (++s == Gm::NB) { s = 0; ph ^= 1; }
       }
-      {  // the stage's 256 scales -> fp32 (lane handles rows 8*lane .. 8*lane+7)
-        const uint32_t h[8] = {sv.x & 0xFFFFu, sv.x >> 16, sv.y & 0xFFFFu, sv.y >> 16,
-                               sv2.x & 0xFFFFu, sv2.x >> 16, sv2.y & 0xFFFFu, sv2.y >> 16};
-        float sc[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const unsigned short hv = (unsigned short)h[e];
-          sc[e] = Dt<T>::to_f(*reinterpret_cast<const T*>(&hv));
-        }
-        const uint32_t fa = smem_u32(fdp + NT + lane * 8);
-        sts128(fa, make_uint4(__float_as_uint(sc[0]), __float_as_uint(sc[1]), __float_as_uint(sc[2]),
-                              __float_as_uint(sc[3])));
-        sts128(fa + 16, make_uint4(__float_as_uint(sc[4]), __float_as_uint(sc[5]), __float_as_uint(sc[6]),
-                                   __float_as_uint(sc[7])));
-      }
-      fence_proxy_async_smem();  // generic-proxy B-tile stores -> visible to the tensor core
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bready[b]);
-      if (++s == SST) { s = 0; ph ^= 1; }
-      if (++b == NB) { b = 0; bph ^= 1; }
-      if (++f == FD) { f = 0; fph ^= 1; }
-      cur_next(batch, cur);
+      griddep_launch_dependents();
     }
-  } else if (warp < 11) {
-    // ------------------------------------------------------------------ dequant -> TMEM
-    const int quarter = warp & 3;             // TMEM lane quarter this warp may access
-    const int half = (warp - 3) >> 2;         // UMMA M half (rows 0..127 / 128..255)
-    const int row = half * 128 + quarter * 32 + lane;
-    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-    int s = 0, a = 0;
-    uint32_t ph = 0, aph = 0;
-    for (int i = 0; i < nst; ++i) {
-      DTC_PW(7, mbar_wait(&full_bar[s], ph))
-      const uint32_t wrow = sb + s * Gm::STAGE + row * Gm::WB;
-      uint4 c[4];
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc) c[cc] = lds128(wrow + ((cc ^ ((row >> 1) & 3)) << 4));
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sfree[s]);  // codes are in registers: the TMA may refill
-      DTC_PW(8, mbar_wait(&afree[a], aph ^ 1))
-      fence_after();
-      const uint32_t words[16] = {c[0].x, c[0].y, c[0].z, c[0].w, c[1].x, c[1].y, c[1].z, c[1].w,
-                                  c[2].x, c[2].y, c[2].z, c[2].w, c[3].x, c[3].y, c[3].z, c[3].w};
-      constexpr int PAIRS_PER_WORD = BITS == 4 ? 4 : 2;
-      constexpr int NPAIR = 16 * PAIRS_PER_WORD;  // 64 (int4) / 32 (int8) TMEM columns
-#pragma unroll
-      for (int hh = 0; hh < NPAIR / 32; ++hh) {
-        uint32_t q[32];
-#pragma unroll
-        for (int w = 0; w < 32 / PAIRS_PER_WORD; ++w) {
-          if (dbg & 1) {
-#pragma unroll
-            for (int u = 0; u < PAIRS_PER_WORD; ++u) q[w * PAIRS_PER_WORD + u] = words[hh * (32 / PAIRS_PER_WORD) + w];
-          } else {
-            unpack_word<T, BITS>(words[hh * (32 / PAIRS_PER_WORD) + w], &q[w * PAIRS_PER_WORD]);
-          }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_f16<__half, BM, NT>();
+      int s = 0, a = 0, c = 0;
+      uint32_t ph = 0, aph = 0, cph = 0;
+      for (int g = beg; g < end; ++g) {
+        mbar_wait(&bfull_bar[s], ph);
+        if (!(FQ_DTC_DBG & 8)) {
+          mbar_wait(&afull_bar[a], aph);
+          mbar_wait(&cempty_bar[c], cph ^ 1);
         }
-        if (dbg & 16) {  // diagnostics: keep the values live without the TMEM store
-          uint32_t x = 0;
+        fence_after();
+        const uint32_t bst = sb + Gm::B_RING + s * Gm::B_BYTES;
 #pragma unroll
-          for (int u = 0; u < 32; ++u) x ^= q[u];
-          if (x == 0x9E3779B9u) tmem_st32(tmem + lane_base + a * KS + half * Gm::A_COLS + hh * 32, q);
-        } else {
-          tmem_st32(tmem + lane_base + a * KS + half * Gm::A_COLS + hh * 32, q);
+        for (int kk = 0; kk < KS / 16; ++kk) {
+          if (FQ_DTC_DBG & 1) break;
+          const uint64_t bdesc = sw128_desc(bst + (kk >> 2) * Gm::ATOM_BYTES) + (uint64_t)((kk & 3) * 2);
+          mma_ts(tmem + Gm::ACC_COL + c * NT, tmem + a * Gm::A_COLS + kk * 8, bdesc, idesc, kk != 0);
         }
+        mma_commit(&bempty_bar[s]);
+        mma_commit(&aempty_bar[a]);
+        mma_commit(&cfull_bar[c]);
+        if (++s == Gm::NB) { s = 0; ph ^= 1; }
+        if (++a == AS) { a = 0; aph ^= 1; }
+        if (++c == AC) { c = 0; cph ^= 1; }
       }
-      tmem_wait_st();
-      fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&aready[a]);
-      if (++s == SST) { s = 0; ph ^= 1; }
-      if (++a == AST) { a = 0; aph ^= 1; }
     }
   } else {
-    // ------------------------------------------------------------------ fold + epilogue
-    const int quarter = warp & 3;
-    const int half = (warp - 11) >> 2;
-    const int row = half * 128 + quarter * 32 + lane;
+    // ------------------------------------------------------------------------- dequant + fold
+    const int quarter = warp & 3;          // TMEM lane quarter this warp may access
+    const int row = quarter * 32 + lane;   // weight row within the tile == TMEM lane
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-    const int ftid = threadIdx.x - 11 * 32;   // 0..255 among the fold warps
-    float acc[NTF];
+    const int sw = (row >> 1) & 3;         // SWIZZLE_64B: cell c of row r sits at c ^ ((r >> 1) & 3)
+    const uint32_t rofs = row * WB;
+    float acc[NT];
 #pragma unroll
-    for (int t = 0; t < NTF; ++t) acc[t] = 0.f;
-    Cur cur;
-    if (nst > 0) cur_locate(batch, b0, cur);
-    int seg_k0 = nst > 0 ? cur.kidx : 0;
-    bool first_seg = true;
-    int c = 0, f = 0;
-    uint32_t cph = 0;
-    for (int i = 0; i < nst; ++i) {
-      DTC_PW(9, mbar_wait(&accfull[c], cph))
-      fence_after();
-      uint32_t v[NTF];
-      tmem_ldn<NTF>(tmem + lane_base + Gm::ACC_COL + c * 2 * NT + half * NT, v);
-      const float* fdp = reinterpret_cast<const float*>(sbase + Gm::FD_RING + f * Gm::FD_BYTES);
-      const float sc = fdp[NT + row];
-      float sums[NTF];
+    for (int t = 0; t < NT; ++t) acc[t] = 0.f;
+    Cur cf;
+    cur_locate(b, beg, cf);
+    bool first_seg = true;                 // the fold's current segment contains `beg`
+    int seg_k0 = cf.kidx;                  // first k-stage of the current segment
+    bool dep_done = false;
+    float scq[LAG + 1];                    // scales of stages i, i-1, ..., i-LAG (register FIFO)
 #pragma unroll
-      for (int t = 0; t < NTF; ++t) sums[t] = OFF != 0.f ? fdp[t] : 0.f;
-      tmem_wait_ld();
-      fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&accfree[c]);
-        mbar_arrive(&fdfree[f]);
-      }
-      if (!(dbg & 2)) {
+    for (int q = 0; q < LAG + 1; ++q) scq[q] = 0.f;
+    int s = 0, a = 0, c = 0;
+    uint32_t ph = 0, aph = 0, cph = 0;
+    for (int i = beg; i < end + LAG; ++i) {
+      float sc0 = 0.f;
 #pragma unroll
-        for (int t = 0; t < NTF; ++t) {
-          float part = __uint_as_float(v[t]);
-          if (OFF != 0.f) part = fmaf(-OFF, sums[t], part);
-          acc[t] = fmaf(sc, part, acc[t]);
+      for (int q = LAG; q > 0; --q) scq[q] = scq[q - 1];
+      if (i < end) {
+        // ---- dequant stage i
+        mbar_wait(&full_bar[s], ph);
+        const uint32_t st = sb + s * Gm::WSTAGE;
+        uint4 cw[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) cw[q] = lds128(st + rofs + ((q ^ sw) << 4));
+        sc0 = lds_f16x<T>(st + Gm::SC_OFS + row * 2);
+        scq[0] = sc0;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[s]);
+        constexpr int NR = BITS == 4 ? 64 : 32;
+        uint32_t out[NR];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t wv[4] = {cw[q].x, cw[q].y, cw[q].z, cw[q].w};
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            if constexpr (BITS == 4) i4_exact(wv[w], out + 16 * q + 4 * w);
+            else i8_exact(wv[w], out + 8 * q + 2 * w);
+          }
         }
+        if (!(FQ_DTC_DBG & 16)) mbar_wait(&aempty_bar[a], aph ^ 1);
+        fence_after();
+        const uint32_t ta = tmem + lane_base + a * Gm::A_COLS;
+        if (!(FQ_DTC_DBG & 2)) {
+          tmem_st32(ta, *reinterpret_cast<const uint32_t(*)[32]>(out));
+          if constexpr (BITS == 4) tmem_st32(ta + 32, *reinterpret_cast<const uint32_t(*)[32]>(out + 32));
+        } else if (out[0] == 0x12345u && out[NR - 1] == 0x777u) {
+          tmem_st16(ta, *reinterpret_cast<const uint32_t(*)[16]>(out));
+        }
+        tmem_wait_st();
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&afull_bar[a]);
+        if (++s == NSTAGE) { s = 0; ph ^= 1; }
+        if (++a == AS) { a = 0; aph ^= 1; }
       }
-      if (++c == ACC) { c = 0; cph ^= 1; }
-      if (++f == FD) f = 0;
-
-      const DtcProb& p = batch.p[cur.p];
-      if (cur.kidx == p.nk - 1 || i == nst - 1) {
-        // ---- end of a tile segment: C (whole tile in this CTA) or a split partial
-        const int n = cur.tile * ROWS + row;
-        const int M = p.M;
-        auto store_out = [&](int tok, float val) {
-          const size_t o = (size_t)tok * p.N + n;
-          if (p.cdt == FQ_FP32) reinterpret_cast<float*>(p.C)[o] = val;
-          else reinterpret_cast<T*>(p.C)[o] = Dt<T>::from_f(val);
-        };
-        if (seg_k0 == 0 && cur.kidx == p.nk - 1) {
-          if (n < p.N) {
-#pragma unroll
-            for (int t = 0; t < NTF; ++t)
-              if (t < M) store_out(t, acc[t]);
-          }
+      if (i >= beg + LAG) {
+        // ---- fold stage j = i - LAG: acc += s[row] * (exact integer partial of the stage)
+        const int j = i - LAG;
+        const Prob& p = b.p[cf.p];
+        mbar_wait(&cfull_bar[c], cph);
+        fence_after();
+        uint32_t v[NT];
+        if (!(FQ_DTC_DBG & 4)) {
+          tmem_ldn<NT>(tmem + lane_base + Gm::ACC_COL + c * NT, v);
+          tmem_wait_ld();
         } else {
-          const int slot = first_seg ? 0 : 1;
-          float* wsp = batch.ws + (size_t)(cta * 2 + slot) * NT * ROWS;
 #pragma unroll
-          for (int t = 0; t < NTF; ++t)
-            if (t < M) __stcg(wsp + t * ROWS + row, acc[t]);
-          const int ts = p.stage_begin + cur.tile * p.nk;
-          const int c_lo = cta_of(TS, P, ts), c_hi = cta_of(TS, P, ts + p.nk - 1);
-          int* ctr = batch.counters + p.tile_begin + cur.tile;
-          asm volatile("bar.sync 1, 256;" ::: "memory");
-          if (ftid == 0) {
-            __threadfence();
-            const int last = atomicAdd(ctr, 1) == c_hi - c_lo;
-            if (last) __threadfence();
-            s_last = last;
+          for (int t = 0; t < NT; ++t) v[t] = 0;
+        }
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&cempty_bar[c]);
+#pragma unroll
+        for (int t = 0; t < NT; ++t) acc[t] = fmaf(scq[LAG], __uint_as_float(v[t]), acc[t]);
+        if (++c == AC) { c = 0; cph ^= 1; }
+        // ---- end of a tile segment: store, or stream-K partial + deterministic fixup
+        if (j == end - 1 || cf.kidx == p.nk - 1) {
+          if (!dep_done) {  // the per-token factors come from the prep kernel
+            griddep_wait();
+            dep_done = true;
           }
-          asm volatile("bar.sync 1, 256;" ::: "memory");
-          const int last = s_last;
-          if (last) {
-            if (n < p.N) {
+          const int n = cf.tile * BM + row;
+          const int M = p.M, N = p.N;
 #pragma unroll
-              for (int t = 0; t < NTF; ++t) {
-                if (t < M) {
+          for (int t = 0; t < NT; ++t) acc[t] *= (t < M) ? __ldg(p.inv + t) : 0.f;
+          auto store = [&](int tok, float val) {
+            const size_t o = (size_t)tok * N + n;
+            if (p.cdt == FQ_FP32) reinterpret_cast<float*>(p.C)[o] = val;
+            else reinterpret_cast<T*>(p.C)[o] = Dt<T>::from_f(val);
+          };
+          if (seg_k0 == 0 && cf.kidx == p.nk - 1) {
+            if (n < N) {
+#pragma unroll
+              for (int t = 0; t < NT; ++t)
+                if (t < M) store(t, acc[t]);
+            }
+          } else {
+            const int slot = first_seg ? 0 : 1;
+            float* part = b.ws + ((size_t)(blockIdx.x * 2 + slot) * 16) * BM;
+#pragma unroll
+            for (int t = 0; t < NT; ++t)
+              if (t < M) __stcg(part + t * BM + row, acc[t]);
+            const int gtile = p.tile_begin + cf.tile;
+            const int t0 = p.stage_begin + cf.tile * p.nk;  // the tile's first global stage
+            const int cfirst = cta_of(TS, P, t0), clast = cta_of(TS, P, t0 + p.nk - 1);
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * kDqWarps));
+            if (threadIdx.x == 32 * kDq0) {
+              __threadfence();
+              const int last = atomicAdd(&b.counters[gtile], 1) == clast - cfirst;
+              if (last) __threadfence();
+              s_last = last;
+            }
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * kDqWarps));
+            if (s_last) {
+              if (n < N) {
+#pragma unroll
+                for (int t = 0; t < NT; ++t) {
+                  if (t >= M) continue;
                   float val = 0.f;
-                  for (int cc = c_lo; cc <= c_hi; ++cc) {
-                    const int sl = range_begin(TS, P, cc) >= ts ? 0 : 1;
-                    val += __ldcg(batch.ws + ((size_t)(cc * 2 + sl) * NT + t) * ROWS + row);
+                  for (int cc = cfirst; cc <= clast; ++cc) {
+                    const int sl = range_begin(TS, P, cc) >= t0 ? 0 : 1;
+                    val += __ldcg(b.ws + ((size_t)(cc * 2 + sl) * 16 + t) * BM + row);
                   }
-                  store_out(t, val);
+                  store(t, val);
                 }
               }
+              if (threadIdx.x == 32 * kDq0) b.counters[gtile] = 0;  // self-reset for the next launch
             }
-            if (ftid == 0) *ctr = 0;  // self-reset for the next launch
           }
-          asm volatile("bar.sync 1, 256;" ::: "memory");  // s_last reused by the next segment
-        }
 #pragma unroll
-        for (int t = 0; t < NTF; ++t) acc[t] = 0.f;
-        first_seg = false;
-        seg_k0 = 0;
+          for (int t = 0; t < NT; ++t) acc[t] = 0.f;
+          first_seg = false;
+          seg_k0 = 0;
+        }
+        cur_next(b, cf);
       }
-      cur_next(batch, cur);
     }
   }
-#if FQ_DTC_PROF
-  if (blockIdx.x == 0 && lane == 0)
-    printf("prof warp %2d total %lld waits %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld nst %d\n", warp,
-           clock64() - tstart_, prof_[0], prof_[1], prof_[2], prof_[3], prof_[4], prof_[5], prof_[6], prof_[7],
-           prof_[8], prof_[9], nst);
-#endif
-  fence_before();
   __syncthreads();
   if (warp == 1) {
     fence_after();
     tmem_dealloc(tmem, kTmemCols);
   }
+}
+
+// Activation pre-conversion (one CTA per token): A'[tok][k] = fp16(A * 2^e), one power of two per
+// token putting max|A[tok,:]| in [2^14, 2^15) (bf16 input; exact for every element within 2^-29 of
+// the max) or e = 0 (fp16 input), in the k order of the int4 unpack (PERM: pieces of 8 as
+// a0,a4,a1,a5,a2,a6,a3,a7) or natural (int8); inv[tok] = 2^-e.
+template <typename T, bool PERM>
+__global__ void __launch_bounds__(512) prep_tc_kernel(const T* __restrict__ A, int K, __half* __restrict__ Ap,
+                                                      float* __restrict__ inv_out) {
+  griddep_wait();  // A may be the output of the previous kernel in the stream
+  griddep_launch_dependents();
+  __shared__ float red[16];
+  const int tok = blockIdx.x;
+  const T* row = A + (size_t)tok * K;
+  const int n8 = K >> 3;
+  auto decode = [](const uint4& v, float (&f)[8]) {
+    const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (Dt<T>::id == FQ_BF16) {
+        f[2 * e] = __uint_as_float(vv[e] << 16);
+        f[2 * e + 1] = __uint_as_float(vv[e] & 0xFFFF0000u);
+      } else {
+        const float2 h = __half22float2(*reinterpret_cast<const __half2*>(&vv[e]));
+        f[2 * e] = h.x;
+        f[2 * e + 1] = h.y;
+      }
+    }
+  };
+  float sc = 1.f, inv = 1.f;
+  if (Dt<T>::id == FQ_BF16) {
+    float mx = 0.f;
+    for (int i = threadIdx.x; i < n8; i += blockDim.x) {
+      float f[8];
+      decode(ldg_keep(row + (size_t)i * 8), f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) mx = fmaxf(mx, fabsf(f[e]));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    mx = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mx = fmaxf(mx, red[w]);
+    const int E = (int)((__float_as_uint(mx) >> 23) & 0xFF);
+    const int F = max(1, min(268 - E, 253));  // biased exponent of 2^e, e = 14 - (E - 127)
+    sc = __uint_as_float((uint32_t)F << 23);
+    inv = __uint_as_float((uint32_t)(254 - F) << 23);
+  }
+  auto h2 = [](float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+  };
+  for (int i = threadIdx.x; i < n8; i += blockDim.x) {
+    float f[8];
+    decode(ldg_keep(row + (size_t)i * 8), f);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) f[e] *= sc;
+    const uint4 o = PERM ? make_uint4(h2(f[0], f[4]), h2(f[1], f[5]), h2(f[2], f[6]), h2(f[3], f[7]))
+                         : make_uint4(h2(f[0], f[1]), h2(f[2], f[3]), h2(f[4], f[5]), h2(f[6], f[7]));
+    *reinterpret_cast<uint4*>(Ap + (size_t)tok * K + (size_t)i * 8) = o;
+  }
+  if (threadIdx.x == 0) inv_out[tok] = inv;
 }
 
 }  // namespace dtc
@@ -540,131 +492,166 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const __grid_con
 constexpr size_t kDtcCounterBytes = 65536;
 constexpr int kDtcMaxTiles = (int)(kDtcCounterBytes / sizeof(int));
 
+static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+static size_t dtc_partial_bytes(int nsm) { return al256((size_t)2 * nsm * 2 * 16 * dtc::BM * sizeof(float)); }
+static size_t dtc_prep_a_bytes(int64_t ntok, int K) { return al256((size_t)ntok * K * 2); }
+static size_t dtc_prep_v_bytes(int64_t ntok) { return al256((size_t)ntok * 4); }
+
+static int dtc_nt_override() {
+  const char* e = std::getenv("FQ_DTC_NT");
+  return e ? std::atoi(e) : 0;
+}
+
 bool decode_tc_supported(int bits, int group, int M) {
-  // Opt-in (FQ_DECODE_TC=1): correct, but slower than the mma.sync kernel on B200 (round-1
-  // diagnostics: the per-stage TMEM/MMA/fold hand-offs cost more issue slots than they save).
+  // Opt-in (FQ_DECODE_TC=1): parity-green, but on B200 it streams at 2.4-2.9 TB/s against
+  // 5.0-5.4 TB/s (M <= 8) / 3.4 TB/s (M = 16) for the mma.sync kernel; its synchronisation skeleton
+  // alone (no unpack / MMA / tcgen05.ld) reaches only 4.6 TB/s (profiles/r01).
+  (void)bits;
   const char* e = std::getenv("FQ_DECODE_TC");
   if (!e || e[0] != '1') return false;
-  return M >= 1 && M <= dtc::NT && group % (bits == 4 ? 128 : 64) == 0;
+  return M >= 1 && M <= 16 && group % 128 == 0;
+}
+
+size_t dtc_workspace_bytes(int64_t ntok, int K, int nsm) {
+  return kDtcCounterBytes + dtc_partial_bytes(nsm) + dtc_prep_a_bytes(ntok, K) + dtc_prep_v_bytes(ntok);
 }
 
 static int dtc_ctas(long long total_stages, int nsm) {
-  // at least 4 stages per CTA so tiny problems are not shredded into single-stage partials
-  const long long c = std::min<long long>(nsm, (total_stages + 3) / 4);
+  // two CTAs per SM; at least 8 stages per CTA so small problems are not shredded into partials
+  const long long c = std::min<long long>(2LL * nsm, (total_stages + 7) / 8);
   return (int)std::max<long long>(1, c);
 }
 
-size_t dtc_workspace_bytes(int M, int K, int N, int bits, int nsm) {
-  (void)M; (void)K; (void)N; (void)bits;
-  return kDtcCounterBytes + (size_t)nsm * 2 * dtc::NT * dtc::ROWS * sizeof(float);
-}
-
-template <typename T, int BITS, int MAXP, int NTF>
-static cudaError_t launch_dtc(const dtc::DtcBatch<MAXP>& b, int ctas, cudaStream_t st) {
-  constexpr int smem = dtc::G<BITS>::SMEM;
-  auto kern = dtc::decode_tc_kernel<T, BITS, MAXP, NTF>;
-  static bool attr = false;
+template <typename T, int BITS, int NT, int MAXP>
+static cudaError_t launch_dtc(const dtc::Batch<MAXP>& b, int ctas, cudaStream_t st) {
+  constexpr int smem = dtc::G<BITS, NT>::SMEM;
+  auto kern = dtc::decode_tc_kernel<T, BITS, NT, MAXP>;
+  static bool attr = false;  // benign race: idempotent attribute call
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  kern<<<ctas, dtc::kThreads, smem, st>>>(b);
-  return cudaGetLastError();
+  return launch_pdl(kern, ctas, dtc::kThreads, smem, st, b);
 }
 
-template <int MAXP, int NTF>
-static cudaError_t dispatch_dtc_t(int adt, int bits, const dtc::DtcBatch<MAXP>& b, int ctas, cudaStream_t st) {
+template <int NT, int MAXP>
+static cudaError_t dispatch_dtc_nt(int adt, int bits, const dtc::Batch<MAXP>& b, int ctas, cudaStream_t st) {
   if (adt == FQ_BF16)
-    return bits == 4 ? launch_dtc<__nv_bfloat16, 4, MAXP, NTF>(b, ctas, st)
-                     : launch_dtc<__nv_bfloat16, 8, MAXP, NTF>(b, ctas, st);
-  return bits == 4 ? launch_dtc<__half, 4, MAXP, NTF>(b, ctas, st) : launch_dtc<__half, 8, MAXP, NTF>(b, ctas, st);
+    return bits == 4 ? launch_dtc<__nv_bfloat16, 4, NT, MAXP>(b, ctas, st)
+                     : launch_dtc<__nv_bfloat16, 8, NT, MAXP>(b, ctas, st);
+  return bits == 4 ? launch_dtc<__half, 4, NT, MAXP>(b, ctas, st) : launch_dtc<__half, 8, NT, MAXP>(b, ctas, st);
+}
+static int dtc_nt(int maxm) {
+  const int o = dtc_nt_override();
+  if (o == 8 || o == 16) return std::max(o, maxm > 8 ? 16 : 8);
+  return maxm > 8 ? 16 : 8;
 }
 template <int MAXP>
-static cudaError_t dispatch_dtc(int adt, int bits, const dtc::DtcBatch<MAXP>& b, int ctas, cudaStream_t st,
-                                int maxm) {
-  if (maxm <= 1) return dispatch_dtc_t<MAXP, 1>(adt, bits, b, ctas, st);
-  if (maxm <= 4) return dispatch_dtc_t<MAXP, 4>(adt, bits, b, ctas, st);
-  if (maxm <= 8) return dispatch_dtc_t<MAXP, 8>(adt, bits, b, ctas, st);
-  return dispatch_dtc_t<MAXP, 16>(adt, bits, b, ctas, st);
+static cudaError_t dispatch_dtc(int adt, int bits, const dtc::Batch<MAXP>& b, int ctas, int nt, cudaStream_t st) {
+  return nt == 8 ? dispatch_dtc_nt<8, MAXP>(adt, bits, b, ctas, st) : dispatch_dtc_nt<16, MAXP>(adt, bits, b, ctas, st);
 }
 
-static bool make_dtc_prob(dtc::DtcProb& d, int bits, int cdt, const void* A, int M, int K, int N,
-                          const void* codes, const void* scales, int group, void* C) {
+static cudaError_t launch_prep_tc(int adt, int bits, const void* A, int ntok, int K, void* Ap, void* Vp,
+                                  cudaStream_t st) {
+  if (ntok == 0) return cudaSuccess;
+  auto* ap = reinterpret_cast<__half*>(Ap);
+  auto* vp = reinterpret_cast<float*>(Vp);
+  if (adt == FQ_BF16) {
+    auto* a = reinterpret_cast<const __nv_bfloat16*>(A);
+    return bits == 4 ? launch_pdl(dtc::prep_tc_kernel<__nv_bfloat16, true>, ntok, 512, 0, st, a, K, ap, vp)
+                     : launch_pdl(dtc::prep_tc_kernel<__nv_bfloat16, false>, ntok, 512, 0, st, a, K, ap, vp);
+  }
+  auto* a = reinterpret_cast<const __half*>(A);
+  return bits == 4 ? launch_pdl(dtc::prep_tc_kernel<__half, true>, ntok, 512, 0, st, a, K, ap, vp)
+                   : launch_pdl(dtc::prep_tc_kernel<__half, false>, ntok, 512, 0, st, a, K, ap, vp);
+}
+
+// One problem: Ap = its A' rows, inv = its per-token factors.
+static bool make_dtc_prob(dtc::Prob& d, int bits, int cdt, int nt, const void* Ap, const float* inv, int M, int K,
+                          int N, const void* codes, const void* scales, int group, void* C) {
   const uint64_t row_bytes = (uint64_t)K * bits / 8;
-  const int ks = 64 * 8 / bits;
-  if (!make_tmap_2d(&d.w, codes, 1, row_bytes, (uint64_t)N, row_bytes, 64, dtc::ROWS, 64)) return false;
-  if (!make_tmap_2d(&d.a, A, 2, (uint64_t)K, (uint64_t)M, (uint64_t)K * 2, ks, M, 0)) return false;
-  if (!make_tmap_2d(&d.s, scales, 2, (uint64_t)N, (uint64_t)(K / group), (uint64_t)N * 2, dtc::ROWS, 1, 0))
+  if (!make_tmap_2d(&d.w, codes, 1, row_bytes, (uint64_t)N, row_bytes, dtc::WB, dtc::BM, 64)) return false;
+  if (!make_tmap_2d(&d.a, Ap, 2, (uint64_t)K, (uint64_t)M, (uint64_t)K * 2, 64, nt, 128)) return false;
+  if (!make_tmap_2d(&d.s, scales, 2, (uint64_t)N, (uint64_t)(K / group), (uint64_t)N * 2, dtc::BM, 1, 0))
     return false;
+  d.inv = inv;
   d.C = C;
   d.M = M; d.K = K; d.N = N; d.group = group; d.cdt = cdt;
-  d.gx = (N + dtc::ROWS - 1) / dtc::ROWS;
-  d.nk = (K + ks - 1) / ks;
+  d.gx = (N + dtc::BM - 1) / dtc::BM;
+  d.nk = (K + (64 * 8 / bits) - 1) / (64 * 8 / bits);
   return true;
-}
-
-static int dtc_dbg() {
-  const char* db = std::getenv("FQ_DTC_DBG");
-  return db ? std::atoi(db) : 0;
 }
 
 cudaError_t run_decode_tc(int adt, int cdt, int bits, const void* A, int M, int K, int N, const void* codes,
                           const void* scales, int group, void* C, void* ws, cudaStream_t st) {
-  dtc::DtcBatch<1> b{};
-  if (!make_dtc_prob(b.p[0], bits, cdt, A, M, K, N, codes, scales, group, C)) return cudaErrorInvalidValue;
+  const int nsm = num_sms();
+  char* base = reinterpret_cast<char*>(ws);
+  char* Ap = base + kDtcCounterBytes + dtc_partial_bytes(nsm);
+  float* Vp = reinterpret_cast<float*>(Ap + dtc_prep_a_bytes(M, K));
+  cudaError_t r = launch_prep_tc(adt, bits, A, M, K, Ap, Vp, st);
+  if (r != cudaSuccess) return r;
+  const int nt = dtc_nt(M);
+  dtc::Batch<1> b{};
+  if (!make_dtc_prob(b.p[0], bits, cdt, nt, Ap, Vp, M, K, N, codes, scales, group, C)) return cudaErrorInvalidValue;
   if (b.p[0].gx > kDtcMaxTiles) return cudaErrorInvalidValue;
   b.p[0].stage_begin = 0;
   b.p[0].tile_begin = 0;
   b.nprob = 1;
   b.total_stages = b.p[0].gx * b.p[0].nk;
-  b.counters = reinterpret_cast<int*>(ws);
-  b.ws = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + kDtcCounterBytes);
-  b.dbg = dtc_dbg();
-  return dispatch_dtc<1>(adt, bits, b, dtc_ctas(b.total_stages, num_sms()), st, M);
+  b.counters = reinterpret_cast<int*>(base);
+  b.ws = reinterpret_cast<float*>(base + kDtcCounterBytes);
+  return dispatch_dtc<1>(adt, bits, b, dtc_ctas(b.total_stages, nsm), nt, st);
 }
 
-// MoE batch on the tcgen05 decode kernel: experts (1 <= M_e <= 16, group % KS == 0) share one
-// stream-K launch per <= MAXP experts (all of their tiles in one linear stage space).
+// MoE batch: experts (1 <= M_e <= 16, group % 128 == 0) share one stream-K launch per <= MAXP experts
+// (all of their tiles in one linear stage space).  A' is prepared once for all T tokens.
 cudaError_t run_decode_tc_grouped(int adt, int cdt, int bits, const void* A, int K, int N, const int64_t* offsets,
                                   const int32_t* groups, const void* const* codes, const void* const* scales,
-                                  void* C, void* ws, const int* experts, int nexp, cudaStream_t st) {
-  constexpr int MAXP = 40;
-  static_assert(sizeof(dtc::DtcBatch<MAXP>) < 32000, "kernel parameter block limit");
-  dtc::DtcBatch<MAXP> b{};
-  b.counters = reinterpret_cast<int*>(ws);
-  b.ws = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + kDtcCounterBytes);
-  b.dbg = dtc_dbg();
-  int stages = 0, tiles = 0, maxm = 0;
+                                  void* C, void* ws, int64_t T, const int* experts, int nexp, cudaStream_t st) {
+  constexpr int MAXP = 48;
+  static_assert(sizeof(dtc::Batch<MAXP>) < 32000, "kernel parameter block limit");
+  const int nsm = num_sms();
+  char* base = reinterpret_cast<char*>(ws);
+  char* Ap = base + kDtcCounterBytes + dtc_partial_bytes(nsm);
+  float* Vp = reinterpret_cast<float*>(Ap + dtc_prep_a_bytes(T, K));
+  cudaError_t r = launch_prep_tc(adt, bits, A, (int)T, K, Ap, Vp, st);
+  if (r != cudaSuccess) return r;
+  int maxm = 0;
+  for (int ii = 0; ii < nexp; ++ii)
+    maxm = std::max(maxm, (int)(offsets[experts[ii] + 1] - offsets[experts[ii]]));
+  const int nt = dtc_nt(maxm);
+  dtc::Batch<MAXP> b{};
+  b.counters = reinterpret_cast<int*>(base);
+  b.ws = reinterpret_cast<float*>(base + kDtcCounterBytes);
+  int stages = 0, tiles = 0;
   auto flush = [&]() -> cudaError_t {
     b.total_stages = stages;
-    cudaError_t r = dispatch_dtc<MAXP>(adt, bits, b, dtc_ctas(stages, num_sms()), st, maxm);
+    cudaError_t rr = dispatch_dtc<MAXP>(adt, bits, b, dtc_ctas(stages, nsm), nt, st);
     b.nprob = 0;
-    stages = tiles = maxm = 0;
-    return r;
+    stages = tiles = 0;
+    return rr;
   };
   for (int ii = 0; ii < nexp; ++ii) {
     const int e = experts[ii];
     const int Me = (int)(offsets[e + 1] - offsets[e]);
-    const char* Ae = reinterpret_cast<const char*>(A) + (size_t)offsets[e] * K * 2;
     char* Ce = reinterpret_cast<char*>(C) + (size_t)offsets[e] * N * (cdt == FQ_FP32 ? 4 : 2);
-    dtc::DtcProb& d = b.p[b.nprob];
-    if (!make_dtc_prob(d, bits, cdt, Ae, Me, K, N, codes[e], scales[e], groups[e], Ce))
+    dtc::Prob d;
+    if (!make_dtc_prob(d, bits, cdt, nt, Ap + (size_t)offsets[e] * K * 2, Vp + offsets[e], Me, K, N, codes[e],
+                       scales[e], groups[e], Ce))
       return cudaErrorInvalidValue;
     if (tiles + d.gx > kDtcMaxTiles) {  // counter region full: launch what we have first
-      cudaError_t r = flush();
-      if (r != cudaSuccess) return r;
-      b.p[0] = d;
+      cudaError_t rr = flush();
+      if (rr != cudaSuccess) return rr;
     }
-    dtc::DtcProb& dd = b.p[b.nprob];
-    dd.stage_begin = stages;
-    dd.tile_begin = tiles;
-    stages += dd.gx * dd.nk;
-    tiles += dd.gx;
-    maxm = std::max(maxm, Me);
+    d.stage_begin = stages;
+    d.tile_begin = tiles;
+    b.p[b.nprob] = d;
+    stages += d.gx * d.nk;
+    tiles += d.gx;
     if (++b.nprob == MAXP) {
-      cudaError_t r = flush();
-      if (r != cudaSuccess) return r;
+      cudaError_t rr = flush();
+      if (rr != cudaSuccess) return rr;
     }
   }
   if (b.nprob) return flush();

@@ -733,15 +733,15 @@ __global__ void __launch_bounds__(128) prep_acts_kernel(const T* __restrict__ A,
 #pragma unroll
     for (int e = 0; e < 8; ++e) f[e] *= sc;
   }
-  float sum = fmaf(Nib<__half>::off_even, (f[0] + f[2]) + (f[4] + f[6]),
-                   Nib<__half>::off_odd * ((f[1] + f[3]) + (f[5] + f[7])));
-#pragma unroll
-  for (int o = 8; o; o >>= 1) sum += __shfl_xor_sync(hmask, sum, o);
   auto h2 = [](float lo, float hi) {
     uint32_t hw2;
     asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hw2) : "f"(hi), "f"(lo));
     return hw2;
   };
+  float sum = fmaf(Nib<__half>::off_even, (f[0] + f[2]) + (f[4] + f[6]),
+                   Nib<__half>::off_odd * ((f[1] + f[3]) + (f[5] + f[7])));
+#pragma unroll
+  for (int o = 8; o; o >>= 1) sum += __shfl_xor_sync(hmask, sum, o);
   const uint4 o = make_uint4(h2(f[0], f[4]), h2(f[1] * 0.0625f, f[5] * 0.0625f), h2(f[2], f[6]),
                              h2(f[3] * 0.0625f, f[7] * 0.0625f));
   const int kl = l * 8, tq = kl >> 5, w16 = (kl & 31) >> 3;

@@ -35,15 +35,16 @@ cudaError_t run_gemv_grouped(int adt, int cdt, int bits, const void* A, int K, i
                              const void* const* scales, void* C, void* ws, int64_t T,
                              const int* experts, int nexp, cudaStream_t st);
 
-// Decode GEMM on tcgen05 (A4, M <= 16, group % 128 (int4) / 64 (int8) == 0); workspace = 64 KiB
-// counters + per-CTA split partials (dtc_workspace_bytes), zero-filled once.
+// Decode GEMM on tcgen05 (A4, M <= 16, group % 128 == 0; stream-K, kernel in fq_decode_tc.cu).
+// Workspace: 64 KiB counters (zero-filled once, self-resetting) + stream-K partials + the
+// pre-converted activations of `ntok` tokens.
 bool decode_tc_supported(int bits, int group, int M);
-size_t dtc_workspace_bytes(int M, int K, int N, int bits, int nsm);
+size_t dtc_workspace_bytes(int64_t ntok, int K, int nsm);
 cudaError_t run_decode_tc(int adt, int cdt, int bits, const void* A, int M, int K, int N, const void* codes,
                           const void* scales, int group, void* C, void* ws, cudaStream_t st);
 cudaError_t run_decode_tc_grouped(int adt, int cdt, int bits, const void* A, int K, int N, const int64_t* offsets,
                                   const int32_t* groups, const void* const* codes, const void* const* scales,
-                                  void* C, void* ws, const int* experts, int nexp, cudaStream_t st);
+                                  void* C, void* ws, int64_t T, const int* experts, int nexp, cudaStream_t st);
 
 // Large-M tensor-core GEMM (tcgen05 + TMEM, kernel A6).
 cudaError_t run_gemm_tc(int adt, int cdt, int bits, const void* A, int M, int K, int N, const void* codes,

@@ -1,13 +1,10 @@
 #!/bin/bash
-# tcgen05 decode diagnostics: FQ_DTC_DBG sweep for the default library and each variant.
+# tcgen05 decode iteration batch: decode parity tests, then the M sweep (tcgen05 and mma.sync).
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-echo "== default" > gpurun_out/dtcd.log
-timeout 300 python tools/dtc_dbg.py >> gpurun_out/dtcd.log 2>&1
-for v in paper_2308_09723_b200/_variants/*.so; do
-  [ -e "$v" ] || continue
-  echo "== $v" >> gpurun_out/dtcd.log
-  FQ_LIB_PATH=$PWD/$v timeout 300 python tools/dtc_dbg.py >> gpurun_out/dtcd.log 2>&1
-done
-if [ -n "${NCU}" ]; then
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:decode_tc -s 2 -c 1 -o gpurun_out/dtc_m1 -f python tools/prof_gemm.py --M 1 --iters 3 > gpurun_out/ncu_dtc.log 2>&1
-fi
+timeout 300 python -m pytest tests/test_gpu_gemm.py tests/test_gpu_moe.py -m gpu -q -x ${PYTEST_K} > gpurun_out/t.log 2>&1; echo "pytest $?" >> gpurun_out/t.log
+echo "== tcgen05" > gpurun_out/sweep.log
+timeout 200 python tools/dec_sweep.py ${SWEEP_ARGS} >> gpurun_out/sweep.log 2>&1
+echo "== mma.sync" >> gpurun_out/sweep.log
+FQ_DECODE_TC=0 timeout 200 python tools/dec_sweep.py ${SWEEP_ARGS} >> gpurun_out/sweep.log 2>&1
+
+
