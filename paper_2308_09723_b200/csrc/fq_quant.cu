@@ -31,6 +31,7 @@ struct Chunk8 {
     for (int i = 0; i < NV; ++i) r[i] = __ldg(reinterpret_cast<const uint4*>(p) + i);
   }
   __device__ __forceinline__ void decode(float (&v)[8]) const;
+  __device__ __forceinline__ float amax() const;
 };
 template <>
 __device__ __forceinline__ void Chunk8<__nv_bfloat16>::decode(float (&v)[8]) const {
@@ -59,6 +60,25 @@ __device__ __forceinline__ void Chunk8<float>::decode(float (&v)[8]) const {
   v[6] = __uint_as_float(r[1].z); v[7] = __uint_as_float(r[1].w);
 }
 
+// max|x| of a chunk of 16-bit values straight from the bit patterns: with the sign bit cleared,
+// finite values order like unsigned integers and every Inf/NaN pattern lies above all of them, so
+// two packed 16-bit unsigned max operations per pair replace the per-element decode + FMNMX.
+// Returns +inf if any element is non-finite (the group is then flagged).
+template <>
+__device__ __forceinline__ float Chunk8<__nv_bfloat16>::amax() const {
+  const uint32_t m = __vmaxu2(__vmaxu2(r[0].x & 0x7FFF7FFFu, r[0].y & 0x7FFF7FFFu),
+                              __vmaxu2(r[0].z & 0x7FFF7FFFu, r[0].w & 0x7FFF7FFFu));
+  const uint32_t h = max(m & 0xFFFFu, m >> 16);
+  return h >= 0x7F80u ? __int_as_float(0x7f800000) : __uint_as_float(h << 16);
+}
+template <>
+__device__ __forceinline__ float Chunk8<__half>::amax() const {
+  const uint32_t m = __vmaxu2(__vmaxu2(r[0].x & 0x7FFF7FFFu, r[0].y & 0x7FFF7FFFu),
+                              __vmaxu2(r[0].z & 0x7FFF7FFFu, r[0].w & 0x7FFF7FFFu));
+  const uint32_t h = max(m & 0xFFFFu, m >> 16);
+  return h >= 0x7C00u ? __int_as_float(0x7f800000) : __half2float(__ushort_as_half((unsigned short)h));
+}
+
 // max|x| over a chunk; +inf if any element is non-finite (the group is then flagged).
 __device__ __forceinline__ float chunk_amax(const float (&v)[8]) {
   float m = 0.f;
@@ -69,6 +89,13 @@ __device__ __forceinline__ float chunk_amax(const float (&v)[8]) {
     m = fmaxf(m, fabsf(v[i]));
   }
   return fin ? m : __int_as_float(0x7f800000);
+}
+
+template <>
+__device__ __forceinline__ float Chunk8<float>::amax() const {
+  float v[8];
+  decode(v);
+  return chunk_amax(v);
 }
 
 constexpr int kQThreads = 256;
@@ -107,11 +134,7 @@ __global__ void __launch_bounds__(sizeof(TIn) == 4 ? 512 : 1024) quantize_kernel
 #pragma unroll
   for (int i = 0; i < CPT; ++i) {
     const int c = threadIdx.x + i * T;
-    if (c < nchunk) {
-      float v[8];
-      raw[i].decode(v);
-      pm[c] = chunk_amax(v);
-    }
+    if (c < nchunk) pm[c] = raw[i].amax();
   }
   __syncthreads();
 
@@ -156,6 +179,7 @@ __global__ void __launch_bounds__(sizeof(TIn) == 4 ? 512 : 1024) quantize_kernel
   __syncthreads();
 
   // pass 3: codes
+  const uint32_t cpg_magic = 0xFFFFFFFFu / (uint32_t)cpg + 1u;  // ceil(2^32 / cpg), cpg >= 2
   constexpr int lo = -(1 << (BITS - 1)), hi = (1 << (BITS - 1)) - 1;
 #pragma unroll
   for (int ci = 0; ci < CPT; ++ci) {
@@ -163,28 +187,31 @@ __global__ void __launch_bounds__(sizeof(TIn) == 4 ? 512 : 1024) quantize_kernel
     if (c >= nchunk) break;
     float v[8];
     raw[ci].decode(v);
-    const float s = sc[c / cpg];
-    const float rs = sr[c / cpg];  // rcp(s), 0 when s == 0
+    const int j = (int)__umulhi((uint32_t)c, cpg_magic);  // c / cpg, exact for c < 2^32 / cpg
+    const float s = sc[j];
+    const float rs = sr[j];  // rcp(s), 0 when s == 0
     const float hs = 0.5f * s;     // exact
     // offset-binary code u = q + 2^(b-1) in [0, 2^b - 1]; the stored two's complement field is
     // u ^ 2^(b-1).  Kept in float until the final pack (all values are small exact integers).
     uint32_t u[8];
     if (Dt<TIn>::id != FQ_FP32 && s >= 1e-30f) {
-      // 16-bit W: m = floor(|x| * rcp(s) + 1/2) is exact except possibly at an exact tie
-      // |x| = (m + 1/2) s, where the estimate may fall one short; the tie is detected exactly
-      // because (m + 1/2) s = fma(m, s, s/2) is an exact fp32 value (<= 20 significant bits).
-      // Off-tie quotients are >= 2^-13 (absolute) away from a half-integer (x, s have <= 11
-      // significant bits), far beyond the ~2^-16 error of the estimate.
+      // 16-bit W: m = rn(|x| * rcp(s)) (magic-number rounding, no F2I/FRND) is the correctly rounded
+      // quotient except possibly at an exact tie |x| = (m + 1/2) s, where round-half-away needs m + 1;
+      // the tie is detected exactly because (m + 1/2) s = fma(m, s, s/2) is an exact fp32 value
+      // (<= 20 significant bits).  Off-tie quotients are >= 2^-13 (absolute) away from a half-integer
+      // (x, s have <= 11 significant bits), far beyond the ~2^-16 error of the estimate.
+      constexpr float kMagic = 12582912.f;  // 1.5 * 2^23: t + kMagic holds rn(t) in its low mantissa bits
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const float ax = fabsf(v[i]);
-        float m = floorf(fmaf(ax, rs, 0.5f));
-        m = (fmaf(m, s, hs) == ax) ? m + 1.f : m;
-        const bool neg = v[i] < 0.f;
-        m = fminf(m, neg ? (float)-lo : (float)hi);
-        u[i] = (uint32_t)(int)((neg ? -m : m) + (float)-lo);
-      }
-    } else {
+        const float t = fmaf(ax, rs, kMagic);
+        const float mf = t - kMagic;                        // rn(|x| / s) as an exact float
+        int m = __float_as_int(t) - 0x4B400000;
+        m += (fmaf(mf, s, hs) == ax) ? 1 : 0;
+        const bool neg = __float_as_uint(v[i]) >> 31;
+        m = min(m, neg ? -lo : hi);
+        u[i] = (uint32_t)((neg ? -m : m) - lo);
+      }    } else {
       // fp32 W (no tie-distance guarantee) and tiny/subnormal scales: IEEE division decides.
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
