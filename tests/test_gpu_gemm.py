@@ -120,6 +120,21 @@ def test_split_k_paths(fq, env, splits, M):
         assert O.rel_err(torch_to_f64(C), Cr, D) <= TOL
 
 
+@pytest.mark.parametrize("M,K,N", [(1, 4096, 512), (16, 4096, 768), (17, 2048, 512), (33, 1536, 1280),
+                                   (5, 12288, 2048)])
+def test_decode_multi_tile_determinism(fq, env, M, K, N):
+    """Decode kernel with split-K fixups over several column and token tiles (M > 16 on the decode
+    path): the fixup sums partials in a fixed order, so repeated calls are bit-identical (and the
+    self-resetting counters are exercised)."""
+    env("FQ_GEMM_PATH", "decode")
+    Wb, Ab = make_case(M, K, N, 4, 128, seed=M + K + N)
+    _, C0 = run_case(fq, Wb, Ab, 4, 128, "bf16", "fp32")
+    _, C1 = run_case(fq, Wb, Ab, 4, 128, "bf16", "fp32")
+    assert torch.equal(C0, C1)
+    Cr, D = oracle_ref(Wb, Ab, 4, 128, "bf16")
+    assert O.rel_err(torch_to_f64(C0), Cr, D) <= TOL
+
+
 @pytest.mark.parametrize("path", ["decode", "tc"])
 def test_identity_exact_fp32_out(fq, env, path):
     """A = I (M = K = 256): C[k, n] = q[n,k] * s[k/g, n] exactly in fp32-output mode — catches any
