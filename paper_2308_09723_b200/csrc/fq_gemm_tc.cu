@@ -32,7 +32,8 @@ namespace fq {
 namespace tc {
 
 constexpr int BM = 128;        // weight rows per tile (UMMA M)
-constexpr int BN = 256;        // tokens per tile (UMMA N)
+constexpr int BN = 256;        // max tokens per tile (UMMA N); a problem with M < 256 uses
+                               // bn = round_up(M, 16) (TcProb::bn): no wasted MMA / activation TMA
 constexpr int BK = 64;         // K per stage (one SWIZZLE_128B atom of bf16)
 constexpr int STAGES = 4;
 constexpr int kDqWarps = 8;
@@ -112,6 +113,7 @@ struct TcProb {
   void* C;
   int M, K, N, group, cdt;
   int m_tiles, n_tiles;
+  int bn;            // tokens per tile (UMMA N): min(256, round_up(M, 16))
   int gm;            // token tiles per raster group
   int tile_begin;
 };
@@ -179,9 +181,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
           while (r0 >= p.group) { r0 -= p.group; ++j0; }
           mbar_wait(&empty_bar[s], ph ^ 1);
           uint8_t* st = sbase + s * Gm::STAGE;
-          mbar_arrive_expect_tx(&full_bar[s], kActBytes + Gm::CODE_BYTES + kScRows * BM * 2);
+          mbar_arrive_expect_tx(&full_bar[s], p.bn * BK * 2 + Gm::CODE_BYTES + kScRows * BM * 2);
           tma_load_2d(st + Gm::SC_OFS, &p.s, &full_bar[s], nt * BM, j0, pol_q);
-          tma_load_2d(st, &p.a, &full_bar[s], kb * BK, mt * BN, pol_a);
+          tma_load_2d(st, &p.a, &full_bar[s], kb * BK, mt * p.bn, pol_a);
           tma_load_2d(st + kActBytes, &p.q, &full_bar[s], kb * Gm::CODE_BYTES_ROW, nt * BM, pol_q);
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
@@ -190,12 +192,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_f16<T, BM, BN>();
       const uint32_t sb = smem_u32(sbase);
       int s = 0;
       uint32_t ph = 0, acc_ph = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int kblocks = (find_prob(batch, tile).K + BK - 1) / BK;
+        const TcProb& pp = find_prob(batch, tile);
+        const int kblocks = (pp.K + BK - 1) / BK;
+        const uint32_t idesc = idesc_f16<T, BM, 16>() + ((uint32_t)((pp.bn >> 3) - 2) << 17);  // N = bn
         mbar_wait(&acc_empty, acc_ph ^ 1);  // epilogue drained the accumulator
         fence_after();
         for (int kb = 0; kb < kblocks; ++kb) {
@@ -292,9 +295,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       mbar_wait(&acc_full, acc_ph);
       acc_ph ^= 1;
       fence_after();
-      const int tok_base = mt * BN + half * 128;
+      const int tok_base = mt * p.bn + half * 128;
 #pragma unroll 1
-      for (int c0 = 0; c0 < 128; c0 += 32) {
+      for (int c0 = 0; c0 < 128 && half * 128 + c0 < p.bn; c0 += 32) {
         uint32_t v[32];
         tmem_ld32(tmem + lane_base + kAccCol + half * 128 + c0, v);
         tmem_wait_ld();
@@ -327,7 +330,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
 // ------------------------------------------------------------------------------------- host side
 static bool make_tc_prob(tc::TcProb& d, int bits, const void* A, int M, int K, int N, const void* codes,
                          const void* scales, int group, void* C, int cdt) {
-  if (!make_tmap_2d(&d.a, A, 2, (uint64_t)K, (uint64_t)M, (uint64_t)K * 2, tc::BK, tc::BN, 128)) return false;
+#ifdef FQ_TC_FULLBN
+  d.bn = tc::BN;  // diagnostics: always 256-token tiles
+#else
+  d.bn = std::min(tc::BN, (M + 15) / 16 * 16);
+#endif
+  if (!make_tmap_2d(&d.a, A, 2, (uint64_t)K, (uint64_t)M, (uint64_t)K * 2, tc::BK, d.bn, 128)) return false;
   const uint64_t row_bytes = (uint64_t)K * bits / 8;
   if (!make_tmap_2d(&d.q, codes, 1, row_bytes, (uint64_t)N, row_bytes, tc::BK * bits / 8, tc::BM,
                     bits == 4 ? 32 : 64))
@@ -338,7 +346,7 @@ static bool make_tc_prob(tc::TcProb& d, int bits, const void* A, int M, int K, i
   d.scales = scales;
   d.C = C;
   d.M = M; d.K = K; d.N = N; d.group = group; d.cdt = cdt;
-  d.m_tiles = (M + tc::BN - 1) / tc::BN;
+  d.m_tiles = (M + d.bn - 1) / d.bn;
   d.n_tiles = (N + tc::BM - 1) / tc::BM;
   const char* gme = std::getenv("FQ_TC_GM");
   d.gm = gme ? std::max(1, std::atoi(gme)) : 8;
