@@ -40,6 +40,9 @@ namespace fq {
 #ifndef FQ_DEC_EARLY
 #define FQ_DEC_EARLY 1  // consumers release a stage as soon as its data is in registers
 #endif
+#ifndef FQ_DEC_EARLY2
+#define FQ_DEC_EARLY2 0  // two 8-token MMA tiles (9 <= M <= 16): release after the MMAs (measured 8% faster)
+#endif
 constexpr int kConsumerWarps = FQ_DEC_CW;
 // TMA warp + consumers (+ one activation-stager warp unless the activations were pre-converted)
 template <bool PRE> constexpr int dec_threads() { return 32 * (1 + kConsumerWarps + (PRE ? 0 : 1)); }
@@ -270,7 +273,11 @@ template <typename T, int BITS, int MT, bool SACC, int DBG, int MAXP>
 #ifndef FQ_DEC_NIB_MAXREG
 #define FQ_DEC_NIB_MAXREG 96  // measured: faster than 104 or 112 (which ptxas schedules worse)
 #endif
-__global__ void __maxnreg__((FQ_NIB && BITS == 4 && SACC) ? FQ_DEC_NIB_MAXREG : 96) decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
+#ifndef FQ_DEC_NIB2_MAXREG
+#define FQ_DEC_NIB2_MAXREG 112  // two 8-token MMA tiles (9 <= M <= 16); 2 CTAs x 288 threads fit 113
+#endif
+__global__ void __maxnreg__((FQ_NIB && BITS == 4 && SACC) ? (MT == 2 ? FQ_DEC_NIB2_MAXREG : FQ_DEC_NIB_MAXREG) : 96)
+decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
   using G = DecGeom<BITS>;
   using SG = DecStage<BITS, MT>;
   constexpr int KS = G::KS, SEG = G::SEG, KCH = G::KCH, CHUNKS = G::CHUNKS, PIECES = G::PIECES;
@@ -286,6 +293,7 @@ __global__ void __maxnreg__((FQ_NIB && BITS == 4 && SACC) ? FQ_DEC_NIB_MAXREG : 
   using TC = typename std::conditional<NIB, __half, T>::type;  // MMA operand type
   constexpr float OFF = NIB ? 1.f : (SACC ? CodeOffset<T, BITS>::v : 0.f);  // NIB: sums hold the correction
   constexpr int PPC = KCH / 8;  // 8-element pieces per chunk (16 int4, 8 int8): divides 32
+  constexpr bool EARLY = MT == 2 ? FQ_DEC_EARLY2 : FQ_DEC_EARLY;
 
   extern __shared__ __align__(1024) uint8_t dsmem[];
   __shared__ __align__(8) uint64_t full_bar[kMaxDecStages], empty_bar[kMaxDecStages], raw_bar[kMaxDecStages];
@@ -508,7 +516,7 @@ __global__ void __maxnreg__((FQ_NIB && BITS == 4 && SACC) ? FQ_DEC_NIB_MAXREG : 
         wgv[rt] = lds128(wst + wofs_g[rt]);
         whv[rt] = lds128(wst + wofs_h[rt]);
       }
-      if (FQ_DEC_EARLY) {
+      if (EARLY) {
         // everything this warp needs from the stage is in registers: hand the slot back to the TMA
         // producer now, so the next loads overlap this warp's dequant + MMA work
         __syncwarp();
@@ -616,7 +624,7 @@ __global__ void __maxnreg__((FQ_NIB && BITS == 4 && SACC) ? FQ_DEC_NIB_MAXREG : 
         }
       }
     }
-    if (!FQ_DEC_EARLY || DBG == 3) {
+    if (!EARLY || DBG == 3) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[s]);
     }
