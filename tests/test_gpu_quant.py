@@ -59,6 +59,19 @@ def test_quantize_exact_groups(fq, bits, group):
     check_exact(fq, W, "bf16", bits, group, "bf16")
 
 
+@pytest.mark.parametrize("wdt,sdt", [("bf16", "bf16"), ("fp16", "fp16"), ("bf16", "fp16")])
+def test_quantize_nonfinite_zero_groups(fq, wdt, sdt):
+    """Non-finite elements and all-zero groups at a 512-wide shape, three (bits, group) pairs."""
+    from synth import f32_to_bf16_bits
+    W = np.random.default_rng(5).normal(0, 0.02, (24, 512)).astype(np.float32)
+    W[1, 3] = np.inf
+    W[2, 300] = np.nan
+    W[5, 128:256] = 0.0
+    bitsW = f32_to_bf16_bits(W) if wdt == "bf16" else W.astype(np.float16).view(np.uint16)
+    for bits, group in ((4, 128), (8, 64), (4, 16)):
+        check_exact(fq, bitsW, wdt, bits, group, sdt)
+
+
 @pytest.mark.parametrize("wdt", ["bf16", "fp16", "fp32"])
 @pytest.mark.parametrize("sdt", ["bf16", "fp16"])
 def test_quantize_exact_dtypes(fq, wdt, sdt):
