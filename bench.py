@@ -330,13 +330,19 @@ def main():
     # ---- roofline of the dominant kernel (A4 decode GEMM = every GEMM launch of the step)
     gemv_s = sum(per.values()) / 1e3
     achieved_gbs = step_bytes_rank / gemv_s / 1e9
-    traffic = None
+    # DRAM traffic per launch of the dominant kernel from the committed ncu --set full capture
+    # (FC1, M=1): compare with the algorithmic bytes of the same launch (311,427,072).
+    traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get("decode_dram_bytes_per_step")
+            tj = json.load(f)
+        d1 = tj.get("decode_fc1_m1")
+        if d1:
+            traffic = d1["dram_bytes_read"] + d1["dram_bytes_write"]
+            traffic_src = "bytes per launch, FC1 M=1, " + tj.get("source", "")
     roof = {"bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-            "frac": round(achieved_gbs / peaks["hbm_gbs"], 4), "traffic": traffic,
+            "frac": round(achieved_gbs / peaks["hbm_gbs"], 4), "traffic": traffic, "traffic_source": traffic_src,
             "peak_source": peaks["source"], "kernel": "fq::decode_kernel (A4/A5) + its fq::prep_acts_kernel (bracketed together)",
             "algorithmic_bytes_per_step_per_rank": step_bytes_rank,
             "per_launch_us": {n: round(v * 1e3, 2) for n, v in per.items()},
