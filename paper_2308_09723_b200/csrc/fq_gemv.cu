@@ -66,13 +66,13 @@ struct DecGeom {
 
 // Stage = [packed weights 256 x 64 B][activations MT*8 x KS (TMA, then permuted in place by the
 // stager)][256 scales][per-token activation sums].  As many stages as fit two CTAs per SM.
-template <int BITS, int MT>
+template <int BITS, int MT, bool SACC>
 struct DecStage {
   using G = DecGeom<BITS>;
   static constexpr int ACT_OFS = kStageW;
   static constexpr int ACT_BYTES = MT * 8 * G::ROWB;
   static constexpr int SC_OFS = ACT_OFS + ACT_BYTES;  // TMA destinations: 128-byte aligned
-  static constexpr int SC_BYTES = kRowsPerCta * 2;
+  static constexpr int SC_BYTES = kRowsPerCta * 2 * (SACC ? 1 : 8);  // per-element path: up to 8 rows
   static constexpr int SUM_OFS = SC_OFS + SC_BYTES;
   static constexpr int SUM_BYTES = MT * 8 * 16;  // per token: offset correction, inverse scale (+pad)
   static constexpr int BYTES = ((SUM_OFS + SUM_BYTES + 1023) / 1024) * 1024;
@@ -98,6 +98,9 @@ struct DecProb {
   int M, K, N, group, klen, cdt;
   int gx, splits, ktiles, cta_begin;
   int tok_base;   // nibble path: global token index of row 0 (parity of the pre-converted layout)
+  int sc_rows;    // per-element-scale path: scale rows per stage staged by TMA (KS / group), 0 = read
+                  // from global memory (groups that do not divide the stage)
+  int sc_shift;   // log2(group) when sc_rows > 0
 };
 template <int MAXP>
 struct DecBatch {
@@ -279,7 +282,7 @@ template <typename T, int BITS, int MT, bool SACC, int DBG, int MAXP>
 __global__ void __maxnreg__((FQ_NIB && BITS == 4 && SACC) ? (MT == 2 ? FQ_DEC_NIB2_MAXREG : FQ_DEC_NIB_MAXREG) : 96)
 decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
   using G = DecGeom<BITS>;
-  using SG = DecStage<BITS, MT>;
+  using SG = DecStage<BITS, MT, SACC>;
   constexpr int KS = G::KS, SEG = G::SEG, KCH = G::KCH, CHUNKS = G::CHUNKS, PIECES = G::PIECES;
   constexpr int ROWB = G::ROWB;
   constexpr int NSTG = SG::N;
@@ -340,7 +343,8 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
       auto issue_w = [&](int i, int s) {  // the stage's packed weights + scales (+ expect_tx)
         uint8_t* st = sbase + s * STAGE_BYTES;
         const int k0 = kbeg + i * KS;
-        mbar_arrive_expect_tx(&full_bar[s], kStageW + (SACC ? SC_BYTES : 0) + (NIB ? RAW_BYTES + MT * 8 * 16 : 0));
+        const int scb = SACC ? kRowsPerCta * 2 : p.sc_rows * kRowsPerCta * 2;
+        mbar_arrive_expect_tx(&full_bar[s], kStageW + scb + (NIB ? RAW_BYTES + MT * 8 * 16 : 0));
 #pragma unroll
         for (int bx2 = 0; bx2 < kWBoxes; ++bx2)
           tma_load_2d(st + bx2 * kWBoxRows * kWBytesPerRow, &p.w, &full_bar[s], k0 * BITS / 8,
@@ -350,6 +354,11 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
           for (int bx2 = 0; bx2 < kWBoxes; ++bx2)
             tma_load_2d(st + SC_OFS + bx2 * kWBoxRows * 2, &p.s, &full_bar[s], n0 + bx2 * kWBoxRows, gj, polw);
           if (++grem == gm) { grem = 0; ++gj; }
+        } else if (p.sc_rows) {
+#pragma unroll
+          for (int bx2 = 0; bx2 < kWBoxes; ++bx2)
+            tma_load_2d(st + SC_OFS + bx2 * kWBoxRows * 2, &p.s, &full_bar[s], n0 + bx2 * kWBoxRows,
+                        k0 >> p.sc_shift, polw);
         }
       };
       auto issue_a = [&](int i, int s) {  // the stage's activations (+ per-chunk sums)
@@ -516,6 +525,21 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
         wgv[rt] = lds128(wst + wofs_g[rt]);
         whv[rt] = lds128(wst + wofs_h[rt]);
       }
+      // per-element-scale path with TMA-staged scale rows: into registers before the stage is
+      // released (the producer may overwrite it right after the early release below)
+      uint32_t scg[2][4], sch[2][4];
+      if (!SACC && p.sc_rows) {
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const uint32_t so = wst + SC_OFS + (((t * SEG + w * (SEG / 4)) >> p.sc_shift) * kRowsPerCta) * 2;
+#pragma unroll
+          for (int rt = 0; rt < 2; ++rt) {
+            const uint32_t vg = lds_u16(so + Rg[rt] * 2), vh = lds_u16(so + Rh[rt] * 2);
+            scg[rt][w] = vg | (vg << 16);
+            sch[rt][w] = vh | (vh << 16);
+          }
+        }
+      }
       if (EARLY) {
         // everything this warp needs from the stage is in registers: hand the slot back to the TMA
         // producer now, so the next loads overlap this warp's dequant + MMA work
@@ -539,10 +563,15 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
         for (int w = 0; w < 4; ++w) {
           uint32_t sgs = 0, shs = 0;
           if (!SACC) {  // small / odd groups: q*s in the activation dtype before the MMA
-            const int kw = k0 + t * SEG + w * (SEG / 4);
-            const size_t j = (size_t)(kw / p.group) * N;
-            sgs = splat_scale<T>(S, j + ng[rt]);
-            shs = splat_scale<T>(S, j + nh[rt]);
+            if (p.sc_rows) {  // the stage's scale rows (TMA-staged, read above)
+              sgs = scg[rt][w];
+              shs = sch[rt][w];
+            } else {
+              const int kw = k0 + t * SEG + w * (SEG / 4);
+              const size_t j = (size_t)(kw / p.group) * N;
+              sgs = splat_scale<T>(S, j + ng[rt]);
+              shs = splat_scale<T>(S, j + nh[rt]);
+            }
           }
           float(*dst)[4] = SACC ? part : acc[rt];
           if (BITS == 4) {
@@ -832,7 +861,7 @@ static cudaError_t launch_prep(int adt, const void* A, int ntok, int K, void* Ap
 
 template <typename T, int BITS, int MT, bool SACC, int DBG, int MAXP>
 static cudaError_t launch_dec(const DecBatch<MAXP>& b, int ctas, cudaStream_t st) {
-  constexpr int smem = DecStage<BITS, MT>::SMEM;
+  constexpr int smem = DecStage<BITS, MT, SACC>::SMEM;
   auto kern = decode_kernel<T, BITS, MT, SACC, DBG, MAXP>;
   static bool attr_set = false;  // benign race: idempotent attribute call
   if (!attr_set) {
@@ -884,7 +913,13 @@ static bool make_dec_prob(DecProb& d, const GemvPlan& pl, int bits, int cdt, con
   if (Sp && !make_tmap_2d(&d.sm, reinterpret_cast<const char*>(Sp) + (size_t)tok_base * 16, 4, (uint64_t)M * 4,
                           (uint64_t)(K / 128), (uint64_t)ntok_all * 16, pl.mt * 8 * 4, 1, 0))
     return false;
-  if (!make_tmap_2d(&d.s, scales, 2, (uint64_t)N, (uint64_t)(K / group), (uint64_t)N * 2, kWBoxRows, 1, 0))
+  // per-element-scale path (group does not cover a stage): stage the KS / group scale rows by TMA
+  // when the group divides the stage (then a power of two >= 16), else read them from global memory
+  const bool sacc = group % ks == 0;
+  d.sc_rows = (!sacc && ks % group == 0) ? ks / group : 0;
+  d.sc_shift = d.sc_rows ? __builtin_ctz((unsigned)group) : 0;
+  if (!make_tmap_2d(&d.s, scales, 2, (uint64_t)N, (uint64_t)(K / group), (uint64_t)N * 2, kWBoxRows,
+                    d.sc_rows ? d.sc_rows : 1, 0))
     return false;
   d.scales = scales;
   d.C = C;

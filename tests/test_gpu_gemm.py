@@ -135,6 +135,20 @@ def test_decode_multi_tile_determinism(fq, env, M, K, N):
     assert O.rel_err(torch_to_f64(C0), Cr, D) <= TOL
 
 
+@pytest.mark.parametrize("bits,group", [(4, 16), (4, 32), (4, 64), (8, 16), (8, 32)])
+@pytest.mark.parametrize("M", [1, 5, 12])
+def test_decode_small_groups_long_k(fq, env, bits, group, M):
+    """Groups smaller than the decode stage (scale rows staged by TMA per stage) with one CTA per
+    column tile streaming many more stages than its ring holds (FQ_GEMV_SPLITS=1): the scales must
+    be consumed before the stage is handed back to the producer."""
+    env("FQ_GEMM_PATH", "decode")
+    env("FQ_GEMV_SPLITS", 1)
+    Wb, Ab = make_case(M, 4096, 512, bits, group, seed=group + M, outliers=2)
+    _, C = run_case(fq, Wb, Ab, bits, group, "bf16", "fp32")
+    Cr, D = oracle_ref(Wb, Ab, bits, group, "bf16")
+    assert O.rel_err(torch_to_f64(C), Cr, D) <= TOL
+
+
 @pytest.mark.parametrize("path", ["decode", "tc"])
 def test_identity_exact_fp32_out(fq, env, path):
     """A = I (M = K = 256): C[k, n] = q[n,k] * s[k/g, n] exactly in fp32-output mode — catches any
