@@ -122,7 +122,10 @@ fq_status fq_quantize(const void* W, int32_t wdt, const fq_wdesc* d, void* codes
  *   ZERO-FILLED once before its first use; every call leaves the counters zeroed again, so one
  *   buffer (sized for the largest call) can be shared by calls of any shape and graph-captured
  *   without re-clearing.  Calls sharing one ws must be stream-ordered.
- * Accumulation is fp32; results are deterministic (fixed-order split-K reduction).
+ * Accumulation is fp32; results are deterministic (fixed-order split-K reduction).  Both paths
+ *   split K over CTAs when the output tiles alone cannot fill the GPU (A4: always planned; A6: when
+ *   its 128-row x round_up(M,16)-token tiles are fewer than the SMs); a NULL/short ws on the A6 path
+ *   just disables its split.
  * ------------------------------------------------------------------------------------------- */
 size_t fq_gemm_workspace_bytes(int64_t M, const fq_wdesc* d);
 fq_status fq_gemm(const void* A, int32_t adt, int64_t M, const fq_wdesc* d, const void* codes,

@@ -141,7 +141,7 @@ fq_status fq_quantize(const void* W, int32_t wdt, const fq_wdesc* d, void* codes
 
 size_t fq_gemm_workspace_bytes(int64_t M, const fq_wdesc* d) {
   if (check_wdesc(d) != FQ_OK || M <= 0) return 0;
-  if (use_tc_path(M)) return 256;
+  if (use_tc_path(M)) return gemm_tc_workspace_bytes((int)M, (int)d->K, (int)d->N);
   if (decode_tc_supported(d->bits, d->group, (int)M))
     return dtc_workspace_bytes(M, (int)d->K, num_sms());
   const GemvPlan p = plan_gemv((int)M, (int)d->K, (int)d->N, d->bits, d->group, num_sms());
@@ -159,7 +159,7 @@ fq_status fq_gemm(const void* A, int32_t adt, int64_t M, const fq_wdesc* d, cons
   if (M <= 0 || M > (1 << 20)) return FQ_ERR_SHAPE;
   if (use_tc_path(M))
     return from_cuda(run_gemm_tc(adt, cdt, d->bits, A, (int)M, (int)d->K, (int)d->N, codes, scales,
-                                 d->group, C, as_stream(stream)));
+                                 d->group, C, ws, ws_bytes, as_stream(stream)));
   if (decode_tc_supported(d->bits, d->group, (int)M)) {
     const size_t need = dtc_workspace_bytes(M, (int)d->K, num_sms());
     if (need > 65536 && (!ws || ws_bytes < need)) return FQ_ERR_WORKSPACE;

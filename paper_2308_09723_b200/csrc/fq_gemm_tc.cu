@@ -35,23 +35,32 @@ constexpr int BM = 128;        // weight rows per tile (UMMA M)
 constexpr int BN = 256;        // max tokens per tile (UMMA N); a problem with M < 256 uses
                                // bn = round_up(M, 16) (TcProb::bn): no wasted MMA / activation TMA
 constexpr int BK = 64;         // K per stage (one SWIZZLE_128B atom of bf16)
-constexpr int STAGES = 4;
 constexpr int kDqWarps = 8;
 constexpr int kThreads = 32 * (2 + kDqWarps);
-constexpr int kActBytes = BN * BK * 2;     // 32 KB
 constexpr int kTmemCols = 512;
-constexpr int kAccCol = 0;                 // accumulator columns [0, 256)
-constexpr int kACol = 256;                 // A stages: [256 + 32 s, 256 + 32 s + 32)
+constexpr int kAccCol = 0;                 // accumulator columns [0, BNMAX)
 constexpr int kScRows = 5;                 // scale rows staged per K block (>= ceil(63/g) + 1, g >= 16)
+constexpr int kSmemMax = 227 * 1024 - 2048;
 
-template <int BITS>
+// Stage geometry of one kernel variant.  BNMAX = widest token tile it serves: a small-M variant
+// has small activation tiles, so it keeps many more K blocks (codes) in flight -- at M <= 128 the
+// kernel is bound by HBM latency x bytes in flight, not by the tensor cores.
+//   TMEM: accumulator columns [0, BNMAX), A slot s at BNMAX + 32 s (one per stage).
+template <int BITS, int BNMAX>
 struct Geo {
+  static constexpr int ACT_BYTES = BNMAX * BK * 2;            // 32 / 16 / 8 KB
   static constexpr int CODE_BYTES_ROW = BK * BITS / 8;        // 32 (int4) / 64 (int8)
   static constexpr int CODE_BYTES = BM * CODE_BYTES_ROW;      // 4 KB / 8 KB
-  static constexpr int SC_OFS = kActBytes + CODE_BYTES;       // scale rows of the K block
+  static constexpr int SC_OFS = ACT_BYTES + CODE_BYTES;       // scale rows of the K block
   static constexpr int SC_BYTES = kScRows * BM * 2;
   static constexpr int STAGE = ((SC_OFS + SC_BYTES + 1023) / 1024) * 1024;
+  static constexpr int S_SMEM = (kSmemMax - 1024) / STAGE;
+  static constexpr int S_TMEM = (kTmemCols - BNMAX) / 32;
+  static constexpr int S0 = S_SMEM < S_TMEM ? S_SMEM : S_TMEM;
+  static constexpr int STAGES = S0 > 16 ? 16 : S0;
   static constexpr int SMEM = STAGES * STAGE + 1024;
+  static constexpr int A_COL = BNMAX;
+  static_assert(STAGES >= 4, "stages");
 };
 
 using namespace tc5;
@@ -116,7 +125,22 @@ struct TcProb {
   int bn;            // tokens per tile (UMMA N): min(256, round_up(M, 16))
   int gm;            // token tiles per raster group
   int tile_begin;
+  int splits, kbs;   // split-K (few output tiles): K-block ranges of kbs blocks per work item
+  float* ws;         // split-K fp32 partials [tiles * splits][bn][128]
+  int* ctr;          // split-K arrival counters per output tile (self-resetting)
 };
+// work item -> (token tile, weight-row tile, K-block range); work items of one output tile are
+// consecutive (its K splits run concurrently on neighbouring CTAs)
+__device__ __forceinline__ void work_coords(const TcProb& p, int item, int& mt, int& nt, int& t, int& ks,
+                                            int& kb0, int& kb1) {
+  const int local = item - p.tile_begin;
+  t = local / p.splits;
+  ks = local - t * p.splits;
+  tile_coords(t, p.m_tiles, p.n_tiles, p.gm, mt, nt);
+  const int kblocks = (p.K + BK - 1) / BK;
+  kb0 = ks * p.kbs;
+  kb1 = min(kblocks, kb0 + p.kbs);
+}
 template <int MAXP>
 struct TcBatch {
   TcProb p[MAXP];
@@ -130,13 +154,16 @@ __device__ __forceinline__ const TcProb& find_prob(const TcBatch<MAXP>& b, int t
   return b.p[pi];
 }
 
-template <typename T, int BITS, int MAXP>
+template <typename T, int BITS, int MAXP, int BNMAX>
 __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_constant__ TcBatch<MAXP> batch) {
-  using Gm = Geo<BITS>;
+  using Gm = Geo<BITS, BNMAX>;
+  constexpr int STAGES = Gm::STAGES;
+  constexpr int kACol = Gm::A_COL;
   extern __shared__ __align__(1024) uint8_t dsmem[];
   __shared__ __align__(8) uint64_t full_bar[STAGES], afull_bar[STAGES], empty_bar[STAGES];
   __shared__ __align__(8) uint64_t acc_full, acc_empty;
   __shared__ uint32_t tmem_base_sh;
+  __shared__ int s_last;
   uint8_t* sbase = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsmem) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = batch.total_tiles;
@@ -173,18 +200,18 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       uint32_t ph = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const TcProb& p = find_prob(batch, tile);
-        const int kblocks = (p.K + BK - 1) / BK;
-        int mt, nt;
-        tile_coords(tile - p.tile_begin, p.m_tiles, p.n_tiles, p.gm, mt, nt);
-        int j0 = 0, r0 = 0;  // first scale row of the K block = floor(64 kb / g), division-free
-        for (int kb = 0; kb < kblocks; ++kb, r0 += BK) {
+        int mt, nt, tt, ks, kb0, kb1;
+        work_coords(p, tile, mt, nt, tt, ks, kb0, kb1);
+        // first scale row of the K block = floor(64 kb / g), division-free after the first block
+        int j0 = (kb0 * BK) / p.group, r0 = (kb0 * BK) - j0 * p.group;
+        for (int kb = kb0; kb < kb1; ++kb, r0 += BK) {
           while (r0 >= p.group) { r0 -= p.group; ++j0; }
           mbar_wait(&empty_bar[s], ph ^ 1);
           uint8_t* st = sbase + s * Gm::STAGE;
           mbar_arrive_expect_tx(&full_bar[s], p.bn * BK * 2 + Gm::CODE_BYTES + kScRows * BM * 2);
           tma_load_2d(st + Gm::SC_OFS, &p.s, &full_bar[s], nt * BM, j0, pol_q);
           tma_load_2d(st, &p.a, &full_bar[s], kb * BK, mt * p.bn, pol_a);
-          tma_load_2d(st + kActBytes, &p.q, &full_bar[s], kb * Gm::CODE_BYTES_ROW, nt * BM, pol_q);
+          tma_load_2d(st + Gm::ACT_BYTES, &p.q, &full_bar[s], kb * Gm::CODE_BYTES_ROW, nt * BM, pol_q);
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
       }
@@ -197,11 +224,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       uint32_t ph = 0, acc_ph = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const TcProb& pp = find_prob(batch, tile);
-        const int kblocks = (pp.K + BK - 1) / BK;
+        int mt_, nt_, tt_, ks_, kb0, kb1;
+        work_coords(pp, tile, mt_, nt_, tt_, ks_, kb0, kb1);
         const uint32_t idesc = idesc_f16<T, BM, 16>() + ((uint32_t)((pp.bn >> 3) - 2) << 17);  // N = bn
         mbar_wait(&acc_empty, acc_ph ^ 1);  // epilogue drained the accumulator
         fence_after();
-        for (int kb = 0; kb < kblocks; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[s], ph);
           mbar_wait(&afull_bar[s], ph);
           fence_after();
@@ -209,7 +237,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk)
             mma_ts(tmem + kAccCol, tmem + kACol + s * 32 + kk * 8, bdesc + (uint64_t)(kk * 2), idesc,
-                   (kb | kk) != 0);
+                   (kb != kb0) || (kk != 0));
           mma_commit(&empty_bar[s]);
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
@@ -229,16 +257,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     uint32_t ph = 0, acc_ph = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const TcProb& p = find_prob(batch, tile);
-      const int K = p.K, N = p.N, M = p.M;
-      const int kblocks = (K + BK - 1) / BK;
-      int mt, nt;
-      tile_coords(tile - p.tile_begin, p.m_tiles, p.n_tiles, p.gm, mt, nt);
+      const int N = p.N, M = p.M;
+      int mt, nt, tt, ks, kb0, kb1;
+      work_coords(p, tile, mt, nt, tt, ks, kb0, kb1);
       const int n = nt * BM + row;
       const int nc = min(n, N - 1);
-      int j0 = 0, r0 = 0;            // first staged scale row = floor(64 kb / g)
-      int jb = 0, gk = half * 32;     // group of this thread's first k (kb*64 + half*32) and offset
-      while (gk >= p.group) { gk -= p.group; ++jb; }
-      for (int kb = 0; kb < kblocks; ++kb) {
+      int j0 = (kb0 * BK) / p.group, r0 = kb0 * BK - j0 * p.group;  // first staged scale row
+      // group of this thread's first k (kb0*64 + half*32) and its offset in the group
+      int jb = (kb0 * BK + half * 32) / p.group, gk = kb0 * BK + half * 32 - jb * p.group;
+      for (int kb = kb0; kb < kb1; ++kb) {
         // scales of this thread's 8-k words from the TMA-staged rows: word w lies in group
         // jb + t, t = [gk + 8w >= g] + [gk + 8w >= 2g]; row index in smem = group - j0.
         mbar_wait(&full_bar[s], ph);
@@ -250,7 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
           const uint32_t v = lds_u16(sb + s * Gm::STAGE + Gm::SC_OFS + (jr * BM + row) * 2);
           sc[w] = v | (v << 16);
         }
-        const uint32_t qbase = sb + s * Gm::STAGE + kActBytes + row * Gm::CODE_BYTES_ROW;
+        const uint32_t qbase = sb + s * Gm::STAGE + Gm::ACT_BYTES + row * Gm::CODE_BYTES_ROW;
         uint32_t out[16];
         if (BITS == 4) {
           // 16 bytes = 32 codes; SWIZZLE_32B: 16-byte chunk c of row r sits at c ^ ((r >> 2) & 1)
@@ -296,26 +323,73 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       acc_ph ^= 1;
       fence_after();
       const int tok_base = mt * p.bn + half * 128;
+      auto store = [&](int tok, float f) {
+        if (p.cdt == FQ_FP32) reinterpret_cast<float*>(p.C)[(size_t)tok * N + n] = f;
+        else reinterpret_cast<T*>(p.C)[(size_t)tok * N + n] = Dt<T>::from_f(f);
+      };
+      // split-K: this item's fp32 partial [bn][128] of output tile tt, slot ks
+      float* part = p.splits > 1 ? p.ws + (size_t)(tt * p.splits + ks) * p.bn * BM : nullptr;
 #pragma unroll 1
       for (int c0 = 0; c0 < 128 && half * 128 + c0 < p.bn; c0 += 32) {
         uint32_t v[32];
         tmem_ld32(tmem + lane_base + kAccCol + half * 128 + c0, v);
         tmem_wait_ld();
-        if (n < N) {
+        if (part) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (half * 128 + c0 + i < p.bn) __stcg(part + (half * 128 + c0 + i) * BM + row, __uint_as_float(v[i]));
+        } else if (n < N) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             const int tok = tok_base + c0 + i;
-            if (tok < M) {
-              const float f = __uint_as_float(v[i]);
-              if (p.cdt == FQ_FP32) reinterpret_cast<float*>(p.C)[(size_t)tok * N + n] = f;
-              else reinterpret_cast<T*>(p.C)[(size_t)tok * N + n] = Dt<T>::from_f(f);
-            }
+            if (tok < M) store(tok, __uint_as_float(v[i]));
           }
         }
       }
       fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty);
+      if (lane == 0) mbar_arrive(&acc_empty);  // the accumulator is free for the next item
+      if (part) {
+        // last-arriving split of the tile sums the partials in split order (deterministic)
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kDqWarps));
+        if (threadIdx.x == 64) {
+          __threadfence();
+          const int last = atomicAdd(&p.ctr[tt], 1) == p.splits - 1;
+          if (last) __threadfence();
+          s_last = last;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kDqWarps));
+        if (s_last) {
+          // 256 threads: thread -> (row = tid % 128, tokens tid / 128 + 2i); 4 tokens per round so
+          // their split loads are in flight together; rows are contiguous -> coalesced
+          const float* base = p.ws + (size_t)tt * p.splits * p.bn * BM;
+          const int tid = threadIdx.x - 64, r = tid & (BM - 1);
+          const int nr = nt * BM + r;
+          const int tmax = min(p.bn, M - mt * p.bn);
+          if (nr < N) {
+            for (int tl0 = tid >> 7; tl0 < tmax; tl0 += 8) {
+              float acc[4] = {0.f, 0.f, 0.f, 0.f};
+              for (int q = 0; q < p.splits; ++q) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  const int tl = tl0 + 2 * u;
+                  if (tl < tmax) acc[u] += __ldcg(base + ((size_t)q * p.bn + tl) * BM + r);
+                }
+              }
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int tl = tl0 + 2 * u;
+                if (tl < tmax) {
+                  const size_t o = (size_t)(mt * p.bn + tl) * N + nr;
+                  if (p.cdt == FQ_FP32) reinterpret_cast<float*>(p.C)[o] = acc[u];
+                  else reinterpret_cast<T*>(p.C)[o] = Dt<T>::from_f(acc[u]);
+                }
+              }
+            }
+          }
+          if (threadIdx.x == 64) p.ctr[tt] = 0;  // self-reset for the next launch
+        }
+      }
     }
   }
   __syncthreads();
@@ -350,13 +424,39 @@ static bool make_tc_prob(tc::TcProb& d, int bits, const void* A, int M, int K, i
   d.n_tiles = (N + tc::BM - 1) / tc::BM;
   const char* gme = std::getenv("FQ_TC_GM");
   d.gm = gme ? std::max(1, std::atoi(gme)) : 8;
+  d.splits = 1;
+  d.kbs = (K + tc::BK - 1) / tc::BK;
+  d.ws = nullptr;
+  d.ctr = nullptr;
   return true;
 }
 
-template <typename T, int BITS, int MAXP>
+// Split-K plan of one GEMM: when its output tiles cannot fill the SMs (e.g. M <= 256 on a weight
+// matrix of < 148 x 128 rows), K is cut into ranges of >= 8 K blocks so ~one work item per SM runs.
+constexpr size_t kTcCounterBytes = 65536;
+static int tc_splits(int M, int K, int N) {
+  const int bn = std::min(tc::BN, (M + 15) / 16 * 16);
+  const int tiles = ((M + bn - 1) / bn) * ((N + tc::BM - 1) / tc::BM);
+  const int kblocks = (K + tc::BK - 1) / tc::BK;
+  const char* e = std::getenv("FQ_TC_SPLITS");
+  int s = e ? std::atoi(e) : num_sms() / std::max(1, tiles);
+  s = std::max(1, std::min(s, kblocks / 8));
+  if (tiles > (int)(kTcCounterBytes / sizeof(int))) s = 1;
+  const int kbs = (kblocks + s - 1) / s;
+  return (kblocks + kbs - 1) / kbs;
+}
+size_t gemm_tc_workspace_bytes(int M, int K, int N) {
+  const int s = tc_splits(M, K, N);
+  if (s == 1) return 256;
+  const int bn = std::min(tc::BN, (M + 15) / 16 * 16);
+  const size_t tiles = (size_t)((M + bn - 1) / bn) * ((N + tc::BM - 1) / tc::BM);
+  return kTcCounterBytes + tiles * s * bn * tc::BM * sizeof(float);
+}
+
+template <typename T, int BITS, int MAXP, int BNMAX>
 static cudaError_t launch_tc(const tc::TcBatch<MAXP>& b, cudaStream_t st) {
-  using Gm = tc::Geo<BITS>;
-  auto kern = tc::gemm_tc_kernel<T, BITS, MAXP>;
+  using Gm = tc::Geo<BITS, BNMAX>;
+  auto kern = tc::gemm_tc_kernel<T, BITS, MAXP, BNMAX>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Gm::SMEM);
@@ -368,20 +468,39 @@ static cudaError_t launch_tc(const tc::TcBatch<MAXP>& b, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+template <int MAXP, int BNMAX>
+static cudaError_t dispatch_tc_bn(int adt, int bits, const tc::TcBatch<MAXP>& b, cudaStream_t st) {
+  if (adt == FQ_BF16)
+    return bits == 4 ? launch_tc<__nv_bfloat16, 4, MAXP, BNMAX>(b, st) : launch_tc<__nv_bfloat16, 8, MAXP, BNMAX>(b, st);
+  return bits == 4 ? launch_tc<__half, 4, MAXP, BNMAX>(b, st) : launch_tc<__half, 8, MAXP, BNMAX>(b, st);
+}
+// kernel variant = the widest token tile of the launch (64 / 128 / 256 tokens)
 template <int MAXP>
 static cudaError_t dispatch_tc(int adt, int bits, const tc::TcBatch<MAXP>& b, cudaStream_t st) {
-  if (adt == FQ_BF16)
-    return bits == 4 ? launch_tc<__nv_bfloat16, 4, MAXP>(b, st) : launch_tc<__nv_bfloat16, 8, MAXP>(b, st);
-  return bits == 4 ? launch_tc<__half, 4, MAXP>(b, st) : launch_tc<__half, 8, MAXP>(b, st);
+  int bn = 0;
+  for (int i = 0; i < b.nprob; ++i) bn = std::max(bn, b.p[i].bn);
+  if (std::getenv("FQ_TC_BNMAX256")) bn = 256;  // diagnostics: the large-M variant for every M
+  if (bn <= 64) return dispatch_tc_bn<MAXP, 64>(adt, bits, b, st);
+  if (bn <= 128) return dispatch_tc_bn<MAXP, 128>(adt, bits, b, st);
+  return dispatch_tc_bn<MAXP, 256>(adt, bits, b, st);
 }
 
 cudaError_t run_gemm_tc(int adt, int cdt, int bits, const void* A, int M, int K, int N, const void* codes,
-                        const void* scales, int group, void* C, cudaStream_t st) {
+                        const void* scales, int group, void* C, void* ws, size_t ws_bytes, cudaStream_t st) {
   tc::TcBatch<1> b{};
-  if (!make_tc_prob(b.p[0], bits, A, M, K, N, codes, scales, group, C, cdt)) return cudaErrorInvalidValue;
-  b.p[0].tile_begin = 0;
+  tc::TcProb& d = b.p[0];
+  if (!make_tc_prob(d, bits, A, M, K, N, codes, scales, group, C, cdt)) return cudaErrorInvalidValue;
+  const int s = tc_splits(M, K, N);
+  if (s > 1 && ws && ws_bytes >= gemm_tc_workspace_bytes(M, K, N)) {
+    const int kblocks = (K + tc::BK - 1) / tc::BK;
+    d.kbs = (kblocks + s - 1) / s;
+    d.splits = s;
+    d.ctr = reinterpret_cast<int*>(ws);
+    d.ws = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + kTcCounterBytes);
+  }
+  d.tile_begin = 0;
   b.nprob = 1;
-  b.total_tiles = b.p[0].m_tiles * b.p[0].n_tiles;
+  b.total_tiles = d.m_tiles * d.n_tiles * d.splits;
   return dispatch_tc<1>(adt, bits, b, st);
 }
 

@@ -800,7 +800,7 @@ static int env_int(const char* name, int dflt) {
 GemvPlan plan_gemv(int M, int K, int N, int bits, int group, int nsm) {
   (void)group;
   GemvPlan p{};
-  p.kchunk = bits == 4 ? 256 : 128;  // K per pipeline stage (splits are multiples of it)
+  p.kchunk = bits == 4 ? 256 : 128;  // split-K granularity (two kernel stages; one stage measured slower on small matrices)
   p.mt = M <= 8 ? 1 : 2;
   p.ktiles = (M + 15) / 16;
   p.rt = 2;

@@ -149,6 +149,23 @@ def test_decode_small_groups_long_k(fq, env, bits, group, M):
     assert O.rel_err(torch_to_f64(C), Cr, D) <= TOL
 
 
+@pytest.mark.parametrize("M,K,N,bits,group", [(32, 4096, 512, 4, 128), (100, 2048, 1280, 4, 64),
+                                               (300, 2048, 640, 8, 128), (17, 8192, 256, 4, 16)])
+def test_tc_split_k(fq, env, M, K, N, bits, group):
+    """A6 with few output tiles splits K over CTAs (fixed-order fp32 fixup): parity with the oracle,
+    bit-identical repeated calls, and the same result as the unsplit kernel within rounding."""
+    env("FQ_GEMM_PATH", "tc")
+    Wb, Ab = make_case(M, K, N, bits, group, seed=M + N)
+    _, C0 = run_case(fq, Wb, Ab, bits, group, "bf16", "fp32")
+    _, C1 = run_case(fq, Wb, Ab, bits, group, "bf16", "fp32")
+    assert torch.equal(C0, C1)
+    Cr, D = oracle_ref(Wb, Ab, bits, group, "bf16")
+    assert O.rel_err(torch_to_f64(C0), Cr, D) <= TOL
+    env("FQ_TC_SPLITS", 1)
+    _, C2 = run_case(fq, Wb, Ab, bits, group, "bf16", "fp32")
+    assert O.rel_err(torch_to_f64(C2), Cr, D) <= TOL
+
+
 @pytest.mark.parametrize("path", ["decode", "tc"])
 def test_identity_exact_fp32_out(fq, env, path):
     """A = I (M = K = 256): C[k, n] = q[n,k] * s[k/g, n] exactly in fp32-output mode — catches any
