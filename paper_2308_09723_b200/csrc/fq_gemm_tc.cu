@@ -35,8 +35,14 @@ constexpr int BM = 128;        // weight rows per tile (UMMA M)
 constexpr int BN = 256;        // max tokens per tile (UMMA N); a problem with M < 256 uses
                                // bn = round_up(M, 16) (TcProb::bn): no wasted MMA / activation TMA
 constexpr int BK = 64;         // K per stage (one SWIZZLE_128B atom of bf16)
-constexpr int kDqWarps = 8;
-constexpr int kThreads = 32 * (2 + kDqWarps);
+// Dequant warps per CTA: dq_warps(BNMAX) / 4 per TMEM lane quarter, each covering BK / parts k of a
+// K block.  Measured: 16 warps are faster for the small-tile variants (memory/latency-bound
+// regime), 8 for the 256-token variant (tensor-bound prefill).
+#ifndef FQ_TC_DQW
+#define FQ_TC_DQW 0  // diagnostics: force 8 or 16 for every variant
+#endif
+__host__ __device__ constexpr int dq_warps(int bnmax) { return FQ_TC_DQW ? FQ_TC_DQW : (bnmax == 256 ? 8 : 16); }
+__host__ __device__ constexpr int tc_threads(int bnmax) { return 32 * (2 + dq_warps(bnmax)); }
 constexpr int kTmemCols = 512;
 constexpr int kAccCol = 0;                 // accumulator columns [0, BNMAX)
 constexpr int kScRows = 5;                 // scale rows staged per K block (>= ceil(63/g) + 1, g >= 16)
@@ -155,7 +161,10 @@ __device__ __forceinline__ const TcProb& find_prob(const TcBatch<MAXP>& b, int t
 }
 
 template <typename T, int BITS, int MAXP, int BNMAX>
-__global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_constant__ TcBatch<MAXP> batch) {
+__global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __grid_constant__ TcBatch<MAXP> batch) {
+  constexpr int kDqWarps = dq_warps(BNMAX);
+  constexpr int kParts = kDqWarps / 4;
+  constexpr int kKPW = BK / kParts;  // k per dequant thread per K block (32 or 16)
   using Gm = Geo<BITS, BNMAX>;
   constexpr int STAGES = Gm::STAGES;
   constexpr int kACol = Gm::A_COL;
@@ -249,7 +258,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     // ------------------------------------------------------------------ dequant + epilogue
     const int dq = warp - 2;
     const int quarter = warp & 3;            // TMEM lane quarter this warp may access
-    const int half = dq >> 2;                // which 32 k of the 64-k block
+    const int half = dq >> 2;                // which kKPW k of the 64-k block (and token part)
     const int row = quarter * 32 + lane;     // weight row within the tile == TMEM lane
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const uint32_t sb = smem_u32(sbase);
@@ -263,38 +272,45 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       const int n = nt * BM + row;
       const int nc = min(n, N - 1);
       int j0 = (kb0 * BK) / p.group, r0 = kb0 * BK - j0 * p.group;  // first staged scale row
-      // group of this thread's first k (kb0*64 + half*32) and its offset in the group
-      int jb = (kb0 * BK + half * 32) / p.group, gk = kb0 * BK + half * 32 - jb * p.group;
+      // group of this thread's first k (kb0*64 + half*kKPW) and its offset in the group
+      int jb = (kb0 * BK + half * kKPW) / p.group, gk = kb0 * BK + half * kKPW - jb * p.group;
       for (int kb = kb0; kb < kb1; ++kb) {
         // scales of this thread's 8-k words from the TMA-staged rows: word w lies in group
         // jb + t, t = [gk + 8w >= g] + [gk + 8w >= 2g]; row index in smem = group - j0.
         mbar_wait(&full_bar[s], ph);
-        uint32_t sc[4];
+        constexpr int NW = kKPW / 8;  // 8-k words of this thread
+        uint32_t sc[NW];
 #pragma unroll
-        for (int w = 0; w < 4; ++w) {
+        for (int w = 0; w < NW; ++w) {
           const int o = gk + 8 * w;
           const int jr = jb - j0 + (o >= p.group) + (o >= 2 * p.group);
           const uint32_t v = lds_u16(sb + s * Gm::STAGE + Gm::SC_OFS + (jr * BM + row) * 2);
           sc[w] = v | (v << 16);
         }
         const uint32_t qbase = sb + s * Gm::STAGE + Gm::ACT_BYTES + row * Gm::CODE_BYTES_ROW;
-        uint32_t out[16];
+        uint32_t out[kKPW / 2];
         if (BITS == 4) {
-          // 16 bytes = 32 codes; SWIZZLE_32B: 16-byte chunk c of row r sits at c ^ ((r >> 2) & 1)
-          const uint4 c = lds128(qbase + ((half ^ ((row >> 2) & 1)) << 4));
-          const uint32_t words[4] = {c.x, c.y, c.z, c.w};
+          // kKPW/2 bytes; SWIZZLE_32B: 16-byte chunk c of row r sits at c ^ ((r >> 2) & 1)
+          uint32_t words[NW];
+          if constexpr (kKPW == 32) {
+            const uint4 c = lds128(qbase + ((half ^ ((row >> 2) & 1)) << 4));
+            words[0] = c.x; words[1] = c.y; words[2] = c.z; words[3] = c.w;
+          } else {
+            const uint2 c = lds64(qbase + (((half >> 1) ^ ((row >> 2) & 1)) << 4) + (half & 1) * 8);
+            words[0] = c.x; words[1] = c.y;
+          }
 #pragma unroll
-          for (int w = 0; w < 4; ++w) {
+          for (int w = 0; w < NW; ++w) {
             uint32_t q[4];
             i4_nat_pairs<T>(words[w], q);
 #pragma unroll
             for (int i = 0; i < 4; ++i) out[4 * w + i] = mul2x<T>(q[i], sc[w]);
           }
         } else {
-          // 32 bytes = 32 codes; SWIZZLE_64B: chunk c of row r sits at c ^ ((r >> 1) & 3)
+          // kKPW bytes; SWIZZLE_64B: chunk c of row r sits at c ^ ((r >> 1) & 3)
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            const int cidx = half * 2 + hh;
+          for (int hh = 0; hh < kKPW / 16; ++hh) {
+            const int cidx = half * (kKPW / 16) + hh;
             const uint4 c = lds128(qbase + ((cidx ^ ((row >> 1) & 3)) << 4));
             const uint32_t words[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
@@ -307,7 +323,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
             }
           }
         }
-        tmem_st16(tmem + lane_base + kACol + s * 32 + half * 16, out);
+        if constexpr (kKPW == 32)
+          tmem_st16(tmem + lane_base + kACol + s * 32 + half * 16, *reinterpret_cast<const uint32_t(*)[16]>(out));
+        else
+          tmem_st8(tmem + lane_base + kACol + s * 32 + half * 8, *reinterpret_cast<const uint32_t(*)[8]>(out));
         tmem_wait_st();
         fence_before();
         __syncwarp();
@@ -318,11 +337,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
         gk += BK;
         while (gk >= p.group) { gk -= p.group; ++jb; }
       }
-      // ---- epilogue: accumulator row `row` (weight n), tokens [half*128, half*128+128)
+      // ---- epilogue: accumulator row `row` (weight n), tokens [half*TPP, half*TPP+TPP)
       mbar_wait(&acc_full, acc_ph);
       acc_ph ^= 1;
       fence_after();
-      const int tok_base = mt * p.bn + half * 128;
+      constexpr int TPP = 256 / kParts;  // accumulator (token) columns drained per dequant warp
+      const int tok_base = mt * p.bn + half * TPP;
       auto store = [&](int tok, float f) {
         if (p.cdt == FQ_FP32) reinterpret_cast<float*>(p.C)[(size_t)tok * N + n] = f;
         else reinterpret_cast<T*>(p.C)[(size_t)tok * N + n] = Dt<T>::from_f(f);
@@ -330,14 +350,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       // split-K: this item's fp32 partial [bn][128] of output tile tt, slot ks
       float* part = p.splits > 1 ? p.ws + (size_t)(tt * p.splits + ks) * p.bn * BM : nullptr;
 #pragma unroll 1
-      for (int c0 = 0; c0 < 128 && half * 128 + c0 < p.bn; c0 += 32) {
+      for (int c0 = 0; c0 < TPP && half * TPP + c0 < p.bn; c0 += 32) {
         uint32_t v[32];
-        tmem_ld32(tmem + lane_base + kAccCol + half * 128 + c0, v);
+        tmem_ld32(tmem + lane_base + kAccCol + half * TPP + c0, v);
         tmem_wait_ld();
         if (part) {
 #pragma unroll
           for (int i = 0; i < 32; ++i)
-            if (half * 128 + c0 + i < p.bn) __stcg(part + (half * 128 + c0 + i) * BM + row, __uint_as_float(v[i]));
+            if (half * TPP + c0 + i < p.bn) __stcg(part + (half * TPP + c0 + i) * BM + row, __uint_as_float(v[i]));
         } else if (n < N) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
@@ -363,22 +383,23 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
           // 256 threads: thread -> (row = tid % 128, tokens tid / 128 + 2i); 4 tokens per round so
           // their split loads are in flight together; rows are contiguous -> coalesced
           const float* base = p.ws + (size_t)tt * p.splits * p.bn * BM;
+          constexpr int NPAR = kDqWarps * 32 / BM;  // threads per row
           const int tid = threadIdx.x - 64, r = tid & (BM - 1);
           const int nr = nt * BM + r;
           const int tmax = min(p.bn, M - mt * p.bn);
           if (nr < N) {
-            for (int tl0 = tid >> 7; tl0 < tmax; tl0 += 8) {
+            for (int tl0 = tid / BM; tl0 < tmax; tl0 += 4 * NPAR) {
               float acc[4] = {0.f, 0.f, 0.f, 0.f};
               for (int q = 0; q < p.splits; ++q) {
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                  const int tl = tl0 + 2 * u;
+                  const int tl = tl0 + NPAR * u;
                   if (tl < tmax) acc[u] += __ldcg(base + ((size_t)q * p.bn + tl) * BM + r);
                 }
               }
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
-                const int tl = tl0 + 2 * u;
+                const int tl = tl0 + NPAR * u;
                 if (tl < tmax) {
                   const size_t o = (size_t)(mt * p.bn + tl) * N + nr;
                   if (p.cdt == FQ_FP32) reinterpret_cast<float*>(p.C)[o] = acc[u];
@@ -464,7 +485,7 @@ static cudaError_t launch_tc(const tc::TcBatch<MAXP>& b, cudaStream_t st) {
     attr = true;
   }
   const int grid = std::min(b.total_tiles, num_sms());
-  kern<<<grid, tc::kThreads, Gm::SMEM, st>>>(b);
+  kern<<<grid, tc::tc_threads(BNMAX), Gm::SMEM, st>>>(b);
   return cudaGetLastError();
 }
 
