@@ -460,6 +460,22 @@ def measure_extras(fq, dev, peaks):
                             "TFLOP_s": round(fl / tt / 1e12, 1)}
         del A
     out["moe_64x16384x4096_int4_adaptive"] = moe
+    del experts
+    torch.cuda.empty_cache()
+
+    # ---- the paper's own kernel benchmark: speed-up over a dense
+    # FP16 x FP16 GEMM (cuBLAS via torch.matmul) on OPT-13B / OPT-30B QKV, attention-out, FFN1,
+    # FFN2, geometric mean over the 4 GEMMs; int4, block size 64 as in the paper (and 128), fp16
+    # activations, L2 flushed before every timed GEMM.  The paper reports "up to 2.5X" on A100.
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import paper_microbench as PM
+    pm = {}
+    for g in (64, 128):
+        r = PM.run(bits=4, group=g, rows=(1, 8, 16, 64, 256, 2048), reps=5)
+        pm[f"int4_g{g}"] = {m: v["geomean_speedup"] for m, v in r["models"].items()}
+    pm["baseline"] = "torch.matmul fp16 (cuBLAS), L2 flushed per GEMM; geomean of QKV/AttnOut/FFN1/FFN2 speed-ups by rows"
+    pm["paper_a100"] = "up to 2.5x (int4, block 64, small row counts; figure data not in the text, P:189/P:308)"
+    out["paper_microbench_opt13b_opt30b"] = pm
     return out
 
 
