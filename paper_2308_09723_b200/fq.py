@@ -75,9 +75,15 @@ def _ptr(t):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def _stream(stream=None):
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return ctypes.c_void_p(s.cuda_stream)
+    if stream is not None:
+        return ctypes.c_void_p(stream.cuda_stream)
+    if _raw_stream is not None:  # the current stream's handle without building a Stream object
+        return ctypes.c_void_p(_raw_stream(torch.cuda.current_device()))
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
 def _check(st: int, what: str):
@@ -248,7 +254,13 @@ def gemm(A: torch.Tensor, qw: QuantizedWeight, out: torch.Tensor | None = None,
     d = qw.desc
     if out is None:
         out = torch.empty((M, qw.N), dtype=out_dtype or A.dtype, device=A.device)
-    nb = fq_gemm_workspace_bytes(M, d)
+    key = (M, qw.K, qw.N, qw.bits, qw.group)
+    nb = _WS_BYTES.get(key)
+    if nb is None:
+        nb = _WS_BYTES[key] = fq_gemm_workspace_bytes(M, d)
     ws = workspace(nb, A.device)
     fq_gemm(A, M, d, qw.codes, qw.scales, out, ws, stream)
     return out
+
+
+_WS_BYTES: dict = {}  # (M, K, N, bits, group) -> fq_gemm_workspace_bytes (a pure function of the shape)
