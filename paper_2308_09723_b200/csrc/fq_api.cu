@@ -46,13 +46,14 @@ static cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 static fq_status from_cuda(cudaError_t e) { return e == cudaSuccess ? FQ_OK : FQ_ERR_CUDA; }
 
-// M <= 16: memory-bound decode kernel (A4/A5); larger M: tcgen05 tensor-core kernel (A6).
-// FQ_GEMM_PATH=decode|tc forces a path (tests and A/B measurements).
-static bool use_tc_path(int64_t M) {
+// M <= 16 (32 on the int4 nibble path): memory-bound decode kernel (A4/A5), every weight streamed
+// once; larger M: tcgen05 tensor-core kernel (A6).  FQ_GEMM_PATH=decode|tc forces a path (tests and
+// A/B measurements).
+static bool use_tc_path(int64_t M, int bits, int group) {
   const char* e = std::getenv("FQ_GEMM_PATH");
   if (e && std::strcmp(e, "decode") == 0) return false;
   if (e && std::strcmp(e, "tc") == 0) return true;
-  return M > 16;
+  return M > gemv_max_m(bits, group);
 }
 
 }  // namespace fq
@@ -141,7 +142,7 @@ fq_status fq_quantize(const void* W, int32_t wdt, const fq_wdesc* d, void* codes
 
 size_t fq_gemm_workspace_bytes(int64_t M, const fq_wdesc* d) {
   if (check_wdesc(d) != FQ_OK || M <= 0) return 0;
-  if (use_tc_path(M)) return gemm_tc_workspace_bytes((int)M, (int)d->K, (int)d->N);
+  if (use_tc_path(M, d->bits, d->group)) return gemm_tc_workspace_bytes((int)M, (int)d->K, (int)d->N);
   if (decode_tc_supported(d->bits, d->group, (int)M))
     return dtc_workspace_bytes(M, (int)d->K, num_sms());
   const GemvPlan p = plan_gemv((int)M, (int)d->K, (int)d->N, d->bits, d->group, num_sms());
@@ -157,7 +158,7 @@ fq_status fq_gemm(const void* A, int32_t adt, int64_t M, const fq_wdesc* d, cons
   if (d->scale_dtype != adt) return FQ_ERR_UNSUPPORTED;
   if (cdt != adt && cdt != FQ_FP32) return FQ_ERR_UNSUPPORTED;
   if (M <= 0 || M > (1 << 20)) return FQ_ERR_SHAPE;
-  if (use_tc_path(M))
+  if (use_tc_path(M, d->bits, d->group))
     return from_cuda(run_gemm_tc(adt, cdt, d->bits, A, (int)M, (int)d->K, (int)d->N, codes, scales,
                                  d->group, C, ws, ws_bytes, as_stream(stream)));
   if (decode_tc_supported(d->bits, d->group, (int)M)) {
@@ -205,7 +206,7 @@ fq_status fq_gemm_grouped(const void* A, int32_t adt, int64_t T, const int64_t* 
   for (int32_t e = 0; e < E; ++e) {
     const int64_t Me = offsets_host[e + 1] - offsets_host[e];
     if (Me == 0) continue;
-    (Me <= 16 && !use_tc_path(Me) ? small : large).push_back(e);
+    (!use_tc_path(Me, d->bits, groups_host[e]) ? small : large).push_back(e);
   }
   if (!large.empty()) {  // every large expert in one persistent tcgen05 launch (per <= 48 experts)
     cudaError_t r = run_gemm_tc_grouped(adt, cdt, d->bits, A, (int)d->K, (int)d->N, offsets_host, groups_host,

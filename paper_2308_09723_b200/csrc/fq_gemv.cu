@@ -277,9 +277,14 @@ template <typename T, int BITS, int MT, bool SACC, int DBG, int MAXP>
 #define FQ_DEC_NIB_MAXREG 96  // measured: faster than 104 or 112 (which ptxas schedules worse)
 #endif
 #ifndef FQ_DEC_NIB2_MAXREG
-#define FQ_DEC_NIB2_MAXREG 112  // two 8-token MMA tiles (9 <= M <= 16); 2 CTAs x 288 threads fit 113
+#define FQ_DEC_NIB2_MAXREG 104  // two 8-token MMA tiles (9 <= M <= 16); measured best of 96/104/112
 #endif
-__global__ void __maxnreg__((FQ_NIB && BITS == 4 && SACC) ? (MT == 2 ? FQ_DEC_NIB2_MAXREG : FQ_DEC_NIB_MAXREG) : 96)
+#ifndef FQ_DEC_NIB4_MAXREG
+#define FQ_DEC_NIB4_MAXREG 112  // four 8-token MMA tiles (17 <= M <= 32); 2 CTAs x 288 threads fit 113
+#endif
+__global__ void __maxnreg__((FQ_NIB && BITS == 4 && SACC)
+                               ? (MT == 4 ? FQ_DEC_NIB4_MAXREG : MT == 2 ? FQ_DEC_NIB2_MAXREG : FQ_DEC_NIB_MAXREG)
+                               : 96)
 decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
   using G = DecGeom<BITS>;
   using SG = DecStage<BITS, MT, SACC>;
@@ -296,7 +301,10 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
   using TC = typename std::conditional<NIB, __half, T>::type;  // MMA operand type
   constexpr float OFF = NIB ? 1.f : (SACC ? CodeOffset<T, BITS>::v : 0.f);  // NIB: sums hold the correction
   constexpr int PPC = KCH / 8;  // 8-element pieces per chunk (16 int4, 8 int8): divides 32
-  constexpr bool EARLY = MT == 2 ? FQ_DEC_EARLY2 : FQ_DEC_EARLY;
+  // MT = 4 (17..32 tokens): the activation fragments are read from shared memory per 8-code word
+  // (LAZY) instead of all up front, so the stage is held until the MMAs are done
+  constexpr bool LAZY = MT == 4;
+  constexpr bool EARLY = LAZY ? false : (MT == 2 ? FQ_DEC_EARLY2 : FQ_DEC_EARLY);
 
   extern __shared__ __align__(1024) uint8_t dsmem[];
   __shared__ __align__(8) uint64_t full_bar[kMaxDecStages], empty_bar[kMaxDecStages], raw_bar[kMaxDecStages];
@@ -314,7 +322,7 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
   const int kbeg = by * p.klen;
   const int kend = min(K, kbeg + p.klen);
   const int nst = (kend - kbeg + KS - 1) / KS;
-  const int tok0 = bz * 16;
+  const int tok0 = bz * MT * 8;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSTG; ++s) {
@@ -502,11 +510,13 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
       }
     }
     if (DBG != 3) {
-      uint4 b[MT][PIECES];
+      uint4 b[LAZY ? 1 : MT][PIECES];
+      if (!LAZY) {
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
+        for (int mt = 0; mt < (LAZY ? 1 : MT); ++mt)
 #pragma unroll
-        for (int w16 = 0; w16 < PIECES; ++w16) b[mt][w16] = lds128(wst + aofs[mt][w16]);
+          for (int w16 = 0; w16 < PIECES; ++w16) b[mt][w16] = lds128(wst + aofs[mt][w16]);
+      }
       float2 sa[MT], iv[MT];
       if (NIB) {  // {corr, 2^-e} of tokens 2t and 2t+1
 #pragma unroll
@@ -598,8 +608,9 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
               const uint32_t a[4] = {qg[2 * pp], qh[2 * pp], qg[2 * pp + 1], qh[2 * pp + 1]};
 #pragma unroll
               for (int mt = 0; mt < MT; ++mt) {
-                const uint32_t b0 = pp ? b[mt][w].z : b[mt][w].x;
-                const uint32_t b1 = pp ? b[mt][w].w : b[mt][w].y;
+                const uint4 bw = LAZY ? lds128(wst + aofs[mt][w]) : b[LAZY ? 0 : mt][w];
+                const uint32_t b0 = pp ? bw.z : bw.x;
+                const uint32_t b1 = pp ? bw.w : bw.y;
                 if (DBG == 1) {
 #pragma unroll
                   for (int q = 0; q < 4; ++q) dst[mt][q] += __uint_as_float(a[q] ^ b0);
@@ -624,7 +635,7 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
             const uint32_t a[4] = {qg[0], qh[0], qg[1], qh[1]};
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt) {
-              const uint4 bb = b[mt][w >> 1];
+              const uint4 bb = LAZY ? lds128(wst + aofs[mt][w >> 1]) : b[LAZY ? 0 : mt][w >> 1];
               mma16816<T>(dst[mt], a, (w & 1) ? bb.z : bb.x, (w & 1) ? bb.w : bb.y);
             }
           }
@@ -707,20 +718,26 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
   }
   asm volatile("bar.sync 1, %0;" ::"n"(32 * kConsumerWarps));
   if (!s_last) return;
+  // Fixup: consumer thread c owns column n0 + c (coalesced across the CTA); its tokens are summed
+  // over the splits in split order, 4 tokens per round so their loads are in flight together.
+  {
+    const int c = threadIdx.x - 32;  // 0 .. kRowsPerCta-1
+    const int n = n0 + c;
+    const int ntok = min(M - tok0, MT * 8);
+    if (n < N) {
+      for (int j0 = 0; j0 < ntok; j0 += 4) {
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int s = 0; s < S_; ++s) {
 #pragma unroll
-  for (int rt = 0; rt < 2; ++rt)
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        int n, tok;
-        out_idx(rt, mt, i, n, tok);
-        if (n < N && tok < M) {
-          float v = 0.f;
-          for (int s = 0; s < S_; ++s) v += __ldcg(p.ws + ((size_t)s * M + tok) * N + n);
-          store_out(tok, n, v);
+          for (int u = 0; u < 4; ++u)
+            if (j0 + u < ntok) v[u] += __ldcg(p.ws + ((size_t)s * M + tok0 + j0 + u) * N + n);
         }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (j0 + u < ntok) store_out(tok0 + j0 + u, n, v[u]);
       }
+    }
+  }
   if (threadIdx.x == 32) *ctr = 0;  // self-reset for the next call / graph replay
 }
 
@@ -797,12 +814,18 @@ static int env_int(const char* name, int dflt) {
   return v ? std::atoi(v) : dflt;
 }
 
+static bool nib_of(int bits, int group) { return FQ_NIB && bits == 4 && group % 128 == 0; }
+
+int gemv_max_m(int bits, int group) { return nib_of(bits, group) ? 32 : 16; }
+
 GemvPlan plan_gemv(int M, int K, int N, int bits, int group, int nsm) {
   (void)group;
   GemvPlan p{};
   p.kchunk = bits == 4 ? 256 : 128;  // split-K granularity (two kernel stages; one stage measured slower on small matrices)
-  p.mt = M <= 8 ? 1 : 2;
-  p.ktiles = (M + 15) / 16;
+  // 8-token MMA tiles per token tile: 1 (M <= 8), 2 (<= 16), 4 (int4 nibble path, > 16 tokens:
+  // every weight is streamed once per 32 tokens)
+  p.mt = M <= 8 ? 1 : (M <= 16 || !nib_of(bits, group)) ? 2 : 4;
+  p.ktiles = (M + p.mt * 8 - 1) / (p.mt * 8);
   p.rt = 2;
   p.rows_per_cta = kRowsPerCta;
   const int gx = (N + p.rows_per_cta - 1) / p.rows_per_cta;
@@ -835,7 +858,6 @@ GemvPlan plan_gemv(int M, int K, int N, int bits, int group, int nsm) {
 //   [0, kCounterBytes)  arrival counters (zeroed once by the caller, self-resetting)
 //   then split-K fp32 partials [S][M][N] (fully overwritten by every call)
 //   then, on the nibble path, the pre-converted activations A' [M][K] fp16 and S' [K/128][M][4].
-static bool nib_of(int bits, int group) { return FQ_NIB && bits == 4 && group % 128 == 0; }
 static size_t prep_bytes(int M, int K) {
   return align256((size_t)M * K * 2) + align256((size_t)(K / 128) * M * 16);
 }
@@ -885,11 +907,13 @@ static cudaError_t dispatch_dec(int adt, int bits, int mt, bool sacc, int dbg, c
   if (adt == FQ_BF16) {
     FQ_DEC_CASE(__nv_bfloat16, 4, 1, true) FQ_DEC_CASE(__nv_bfloat16, 4, 1, false)
     FQ_DEC_CASE(__nv_bfloat16, 4, 2, true) FQ_DEC_CASE(__nv_bfloat16, 4, 2, false)
+    FQ_DEC_CASE(__nv_bfloat16, 4, 4, true)
     FQ_DEC_CASE(__nv_bfloat16, 8, 1, true) FQ_DEC_CASE(__nv_bfloat16, 8, 1, false)
     FQ_DEC_CASE(__nv_bfloat16, 8, 2, true) FQ_DEC_CASE(__nv_bfloat16, 8, 2, false)
   } else {
     FQ_DEC_CASE(__half, 4, 1, true) FQ_DEC_CASE(__half, 4, 1, false)
     FQ_DEC_CASE(__half, 4, 2, true) FQ_DEC_CASE(__half, 4, 2, false)
+    FQ_DEC_CASE(__half, 4, 4, true)
     FQ_DEC_CASE(__half, 8, 1, true) FQ_DEC_CASE(__half, 8, 1, false)
     FQ_DEC_CASE(__half, 8, 2, true) FQ_DEC_CASE(__half, 8, 2, false)
   }
@@ -975,8 +999,8 @@ cudaError_t run_gemv_grouped(int adt, int cdt, int bits, const void* A, int K, i
     cudaError_t r = launch_prep(adt, A, (int)T, K, pre, Sp, st);
     if (r != cudaSuccess) return r;
   }
-  for (int cls = 0; cls < 4; ++cls) {
-    const int mt = 1 + (cls >> 1);
+  for (int cls = 0; cls < 6; ++cls) {
+    const int mt = 1 << (cls >> 1);  // 1, 2, 4 MMA token tiles
     const bool sacc = cls & 1;
     DecBatch<kMaxBatch> b{};
     int ctas = 0;

@@ -23,6 +23,8 @@ struct GemvPlan {
   int klen;           // K elements per split (multiple of kchunk)
 };
 GemvPlan plan_gemv(int M, int K, int N, int bits, int group, int num_sms);
+// Largest M the decode kernel serves in one pass over the weights (32 on the int4 nibble path, else 16).
+int gemv_max_m(int bits, int group);
 size_t gemv_workspace_bytes(const GemvPlan& p, int M, int K, int N, int bits, int group);
 size_t gemv_grouped_workspace_bytes(int64_t T, int K, int bits);
 cudaError_t run_gemv(const GemvPlan& p, int adt, int cdt, int bits, const void* A, int M, int K,
