@@ -66,13 +66,13 @@ struct DecGeom {
 
 // Stage = [packed weights 256 x 64 B][activations MT*8 x KS (TMA, then permuted in place by the
 // stager)][256 scales][per-token activation sums].  As many stages as fit two CTAs per SM.
-template <int BITS, int MT, bool SACC>
+template <int BITS, int MT, int SACC>
 struct DecStage {
   using G = DecGeom<BITS>;
   static constexpr int ACT_OFS = kStageW;
   static constexpr int ACT_BYTES = MT * 8 * G::ROWB;
   static constexpr int SC_OFS = ACT_OFS + ACT_BYTES;  // TMA destinations: 128-byte aligned
-  static constexpr int SC_BYTES = kRowsPerCta * 2 * (SACC ? 1 : 8);  // per-element path: up to 8 rows
+  static constexpr int SC_BYTES = kRowsPerCta * 2 * (SACC ? SACC : 8);  // scale rows per stage (<= 8)
   static constexpr int SUM_OFS = SC_OFS + SC_BYTES;
   static constexpr int SUM_BYTES = MT * 8 * 16;  // per token: offset correction, inverse scale (+pad)
   static constexpr int BYTES = ((SUM_OFS + SUM_BYTES + 1023) / 1024) * 1024;
@@ -270,7 +270,7 @@ __device__ __forceinline__ int swz64(int c, int R) { return c ^ ((R >> 1) & 3); 
 
 // DBG (diagnostics only, selected by FQ_DEC_DEBUG for bf16/int4/M<=8): 1 = no MMA (fake FADD
 // accumulate), 2 = no dequant (raw code words as MMA operands), 3 = consumers skip all compute.
-template <typename T, int BITS, int MT, bool SACC, int DBG, int MAXP>
+template <typename T, int BITS, int MT, int SACC, int DBG, int MAXP>
 // Register caps (two CTAs per SM fit up to 112 / 96 registers at 288 / 320 threads), set without
 // ptxas's launch_bounds heuristic.
 #ifndef FQ_DEC_NIB_MAXREG
@@ -298,6 +298,11 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
   // Nibble path: activations were pre-converted by prep_acts_kernel (fp16, fragment order) and
   // arrive by TMA with their per-chunk {correction, 2^-e}; there is no stager warp.
   constexpr bool NIB = FQ_NIB && BITS == 4 && SACC;
+  // GS = 2 (int4, group 64, nibble path): each thread's four 8-code words come from the four 32-k
+  // blocks of the stage (4 x LDS.32 instead of one LDS.128), so the MMAs of words 0-1 and 2-3 cover
+  // the two 64-k groups separately; two exact partials per stage, folded with their own scales.
+  constexpr int GS = SACC == 2 ? 2 : 1;
+  static_assert(GS == 1 || NIB, "group split only on the nibble path");
   using TC = typename std::conditional<NIB, __half, T>::type;  // MMA operand type
   constexpr float OFF = NIB ? 1.f : (SACC ? CodeOffset<T, BITS>::v : 0.f);  // NIB: sums hold the correction
   constexpr int PPC = KCH / 8;  // 8-element pieces per chunk (16 int4, 8 int8): divides 32
@@ -346,12 +351,12 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
       const uint64_t polw = policy_evict_first();
       const uint64_t pola = policy_evict_last();
       // chunk c = kbeg/KCH + i (one chunk per stage) lies in scale group c / gm
-      const int gm = SACC ? p.group / KCH : 1;
-      int grem = SACC ? (kbeg / KCH) % gm : 0, gj = SACC ? (kbeg / KCH) / gm : 0;
+      const int gm = SACC == 1 ? p.group / KCH : 1;
+      int grem = SACC == 1 ? (kbeg / KCH) % gm : 0, gj = SACC == 1 ? (kbeg / KCH) / gm : 0;
       auto issue_w = [&](int i, int s) {  // the stage's packed weights + scales (+ expect_tx)
         uint8_t* st = sbase + s * STAGE_BYTES;
         const int k0 = kbeg + i * KS;
-        const int scb = SACC ? kRowsPerCta * 2 : p.sc_rows * kRowsPerCta * 2;
+        const int scb = SACC ? SACC * kRowsPerCta * 2 : p.sc_rows * kRowsPerCta * 2;
         mbar_arrive_expect_tx(&full_bar[s], kStageW + scb + (NIB ? RAW_BYTES + MT * 8 * 16 : 0));
 #pragma unroll
         for (int bx2 = 0; bx2 < kWBoxes; ++bx2)
@@ -360,7 +365,8 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
         if (SACC) {
 #pragma unroll
           for (int bx2 = 0; bx2 < kWBoxes; ++bx2)
-            tma_load_2d(st + SC_OFS + bx2 * kWBoxRows * 2, &p.s, &full_bar[s], n0 + bx2 * kWBoxRows, gj, polw);
+            tma_load_2d(st + SC_OFS + bx2 * kWBoxRows * 2, &p.s, &full_bar[s], n0 + bx2 * kWBoxRows,
+                        GS == 2 ? (k0 >> 6) : gj, polw);  // GS: the stage's two 64-k rows (box of 2)
           if (++grem == gm) { grem = 0; ++gj; }
         } else if (p.sc_rows) {
 #pragma unroll
@@ -501,13 +507,15 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
     const int k0 = kbeg + i * KS;
     mbar_wait(&full_bar[s], ph);
     const uint32_t wst = sb + s * STAGE_BYTES;
-    float sg[2], sh[2];  // this stage's scales (TMA-staged with the weights)
+    float sg[2][GS], sh[2][GS];  // this stage's scales (TMA-staged with the weights), per 64-k group
     if (SACC) {
 #pragma unroll
-      for (int rt = 0; rt < 2; ++rt) {
-        sg[rt] = lds_scale<T>(wst + SC_OFS + Rg[rt] * 2);
-        sh[rt] = lds_scale<T>(wst + SC_OFS + Rh[rt] * 2);
-      }
+      for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+        for (int gi = 0; gi < GS; ++gi) {
+          sg[rt][gi] = lds_scale<T>(wst + SC_OFS + gi * kRowsPerCta * 2 + Rg[rt] * 2);
+          sh[rt][gi] = lds_scale<T>(wst + SC_OFS + gi * kRowsPerCta * 2 + Rh[rt] * 2);
+        }
     }
     if (DBG != 3) {
       uint4 b[LAZY ? 1 : MT][PIECES];
@@ -517,23 +525,41 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
 #pragma unroll
           for (int w16 = 0; w16 < PIECES; ++w16) b[mt][w16] = lds128(wst + aofs[mt][w16]);
       }
-      float2 sa[MT], iv[MT];
-      if (NIB) {  // {corr, 2^-e} of tokens 2t and 2t+1
+      float2 sa[MT][GS], iv[MT];
+      if (NIB) {  // {corr, 2^-e, corr_lo, corr_hi} of tokens 2t and 2t+1 (lo / hi: the 64-k halves)
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
-          const float2 x0 = lds64f(wst + saofs + mt * 128), x1 = lds64f(wst + saofs + mt * 128 + 16);
-          sa[mt] = make_float2(x0.x, x1.x);
-          iv[mt] = make_float2(x0.y, x1.y);
+          if (GS == 1) {
+            const float2 x0 = lds64f(wst + saofs + mt * 128), x1 = lds64f(wst + saofs + mt * 128 + 16);
+            sa[mt][0] = make_float2(x0.x, x1.x);
+            iv[mt] = make_float2(x0.y, x1.y);
+          } else {
+            const uint4 x0 = lds128(wst + saofs + mt * 128), x1 = lds128(wst + saofs + mt * 128 + 16);
+            sa[mt][0] = make_float2(__uint_as_float(x0.z), __uint_as_float(x1.z));
+            sa[mt][GS - 1] = make_float2(__uint_as_float(x0.w), __uint_as_float(x1.w));
+            iv[mt] = make_float2(__uint_as_float(x0.y), __uint_as_float(x1.y));
+          }
         }
       } else if (OFF != 0.f) {
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) sa[mt] = lds64f(wst + saofs + mt * 32);
+        for (int mt = 0; mt < MT; ++mt) sa[mt][0] = lds64f(wst + saofs + mt * 32);
       }
       uint4 wgv[2], whv[2];
 #pragma unroll
       for (int rt = 0; rt < 2; ++rt) {
-        wgv[rt] = lds128(wst + wofs_g[rt]);
-        whv[rt] = lds128(wst + wofs_h[rt]);
+        if (GS == 1) {
+          wgv[rt] = lds128(wst + wofs_g[rt]);
+          whv[rt] = lds128(wst + wofs_h[rt]);
+        } else {  // word w = 8 codes at k = 32 w + 8 t: cell w (swizzled), word t of the cell
+          uint32_t g4[4], h4[4];
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            g4[w] = lds32(wst + Rg[rt] * kWBytesPerRow + (swz64(w, Rg[rt]) << 4) + t * 4);
+            h4[w] = lds32(wst + Rh[rt] * kWBytesPerRow + (swz64(w, Rh[rt]) << 4) + t * 4);
+          }
+          wgv[rt] = make_uint4(g4[0], g4[1], g4[2], g4[3]);
+          whv[rt] = make_uint4(h4[0], h4[1], h4[2], h4[3]);
+        }
       }
       // per-element-scale path with TMA-staged scale rows: into registers before the stage is
       // released (the producer may overwrite it right after the early release below)
@@ -562,12 +588,14 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
         const uint4 wh = whv[rt];
         const uint32_t wgw[4] = {wg.x, wg.y, wg.z, wg.w};
         const uint32_t whw[4] = {wh.x, wh.y, wh.z, wh.w};
-        float part[MT][4];
+        float part[GS][MT][4];
         if (SACC) {
 #pragma unroll
-          for (int mt = 0; mt < MT; ++mt)
+          for (int gi = 0; gi < GS; ++gi)
 #pragma unroll
-            for (int q = 0; q < 4; ++q) part[mt][q] = 0.f;
+            for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+              for (int q = 0; q < 4; ++q) part[gi][mt][q] = 0.f;
         }
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
@@ -583,7 +611,7 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
               shs = splat_scale<T>(S, j + nh[rt]);
             }
           }
-          float(*dst)[4] = SACC ? part : acc[rt];
+          float(*dst)[4] = SACC ? part[(w * GS) >> 2] : acc[rt];
           if (BITS == 4) {
             uint32_t qg[4], qh[4];
             if (DBG == 2) {
@@ -642,23 +670,26 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
         }
         if (SACC) {
 #pragma unroll
+          for (int gi = 0; gi < GS; ++gi)
+#pragma unroll
           for (int mt = 0; mt < MT; ++mt) {
+            float(&pp)[4] = part[gi][mt];
             if (OFF != 0.f) {  // remove OFF * sum_k a[tok, k] (tokens 2t, 2t+1 of this MMA tile)
-              part[mt][0] = fmaf(-OFF, sa[mt].x, part[mt][0]);
-              part[mt][1] = fmaf(-OFF, sa[mt].y, part[mt][1]);
-              part[mt][2] = fmaf(-OFF, sa[mt].x, part[mt][2]);
-              part[mt][3] = fmaf(-OFF, sa[mt].y, part[mt][3]);
+              pp[0] = fmaf(-OFF, sa[mt][gi].x, pp[0]);
+              pp[1] = fmaf(-OFF, sa[mt][gi].y, pp[1]);
+              pp[2] = fmaf(-OFF, sa[mt][gi].x, pp[2]);
+              pp[3] = fmaf(-OFF, sa[mt][gi].y, pp[3]);
             }
             if (NIB) {  // undo the chunk's power-of-two activation scale
-              acc[rt][mt][0] = fmaf(sg[rt] * iv[mt].x, part[mt][0], acc[rt][mt][0]);
-              acc[rt][mt][1] = fmaf(sg[rt] * iv[mt].y, part[mt][1], acc[rt][mt][1]);
-              acc[rt][mt][2] = fmaf(sh[rt] * iv[mt].x, part[mt][2], acc[rt][mt][2]);
-              acc[rt][mt][3] = fmaf(sh[rt] * iv[mt].y, part[mt][3], acc[rt][mt][3]);
+              acc[rt][mt][0] = fmaf(sg[rt][gi] * iv[mt].x, pp[0], acc[rt][mt][0]);
+              acc[rt][mt][1] = fmaf(sg[rt][gi] * iv[mt].y, pp[1], acc[rt][mt][1]);
+              acc[rt][mt][2] = fmaf(sh[rt][gi] * iv[mt].x, pp[2], acc[rt][mt][2]);
+              acc[rt][mt][3] = fmaf(sh[rt][gi] * iv[mt].y, pp[3], acc[rt][mt][3]);
             } else {
-              acc[rt][mt][0] = fmaf(sg[rt], part[mt][0], acc[rt][mt][0]);
-              acc[rt][mt][1] = fmaf(sg[rt], part[mt][1], acc[rt][mt][1]);
-              acc[rt][mt][2] = fmaf(sh[rt], part[mt][2], acc[rt][mt][2]);
-              acc[rt][mt][3] = fmaf(sh[rt], part[mt][3], acc[rt][mt][3]);
+              acc[rt][mt][0] = fmaf(sg[rt][gi], pp[0], acc[rt][mt][0]);
+              acc[rt][mt][1] = fmaf(sg[rt][gi], pp[1], acc[rt][mt][1]);
+              acc[rt][mt][2] = fmaf(sh[rt][gi], pp[2], acc[rt][mt][2]);
+              acc[rt][mt][3] = fmaf(sh[rt][gi], pp[3], acc[rt][mt][3]);
             }
           }
         }
@@ -746,8 +777,10 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
 // chunk's 8-element pieces permuted into the decode consumers' fragment order (words (a0,a4),
 // (a1,a5)/16, (a2,a6), (a3,a7)/16; cell c -> (c % 4) * 4 + c / 4, XOR (tok & 1) * 4), values
 // scaled by 2^e (bf16 input: the chunk max |a| lands in [2^14, 2^15); fp16 input: e = 0).
-// S'[chunk][tok] = {1032 * sum_even(a') + 72 * sum_odd(a'), 2^-e, 0, 0}.
-template <typename T>
+// S'[chunk][tok] = {1032 * sum_even(a') + 72 * sum_odd(a'), 2^-e, same sum over k < 64, over k >= 64}.
+// GS (group-split consumers, group 64): pieces stay at cell c (XOR (tok & 1) * 4): the consumers'
+// word w of thread t is piece 4 w + t there.
+template <typename T, bool GS>
 __global__ void __launch_bounds__(128) prep_acts_kernel(const T* __restrict__ A, int ntok, int K,
                                                         __half* __restrict__ Ap, float* __restrict__ Sp) {
   griddep_wait();  // A may be the output of the previous kernel in the stream
@@ -795,13 +828,15 @@ __global__ void __launch_bounds__(128) prep_acts_kernel(const T* __restrict__ A,
   float sum = fmaf(Nib<__half>::off_even, (f[0] + f[2]) + (f[4] + f[6]),
                    Nib<__half>::off_odd * ((f[1] + f[3]) + (f[5] + f[7])));
 #pragma unroll
-  for (int o = 8; o; o >>= 1) sum += __shfl_xor_sync(hmask, sum, o);
+  for (int o = 1; o < 8; o <<= 1) sum += __shfl_xor_sync(hmask, sum, o);  // 64-k half sums
+  const float half_sum = sum, other = __shfl_xor_sync(hmask, sum, 8);
+  sum += other;
   const uint4 o = make_uint4(h2(f[0], f[4]), h2(f[1] * 0.0625f, f[5] * 0.0625f), h2(f[2], f[6]),
                              h2(f[3] * 0.0625f, f[7] * 0.0625f));
   const int kl = l * 8, tq = kl >> 5, w16 = (kl & 31) >> 3;
-  const int cell = (w16 * 4 + tq) ^ ((tok & 1) << 2);
+  const int cell = (GS ? l : (w16 * 4 + tq)) ^ ((tok & 1) << 2);
   *reinterpret_cast<uint4*>(Ap + base + cell * 8) = o;
-  if (l == 0) *reinterpret_cast<float4*>(Sp + ((size_t)ch * ntok + tok) * 4) = make_float4(sum, inv, 0.f, 0.f);
+  if (l == 0) *reinterpret_cast<float4*>(Sp + ((size_t)ch * ntok + tok) * 4) = make_float4(sum, inv, half_sum, other);
 }
 
 // ------------------------------------------------------------------------------------- host side
@@ -814,7 +849,13 @@ static int env_int(const char* name, int dflt) {
   return v ? std::atoi(v) : dflt;
 }
 
-static bool nib_of(int bits, int group) { return FQ_NIB && bits == 4 && group % 128 == 0; }
+// Group-split nibble path (int4, group 64, single-problem launches): K % 128 == 0 for the prep.
+static bool gs_of(int bits, int group, int K) {
+  return FQ_NIB && bits == 4 && group == 64 && K % 128 == 0 && env_int("FQ_DEC_GS", 1) != 0;
+}
+static bool nib_of(int bits, int group, int K = -1) {
+  return FQ_NIB && bits == 4 && (group % 128 == 0 || (K >= 0 && gs_of(bits, group, K)));
+}
 
 int gemv_max_m(int bits, int group) { return nib_of(bits, group) ? 32 : 16; }
 
@@ -824,7 +865,7 @@ GemvPlan plan_gemv(int M, int K, int N, int bits, int group, int nsm) {
   p.kchunk = bits == 4 ? 256 : 128;  // split-K granularity (two kernel stages; one stage measured slower on small matrices)
   // 8-token MMA tiles per token tile: 1 (M <= 8), 2 (<= 16), 4 (int4 nibble path, > 16 tokens:
   // every weight is streamed once per 32 tokens)
-  p.mt = M <= 8 ? 1 : (M <= 16 || !nib_of(bits, group)) ? 2 : 4;
+  p.mt = M <= 8 ? 1 : (M <= 16 || !nib_of(bits, group)) ? 2 : 4;  // MT = 4: group % 128 nibble path only
   p.ktiles = (M + p.mt * 8 - 1) / (p.mt * 8);
   p.rt = 2;
   p.rows_per_cta = kRowsPerCta;
@@ -864,24 +905,29 @@ static size_t prep_bytes(int M, int K) {
 size_t gemv_workspace_bytes(const GemvPlan& p, int M, int K, int N, int bits, int group) {
   size_t b = kCounterBytes;
   if (p.splits > 1) b += align256((size_t)p.splits * M * N * sizeof(float));
-  if (nib_of(bits, group)) b += prep_bytes(M, K);
+  if (nib_of(bits, group, K)) b += prep_bytes(M, K);
   return b;
 }
 size_t gemv_grouped_workspace_bytes(int64_t T, int K, int bits) {
   return kCounterBytes + (bits == 4 ? prep_bytes((int)T, K) : 0);
 }
-static cudaError_t launch_prep(int adt, const void* A, int ntok, int K, void* Ap, void* Sp, cudaStream_t st) {
+template <bool GS>
+static cudaError_t launch_prep_g(int adt, const void* A, int ntok, int K, void* Ap, void* Sp, cudaStream_t st) {
   const int blocks = (int)(((long long)ntok * (K / 128) + 7) / 8);
   if (blocks == 0) return cudaSuccess;
   if (adt == FQ_BF16)
-    return launch_pdl(prep_acts_kernel<__nv_bfloat16>, blocks, 128, 0, st,
+    return launch_pdl(prep_acts_kernel<__nv_bfloat16, GS>, blocks, 128, 0, st,
                       reinterpret_cast<const __nv_bfloat16*>(A), ntok, K, reinterpret_cast<__half*>(Ap),
                       reinterpret_cast<float*>(Sp));
-  return launch_pdl(prep_acts_kernel<__half>, blocks, 128, 0, st, reinterpret_cast<const __half*>(A), ntok, K,
+  return launch_pdl(prep_acts_kernel<__half, GS>, blocks, 128, 0, st, reinterpret_cast<const __half*>(A), ntok, K,
                     reinterpret_cast<__half*>(Ap), reinterpret_cast<float*>(Sp));
 }
+static cudaError_t launch_prep(int adt, const void* A, int ntok, int K, void* Ap, void* Sp, cudaStream_t st,
+                               bool gs = false) {
+  return gs ? launch_prep_g<true>(adt, A, ntok, K, Ap, Sp, st) : launch_prep_g<false>(adt, A, ntok, K, Ap, Sp, st);
+}
 
-template <typename T, int BITS, int MT, bool SACC, int DBG, int MAXP>
+template <typename T, int BITS, int MT, int SACC, int DBG, int MAXP>
 static cudaError_t launch_dec(const DecBatch<MAXP>& b, int ctas, cudaStream_t st) {
   constexpr int smem = DecStage<BITS, MT, SACC>::SMEM;
   auto kern = decode_kernel<T, BITS, MT, SACC, DBG, MAXP>;
@@ -895,27 +941,29 @@ static cudaError_t launch_dec(const DecBatch<MAXP>& b, int ctas, cudaStream_t st
 }
 
 template <int MAXP>
-static cudaError_t dispatch_dec(int adt, int bits, int mt, bool sacc, int dbg, const DecBatch<MAXP>& b,
+static cudaError_t dispatch_dec(int adt, int bits, int mt, int sacc, int dbg, const DecBatch<MAXP>& b,
                                 int ctas, cudaStream_t st) {
-  if (dbg && adt == FQ_BF16 && bits == 4 && mt == 1 && sacc && MAXP == 1) {
-    if (dbg == 1) return launch_dec<__nv_bfloat16, 4, 1, true, 1, MAXP>(b, ctas, st);
-    if (dbg == 2) return launch_dec<__nv_bfloat16, 4, 1, true, 2, MAXP>(b, ctas, st);
-    if (dbg == 3) return launch_dec<__nv_bfloat16, 4, 1, true, 3, MAXP>(b, ctas, st);
+  if (dbg && adt == FQ_BF16 && bits == 4 && mt == 1 && sacc == 1 && MAXP == 1) {
+    if (dbg == 1) return launch_dec<__nv_bfloat16, 4, 1, 1, 1, MAXP>(b, ctas, st);
+    if (dbg == 2) return launch_dec<__nv_bfloat16, 4, 1, 1, 2, MAXP>(b, ctas, st);
+    if (dbg == 3) return launch_dec<__nv_bfloat16, 4, 1, 1, 3, MAXP>(b, ctas, st);
   }
 #define FQ_DEC_CASE(TT, BB, MM, SS) \
   if (bits == BB && mt == MM && sacc == SS) return launch_dec<TT, BB, MM, SS, 0, MAXP>(b, ctas, st);
   if (adt == FQ_BF16) {
-    FQ_DEC_CASE(__nv_bfloat16, 4, 1, true) FQ_DEC_CASE(__nv_bfloat16, 4, 1, false)
-    FQ_DEC_CASE(__nv_bfloat16, 4, 2, true) FQ_DEC_CASE(__nv_bfloat16, 4, 2, false)
-    FQ_DEC_CASE(__nv_bfloat16, 4, 4, true)
-    FQ_DEC_CASE(__nv_bfloat16, 8, 1, true) FQ_DEC_CASE(__nv_bfloat16, 8, 1, false)
-    FQ_DEC_CASE(__nv_bfloat16, 8, 2, true) FQ_DEC_CASE(__nv_bfloat16, 8, 2, false)
+    FQ_DEC_CASE(__nv_bfloat16, 4, 1, 1) FQ_DEC_CASE(__nv_bfloat16, 4, 1, 0)
+    FQ_DEC_CASE(__nv_bfloat16, 4, 2, 1) FQ_DEC_CASE(__nv_bfloat16, 4, 2, 0)
+    FQ_DEC_CASE(__nv_bfloat16, 4, 4, 1)
+    FQ_DEC_CASE(__nv_bfloat16, 4, 1, 2) FQ_DEC_CASE(__nv_bfloat16, 4, 2, 2)
+    FQ_DEC_CASE(__nv_bfloat16, 8, 1, 1) FQ_DEC_CASE(__nv_bfloat16, 8, 1, 0)
+    FQ_DEC_CASE(__nv_bfloat16, 8, 2, 1) FQ_DEC_CASE(__nv_bfloat16, 8, 2, 0)
   } else {
-    FQ_DEC_CASE(__half, 4, 1, true) FQ_DEC_CASE(__half, 4, 1, false)
-    FQ_DEC_CASE(__half, 4, 2, true) FQ_DEC_CASE(__half, 4, 2, false)
-    FQ_DEC_CASE(__half, 4, 4, true)
-    FQ_DEC_CASE(__half, 8, 1, true) FQ_DEC_CASE(__half, 8, 1, false)
-    FQ_DEC_CASE(__half, 8, 2, true) FQ_DEC_CASE(__half, 8, 2, false)
+    FQ_DEC_CASE(__half, 4, 1, 1) FQ_DEC_CASE(__half, 4, 1, 0)
+    FQ_DEC_CASE(__half, 4, 2, 1) FQ_DEC_CASE(__half, 4, 2, 0)
+    FQ_DEC_CASE(__half, 4, 4, 1)
+    FQ_DEC_CASE(__half, 4, 1, 2) FQ_DEC_CASE(__half, 4, 2, 2)
+    FQ_DEC_CASE(__half, 8, 1, 1) FQ_DEC_CASE(__half, 8, 1, 0)
+    FQ_DEC_CASE(__half, 8, 2, 1) FQ_DEC_CASE(__half, 8, 2, 0)
   }
 #undef FQ_DEC_CASE
   return cudaErrorInvalidValue;
@@ -927,7 +975,7 @@ static cudaError_t dispatch_dec(int adt, int bits, int mt, bool sacc, int dbg, c
 // [K/128][ntok_all][4] array.
 static bool make_dec_prob(DecProb& d, const GemvPlan& pl, int bits, int cdt, const void* A, int M, int K,
                           int N, const void* codes, const void* scales, int group, void* C, void* ws,
-                          const void* Sp = nullptr, int ntok_all = 0, int tok_base = 0) {
+                          const void* Sp = nullptr, int ntok_all = 0, int tok_base = 0, bool gs = false) {
   const uint64_t row_bytes = (uint64_t)K * bits / 8;
   if (!make_tmap_2d(&d.w, codes, 1, row_bytes, (uint64_t)N, row_bytes, kWBytesPerRow, kWBoxRows, 64))
     return false;
@@ -939,11 +987,11 @@ static bool make_dec_prob(DecProb& d, const GemvPlan& pl, int bits, int cdt, con
     return false;
   // per-element-scale path (group does not cover a stage): stage the KS / group scale rows by TMA
   // when the group divides the stage (then a power of two >= 16), else read them from global memory
-  const bool sacc = group % ks == 0;
+  const int sacc = gs ? 2 : (group % ks == 0 ? 1 : 0);
   d.sc_rows = (!sacc && ks % group == 0) ? ks / group : 0;
   d.sc_shift = d.sc_rows ? __builtin_ctz((unsigned)group) : 0;
   if (!make_tmap_2d(&d.s, scales, 2, (uint64_t)N, (uint64_t)(K / group), (uint64_t)N * 2, kWBoxRows,
-                    d.sc_rows ? d.sc_rows : 1, 0))
+                    d.sc_rows ? d.sc_rows : (sacc == 2 ? 2 : 1), 0))
     return false;
   d.scales = scales;
   d.C = C;
@@ -957,19 +1005,24 @@ static bool make_dec_prob(DecProb& d, const GemvPlan& pl, int bits, int cdt, con
   return true;
 }
 
-static bool sacc_of(int bits, int group) { return group % (bits == 4 ? 128 : 64) == 0; }
+// scale path: 1 = one scale group per stage, 2 = two 64-k groups (group split), 0 = per element
+static int sacc_of(int bits, int group, int K = -1) {
+  if (group % (bits == 4 ? 128 : 64) == 0) return 1;
+  return (K >= 0 && gs_of(bits, group, K)) ? 2 : 0;
+}
 
 cudaError_t run_gemv(const GemvPlan& pl, int adt, int cdt, int bits, const void* A, int M, int K,
                      int N, const void* codes, const void* scales, int group, void* C, void* ws,
                      cudaStream_t st) {
   DecBatch<1> b{};
-  if (nib_of(bits, group)) {
+  if (nib_of(bits, group, K)) {
     char* pre = reinterpret_cast<char*>(ws) + kCounterBytes +
                 (pl.splits > 1 ? align256((size_t)pl.splits * M * N * sizeof(float)) : 0);
     char* Sp = pre + align256((size_t)M * K * 2);
-    cudaError_t r = launch_prep(adt, A, M, K, pre, Sp, st);
+    cudaError_t r = launch_prep(adt, A, M, K, pre, Sp, st, sacc_of(bits, group, K) == 2);
     if (r != cudaSuccess) return r;
-    if (!make_dec_prob(b.p[0], pl, bits, cdt, pre, M, K, N, codes, scales, group, C, ws, Sp, M, 0))
+    if (!make_dec_prob(b.p[0], pl, bits, cdt, pre, M, K, N, codes, scales, group, C, ws, Sp, M, 0,
+                       sacc_of(bits, group, K) == 2))
       return cudaErrorInvalidValue;
   } else if (!make_dec_prob(b.p[0], pl, bits, cdt, A, M, K, N, codes, scales, group, C, ws)) {
     return cudaErrorInvalidValue;
@@ -977,7 +1030,7 @@ cudaError_t run_gemv(const GemvPlan& pl, int adt, int cdt, int bits, const void*
   b.p[0].cta_begin = 0;
   b.nprob = 1;
   const int ctas = b.p[0].gx * pl.splits * pl.ktiles;
-  return dispatch_dec<1>(adt, bits, pl.mt, sacc_of(bits, group), env_int("FQ_DEC_DEBUG", 0), b, ctas, st);
+  return dispatch_dec<1>(adt, bits, pl.mt, sacc_of(bits, group, K), env_int("FQ_DEC_DEBUG", 0), b, ctas, st);
 }
 
 // ---- MoE batch (kernel A7, decode side): experts listed in `experts` (each with 1 <= M_e <= 16)

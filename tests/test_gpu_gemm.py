@@ -293,6 +293,8 @@ def test_opt175b_prefill_sampled(fq, shape, bits):
     (9, 2048, 640, 8, 64, "bf16", None),
     (5, 2048, 384, 8, 128, "fp16", 2),
     (12, 1024, 512, 4, 1024, "fp16", None),  # per-column
+    (7, 1024, 768, 4, 64, "fp16", None),     # group 64: group-split nibble path
+    (13, 2048, 512, 4, 64, "bf16", 3),       # group 64, two MMA token tiles, split-K
 ])
 def test_decode_kernels(fq, env, impl, M, K, N, bits, group, adt, splits):
     """Both decode kernels (tcgen05 A4 and the mma.sync A4) against the oracle."""
