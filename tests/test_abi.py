@@ -70,3 +70,21 @@ def test_validation_is_synchronous_and_launch_free(fq):
     assert fq._lib.fq_adapt_flags(dummy, 0, 256, 8, 0, 16, dummy, None, None) == fq.FQ_ERR_INVALID_ARG
     assert fq._lib.fq_adapt_flags(dummy, 0, 256, 8, 1001, 16, dummy, None, None) == fq.FQ_ERR_INVALID_ARG
     assert fq.fq_status_str(fq.FQ_ERR_SHAPE) == "FQ_ERR_SHAPE"
+
+
+def test_gemm_workspace_sizes(fq):
+    """Workspace contract (fq.h): 64 KiB counter region first; decode paths add partials + the
+    pre-converted activations; the tensor-core path adds split-K partials only when its output
+    tiles cannot fill the GPU.  Pure host logic (no device calls)."""
+    d = fq.make_wdesc(12288, 49152, 4, 128, fq.FQ_BF16)
+    for M in (1, 8, 16, 32):  # decode path (int4 g128 serves M <= 32)
+        assert fq.fq_gemm_workspace_bytes(M, d) >= 65536 + M * 12288 * 2
+    big = fq.make_wdesc(12288, 49152, 4, 128, fq.FQ_BF16)
+    assert fq.fq_gemm_workspace_bytes(2048, big) == 256           # 384 x 8 tiles fill the GPU: no split
+    small = fq.make_wdesc(4096, 512, 4, 128, fq.FQ_BF16)
+    nb = fq.fq_gemm_workspace_bytes(64, small)                    # 4 tiles: split-K partials
+    assert nb > 65536 and (nb - 65536) % (4 * 64 * 128 * 4) == 0
+    g64 = fq.make_wdesc(5120, 5120, 4, 64, fq.FQ_FP16)
+    assert fq.fq_gemm_workspace_bytes(16, g64) >= 65536 + 16 * 5120 * 2  # group-split nibble path
+    assert fq.fq_gemm_workspace_bytes(0, d) == 0
+    assert fq.fq_gemm_grouped_workspace_bytes(64 * 16, 64, fq.make_wdesc(4096, 16384, 4, 4096, 0)) >= 65536
