@@ -271,21 +271,31 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
       work_coords(p, tile, mt, nt, tt, ks, kb0, kb1);
       const int n = nt * BM + row;
       const int nc = min(n, N - 1);
-      int j0 = (kb0 * BK) / p.group, r0 = kb0 * BK - j0 * p.group;  // first staged scale row
+      const int grp = p.group;                     // hoisted: p lives in the parameter space
+      const bool one_scale = grp % kKPW == 0;      // this thread's kKPW k lie in one group
+      int j0 = (kb0 * BK) / grp, r0 = kb0 * BK - j0 * grp;  // first staged scale row
       // group of this thread's first k (kb0*64 + half*kKPW) and its offset in the group
-      int jb = (kb0 * BK + half * kKPW) / p.group, gk = kb0 * BK + half * kKPW - jb * p.group;
+      int jb = (kb0 * BK + half * kKPW) / grp, gk = kb0 * BK + half * kKPW - jb * grp;
+      const uint32_t srow = sb + Gm::SC_OFS + row * 2;
       for (int kb = kb0; kb < kb1; ++kb) {
         // scales of this thread's 8-k words from the TMA-staged rows: word w lies in group
         // jb + t, t = [gk + 8w >= g] + [gk + 8w >= 2g]; row index in smem = group - j0.
         mbar_wait(&full_bar[s], ph);
         constexpr int NW = kKPW / 8;  // 8-k words of this thread
         uint32_t sc[NW];
+        if (one_scale) {
+          const uint32_t v = lds_u16(srow + s * Gm::STAGE + (jb - j0) * BM * 2);
+          const uint32_t v2 = prmt(v, v, 0x1010u);
 #pragma unroll
-        for (int w = 0; w < NW; ++w) {
-          const int o = gk + 8 * w;
-          const int jr = jb - j0 + (o >= p.group) + (o >= 2 * p.group);
-          const uint32_t v = lds_u16(sb + s * Gm::STAGE + Gm::SC_OFS + (jr * BM + row) * 2);
-          sc[w] = v | (v << 16);
+          for (int w = 0; w < NW; ++w) sc[w] = v2;
+        } else {
+#pragma unroll
+          for (int w = 0; w < NW; ++w) {
+            const int o = gk + 8 * w;
+            const int jr = jb - j0 + (o >= grp) + (o >= 2 * grp);
+            const uint32_t v = lds_u16(srow + s * Gm::STAGE + jr * BM * 2);
+            sc[w] = prmt(v, v, 0x1010u);
+          }
         }
         const uint32_t qbase = sb + s * Gm::STAGE + Gm::ACT_BYTES + row * Gm::CODE_BYTES_ROW;
         uint32_t out[kKPW / 2];
@@ -333,9 +343,9 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
         if (lane == 0) mbar_arrive(&afull_bar[s]);
         if (++s == STAGES) { s = 0; ph ^= 1; }
         r0 += BK;
-        while (r0 >= p.group) { r0 -= p.group; ++j0; }
+        while (r0 >= grp) { r0 -= grp; ++j0; }
         gk += BK;
-        while (gk >= p.group) { gk -= p.group; ++jb; }
+        while (gk >= grp) { gk -= grp; ++jb; }
       }
       // ---- epilogue: accumulator row `row` (weight n), tokens [half*TPP, half*TPP+TPP)
       mbar_wait(&acc_full, acc_ph);
