@@ -212,15 +212,18 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
         int mt, nt, tt, ks, kb0, kb1;
         work_coords(p, tile, mt, nt, tt, ks, kb0, kb1);
         // first scale row of the K block = floor(64 kb / g), division-free after the first block
-        int j0 = (kb0 * BK) / p.group, r0 = (kb0 * BK) - j0 * p.group;
+        const int grp = p.group;  // hoisted out of the parameter space
+        const uint32_t tx = p.bn * BK * 2 + Gm::CODE_BYTES + kScRows * BM * 2;
+        const int arow = mt * p.bn, wrow = nt * BM;
+        int j0 = (kb0 * BK) / grp, r0 = (kb0 * BK) - j0 * grp;
         for (int kb = kb0; kb < kb1; ++kb, r0 += BK) {
-          while (r0 >= p.group) { r0 -= p.group; ++j0; }
+          while (r0 >= grp) { r0 -= grp; ++j0; }
           mbar_wait(&empty_bar[s], ph ^ 1);
           uint8_t* st = sbase + s * Gm::STAGE;
-          mbar_arrive_expect_tx(&full_bar[s], p.bn * BK * 2 + Gm::CODE_BYTES + kScRows * BM * 2);
-          tma_load_2d(st + Gm::SC_OFS, &p.s, &full_bar[s], nt * BM, j0, pol_q);
-          tma_load_2d(st, &p.a, &full_bar[s], kb * BK, mt * p.bn, pol_a);
-          tma_load_2d(st + Gm::ACT_BYTES, &p.q, &full_bar[s], kb * Gm::CODE_BYTES_ROW, nt * BM, pol_q);
+          mbar_arrive_expect_tx(&full_bar[s], tx);
+          tma_load_2d(st + Gm::SC_OFS, &p.s, &full_bar[s], wrow, j0, pol_q);
+          tma_load_2d(st, &p.a, &full_bar[s], kb * BK, arow, pol_a);
+          tma_load_2d(st + Gm::ACT_BYTES, &p.q, &full_bar[s], kb * Gm::CODE_BYTES_ROW, wrow, pol_q);
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
       }
