@@ -268,7 +268,7 @@ __device__ __forceinline__ int prow(int m) { return m; }
 // physical 16-byte cell of logical cell c in tile row R under CU_TENSOR_MAP_SWIZZLE_64B
 __device__ __forceinline__ int swz64(int c, int R) { return c ^ ((R >> 1) & 3); }
 
-// DBG (diagnostics only, selected by FQ_DEC_DEBUG for bf16/int4/M<=8): 1 = no MMA (fake FADD
+// DBG (diagnostics only, selected by FQ_DEC_DEBUG for bf16/int4/M<=8; 4 = skeleton streaming codes only): 1 = no MMA (fake FADD
 // accumulate), 2 = no dequant (raw code words as MMA operands), 3 = consumers skip all compute.
 template <typename T, int BITS, int MT, int SACC, int DBG, int MAXP>
 // Register caps (two CTAs per SM fit up to 112 / 96 registers at 288 / 320 threads), set without
@@ -357,6 +357,11 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
         uint8_t* st = sbase + s * STAGE_BYTES;
         const int k0 = kbeg + i * KS;
         const int scb = SACC ? SACC * kRowsPerCta * 2 : p.sc_rows * kRowsPerCta * 2;
+        if (DBG == 4) {  // diagnostics: codes only
+          mbar_arrive_expect_tx(&full_bar[s], kStageW);
+          tma_load_2d(st, &p.w, &full_bar[s], k0 * BITS / 8, n0, polw);
+          return;
+        }
         mbar_arrive_expect_tx(&full_bar[s], kStageW + scb + (NIB ? RAW_BYTES + MT * 8 * 16 : 0));
 #pragma unroll
         for (int bx2 = 0; bx2 < kWBoxes; ++bx2)
@@ -376,6 +381,7 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
         }
       };
       auto issue_a = [&](int i, int s) {  // the stage's activations (+ per-chunk sums)
+        if (DBG == 4) return;
         uint8_t* st = sbase + s * STAGE_BYTES;
         const int k0 = kbeg + i * KS;
         if (NIB) {
@@ -517,7 +523,7 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
           sh[rt][gi] = lds_scale<T>(wst + SC_OFS + gi * kRowsPerCta * 2 + Rh[rt] * 2);
         }
     }
-    if (DBG != 3) {
+    if (DBG != 3 && DBG != 4) {
       uint4 b[LAZY ? 1 : MT][PIECES];
       if (!LAZY) {
 #pragma unroll
@@ -695,7 +701,7 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
         }
       }
     }
-    if (!EARLY || DBG == 3) {
+    if (!EARLY || DBG == 3 || DBG == 4) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[s]);
     }
@@ -947,6 +953,7 @@ static cudaError_t dispatch_dec(int adt, int bits, int mt, int sacc, int dbg, co
     if (dbg == 1) return launch_dec<__nv_bfloat16, 4, 1, 1, 1, MAXP>(b, ctas, st);
     if (dbg == 2) return launch_dec<__nv_bfloat16, 4, 1, 1, 2, MAXP>(b, ctas, st);
     if (dbg == 3) return launch_dec<__nv_bfloat16, 4, 1, 1, 3, MAXP>(b, ctas, st);
+    if (dbg == 4) return launch_dec<__nv_bfloat16, 4, 1, 1, 4, MAXP>(b, ctas, st);
   }
 #define FQ_DEC_CASE(TT, BB, MM, SS) \
   if (bits == BB && mt == MM && sacc == SS) return launch_dec<TT, BB, MM, SS, 0, MAXP>(b, ctas, st);

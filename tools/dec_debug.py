@@ -18,7 +18,7 @@ for K, N in ((12288, 49152), (49152, 12288)):
     q = fq.quantize(W, 4, 128); del W
     A = gaussian_torch((1, K), 1.0, 2)
     C = torch.empty(1, N, dtype=torch.bfloat16, device="cuda")
-    for dbg in ("0", "1", "2", "3"):
+    for dbg in ("0", "3", "4"):
         os.environ["FQ_DEC_DEBUG"] = dbg
         for sp in (os.environ.get("SPLITS_LIST", "0").split(",")):
             if sp != "0": os.environ["FQ_GEMV_SPLITS"] = sp
