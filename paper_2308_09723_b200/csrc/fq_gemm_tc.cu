@@ -38,6 +38,9 @@ constexpr int BK = 64;         // K per stage (one SWIZZLE_128B atom of bf16)
 // Dequant warps per CTA: dq_warps(BNMAX) / 4 per TMEM lane quarter, each covering BK / parts k of a
 // K block.  Measured: 16 warps are faster for the small-tile variants (memory/latency-bound
 // regime), 8 for the 256-token variant (tensor-bound prefill).
+#ifndef FQ_TC_DBG
+#define FQ_TC_DBG 0  // diagnostics only: 1 = no MMA, 2 = no dequant / tcgen05.st, 3 = both (TMA pipeline alone)
+#endif
 #ifndef FQ_TC_DQW
 #define FQ_TC_DQW 0  // diagnostics: force 8 or 16 for every variant
 #endif
@@ -248,7 +251,7 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
           const uint64_t bdesc = sw128_desc(sb + s * Gm::STAGE);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk)
-            mma_ts(tmem + kAccCol, tmem + kACol + s * 32 + kk * 8, bdesc + (uint64_t)(kk * 2), idesc,
+            if (!(FQ_TC_DBG & 1)) mma_ts(tmem + kAccCol, tmem + kACol + s * 32 + kk * 8, bdesc + (uint64_t)(kk * 2), idesc,
                    (kb != kb0) || (kk != 0));
           mma_commit(&empty_bar[s]);
           if (++s == STAGES) { s = 0; ph ^= 1; }
@@ -302,7 +305,8 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
         }
         const uint32_t qbase = sb + s * Gm::STAGE + Gm::ACT_BYTES + row * Gm::CODE_BYTES_ROW;
         uint32_t out[kKPW / 2];
-        if (BITS == 4) {
+        if (FQ_TC_DBG & 2) {
+        } else if (BITS == 4) {
           // kKPW/2 bytes; SWIZZLE_32B: 16-byte chunk c of row r sits at c ^ ((r >> 2) & 1)
           uint32_t words[NW];
           if constexpr (kKPW == 32) {
@@ -336,7 +340,8 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
             }
           }
         }
-        if constexpr (kKPW == 32)
+        if (FQ_TC_DBG & 2) {
+        } else if constexpr (kKPW == 32)
           tmem_st16(tmem + lane_base + kACol + s * 32 + half * 16, *reinterpret_cast<const uint32_t(*)[16]>(out));
         else
           tmem_st8(tmem + lane_base + kACol + s * 32 + half * 8, *reinterpret_cast<const uint32_t(*)[8]>(out));
