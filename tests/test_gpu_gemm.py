@@ -225,7 +225,7 @@ def test_large_m(fq, M):
 
 @pytest.mark.parametrize("shape", [(12288, 49152), (49152, 12288)])
 @pytest.mark.parametrize("bits", [4, 8])
-@pytest.mark.parametrize("M", [1, 16])
+@pytest.mark.parametrize("M", [1, 16, 32])
 def test_opt175b_full_size_sampled(fq, shape, bits, M):
     """configs[1] at full size in the bench's launch configuration; parity on 64 sampled columns
     computed by the oracle one by one (scales/codes of those columns only)."""
