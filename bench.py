@@ -303,13 +303,29 @@ def main():
     h2d = sum(v.numel() * v.element_size() for v in h_x.values())
     d2h = sum(v.numel() * v.element_size() for v in h_z.values())
 
+    # Host <-> device traffic on its own stream (a serving loop overlaps its input upload and
+    # result download with compute): every input of the step is uploaded up front, each GEMM
+    # pair waits only for its own input, each result is downloaded as soon as it is ready.
+    copy_stream = torch.cuda.Stream(device=dev)
+    up_ev = {M: torch.cuda.Event() for M in M_SWEEP}
+    done_ev = {M: torch.cuda.Event() for M in M_SWEEP}
+
     def e2e_step():
+        copy_stream.wait_stream(stream)  # previous step's results are consumed in order
+        with torch.cuda.stream(copy_stream):
+            for M in M_SWEEP:
+                d_x[M].copy_(h_x[M], non_blocking=True)
+                up_ev[M].record(copy_stream)
         for M in M_SWEEP:
-            d_x[M].copy_(h_x[M], non_blocking=True)
+            stream.wait_event(up_ev[M])
             y = fq.gemm(d_x[M], q1, out=ys[M])
             fq.gemm(y, q2, out=zs[M])
             reduce(M)
-            h_z[M].copy_(zs[M], non_blocking=True)
+            done_ev[M].record(stream)
+            with torch.cuda.stream(copy_stream):
+                copy_stream.wait_event(done_ev[M])
+                h_z[M].copy_(zs[M], non_blocking=True)
+        stream.wait_stream(copy_stream)  # the step ends when its results are on the host
 
     for _ in range(3):
         e2e_step()
