@@ -101,24 +101,28 @@ __device__ __forceinline__ float Chunk8<float>::amax() const {
 constexpr int kQThreads = 256;
 
 // ------------------------------------------------------------------------------------- A3
-constexpr int kQCpt = 8;  // chunks per thread cached in registers by the quantizer
+constexpr int kQCpt = 8;      // chunks per thread cached in registers by the quantizer
+constexpr int kQSlice = 12288;  // target K-slice per CTA (192 threads at kQCpt = 8)
 
 template <typename TIn, typename TS, int BITS, int CPT = kQCpt>
 __global__ void __launch_bounds__(sizeof(TIn) == 4 ? 512 : 1024) quantize_kernel(const TIn* __restrict__ W, int K,
-                                                             int N, int group,
+                                                             int KS, int N, int group,
                                                              uint8_t* __restrict__ codes,
                                                              TS* __restrict__ scales,
                                                              int32_t* __restrict__ status) {
   extern __shared__ float smem[];
-  const int nchunk = K >> 3;
-  const int G = K / group;
+  // CTA = one K-slice of KS elements (a multiple of the group) of one paper column: long columns
+  // are split so that every CTA stays small enough for several to share an SM.
+  const int nsl = K / KS;
+  const int n = blockIdx.x / nsl, sl = blockIdx.x - n * nsl;
+  const int nchunk = KS >> 3;
+  const int G = KS / group;
   const int cpg = group >> 3;  // chunks per group
   float* pm = smem;            // [nchunk]
   float* sc = smem + nchunk;   // [G] scale as float (0 => codes 0)
   float* sr = sc + G;          // [G] rcp(scale) (0 when the scale is 0)
   __shared__ int s_status;
-  const int n = blockIdx.x;
-  const TIn* row = W + (size_t)n * K;
+  const TIn* row = W + (size_t)n * K + (size_t)sl * KS;
   if (threadIdx.x == 0) s_status = 0;
 
   // pass 1: chunk maxima; the raw chunks stay in registers for pass 3 (CPT chunks per thread,
@@ -158,7 +162,7 @@ __global__ void __launch_bounds__(sizeof(TIn) == 4 ? 512 : 1024) quantize_kernel
     }
     sc[j] = s;
     sr[j] = s == 0.f ? 0.f : __frcp_rn(s);
-    scales[(size_t)j * N + n] = s_t;
+    scales[(size_t)(sl * G + j) * N + n] = s_t;
     if (st) atomicOr(&s_status, st);
   };
   if (cpg <= 32) {
@@ -192,27 +196,49 @@ __global__ void __launch_bounds__(sizeof(TIn) == 4 ? 512 : 1024) quantize_kernel
     const float rs = sr[j];  // rcp(s), 0 when s == 0
     const float hs = 0.5f * s;     // exact
     // offset-binary code u = q + 2^(b-1) in [0, 2^b - 1]; the stored two's complement field is
-    // u ^ 2^(b-1).  Kept in float until the final pack (all values are small exact integers).
-    uint32_t u[8];
+    // u ^ 2^(b-1).
     if (Dt<TIn>::id != FQ_FP32 && s >= 1e-30f) {
-      // 16-bit W: m = rn(|x| * rcp(s)) (magic-number rounding, no F2I/FRND) is the correctly rounded
-      // quotient except possibly at an exact tie |x| = (m + 1/2) s, where round-half-away needs m + 1;
-      // the tie is detected exactly because (m + 1/2) s = fma(m, s, s/2) is an exact fp32 value
-      // (<= 20 significant bits).  Off-tie quotients are >= 2^-13 (absolute) away from a half-integer
-      // (x, s have <= 11 significant bits), far beyond the ~2^-16 error of the estimate.
-      constexpr float kMagic = 12582912.f;  // 1.5 * 2^23: t + kMagic holds rn(t) in its low mantissa bits
+      // 16-bit W, signed magic-number rounding: t = fma(x, rcp(s), 1.5 * 2^23 + 2^(b-1)) holds
+      // u' = rn_even(x / s) + 2^(b-1) in its low mantissa bits (the magic is even, the sum stays in
+      // [2^23, 2^24)), so the raw bits ARE 0x4B400000 + u'.  rn_even(x * rcp(s)) is the correctly
+      // rounded quotient except possibly at an exact tie |x| = (|m| + 1/2) s, where round-half-away
+      // needs one more step away from zero; the tie is detected exactly because
+      // m s + sign(x) s/2 = fma(m, s, +-s/2) is an exact fp32 value (<= 20 significant bits).
+      // Off-tie quotients are >= 2^-13 (absolute) away from a half-integer (x, s have <= 11
+      // significant bits), far beyond the ~2^-16 error of the estimate.  |x| <= amax
+      // keeps x / s within (-2^(b-1) - 1/2, 2^(b-1) + 1/2), so only the top needs a clamp.
+      constexpr float kMagic = 12582912.f + (float)(1 << (BITS - 1));
+      constexpr int32_t kBase = 0x4B400000;
+      const uint32_t hsb = __float_as_uint(hs);
+      int32_t tb[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const float ax = fabsf(v[i]);
-        const float t = fmaf(ax, rs, kMagic);
-        const float mf = t - kMagic;                        // rn(|x| / s) as an exact float
-        int m = __float_as_int(t) - 0x4B400000;
-        m += (fmaf(mf, s, hs) == ax) ? 1 : 0;
-        const bool neg = __float_as_uint(v[i]) >> 31;
-        m = min(m, neg ? -lo : hi);
-        u[i] = (uint32_t)((neg ? -m : m) - lo);
-      }    } else {
+        const uint32_t sgn = __float_as_uint(v[i]) & 0x80000000u;
+        float t = fmaf(v[i], rs, kMagic);
+        const float mf = t - kMagic;                                   // rn_even(x / s), exact
+        const bool tie = fmaf(mf, s, __uint_as_float(sgn | hsb)) == v[i];
+        if (tie) t += __uint_as_float(sgn | 0x3F800000u);              // +-1 away from zero
+        tb[i] = min(__float_as_int(t), kBase + (1 << BITS) - 1);
+      }
+      // pack the raw bit patterns: every field carries kBase, whose packed sum is one constant
+      if (BITS == 4) {
+        uint32_t w = (uint32_t)tb[7];
+#pragma unroll
+        for (int i = 6; i >= 0; --i) w = w * 16u + (uint32_t)tb[i];
+        constexpr uint32_t kBias = (uint32_t)kBase * 0x11111111u;
+        reinterpret_cast<uint32_t*>(codes + (size_t)n * (K / 2))[sl * nchunk + c] = (w - kBias) ^ 0x88888888u;
+      } else {
+        constexpr uint32_t kBias = (uint32_t)kBase * 0x01010101u;
+        uint2 w;
+        w.x = ((uint32_t)tb[3] * 256u + (uint32_t)tb[2]) * 256u * 256u + (uint32_t)tb[1] * 256u + (uint32_t)tb[0];
+        w.y = ((uint32_t)tb[7] * 256u + (uint32_t)tb[6]) * 256u * 256u + (uint32_t)tb[5] * 256u + (uint32_t)tb[4];
+        w.x = (w.x - kBias) ^ 0x80808080u;
+        w.y = (w.y - kBias) ^ 0x80808080u;
+        reinterpret_cast<uint2*>(codes + (size_t)n * K)[sl * nchunk + c] = w;
+      }
+    } else {
       // fp32 W (no tie-distance guarantee) and tiny/subnormal scales: IEEE division decides.
+      uint32_t u[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         float m = 0.f;
@@ -221,19 +247,19 @@ __global__ void __launch_bounds__(sizeof(TIn) == 4 ? 512 : 1024) quantize_kernel
         m = fminf(m, neg ? (float)-lo : (float)hi);
         u[i] = (uint32_t)(int)((neg ? -m : m) + (float)-lo);
       }
-    }
-    if (BITS == 4) {
-      uint32_t w = u[7];
+      if (BITS == 4) {
+        uint32_t w = u[7];
 #pragma unroll
-      for (int i = 6; i >= 0; --i) w = w * 16u + u[i];
-      reinterpret_cast<uint32_t*>(codes + (size_t)n * (K / 2))[c] = w ^ 0x88888888u;
-    } else {
-      uint2 w;
-      w.x = ((u[3] * 256u + u[2]) * 256u + u[1]) * 256u + u[0];
-      w.y = ((u[7] * 256u + u[6]) * 256u + u[5]) * 256u + u[4];
-      w.x ^= 0x80808080u;
-      w.y ^= 0x80808080u;
-      reinterpret_cast<uint2*>(codes + (size_t)n * K)[c] = w;
+        for (int i = 6; i >= 0; --i) w = w * 16u + u[i];
+        reinterpret_cast<uint32_t*>(codes + (size_t)n * (K / 2))[sl * nchunk + c] = w ^ 0x88888888u;
+      } else {
+        uint2 w;
+        w.x = ((u[3] * 256u + u[2]) * 256u + u[1]) * 256u + u[0];
+        w.y = ((u[7] * 256u + u[6]) * 256u + u[5]) * 256u + u[4];
+        w.x ^= 0x80808080u;
+        w.y ^= 0x80808080u;
+        reinterpret_cast<uint2*>(codes + (size_t)n * K)[sl * nchunk + c] = w;
+      }
     }
   }
   __syncthreads();
@@ -266,9 +292,7 @@ __global__ void __launch_bounds__(kQThreads) adapt_flags_kernel(const TIn* __res
   for (int c = threadIdx.x; c < nchunk; c += kQThreads) {
     Chunk8<TIn> ch;
     ch.load(row + (size_t)c * 8);
-    float v[8];
-    ch.decode(v);
-    pm[c] = chunk_amax(v);
+    pm[c] = ch.amax();
   }
   __syncthreads();
   // finest level L = nlev-1 stored at lev[0 .. Gf)
@@ -306,18 +330,26 @@ __global__ void __launch_bounds__(kQThreads) adapt_flags_kernel(const TIn* __res
 template <typename TIn, typename TS, int BITS>
 static cudaError_t launch_quant(const void* W, int K, int N, int group, void* codes, void* scales,
                                 int32_t* status, cudaStream_t st) {
-  const size_t smem = (size_t)(K / 8 + 2 * (K / group)) * sizeof(float);
+  // K-slice per CTA: the fewest slices that bring it to <= kQSlice elements (slices are whole
+  // groups; a group longer than that, e.g. one scale per column, keeps the whole column).
+  const int G = K / group;
+  int nsl = G;
+  for (int d = 1; d <= G; ++d)
+    if (G % d == 0 && K / d <= kQSlice) { nsl = d; break; }
+  const int KS = K / nsl;
+  const size_t smem = (size_t)(KS / 8 + 2 * (KS / group)) * sizeof(float);
   auto kern = quantize_kernel<TIn, TS, BITS>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
   // threads: enough that every 8-element chunk is cached in registers (<= kQCpt per thread)
-  const int nchunk = K / 8;
+  const int nchunk = KS / 8;
   int threads = ((nchunk + kQCpt - 1) / kQCpt + 31) / 32 * 32;
   threads = threads < 128 ? 128 : threads;
   if (threads > (sizeof(TIn) == 4 ? 512 : 1024)) return cudaErrorInvalidValue;  // rejected by the API
-  kern<<<N, threads, smem, st>>>((const TIn*)W, K, N, group, (uint8_t*)codes, (TS*)scales, status);
+  kern<<<(unsigned)N * nsl, threads, smem, st>>>((const TIn*)W, K, KS, N, group, (uint8_t*)codes, (TS*)scales,
+                                                 status);
   return cudaGetLastError();
 }
 

@@ -80,6 +80,15 @@ def test_quantize_exact_dtypes(fq, wdt, sdt):
     check_exact(fq, W, wdt, 8, 512, sdt)  # per-column
 
 
+@pytest.mark.parametrize("wdt,K,bits,group", [("bf16", 32768, 4, 128), ("fp16", 49152, 8, 64),
+                                               ("bf16", 30720, 4, 15360), ("fp32", 24576, 4, 256)])
+def test_quantize_exact_long_columns(fq, wdt, K, bits, group):
+    """Columns longer than one CTA's K-slice are quantized by several CTAs (whole groups each);
+    a group longer than the slice target keeps one group per CTA."""
+    W = gaussian_bits((8, K), 0.02, K + bits, wdt)
+    check_exact(fq, W, wdt, bits, group, "bf16")
+
+
 def test_quantize_exact_tiny_config(fq):
     # configs[0]: M=1, K=256, N=256, int4 group=64, bf16
     W = gaussian_bits((256, 256), 0.02, 1001)
@@ -99,6 +108,35 @@ def test_quantize_ties_all_bf16_patterns(fq):
     W = buf.reshape(n, K)
     for bits in (4, 8):
         check_exact(fq, W, "bf16", bits, 32, "bf16")
+
+
+@pytest.mark.parametrize("wdt", ["bf16", "fp16"])
+def test_quantize_exact_ties_both_signs(fq, wdt):
+    """Groups whose scale is exact (amax = (2^b - 1)/2 * 2^-e, so s = 2^-e) holding every
+    half-integer multiple (k + 1/2) s of both signs: each is an exact tie of |x|/s that App. A's
+    rounding (read as round-half-away, DESIGN R3) must send away from zero, plus the integer
+    multiples and -0.  Codes and scales must match the oracle bit for bit."""
+    for bits in (4, 8):
+        qmax = (1 << (bits - 1))
+        e = 6
+        halves = [(k + 0.5) * 2.0 ** -e for k in range(-qmax, qmax)]  # -(qmax - 1/2) s .. (qmax - 1/2) s
+        ints = [k * 2.0 ** -e for k in range(-qmax + 1, qmax)]
+        vals = np.array(halves + ints + [-0.0], dtype=np.float32)
+        group = 64 if bits == 4 else 512
+        K = 1024
+        rows = []
+        for r in range(8):
+            row = np.resize(np.random.default_rng(r).permutation(vals), K).astype(np.float32)
+            for g0 in range(0, K, group):  # plant the anchor amax = (qmax - 1/2) s in every group
+                row[g0 + r % group] = (qmax - 0.5) * 2.0 ** -e * (1 if r % 2 else -1)
+            rows.append(row)
+        W = np.stack(rows)
+        if wdt == "bf16":
+            from synth import f32_to_bf16_bits
+            bitsW = f32_to_bf16_bits(W)
+        else:
+            bitsW = W.astype(np.float16).view(np.uint16)
+        check_exact(fq, bitsW, wdt, bits, group, wdt)
 
 
 def test_zero_and_nonfinite_status(fq):
