@@ -327,30 +327,38 @@ __global__ void __launch_bounds__(kQThreads) adapt_flags_kernel(const TIn* __res
 }
 
 // ------------------------------------------------------------------------------------- launchers
-template <typename TIn, typename TS, int BITS>
-static cudaError_t launch_quant(const void* W, int K, int N, int group, void* codes, void* scales,
-                                int32_t* status, cudaStream_t st) {
+template <typename TIn, typename TS, int BITS, int CPT>
+static cudaError_t launch_quant_c(const void* W, int K, int N, int group, void* codes, void* scales,
+                                  int32_t* status, cudaStream_t st, int slice) {
   // K-slice per CTA: the fewest slices that bring it to <= kQSlice elements (slices are whole
   // groups; a group longer than that, e.g. one scale per column, keeps the whole column).
   const int G = K / group;
   int nsl = G;
   for (int d = 1; d <= G; ++d)
-    if (G % d == 0 && K / d <= kQSlice) { nsl = d; break; }
+    if (G % d == 0 && K / d <= slice) { nsl = d; break; }
   const int KS = K / nsl;
   const size_t smem = (size_t)(KS / 8 + 2 * (KS / group)) * sizeof(float);
-  auto kern = quantize_kernel<TIn, TS, BITS>;
+  auto kern = quantize_kernel<TIn, TS, BITS, CPT>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
   // threads: enough that every 8-element chunk is cached in registers (<= kQCpt per thread)
   const int nchunk = KS / 8;
-  int threads = ((nchunk + kQCpt - 1) / kQCpt + 31) / 32 * 32;
+  int threads = ((nchunk + CPT - 1) / CPT + 31) / 32 * 32;
   threads = threads < 128 ? 128 : threads;
   if (threads > (sizeof(TIn) == 4 ? 512 : 1024)) return cudaErrorInvalidValue;  // rejected by the API
   kern<<<(unsigned)N * nsl, threads, smem, st>>>((const TIn*)W, K, KS, N, group, (uint8_t*)codes, (TS*)scales,
                                                  status);
   return cudaGetLastError();
+}
+
+template <typename TIn, typename TS, int BITS>
+static cudaError_t launch_quant(const void* W, int K, int N, int group, void* codes, void* scales,
+                                int32_t* status, cudaStream_t st) {
+  // measured on B200 (OPT FC1/FC2): 8 chunks per thread and 12288-element slices beat 4 chunks
+  // and 4096 / 6144 / 24576-element slices
+  return launch_quant_c<TIn, TS, BITS, kQCpt>(W, K, N, group, codes, scales, status, st, kQSlice);
 }
 
 template <typename TIn, typename TS>
