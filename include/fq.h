@@ -101,8 +101,9 @@ fq_status fq_adapt_flags(const void* W, int32_t wdt, int64_t K, int64_t N, uint3
 int32_t fq_adapt_decide(int64_t K, int32_t min_group, const int32_t* flags_host);
 
 /* ---------------------------------------------------------------------------------------------
- * Quantize + pack (kernel A3), App. A with groups.  K <= 65536 for 16-bit W,
- * K <= 32768 for fp32 W (one CTA holds a whole column in registers), else FQ_ERR_SHAPE.
+ * Quantize + pack (kernel A3), App. A with groups.  One CTA holds a K-slice
+ * of whole groups of one column in registers, so group <= 65536 for 16-bit W and <= 32768 for
+ * fp32 W (any K otherwise), else FQ_ERR_SHAPE.
  *   s[j,n] = RNE_scale_dtype( 2 * max_{k in group j} |W[n,k]| / (2^bits - 1) )   (one rounding)
  *   q[n,k] = clamp( round_half_away( W[n,k] / s[k/group, n] ), -2^(bits-1), 2^(bits-1)-1 ),
  *            q = 0 where s == 0.
@@ -113,10 +114,13 @@ fq_status fq_quantize(const void* W, int32_t wdt, const fq_wdesc* d, void* codes
                       int32_t* status_dev, void* stream);
 
 /* ---------------------------------------------------------------------------------------------
- * Fused dequantize + GEMM (kernels A4/A5 for M <= 16, A6 for large M), §4.1:
+ * Fused dequantize + GEMM (kernels A4/A5 for M <= 32 on the int4 nibble path with group % 128 == 0
+ * and M <= 16 otherwise, A6 above), §4.1:
  *   C[m,n] = sum_k A[m,k] * q[n,k] * s[k/group, n]
  * A: [M, K] row-major, dtype adt in {BF16, FP16}; the scales must have dtype adt.
  * C: [M, N] row-major, dtype cdt in {adt, FP32} (FP32 is a diagnostic mode).
+ * M == 0 is an empty batch: validated (A and C may be NULL), nothing launched, FQ_OK.
+ * M < 0 or M > 2^20: FQ_ERR_SHAPE.
  * ws/ws_bytes: device scratch of at least fq_gemm_workspace_bytes(M, d) bytes.  Layout: a fixed
  *   64 KiB region of arrival counters at offset 0, then split-K fp32 partials.  The buffer must be
  *   ZERO-FILLED once before its first use; every call leaves the counters zeroed again, so one
@@ -139,9 +143,10 @@ fq_status fq_gemm(const void* A, int32_t adt, int64_t M, const fq_wdesc* d, cons
  *   rows offsets[e] .. offsets[e+1]-1 of A ([T, K]) use expert e; C is [T, N].
  * offsets_host: HOST array of E+1 int64 (non-decreasing, offsets[0] = 0, offsets[E] = T).
  * codes_host / scales_host: HOST arrays of E DEVICE pointers (canonical layout per expert);
- * groups_host: HOST array of E group sizes (each valid for K).  Experts with 1 <= M_e <= 16 run
- * in one launch per kernel class of the decode kernel (A4, batched); larger experts run the
- * tcgen05 kernel (A6).  ws: fq_gemm_grouped_workspace_bytes(...) bytes, zero-filled once (same
+ * groups_host: HOST array of E group sizes (each valid for K).  Experts with 1 <= M_e <= 16 (32
+ * on the int4 nibble path) run in one launch per kernel class of the decode kernel (A4, batched);
+ * larger experts run the tcgen05 kernel (A6); empty experts launch nothing (T == 0: A and C may be
+ * NULL, FQ_OK).  ws: fq_gemm_grouped_workspace_bytes(...) bytes, zero-filled once (same
  * contract as fq_gemm's ws); FQ_ERR_WORKSPACE if too small while decode experts are present.
  * ------------------------------------------------------------------------------------------- */
 size_t fq_gemm_grouped_workspace_bytes(int64_t T, int32_t E, const fq_wdesc* d);

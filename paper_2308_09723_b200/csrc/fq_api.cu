@@ -134,8 +134,9 @@ fq_status fq_quantize(const void* W, int32_t wdt, const fq_wdesc* d, void* codes
   fq_status s = check_wdesc(d);
   if (s != FQ_OK) return s;
   if (!W || !codes || !scales || !valid_dtype(wdt)) return FQ_ERR_INVALID_ARG;
-  // one CTA per column holds the whole column in registers: K <= 65536 (16-bit W), 32768 (fp32 W)
-  if (d->K > (wdt == FQ_FP32 ? 32768 : 65536)) return FQ_ERR_SHAPE;
+  // one CTA holds a K-slice of whole groups in registers (slices of <= 12288 elements where the
+  // group allows, else one group): group <= 65536 (16-bit W), 32768 (fp32 W)
+  if (d->group > (wdt == FQ_FP32 ? 32768 : 65536)) return FQ_ERR_SHAPE;
   return from_cuda(run_quantize(wdt, d->scale_dtype, d->bits, W, (int)d->K, (int)d->N, d->group,
                                 codes, scales, status_dev, as_stream(stream)));
 }
@@ -154,10 +155,13 @@ fq_status fq_gemm(const void* A, int32_t adt, int64_t M, const fq_wdesc* d, cons
                   void* stream) {
   fq_status s = check_wdesc(d);
   if (s != FQ_OK) return s;
-  if (!A || !codes || !scales || !C || !valid_half(adt)) return FQ_ERR_INVALID_ARG;
+  if (!valid_half(adt)) return FQ_ERR_INVALID_ARG;
   if (d->scale_dtype != adt) return FQ_ERR_UNSUPPORTED;
   if (cdt != adt && cdt != FQ_FP32) return FQ_ERR_UNSUPPORTED;
-  if (M <= 0 || M > (1 << 20)) return FQ_ERR_SHAPE;
+  if (M < 0 || M > (1 << 20)) return FQ_ERR_SHAPE;
+  if (!codes || !scales) return FQ_ERR_INVALID_ARG;
+  if (M == 0) return FQ_OK;  // empty batch (A and C may be NULL): nothing to compute, nothing launched
+  if (!A || !C) return FQ_ERR_INVALID_ARG;
   if (use_tc_path(M, d->bits, d->group))
     return from_cuda(run_gemm_tc(adt, cdt, d->bits, A, (int)M, (int)d->K, (int)d->N, codes, scales,
                                  d->group, C, ws, ws_bytes, as_stream(stream)));
@@ -187,8 +191,9 @@ fq_status fq_gemm_grouped(const void* A, int32_t adt, int64_t T, const int64_t* 
                           int32_t E, const fq_wdesc* d, const int32_t* groups_host,
                           const void* const* codes_host, const void* const* scales_host, void* C,
                           int32_t cdt, void* ws, size_t ws_bytes, void* stream) {
-  if (!d || !offsets_host || !groups_host || !codes_host || !scales_host || !A || !C || E <= 0)
+  if (!d || !offsets_host || !groups_host || !codes_host || !scales_host || E <= 0)
     return FQ_ERR_INVALID_ARG;
+  if (T > 0 && (!A || !C)) return FQ_ERR_INVALID_ARG;  // T == 0: A and C may be NULL
   if (!valid_half(adt) || d->scale_dtype != adt || (cdt != adt && cdt != FQ_FP32)) return FQ_ERR_UNSUPPORTED;
   if (offsets_host[0] != 0 || offsets_host[E] != T || T < 0) return FQ_ERR_SHAPE;
   std::vector<int> small;

@@ -611,7 +611,9 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
               sgs = scg[rt][w];
               shs = sch[rt][w];
             } else {
-              const int kw = k0 + t * SEG + w * (SEG / 4);
+              // past the end of K (the last, partial stage) the codes and activations are TMA zero
+              // fill: clamp to the last group so the scale read stays in bounds (and finite)
+              const int kw = min(k0 + t * SEG + w * (SEG / 4), p.K - 1);
               const size_t j = (size_t)(kw / p.group) * N;
               sgs = splat_scale<T>(S, j + ng[rt]);
               shs = splat_scale<T>(S, j + nh[rt]);

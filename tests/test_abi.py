@@ -70,6 +70,35 @@ def test_validation_is_synchronous_and_launch_free(fq):
     assert fq._lib.fq_adapt_flags(dummy, 0, 256, 8, 0, 16, dummy, None, None) == fq.FQ_ERR_INVALID_ARG
     assert fq._lib.fq_adapt_flags(dummy, 0, 256, 8, 1001, 16, dummy, None, None) == fq.FQ_ERR_INVALID_ARG
     assert fq.fq_status_str(fq.FQ_ERR_SHAPE) == "FQ_ERR_SHAPE"
+    # long columns are quantized in K-slices: only a group longer than one CTA can hold is refused
+    per_col = fq.make_wdesc(131072, 256, 4, 131072, fq.FQ_BF16)
+    assert fq._lib.fq_quantize(dummy, 0, ctypes.byref(per_col), dummy, dummy, None, None) == fq.FQ_ERR_SHAPE
+    g32k = fq.make_wdesc(65536, 256, 4, 65536, fq.FQ_BF16)
+    assert fq._lib.fq_quantize(dummy, fq.FQ_FP32, ctypes.byref(g32k), dummy, dummy, None, None) == fq.FQ_ERR_SHAPE
+
+
+def test_empty_batches_are_launch_free_noops(fq):
+    """M == 0 (fq_gemm) and T == 0 / empty experts (fq_gemm_grouped) validate their arguments and
+    return FQ_OK without touching the device (dummy pointers, no GPU needed)."""
+    dummy = ctypes.c_void_p(16)
+    d = fq.make_wdesc(4096, 16384, 4, 128, fq.FQ_BF16)
+    assert fq._lib.fq_gemm(dummy, fq.FQ_BF16, 0, ctypes.byref(d), dummy, dummy, dummy, fq.FQ_BF16,
+                           None, 0, None) == fq.FQ_OK
+    assert fq._lib.fq_gemm(None, fq.FQ_BF16, 0, ctypes.byref(d), dummy, dummy, None, fq.FQ_BF16,
+                           None, 0, None) == fq.FQ_OK  # zero-size A / C buffers may be NULL
+    assert fq._lib.fq_gemm(dummy, fq.FQ_BF16, -1, ctypes.byref(d), dummy, dummy, dummy, fq.FQ_BF16,
+                           None, 0, None) == fq.FQ_ERR_SHAPE
+    bad = fq.make_wdesc(4096, 16384, 4, 96, fq.FQ_BF16)  # the empty batch still validates the descriptor
+    assert fq._lib.fq_gemm(dummy, fq.FQ_BF16, 0, ctypes.byref(bad), dummy, dummy, dummy, fq.FQ_BF16,
+                           None, 0, None) == fq.FQ_ERR_SHAPE
+    E = 4
+    offs = (ctypes.c_int64 * (E + 1))(*([0] * (E + 1)))
+    groups = (ctypes.c_int32 * E)(*([128] * E))
+    ptrs = (ctypes.c_void_p * E)(*([16] * E))
+    assert fq._lib.fq_gemm_grouped(dummy, fq.FQ_BF16, 0, offs, E, ctypes.byref(d), groups, ptrs, ptrs, dummy,
+                                   fq.FQ_BF16, None, 0, None) == fq.FQ_OK
+    assert fq._lib.fq_gemm_grouped(None, fq.FQ_BF16, 0, offs, E, ctypes.byref(d), groups, ptrs, ptrs, None,
+                                   fq.FQ_BF16, None, 0, None) == fq.FQ_OK
 
 
 def test_gemm_workspace_sizes(fq):

@@ -83,6 +83,39 @@ def test_group_sizes_multi_tile_ragged(fq, bits, group):
     assert O.rel_err(torch_to_f64(C), Cr, D) <= TOL
 
 
+@pytest.mark.parametrize("M,K,N,bits,group", [
+    (1, 1088, 264, 4, 64),     # K = 4.25 decode stages (group-split path), ragged N
+    (9, 1088, 264, 8, 64),     # int8, two token tiles
+    (3, 800, 520, 4, 32),      # per-element-scale path, K tail of 32
+    (16, 800, 296, 8, 16),
+    (5, 352, 256, 8, 32),      # int8 per-element path (128-k stages), K tail of 96
+    (1, 96, 256, 4, 96),       # K shorter than one stage, one group per column
+    (24, 1152, 392, 4, 128),   # four token tiles (nibble path), K = 4.5 stages
+    (40, 1088, 264, 4, 64),    # tcgen05 path, K = 17 blocks of 64
+    (200, 800, 136, 8, 32),    # tcgen05 path, K = 12.5 blocks
+])
+def test_ragged_k_tails(fq, M, K, N, bits, group):
+    """K not a multiple of the decode stage (256 / 128 k) or of the A6 K block (64): the partial
+    last stage / block must contribute exactly its own k range."""
+    Wb, Ab = make_case(M, K, N, bits, group, seed=K + M, outliers=1)
+    _, C = run_case(fq, Wb, Ab, bits, group)
+    Cr, D = oracle_ref(Wb, Ab, bits, group, "bf16")
+    assert O.rel_err(torch_to_f64(C), Cr, D) <= TOL
+
+
+def test_empty_batches(fq):
+    """M == 0 through fq.gemm and T == 0 / all-empty experts through fq.gemm_grouped: empty
+    outputs, FQ_OK, nothing launched (the C-ABI accepts the NULL pointers of zero-size tensors)."""
+    W = bits_to_torch(gaussian_bits((256, 512), 0.02, 9, "bf16"), "bf16")
+    qw = fq.quantize(W, 4, 128)
+    A = torch.empty((0, 512), dtype=torch.bfloat16, device="cuda")
+    C = fq.gemm(A, qw)
+    assert C.shape == (0, 256)
+    Cg = fq.gemm_grouped(A, [0, 0, 0], [qw, qw])
+    assert Cg.shape == (0, 256)
+    torch.cuda.synchronize()
+
+
 @pytest.mark.parametrize("adt", ["bf16", "fp16"])
 @pytest.mark.parametrize("bits", [4, 8])
 @pytest.mark.parametrize("cdt", [None, "fp32"])
