@@ -34,7 +34,9 @@ namespace tc {
 constexpr int BM = 128;        // weight rows per tile (UMMA M)
 constexpr int BN = 256;        // max tokens per tile (UMMA N); a problem with M < 256 uses
                                // bn = round_up(M, 16) (TcProb::bn): no wasted MMA / activation TMA
-constexpr int BK = 64;         // K per stage (one SWIZZLE_128B atom of bf16)
+constexpr int BKA = 64;        // K per activation TMA box (one SWIZZLE_128B atom of bf16)
+// K per stage (template BK): 64, or 128 for the 64/128-token variants -- two activation boxes, and
+// 64-byte (int4) / 128-byte (int8) code rows, which TMA streams far better than 32-byte rows
 // Dequant warps per CTA: dq_warps(BNMAX) / 4 per TMEM lane quarter, each covering BK / parts k of a
 // K block.  Measured: 16 warps are faster for the small-tile variants (memory/latency-bound
 // regime), 8 for the 256-token variant (tensor-bound prefill).
@@ -48,23 +50,26 @@ __host__ __device__ constexpr int dq_warps(int bnmax) { return FQ_TC_DQW ? FQ_TC
 __host__ __device__ constexpr int tc_threads(int bnmax) { return 32 * (2 + dq_warps(bnmax)); }
 constexpr int kTmemCols = 512;
 constexpr int kAccCol = 0;                 // accumulator columns [0, BNMAX)
-constexpr int kScRows = 5;                 // scale rows staged per K block (>= ceil(63/g) + 1, g >= 16)
+__host__ __device__ constexpr int sc_rows_max(int bk) { return bk / 16 + 1; }  // >= ceil((bk-1)/g) + 1, g >= 16
 constexpr int kSmemMax = 227 * 1024 - 2048;
 
 // Stage geometry of one kernel variant.  BNMAX = widest token tile it serves: a small-M variant
 // has small activation tiles, so it keeps many more K blocks (codes) in flight -- at M <= 128 the
 // kernel is bound by HBM latency x bytes in flight, not by the tensor cores.
 //   TMEM: accumulator columns [0, BNMAX), A slot s at BNMAX + 32 s (one per stage).
-template <int BITS, int BNMAX>
+template <int BITS, int BNMAX, int BK>
 struct Geo {
-  static constexpr int ACT_BYTES = BNMAX * BK * 2;            // 32 / 16 / 8 KB
-  static constexpr int CODE_BYTES_ROW = BK * BITS / 8;        // 32 (int4) / 64 (int8)
-  static constexpr int CODE_BYTES = BM * CODE_BYTES_ROW;      // 4 KB / 8 KB
+  static constexpr int ACT_BOX = BNMAX * BKA * 2;             // one activation box slot (SW128 atoms)
+  static constexpr int ACT_BYTES = ACT_BOX * (BK / BKA);
+  static constexpr int CODE_BYTES_ROW = BK * BITS / 8;        // 32 / 64 / 128 bytes
+  static constexpr int CODE_BYTES = BM * CODE_BYTES_ROW;
   static constexpr int SC_OFS = ACT_BYTES + CODE_BYTES;       // scale rows of the K block
-  static constexpr int SC_BYTES = kScRows * BM * 2;
+  static constexpr int SC_ROWS = sc_rows_max(BK);
+  static constexpr int SC_BYTES = SC_ROWS * BM * 2;
   static constexpr int STAGE = ((SC_OFS + SC_BYTES + 1023) / 1024) * 1024;
   static constexpr int S_SMEM = (kSmemMax - 1024) / STAGE;
-  static constexpr int S_TMEM = (kTmemCols - BNMAX) / 32;
+  static constexpr int A_COLS = BK / 2;                       // TMEM columns of one stage's A slot
+  static constexpr int S_TMEM = (kTmemCols - BNMAX) / A_COLS;
   static constexpr int S0 = S_SMEM < S_TMEM ? S_SMEM : S_TMEM;
   static constexpr int STAGES = S0 > 16 ? 16 : S0;
   static constexpr int SMEM = STAGES * STAGE + 1024;
@@ -125,8 +130,8 @@ __device__ __forceinline__ void tile_coords(int tile, int m_tiles, int n_tiles, 
 // consecutively across problems and the persistent CTAs walk the global tile list).
 struct TcProb {
   CUtensorMap a, q;  // activations [M][K] (box 256 x 64, SWIZZLE_128B); codes [N][K*b/8]
-  CUtensorMap s;     // scales [G][N] (box 5 rows x 128 columns, OOB rows zero)
-  int sc_rows;       // scale rows actually needed per K block (ceil(63/g) + 1, <= kScRows)
+  CUtensorMap s;     // scales [G][N] (box sc_rows_max(BK) rows x 128 columns, OOB rows zero)
+  int bk;            // K per stage of the kernel variant this problem was prepared for
   const void* scales;
   void* C;
   int M, K, N, group, cdt;
@@ -140,6 +145,7 @@ struct TcProb {
 };
 // work item -> (token tile, weight-row tile, K-block range); work items of one output tile are
 // consecutive (its K splits run concurrently on neighbouring CTAs)
+template <int BK>
 __device__ __forceinline__ void work_coords(const TcProb& p, int item, int& mt, int& nt, int& t, int& ks,
                                             int& kb0, int& kb1) {
   const int local = item - p.tile_begin;
@@ -163,12 +169,18 @@ __device__ __forceinline__ const TcProb& find_prob(const TcBatch<MAXP>& b, int t
   return b.p[pi];
 }
 
-template <typename T, int BITS, int MAXP, int BNMAX>
+// 16-byte chunk c of code row r in shared memory under the TMA swizzle of ROWB-byte rows
+template <int ROWB>
+__device__ __forceinline__ int swz_chunk(int c, int r) {
+  return ROWB == 32 ? c ^ ((r >> 2) & 1) : ROWB == 64 ? c ^ ((r >> 1) & 3) : c ^ (r & 7);
+}
+
+template <typename T, int BITS, int MAXP, int BNMAX, int BK>
 __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __grid_constant__ TcBatch<MAXP> batch) {
   constexpr int kDqWarps = dq_warps(BNMAX);
   constexpr int kParts = kDqWarps / 4;
-  constexpr int kKPW = BK / kParts;  // k per dequant thread per K block (32 or 16)
-  using Gm = Geo<BITS, BNMAX>;
+  constexpr int kKPW = BK / kParts;  // k per dequant thread per K block (16 / 32 / 64)
+  using Gm = Geo<BITS, BNMAX, BK>;
   constexpr int STAGES = Gm::STAGES;
   constexpr int kACol = Gm::A_COL;
   extern __shared__ __align__(1024) uint8_t dsmem[];
@@ -213,10 +225,10 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const TcProb& p = find_prob(batch, tile);
         int mt, nt, tt, ks, kb0, kb1;
-        work_coords(p, tile, mt, nt, tt, ks, kb0, kb1);
-        // first scale row of the K block = floor(64 kb / g), division-free after the first block
+        work_coords<BK>(p, tile, mt, nt, tt, ks, kb0, kb1);
+        // first scale row of the K block = floor(BK kb / g), division-free after the first block
         const int grp = p.group;  // hoisted out of the parameter space
-        const uint32_t tx = p.bn * BK * 2 + Gm::CODE_BYTES + kScRows * BM * 2;
+        const uint32_t tx = p.bn * BK * 2 + Gm::CODE_BYTES + Gm::SC_BYTES;
         const int arow = mt * p.bn, wrow = nt * BM;
         int j0 = (kb0 * BK) / grp, r0 = (kb0 * BK) - j0 * grp;
         for (int kb = kb0; kb < kb1; ++kb, r0 += BK) {
@@ -225,7 +237,9 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
           uint8_t* st = sbase + s * Gm::STAGE;
           mbar_arrive_expect_tx(&full_bar[s], tx);
           tma_load_2d(st + Gm::SC_OFS, &p.s, &full_bar[s], wrow, j0, pol_q);
-          tma_load_2d(st, &p.a, &full_bar[s], kb * BK, arow, pol_a);
+#pragma unroll
+          for (int h = 0; h < BK / BKA; ++h)
+            tma_load_2d(st + h * Gm::ACT_BOX, &p.a, &full_bar[s], kb * BK + h * BKA, arow, pol_a);
           tma_load_2d(st + Gm::ACT_BYTES, &p.q, &full_bar[s], kb * Gm::CODE_BYTES_ROW, wrow, pol_q);
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
@@ -240,7 +254,7 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const TcProb& pp = find_prob(batch, tile);
         int mt_, nt_, tt_, ks_, kb0, kb1;
-        work_coords(pp, tile, mt_, nt_, tt_, ks_, kb0, kb1);
+        work_coords<BK>(pp, tile, mt_, nt_, tt_, ks_, kb0, kb1);
         const uint32_t idesc = idesc_f16<T, BM, 16>() + ((uint32_t)((pp.bn >> 3) - 2) << 17);  // N = bn
         mbar_wait(&acc_empty, acc_ph ^ 1);  // epilogue drained the accumulator
         fence_after();
@@ -248,11 +262,13 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
           mbar_wait(&full_bar[s], ph);
           mbar_wait(&afull_bar[s], ph);
           fence_after();
-          const uint64_t bdesc = sw128_desc(sb + s * Gm::STAGE);
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk)
-            if (!(FQ_TC_DBG & 1)) mma_ts(tmem + kAccCol, tmem + kACol + s * 32 + kk * 8, bdesc + (uint64_t)(kk * 2), idesc,
-                   (kb != kb0) || (kk != 0));
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t bdesc = sw128_desc(sb + s * Gm::STAGE + (kk / 4) * Gm::ACT_BOX);
+            if (!(FQ_TC_DBG & 1))
+              mma_ts(tmem + kAccCol, tmem + kACol + s * Gm::A_COLS + kk * 8, bdesc + (uint64_t)((kk % 4) * 2), idesc,
+                     (kb != kb0) || (kk != 0));
+          }
           mma_commit(&empty_bar[s]);
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
@@ -274,13 +290,13 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
       const TcProb& p = find_prob(batch, tile);
       const int N = p.N, M = p.M;
       int mt, nt, tt, ks, kb0, kb1;
-      work_coords(p, tile, mt, nt, tt, ks, kb0, kb1);
+      work_coords<BK>(p, tile, mt, nt, tt, ks, kb0, kb1);
       const int n = nt * BM + row;
       const int nc = min(n, N - 1);
       const int grp = p.group;                     // hoisted: p lives in the parameter space
       const bool one_scale = grp % kKPW == 0;      // this thread's kKPW k lie in one group
       int j0 = (kb0 * BK) / grp, r0 = kb0 * BK - j0 * grp;  // first staged scale row
-      // group of this thread's first k (kb0*64 + half*kKPW) and its offset in the group
+      // group of this thread's first k (kb0*BK + half*kKPW) and its offset in the group
       int jb = (kb0 * BK + half * kKPW) / grp, gk = kb0 * BK + half * kKPW - jb * grp;
       const uint32_t srow = sb + Gm::SC_OFS + row * 2;
       for (int kb = kb0; kb < kb1; ++kb) {
@@ -297,8 +313,10 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
         } else {
 #pragma unroll
           for (int w = 0; w < NW; ++w) {
-            const int o = gk + 8 * w;
-            const int jr = jb - j0 + (o >= grp) + (o >= 2 * grp);
+            const int o = gk + 8 * w;  // < grp + kKPW: at most kKPW / 16 group boundaries
+            int jr = jb - j0;
+#pragma unroll
+            for (int m = 1; m <= kKPW / 16; ++m) jr += (o >= m * grp);
             const uint32_t v = lds_u16(srow + s * Gm::STAGE + jr * BM * 2);
             sc[w] = prmt(v, v, 0x1010u);
           }
@@ -307,13 +325,17 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
         uint32_t out[kKPW / 2];
         if (FQ_TC_DBG & 2) {
         } else if (BITS == 4) {
-          // kKPW/2 bytes; SWIZZLE_32B: 16-byte chunk c of row r sits at c ^ ((r >> 2) & 1)
+          // kKPW/2 bytes of the swizzled code row
+          constexpr int ROWB = Gm::CODE_BYTES_ROW;
           uint32_t words[NW];
-          if constexpr (kKPW == 32) {
-            const uint4 c = lds128(qbase + ((half ^ ((row >> 2) & 1)) << 4));
-            words[0] = c.x; words[1] = c.y; words[2] = c.z; words[3] = c.w;
+          if constexpr (kKPW >= 32) {
+#pragma unroll
+            for (int i = 0; i < kKPW / 32; ++i) {
+              const uint4 c = lds128(qbase + (swz_chunk<ROWB>(half * (kKPW / 32) + i, row) << 4));
+              words[4 * i] = c.x; words[4 * i + 1] = c.y; words[4 * i + 2] = c.z; words[4 * i + 3] = c.w;
+            }
           } else {
-            const uint2 c = lds64(qbase + (((half >> 1) ^ ((row >> 2) & 1)) << 4) + (half & 1) * 8);
+            const uint2 c = lds64(qbase + (swz_chunk<ROWB>(half >> 1, row) << 4) + (half & 1) * 8);
             words[0] = c.x; words[1] = c.y;
           }
 #pragma unroll
@@ -324,11 +346,11 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
             for (int i = 0; i < 4; ++i) out[4 * w + i] = mul2x<T>(q[i], sc[w]);
           }
         } else {
-          // kKPW bytes; SWIZZLE_64B: chunk c of row r sits at c ^ ((r >> 1) & 3)
+          // kKPW bytes of the swizzled code row
 #pragma unroll
           for (int hh = 0; hh < kKPW / 16; ++hh) {
             const int cidx = half * (kKPW / 16) + hh;
-            const uint4 c = lds128(qbase + ((cidx ^ ((row >> 1) & 3)) << 4));
+            const uint4 c = lds128(qbase + (swz_chunk<Gm::CODE_BYTES_ROW>(cidx, row) << 4));
             const uint32_t words[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
             for (int w = 0; w < 4; ++w) {
@@ -341,10 +363,12 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
           }
         }
         if (FQ_TC_DBG & 2) {
-        } else if constexpr (kKPW == 32)
-          tmem_st16(tmem + lane_base + kACol + s * 32 + half * 16, *reinterpret_cast<const uint32_t(*)[16]>(out));
+        } else if constexpr (kKPW == 64)
+          tmem_st32(tmem + lane_base + kACol + s * Gm::A_COLS + half * 32, *reinterpret_cast<const uint32_t(*)[32]>(out));
+        else if constexpr (kKPW == 32)
+          tmem_st16(tmem + lane_base + kACol + s * Gm::A_COLS + half * 16, *reinterpret_cast<const uint32_t(*)[16]>(out));
         else
-          tmem_st8(tmem + lane_base + kACol + s * 32 + half * 8, *reinterpret_cast<const uint32_t(*)[8]>(out));
+          tmem_st8(tmem + lane_base + kACol + s * Gm::A_COLS + half * 8, *reinterpret_cast<const uint32_t(*)[8]>(out));
         tmem_wait_st();
         fence_before();
         __syncwarp();
@@ -441,21 +465,34 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
 }  // namespace tc
 
 // ------------------------------------------------------------------------------------- host side
-static bool make_tc_prob(tc::TcProb& d, int bits, const void* A, int M, int K, int N, const void* codes,
-                         const void* scales, int group, void* C, int cdt) {
+// K per stage of the kernel variant serving a launch whose widest token tile is bnmax tokens:
+// 128 for the 64/128-token variants (64-byte int4 code rows), 64 for the 256-token variant (its
+// activation tiles leave no room for 128-k stages).  FQ_TC_BK=64 forces the narrow stages.
+static int tc_bk(int bnmax) {
+  static const int forced = std::getenv("FQ_TC_BK") ? std::atoi(std::getenv("FQ_TC_BK")) : 0;
+  if (bnmax > 128 || std::getenv("FQ_TC_BNMAX256")) return 64;
+  return forced == 64 ? 64 : 128;
+}
+static int tc_bn(int M) {
 #ifdef FQ_TC_FULLBN
-  d.bn = tc::BN;  // diagnostics: always 256-token tiles
+  (void)M;
+  return tc::BN;  // diagnostics: always 256-token tiles
 #else
-  d.bn = std::min(tc::BN, (M + 15) / 16 * 16);
+  return std::min(tc::BN, (M + 15) / 16 * 16);
 #endif
-  if (!make_tmap_2d(&d.a, A, 2, (uint64_t)K, (uint64_t)M, (uint64_t)K * 2, tc::BK, d.bn, 128)) return false;
+}
+
+static bool make_tc_prob(tc::TcProb& d, int bits, const void* A, int M, int K, int N, const void* codes,
+                         const void* scales, int group, void* C, int cdt, int bk) {
+  d.bn = tc_bn(M);
+  d.bk = bk;
+  if (!make_tmap_2d(&d.a, A, 2, (uint64_t)K, (uint64_t)M, (uint64_t)K * 2, tc::BKA, d.bn, 128)) return false;
   const uint64_t row_bytes = (uint64_t)K * bits / 8;
-  if (!make_tmap_2d(&d.q, codes, 1, row_bytes, (uint64_t)N, row_bytes, tc::BK * bits / 8, tc::BM,
-                    bits == 4 ? 32 : 64))
+  const int code_row = bk * bits / 8;  // box row bytes = swizzle span (32 / 64 / 128)
+  if (!make_tmap_2d(&d.q, codes, 1, row_bytes, (uint64_t)N, row_bytes, code_row, tc::BM, code_row)) return false;
+  if (!make_tmap_2d(&d.s, scales, 2, (uint64_t)N, (uint64_t)(K / group), (uint64_t)N * 2, tc::BM,
+                    tc::sc_rows_max(bk), 0))
     return false;
-  if (!make_tmap_2d(&d.s, scales, 2, (uint64_t)N, (uint64_t)(K / group), (uint64_t)N * 2, tc::BM, tc::kScRows, 0))
-    return false;
-  d.sc_rows = (63 + group - 1) / group + 1;
   d.scales = scales;
   d.C = C;
   d.M = M; d.K = K; d.N = N; d.group = group; d.cdt = cdt;
@@ -464,38 +501,40 @@ static bool make_tc_prob(tc::TcProb& d, int bits, const void* A, int M, int K, i
   const char* gme = std::getenv("FQ_TC_GM");
   d.gm = gme ? std::max(1, std::atoi(gme)) : 8;
   d.splits = 1;
-  d.kbs = (K + tc::BK - 1) / tc::BK;
+  d.kbs = (K + bk - 1) / bk;
   d.ws = nullptr;
   d.ctr = nullptr;
   return true;
 }
 
 // Split-K plan of one GEMM: when its output tiles cannot fill the SMs (e.g. M <= 256 on a weight
-// matrix of < 148 x 128 rows), K is cut into ranges of >= 8 K blocks so ~one work item per SM runs.
+// matrix of < 148 x 128 rows), K is cut into ranges of >= 512 k so ~one work item per SM runs.
 constexpr size_t kTcCounterBytes = 65536;
-static int tc_splits(int M, int K, int N) {
-  const int bn = std::min(tc::BN, (M + 15) / 16 * 16);
+static int tc_splits(int M, int K, int N, int* kbs_out = nullptr) {
+  const int bn = tc_bn(M);
+  const int bk = tc_bk(bn);
   const int tiles = ((M + bn - 1) / bn) * ((N + tc::BM - 1) / tc::BM);
-  const int kblocks = (K + tc::BK - 1) / tc::BK;
+  const int kblocks = (K + bk - 1) / bk;
   const char* e = std::getenv("FQ_TC_SPLITS");
   int s = e ? std::atoi(e) : num_sms() / std::max(1, tiles);
-  s = std::max(1, std::min(s, kblocks / 8));
+  s = std::max(1, std::min(s, kblocks / (512 / bk)));
   if (tiles > (int)(kTcCounterBytes / sizeof(int))) s = 1;
   const int kbs = (kblocks + s - 1) / s;
+  if (kbs_out) *kbs_out = kbs;
   return (kblocks + kbs - 1) / kbs;
 }
 size_t gemm_tc_workspace_bytes(int M, int K, int N) {
   const int s = tc_splits(M, K, N);
   if (s == 1) return 256;
-  const int bn = std::min(tc::BN, (M + 15) / 16 * 16);
+  const int bn = tc_bn(M);
   const size_t tiles = (size_t)((M + bn - 1) / bn) * ((N + tc::BM - 1) / tc::BM);
   return kTcCounterBytes + tiles * s * bn * tc::BM * sizeof(float);
 }
 
-template <typename T, int BITS, int MAXP, int BNMAX>
+template <typename T, int BITS, int MAXP, int BNMAX, int BK>
 static cudaError_t launch_tc(const tc::TcBatch<MAXP>& b, cudaStream_t st) {
-  using Gm = tc::Geo<BITS, BNMAX>;
-  auto kern = tc::gemm_tc_kernel<T, BITS, MAXP, BNMAX>;
+  using Gm = tc::Geo<BITS, BNMAX, BK>;
+  auto kern = tc::gemm_tc_kernel<T, BITS, MAXP, BNMAX, BK>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Gm::SMEM);
@@ -507,32 +546,38 @@ static cudaError_t launch_tc(const tc::TcBatch<MAXP>& b, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-template <int MAXP, int BNMAX>
+template <int MAXP, int BNMAX, int BK>
 static cudaError_t dispatch_tc_bn(int adt, int bits, const tc::TcBatch<MAXP>& b, cudaStream_t st) {
   if (adt == FQ_BF16)
-    return bits == 4 ? launch_tc<__nv_bfloat16, 4, MAXP, BNMAX>(b, st) : launch_tc<__nv_bfloat16, 8, MAXP, BNMAX>(b, st);
-  return bits == 4 ? launch_tc<__half, 4, MAXP, BNMAX>(b, st) : launch_tc<__half, 8, MAXP, BNMAX>(b, st);
+    return bits == 4 ? launch_tc<__nv_bfloat16, 4, MAXP, BNMAX, BK>(b, st)
+                     : launch_tc<__nv_bfloat16, 8, MAXP, BNMAX, BK>(b, st);
+  return bits == 4 ? launch_tc<__half, 4, MAXP, BNMAX, BK>(b, st) : launch_tc<__half, 8, MAXP, BNMAX, BK>(b, st);
 }
-// kernel variant = the widest token tile of the launch (64 / 128 / 256 tokens)
+// kernel variant = the widest token tile of the launch (64 / 128 / 256 tokens) and the stage K its
+// problems were prepared for
 template <int MAXP>
 static cudaError_t dispatch_tc(int adt, int bits, const tc::TcBatch<MAXP>& b, cudaStream_t st) {
   int bn = 0;
   for (int i = 0; i < b.nprob; ++i) bn = std::max(bn, b.p[i].bn);
   if (std::getenv("FQ_TC_BNMAX256")) bn = 256;  // diagnostics: the large-M variant for every M
-  if (bn <= 64) return dispatch_tc_bn<MAXP, 64>(adt, bits, b, st);
-  if (bn <= 128) return dispatch_tc_bn<MAXP, 128>(adt, bits, b, st);
-  return dispatch_tc_bn<MAXP, 256>(adt, bits, b, st);
+  const int bk = b.p[0].bk;
+  for (int i = 1; i < b.nprob; ++i)
+    if (b.p[i].bk != bk) return cudaErrorInvalidValue;
+  if (bn > 128) return bk == 64 ? dispatch_tc_bn<MAXP, 256, 64>(adt, bits, b, st) : cudaErrorInvalidValue;
+  if (bn <= 64)
+    return bk == 128 ? dispatch_tc_bn<MAXP, 64, 128>(adt, bits, b, st) : dispatch_tc_bn<MAXP, 64, 64>(adt, bits, b, st);
+  return bk == 128 ? dispatch_tc_bn<MAXP, 128, 128>(adt, bits, b, st) : dispatch_tc_bn<MAXP, 128, 64>(adt, bits, b, st);
 }
 
 cudaError_t run_gemm_tc(int adt, int cdt, int bits, const void* A, int M, int K, int N, const void* codes,
                         const void* scales, int group, void* C, void* ws, size_t ws_bytes, cudaStream_t st) {
   tc::TcBatch<1> b{};
   tc::TcProb& d = b.p[0];
-  if (!make_tc_prob(d, bits, A, M, K, N, codes, scales, group, C, cdt)) return cudaErrorInvalidValue;
-  const int s = tc_splits(M, K, N);
+  if (!make_tc_prob(d, bits, A, M, K, N, codes, scales, group, C, cdt, tc_bk(tc_bn(M)))) return cudaErrorInvalidValue;
+  int kbs = 0;
+  const int s = tc_splits(M, K, N, &kbs);
   if (s > 1 && ws && ws_bytes >= gemm_tc_workspace_bytes(M, K, N)) {
-    const int kblocks = (K + tc::BK - 1) / tc::BK;
-    d.kbs = (kblocks + s - 1) / s;
+    d.kbs = kbs;
     d.splits = s;
     d.ctr = reinterpret_cast<int*>(ws);
     d.ws = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + kTcCounterBytes);
@@ -550,13 +595,17 @@ cudaError_t run_gemm_tc_grouped(int adt, int cdt, int bits, const void* A, int K
   constexpr int MAXP = 48;
   static_assert(sizeof(tc::TcBatch<MAXP>) < 32000, "kernel parameter block limit");
   tc::TcBatch<MAXP> b{};
+  int bnmax = 0;  // one stage K for every launch of the call (all chunks fit its variant)
+  for (int ii = 0; ii < nexp; ++ii)
+    bnmax = std::max(bnmax, tc_bn((int)(offsets[experts[ii] + 1] - offsets[experts[ii]])));
+  const int bk = tc_bk(bnmax);
   for (int ii = 0; ii < nexp; ++ii) {
     const int e = experts[ii];
     const int Me = (int)(offsets[e + 1] - offsets[e]);
     const char* Ae = reinterpret_cast<const char*>(A) + (size_t)offsets[e] * K * 2;
     char* Ce = reinterpret_cast<char*>(C) + (size_t)offsets[e] * N * (cdt == FQ_FP32 ? 4 : 2);
     tc::TcProb& d = b.p[b.nprob];
-    if (!make_tc_prob(d, bits, Ae, Me, K, N, codes[e], scales[e], groups[e], Ce, cdt)) return cudaErrorInvalidValue;
+    if (!make_tc_prob(d, bits, Ae, Me, K, N, codes[e], scales[e], groups[e], Ce, cdt, bk)) return cudaErrorInvalidValue;
     d.tile_begin = b.total_tiles;
     b.total_tiles += d.m_tiles * d.n_tiles;
     if (++b.nprob == MAXP) {
