@@ -17,12 +17,15 @@ def bench(fn, reps=5):
     return s.elapsed_time(e) / reps / 1e3
 
 
-tag = f"BK={os.environ.get('FQ_TC_BK', 'default')}"
-for name, K, N in (("OPT13B-FFN1", 5120, 20480), ("OPT175B-FC1", 12288, 49152), ("OPT175B-FC2", 49152, 12288)):
+QUICK = "quick" in sys.argv  # OPT-175B FC1 at M = 64 / 128 and the MoE batch only
+tag = f"BK={os.environ.get('FQ_TC_BK', 'default')} lib={os.path.basename(os.environ.get('FQ_LIB_PATH', 'libfq.so'))}"
+SHAPES = (("OPT175B-FC1", 12288, 49152),) if QUICK else (("OPT13B-FFN1", 5120, 20480), ("OPT175B-FC1", 12288, 49152),
+                                                          ("OPT175B-FC2", 49152, 12288))
+for name, K, N in SHAPES:
     W = gaussian_torch((N, K), 0.02, 1)
     for bits in (4, 8):
         q = fq.quantize(W, bits, 128)
-        for M in (48, 64, 128, 256, 2048):
+        for M in ((64, 128) if QUICK else (48, 64, 128, 256, 2048)):
             A = gaussian_torch((M, K), 1.0, 2)
             C = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
             t = bench(lambda: fq.gemm(A, q, out=C))
@@ -38,7 +41,7 @@ for e in range(E):
         W[e % N, (37 * e) % K] = 1.0
     experts.append(fq.quantize(W, 4, None)); del W
 wb = sum(q.nbytes for q in experts)
-for me in (32, 64, 128, 256):
+for me in ((64, 128) if QUICK else (32, 64, 128, 256)):
     off = [e * me for e in range(E + 1)]
     A = gaussian_torch((E * me, K), 1.0, 3)
     t = bench(lambda: fq.gemm_grouped(A, off, experts))
