@@ -8,17 +8,22 @@
 // conversion off the tensor core's critical path by warp specialisation and by writing the
 // dequantized weights straight into tensor memory (no shared-memory round trip):
 //
-//   tile = 128 weight rows (output columns n) x 256 tokens, K block = 64, persistent CTAs.
-//   warp 0      TMA producer: activations [256 tokens x 64 k] (SWIZZLE_128B, the UMMA K-major
-//               canonical layout) + packed codes [128 rows x 64 k] (SWIZZLE_32B) per stage.
+//   tile = 128 weight rows (output columns n) x bn tokens (bn = round_up(M, 16) <= 256), persistent
+//   CTAs.  Kernel variant by the launch's widest token tile: 256 tokens with 64-k stages and 8
+//   dequant warps; 128 / 64 tokens with 128-k stages (two activation boxes, 64 / 128-byte code
+//   rows) and 16 dequant warps.
+//   warp 0      TMA producer: activations [bn tokens x 64 k] per box (SWIZZLE_128B, the UMMA K-major
+//               canonical layout) + packed codes [128 rows x BK k] (SWIZZLE_32B/64B/128B by row
+//               bytes) + the K block's scale rows, one mbarrier ring.
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer:
-//                 D[n, tok] (fp32, TMEM, 256 columns) += A[n, k] (bf16, TMEM) * B[k, tok] (smem)
-//               "kind::f16", M=128, N=256, K=16; tcgen05.commit releases the stage.
-//   warps 2..9  dequant: thread = one weight row (its TMEM lane) x 32 k; codes -> exact bf16 codes
-//               (PRMT/IMAD/LOP3 magic-number unpack, natural (k,k+1) pairs) -> * scale ->
-//               tcgen05.st into the stage's A slot.  After the last K block of a tile the same
-//               warps drain the accumulator (tcgen05.ld) and store C.
-//   TMEM: 256 accumulator columns + 4 stages x 32 columns of A.
+//                 D[n, tok] (fp32, TMEM, bn columns) += A[n, k] (bf16, TMEM) * B[k, tok] (smem)
+//               "kind::f16", M=128, N=bn, K=16; tcgen05.commit releases the stage.
+//   warps 2..   dequant: thread = one weight row (its TMEM lane) x BK / (warps / 4) k; codes ->
+//               exact bf16 codes (PRMT/IMAD/LOP3 magic-number unpack, natural (k,k+1) pairs) ->
+//               * scale -> tcgen05.st into the stage's A slot.  After the last K block of a work
+//               item the same warps drain the accumulator (tcgen05.ld) and store C, or an fp32
+//               split-K partial that the last-arriving split reduces in split order.
+//   TMEM: accumulator columns [0, BNMAX) + one A slot of BK/2 columns per stage.
 #include <cuda.h>
 
 #include <algorithm>
