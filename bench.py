@@ -264,27 +264,32 @@ def main():
             dist.barrier()
         # per-launch durations: each launch of the step repeated R times back to back between one
         # pair of CUDA events on the launching stream (steady state, PDL overlap included)
+        # Three rounds; each launch's figure is the median of its three round averages, so one
+        # transient (a power-cap clock dip, a neighbour's interference) cannot skew the roofline.
         names = [f"FC1_M{M}" for M in M_SWEEP] + [f"FC2_M{M}" for M in M_SWEEP]
-        per = {n: 0.0 for n in names}
-        comm = 0.0
+        rounds = {n: [] for n in names}
+        comms = []
         reps = 20
-        evs = []
-        for M in M_SWEEP:
-            for n, fn in ((f"FC1_M{M}", gemm1), (f"FC2_M{M}", gemm2), (f"AR_M{M}", reduce)):
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-                for _ in range(reps):
-                    fn(M)
-                b.record(stream)
-                evs.append((n, a, b))
-        torch.cuda.synchronize()
-        for n, a, b in evs:
-            if n.startswith("AR"):
-                comm += a.elapsed_time(b)
-            else:
-                per[n] += a.elapsed_time(b)
-        per = {n: v / reps for n, v in per.items()}
-        comm /= reps
+        for _ in range(3):
+            evs = []
+            for M in M_SWEEP:
+                for n, fn in ((f"FC1_M{M}", gemm1), (f"FC2_M{M}", gemm2), (f"AR_M{M}", reduce)):
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(stream)
+                    for _ in range(reps):
+                        fn(M)
+                    b.record(stream)
+                    evs.append((n, a, b))
+            torch.cuda.synchronize()
+            c = 0.0
+            for n, a, b in evs:
+                if n.startswith("AR"):
+                    c += a.elapsed_time(b) / reps
+                else:
+                    rounds[n].append(a.elapsed_time(b) / reps)
+            comms.append(c)
+        per = {n: sorted(v)[1] for n, v in rounds.items()}
+        comm = sorted(comms)[1]
         if world > 1:
             dist.barrier()
     clocks = clk.summary()

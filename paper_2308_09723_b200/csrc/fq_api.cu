@@ -143,7 +143,7 @@ fq_status fq_quantize(const void* W, int32_t wdt, const fq_wdesc* d, void* codes
 
 size_t fq_gemm_workspace_bytes(int64_t M, const fq_wdesc* d) {
   if (check_wdesc(d) != FQ_OK || M <= 0) return 0;
-  if (use_tc_path(M, d->bits, d->group)) return gemm_tc_workspace_bytes((int)M, (int)d->K, (int)d->N);
+  if (use_tc_path(M, d->bits, d->group)) return gemm_tc_workspace_bytes((int)M, (int)d->K, (int)d->N, d->bits);
   if (decode_tc_supported(d->bits, d->group, (int)M))
     return dtc_workspace_bytes(M, (int)d->K, num_sms());
   const GemvPlan p = plan_gemv((int)M, (int)d->K, (int)d->N, d->bits, d->group, num_sms());

@@ -24,6 +24,11 @@
 //               item the same warps drain the accumulator (tcgen05.ld) and store C, or an fp32
 //               split-K partial that the last-arriving split reduces in split order.
 //   TMEM: accumulator columns [0, BNMAX) + one A slot of BK/2 columns per stage.
+//   Two-half tiles (HM = 2, the <= 64-token variant): 256 weight rows per tile as two UMMA M=128
+//   halves that share each staged activation tile, so a stage carries twice the code bytes for the
+//   same activation bytes (the small-M regime is bound by code bytes in flight per SM).  The
+//   halves' A operands then need 2 x BK/2 TMEM columns per K block, fewer slots than smem stages:
+//   the A slots form their own ring (released by the MMA commit) behind the smem stage ring.
 #include <cuda.h>
 
 #include <algorithm>
@@ -62,24 +67,31 @@ constexpr int kSmemMax = 227 * 1024 - 2048;
 // has small activation tiles, so it keeps many more K blocks (codes) in flight -- at M <= 128 the
 // kernel is bound by HBM latency x bytes in flight, not by the tensor cores.
 //   TMEM: accumulator columns [0, BNMAX), A slot s at BNMAX + 32 s (one per stage).
-template <int BITS, int BNMAX, int BK>
+template <int BITS, int BNMAX, int BK, int HM>
 struct Geo {
+  static constexpr int BMT = BM * HM;                         // weight rows per tile
   static constexpr int ACT_BOX = BNMAX * BKA * 2;             // one activation box slot (SW128 atoms)
   static constexpr int ACT_BYTES = ACT_BOX * (BK / BKA);
   static constexpr int CODE_BYTES_ROW = BK * BITS / 8;        // 32 / 64 / 128 bytes
-  static constexpr int CODE_BYTES = BM * CODE_BYTES_ROW;
+  static constexpr int CODE_HALF = BM * CODE_BYTES_ROW;       // codes of one 128-row half
+  static constexpr int CODE_BYTES = CODE_HALF * HM;
   static constexpr int SC_OFS = ACT_BYTES + CODE_BYTES;       // scale rows of the K block
   static constexpr int SC_ROWS = sc_rows_max(BK);
-  static constexpr int SC_BYTES = SC_ROWS * BM * 2;
+  static constexpr int SC_HALF = SC_ROWS * BM * 2;            // scale rows of one half
+  static constexpr int SC_BYTES = SC_HALF * HM;
   static constexpr int STAGE = ((SC_OFS + SC_BYTES + 1023) / 1024) * 1024;
   static constexpr int S_SMEM = (kSmemMax - 1024) / STAGE;
-  static constexpr int A_COLS = BK / 2;                       // TMEM columns of one stage's A slot
-  static constexpr int S_TMEM = (kTmemCols - BNMAX) / A_COLS;
-  static constexpr int S0 = S_SMEM < S_TMEM ? S_SMEM : S_TMEM;
+  static constexpr int A_HALF = BK / 2;                       // TMEM columns of one half's A operand
+  static constexpr int A_COLS = A_HALF * HM;                  // TMEM columns of one A slot
+  static constexpr int ACC_COLS = BNMAX * HM;                 // accumulator columns (half h at h*BNMAX)
+  static constexpr int S_TMEM = (kTmemCols - ACC_COLS) / A_COLS;
+  // HM = 1: one A slot per smem stage (slot index = stage index); HM = 2: a separate slot ring
+  static constexpr int S0 = (HM == 1 && S_TMEM < S_SMEM) ? S_TMEM : S_SMEM;
   static constexpr int STAGES = S0 > 16 ? 16 : S0;
+  static constexpr int ASLOTS = HM == 1 ? STAGES : (S_TMEM < STAGES ? S_TMEM : STAGES);
   static constexpr int SMEM = STAGES * STAGE + 1024;
-  static constexpr int A_COL = BNMAX;
-  static_assert(STAGES >= 4, "stages");
+  static constexpr int A_COL = ACC_COLS;
+  static_assert(STAGES >= (HM == 1 ? 4 : 3) && ASLOTS >= 2, "stages");
 };
 
 using namespace tc5;
@@ -137,6 +149,7 @@ struct TcProb {
   CUtensorMap a, q;  // activations [M][K] (box 256 x 64, SWIZZLE_128B); codes [N][K*b/8]
   CUtensorMap s;     // scales [G][N] (box sc_rows_max(BK) rows x 128 columns, OOB rows zero)
   int bk;            // K per stage of the kernel variant this problem was prepared for
+  int hm;            // 128-row halves per tile of that variant (tile = 128 * hm weight rows)
   const void* scales;
   void* C;
   int M, K, N, group, cdt;
@@ -180,16 +193,19 @@ __device__ __forceinline__ int swz_chunk(int c, int r) {
   return ROWB == 32 ? c ^ ((r >> 2) & 1) : ROWB == 64 ? c ^ ((r >> 1) & 3) : c ^ (r & 7);
 }
 
-template <typename T, int BITS, int MAXP, int BNMAX, int BK>
+template <typename T, int BITS, int MAXP, int BNMAX, int BK, int HM>
 __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __grid_constant__ TcBatch<MAXP> batch) {
   constexpr int kDqWarps = dq_warps(BNMAX);
   constexpr int kParts = kDqWarps / 4;
   constexpr int kKPW = BK / kParts;  // k per dequant thread per K block (16 / 32 / 64)
-  using Gm = Geo<BITS, BNMAX, BK>;
+  using Gm = Geo<BITS, BNMAX, BK, HM>;
   constexpr int STAGES = Gm::STAGES;
+  constexpr int ASLOTS = Gm::ASLOTS;
+  constexpr bool kSepA = HM > 1;     // A slots in their own ring (see Geo)
+  constexpr int BMT = Gm::BMT;
   constexpr int kACol = Gm::A_COL;
   extern __shared__ __align__(1024) uint8_t dsmem[];
-  __shared__ __align__(8) uint64_t full_bar[STAGES], afull_bar[STAGES], empty_bar[STAGES];
+  __shared__ __align__(8) uint64_t full_bar[STAGES], afull_bar[ASLOTS], empty_bar[STAGES], aempty_bar[ASLOTS];
   __shared__ __align__(8) uint64_t acc_full, acc_empty;
   __shared__ uint32_t tmem_base_sh;
   __shared__ int s_last;
@@ -200,8 +216,11 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&afull_bar[s], kDqWarps);  // one arrival per dequant warp
       mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < ASLOTS; ++a) {
+      mbar_init(&afull_bar[a], kDqWarps);  // one arrival per dequant warp
+      mbar_init(&aempty_bar[a], 1);        // MMA commit (separate slot ring only)
     }
     mbar_init(&acc_full, 1);
     mbar_init(&acc_empty, kDqWarps);
@@ -233,19 +252,24 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
         work_coords<BK>(p, tile, mt, nt, tt, ks, kb0, kb1);
         // first scale row of the K block = floor(BK kb / g), division-free after the first block
         const int grp = p.group;  // hoisted out of the parameter space
-        const uint32_t tx = p.bn * BK * 2 + Gm::CODE_BYTES + Gm::SC_BYTES;
-        const int arow = mt * p.bn, wrow = nt * BM;
+        // halves entirely past the last weight row are not loaded (their TMEM rows are never stored)
+        const int nh = HM == 1 ? 1 : min(HM, (p.N - nt * BMT + BM - 1) / BM);
+        const uint32_t tx = p.bn * BK * 2 + nh * (Gm::CODE_HALF + Gm::SC_HALF);
+        const int arow = mt * p.bn, wrow = nt * BMT;
         int j0 = (kb0 * BK) / grp, r0 = (kb0 * BK) - j0 * grp;
         for (int kb = kb0; kb < kb1; ++kb, r0 += BK) {
           while (r0 >= grp) { r0 -= grp; ++j0; }
           mbar_wait(&empty_bar[s], ph ^ 1);
           uint8_t* st = sbase + s * Gm::STAGE;
           mbar_arrive_expect_tx(&full_bar[s], tx);
-          tma_load_2d(st + Gm::SC_OFS, &p.s, &full_bar[s], wrow, j0, pol_q);
+          for (int hh = 0; hh < nh; ++hh)
+            tma_load_2d(st + Gm::SC_OFS + hh * Gm::SC_HALF, &p.s, &full_bar[s], wrow + hh * BM, j0, pol_q);
 #pragma unroll
           for (int h = 0; h < BK / BKA; ++h)
             tma_load_2d(st + h * Gm::ACT_BOX, &p.a, &full_bar[s], kb * BK + h * BKA, arow, pol_a);
-          tma_load_2d(st + Gm::ACT_BYTES, &p.q, &full_bar[s], kb * Gm::CODE_BYTES_ROW, wrow, pol_q);
+          for (int hh = 0; hh < nh; ++hh)
+            tma_load_2d(st + Gm::ACT_BYTES + hh * Gm::CODE_HALF, &p.q, &full_bar[s], kb * Gm::CODE_BYTES_ROW,
+                        wrow + hh * BM, pol_q);
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
       }
@@ -254,8 +278,8 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
     // ------------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       const uint32_t sb = smem_u32(sbase);
-      int s = 0;
-      uint32_t ph = 0, acc_ph = 0;
+      int s = 0, a = 0;
+      uint32_t ph = 0, aph = 0, acc_ph = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const TcProb& pp = find_prob(batch, tile);
         int mt_, nt_, tt_, ks_, kb0, kb1;
@@ -264,17 +288,24 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
         mbar_wait(&acc_empty, acc_ph ^ 1);  // epilogue drained the accumulator
         fence_after();
         for (int kb = kb0; kb < kb1; ++kb) {
+          const int slot = kSepA ? a : s;
           mbar_wait(&full_bar[s], ph);
-          mbar_wait(&afull_bar[s], ph);
+          mbar_wait(&afull_bar[slot], kSepA ? aph : ph);
           fence_after();
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t bdesc = sw128_desc(sb + s * Gm::STAGE + (kk / 4) * Gm::ACT_BOX);
-            if (!(FQ_TC_DBG & 1))
-              mma_ts(tmem + kAccCol, tmem + kACol + s * Gm::A_COLS + kk * 8, bdesc + (uint64_t)((kk % 4) * 2), idesc,
-                     (kb != kb0) || (kk != 0));
+#pragma unroll
+            for (int h = 0; h < HM; ++h)
+              if (!(FQ_TC_DBG & 1))
+                mma_ts(tmem + kAccCol + h * BNMAX, tmem + kACol + slot * Gm::A_COLS + h * Gm::A_HALF + kk * 8,
+                       bdesc + (uint64_t)((kk % 4) * 2), idesc, (kb != kb0) || (kk != 0));
           }
           mma_commit(&empty_bar[s]);
+          if (kSepA) {
+            mma_commit(&aempty_bar[slot]);
+            if (++a == ASLOTS) { a = 0; aph ^= 1; }
+          }
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
         mma_commit(&acc_full);
@@ -289,15 +320,13 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
     const int row = quarter * 32 + lane;     // weight row within the tile == TMEM lane
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const uint32_t sb = smem_u32(sbase);
-    int s = 0;
-    uint32_t ph = 0, acc_ph = 0;
+    int s = 0, a = 0;
+    uint32_t ph = 0, aph = 0, acc_ph = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const TcProb& p = find_prob(batch, tile);
       const int N = p.N, M = p.M;
       int mt, nt, tt, ks, kb0, kb1;
       work_coords<BK>(p, tile, mt, nt, tt, ks, kb0, kb1);
-      const int n = nt * BM + row;
-      const int nc = min(n, N - 1);
       const int grp = p.group;                     // hoisted: p lives in the parameter space
       const bool one_scale = grp % kKPW == 0;      // this thread's kKPW k lie in one group
       int j0 = (kb0 * BK) / grp, r0 = kb0 * BK - j0 * grp;  // first staged scale row
@@ -309,75 +338,87 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
         // jb + t, t = [gk + 8w >= g] + [gk + 8w >= 2g]; row index in smem = group - j0.
         mbar_wait(&full_bar[s], ph);
         constexpr int NW = kKPW / 8;  // 8-k words of this thread
-        uint32_t sc[NW];
-        if (one_scale) {
-          const uint32_t v = lds_u16(srow + s * Gm::STAGE + (jb - j0) * BM * 2);
-          const uint32_t v2 = prmt(v, v, 0x1010u);
+        const int slot = kSepA ? a : s;
 #pragma unroll
-          for (int w = 0; w < NW; ++w) sc[w] = v2;
-        } else {
+        for (int h = 0; h < HM; ++h) {
+          uint32_t sc[NW];
+          const uint32_t srh = srow + s * Gm::STAGE + h * Gm::SC_HALF;
+          if (one_scale) {
+            const uint32_t v = lds_u16(srh + (jb - j0) * BM * 2);
+            const uint32_t v2 = prmt(v, v, 0x1010u);
 #pragma unroll
-          for (int w = 0; w < NW; ++w) {
-            const int o = gk + 8 * w;  // < grp + kKPW: at most kKPW / 16 group boundaries
-            int jr = jb - j0;
+            for (int w = 0; w < NW; ++w) sc[w] = v2;
+          } else {
 #pragma unroll
-            for (int m = 1; m <= kKPW / 16; ++m) jr += (o >= m * grp);
-            const uint32_t v = lds_u16(srow + s * Gm::STAGE + jr * BM * 2);
-            sc[w] = prmt(v, v, 0x1010u);
+            for (int w = 0; w < NW; ++w) {
+              const int o = gk + 8 * w;  // < grp + kKPW: at most kKPW / 16 group boundaries
+              int jr = jb - j0;
+#pragma unroll
+              for (int m = 1; m <= kKPW / 16; ++m) jr += (o >= m * grp);
+              const uint32_t v = lds_u16(srh + jr * BM * 2);
+              sc[w] = prmt(v, v, 0x1010u);
+            }
           }
-        }
-        const uint32_t qbase = sb + s * Gm::STAGE + Gm::ACT_BYTES + row * Gm::CODE_BYTES_ROW;
-        uint32_t out[kKPW / 2];
-        if (FQ_TC_DBG & 2) {
-        } else if (BITS == 4) {
-          // kKPW/2 bytes of the swizzled code row
-          constexpr int ROWB = Gm::CODE_BYTES_ROW;
-          uint32_t words[NW];
-          if constexpr (kKPW >= 32) {
+          const uint32_t qbase = sb + s * Gm::STAGE + Gm::ACT_BYTES + h * Gm::CODE_HALF + row * Gm::CODE_BYTES_ROW;
+          uint32_t out[kKPW / 2];
+          if (FQ_TC_DBG & 2) {
+          } else if (BITS == 4) {
+            // kKPW/2 bytes of the swizzled code row
+            constexpr int ROWB = Gm::CODE_BYTES_ROW;
+            uint32_t words[NW];
+            if constexpr (kKPW >= 32) {
 #pragma unroll
-            for (int i = 0; i < kKPW / 32; ++i) {
-              const uint4 c = lds128(qbase + (swz_chunk<ROWB>(half * (kKPW / 32) + i, row) << 4));
-              words[4 * i] = c.x; words[4 * i + 1] = c.y; words[4 * i + 2] = c.z; words[4 * i + 3] = c.w;
+              for (int i = 0; i < kKPW / 32; ++i) {
+                const uint4 c = lds128(qbase + (swz_chunk<ROWB>(half * (kKPW / 32) + i, row) << 4));
+                words[4 * i] = c.x; words[4 * i + 1] = c.y; words[4 * i + 2] = c.z; words[4 * i + 3] = c.w;
+              }
+            } else {
+              const uint2 c = lds64(qbase + (swz_chunk<ROWB>(half >> 1, row) << 4) + (half & 1) * 8);
+              words[0] = c.x; words[1] = c.y;
+            }
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+              uint32_t q[4];
+              i4_nat_pairs<T>(words[w], q);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) out[4 * w + i] = mul2x<T>(q[i], sc[w]);
             }
           } else {
-            const uint2 c = lds64(qbase + (swz_chunk<ROWB>(half >> 1, row) << 4) + (half & 1) * 8);
-            words[0] = c.x; words[1] = c.y;
-          }
+            // kKPW bytes of the swizzled code row
 #pragma unroll
-          for (int w = 0; w < NW; ++w) {
-            uint32_t q[4];
-            i4_nat_pairs<T>(words[w], q);
+            for (int hh = 0; hh < kKPW / 16; ++hh) {
+              const int cidx = half * (kKPW / 16) + hh;
+              const uint4 c = lds128(qbase + (swz_chunk<Gm::CODE_BYTES_ROW>(cidx, row) << 4));
+              const uint32_t words[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
-            for (int i = 0; i < 4; ++i) out[4 * w + i] = mul2x<T>(q[i], sc[w]);
-          }
-        } else {
-          // kKPW bytes of the swizzled code row
-#pragma unroll
-          for (int hh = 0; hh < kKPW / 16; ++hh) {
-            const int cidx = half * (kKPW / 16) + hh;
-            const uint4 c = lds128(qbase + (swz_chunk<Gm::CODE_BYTES_ROW>(cidx, row) << 4));
-            const uint32_t words[4] = {c.x, c.y, c.z, c.w};
-#pragma unroll
-            for (int w = 0; w < 4; ++w) {
-              uint32_t q[2];
-              i8_nat_pairs<T>(words[w], q);
-              const uint32_t scw = sc[hh * 2 + (w >> 1)];
-              out[8 * hh + 2 * w] = mul2x<T>(q[0], scw);
-              out[8 * hh + 2 * w + 1] = mul2x<T>(q[1], scw);
+              for (int w = 0; w < 4; ++w) {
+                uint32_t q[2];
+                i8_nat_pairs<T>(words[w], q);
+                const uint32_t scw = sc[hh * 2 + (w >> 1)];
+                out[8 * hh + 2 * w] = mul2x<T>(q[0], scw);
+                out[8 * hh + 2 * w + 1] = mul2x<T>(q[1], scw);
+              }
             }
           }
+          // separate slot ring: the MMAs that last read this A slot must have completed
+          if (kSepA && h == 0) {
+            mbar_wait(&aempty_bar[slot], aph ^ 1);
+            fence_after();
+          }
+          const uint32_t acol = tmem + lane_base + kACol + slot * Gm::A_COLS + h * Gm::A_HALF;
+          if (FQ_TC_DBG & 2) {
+          } else if constexpr (kKPW == 64)
+            tmem_st32(acol + half * 32, *reinterpret_cast<const uint32_t(*)[32]>(out));
+          else if constexpr (kKPW == 32)
+            tmem_st16(acol + half * 16, *reinterpret_cast<const uint32_t(*)[16]>(out));
+          else
+            tmem_st8(acol + half * 8, *reinterpret_cast<const uint32_t(*)[8]>(out));
         }
-        if (FQ_TC_DBG & 2) {
-        } else if constexpr (kKPW == 64)
-          tmem_st32(tmem + lane_base + kACol + s * Gm::A_COLS + half * 32, *reinterpret_cast<const uint32_t(*)[32]>(out));
-        else if constexpr (kKPW == 32)
-          tmem_st16(tmem + lane_base + kACol + s * Gm::A_COLS + half * 16, *reinterpret_cast<const uint32_t(*)[16]>(out));
-        else
-          tmem_st8(tmem + lane_base + kACol + s * Gm::A_COLS + half * 8, *reinterpret_cast<const uint32_t(*)[8]>(out));
         tmem_wait_st();
         fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&afull_bar[s]);
+        if (lane == 0) mbar_arrive(&afull_bar[slot]);
+        if (kSepA && ++a == ASLOTS) { a = 0; aph ^= 1; }
         if (++s == STAGES) { s = 0; ph ^= 1; }
         r0 += BK;
         while (r0 >= grp) { r0 -= grp; ++j0; }
@@ -390,26 +431,31 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
       fence_after();
       constexpr int TPP = 256 / kParts;  // accumulator (token) columns drained per dequant warp
       const int tok_base = mt * p.bn + half * TPP;
-      auto store = [&](int tok, float f) {
-        if (p.cdt == FQ_FP32) reinterpret_cast<float*>(p.C)[(size_t)tok * N + n] = f;
-        else reinterpret_cast<T*>(p.C)[(size_t)tok * N + n] = Dt<T>::from_f(f);
-      };
-      // split-K: this item's fp32 partial [bn][128] of output tile tt, slot ks
-      float* part = p.splits > 1 ? p.ws + (size_t)(tt * p.splits + ks) * p.bn * BM : nullptr;
+      // split-K: this item's fp32 partial [bn][BMT] of output tile tt, slot ks
+      float* part = p.splits > 1 ? p.ws + (size_t)(tt * p.splits + ks) * p.bn * BMT : nullptr;
+#pragma unroll
+      for (int h = 0; h < HM; ++h) {
+        const int n = nt * BMT + h * BM + row;
+        auto store = [&](int tok, float f) {
+          if (p.cdt == FQ_FP32) reinterpret_cast<float*>(p.C)[(size_t)tok * N + n] = f;
+          else reinterpret_cast<T*>(p.C)[(size_t)tok * N + n] = Dt<T>::from_f(f);
+        };
 #pragma unroll 1
-      for (int c0 = 0; c0 < TPP && half * TPP + c0 < p.bn; c0 += 32) {
-        uint32_t v[32];
-        tmem_ld32(tmem + lane_base + kAccCol + half * TPP + c0, v);
-        tmem_wait_ld();
-        if (part) {
+        for (int c0 = 0; c0 < TPP && half * TPP + c0 < p.bn; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32(tmem + lane_base + kAccCol + h * BNMAX + half * TPP + c0, v);
+          tmem_wait_ld();
+          if (part) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (half * TPP + c0 + i < p.bn) __stcg(part + (half * TPP + c0 + i) * BM + row, __uint_as_float(v[i]));
-        } else if (n < N) {
+            for (int i = 0; i < 32; ++i)
+              if (half * TPP + c0 + i < p.bn)
+                __stcg(part + (half * TPP + c0 + i) * BMT + h * BM + row, __uint_as_float(v[i]));
+          } else if (n < N) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int tok = tok_base + c0 + i;
-            if (tok < M) store(tok, __uint_as_float(v[i]));
+            for (int i = 0; i < 32; ++i) {
+              const int tok = tok_base + c0 + i;
+              if (tok < M) store(tok, __uint_as_float(v[i]));
+            }
           }
         }
       }
@@ -427,21 +473,22 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
         }
         asm volatile("bar.sync 1, %0;" ::"n"(32 * kDqWarps));
         if (s_last) {
-          // 256 threads: thread -> (row = tid % 128, tokens tid / 128 + 2i); 4 tokens per round so
+          // thread -> (row = tid % BMT, tokens tid / BMT + NPAR i); 4 tokens per round so
           // their split loads are in flight together; rows are contiguous -> coalesced
-          const float* base = p.ws + (size_t)tt * p.splits * p.bn * BM;
-          constexpr int NPAR = kDqWarps * 32 / BM;  // threads per row
-          const int tid = threadIdx.x - 64, r = tid & (BM - 1);
-          const int nr = nt * BM + r;
+          const float* base = p.ws + (size_t)tt * p.splits * p.bn * BMT;
+          constexpr int NPAR = kDqWarps * 32 / BMT;  // threads per row
+          static_assert(NPAR >= 1, "fixup: one thread per row at least");
+          const int tid = threadIdx.x - 64, r = tid & (BMT - 1);
+          const int nr = nt * BMT + r;
           const int tmax = min(p.bn, M - mt * p.bn);
           if (nr < N) {
-            for (int tl0 = tid / BM; tl0 < tmax; tl0 += 4 * NPAR) {
+            for (int tl0 = tid / BMT; tl0 < tmax; tl0 += 4 * NPAR) {
               float acc[4] = {0.f, 0.f, 0.f, 0.f};
               for (int q = 0; q < p.splits; ++q) {
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                   const int tl = tl0 + NPAR * u;
-                  if (tl < tmax) acc[u] += __ldcg(base + ((size_t)q * p.bn + tl) * BM + r);
+                  if (tl < tmax) acc[u] += __ldcg(base + ((size_t)q * p.bn + tl) * BMT + r);
                 }
               }
 #pragma unroll
@@ -478,6 +525,39 @@ static int tc_bk(int bnmax) {
   if (bnmax > 128 || std::getenv("FQ_TC_BNMAX256")) return 64;
   return forced == 64 ? 64 : 128;
 }
+// 128-row halves per tile (tile = 128 * hm weight rows) for the 64/128-token variants.  Two halves
+// carry twice the code bytes per staged activation tile, which is what bounds the small-M regime;
+// but with half as many tiles a matrix needs more K splits to fill the SMs, and short split items
+// (pipeline fill + fixup, which stalls the dequant warps) lose more than the halves gain.  Measured
+// (tools/tc_mid.py, tools/paper_microbench.py): two halves win for the MoE batch (M_e = 32 / 64 / 128:
+// -20 / -28 / -17%) and for long-K matrices with fewer one-half tiles than SMs (OPT-175B FC2,
+// M = 48..128: -30..-40%); they lose for OPT-175B FC1 (384 one-half tiles: +7..+16%) and for the
+// OPT-13B/30B matrices (K <= 28672: split items of 5-40 K blocks, up to 1.9x slower).  Rule: two
+// halves for MoE batches, and for a single GEMM when its one-half tiles do not fill the SMs and the
+// two-half split plan keeps >= 64 K blocks (8192 k) per item.  FQ_TC_HM=1|2 overrides (diagnostics).
+static int tc_hm_forced() {  // read per call (tests switch it within one process)
+  const char* e = std::getenv("FQ_TC_HM");
+  return e ? std::atoi(e) : 0;
+}
+static int tc_bn(int M);
+static int tc_splits_hm(int M, int K, int N, int bits, int hm, int* kbs_out);
+static bool tc_hm_ok(int bnmax) { return bnmax <= 128 && tc_bk(bnmax) == 128; }
+static int tc_hm_batch(int bnmax) {  // MoE batch
+  if (!tc_hm_ok(bnmax)) return 1;
+  const int forced = tc_hm_forced();
+  return (forced == 1 || forced == 2) ? forced : 2;
+}
+static int tc_hm_gemm(int M, int K, int N, int bits) {
+  const int bn = tc_bn(M);
+  if (!tc_hm_ok(bn)) return 1;
+  const int forced = tc_hm_forced();
+  if (forced == 1 || forced == 2) return forced;
+  const long long tiles1 = (long long)((M + bn - 1) / bn) * ((N + tc::BM - 1) / tc::BM);
+  if (tiles1 >= num_sms()) return 1;
+  int kbs2 = 0;
+  tc_splits_hm(M, K, N, bits, 2, &kbs2);
+  return kbs2 >= 64 ? 2 : 1;
+}
 static int tc_bn(int M) {
 #ifdef FQ_TC_FULLBN
   (void)M;
@@ -488,9 +568,10 @@ static int tc_bn(int M) {
 }
 
 static bool make_tc_prob(tc::TcProb& d, int bits, const void* A, int M, int K, int N, const void* codes,
-                         const void* scales, int group, void* C, int cdt, int bk) {
+                         const void* scales, int group, void* C, int cdt, int bk, int hm) {
   d.bn = tc_bn(M);
   d.bk = bk;
+  d.hm = hm;
   if (!make_tmap_2d(&d.a, A, 2, (uint64_t)K, (uint64_t)M, (uint64_t)K * 2, tc::BKA, d.bn, 128)) return false;
   const uint64_t row_bytes = (uint64_t)K * bits / 8;
   const int code_row = bk * bits / 8;  // box row bytes = swizzle span (32 / 64 / 128)
@@ -502,7 +583,7 @@ static bool make_tc_prob(tc::TcProb& d, int bits, const void* A, int M, int K, i
   d.C = C;
   d.M = M; d.K = K; d.N = N; d.group = group; d.cdt = cdt;
   d.m_tiles = (M + d.bn - 1) / d.bn;
-  d.n_tiles = (N + tc::BM - 1) / tc::BM;
+  d.n_tiles = (N + tc::BM * hm - 1) / (tc::BM * hm);
   const char* gme = std::getenv("FQ_TC_GM");
   d.gm = gme ? std::max(1, std::atoi(gme)) : 8;
   d.splits = 1;
@@ -514,32 +595,57 @@ static bool make_tc_prob(tc::TcProb& d, int bits, const void* A, int M, int K, i
 
 // Split-K plan of one GEMM: when its output tiles cannot fill the SMs (e.g. M <= 256 on a weight
 // matrix of < 148 x 128 rows), K is cut into ranges of >= 512 k so ~one work item per SM runs.
+// Two-half tiles (fewer, larger tiles): the split count minimises (code bytes + partial traffic) /
+// last-round efficiency of the persistent schedule, e.g. OPT-175B FC1 at M <= 64: 192 tiles on
+// 148 SMs (65% in the last round) -> 3 splits (576 items, 97%) for 24% more traffic.
 constexpr size_t kTcCounterBytes = 65536;
-static int tc_splits(int M, int K, int N, int* kbs_out = nullptr) {
+static int tc_splits_hm(int M, int K, int N, int bits, int hm, int* kbs_out) {
   const int bn = tc_bn(M);
   const int bk = tc_bk(bn);
-  const int tiles = ((M + bn - 1) / bn) * ((N + tc::BM - 1) / tc::BM);
+  const int tiles = ((M + bn - 1) / bn) * ((N + tc::BM * hm - 1) / (tc::BM * hm));
   const int kblocks = (K + bk - 1) / bk;
+  const int smax = std::max(1, kblocks / (512 / bk));
   const char* e = std::getenv("FQ_TC_SPLITS");
-  int s = e ? std::atoi(e) : num_sms() / std::max(1, tiles);
-  s = std::max(1, std::min(s, kblocks / (512 / bk)));
+  int s;
+  if (e) {
+    s = std::atoi(e);
+  } else if (hm == 1) {
+    s = num_sms() / std::max(1, tiles);
+  } else {
+    const double code = (double)N * K * bits / 8;
+    double best = 1e300;
+    s = 1;
+    for (int c = 1; c <= std::min(8, smax); ++c) {
+      const int kbs = (kblocks + c - 1) / c, ce = (kblocks + kbs - 1) / kbs;
+      const double items = (double)tiles * ce, rounds = items / num_sms();
+      const double eff = rounds / std::ceil(rounds);
+      const double part = ce > 1 ? 2.0 * items * bn * tc::BM * hm * sizeof(float) : 0.0;
+      const double cost = (code + part) / eff;
+      if (cost < best * 0.99) { best = cost; s = c; }
+    }
+  }
+  s = std::max(1, std::min(s, smax));
   if (tiles > (int)(kTcCounterBytes / sizeof(int))) s = 1;
   const int kbs = (kblocks + s - 1) / s;
   if (kbs_out) *kbs_out = kbs;
   return (kblocks + kbs - 1) / kbs;
 }
-size_t gemm_tc_workspace_bytes(int M, int K, int N) {
-  const int s = tc_splits(M, K, N);
+static int tc_splits(int M, int K, int N, int bits, int* kbs_out = nullptr) {
+  return tc_splits_hm(M, K, N, bits, tc_hm_gemm(M, K, N, bits), kbs_out);
+}
+size_t gemm_tc_workspace_bytes(int M, int K, int N, int bits) {
+  const int s = tc_splits(M, K, N, bits);
   if (s == 1) return 256;
   const int bn = tc_bn(M);
-  const size_t tiles = (size_t)((M + bn - 1) / bn) * ((N + tc::BM - 1) / tc::BM);
-  return kTcCounterBytes + tiles * s * bn * tc::BM * sizeof(float);
+  const int bmt = tc::BM * tc_hm_gemm(M, K, N, bits);
+  const size_t tiles = (size_t)((M + bn - 1) / bn) * ((N + bmt - 1) / bmt);
+  return kTcCounterBytes + tiles * s * bn * bmt * sizeof(float);
 }
 
-template <typename T, int BITS, int MAXP, int BNMAX, int BK>
+template <typename T, int BITS, int MAXP, int BNMAX, int BK, int HM>
 static cudaError_t launch_tc(const tc::TcBatch<MAXP>& b, cudaStream_t st) {
-  using Gm = tc::Geo<BITS, BNMAX, BK>;
-  auto kern = tc::gemm_tc_kernel<T, BITS, MAXP, BNMAX, BK>;
+  using Gm = tc::Geo<BITS, BNMAX, BK, HM>;
+  auto kern = tc::gemm_tc_kernel<T, BITS, MAXP, BNMAX, BK, HM>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Gm::SMEM);
@@ -551,12 +657,12 @@ static cudaError_t launch_tc(const tc::TcBatch<MAXP>& b, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-template <int MAXP, int BNMAX, int BK>
+template <int MAXP, int BNMAX, int BK, int HM = 1>
 static cudaError_t dispatch_tc_bn(int adt, int bits, const tc::TcBatch<MAXP>& b, cudaStream_t st) {
   if (adt == FQ_BF16)
-    return bits == 4 ? launch_tc<__nv_bfloat16, 4, MAXP, BNMAX, BK>(b, st)
-                     : launch_tc<__nv_bfloat16, 8, MAXP, BNMAX, BK>(b, st);
-  return bits == 4 ? launch_tc<__half, 4, MAXP, BNMAX, BK>(b, st) : launch_tc<__half, 8, MAXP, BNMAX, BK>(b, st);
+    return bits == 4 ? launch_tc<__nv_bfloat16, 4, MAXP, BNMAX, BK, HM>(b, st)
+                     : launch_tc<__nv_bfloat16, 8, MAXP, BNMAX, BK, HM>(b, st);
+  return bits == 4 ? launch_tc<__half, 4, MAXP, BNMAX, BK, HM>(b, st) : launch_tc<__half, 8, MAXP, BNMAX, BK, HM>(b, st);
 }
 // kernel variant = the widest token tile of the launch (64 / 128 / 256 tokens) and the stage K its
 // problems were prepared for
@@ -565,10 +671,14 @@ static cudaError_t dispatch_tc(int adt, int bits, const tc::TcBatch<MAXP>& b, cu
   int bn = 0;
   for (int i = 0; i < b.nprob; ++i) bn = std::max(bn, b.p[i].bn);
   if (std::getenv("FQ_TC_BNMAX256")) bn = 256;  // diagnostics: the large-M variant for every M
-  const int bk = b.p[0].bk;
+  const int bk = b.p[0].bk, hm = b.p[0].hm;
   for (int i = 1; i < b.nprob; ++i)
-    if (b.p[i].bk != bk) return cudaErrorInvalidValue;
-  if (bn > 128) return bk == 64 ? dispatch_tc_bn<MAXP, 256, 64>(adt, bits, b, st) : cudaErrorInvalidValue;
+    if (b.p[i].bk != bk || b.p[i].hm != hm) return cudaErrorInvalidValue;
+  if (bn > 128) return (bk == 64 && hm == 1) ? dispatch_tc_bn<MAXP, 256, 64>(adt, bits, b, st) : cudaErrorInvalidValue;
+  if (hm == 2) {
+    if (bk != 128) return cudaErrorInvalidValue;
+    return bn <= 64 ? dispatch_tc_bn<MAXP, 64, 128, 2>(adt, bits, b, st) : dispatch_tc_bn<MAXP, 128, 128, 2>(adt, bits, b, st);
+  }
   if (bn <= 64)
     return bk == 128 ? dispatch_tc_bn<MAXP, 64, 128>(adt, bits, b, st) : dispatch_tc_bn<MAXP, 64, 64>(adt, bits, b, st);
   return bk == 128 ? dispatch_tc_bn<MAXP, 128, 128>(adt, bits, b, st) : dispatch_tc_bn<MAXP, 128, 64>(adt, bits, b, st);
@@ -578,10 +688,11 @@ cudaError_t run_gemm_tc(int adt, int cdt, int bits, const void* A, int M, int K,
                         const void* scales, int group, void* C, void* ws, size_t ws_bytes, cudaStream_t st) {
   tc::TcBatch<1> b{};
   tc::TcProb& d = b.p[0];
-  if (!make_tc_prob(d, bits, A, M, K, N, codes, scales, group, C, cdt, tc_bk(tc_bn(M)))) return cudaErrorInvalidValue;
+  if (!make_tc_prob(d, bits, A, M, K, N, codes, scales, group, C, cdt, tc_bk(tc_bn(M)), tc_hm_gemm(M, K, N, bits)))
+    return cudaErrorInvalidValue;
   int kbs = 0;
-  const int s = tc_splits(M, K, N, &kbs);
-  if (s > 1 && ws && ws_bytes >= gemm_tc_workspace_bytes(M, K, N)) {
+  const int s = tc_splits(M, K, N, bits, &kbs);
+  if (s > 1 && ws && ws_bytes >= gemm_tc_workspace_bytes(M, K, N, bits)) {
     d.kbs = kbs;
     d.splits = s;
     d.ctr = reinterpret_cast<int*>(ws);
@@ -603,14 +714,14 @@ cudaError_t run_gemm_tc_grouped(int adt, int cdt, int bits, const void* A, int K
   int bnmax = 0;  // one stage K for every launch of the call (all chunks fit its variant)
   for (int ii = 0; ii < nexp; ++ii)
     bnmax = std::max(bnmax, tc_bn((int)(offsets[experts[ii] + 1] - offsets[experts[ii]])));
-  const int bk = tc_bk(bnmax);
+  const int bk = tc_bk(bnmax), hm = tc_hm_batch(bnmax);
   for (int ii = 0; ii < nexp; ++ii) {
     const int e = experts[ii];
     const int Me = (int)(offsets[e + 1] - offsets[e]);
     const char* Ae = reinterpret_cast<const char*>(A) + (size_t)offsets[e] * K * 2;
     char* Ce = reinterpret_cast<char*>(C) + (size_t)offsets[e] * N * (cdt == FQ_FP32 ? 4 : 2);
     tc::TcProb& d = b.p[b.nprob];
-    if (!make_tc_prob(d, bits, Ae, Me, K, N, codes[e], scales[e], groups[e], Ce, cdt, bk)) return cudaErrorInvalidValue;
+    if (!make_tc_prob(d, bits, Ae, Me, K, N, codes[e], scales[e], groups[e], Ce, cdt, bk, hm)) return cudaErrorInvalidValue;
     d.tile_begin = b.total_tiles;
     b.total_tiles += d.m_tiles * d.n_tiles;
     if (++b.nprob == MAXP) {

@@ -199,6 +199,22 @@ def test_tc_split_k(fq, env, M, K, N, bits, group):
     assert O.rel_err(torch_to_f64(C2), Cr, D) <= TOL
 
 
+@pytest.mark.parametrize("hm", [1, 2])
+@pytest.mark.parametrize("M,K,N,bits,group,adt", [(32, 4096, 512, 4, 128, "bf16"), (48, 2048, 392, 8, 64, "fp16"),
+                                                  (100, 3072, 640, 4, 32, "bf16"), (17, 8192, 136, 4, 16, "bf16")])
+def test_tc_tile_halves_split_k(fq, env, hm, M, K, N, bits, group, adt):
+    """A6 with one- and two-half tiles (128 / 256 weight rows, FQ_TC_HM forces the choice) under
+    split-K: parity, bit-identical repeated calls, and N tails inside / past the second half."""
+    env("FQ_GEMM_PATH", "tc")
+    env("FQ_TC_HM", hm)
+    Wb, Ab = make_case(M, K, N, bits, group, adt, seed=M + K + hm)
+    _, C0 = run_case(fq, Wb, Ab, bits, group, adt, "fp32")
+    _, C1 = run_case(fq, Wb, Ab, bits, group, adt, "fp32")
+    assert torch.equal(C0, C1)
+    Cr, D = oracle_ref(Wb, Ab, bits, group, adt)
+    assert O.rel_err(torch_to_f64(C0), Cr, D) <= TOL
+
+
 @pytest.mark.parametrize("path", ["decode", "tc"])
 def test_identity_exact_fp32_out(fq, env, path):
     """A = I (M = K = 256): C[k, n] = q[n,k] * s[k/g, n] exactly in fp32-output mode — catches any
@@ -286,6 +302,11 @@ def test_opt175b_full_size_sampled(fq, shape, bits, M):
     (512, 2048, 1024, 4, 32, "fp16"),
     (384, 1024, 512, 8, 1024, "fp16"),     # per-column
     (17, 512, 256, 4, 16, "bf16"),         # smallest M routed to the tcgen05 kernel
+    # two-half (256-row) tiles of the <= 64-token variant: N tail inside the second half, and a
+    # last tile whose second half lies entirely past N (not loaded)
+    (48, 1024, 456, 4, 32, "fp16"),
+    (64, 2048, 392, 8, 128, "bf16"),
+    (33, 1536, 1160, 4, 64, "bf16"),
 ])
 def test_tc_path_parity(fq, env, M, K, N, bits, group, adt):
     """Large-M tcgen05 kernel (A6) vs the fp64 oracle on full outputs."""
