@@ -85,10 +85,13 @@ struct Geo {
   static constexpr int A_COLS = A_HALF * HM;                  // TMEM columns of one A slot
   static constexpr int ACC_COLS = BNMAX * HM;                 // accumulator columns (half h at h*BNMAX)
   static constexpr int S_TMEM = (kTmemCols - ACC_COLS) / A_COLS;
-  // HM = 1: one A slot per smem stage (slot index = stage index); HM = 2: a separate slot ring
-  static constexpr int S0 = (HM == 1 && S_TMEM < S_SMEM) ? S_TMEM : S_SMEM;
+  // One-half tiles of >= 64 tokens: one A slot per smem stage (slot index = stage index).  Two-half
+  // tiles and the 32-token variant: more smem stages than TMEM holds A slots, so the A slots form a
+  // separate ring behind the stage ring.
+  static constexpr int S0 = (HM == 1 && BNMAX > 32 && S_TMEM < S_SMEM) ? S_TMEM : S_SMEM;
   static constexpr int STAGES = S0 > 16 ? 16 : S0;
-  static constexpr int ASLOTS = HM == 1 ? STAGES : (S_TMEM < STAGES ? S_TMEM : STAGES);
+  static constexpr int ASLOTS = S_TMEM < STAGES ? S_TMEM : STAGES;
+  static constexpr bool SEP_A = ASLOTS < STAGES;
   static constexpr int SMEM = STAGES * STAGE + 1024;
   static constexpr int A_COL = ACC_COLS;
   static_assert(STAGES >= (HM == 1 ? 4 : 3) && ASLOTS >= 2, "stages");
@@ -193,15 +196,20 @@ __device__ __forceinline__ int swz_chunk(int c, int r) {
   return ROWB == 32 ? c ^ ((r >> 2) & 1) : ROWB == 64 ? c ^ ((r >> 1) & 3) : c ^ (r & 7);
 }
 
-template <typename T, int BITS, int MAXP, int BNMAX, int BK, int HM>
+template <typename T, int BITS, int MAXP, int BNMAX, int BK, int HM, int DQG>
 __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __grid_constant__ TcBatch<MAXP> batch) {
   constexpr int kDqWarps = dq_warps(BNMAX);
   constexpr int kParts = kDqWarps / 4;
-  constexpr int kKPW = BK / kParts;  // k per dequant thread per K block (16 / 32 / 64)
+  // With 16 dequant warps, two groups of 8 take alternate K blocks, so one group's tcgen05.st /
+  // wait::st / arrive latency overlaps the other's loads and unpacking (each group covers a whole
+  // K block: two warps per TMEM lane quarter, kKPW = BK / 2).
+  constexpr int kDqGroups = kDqWarps == 16 ? DQG : 1;
+  constexpr int kPartsG = kParts / kDqGroups;
+  constexpr int kKPW = BK / kPartsG;  // k per dequant thread per K block (16 / 32 / 64)
   using Gm = Geo<BITS, BNMAX, BK, HM>;
   constexpr int STAGES = Gm::STAGES;
   constexpr int ASLOTS = Gm::ASLOTS;
-  constexpr bool kSepA = HM > 1;     // A slots in their own ring (see Geo)
+  constexpr bool kSepA = Gm::SEP_A;  // A slots in their own ring (see Geo)
   constexpr int BMT = Gm::BMT;
   constexpr int kACol = Gm::A_COL;
   extern __shared__ __align__(1024) uint8_t dsmem[];
@@ -219,7 +227,7 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
       mbar_init(&empty_bar[s], 1);
     }
     for (int a = 0; a < ASLOTS; ++a) {
-      mbar_init(&afull_bar[a], kDqWarps);  // one arrival per dequant warp
+      mbar_init(&afull_bar[a], kDqWarps / kDqGroups);  // one arrival per warp of the block's group
       mbar_init(&aempty_bar[a], 1);        // MMA commit (separate slot ring only)
     }
     mbar_init(&acc_full, 1);
@@ -316,11 +324,13 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
     // ------------------------------------------------------------------ dequant + epilogue
     const int dq = warp - 2;
     const int quarter = warp & 3;            // TMEM lane quarter this warp may access
-    const int half = dq >> 2;                // which kKPW k of the 64-k block (and token part)
+    const int half = dq >> 2;                // accumulator (token) part this warp drains
+    const int kp = half % kPartsG;           // which kKPW k of the K block this warp dequantizes
+    const int dgrp = half / kPartsG;         // its group: K blocks with (block counter % groups) == dgrp
     const int row = quarter * 32 + lane;     // weight row within the tile == TMEM lane
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const uint32_t sb = smem_u32(sbase);
-    int s = 0, a = 0;
+    int s = 0, a = 0, blk = 0;
     uint32_t ph = 0, aph = 0, acc_ph = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const TcProb& p = find_prob(batch, tile);
@@ -331,14 +341,15 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
       const bool one_scale = grp % kKPW == 0;      // this thread's kKPW k lie in one group
       int j0 = (kb0 * BK) / grp, r0 = kb0 * BK - j0 * grp;  // first staged scale row
       // group of this thread's first k (kb0*BK + half*kKPW) and its offset in the group
-      int jb = (kb0 * BK + half * kKPW) / grp, gk = kb0 * BK + half * kKPW - jb * grp;
+      int jb = (kb0 * BK + kp * kKPW) / grp, gk = kb0 * BK + kp * kKPW - jb * grp;
       const uint32_t srow = sb + Gm::SC_OFS + row * 2;
       for (int kb = kb0; kb < kb1; ++kb) {
         // scales of this thread's 8-k words from the TMA-staged rows: word w lies in group
         // jb + t, t = [gk + 8w >= g] + [gk + 8w >= 2g]; row index in smem = group - j0.
+        const int slot = kSepA ? a : s;
+        if (kDqGroups == 1 || (blk % kDqGroups) == dgrp) {
         mbar_wait(&full_bar[s], ph);
         constexpr int NW = kKPW / 8;  // 8-k words of this thread
-        const int slot = kSepA ? a : s;
 #pragma unroll
         for (int h = 0; h < HM; ++h) {
           uint32_t sc[NW];
@@ -369,11 +380,11 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
             if constexpr (kKPW >= 32) {
 #pragma unroll
               for (int i = 0; i < kKPW / 32; ++i) {
-                const uint4 c = lds128(qbase + (swz_chunk<ROWB>(half * (kKPW / 32) + i, row) << 4));
+                const uint4 c = lds128(qbase + (swz_chunk<ROWB>(kp * (kKPW / 32) + i, row) << 4));
                 words[4 * i] = c.x; words[4 * i + 1] = c.y; words[4 * i + 2] = c.z; words[4 * i + 3] = c.w;
               }
             } else {
-              const uint2 c = lds64(qbase + (swz_chunk<ROWB>(half >> 1, row) << 4) + (half & 1) * 8);
+              const uint2 c = lds64(qbase + (swz_chunk<ROWB>(kp >> 1, row) << 4) + (kp & 1) * 8);
               words[0] = c.x; words[1] = c.y;
             }
 #pragma unroll
@@ -387,7 +398,7 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
             // kKPW bytes of the swizzled code row
 #pragma unroll
             for (int hh = 0; hh < kKPW / 16; ++hh) {
-              const int cidx = half * (kKPW / 16) + hh;
+              const int cidx = kp * (kKPW / 16) + hh;
               const uint4 c = lds128(qbase + (swz_chunk<Gm::CODE_BYTES_ROW>(cidx, row) << 4));
               const uint32_t words[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
@@ -408,16 +419,18 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
           const uint32_t acol = tmem + lane_base + kACol + slot * Gm::A_COLS + h * Gm::A_HALF;
           if (FQ_TC_DBG & 2) {
           } else if constexpr (kKPW == 64)
-            tmem_st32(acol + half * 32, *reinterpret_cast<const uint32_t(*)[32]>(out));
+            tmem_st32(acol + kp * 32, *reinterpret_cast<const uint32_t(*)[32]>(out));
           else if constexpr (kKPW == 32)
-            tmem_st16(acol + half * 16, *reinterpret_cast<const uint32_t(*)[16]>(out));
+            tmem_st16(acol + kp * 16, *reinterpret_cast<const uint32_t(*)[16]>(out));
           else
-            tmem_st8(acol + half * 8, *reinterpret_cast<const uint32_t(*)[8]>(out));
+            tmem_st8(acol + kp * 8, *reinterpret_cast<const uint32_t(*)[8]>(out));
         }
         tmem_wait_st();
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&afull_bar[slot]);
+        }
+        ++blk;
         if (kSepA && ++a == ASLOTS) { a = 0; aph ^= 1; }
         if (++s == STAGES) { s = 0; ph ^= 1; }
         r0 += BK;
@@ -642,10 +655,10 @@ size_t gemm_tc_workspace_bytes(int M, int K, int N, int bits) {
   return kTcCounterBytes + tiles * s * bn * bmt * sizeof(float);
 }
 
-template <typename T, int BITS, int MAXP, int BNMAX, int BK, int HM>
+template <typename T, int BITS, int MAXP, int BNMAX, int BK, int HM, int DQG>
 static cudaError_t launch_tc(const tc::TcBatch<MAXP>& b, cudaStream_t st) {
   using Gm = tc::Geo<BITS, BNMAX, BK, HM>;
-  auto kern = tc::gemm_tc_kernel<T, BITS, MAXP, BNMAX, BK, HM>;
+  auto kern = tc::gemm_tc_kernel<T, BITS, MAXP, BNMAX, BK, HM, DQG>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Gm::SMEM);
@@ -657,12 +670,19 @@ static cudaError_t launch_tc(const tc::TcBatch<MAXP>& b, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// dqg: dequant warp groups (2 = two groups of 8 warps on alternate K blocks; int4, 128-k stages,
+// 16-warp variants only -- see the kernel).
 template <int MAXP, int BNMAX, int BK, int HM = 1>
-static cudaError_t dispatch_tc_bn(int adt, int bits, const tc::TcBatch<MAXP>& b, cudaStream_t st) {
+static cudaError_t dispatch_tc_bn(int adt, int bits, const tc::TcBatch<MAXP>& b, cudaStream_t st, int dqg = 1) {
+  if constexpr (BK == 128 && tc::dq_warps(BNMAX) == 16) {
+    if (dqg == 2 && bits == 4)
+      return adt == FQ_BF16 ? launch_tc<__nv_bfloat16, 4, MAXP, BNMAX, BK, HM, 2>(b, st)
+                            : launch_tc<__half, 4, MAXP, BNMAX, BK, HM, 2>(b, st);
+  }
   if (adt == FQ_BF16)
-    return bits == 4 ? launch_tc<__nv_bfloat16, 4, MAXP, BNMAX, BK, HM>(b, st)
-                     : launch_tc<__nv_bfloat16, 8, MAXP, BNMAX, BK, HM>(b, st);
-  return bits == 4 ? launch_tc<__half, 4, MAXP, BNMAX, BK, HM>(b, st) : launch_tc<__half, 8, MAXP, BNMAX, BK, HM>(b, st);
+    return bits == 4 ? launch_tc<__nv_bfloat16, 4, MAXP, BNMAX, BK, HM, 1>(b, st)
+                     : launch_tc<__nv_bfloat16, 8, MAXP, BNMAX, BK, HM, 1>(b, st);
+  return bits == 4 ? launch_tc<__half, 4, MAXP, BNMAX, BK, HM, 1>(b, st) : launch_tc<__half, 8, MAXP, BNMAX, BK, HM, 1>(b, st);
 }
 // kernel variant = the widest token tile of the launch (64 / 128 / 256 tokens) and the stage K its
 // problems were prepared for
@@ -675,13 +695,26 @@ static cudaError_t dispatch_tc(int adt, int bits, const tc::TcBatch<MAXP>& b, cu
   for (int i = 1; i < b.nprob; ++i)
     if (b.p[i].bk != bk || b.p[i].hm != hm) return cudaErrorInvalidValue;
   if (bn > 128) return (bk == 64 && hm == 1) ? dispatch_tc_bn<MAXP, 256, 64>(adt, bits, b, st) : cudaErrorInvalidValue;
+  // <= 32-token variant: the small activation tile leaves room for more code stages in flight
+  const bool v32 = bn <= 32 && bk == 128 && !std::getenv("FQ_TC_NO32");
+  // Two alternating dequant warp groups (each thread then covers 64 k of a block): measured
+  // (profiles/r01/a6_two_half_tiles.txt) OPT-175B FC2 int4 M = 48..128 -8..-12%, FC1 int4 -1.5%,
+  // MoE g128 -3%; but +10-13% on MoE batches with 16-element groups (8 scale words per thread) and
+  // +5% on int8 FC1 -> int4 with every group a multiple of 64 only.  FQ_TC_DQG=1|2 overrides.
+  int dqg = bits == 4 ? 2 : 1;
+  for (int i = 0; i < b.nprob; ++i)
+    if (b.p[i].group % 64) dqg = 1;
+  if (const char* e = std::getenv("FQ_TC_DQG")) dqg = std::atoi(e) == 2 ? 2 : 1;
   if (hm == 2) {
     if (bk != 128) return cudaErrorInvalidValue;
-    return bn <= 64 ? dispatch_tc_bn<MAXP, 64, 128, 2>(adt, bits, b, st) : dispatch_tc_bn<MAXP, 128, 128, 2>(adt, bits, b, st);
+    if (v32) return dispatch_tc_bn<MAXP, 32, 128, 2>(adt, bits, b, st, dqg);
+    return bn <= 64 ? dispatch_tc_bn<MAXP, 64, 128, 2>(adt, bits, b, st, dqg)
+                    : dispatch_tc_bn<MAXP, 128, 128, 2>(adt, bits, b, st, dqg);
   }
+  if (v32) return dispatch_tc_bn<MAXP, 32, 128>(adt, bits, b, st, dqg);
   if (bn <= 64)
-    return bk == 128 ? dispatch_tc_bn<MAXP, 64, 128>(adt, bits, b, st) : dispatch_tc_bn<MAXP, 64, 64>(adt, bits, b, st);
-  return bk == 128 ? dispatch_tc_bn<MAXP, 128, 128>(adt, bits, b, st) : dispatch_tc_bn<MAXP, 128, 64>(adt, bits, b, st);
+    return bk == 128 ? dispatch_tc_bn<MAXP, 64, 128>(adt, bits, b, st, dqg) : dispatch_tc_bn<MAXP, 64, 64>(adt, bits, b, st);
+  return bk == 128 ? dispatch_tc_bn<MAXP, 128, 128>(adt, bits, b, st, dqg) : dispatch_tc_bn<MAXP, 128, 64>(adt, bits, b, st);
 }
 
 cudaError_t run_gemm_tc(int adt, int cdt, int bits, const void* A, int M, int K, int N, const void* codes,

@@ -199,14 +199,19 @@ def test_tc_split_k(fq, env, M, K, N, bits, group):
     assert O.rel_err(torch_to_f64(C2), Cr, D) <= TOL
 
 
+@pytest.mark.parametrize("dqg", [1, 2])
 @pytest.mark.parametrize("hm", [1, 2])
 @pytest.mark.parametrize("M,K,N,bits,group,adt", [(32, 4096, 512, 4, 128, "bf16"), (48, 2048, 392, 8, 64, "fp16"),
-                                                  (100, 3072, 640, 4, 32, "bf16"), (17, 8192, 136, 4, 16, "bf16")])
-def test_tc_tile_halves_split_k(fq, env, hm, M, K, N, bits, group, adt):
-    """A6 with one- and two-half tiles (128 / 256 weight rows, FQ_TC_HM forces the choice) under
-    split-K: parity, bit-identical repeated calls, and N tails inside / past the second half."""
+                                                  (100, 3072, 640, 4, 32, "bf16"), (17, 8192, 136, 4, 16, "bf16"),
+                                                  (24, 1536, 264, 4, 48, "fp16"), (64, 2048, 520, 4, 64, "bf16")])
+def test_tc_tile_halves_split_k(fq, env, dqg, hm, M, K, N, bits, group, adt):
+    """A6 with one- and two-half tiles (128 / 256 weight rows, FQ_TC_HM forces the choice) and one or
+    two alternating dequant warp groups (FQ_TC_DQG; int4 only, each thread then covers 64 k and up to
+    four group boundaries), under split-K: parity, bit-identical repeated calls, and N tails inside /
+    past the second half."""
     env("FQ_GEMM_PATH", "tc")
     env("FQ_TC_HM", hm)
+    env("FQ_TC_DQG", dqg)
     Wb, Ab = make_case(M, K, N, bits, group, adt, seed=M + K + hm)
     _, C0 = run_case(fq, Wb, Ab, bits, group, adt, "fp32")
     _, C1 = run_case(fq, Wb, Ab, bits, group, adt, "fp32")
