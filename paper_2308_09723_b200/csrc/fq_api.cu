@@ -49,11 +49,18 @@ static fq_status from_cuda(cudaError_t e) { return e == cudaSuccess ? FQ_OK : FQ
 // M <= 16 (32 on the int4 nibble path): memory-bound decode kernel (A4/A5), every weight streamed
 // once; larger M: tcgen05 tensor-core kernel (A6).  FQ_GEMM_PATH=decode|tc forces a path (tests and
 // A/B measurements).
-static bool use_tc_path(int64_t M, int bits, int group) {
+// A single GEMM (N > 0) of 17..32 tokens on the int4 nibble path goes to A6 when A6's 128-row tiles
+// do not fill the SMs (A6 then splits K, or uses two-half tiles): measured at M = 17 / 24 / 32
+// (profiles/r01/a6_two_half_tiles.txt) OPT-13B attn-out 34-44 -> 24 us, QKV 42-46 -> 36, FFN2
+// 56-69 -> 47-48, OPT-30B attn-out 40-50 -> 32, OPT-175B FC2 146 -> 131 (M = 32); matrices with
+// >= 148 tiles (OPT-175B FC1, OPT-13B FFN1, OPT-30B QKV / FFN1) stay on the decode kernel.
+static bool use_tc_path(int64_t M, int bits, int group, int64_t N = 0) {
   const char* e = std::getenv("FQ_GEMM_PATH");
   if (e && std::strcmp(e, "decode") == 0) return false;
   if (e && std::strcmp(e, "tc") == 0) return true;
-  return M > gemv_max_m(bits, group);
+  const int dmax = gemv_max_m(bits, group);
+  if (M > dmax) return true;
+  return M > 16 && N > 0 && tc_short_of_tiles((int)M, (int)N);
 }
 
 }  // namespace fq
@@ -143,7 +150,7 @@ fq_status fq_quantize(const void* W, int32_t wdt, const fq_wdesc* d, void* codes
 
 size_t fq_gemm_workspace_bytes(int64_t M, const fq_wdesc* d) {
   if (check_wdesc(d) != FQ_OK || M <= 0) return 0;
-  if (use_tc_path(M, d->bits, d->group)) return gemm_tc_workspace_bytes((int)M, (int)d->K, (int)d->N, d->bits);
+  if (use_tc_path(M, d->bits, d->group, d->N)) return gemm_tc_workspace_bytes((int)M, (int)d->K, (int)d->N, d->bits);
   if (decode_tc_supported(d->bits, d->group, (int)M))
     return dtc_workspace_bytes(M, (int)d->K, num_sms());
   const GemvPlan p = plan_gemv((int)M, (int)d->K, (int)d->N, d->bits, d->group, num_sms());
@@ -162,7 +169,7 @@ fq_status fq_gemm(const void* A, int32_t adt, int64_t M, const fq_wdesc* d, cons
   if (!codes || !scales) return FQ_ERR_INVALID_ARG;
   if (M == 0) return FQ_OK;  // empty batch (A and C may be NULL): nothing to compute, nothing launched
   if (!A || !C) return FQ_ERR_INVALID_ARG;
-  if (use_tc_path(M, d->bits, d->group))
+  if (use_tc_path(M, d->bits, d->group, d->N))
     return from_cuda(run_gemm_tc(adt, cdt, d->bits, A, (int)M, (int)d->K, (int)d->N, codes, scales,
                                  d->group, C, ws, ws_bytes, as_stream(stream)));
   if (decode_tc_supported(d->bits, d->group, (int)M)) {

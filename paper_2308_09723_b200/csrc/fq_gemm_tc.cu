@@ -643,6 +643,11 @@ static int tc_splits_hm(int M, int K, int N, int bits, int hm, int* kbs_out) {
   if (kbs_out) *kbs_out = kbs;
   return (kblocks + kbs - 1) / kbs;
 }
+// Do the 128-row tiles of a single GEMM leave SMs idle (so A6 splits K to fill them)?
+bool tc_short_of_tiles(int M, int N) {
+  const int bn = tc_bn(M);
+  return (long long)((M + bn - 1) / bn) * ((N + tc::BM - 1) / tc::BM) < num_sms();
+}
 static int tc_splits(int M, int K, int N, int bits, int* kbs_out = nullptr) {
   return tc_splits_hm(M, K, N, bits, tc_hm_gemm(M, K, N, bits), kbs_out);
 }
