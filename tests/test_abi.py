@@ -117,3 +117,22 @@ def test_gemm_workspace_sizes(fq):
     assert fq.fq_gemm_workspace_bytes(16, g64) >= 65536 + 16 * 5120 * 2  # group-split nibble path
     assert fq.fq_gemm_workspace_bytes(0, d) == 0
     assert fq.fq_gemm_grouped_workspace_bytes(64 * 16, 64, fq.make_wdesc(4096, 16384, 4, 4096, 0)) >= 65536
+    # OPT-175B FC2 (K = 49152, N = 12288): 96 one-half tiles leave SMs idle -> two-half (256-row)
+    # tiles with split-K partials [items][bn][256]; 17..32 tokens route to the same tensor-core path
+    fc2 = fq.make_wdesc(49152, 12288, 4, 128, fq.FQ_BF16)
+    nb = fq.fq_gemm_workspace_bytes(64, fc2)
+    assert nb > 65536 and (nb - 65536) % (64 * 256 * 4) == 0
+    saved = os.environ.get("FQ_GEMM_PATH")
+    try:
+        os.environ["FQ_GEMM_PATH"] = "tc"
+        forced = fq.fq_gemm_workspace_bytes(32, fc2)
+        os.environ["FQ_GEMM_PATH"] = "decode"
+        dec = fq.fq_gemm_workspace_bytes(32, fc2)
+    finally:
+        if saved is None:
+            os.environ.pop("FQ_GEMM_PATH", None)
+        else:
+            os.environ["FQ_GEMM_PATH"] = saved
+    assert forced != dec and fq.fq_gemm_workspace_bytes(32, fc2) == forced
+    # ... while FC1 (384 one-half tiles) keeps 17..32 tokens on the decode kernel
+    assert fq.fq_gemm_workspace_bytes(32, d) >= 65536 + 32 * 12288 * 2
