@@ -189,10 +189,19 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # FQ_BENCH_ONE_GPU=1 (diagnostics only): every rank on cuda:0 with the gloo backend, so the
+    # N > 1 code path (shards, row-parallel all-reduce, max-over-ranks timing) can be exercised on a
+    # one-GPU box; its numbers are not bench values.
+    one_gpu = os.environ.get("FQ_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     from paper_2308_09723_b200 import fq
     from paper_2308_09723_b200.tp import shard_bounds, check_row_group
