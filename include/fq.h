@@ -114,8 +114,8 @@ fq_status fq_quantize(const void* W, int32_t wdt, const fq_wdesc* d, void* codes
                       int32_t* status_dev, void* stream);
 
 /* ---------------------------------------------------------------------------------------------
- * Fused dequantize + GEMM (kernels A4/A5 for M <= 32 on the int4 nibble path with group % 128 == 0
- * and M <= 16 otherwise, A6 above), §4.1:
+ * Fused dequantize + GEMM (kernels A4/A5 for M <= 16, and for 17 <= M <= 32 on the int4 nibble path
+ * (group % 128 == 0) when the matrix has >= 148 A6 tiles; A6 otherwise), §4.1:
  *   C[m,n] = sum_k A[m,k] * q[n,k] * s[k/group, n]
  * A: [M, K] row-major, dtype adt in {BF16, FP16}; the scales must have dtype adt.
  * C: [M, N] row-major, dtype cdt in {adt, FP32} (FP32 is a diagnostic mode).
@@ -128,8 +128,9 @@ fq_status fq_quantize(const void* W, int32_t wdt, const fq_wdesc* d, void* codes
  *   without re-clearing.  Calls sharing one ws must be stream-ordered.
  * Accumulation is fp32; results are deterministic (fixed-order split-K reduction).  Both paths
  *   split K over CTAs when the output tiles alone cannot fill the GPU (A4: always planned; A6: when
- *   its 128-row x round_up(M,16)-token tiles are fewer than the SMs); a NULL/short ws on the A6 path
- *   just disables its split.
+ *   its 128-row x round_up(M,16)-token tiles are fewer than the SMs, then possibly as 256-row
+ *   tiles); a NULL/short ws on the A6 path just disables its split.  The routing and the split plan
+ *   are pure functions of (M, K, N, bits, group), so fq_gemm_workspace_bytes is exact for a call.
  * ------------------------------------------------------------------------------------------- */
 size_t fq_gemm_workspace_bytes(int64_t M, const fq_wdesc* d);
 fq_status fq_gemm(const void* A, int32_t adt, int64_t M, const fq_wdesc* d, const void* codes,
