@@ -462,7 +462,10 @@ def measure_extras(fq, dev, peaks):
                     tt = timeit(lambda: fq.gemm(A, q), 3)
                     out[f"prefill_int{bits}_{name}_M{M}"] = {
                         "ms": round(tt * 1e3, 3), "TFLOP_s": round(fl / tt / 1e12, 1),
-                        "frac_bf16_peak": round(fl / tt / 1e12 / peaks["bf16_tflops"], 3)}
+                        "frac_bf16_peak": round(fl / tt / 1e12 / peaks["bf16_tflops"], 3),
+                        # the sustained (power-capped, back-to-back) bf16 figure, when measured
+                        "frac_bf16_sustained": (round(fl / tt / 1e12 / peaks["bf16_tflops_sustained"], 3)
+                                                if peaks.get("bf16_tflops_sustained") else None)}
                 if M == 2048:
                     tb = timeit(lambda: torch.matmul(A, W.t()), 3)
                     out[f"torch_matmul_bf16_{name}_M{M}"] = {"ms": round(tb * 1e3, 3),
