@@ -115,16 +115,26 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------ CPU oracle
-def cpu_oracle_sample(target_s: float = 10.0):
-    """Time the oracle (as it stands) on a bounded column sample of the same sweep.
+def nproc() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_oracle_sample(target_s: float = 10.0, bits: int = 4, group: int = 128):
+    """Time the oracle (as it stands) on a bounded column sample of the same sweep, its BLAS
+    threaded over every host core (nproc).
     Returns (TB/s-equivalent of effective weight bytes, seconds, threads, description)."""
     from oracle import fq_oracle as O
     from synth import activations_bits, gaussian_bits
+    threads = nproc()
     try:
-        from threadpoolctl import threadpool_info
-        threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(threads)
     except Exception:
-        threads = os.cpu_count()
+        pass
+    BITS, GROUP = bits, group
     cols = 256
     prep = []
     for (K, N), seed in ((FC1, 1), (FC2, 2)):
@@ -160,11 +170,12 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    v, dt, threads, desc = cpu_oracle_sample(target_s=max(2.0, 10.0 / max(1, args.steps)))
+    v, dt, threads, desc = cpu_oracle_sample(target_s=max(2.0, 10.0 / max(1, args.steps)), bits=args.bits,
+                                             group=args.group)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "opt175b_decode_fc1_fc2_int4_g128_sweep_M1-16", "sample": desc},
+            "config": {"workload": f"opt175b_decode_fc1_fc2_int{BITS}_g{GROUP}_sweep_M1-16", "sample": desc},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -179,7 +190,16 @@ def main():
     ap.add_argument("--impl", default="fq", choices=["fq", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
+    # SURVEY §5 knobs: headline GEMM precision / group; adaptive parameters of the MoE extras
+    ap.add_argument("--bits", type=int, default=4, choices=[4, 8])
+    ap.add_argument("--group", type=int, default=128)
+    ap.add_argument("--alpha", type=int, default=500, help="adaptive alpha in thousandths (MoE extras)")
+    ap.add_argument("--min-group", type=int, default=16, help="adaptive minimum group (MoE extras)")
+    ap.add_argument("--seed", type=int, default=1000, help="base seed of the synthetic weights")
     args = ap.parse_args()
+    global BITS, GROUP, METRIC
+    BITS, GROUP = args.bits, args.group
+    METRIC = (f"int{BITS}xbf16 decode GEMM effective weight TB/s (OPT-175B FC1+FC2, M=1..16 sweep, g={GROUP})")
     if args.impl == "reference":
         return run_reference(args)
 
@@ -215,10 +235,10 @@ def main():
     c0, c1 = shard_bounds(FC1[1], t, rank)
     r0, r1 = shard_bounds(FC2[0], t, rank, 32)
     check_row_group(FC2[0], t, GROUP)
-    W1 = gaussian_torch((FC1[1], FC1[0]), 0.02, 1001, device=dev)
+    W1 = gaussian_torch((FC1[1], FC1[0]), 0.02, args.seed + 1, device=dev)
     q1 = fq.quantize(W1[c0:c1].contiguous(), BITS, GROUP)
     del W1
-    W2 = gaussian_torch((FC2[1], FC2[0]), 0.02, 1002, device=dev)
+    W2 = gaussian_torch((FC2[1], FC2[0]), 0.02, args.seed + 2, device=dev)
     q2 = fq.quantize(W2[:, r0:r1].contiguous(), BITS, GROUP)
     del W2
     torch.cuda.synchronize()
@@ -383,12 +403,12 @@ def main():
         del xs, ys, zs
         q1 = q2 = None
         torch.cuda.empty_cache()
-        extras = measure_extras(fq, dev, peaks)
+        extras = measure_extras(fq, dev, peaks, args)
 
     line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "opt175b_decode_fc1_fc2_int4_g128_sweep_M1-16",
+            "config": {"workload": f"opt175b_decode_fc1_fc2_int{BITS}_g{GROUP}_sweep_M1-16",
                        "shapes": {"FC1": {"K": FC1[0], "N": FC1[1]}, "FC2": {"K": FC2[0], "N": FC2[1]}},
                        "M": list(M_SWEEP), "bits": BITS, "group": GROUP,
                        "l2": "inputs larger than L2 (2 x 311 MB packed weights at N=1), no flush",
@@ -399,7 +419,7 @@ def main():
     if extras:
         line["extras"] = extras
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, dt, threads, desc = cpu_oracle_sample(10.0)
+        v, dt, threads, desc = cpu_oracle_sample(10.0, BITS, GROUP)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc,
                                 "seconds": round(dt, 2)}
     if rank == 0:
@@ -409,7 +429,7 @@ def main():
     return 0
 
 
-def measure_extras(fq, dev, peaks):
+def measure_extras(fq, dev, peaks, args):
     """Secondary paths reported next to the headline (rank 0, N=1): int8 decode, the tcgen05
     prefill GEMM (configs[2]) against torch.matmul bf16, the quantizer and adaptive pass, and the
     MoE expert batch (configs[3])."""
@@ -485,7 +505,7 @@ def measure_extras(fq, dev, peaks):
         W = gaussian_torch((N, K), 0.01 if e % 4 == 0 else 0.02, 7000 + e, device=dev)
         if e % 4 == 0:
             W[e % N, (37 * e) % K] = 1.0
-        experts.append(fq.quantize(W, 4, None, alpha_milli=500, min_group=16))
+        experts.append(fq.quantize(W, 4, None, alpha_milli=args.alpha, min_group=args.min_group))
         del W
     torch.cuda.empty_cache()
     gh = {}

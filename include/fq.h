@@ -26,8 +26,11 @@
  *    dependent conditions the host cannot see (non-finite W, fp16 scale overflow) are reported
  *    through the optional device status word (bit 0: non-finite input in a group, bit 1: scale
  *    overflow); affected groups get scale 0 and codes 0.  No C++ exception crosses the ABI.
- *  Thread safety.  All functions are re-entrant; the only global state is a lazily cached
- *    device-properties struct.
+ *  Thread safety.  All functions are re-entrant and thread-safe.  Process-wide state, all of it
+ *    caches of pure functions: the SM count per device (atomics), a per-device "dynamic shared
+ *    memory attribute applied" bit per kernel (atomics), and a 256-entry cache of encoded TMA
+ *    descriptors keyed by every encoding argument (mutex-protected).  Nothing is read from the
+ *    process environment: routing is a pure function of the arguments (and fq_gemm_opts).
  */
 #ifndef FQ_H_
 #define FQ_H_
@@ -101,6 +104,41 @@ fq_status fq_adapt_flags(const void* W, int32_t wdt, int64_t K, int64_t N, uint3
 int32_t fq_adapt_decide(int64_t K, int32_t min_group, const int32_t* flags_host);
 
 /* ---------------------------------------------------------------------------------------------
+ * Row-parallel (K-sharded) tensor parallelism, SURVEY §8(c) C-T / §8(e).  The paper serves OPT with
+ * tensor parallelism, "an all reduce after each attention and FFN block" (§2.1); out-proj and
+ * FC2 are row-parallel, so rank r of `world` holds W_r = W[:, r*K/world : (r+1)*K/world] ([N, K/world]
+ * row-major).  One g per matrix (R11) is decided on the FULL-K ladder (P:149 starts from the whole
+ * column), and the codes/scales of every shard must be the K-/G-slices of the unsharded result.
+ * world must be a power of two <= 64 with K/world on the ladder of (K, min_group) (K/world % 16 == 0).
+ * Protocol (every rank; "MAX" = an all-reduce MAX across the ranks of the matrix):
+ *   1. zero flags_dev [fq_adapt_levels(K, min_group) - 1] and colmax_dev [world * N] (fp32);
+ *   2. fq_adapt_flags_rowshard(W_r, ...): OR-s the flags of every level whose parent group lies in
+ *      one shard (group <= K/(2 world)) and writes colmax_dev[r*N + n] = max|W_r[n, :]| (+inf if
+ *      W_r[n, :] holds a non-finite value);
+ *   3. MAX over ranks of flags_dev and colmax_dev (non-negative fp32 order like their int32 bits, so
+ *      one int32 MAX all-reduce of both serves);
+ *   4. fq_adapt_flags_cross(colmax_dev, ...): OR-s the flags of the coarse levels 1 .. log2(world)
+ *      (groups spanning shards) -- identical on every rank, no further exchange;
+ *   5. g = fq_adapt_decide(K, min_group, flags copied to the host);
+ *   6. fq_quantize_rowshard(W_r, ..., g, colmax_dev): the shard's codes [N, (K/world)*bits/8] and
+ *      scales [Gs, N], Gs = (K/world)/g when g <= K/world (plain fq_quantize of the shard), else
+ *      Gs = 1: the one scale row of the group holding the shard, from the group's amax =
+ *      max of colmax_dev over the shards of that group.  The shard's fq_wdesc for fq_gemm is then
+ *      { K/world, N, bits, min(g, K/world), scale_dtype }.
+ * For a fixed group > K/world (e.g. per-column) run steps 1-3 with flags_dev = NULL.
+ * ------------------------------------------------------------------------------------------- */
+fq_status fq_adapt_flags_rowshard(const void* W_shard, int32_t wdt, int64_t K, int64_t N, int32_t world,
+                                  int32_t rank, uint32_t alpha_milli, int32_t min_group, int32_t* flags_dev,
+                                  float* colmax_dev, int32_t* status_dev, void* stream);
+fq_status fq_adapt_flags_cross(const float* colmax_dev, int64_t K, int64_t N, int32_t world,
+                               uint32_t alpha_milli, int32_t min_group, int32_t* flags_dev, void* stream);
+/* d describes the FULL matrix (K, N, bits, group = g, scale dtype); colmax_dev may be NULL when
+ * d->group <= K/world. */
+fq_status fq_quantize_rowshard(const void* W_shard, int32_t wdt, const fq_wdesc* d, int32_t world, int32_t rank,
+                               const float* colmax_dev, void* codes, void* scales, int32_t* status_dev,
+                               void* stream);
+
+/* ---------------------------------------------------------------------------------------------
  * Quantize + pack (kernel A3), App. A with groups.  One CTA holds a K-slice
  * of whole groups of one column in registers, so group <= 65536 for 16-bit W and <= 32768 for
  * fp32 W (any K otherwise), else FQ_ERR_SHAPE.
@@ -137,6 +175,22 @@ fq_status fq_gemm(const void* A, int32_t adt, int64_t M, const fq_wdesc* d, cons
                   const void* scales, void* C, int32_t cdt, void* ws, size_t ws_bytes,
                   void* stream);
 
+/* Routing / plan overrides (tests, measurements).  Zero-initialised = fq_gemm's own plan. */
+typedef enum { FQ_PATH_AUTO = 0, FQ_PATH_DECODE = 1, FQ_PATH_TC = 2 } fq_path;
+typedef struct {
+  int32_t path;       /* fq_path: A4 decode kernel (any M: token tiles of <= 16/32 re-stream W) or A6 */
+  int32_t splits;     /* > 0: split-K factor (A4: K ranges of whole stage pairs; A6: item count) */
+  int32_t tc_halves;  /* A6, tiles of <= 128 tokens: 1 or 2 halves of 128 weight rows per tile */
+  int32_t tc_dqg;     /* A6, 16 dequant warps: 1, or 2 groups on alternate K blocks (int4 only) */
+  int32_t reserved[4];/* must be 0 */
+} fq_gemm_opts;
+/* As fq_gemm / fq_gemm_workspace_bytes with explicit overrides (opts NULL = all zero).  Invalid
+ * override values are FQ_ERR_INVALID_ARG. */
+size_t fq_gemm_workspace_bytes_ex(int64_t M, const fq_wdesc* d, const fq_gemm_opts* opts);
+fq_status fq_gemm_ex(const void* A, int32_t adt, int64_t M, const fq_wdesc* d, const void* codes,
+                     const void* scales, void* C, int32_t cdt, void* ws, size_t ws_bytes, void* stream,
+                     const fq_gemm_opts* opts);
+
 /* ---------------------------------------------------------------------------------------------
  * MoE expert batch (kernel A7).  E experts share K, N, bits and scale dtype (d->group ignored);
  * each expert has its own group size (adaptive per expert, "different model weight
@@ -148,7 +202,8 @@ fq_status fq_gemm(const void* A, int32_t adt, int64_t M, const fq_wdesc* d, cons
  * on the int4 nibble path) run in one launch per kernel class of the decode kernel (A4, batched);
  * larger experts run the tcgen05 kernel (A6); empty experts launch nothing (T == 0: A and C may be
  * NULL, FQ_OK).  ws: fq_gemm_grouped_workspace_bytes(...) bytes, zero-filled once (same
- * contract as fq_gemm's ws); FQ_ERR_WORKSPACE if too small while decode experts are present.
+ * contract as fq_gemm's ws); FQ_ERR_WORKSPACE if too small while decode experts are present --
+ * checked, like every other argument, before the first launch.
  * ------------------------------------------------------------------------------------------- */
 size_t fq_gemm_grouped_workspace_bytes(int64_t T, int32_t E, const fq_wdesc* d);
 fq_status fq_gemm_grouped(const void* A, int32_t adt, int64_t T, const int64_t* offsets_host,

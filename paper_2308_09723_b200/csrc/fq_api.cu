@@ -1,10 +1,10 @@
 // fq_api.cu — the C ABI (include/fq.h): argument validation, sizing, dispatch to the kernels.
-// No compute happens here; every step of the hot path runs in the sm_100a kernels.
+// No compute happens here; every step of the hot path runs in the sm_100a kernels.  Every
+// argument (including workspace sizes) is validated before the first launch of a call.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <atomic>
-#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -14,19 +14,15 @@
 namespace fq {
 
 int num_sms() {
-  static std::atomic<int> cached{0};
-  int v = cached.load();
-  if (v) return v;
+  static std::atomic<int> cached[64];
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) return 148;
+  std::atomic<int>& c = cached[dev & 63];
+  int v = c.load(std::memory_order_relaxed);
+  if (v) return v;
   if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
-  cached.store(v);
+  c.store(v, std::memory_order_relaxed);
   return v;
-}
-
-bool pdl_enabled() {
-  const char* e = std::getenv("FQ_PDL");
-  return !(e && e[0] == '0');
 }
 
 static bool valid_dtype(int d) { return d == FQ_BF16 || d == FQ_FP16 || d == FQ_FP32; }
@@ -42,25 +38,55 @@ static fq_status check_wdesc(const fq_wdesc* d) {
   return FQ_OK;
 }
 
+static fq_status to_tune(const fq_gemm_opts* o, Tune& t) {
+  t = Tune{};
+  if (!o) return FQ_OK;
+  for (int i = 0; i < 4; ++i)
+    if (o->reserved[i]) return FQ_ERR_INVALID_ARG;
+  if (o->path < 0 || o->path > 2 || o->splits < 0 || o->splits > 4096 || o->tc_halves < 0 || o->tc_halves > 2 ||
+      o->tc_dqg < 0 || o->tc_dqg > 2)
+    return FQ_ERR_INVALID_ARG;
+  t.path = o->path;
+  t.splits = o->splits;
+  t.hm = o->tc_halves;
+  t.dqg = o->tc_dqg;
+  return FQ_OK;
+}
+
 static cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 static fq_status from_cuda(cudaError_t e) { return e == cudaSuccess ? FQ_OK : FQ_ERR_CUDA; }
 
 // M <= 16 (32 on the int4 nibble path): memory-bound decode kernel (A4/A5), every weight streamed
-// once; larger M: tcgen05 tensor-core kernel (A6).  FQ_GEMM_PATH=decode|tc forces a path (tests and
-// A/B measurements).
+// once; larger M: tcgen05 tensor-core kernel (A6).  Tune::path forces a path (tests, A/B).
 // A single GEMM (N > 0) of 17..32 tokens on the int4 nibble path goes to A6 when A6's 128-row tiles
 // do not fill the SMs (A6 then splits K, or uses two-half tiles): measured at M = 17 / 24 / 32
 // (profiles/r01/a6_two_half_tiles.txt) OPT-13B attn-out 34-44 -> 24 us, QKV 42-46 -> 36, FFN2
 // 56-69 -> 47-48, OPT-30B attn-out 40-50 -> 32, OPT-175B FC2 146 -> 131 (M = 32); matrices with
 // >= 148 tiles (OPT-175B FC1, OPT-13B FFN1, OPT-30B QKV / FFN1) stay on the decode kernel.
-static bool use_tc_path(int64_t M, int bits, int group, int64_t N = 0) {
-  const char* e = std::getenv("FQ_GEMM_PATH");
-  if (e && std::strcmp(e, "decode") == 0) return false;
-  if (e && std::strcmp(e, "tc") == 0) return true;
+static bool use_tc_path(int64_t M, int bits, int group, int64_t N, const Tune& t) {
+  if (t.path == 1) return false;
+  if (t.path == 2) return true;
   const int dmax = gemv_max_m(bits, group);
   if (M > dmax) return true;
   return M > 16 && N > 0 && tc_short_of_tiles((int)M, (int)N);
+}
+
+static int ilog2_exact(int64_t x) {  // log2 of a power of two, else -1
+  if (x <= 0 || (x & (x - 1))) return -1;
+  int l = 0;
+  while ((1ll << l) < x) ++l;
+  return l;
+}
+
+// Row-shard geometry check: world a power of two <= 64 whose K-slices sit on the (K, min_group)
+// ladder.  Returns log2(world) or -1.
+static int rowshard_levels(int64_t K, int32_t world, int32_t min_group) {
+  const int lw = ilog2_exact(world);
+  if (lw < 0 || world > 64) return -1;
+  const int32_t nlev = fq_adapt_levels(K, min_group);
+  if (nlev <= lw) return -1;  // K/world is not a ladder level
+  return lw;
 }
 
 }  // namespace fq
@@ -69,7 +95,7 @@ using namespace fq;
 
 extern "C" {
 
-const char* fq_version(void) { return "fq 0.1.0 (sm_100a)"; }
+const char* fq_version(void) { return "fq 0.2.0 (sm_100a)"; }
 
 const char* fq_status_str(fq_status s) {
   switch (s) {
@@ -132,8 +158,39 @@ fq_status fq_adapt_flags(const void* W, int32_t wdt, int64_t K, int64_t N, uint3
   const int gfin = (int)(K >> (nlev - 1));
   if (gfin % 8) return FQ_ERR_SHAPE;
   if (nlev == 1) return FQ_OK;  // nothing to test
-  return from_cuda(run_adapt_flags(wdt, W, (int)K, (int)N, nlev, gfin, alpha_milli, flags_dev,
+  return from_cuda(run_adapt_flags(wdt, W, (int)K, (int)N, nlev, gfin, alpha_milli, flags_dev, 0, nullptr,
                                    status_dev, as_stream(stream)));
+}
+
+fq_status fq_adapt_flags_rowshard(const void* W_shard, int32_t wdt, int64_t K, int64_t N, int32_t world,
+                                  int32_t rank, uint32_t alpha_milli, int32_t min_group, int32_t* flags_dev,
+                                  float* colmax_dev, int32_t* status_dev, void* stream) {
+  if (!W_shard || !colmax_dev || !valid_dtype(wdt)) return FQ_ERR_INVALID_ARG;
+  if (alpha_milli < 1 || alpha_milli > 1000 || min_group < 16) return FQ_ERR_INVALID_ARG;
+  if (K <= 0 || N <= 0 || K % 32 || K > (1 << 20) || N > (1 << 24)) return FQ_ERR_SHAPE;
+  if (rank < 0 || rank >= world) return FQ_ERR_INVALID_ARG;
+  const int lw = rowshard_levels(K, world, min_group);
+  if (lw < 0) return FQ_ERR_SHAPE;
+  const int64_t Ks = K / world;
+  if (Ks % 32) return FQ_ERR_SHAPE;
+  // the shard's own ladder (from K/world) is the tail of the full ladder, shifted by log2(world)
+  const int32_t nlev_s = fq_adapt_levels(Ks, min_group);
+  if (nlev_s <= 0 || nlev_s > 16 || fq_adapt_levels(K, min_group) != nlev_s + lw) return FQ_ERR_SHAPE;
+  const int gfin = (int)(Ks >> (nlev_s - 1));
+  if (gfin % 8) return FQ_ERR_SHAPE;
+  return from_cuda(run_adapt_flags(wdt, W_shard, (int)Ks, (int)N, nlev_s, gfin, alpha_milli, flags_dev, lw,
+                                   colmax_dev + (size_t)rank * N, status_dev, as_stream(stream)));
+}
+
+fq_status fq_adapt_flags_cross(const float* colmax_dev, int64_t K, int64_t N, int32_t world,
+                               uint32_t alpha_milli, int32_t min_group, int32_t* flags_dev, void* stream) {
+  if (!colmax_dev || !flags_dev) return FQ_ERR_INVALID_ARG;
+  if (alpha_milli < 1 || alpha_milli > 1000 || min_group < 16) return FQ_ERR_INVALID_ARG;
+  if (K <= 0 || N <= 0 || K % 32 || K > (1 << 20) || N > (1 << 24)) return FQ_ERR_SHAPE;
+  const int lw = rowshard_levels(K, world, min_group);
+  if (lw < 0) return FQ_ERR_SHAPE;
+  if (lw == 0) return FQ_OK;  // one shard: no level spans shards
+  return from_cuda(run_adapt_cross(colmax_dev, world, (int)N, lw, alpha_milli, flags_dev, as_stream(stream)));
 }
 
 fq_status fq_quantize(const void* W, int32_t wdt, const fq_wdesc* d, void* codes, void* scales,
@@ -148,20 +205,55 @@ fq_status fq_quantize(const void* W, int32_t wdt, const fq_wdesc* d, void* codes
                                 codes, scales, status_dev, as_stream(stream)));
 }
 
-size_t fq_gemm_workspace_bytes(int64_t M, const fq_wdesc* d) {
-  if (check_wdesc(d) != FQ_OK || M <= 0) return 0;
-  if (use_tc_path(M, d->bits, d->group, d->N)) return gemm_tc_workspace_bytes((int)M, (int)d->K, (int)d->N, d->bits);
-  if (decode_tc_supported(d->bits, d->group, (int)M))
-    return dtc_workspace_bytes(M, (int)d->K, num_sms());
-  const GemvPlan p = plan_gemv((int)M, (int)d->K, (int)d->N, d->bits, d->group, num_sms());
+fq_status fq_quantize_rowshard(const void* W_shard, int32_t wdt, const fq_wdesc* d, int32_t world, int32_t rank,
+                               const float* colmax_dev, void* codes, void* scales, int32_t* status_dev,
+                               void* stream) {
+  fq_status s = check_wdesc(d);
+  if (s != FQ_OK) return s;
+  if (!W_shard || !codes || !scales || !valid_dtype(wdt)) return FQ_ERR_INVALID_ARG;
+  if (rank < 0 || world <= 0 || rank >= world || world > 64 || ilog2_exact(world) < 0) return FQ_ERR_INVALID_ARG;
+  if (d->K % world) return FQ_ERR_SHAPE;
+  const int64_t Ks = d->K / world;
+  if (Ks % 32) return FQ_ERR_SHAPE;
+  const int64_t gs = std::min<int64_t>(d->group, Ks);
+  if (d->group <= Ks) {
+    if (Ks % d->group) return FQ_ERR_SHAPE;
+  } else if (d->group % Ks) {
+    return FQ_ERR_SHAPE;
+  }
+  if (gs > (wdt == FQ_FP32 ? 32768 : 65536)) return FQ_ERR_SHAPE;
+  if (d->group <= Ks)  // whole groups inside the shard: the plain quantizer on the K-slice
+    return from_cuda(run_quantize(wdt, d->scale_dtype, d->bits, W_shard, (int)Ks, (int)d->N, (int)gs, codes,
+                                  scales, status_dev, as_stream(stream)));
+  if (!colmax_dev) return FQ_ERR_INVALID_ARG;
+  const int span = (int)(d->group / Ks);  // shards per group
+  const int r0 = rank / span * span;
+  return from_cuda(run_quantize(wdt, d->scale_dtype, d->bits, W_shard, (int)Ks, (int)d->N, (int)gs, codes, scales,
+                                status_dev, as_stream(stream), colmax_dev, r0, span));
+}
+
+static size_t gemm_ws_bytes(int64_t M, const fq_wdesc* d, const Tune& t) {
+  if (use_tc_path(M, d->bits, d->group, d->N, t))
+    return gemm_tc_workspace_bytes((int)M, (int)d->K, (int)d->N, d->bits, t);
+  const GemvPlan p = plan_gemv((int)M, (int)d->K, (int)d->N, d->bits, d->group, num_sms(), t.splits);
   return gemv_workspace_bytes(p, (int)M, (int)d->K, (int)d->N, d->bits, d->group);
 }
 
-fq_status fq_gemm(const void* A, int32_t adt, int64_t M, const fq_wdesc* d, const void* codes,
-                  const void* scales, void* C, int32_t cdt, void* ws, size_t ws_bytes,
-                  void* stream) {
+size_t fq_gemm_workspace_bytes_ex(int64_t M, const fq_wdesc* d, const fq_gemm_opts* opts) {
+  Tune t;
+  if (check_wdesc(d) != FQ_OK || M <= 0 || to_tune(opts, t) != FQ_OK) return 0;
+  return gemm_ws_bytes(M, d, t);
+}
+
+size_t fq_gemm_workspace_bytes(int64_t M, const fq_wdesc* d) { return fq_gemm_workspace_bytes_ex(M, d, nullptr); }
+
+fq_status fq_gemm_ex(const void* A, int32_t adt, int64_t M, const fq_wdesc* d, const void* codes,
+                     const void* scales, void* C, int32_t cdt, void* ws, size_t ws_bytes, void* stream,
+                     const fq_gemm_opts* opts) {
   fq_status s = check_wdesc(d);
   if (s != FQ_OK) return s;
+  Tune t;
+  if ((s = to_tune(opts, t)) != FQ_OK) return s;
   if (!valid_half(adt)) return FQ_ERR_INVALID_ARG;
   if (d->scale_dtype != adt) return FQ_ERR_UNSUPPORTED;
   if (cdt != adt && cdt != FQ_FP32) return FQ_ERR_UNSUPPORTED;
@@ -169,29 +261,28 @@ fq_status fq_gemm(const void* A, int32_t adt, int64_t M, const fq_wdesc* d, cons
   if (!codes || !scales) return FQ_ERR_INVALID_ARG;
   if (M == 0) return FQ_OK;  // empty batch (A and C may be NULL): nothing to compute, nothing launched
   if (!A || !C) return FQ_ERR_INVALID_ARG;
-  if (use_tc_path(M, d->bits, d->group, d->N))
-    return from_cuda(run_gemm_tc(adt, cdt, d->bits, A, (int)M, (int)d->K, (int)d->N, codes, scales,
-                                 d->group, C, ws, ws_bytes, as_stream(stream)));
-  if (decode_tc_supported(d->bits, d->group, (int)M)) {
-    const size_t need = dtc_workspace_bytes(M, (int)d->K, num_sms());
-    if (need > 65536 && (!ws || ws_bytes < need)) return FQ_ERR_WORKSPACE;
-    return from_cuda(run_decode_tc(adt, cdt, d->bits, A, (int)M, (int)d->K, (int)d->N, codes, scales,
-                                   d->group, C, ws, as_stream(stream)));
-  }
-  const GemvPlan p = plan_gemv((int)M, (int)d->K, (int)d->N, d->bits, d->group, num_sms());
+  if (use_tc_path(M, d->bits, d->group, d->N, t))
+    return from_cuda(run_gemm_tc(adt, cdt, d->bits, A, (int)M, (int)d->K, (int)d->N, codes, scales, d->group, C,
+                                 ws, ws_bytes, as_stream(stream), t));
+  const GemvPlan p = plan_gemv((int)M, (int)d->K, (int)d->N, d->bits, d->group, num_sms(), t.splits);
   const size_t need = gemv_workspace_bytes(p, (int)M, (int)d->K, (int)d->N, d->bits, d->group);
   if (need > 65536 && (!ws || ws_bytes < need)) return FQ_ERR_WORKSPACE;  // counters-only: may be NULL
   return from_cuda(run_gemv(p, adt, cdt, d->bits, A, (int)M, (int)d->K, (int)d->N, codes, scales,
                             d->group, C, ws, as_stream(stream)));
 }
 
+fq_status fq_gemm(const void* A, int32_t adt, int64_t M, const fq_wdesc* d, const void* codes,
+                  const void* scales, void* C, int32_t cdt, void* ws, size_t ws_bytes,
+                  void* stream) {
+  return fq_gemm_ex(A, adt, M, d, codes, scales, C, cdt, ws, ws_bytes, stream, nullptr);
+}
+
 size_t fq_gemm_grouped_workspace_bytes(int64_t T, int32_t E, const fq_wdesc* d) {
   (void)E;
   if (check_wdesc(d) != FQ_OK || T < 0) return 0;
-  // tcgen05 decode experts: counters + per-CTA stream-K partials; mma.sync decode experts:
-  // counters + the pre-converted activations of all T tokens (shared region, stream-ordered)
-  return std::max(dtc_workspace_bytes(T, (int)d->K, num_sms()),
-                  gemv_grouped_workspace_bytes(T, (int)d->K, d->bits));
+  // decode experts: counters + the pre-converted activations of all T tokens (shared region,
+  // stream-ordered)
+  return gemv_grouped_workspace_bytes(T, (int)d->K, d->bits);
 }
 
 fq_status fq_gemm_grouped(const void* A, int32_t adt, int64_t T, const int64_t* offsets_host,
@@ -203,8 +294,6 @@ fq_status fq_gemm_grouped(const void* A, int32_t adt, int64_t T, const int64_t* 
   if (T > 0 && (!A || !C)) return FQ_ERR_INVALID_ARG;  // T == 0: A and C may be NULL
   if (!valid_half(adt) || d->scale_dtype != adt || (cdt != adt && cdt != FQ_FP32)) return FQ_ERR_UNSUPPORTED;
   if (offsets_host[0] != 0 || offsets_host[E] != T || T < 0) return FQ_ERR_SHAPE;
-  std::vector<int> small;
-  small.reserve(E);
   for (int32_t e = 0; e < E; ++e) {
     fq_wdesc de = *d;
     de.group = groups_host[e];
@@ -213,38 +302,25 @@ fq_status fq_gemm_grouped(const void* A, int32_t adt, int64_t T, const int64_t* 
     if (offsets_host[e + 1] < offsets_host[e]) return FQ_ERR_SHAPE;
     if (!codes_host[e] || !scales_host[e]) return FQ_ERR_INVALID_ARG;
   }
-  const cudaStream_t st = as_stream(stream);
-  std::vector<int> large;
+  // classify every expert, then validate the workspace of every class, then launch
+  const Tune t{};
+  std::vector<int> small, large;
   for (int32_t e = 0; e < E; ++e) {
     const int64_t Me = offsets_host[e + 1] - offsets_host[e];
     if (Me == 0) continue;
-    (!use_tc_path(Me, d->bits, groups_host[e]) ? small : large).push_back(e);
+    (!use_tc_path(Me, d->bits, groups_host[e], 0, t) ? small : large).push_back(e);
   }
+  if (!small.empty() && (!ws || ws_bytes < gemv_grouped_workspace_bytes(T, (int)d->K, d->bits)))
+    return FQ_ERR_WORKSPACE;
+  const cudaStream_t st = as_stream(stream);
   if (!large.empty()) {  // every large expert in one persistent tcgen05 launch (per <= 48 experts)
     cudaError_t r = run_gemm_tc_grouped(adt, cdt, d->bits, A, (int)d->K, (int)d->N, offsets_host, groups_host,
                                         codes_host, scales_host, C, large.data(), (int)large.size(), st);
     if (r != cudaSuccess) return FQ_ERR_CUDA;
   }
-  // small experts: tcgen05 decode kernel where the group allows, mma.sync kernel otherwise
-  std::vector<int> small_tc, small_mma;
-  for (int e : small)
-    (decode_tc_supported(d->bits, groups_host[e], (int)(offsets_host[e + 1] - offsets_host[e])) ? small_tc
-                                                                                                 : small_mma)
-        .push_back(e);
-  if (!small_tc.empty()) {
-    if (!ws || ws_bytes < dtc_workspace_bytes(T, (int)d->K, num_sms()))
-      return FQ_ERR_WORKSPACE;
-    cudaError_t r = run_decode_tc_grouped(adt, cdt, d->bits, A, (int)d->K, (int)d->N, offsets_host, groups_host,
-                                          codes_host, scales_host, C, ws, T, small_tc.data(), (int)small_tc.size(),
-                                          st);
-    if (r != cudaSuccess) return FQ_ERR_CUDA;
-  }
-  if (!small_mma.empty() && (!ws || ws_bytes < gemv_grouped_workspace_bytes(T, (int)d->K, d->bits)))
-    return FQ_ERR_WORKSPACE;
-  if (!small_mma.empty())
+  if (!small.empty())
     return from_cuda(run_gemv_grouped(adt, cdt, d->bits, A, (int)d->K, (int)d->N, offsets_host, groups_host,
-                                      codes_host, scales_host, C, ws, T, small_mma.data(), (int)small_mma.size(),
-                                      st));
+                                      codes_host, scales_host, C, ws, T, small.data(), (int)small.size(), st));
   return FQ_OK;
 }
 

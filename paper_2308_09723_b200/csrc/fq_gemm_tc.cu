@@ -532,12 +532,8 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
 // ------------------------------------------------------------------------------------- host side
 // K per stage of the kernel variant serving a launch whose widest token tile is bnmax tokens:
 // 128 for the 64/128-token variants (64-byte int4 code rows), 64 for the 256-token variant (its
-// activation tiles leave no room for 128-k stages).  FQ_TC_BK=64 forces the narrow stages.
-static int tc_bk(int bnmax) {
-  static const int forced = std::getenv("FQ_TC_BK") ? std::atoi(std::getenv("FQ_TC_BK")) : 0;
-  if (bnmax > 128 || std::getenv("FQ_TC_BNMAX256")) return 64;
-  return forced == 64 ? 64 : 128;
-}
+// activation tiles leave no room for 128-k stages).
+static int tc_bk(int bnmax) { return bnmax > 128 ? 64 : 128; }
 // 128-row halves per tile (tile = 128 * hm weight rows) for the 64/128-token variants.  Two halves
 // carry twice the code bytes per staged activation tile, which is what bounds the small-M regime;
 // but with half as many tiles a matrix needs more K splits to fill the SMs, and short split items
@@ -547,38 +543,24 @@ static int tc_bk(int bnmax) {
 // M = 48..128: -30..-40%); they lose for OPT-175B FC1 (384 one-half tiles: +7..+16%) and for the
 // OPT-13B/30B matrices (K <= 28672: split items of 5-40 K blocks, up to 1.9x slower).  Rule: two
 // halves for MoE batches, and for a single GEMM when its one-half tiles do not fill the SMs and the
-// two-half split plan keeps >= 64 K blocks (8192 k) per item.  FQ_TC_HM=1|2 overrides (diagnostics).
-static int tc_hm_forced() {  // read per call (tests switch it within one process)
-  const char* e = std::getenv("FQ_TC_HM");
-  return e ? std::atoi(e) : 0;
-}
+// two-half split plan keeps >= 64 K blocks (8192 k) per item.  Tune::hm = 1 | 2 overrides.
 static int tc_bn(int M);
-static int tc_splits_hm(int M, int K, int N, int bits, int hm, int* kbs_out);
+static int tc_splits_hm(int M, int K, int N, int bits, int hm, int* kbs_out, int forced_splits);
 static bool tc_hm_ok(int bnmax) { return bnmax <= 128 && tc_bk(bnmax) == 128; }
 static int tc_hm_batch(int bnmax) {  // MoE batch
-  if (!tc_hm_ok(bnmax)) return 1;
-  const int forced = tc_hm_forced();
-  return (forced == 1 || forced == 2) ? forced : 2;
+  return tc_hm_ok(bnmax) ? 2 : 1;
 }
-static int tc_hm_gemm(int M, int K, int N, int bits) {
+static int tc_hm_gemm(int M, int K, int N, int bits, const Tune& tune) {
   const int bn = tc_bn(M);
   if (!tc_hm_ok(bn)) return 1;
-  const int forced = tc_hm_forced();
-  if (forced == 1 || forced == 2) return forced;
+  if (tune.hm == 1 || tune.hm == 2) return tune.hm;
   const long long tiles1 = (long long)((M + bn - 1) / bn) * ((N + tc::BM - 1) / tc::BM);
   if (tiles1 >= num_sms()) return 1;
   int kbs2 = 0;
-  tc_splits_hm(M, K, N, bits, 2, &kbs2);
+  tc_splits_hm(M, K, N, bits, 2, &kbs2, 0);
   return kbs2 >= 64 ? 2 : 1;
 }
-static int tc_bn(int M) {
-#ifdef FQ_TC_FULLBN
-  (void)M;
-  return tc::BN;  // diagnostics: always 256-token tiles
-#else
-  return std::min(tc::BN, (M + 15) / 16 * 16);
-#endif
-}
+static int tc_bn(int M) { return std::min(tc::BN, (M + 15) / 16 * 16); }
 
 static bool make_tc_prob(tc::TcProb& d, int bits, const void* A, int M, int K, int N, const void* codes,
                          const void* scales, int group, void* C, int cdt, int bk, int hm) {
@@ -597,8 +579,7 @@ static bool make_tc_prob(tc::TcProb& d, int bits, const void* A, int M, int K, i
   d.M = M; d.K = K; d.N = N; d.group = group; d.cdt = cdt;
   d.m_tiles = (M + d.bn - 1) / d.bn;
   d.n_tiles = (N + tc::BM * hm - 1) / (tc::BM * hm);
-  const char* gme = std::getenv("FQ_TC_GM");
-  d.gm = gme ? std::max(1, std::atoi(gme)) : 8;
+  d.gm = 8;
   d.splits = 1;
   d.kbs = (K + bk - 1) / bk;
   d.ws = nullptr;
@@ -612,16 +593,15 @@ static bool make_tc_prob(tc::TcProb& d, int bits, const void* A, int M, int K, i
 // last-round efficiency of the persistent schedule, e.g. OPT-175B FC1 at M <= 64: 192 tiles on
 // 148 SMs (65% in the last round) -> 3 splits (576 items, 97%) for 24% more traffic.
 constexpr size_t kTcCounterBytes = 65536;
-static int tc_splits_hm(int M, int K, int N, int bits, int hm, int* kbs_out) {
+static int tc_splits_hm(int M, int K, int N, int bits, int hm, int* kbs_out, int forced_splits) {
   const int bn = tc_bn(M);
   const int bk = tc_bk(bn);
   const int tiles = ((M + bn - 1) / bn) * ((N + tc::BM * hm - 1) / (tc::BM * hm));
   const int kblocks = (K + bk - 1) / bk;
   const int smax = std::max(1, kblocks / (512 / bk));
-  const char* e = std::getenv("FQ_TC_SPLITS");
   int s;
-  if (e) {
-    s = std::atoi(e);
+  if (forced_splits > 0) {
+    s = forced_splits;
   } else if (hm == 1) {
     s = num_sms() / std::max(1, tiles);
   } else {
@@ -648,14 +628,14 @@ bool tc_short_of_tiles(int M, int N) {
   const int bn = tc_bn(M);
   return (long long)((M + bn - 1) / bn) * ((N + tc::BM - 1) / tc::BM) < num_sms();
 }
-static int tc_splits(int M, int K, int N, int bits, int* kbs_out = nullptr) {
-  return tc_splits_hm(M, K, N, bits, tc_hm_gemm(M, K, N, bits), kbs_out);
+static int tc_splits(int M, int K, int N, int bits, const Tune& tune, int* kbs_out = nullptr) {
+  return tc_splits_hm(M, K, N, bits, tc_hm_gemm(M, K, N, bits, tune), kbs_out, tune.splits);
 }
-size_t gemm_tc_workspace_bytes(int M, int K, int N, int bits) {
-  const int s = tc_splits(M, K, N, bits);
+size_t gemm_tc_workspace_bytes(int M, int K, int N, int bits, const Tune& tune) {
+  const int s = tc_splits(M, K, N, bits, tune);
   if (s == 1) return 256;
   const int bn = tc_bn(M);
-  const int bmt = tc::BM * tc_hm_gemm(M, K, N, bits);
+  const int bmt = tc::BM * tc_hm_gemm(M, K, N, bits, tune);
   const size_t tiles = (size_t)((M + bn - 1) / bn) * ((N + bmt - 1) / bmt);
   return kTcCounterBytes + tiles * s * bn * bmt * sizeof(float);
 }
@@ -664,12 +644,8 @@ template <typename T, int BITS, int MAXP, int BNMAX, int BK, int HM, int DQG>
 static cudaError_t launch_tc(const tc::TcBatch<MAXP>& b, cudaStream_t st) {
   using Gm = tc::Geo<BITS, BNMAX, BK, HM>;
   auto kern = tc::gemm_tc_kernel<T, BITS, MAXP, BNMAX, BK, HM, DQG>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Gm::SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = ensure_smem_attr<tc::gemm_tc_kernel<T, BITS, MAXP, BNMAX, BK, HM, DQG>>(Gm::SMEM);
+  if (e != cudaSuccess) return e;
   const int grid = std::min(b.total_tiles, num_sms());
   kern<<<grid, tc::tc_threads(BNMAX), Gm::SMEM, st>>>(b);
   return cudaGetLastError();
@@ -692,24 +668,23 @@ static cudaError_t dispatch_tc_bn(int adt, int bits, const tc::TcBatch<MAXP>& b,
 // kernel variant = the widest token tile of the launch (64 / 128 / 256 tokens) and the stage K its
 // problems were prepared for
 template <int MAXP>
-static cudaError_t dispatch_tc(int adt, int bits, const tc::TcBatch<MAXP>& b, cudaStream_t st) {
+static cudaError_t dispatch_tc(int adt, int bits, const tc::TcBatch<MAXP>& b, cudaStream_t st, int forced_dqg = 0) {
   int bn = 0;
   for (int i = 0; i < b.nprob; ++i) bn = std::max(bn, b.p[i].bn);
-  if (std::getenv("FQ_TC_BNMAX256")) bn = 256;  // diagnostics: the large-M variant for every M
   const int bk = b.p[0].bk, hm = b.p[0].hm;
   for (int i = 1; i < b.nprob; ++i)
     if (b.p[i].bk != bk || b.p[i].hm != hm) return cudaErrorInvalidValue;
   if (bn > 128) return (bk == 64 && hm == 1) ? dispatch_tc_bn<MAXP, 256, 64>(adt, bits, b, st) : cudaErrorInvalidValue;
   // <= 32-token variant: the small activation tile leaves room for more code stages in flight
-  const bool v32 = bn <= 32 && bk == 128 && !std::getenv("FQ_TC_NO32");
+  const bool v32 = bn <= 32 && bk == 128;
   // Two alternating dequant warp groups (each thread then covers 64 k of a block): measured
   // (profiles/r01/a6_two_half_tiles.txt) OPT-175B FC2 int4 M = 48..128 -8..-12%, FC1 int4 -1.5%,
   // MoE g128 -3%; but +10-13% on MoE batches with 16-element groups (8 scale words per thread) and
-  // +5% on int8 FC1 -> int4 with every group a multiple of 64 only.  FQ_TC_DQG=1|2 overrides.
+  // +5% on int8 FC1 -> int4 with every group a multiple of 64 only.  Tune::dqg = 1 | 2 overrides.
   int dqg = bits == 4 ? 2 : 1;
   for (int i = 0; i < b.nprob; ++i)
     if (b.p[i].group % 64) dqg = 1;
-  if (const char* e = std::getenv("FQ_TC_DQG")) dqg = std::atoi(e) == 2 ? 2 : 1;
+  if (forced_dqg) dqg = forced_dqg == 2 ? 2 : 1;
   if (hm == 2) {
     if (bk != 128) return cudaErrorInvalidValue;
     if (v32) return dispatch_tc_bn<MAXP, 32, 128, 2>(adt, bits, b, st, dqg);
@@ -723,14 +698,16 @@ static cudaError_t dispatch_tc(int adt, int bits, const tc::TcBatch<MAXP>& b, cu
 }
 
 cudaError_t run_gemm_tc(int adt, int cdt, int bits, const void* A, int M, int K, int N, const void* codes,
-                        const void* scales, int group, void* C, void* ws, size_t ws_bytes, cudaStream_t st) {
+                        const void* scales, int group, void* C, void* ws, size_t ws_bytes, cudaStream_t st,
+                        const Tune& tune) {
   tc::TcBatch<1> b{};
   tc::TcProb& d = b.p[0];
-  if (!make_tc_prob(d, bits, A, M, K, N, codes, scales, group, C, cdt, tc_bk(tc_bn(M)), tc_hm_gemm(M, K, N, bits)))
+  if (!make_tc_prob(d, bits, A, M, K, N, codes, scales, group, C, cdt, tc_bk(tc_bn(M)),
+                    tc_hm_gemm(M, K, N, bits, tune)))
     return cudaErrorInvalidValue;
   int kbs = 0;
-  const int s = tc_splits(M, K, N, bits, &kbs);
-  if (s > 1 && ws && ws_bytes >= gemm_tc_workspace_bytes(M, K, N, bits)) {
+  const int s = tc_splits(M, K, N, bits, tune, &kbs);
+  if (s > 1 && ws && ws_bytes >= gemm_tc_workspace_bytes(M, K, N, bits, tune)) {
     d.kbs = kbs;
     d.splits = s;
     d.ctr = reinterpret_cast<int*>(ws);
@@ -739,7 +716,7 @@ cudaError_t run_gemm_tc(int adt, int cdt, int bits, const void* A, int M, int K,
   d.tile_begin = 0;
   b.nprob = 1;
   b.total_tiles = d.m_tiles * d.n_tiles * d.splits;
-  return dispatch_tc<1>(adt, bits, b, st);
+  return dispatch_tc<1>(adt, bits, b, st, tune.dqg);
 }
 
 // MoE: every listed expert (M_e > 16) in one persistent launch per <= 48 experts.

@@ -268,8 +268,9 @@ __device__ __forceinline__ int prow(int m) { return m; }
 // physical 16-byte cell of logical cell c in tile row R under CU_TENSOR_MAP_SWIZZLE_64B
 __device__ __forceinline__ int swz64(int c, int R) { return c ^ ((R >> 1) & 3); }
 
-// DBG (diagnostics only, selected by FQ_DEC_DEBUG for bf16/int4/M<=8; 4 = skeleton streaming codes only): 1 = no MMA (fake FADD
-// accumulate), 2 = no dequant (raw code words as MMA operands), 3 = consumers skip all compute.
+// DBG (diagnostics build -DFQ_DIAG only, selected by FQ_DEC_DEBUG for bf16/int4/M<=8; 4 = skeleton
+// streaming codes only): 1 = no MMA (fake FADD accumulate), 2 = no dequant (raw code words as MMA
+// operands), 3 = consumers skip all compute.  The product build instantiates DBG = 0 only.
 template <typename T, int BITS, int MT, int SACC, int DBG, int MAXP>
 // Register caps (two CTAs per SM fit up to 112 / 96 registers at 288 / 320 threads), set without
 // ptxas's launch_bounds heuristic.
@@ -852,14 +853,10 @@ static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 constexpr int kMaxCounters = 16384;
 constexpr size_t kCounterBytes = kMaxCounters * sizeof(int);
 
-static int env_int(const char* name, int dflt) {
-  const char* v = std::getenv(name);
-  return v ? std::atoi(v) : dflt;
-}
 
 // Group-split nibble path (int4, group 64, single-problem launches): K % 128 == 0 for the prep.
 static bool gs_of(int bits, int group, int K) {
-  return FQ_NIB && bits == 4 && group == 64 && K % 128 == 0 && env_int("FQ_DEC_GS", 1) != 0;
+  return FQ_NIB && bits == 4 && group == 64 && K % 128 == 0;
 }
 static bool nib_of(int bits, int group, int K = -1) {
   return FQ_NIB && bits == 4 && (group % 128 == 0 || (K >= 0 && gs_of(bits, group, K)));
@@ -867,7 +864,7 @@ static bool nib_of(int bits, int group, int K = -1) {
 
 int gemv_max_m(int bits, int group) { return nib_of(bits, group) ? 32 : 16; }
 
-GemvPlan plan_gemv(int M, int K, int N, int bits, int group, int nsm) {
+GemvPlan plan_gemv(int M, int K, int N, int bits, int group, int nsm, int splits_override) {
   (void)group;
   GemvPlan p{};
   p.kchunk = bits == 4 ? 256 : 128;  // split-K granularity (two kernel stages; one stage measured slower on small matrices)
@@ -894,7 +891,7 @@ GemvPlan plan_gemv(int M, int K, int N, int bits, int group, int nsm) {
     const double score = eff - 0.01 * waves - 0.002 * s;
     if (score > best + 1e-9) { best = score; best_s = s; }
   }
-  int s = env_int("FQ_GEMV_SPLITS", best_s);
+  int s = splits_override > 0 ? splits_override : best_s;
   s = std::max(1, std::min(s, nchunks));
   if ((long long)gx * p.ktiles > kMaxCounters) s = 1;  // counter region is fixed-size
   p.klen = ((nchunks + s - 1) / s) * p.kchunk;
@@ -938,25 +935,26 @@ static cudaError_t launch_prep(int adt, const void* A, int ntok, int K, void* Ap
 template <typename T, int BITS, int MT, int SACC, int DBG, int MAXP>
 static cudaError_t launch_dec(const DecBatch<MAXP>& b, int ctas, cudaStream_t st) {
   constexpr int smem = DecStage<BITS, MT, SACC>::SMEM;
-  auto kern = decode_kernel<T, BITS, MT, SACC, DBG, MAXP>;
-  static bool attr_set = false;  // benign race: idempotent attribute call
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  return launch_pdl(kern, ctas, dec_threads<FQ_NIB && BITS == 4 && SACC>(), smem, st, b);
+  cudaError_t e = ensure_smem_attr<decode_kernel<T, BITS, MT, SACC, DBG, MAXP>>(smem);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(decode_kernel<T, BITS, MT, SACC, DBG, MAXP>, ctas, dec_threads<FQ_NIB && BITS == 4 && SACC>(),
+                    smem, st, b);
 }
 
 template <int MAXP>
 static cudaError_t dispatch_dec(int adt, int bits, int mt, int sacc, int dbg, const DecBatch<MAXP>& b,
                                 int ctas, cudaStream_t st) {
+#ifdef FQ_DIAG
+  // diagnostics build only (-DFQ_DIAG, build.build_variant): kernels with parts of the work removed
   if (dbg && adt == FQ_BF16 && bits == 4 && mt == 1 && sacc == 1 && MAXP == 1) {
     if (dbg == 1) return launch_dec<__nv_bfloat16, 4, 1, 1, 1, MAXP>(b, ctas, st);
     if (dbg == 2) return launch_dec<__nv_bfloat16, 4, 1, 1, 2, MAXP>(b, ctas, st);
     if (dbg == 3) return launch_dec<__nv_bfloat16, 4, 1, 1, 3, MAXP>(b, ctas, st);
     if (dbg == 4) return launch_dec<__nv_bfloat16, 4, 1, 1, 4, MAXP>(b, ctas, st);
   }
+#else
+  (void)dbg;
+#endif
 #define FQ_DEC_CASE(TT, BB, MM, SS) \
   if (bits == BB && mt == MM && sacc == SS) return launch_dec<TT, BB, MM, SS, 0, MAXP>(b, ctas, st);
   if (adt == FQ_BF16) {
@@ -1039,7 +1037,13 @@ cudaError_t run_gemv(const GemvPlan& pl, int adt, int cdt, int bits, const void*
   b.p[0].cta_begin = 0;
   b.nprob = 1;
   const int ctas = b.p[0].gx * pl.splits * pl.ktiles;
-  return dispatch_dec<1>(adt, bits, pl.mt, sacc_of(bits, group, K), env_int("FQ_DEC_DEBUG", 0), b, ctas, st);
+#ifdef FQ_DIAG
+  const char* dbg_env = std::getenv("FQ_DEC_DEBUG");
+  const int dbg = dbg_env ? std::atoi(dbg_env) : 0;
+#else
+  const int dbg = 0;
+#endif
+  return dispatch_dec<1>(adt, bits, pl.mt, sacc_of(bits, group, K), dbg, b, ctas, st);
 }
 
 // ---- MoE batch (kernel A7, decode side): experts listed in `experts` (each with 1 <= M_e <= 16)

@@ -3,16 +3,34 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <utility>
 
 namespace fq {
 
-cudaError_t run_quantize(int wdt, int sdt, int bits, const void* W, int K, int N, int group,
-                         void* codes, void* scales, int32_t* status, cudaStream_t st);
-cudaError_t run_adapt_flags(int wdt, const void* W, int K, int N, int nlev, int gfin,
-                            uint32_t alpha, int32_t* flags, int32_t* status, cudaStream_t st);
+// Routing / planning overrides of one GEMM call (fq_gemm_opts of include/fq.h; all 0 = planned).
+// Routing and split plans are pure functions of (shape, Tune): nothing is read from the process
+// environment on the product path.
+struct Tune {
+  int path = 0;    // 0 auto, 1 decode kernel (A4), 2 tcgen05 kernel (A6)
+  int splits = 0;  // 0 planned, else the split-K factor
+  int hm = 0;      // A6: 0 planned, 1 / 2 halves of 128 weight rows per tile
+  int dqg = 0;     // A6: 0 planned, 1 / 2 dequant warp groups
+};
 
-// Decode / tensor-core-fallback GEMM (mma.sync, kernels A4/A5).
+cudaError_t run_quantize(int wdt, int sdt, int bits, const void* W, int K, int N, int group,
+                         void* codes, void* scales, int32_t* status, cudaStream_t st,
+                         const float* amax_tab = nullptr, int tab_r0 = 0, int tab_span = 0);
+// A1 over W [N, K]: flags of ladder levels 1 .. nlev-1 OR-ed into flags[flag_ofs + L - 1]
+// (flags may be NULL); colmax (nullable) receives max|W[n, :]| per row n (+inf if non-finite).
+cudaError_t run_adapt_flags(int wdt, const void* W, int K, int N, int nlev, int gfin,
+                            uint32_t alpha, int32_t* flags, int flag_ofs, float* colmax, int32_t* status,
+                            cudaStream_t st);
+// Coarse adaptive levels of a K-sharded matrix from the [world][N] table of shard column maxima.
+cudaError_t run_adapt_cross(const float* colmax, int world, int N, int nlev_cross, uint32_t alpha,
+                            int32_t* flags, cudaStream_t st);
+
+// Decode GEMM (mma.sync, kernels A4/A5).
 struct GemvPlan {
   int rows_per_cta;   // 128 * RT
   int rt;             // row tiles (16 rows) per warp
@@ -22,7 +40,7 @@ struct GemvPlan {
   int mt;             // 8-token MMA tiles per token tile (1 or 2)
   int klen;           // K elements per split (multiple of kchunk)
 };
-GemvPlan plan_gemv(int M, int K, int N, int bits, int group, int num_sms);
+GemvPlan plan_gemv(int M, int K, int N, int bits, int group, int num_sms, int splits_override = 0);
 // Largest M the decode kernel serves in one pass over the weights (32 on the int4 nibble path, else 16).
 int gemv_max_m(int bits, int group);
 size_t gemv_workspace_bytes(const GemvPlan& p, int M, int K, int N, int bits, int group);
@@ -37,33 +55,37 @@ cudaError_t run_gemv_grouped(int adt, int cdt, int bits, const void* A, int K, i
                              const void* const* scales, void* C, void* ws, int64_t T,
                              const int* experts, int nexp, cudaStream_t st);
 
-// Decode GEMM on tcgen05 (A4, M <= 16, group % 128 == 0; stream-K, kernel in fq_decode_tc.cu).
-// Workspace: 64 KiB counters (zero-filled once, self-resetting) + stream-K partials + the
-// pre-converted activations of `ntok` tokens.
-bool decode_tc_supported(int bits, int group, int M);
-size_t dtc_workspace_bytes(int64_t ntok, int K, int nsm);
-cudaError_t run_decode_tc(int adt, int cdt, int bits, const void* A, int M, int K, int N, const void* codes,
-                          const void* scales, int group, void* C, void* ws, cudaStream_t st);
-cudaError_t run_decode_tc_grouped(int adt, int cdt, int bits, const void* A, int K, int N, const int64_t* offsets,
-                                  const int32_t* groups, const void* const* codes, const void* const* scales,
-                                  void* C, void* ws, int64_t T, const int* experts, int nexp, cudaStream_t st);
-
 // Large-M tensor-core GEMM (tcgen05 + TMEM, kernel A6).
 // Split-K when the output tiles cannot fill the SMs: workspace = 64 KiB counters (zero-filled once,
 // self-resetting) + fp32 partials; without it (ws == NULL or too small) the kernel runs unsplit.
-size_t gemm_tc_workspace_bytes(int M, int K, int N, int bits);
+size_t gemm_tc_workspace_bytes(int M, int K, int N, int bits, const Tune& tune);
 bool tc_short_of_tiles(int M, int N);  // A6's 128-row tiles of this GEMM do not fill the SMs
 cudaError_t run_gemm_tc(int adt, int cdt, int bits, const void* A, int M, int K, int N, const void* codes,
-                        const void* scales, int group, void* C, void* ws, size_t ws_bytes, cudaStream_t st);
+                        const void* scales, int group, void* C, void* ws, size_t ws_bytes, cudaStream_t st,
+                        const Tune& tune);
 cudaError_t run_gemm_tc_grouped(int adt, int cdt, int bits, const void* A, int K, int N, const int64_t* offsets,
                                 const int32_t* groups, const void* const* codes, const void* const* scales,
                                 void* C, const int* experts, int nexp, cudaStream_t st);
 
 int num_sms();
 
-// Launch with the programmatic-stream-serialization attribute (PDL) unless FQ_PDL=0; the kernel
-// must call griddep_wait() before touching memory written by earlier kernels in the stream.
-bool pdl_enabled();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is a per-device-context setting: remember, per
+// kernel instantiation and per device, that it was applied (thread-safe; idempotent on a race).
+template <auto Kern>
+inline cudaError_t ensure_smem_attr(int bytes) {
+  static std::atomic<uint64_t> done{0};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(Kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
+
+// Launch with the programmatic-stream-serialization attribute (PDL); the kernel must call
+// griddep_wait() before touching memory written by earlier kernels in the stream.
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t st,
                               Args&&... args) {
@@ -76,7 +98,7 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int block, size_
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 

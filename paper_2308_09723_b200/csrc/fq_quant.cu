@@ -16,6 +16,8 @@
 // the raw chunks in registers and writes one max|.| per chunk to shared memory; pass 2 reduces
 // chunks to groups and writes the scales; pass 3 turns the register-resident chunks into codes,
 // written coalesced.  HBM traffic = read W once + write codes/scales (the algorithmic minimum).
+#include <algorithm>
+
 #include "fq_common.cuh"
 #include "fq_internal.h"
 
@@ -109,7 +111,9 @@ __global__ void __launch_bounds__(sizeof(TIn) == 4 ? 512 : 1024) quantize_kernel
                                                              int KS, int N, int group,
                                                              uint8_t* __restrict__ codes,
                                                              TS* __restrict__ scales,
-                                                             int32_t* __restrict__ status) {
+                                                             int32_t* __restrict__ status,
+                                                             const float* __restrict__ amax_tab,
+                                                             int tab_r0, int tab_span) {
   extern __shared__ float smem[];
   // CTA = one K-slice of KS elements (a multiple of the group) of one paper column: long columns
   // are split so that every CTA stays small enough for several to share an SM.
@@ -165,7 +169,16 @@ __global__ void __launch_bounds__(sizeof(TIn) == 4 ? 512 : 1024) quantize_kernel
     scales[(size_t)(sl * G + j) * N + n] = s_t;
     if (st) atomicOr(&s_status, st);
   };
-  if (cpg <= 32) {
+  if (amax_tab) {
+    // row-parallel shard of a group that spans several K-shards (TP, group > K/world): the group
+    // amax is the max of the shards' column maxima (table [world][N] after the MAX all-reduce);
+    // the shard holds one group (G == 1).
+    if (threadIdx.x == 0) {
+      float m = 0.f;
+      for (int r = tab_r0; r < tab_r0 + tab_span; ++r) m = fmaxf(m, amax_tab[(size_t)r * N + n]);
+      finish_group(0, m);
+    }
+  } else if (cpg <= 32) {
     for (int j = threadIdx.x; j < G; j += T) {
       float m = 0.f;
       for (int i = 0; i < cpg; ++i) m = fmaxf(m, pm[j * cpg + i]);  // fmaxf keeps +inf
@@ -275,7 +288,8 @@ template <typename TIn>
 __global__ void __launch_bounds__(kQThreads) adapt_flags_kernel(const TIn* __restrict__ W, int K,
                                                                 int N, int nlev, int gfin,
                                                                 uint32_t alpha_milli,
-                                                                int32_t* __restrict__ flags,
+                                                                int32_t* __restrict__ flags, int flag_ofs,
+                                                                float* __restrict__ colmax,
                                                                 int32_t* __restrict__ status) {
   extern __shared__ float smem[];
   const int nchunk = K >> 3;
@@ -321,15 +335,22 @@ __global__ void __launch_bounds__(kQThreads) adapt_flags_kernel(const TIn* __res
     cnt_child = cnt_par;
   }
   if (threadIdx.x == 0 && !isfinite(lev[off_child])) s_status = 1;
+  if (threadIdx.x == 0 && colmax) colmax[n] = lev[off_child];  // level 0: max|W[n, :]| (+inf: non-finite)
   __syncthreads();
-  if (threadIdx.x >= 1 && threadIdx.x < nlev && s_flag[threadIdx.x]) atomicOr(&flags[threadIdx.x - 1], 1);
+  if (flags && threadIdx.x >= 1 && threadIdx.x < nlev && s_flag[threadIdx.x])
+    atomicOr(&flags[flag_ofs + threadIdx.x - 1], 1);
   if (threadIdx.x == 0 && s_status && status) atomicOr(status, 1);
 }
 
 // ------------------------------------------------------------------------------------- launchers
+struct AmaxTab {
+  const float* tab;
+  int r0, span;
+};
+
 template <typename TIn, typename TS, int BITS, int CPT>
 static cudaError_t launch_quant_c(const void* W, int K, int N, int group, void* codes, void* scales,
-                                  int32_t* status, cudaStream_t st, int slice) {
+                                  int32_t* status, cudaStream_t st, int slice, AmaxTab at) {
   // K-slice per CTA: the fewest slices that bring it to <= kQSlice elements (slices are whole
   // groups; a group longer than that, e.g. one scale per column, keeps the whole column).
   const int G = K / group;
@@ -339,8 +360,8 @@ static cudaError_t launch_quant_c(const void* W, int K, int N, int group, void* 
   const int KS = K / nsl;
   const size_t smem = (size_t)(KS / 8 + 2 * (KS / group)) * sizeof(float);
   auto kern = quantize_kernel<TIn, TS, BITS, CPT>;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (smem > 48 * 1024) {  // sized for the largest group the API accepts (65536 elements)
+    cudaError_t e = ensure_smem_attr<quantize_kernel<TIn, TS, BITS, CPT>>((65536 / 8 + 2) * (int)sizeof(float));
     if (e != cudaSuccess) return e;
   }
   // threads: enough that every 8-element chunk is cached in registers (<= kQCpt per thread)
@@ -349,63 +370,106 @@ static cudaError_t launch_quant_c(const void* W, int K, int N, int group, void* 
   threads = threads < 128 ? 128 : threads;
   if (threads > (sizeof(TIn) == 4 ? 512 : 1024)) return cudaErrorInvalidValue;  // rejected by the API
   kern<<<(unsigned)N * nsl, threads, smem, st>>>((const TIn*)W, K, KS, N, group, (uint8_t*)codes, (TS*)scales,
-                                                 status);
+                                                 status, at.tab, at.r0, at.span);
   return cudaGetLastError();
 }
 
 template <typename TIn, typename TS, int BITS>
 static cudaError_t launch_quant(const void* W, int K, int N, int group, void* codes, void* scales,
-                                int32_t* status, cudaStream_t st) {
+                                int32_t* status, cudaStream_t st, AmaxTab at) {
   // measured on B200 (OPT FC1/FC2): 8 chunks per thread and 12288-element slices beat 4 chunks
   // and 4096 / 6144 / 24576-element slices
-  return launch_quant_c<TIn, TS, BITS, kQCpt>(W, K, N, group, codes, scales, status, st, kQSlice);
+  return launch_quant_c<TIn, TS, BITS, kQCpt>(W, K, N, group, codes, scales, status, st, kQSlice, at);
 }
 
 template <typename TIn, typename TS>
 static cudaError_t launch_quant_b(int bits, const void* W, int K, int N, int group, void* codes,
-                                  void* scales, int32_t* status, cudaStream_t st) {
-  return bits == 4 ? launch_quant<TIn, TS, 4>(W, K, N, group, codes, scales, status, st)
-                   : launch_quant<TIn, TS, 8>(W, K, N, group, codes, scales, status, st);
+                                  void* scales, int32_t* status, cudaStream_t st, AmaxTab at) {
+  return bits == 4 ? launch_quant<TIn, TS, 4>(W, K, N, group, codes, scales, status, st, at)
+                   : launch_quant<TIn, TS, 8>(W, K, N, group, codes, scales, status, st, at);
 }
 
 template <typename TIn>
 static cudaError_t launch_quant_s(int sdt, int bits, const void* W, int K, int N, int group,
-                                  void* codes, void* scales, int32_t* status, cudaStream_t st) {
+                                  void* codes, void* scales, int32_t* status, cudaStream_t st, AmaxTab at) {
   return sdt == FQ_BF16
-             ? launch_quant_b<TIn, __nv_bfloat16>(bits, W, K, N, group, codes, scales, status, st)
-             : launch_quant_b<TIn, __half>(bits, W, K, N, group, codes, scales, status, st);
+             ? launch_quant_b<TIn, __nv_bfloat16>(bits, W, K, N, group, codes, scales, status, st, at)
+             : launch_quant_b<TIn, __half>(bits, W, K, N, group, codes, scales, status, st, at);
 }
 
 cudaError_t run_quantize(int wdt, int sdt, int bits, const void* W, int K, int N, int group,
-                         void* codes, void* scales, int32_t* status, cudaStream_t st) {
+                         void* codes, void* scales, int32_t* status, cudaStream_t st,
+                         const float* amax_tab, int tab_r0, int tab_span) {
+  const AmaxTab at{amax_tab, tab_r0, tab_span};
   switch (wdt) {
-    case FQ_BF16: return launch_quant_s<__nv_bfloat16>(sdt, bits, W, K, N, group, codes, scales, status, st);
-    case FQ_FP16: return launch_quant_s<__half>(sdt, bits, W, K, N, group, codes, scales, status, st);
-    default: return launch_quant_s<float>(sdt, bits, W, K, N, group, codes, scales, status, st);
+    case FQ_BF16: return launch_quant_s<__nv_bfloat16>(sdt, bits, W, K, N, group, codes, scales, status, st, at);
+    case FQ_FP16: return launch_quant_s<__half>(sdt, bits, W, K, N, group, codes, scales, status, st, at);
+    default: return launch_quant_s<float>(sdt, bits, W, K, N, group, codes, scales, status, st, at);
   }
 }
 
 template <typename TIn>
 static cudaError_t launch_adapt(const void* W, int K, int N, int nlev, int gfin, uint32_t alpha,
-                                int32_t* flags, int32_t* status, cudaStream_t st) {
+                                int32_t* flags, int flag_ofs, float* colmax, int32_t* status, cudaStream_t st) {
   const int Gf = K / gfin;
   const size_t smem = (size_t)(K / 8 + 2 * Gf) * sizeof(float);
   auto kern = adapt_flags_kernel<TIn>;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (smem > 48 * 1024) {  // sized for the largest K the API accepts (2^20, finest group >= 16)
+    const size_t smax = (size_t)((1 << 20) / 8 + 2 * ((1 << 20) / 16)) * sizeof(float);
+    cudaError_t e = ensure_smem_attr<adapt_flags_kernel<TIn>>((int)std::min<size_t>(smax, 227 * 1024));
     if (e != cudaSuccess) return e;
+    if (smem > 227 * 1024) return cudaErrorInvalidValue;
   }
-  kern<<<N, kQThreads, smem, st>>>((const TIn*)W, K, N, nlev, gfin, alpha, flags, status);
+  kern<<<N, kQThreads, smem, st>>>((const TIn*)W, K, N, nlev, gfin, alpha, flags, flag_ofs, colmax, status);
   return cudaGetLastError();
 }
 
 cudaError_t run_adapt_flags(int wdt, const void* W, int K, int N, int nlev, int gfin,
-                            uint32_t alpha, int32_t* flags, int32_t* status, cudaStream_t st) {
+                            uint32_t alpha, int32_t* flags, int flag_ofs, float* colmax, int32_t* status,
+                            cudaStream_t st) {
   switch (wdt) {
-    case FQ_BF16: return launch_adapt<__nv_bfloat16>(W, K, N, nlev, gfin, alpha, flags, status, st);
-    case FQ_FP16: return launch_adapt<__half>(W, K, N, nlev, gfin, alpha, flags, status, st);
-    default: return launch_adapt<float>(W, K, N, nlev, gfin, alpha, flags, status, st);
+    case FQ_BF16: return launch_adapt<__nv_bfloat16>(W, K, N, nlev, gfin, alpha, flags, flag_ofs, colmax, status, st);
+    case FQ_FP16: return launch_adapt<__half>(W, K, N, nlev, gfin, alpha, flags, flag_ofs, colmax, status, st);
+    default: return launch_adapt<float>(W, K, N, nlev, gfin, alpha, flags, flag_ofs, colmax, status, st);
   }
+}
+
+// ------------------------------------------------------------------------------------- A1 (TP)
+// Coarse levels of a K-sharded matrix (row-parallel TP, world = 2^c equal K-slices): level L
+// (1 <= L <= c, group K / 2^L) has group j covering shards [j * world / 2^L, (j+1) * world / 2^L),
+// so its range is the max of those shards' column maxima.  Same test as A1:
+// 1000 * amax_L(n, j) < alpha_milli * amax_{L-1}(n, j / 2), exact in fp64.
+__global__ void __launch_bounds__(256) adapt_cross_kernel(const float* __restrict__ colmax, int world, int N,
+                                                           int ncross, uint32_t alpha_milli,
+                                                           int32_t* __restrict__ flags) {
+  __shared__ int s_fire[8];
+  if (threadIdx.x < 8) s_fire[threadIdx.x] = 0;
+  __syncthreads();
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n < N) {
+    float tab[64];  // world <= 64 (checked by the API)
+    for (int r = 0; r < world; ++r) tab[r] = colmax[(size_t)r * N + n];
+    // level 0 -> 1 -> ... -> ncross: halve the span of shards per group
+    for (int L = 1; L <= ncross; ++L) {
+      const int span = world >> L;  // shards per child group
+      bool fire = false;
+      for (int j = 0; j < (1 << L); ++j) {
+        float ch = 0.f, pa = 0.f;
+        for (int r = j * span; r < (j + 1) * span; ++r) ch = fmaxf(ch, tab[r]);
+        for (int r = (j >> 1) * 2 * span; r < ((j >> 1) + 1) * 2 * span; ++r) pa = fmaxf(pa, tab[r]);
+        fire |= (1000.0 * (double)ch < (double)alpha_milli * (double)pa);
+      }
+      if (fire) s_fire[L - 1] = 1;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < ncross && s_fire[threadIdx.x]) atomicOr(&flags[threadIdx.x], 1);
+}
+
+cudaError_t run_adapt_cross(const float* colmax, int world, int N, int nlev_cross, uint32_t alpha,
+                            int32_t* flags, cudaStream_t st) {
+  adapt_cross_kernel<<<(N + 255) / 256, 256, 0, st>>>(colmax, world, N, nlev_cross, alpha, flags);
+  return cudaGetLastError();
 }
 
 }  // namespace fq

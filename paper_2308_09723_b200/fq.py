@@ -35,6 +35,21 @@ class fq_wdesc(ctypes.Structure):
                 ("group", ctypes.c_int32), ("scale_dtype", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
+FQ_PATH_AUTO, FQ_PATH_DECODE, FQ_PATH_TC = 0, 1, 2
+
+
+class fq_gemm_opts(ctypes.Structure):
+    """Routing / plan overrides (include/fq.h); all zero = the library's own plan."""
+    _fields_ = [("path", ctypes.c_int32), ("splits", ctypes.c_int32), ("tc_halves", ctypes.c_int32),
+                ("tc_dqg", ctypes.c_int32), ("reserved", ctypes.c_int32 * 4)]
+
+
+def make_opts(path: str | int = 0, splits: int = 0, tc_halves: int = 0, tc_dqg: int = 0) -> fq_gemm_opts:
+    if isinstance(path, str):
+        path = {"auto": FQ_PATH_AUTO, "decode": FQ_PATH_DECODE, "tc": FQ_PATH_TC}[path]
+    return fq_gemm_opts(path, splits, tc_halves, tc_dqg)
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"libfq.so not built ({LIB_PATH}); run __graft_entry__.build() "
@@ -52,9 +67,14 @@ def _load():
         "fq_adapt_group_at": (I32, [I64, I32, I32]),
         "fq_adapt_flags": (c.c_int, [P, I32, I64, I64, U32, I32, P, P, P]),
         "fq_adapt_decide": (I32, [I64, I32, c.POINTER(I32)]),
+        "fq_adapt_flags_rowshard": (c.c_int, [P, I32, I64, I64, I32, I32, U32, I32, P, P, P, P]),
+        "fq_adapt_flags_cross": (c.c_int, [P, I64, I64, I32, U32, I32, P, P]),
+        "fq_quantize_rowshard": (c.c_int, [P, I32, WD, I32, I32, P, P, P, P, P]),
         "fq_quantize": (c.c_int, [P, I32, WD, P, P, P, P]),
         "fq_gemm_workspace_bytes": (SZ, [I64, WD]),
         "fq_gemm": (c.c_int, [P, I32, I64, WD, P, P, P, I32, P, SZ, P]),
+        "fq_gemm_workspace_bytes_ex": (SZ, [I64, WD, c.POINTER(fq_gemm_opts)]),
+        "fq_gemm_ex": (c.c_int, [P, I32, I64, WD, P, P, P, I32, P, SZ, P, c.POINTER(fq_gemm_opts)]),
         "fq_gemm_grouped_workspace_bytes": (SZ, [I64, I32, WD]),
         "fq_gemm_grouped": (c.c_int, [P, I32, I64, c.POINTER(I64), I32, WD, c.POINTER(I32),
                                       c.POINTER(P), c.POINTER(P), P, I32, P, SZ, P]),
@@ -67,8 +87,10 @@ def _load():
 
 _lib = _load()
 EXPORTED = ("fq_version", "fq_status_str", "fq_codes_bytes", "fq_scales_bytes", "fq_adapt_levels",
-            "fq_adapt_group_at", "fq_adapt_flags", "fq_adapt_decide", "fq_quantize",
-            "fq_gemm_workspace_bytes", "fq_gemm", "fq_gemm_grouped_workspace_bytes", "fq_gemm_grouped")
+            "fq_adapt_group_at", "fq_adapt_flags", "fq_adapt_decide", "fq_adapt_flags_rowshard",
+            "fq_adapt_flags_cross", "fq_quantize", "fq_quantize_rowshard", "fq_gemm_workspace_bytes",
+            "fq_gemm", "fq_gemm_workspace_bytes_ex", "fq_gemm_ex", "fq_gemm_grouped_workspace_bytes",
+            "fq_gemm_grouped")
 
 
 def _ptr(t):
@@ -128,6 +150,29 @@ def fq_adapt_decide(K: int, min_group: int, flags_host) -> int:
     return _lib.fq_adapt_decide(K, min_group, arr)
 
 
+def fq_adapt_flags_rowshard(W_shard: torch.Tensor, K: int, world: int, rank: int, alpha_milli: int,
+                            min_group: int, flags: torch.Tensor | None, colmax: torch.Tensor,
+                            status: torch.Tensor | None = None, stream=None) -> None:
+    N = W_shard.shape[0]
+    _check(_lib.fq_adapt_flags_rowshard(_ptr(W_shard), _DT[W_shard.dtype], K, N, world, rank, alpha_milli,
+                                        min_group, _ptr(flags), _ptr(colmax), _ptr(status), _stream(stream)),
+           "fq_adapt_flags_rowshard")
+
+
+def fq_adapt_flags_cross(colmax: torch.Tensor, K: int, N: int, world: int, alpha_milli: int, min_group: int,
+                         flags: torch.Tensor, stream=None) -> None:
+    _check(_lib.fq_adapt_flags_cross(_ptr(colmax), K, N, world, alpha_milli, min_group, _ptr(flags),
+                                     _stream(stream)), "fq_adapt_flags_cross")
+
+
+def fq_quantize_rowshard(W_shard: torch.Tensor, d: fq_wdesc, world: int, rank: int, colmax: torch.Tensor | None,
+                         codes: torch.Tensor, scales: torch.Tensor, status: torch.Tensor | None = None,
+                         stream=None) -> None:
+    _check(_lib.fq_quantize_rowshard(_ptr(W_shard), _DT[W_shard.dtype], ctypes.byref(d), world, rank,
+                                     _ptr(colmax), _ptr(codes), _ptr(scales), _ptr(status), _stream(stream)),
+           "fq_quantize_rowshard")
+
+
 def make_wdesc(K: int, N: int, bits: int, group: int, scale_dtype: int) -> fq_wdesc:
     return fq_wdesc(K, N, bits, group, scale_dtype, 0)
 
@@ -149,6 +194,17 @@ def fq_gemm(A: torch.Tensor, M: int, d: fq_wdesc, codes: torch.Tensor, scales: t
                         _stream(stream)), "fq_gemm")
 
 
+def fq_gemm_workspace_bytes_ex(M: int, d: fq_wdesc, opts: fq_gemm_opts | None) -> int:
+    return _lib.fq_gemm_workspace_bytes_ex(M, ctypes.byref(d), None if opts is None else ctypes.byref(opts))
+
+
+def fq_gemm_ex(A: torch.Tensor, M: int, d: fq_wdesc, codes: torch.Tensor, scales: torch.Tensor,
+               C: torch.Tensor, ws: torch.Tensor | None, stream=None, opts: fq_gemm_opts | None = None) -> None:
+    _check(_lib.fq_gemm_ex(_ptr(A), _DT[A.dtype], M, ctypes.byref(d), _ptr(codes), _ptr(scales),
+                           _ptr(C), _DT[C.dtype], _ptr(ws), 0 if ws is None else ws.numel() * ws.element_size(),
+                           _stream(stream), None if opts is None else ctypes.byref(opts)), "fq_gemm_ex")
+
+
 def fq_gemm_grouped_workspace_bytes(T: int, E: int, d: fq_wdesc) -> int:
     return _lib.fq_gemm_grouped_workspace_bytes(T, E, ctypes.byref(d))
 
@@ -168,13 +224,27 @@ def fq_gemm_grouped(A, T, offsets_host, E, d, groups_host, codes_ptrs, scales_pt
 _WS: dict = {}
 
 
-def workspace(nbytes: int, device) -> torch.Tensor:
-    """Zero-filled scratch reused across calls (the kernels leave their counters zeroed)."""
-    dev = torch.device(device)
-    key = (dev.type, dev.index)
+def workspace(nbytes: int, device, stream=None) -> torch.Tensor:
+    """Zero-filled scratch reused across calls (the kernels leave their counters zeroed).
+
+    One buffer per (device, stream): calls sharing a workspace must be stream-ordered (fq.h), so
+    calls on different streams get different buffers.  The buffer is allocated and zero-filled on
+    the stream that uses it; a buffer replaced by a larger one is released to the caching allocator
+    on that same stream, i.e. only after the kernels already enqueued there have finished."""
+    dev = device if isinstance(device, torch.device) else torch.device(device)
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    if stream is not None:
+        h = stream.cuda_stream
+    elif _raw_stream is not None:
+        h = _raw_stream(idx)
+    else:
+        h = torch.cuda.current_stream(idx).cuda_stream
+    key = (idx, h)
     ws = _WS.get(key)
     if ws is None or ws.numel() < nbytes:
-        ws = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=dev)
+        st = stream if stream is not None else torch.cuda.current_stream(idx)
+        with torch.cuda.stream(st):
+            ws = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=torch.device("cuda", idx))
         _WS[key] = ws
     return ws
 
@@ -211,6 +281,51 @@ def adapt_group(W: torch.Tensor, alpha_milli: int = 500, min_group: int = 16, pr
     return fq_adapt_decide(K, min_group, flags.cpu().tolist()[: nlev - 1])
 
 
+class _KernelOps:
+    """The row-shard adaptive protocol's device steps (tp.rowshard_protocol) on the libfq kernels."""
+
+    @staticmethod
+    def alloc(nflags: int, world: int, N: int, device):
+        # one int32 buffer [flags | colmax as fp32 bits]: non-negative fp32 values order like their
+        # int32 bit patterns, so a single MAX all-reduce combines both
+        buf = torch.zeros(nflags + world * N, dtype=torch.int32, device=device)
+        return buf, buf[:nflags], buf[nflags:].view(torch.float32)
+
+    @staticmethod
+    def shard_pass(W_shard, K, world, rank, alpha_milli, min_group, flags, colmax):
+        fq_adapt_flags_rowshard(W_shard, K, world, rank, alpha_milli, min_group,
+                                flags if flags.numel() else None, colmax)
+
+    @staticmethod
+    def cross(colmax, K, N, world, alpha_milli, min_group, flags):
+        if world > 1:
+            fq_adapt_flags_cross(colmax, K, N, world, alpha_milli, min_group, flags)
+
+    @staticmethod
+    def decide(K, min_group, flags) -> int:
+        return fq_adapt_decide(K, min_group, flags.cpu().tolist())
+
+
+KERNEL_OPS = _KernelOps()
+
+
+def quantize_rowshard(W_shard: torch.Tensor, K: int, world: int, rank: int, bits: int, group: int,
+                      colmax: torch.Tensor | None = None, scale_dtype=torch.bfloat16,
+                      status: torch.Tensor | None = None) -> QuantizedWeight:
+    """Rank `rank`'s K-slice of the unsharded quantization of a row-parallel matrix (fq.h
+    fq_quantize_rowshard): codes/scales are the K-/G-slices of fq_quantize(W_full, bits, group);
+    `colmax` (the MAX-all-reduced [world, N] shard column maxima) is needed when group > K/world."""
+    assert W_shard.is_cuda and W_shard.dim() == 2 and W_shard.is_contiguous()
+    N, Ks = W_shard.shape
+    assert Ks * world == K
+    gs = min(group, Ks)
+    d = make_wdesc(K, N, bits, group, _DT[scale_dtype])
+    codes = torch.empty((N, Ks * bits // 8), dtype=torch.uint8, device=W_shard.device)
+    scales = torch.empty((Ks // gs, N), dtype=scale_dtype, device=W_shard.device)
+    fq_quantize_rowshard(W_shard, d, world, rank, colmax, codes, scales, status)
+    return QuantizedWeight(codes, scales, Ks, N, bits, gs)
+
+
 def quantize(W: torch.Tensor, bits: int = 4, group: int | None = 128, scale_dtype=torch.bfloat16,
              alpha_milli: int = 500, min_group: int = 16, status: torch.Tensor | None = None) -> QuantizedWeight:
     """fq_quantize(W, bits, group | adaptive): W is [N, K] (nn.Linear layout) on a CUDA device.
@@ -240,27 +355,34 @@ def gemm_grouped(A: torch.Tensor, offsets, experts: list, out: torch.Tensor | No
         out = torch.empty((T, q0.N), dtype=out_dtype or A.dtype, device=A.device)
     d = q0.desc
     nb = fq_gemm_grouped_workspace_bytes(T, E, d)
-    ws = workspace(nb, A.device)
+    ws = workspace(nb, A.device, stream)
     fq_gemm_grouped(A, T, offs, E, d, [q.group for q in experts], [q.codes.data_ptr() for q in experts],
                     [q.scales.data_ptr() for q in experts], out, ws, stream)
     return out
 
 
 def gemm(A: torch.Tensor, qw: QuantizedWeight, out: torch.Tensor | None = None,
-         out_dtype=None, stream=None) -> torch.Tensor:
-    """C[M, N] = A[M, K] . dequant(qw)^T  (fused, on the GPU)."""
+         out_dtype=None, stream=None, opts: fq_gemm_opts | None = None) -> torch.Tensor:
+    """C[M, N] = A[M, K] . dequant(qw)^T  (fused, on the GPU).  `opts` (make_opts(...)) overrides
+    the library's routing / split plan (tests, measurements)."""
     assert A.is_cuda and A.dim() == 2 and A.is_contiguous() and A.shape[1] == qw.K
     M = A.shape[0]
     d = qw.desc
     if out is None:
         out = torch.empty((M, qw.N), dtype=out_dtype or A.dtype, device=A.device)
-    key = (M, qw.K, qw.N, qw.bits, qw.group)
+    okey = None if opts is None else (opts.path, opts.splits, opts.tc_halves, opts.tc_dqg)
+    key = (M, qw.K, qw.N, qw.bits, qw.group, okey)
     nb = _WS_BYTES.get(key)
     if nb is None:
-        nb = _WS_BYTES[key] = fq_gemm_workspace_bytes(M, d)
-    ws = workspace(nb, A.device)
-    fq_gemm(A, M, d, qw.codes, qw.scales, out, ws, stream)
+        nb = _WS_BYTES[key] = fq_gemm_workspace_bytes_ex(M, d, opts)
+    ws = workspace(nb, A.device, stream)
+    if opts is None:
+        fq_gemm(A, M, d, qw.codes, qw.scales, out, ws, stream)
+    else:
+        fq_gemm_ex(A, M, d, qw.codes, qw.scales, out, ws, stream, opts)
     return out
 
 
-_WS_BYTES: dict = {}  # (M, K, N, bits, group) -> fq_gemm_workspace_bytes (a pure function of the shape)
+# (M, K, N, bits, group, opts) -> workspace bytes: a pure function of its key (fq.h: routing reads
+# nothing but the arguments)
+_WS_BYTES: dict = {}

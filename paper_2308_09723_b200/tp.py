@@ -9,8 +9,14 @@ Megatron-style partitioning of a transformer layer:
     column slice of the unsharded ones (bit-exact).
   * row-parallel (out-proj, FC2): the reduction dim K is sharded (requires group | K/t); each rank
     produces a partial C over its K slice, then an all-reduce(SUM) over NCCL (NVLink/NVSwitch).
-  * adaptive group size: the level flags of all shards of one matrix are OR-ed (all-reduce MAX)
-    before the host decision, so every shard uses the same g (reading R11: one g per matrix).
+  * adaptive group size (reading R11: one g per matrix, decided on the FULL matrix):
+      - column shards hold whole columns: the level flags of all shards are OR-ed (all-reduce MAX)
+        before the host decision;
+      - row shards hold K-slices: `rowshard_protocol` decides g on the full-K ladder -- the levels
+        whose groups lie inside one shard come from each shard's own pass (OR-ed), the coarse levels
+        whose groups span shards from the MAX-all-reduced table of shard column maxima (SURVEY §8(c)
+        C-T) -- and groups larger than K/t are quantized from that table's group maxima, so every
+        shard's codes/scales are the K-/G-slices of the unsharded ones.
 
 The GEMM and quantizer are the libfq kernels; this module only shards, calls and reduces.
 The shard arithmetic is kept in pure functions (`shard_bounds`, `tp_forward`) so the multi-process
@@ -34,9 +40,31 @@ def shard_bounds(n: int, world: int, rank: int, align: int = 8) -> tuple[int, in
 
 
 def check_row_group(K: int, world: int, group: int) -> None:
-    """Row-parallel shards need whole groups on every rank (group | K/world)."""
-    if (K // world) % group:
-        raise ValueError(f"row-parallel shard K/t={K // world} is not a multiple of group {group}")
+    """Row-parallel shards hold whole groups (group | K/world) or whole shards of one group
+    ((K/world) | group, the group amax then comes from the shards' column maxima)."""
+    ks = K // world
+    if K % world or (ks % group and group % ks):
+        raise ValueError(f"row-parallel shard K/t={ks} and group {group} do not nest")
+
+
+def rowshard_protocol(W_shard, K: int, world: int, rank: int, alpha_milli: int, min_group: int, ops,
+                      allreduce_max: Callable | None, adaptive: bool = True):
+    """Adaptive group size of a row-parallel (K-sharded) matrix, decided on the full-K ladder
+    (fq.h fq_adapt_flags_rowshard / fq_adapt_flags_cross).  `ops` supplies the device steps
+    (fq.KERNEL_OPS on the GPU); `allreduce_max(t)` MAX-reduces an int32 tensor over the ranks of
+    the matrix in place (None: a single rank).  Returns (g or None, colmax [world, N] fp32)."""
+    from .fq import fq_adapt_levels
+    N = W_shard.shape[0]
+    nflags = max(0, fq_adapt_levels(K, min_group) - 1)
+    buf, flags, colmax = ops.alloc(nflags, world, N, W_shard.device)
+    ops.shard_pass(W_shard, K, world, rank, alpha_milli, min_group, flags, colmax)
+    if allreduce_max is not None and world > 1:
+        allreduce_max(buf)
+    if not adaptive:
+        return None, colmax
+    if nflags:
+        ops.cross(colmax, K, N, world, alpha_milli, min_group, flags)
+    return ops.decide(K, min_group, flags), colmax
 
 
 @dataclass
@@ -73,18 +101,33 @@ def tp_forward(x: torch.Tensor, shards: list, gemm_fn: Callable, allreduce_fn: C
 
 
 class TPLinearFQ:
-    """A quantized linear shard on this rank (canonical libfq layout)."""
+    """A quantized linear shard on this rank (canonical libfq layout).  Its codes/scales are the
+    slices of the unsharded matrix's quantization (bit-exact), adaptive group size included."""
 
     def __init__(self, W_shard: torch.Tensor, spec: ShardSpec, bits: int = 4, group: int | None = 128,
                  alpha_milli: int = 500, min_group: int = 16, process_group=None):
         from . import fq
         self.spec = spec
-        if group is None:  # adaptive: agree on g across the shards of this matrix
+        W_shard = W_shard.contiguous()
+        if spec.kind == "row":
+            ks = spec.K // spec.world
+            colmax = None
+            if group is None or group > ks:
+                def amax(t):
+                    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=process_group)
+                g, colmax = rowshard_protocol(W_shard, spec.K, spec.world, spec.rank, alpha_milli, min_group,
+                                              fq.KERNEL_OPS, amax if spec.world > 1 else None,
+                                              adaptive=group is None)
+                group = g if group is None else group
+            check_row_group(spec.K, spec.world, group)
+            self.group = group
+            self.qw = fq.quantize_rowshard(W_shard, spec.K, spec.world, spec.rank, bits, group, colmax)
+            return
+        if group is None:  # column shards: OR the flags of all shards of this matrix
             group = fq.adapt_group(W_shard, alpha_milli, min_group,
                                    process_group=process_group if spec.world > 1 else None)
-        if spec.kind == "row":
-            check_row_group(spec.K, spec.world, group)
-        self.qw = fq.quantize(W_shard.contiguous(), bits, group)
+        self.group = group
+        self.qw = fq.quantize(W_shard, bits, group)
 
     def __call__(self, x: torch.Tensor, out_dtype=None) -> torch.Tensor:
         from . import fq
@@ -111,12 +154,14 @@ class TPOptLayer:
             dist.all_reduce(part, op=dist.ReduceOp.SUM, group=self.pg)
         return part.to(dtype)
 
-    def forward(self, x: torch.Tensor) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, return_all: bool = False):
         hs = self.out.qw.K  # h / t: the K shard of the out-projection
         q = self.qkv(x)
-        y = self._row(self.out, q[:, :hs].contiguous(), x.dtype)
+        a = q[:, :hs].contiguous()
+        y = self._row(self.out, a, x.dtype)
         f = self.fc1(y)
-        return self._row(self.fc2, f, x.dtype)
+        z = self._row(self.fc2, f, x.dtype)
+        return (z, dict(qkv=q, attn=a, out=y, fc1=f, fc2=z)) if return_all else z
 
     @property
     def weight_bytes(self) -> int:

@@ -122,17 +122,73 @@ def test_gemm_workspace_sizes(fq):
     fc2 = fq.make_wdesc(49152, 12288, 4, 128, fq.FQ_BF16)
     nb = fq.fq_gemm_workspace_bytes(64, fc2)
     assert nb > 65536 and (nb - 65536) % (64 * 256 * 4) == 0
-    saved = os.environ.get("FQ_GEMM_PATH")
-    try:
-        os.environ["FQ_GEMM_PATH"] = "tc"
-        forced = fq.fq_gemm_workspace_bytes(32, fc2)
-        os.environ["FQ_GEMM_PATH"] = "decode"
-        dec = fq.fq_gemm_workspace_bytes(32, fc2)
-    finally:
-        if saved is None:
-            os.environ.pop("FQ_GEMM_PATH", None)
-        else:
-            os.environ["FQ_GEMM_PATH"] = saved
+    forced = fq.fq_gemm_workspace_bytes_ex(32, fc2, fq.make_opts("tc"))
+    dec = fq.fq_gemm_workspace_bytes_ex(32, fc2, fq.make_opts("decode"))
     assert forced != dec and fq.fq_gemm_workspace_bytes(32, fc2) == forced
+    assert fq.fq_gemm_workspace_bytes_ex(32, fc2, None) == forced
     # ... while FC1 (384 one-half tiles) keeps 17..32 tokens on the decode kernel
     assert fq.fq_gemm_workspace_bytes(32, d) >= 65536 + 32 * 12288 * 2
+
+
+def test_routing_is_environment_independent(fq, monkeypatch):
+    """fq.h: routing and split plans read nothing from the process environment (round-1 diagnostic
+    switches are gone from the product build); overrides go through fq_gemm_opts only."""
+    fc2 = fq.make_wdesc(49152, 12288, 4, 128, fq.FQ_BF16)
+    base = {M: fq.fq_gemm_workspace_bytes(M, fc2) for M in (1, 16, 32, 64, 2048)}
+    for k, v in (("FQ_GEMM_PATH", "decode"), ("FQ_GEMV_SPLITS", "1"), ("FQ_TC_HM", "1"), ("FQ_TC_SPLITS", "1"),
+                 ("FQ_DECODE_TC", "1"), ("FQ_PDL", "0")):
+        monkeypatch.setenv(k, v)
+    assert {M: fq.fq_gemm_workspace_bytes(M, fc2) for M in base} == base
+    so = open(fq.LIB_PATH, "rb").read()
+    for name in (b"FQ_GEMM_PATH", b"FQ_GEMV_SPLITS", b"FQ_TC_HM", b"FQ_DECODE_TC", b"FQ_DEC_DEBUG", b"FQ_PDL"):
+        assert name not in so, name
+
+
+def test_gemm_opts_validation(fq):
+    dummy = ctypes.c_void_p(16)
+    d = fq.make_wdesc(4096, 512, 4, 128, fq.FQ_BF16)
+    for bad in (fq.make_opts(3), fq.make_opts(0, -1), fq.make_opts(0, 0, 3), fq.make_opts(0, 0, 0, 5)):
+        assert fq._lib.fq_gemm_ex(dummy, 0, 4, ctypes.byref(d), dummy, dummy, dummy, 0, None, 0, None,
+                                  ctypes.byref(bad)) == fq.FQ_ERR_INVALID_ARG
+        assert fq._lib.fq_gemm_workspace_bytes_ex(4, ctypes.byref(d), ctypes.byref(bad)) == 0
+    o = fq.make_opts()
+    o.reserved[2] = 1
+    assert fq._lib.fq_gemm_ex(dummy, 0, 4, ctypes.byref(d), dummy, dummy, dummy, 0, None, 0, None,
+                              ctypes.byref(o)) == fq.FQ_ERR_INVALID_ARG
+    # decode split plans follow the override; A6 sizes follow tc_halves / splits
+    s1 = fq.fq_gemm_workspace_bytes_ex(4, d, fq.make_opts("decode", 1))
+    s4 = fq.fq_gemm_workspace_bytes_ex(4, d, fq.make_opts("decode", 4))
+    assert s4 - s1 >= 4 * 4 * 512 * 4 - 256
+    t1 = fq.fq_gemm_workspace_bytes_ex(64, d, fq.make_opts("tc", 1))
+    t2 = fq.fq_gemm_workspace_bytes_ex(64, d, fq.make_opts("tc", 0, 2))
+    assert t1 == 256 and t2 > 65536
+
+
+def test_grouped_workspace_error_launches_nothing(fq):
+    """fq.h: a call that returns != FQ_OK has written nothing -- the grouped call checks the
+    workspace of every expert class before its first launch (dummy pointers: any launch would
+    fault or return FQ_ERR_CUDA, and no GPU is needed to reach the check)."""
+    dummy = ctypes.c_void_p(16)
+    E = 3
+    d = fq.make_wdesc(4096, 16384, 4, 128, fq.FQ_BF16)
+    offs = (ctypes.c_int64 * (E + 1))(0, 100, 102, 110)   # one tensor-core expert, two decode experts
+    groups = (ctypes.c_int32 * E)(128, 128, 16)
+    ptrs = (ctypes.c_void_p * E)(16, 16, 16)
+    assert fq._lib.fq_gemm_grouped(dummy, fq.FQ_BF16, 110, offs, E, ctypes.byref(d), groups, ptrs, ptrs, dummy,
+                                   fq.FQ_BF16, dummy, 1024, None) == fq.FQ_ERR_WORKSPACE
+
+
+def test_rowshard_validation(fq):
+    dummy = ctypes.c_void_p(16)
+    L = fq._lib
+    # world must be a power of two whose K-slices sit on the ladder
+    assert L.fq_adapt_flags_rowshard(dummy, 0, 12288, 256, 3, 0, 500, 16, dummy, dummy, None, None) == fq.FQ_ERR_SHAPE
+    assert L.fq_adapt_flags_rowshard(dummy, 0, 12288, 256, 2, 2, 500, 16, dummy, dummy, None, None) == fq.FQ_ERR_INVALID_ARG
+    assert L.fq_adapt_flags_rowshard(dummy, 0, 96, 256, 4, 0, 500, 16, dummy, dummy, None, None) == fq.FQ_ERR_SHAPE
+    assert L.fq_adapt_flags_rowshard(dummy, 0, 12288, 256, 2, 0, 500, 16, dummy, None, None, None) == fq.FQ_ERR_INVALID_ARG
+    assert L.fq_adapt_flags_cross(dummy, 12288, 256, 1, 500, 16, dummy, None) == fq.FQ_OK  # nothing spans shards
+    d = fq.make_wdesc(12288, 256, 4, 12288, fq.FQ_BF16)
+    # group > K/world needs the column-max table
+    assert L.fq_quantize_rowshard(dummy, 0, ctypes.byref(d), 4, 0, None, dummy, dummy, None, None) == fq.FQ_ERR_INVALID_ARG
+    d = fq.make_wdesc(12288, 256, 4, 96 * 16, fq.FQ_BF16)  # 1536 does not nest with 12288/16 = 768?  it does
+    assert L.fq_quantize_rowshard(dummy, 0, ctypes.byref(d), 3, 0, None, dummy, dummy, None, None) == fq.FQ_ERR_INVALID_ARG

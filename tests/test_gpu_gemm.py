@@ -24,17 +24,20 @@ def fq():
 
 @pytest.fixture
 def env():
-    saved = {}
+    """Routing / plan overrides for the next run_case calls (fq_gemm_opts, include/fq.h)."""
+    o = {}
 
     def set_(k, v):
-        saved.setdefault(k, os.environ.get(k))
-        os.environ[k] = str(v)
+        o[k] = v
+    set_.opts = o
     yield set_
-    for k, v in saved.items():
-        if v is None:
-            os.environ.pop(k, None)
-        else:
-            os.environ[k] = v
+
+
+def _opts(fq, env):
+    o = getattr(env, "opts", None) if env is not None else None
+    if not o:
+        return None
+    return fq.make_opts(o.get("path", 0), int(o.get("splits", 0)), int(o.get("hm", 0)), int(o.get("dqg", 0)))
 
 
 def make_case(M, K, N, bits, group, adt="bf16", seed=0, outliers=0):
@@ -46,12 +49,12 @@ def make_case(M, K, N, bits, group, adt="bf16", seed=0, outliers=0):
     return Wb, Ab
 
 
-def run_case(fq, Wb, Ab, bits, group, adt="bf16", cdt=None):
+def run_case(fq, Wb, Ab, bits, group, adt="bf16", cdt=None, env=None):
     W = bits_to_torch(Wb, "bf16")
     A = bits_to_torch(Ab, adt)
     sdt = {"bf16": torch.bfloat16, "fp16": torch.float16}[adt]
     qw = fq.quantize(W, bits, group, scale_dtype=sdt)
-    C = fq.gemm(A, qw, out_dtype={"fp32": torch.float32, None: None}[cdt])
+    C = fq.gemm(A, qw, out_dtype={"fp32": torch.float32, None: None}[cdt], opts=_opts(fq, env))
     torch.cuda.synchronize()
     return qw, C
 
@@ -145,10 +148,10 @@ def test_decode_activation_dynamic_range(fq, M, adt):
 @pytest.mark.parametrize("splits", [1, 2, 3, 7])
 @pytest.mark.parametrize("M", [1, 12])
 def test_split_k_paths(fq, env, splits, M):
-    env("FQ_GEMV_SPLITS", splits)
+    env("splits", splits)
     Wb, Ab = make_case(M, 4096, 512, 4, 128, seed=11)
     for _ in range(2):  # second call checks the self-resetting counters
-        _, C = run_case(fq, Wb, Ab, 4, 128)
+        _, C = run_case(fq, Wb, Ab, 4, 128, env=env)
         Cr, D = oracle_ref(Wb, Ab, 4, 128, "bf16")
         assert O.rel_err(torch_to_f64(C), Cr, D) <= TOL
 
@@ -159,10 +162,10 @@ def test_decode_multi_tile_determinism(fq, env, M, K, N):
     """Decode kernel with split-K fixups over several column and token tiles (M > 16 on the decode
     path): the fixup sums partials in a fixed order, so repeated calls are bit-identical (and the
     self-resetting counters are exercised)."""
-    env("FQ_GEMM_PATH", "decode")
+    env("path", "decode")
     Wb, Ab = make_case(M, K, N, 4, 128, seed=M + K + N)
-    _, C0 = run_case(fq, Wb, Ab, 4, 128, "bf16", "fp32")
-    _, C1 = run_case(fq, Wb, Ab, 4, 128, "bf16", "fp32")
+    _, C0 = run_case(fq, Wb, Ab, 4, 128, "bf16", "fp32", env=env)
+    _, C1 = run_case(fq, Wb, Ab, 4, 128, "bf16", "fp32", env=env)
     assert torch.equal(C0, C1)
     Cr, D = oracle_ref(Wb, Ab, 4, 128, "bf16")
     assert O.rel_err(torch_to_f64(C0), Cr, D) <= TOL
@@ -174,10 +177,10 @@ def test_decode_small_groups_long_k(fq, env, bits, group, M):
     """Groups smaller than the decode stage (scale rows staged by TMA per stage) with one CTA per
     column tile streaming many more stages than its ring holds (FQ_GEMV_SPLITS=1): the scales must
     be consumed before the stage is handed back to the producer."""
-    env("FQ_GEMM_PATH", "decode")
-    env("FQ_GEMV_SPLITS", 1)
+    env("path", "decode")
+    env("splits", 1)
     Wb, Ab = make_case(M, 4096, 512, bits, group, seed=group + M, outliers=2)
-    _, C = run_case(fq, Wb, Ab, bits, group, "bf16", "fp32")
+    _, C = run_case(fq, Wb, Ab, bits, group, "bf16", "fp32", env=env)
     Cr, D = oracle_ref(Wb, Ab, bits, group, "bf16")
     assert O.rel_err(torch_to_f64(C), Cr, D) <= TOL
 
@@ -187,15 +190,15 @@ def test_decode_small_groups_long_k(fq, env, bits, group, M):
 def test_tc_split_k(fq, env, M, K, N, bits, group):
     """A6 with few output tiles splits K over CTAs (fixed-order fp32 fixup): parity with the oracle,
     bit-identical repeated calls, and the same result as the unsplit kernel within rounding."""
-    env("FQ_GEMM_PATH", "tc")
+    env("path", "tc")
     Wb, Ab = make_case(M, K, N, bits, group, seed=M + N)
-    _, C0 = run_case(fq, Wb, Ab, bits, group, "bf16", "fp32")
-    _, C1 = run_case(fq, Wb, Ab, bits, group, "bf16", "fp32")
+    _, C0 = run_case(fq, Wb, Ab, bits, group, "bf16", "fp32", env=env)
+    _, C1 = run_case(fq, Wb, Ab, bits, group, "bf16", "fp32", env=env)
     assert torch.equal(C0, C1)
     Cr, D = oracle_ref(Wb, Ab, bits, group, "bf16")
     assert O.rel_err(torch_to_f64(C0), Cr, D) <= TOL
-    env("FQ_TC_SPLITS", 1)
-    _, C2 = run_case(fq, Wb, Ab, bits, group, "bf16", "fp32")
+    env("splits", 1)
+    _, C2 = run_case(fq, Wb, Ab, bits, group, "bf16", "fp32", env=env)
     assert O.rel_err(torch_to_f64(C2), Cr, D) <= TOL
 
 
@@ -209,12 +212,12 @@ def test_tc_tile_halves_split_k(fq, env, dqg, hm, M, K, N, bits, group, adt):
     two alternating dequant warp groups (FQ_TC_DQG; int4 only, each thread then covers 64 k and up to
     four group boundaries), under split-K: parity, bit-identical repeated calls, and N tails inside /
     past the second half."""
-    env("FQ_GEMM_PATH", "tc")
-    env("FQ_TC_HM", hm)
-    env("FQ_TC_DQG", dqg)
+    env("path", "tc")
+    env("hm", hm)
+    env("dqg", dqg)
     Wb, Ab = make_case(M, K, N, bits, group, adt, seed=M + K + hm)
-    _, C0 = run_case(fq, Wb, Ab, bits, group, adt, "fp32")
-    _, C1 = run_case(fq, Wb, Ab, bits, group, adt, "fp32")
+    _, C0 = run_case(fq, Wb, Ab, bits, group, adt, "fp32", env=env)
+    _, C1 = run_case(fq, Wb, Ab, bits, group, adt, "fp32", env=env)
     assert torch.equal(C0, C1)
     Cr, D = oracle_ref(Wb, Ab, bits, group, adt)
     assert O.rel_err(torch_to_f64(C0), Cr, D) <= TOL
@@ -225,7 +228,7 @@ def test_identity_exact_fp32_out(fq, env, path):
     """A = I (M = K = 256): C[k, n] = q[n,k] * s[k/g, n] exactly in fp32-output mode — catches any
     nibble-order / k-permutation / scale-index bug with zero tolerance.
     decode path: run as 16 token tiles of the M<=16 kernel (FQ_GEMM_PATH=decode)."""
-    env("FQ_GEMM_PATH", path)
+    env("path", path)
     K = N = 256
     Wb = gaussian_bits((N, K), 0.02, 5)
     # decode kernel: groups that are a multiple of its K chunk (128 int4 / 64 int8) apply the scale
@@ -238,7 +241,7 @@ def test_identity_exact_fp32_out(fq, env, path):
         W = bits_to_torch(Wb, "bf16")
         qw = fq.quantize(W, bits, group)
         A = torch.eye(K, dtype=torch.bfloat16, device="cuda")
-        C = fq.gemm(A, qw, out_dtype=torch.float32)
+        C = fq.gemm(A, qw, out_dtype=torch.float32, opts=_opts(fq, env))
         r = O.quantize(O.decode_bits(Wb, "bf16"), bits, group, O.BF16)
         ref = O.dequantize(r.q, r.s, group).T
         if exact:
@@ -297,6 +300,8 @@ def test_opt175b_full_size_sampled(fq, shape, bits, M):
     assert O.rel_err(torch_to_f64(C)[:, cols], Cr, D) <= TOL
     # the sampled columns' codes/scales are bit-exact as well
     assert np.array_equal(qw.codes[torch.from_numpy(cols).cuda()].cpu().numpy(), O.pack_codes(r.q, bits))
+    assert np.array_equal(qw.scales[:, torch.from_numpy(cols).cuda()].cpu().view(torch.int16).numpy().view(np.uint16),
+                          r.s_bits)
 
 
 @pytest.mark.parametrize("M,K,N,bits,group,adt", [
@@ -315,9 +320,9 @@ def test_opt175b_full_size_sampled(fq, shape, bits, M):
 ])
 def test_tc_path_parity(fq, env, M, K, N, bits, group, adt):
     """Large-M tcgen05 kernel (A6) vs the fp64 oracle on full outputs."""
-    env("FQ_GEMM_PATH", "tc")
+    env("path", "tc")
     Wb, Ab = make_case(M, K, N, bits, group, adt, seed=M + K, outliers=1)
-    _, C = run_case(fq, Wb, Ab, bits, group, adt)
+    _, C = run_case(fq, Wb, Ab, bits, group, adt, env=env)
     Cr, D = oracle_ref(Wb, Ab, bits, group, adt)
     assert O.rel_err(torch_to_f64(C), Cr, D) <= TOL
 
@@ -344,7 +349,6 @@ def test_opt175b_prefill_sampled(fq, shape, bits):
     assert O.rel_err(torch_to_f64(C)[np.ix_(rows, cols)], Cr, D) <= TOL
 
 
-@pytest.mark.parametrize("impl", ["tcgen05", "mma_sync"])
 @pytest.mark.parametrize("M,K,N,bits,group,adt,splits", [
     (1, 256, 256, 4, 128, "bf16", None),
     (3, 1536, 776, 4, 128, "bf16", None),    # ragged N tail
@@ -355,13 +359,13 @@ def test_opt175b_prefill_sampled(fq, shape, bits):
     (7, 1024, 768, 4, 64, "fp16", None),     # group 64: group-split nibble path
     (13, 2048, 512, 4, 64, "bf16", 3),       # group 64, two MMA token tiles, split-K
 ])
-def test_decode_kernels(fq, env, impl, M, K, N, bits, group, adt, splits):
-    """Both decode kernels (tcgen05 A4 and the mma.sync A4) against the oracle."""
-    env("FQ_DECODE_TC", "1" if impl == "tcgen05" else "0")
+def test_decode_kernels(fq, env, M, K, N, bits, group, adt, splits):
+    """Decode kernel classes (token tiles x scale paths) with and without forced split-K."""
+    env("path", "decode")
     if splits:
-        env("FQ_GEMV_SPLITS", splits)
+        env("splits", splits)
     Wb, Ab = make_case(M, K, N, bits, group, adt, seed=M * 7 + K, outliers=1)
     for _ in range(2):
-        _, C = run_case(fq, Wb, Ab, bits, group, adt)
+        _, C = run_case(fq, Wb, Ab, bits, group, adt, env=env)
         Cr, D = oracle_ref(Wb, Ab, bits, group, adt)
         assert O.rel_err(torch_to_f64(C), Cr, D) <= TOL

@@ -41,10 +41,8 @@ def build_experts(fq, E, K, N, bits, seed0=1000):
     return qws, ref
 
 
-@pytest.mark.parametrize("decode_tc", ["0", "1"])
 @pytest.mark.parametrize("bits", [4, 8])
-def test_moe_mixed_sizes(fq, bits, decode_tc, monkeypatch):
-    monkeypatch.setenv("FQ_DECODE_TC", decode_tc)
+def test_moe_mixed_sizes(fq, bits):
     E, K, N = 10, 512, 384
     counts = [0, 1, 3, 8, 9, 16, 17, 40, 2, 5]  # empty, decode classes, and tcgen05-sized experts
     off = np.zeros(E + 1, dtype=np.int64)

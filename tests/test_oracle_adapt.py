@@ -91,3 +91,38 @@ def test_alpha_range_rejected():
         O.adapt_report(np.zeros((2, 64)), 0, 16)
     with pytest.raises(ValueError):
         O.adapt_report(np.zeros((2, 64)), 1001, 16)
+
+
+def _hand_column(quarters):
+    col = []
+    for a in quarters:
+        col += [a] + [(-1) ** (i + 1) * a / 2 for i in range(1, 16)]
+    return np.array([col], dtype=np.float64)
+
+
+@pytest.mark.parametrize("name", ["prefix", "pairing"])
+def test_hand_fixtures_levels(golden, name):
+    """tests/golden/adapt_hand.txt (hand-derived, PAPER.md:147-149 + R6/R7): per-level flags, min
+    ratios and counts, and the accepted-prefix decision.  Fixture 'prefix' fails a deepest-fired-level
+    rule; fixture 'pairing' fails a child-to-parent pairing other than j // 2."""
+    g = golden("adapt_hand.txt")
+    W = _hand_column([float(x) for x in g[f"{name}_quarters"]])
+    assert np.max(np.abs(W)) == 1.0
+    rep = O.adapt_report(W, 500, 16)
+    assert [lv.group for lv in rep.levels] == [32, 16]
+    assert [int(lv.flag) for lv in rep.levels] == [int(x) for x in g[f"{name}_flags"]]
+    assert [lv.min_ratio for lv in rep.levels] == [float(x) for x in g[f"{name}_min_ratio"]]
+    assert [lv.count_below for lv in rep.levels] == [int(x) for x in g[f"{name}_count_below"]]
+    assert rep.group == int(g[f"{name}_group"][0])
+    assert O.adapt_group_size(W, 500, 16) == rep.group
+    assert O.adapt_decide(O.adapt_flags(W, 500, 16), 64, 16) == rep.group
+
+
+def test_hand_fixture_pairing_in_multicolumn_matrix(golden):
+    """The same two columns side by side: flags OR over columns (L1 from 'pairing', L2 from 'prefix'),
+    so L1 and L2 both fire -> 16.  Either column alone stops earlier."""
+    g = golden("adapt_hand.txt")
+    W = np.vstack([_hand_column([float(x) for x in g["prefix_quarters"]]),
+                   _hand_column([float(x) for x in g["pairing_quarters"]])])
+    assert O.adapt_flags(W, 500, 16) == [True, True]
+    assert O.adapt_group_size(W, 500, 16) == 16
