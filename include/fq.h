@@ -176,9 +176,16 @@ fq_status fq_gemm(const void* A, int32_t adt, int64_t M, const fq_wdesc* d, cons
                   void* stream);
 
 /* Routing / plan overrides (tests, measurements).  Zero-initialised = fq_gemm's own plan. */
-typedef enum { FQ_PATH_AUTO = 0, FQ_PATH_DECODE = 1, FQ_PATH_TC = 2 } fq_path;
+typedef enum {
+  FQ_PATH_AUTO = 0,
+  FQ_PATH_DECODE = 1,      /* a decode kernel (A4 / A4'), whichever the plan picks for M */
+  FQ_PATH_TC = 2,          /* the tcgen05 prefill kernel A6 */
+  FQ_PATH_DECODE_MMA = 3,  /* the mma.sync decode kernel A4 (any M: token tiles of <= 16/32 re-stream W) */
+  FQ_PATH_DECODE_UMMA = 4  /* the tcgen05 decode kernel A4' (int4, group % 128 == 0, K % 128 == 0, M <= 32;
+                              FQ_ERR_UNSUPPORTED otherwise) */
+} fq_path;
 typedef struct {
-  int32_t path;       /* fq_path: A4 decode kernel (any M: token tiles of <= 16/32 re-stream W) or A6 */
+  int32_t path;       /* fq_path */
   int32_t splits;     /* > 0: split-K factor (A4: K ranges of whole stage pairs; A6: item count) */
   int32_t tc_halves;  /* A6, tiles of <= 128 tokens: 1 or 2 halves of 128 weight rows per tile */
   int32_t tc_dqg;     /* A6, 16 dequant warps: 1, or 2 groups on alternate K blocks (int4 only) */

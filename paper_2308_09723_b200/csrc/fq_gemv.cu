@@ -508,207 +508,218 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
       for (int i = 0; i < 4; ++i) acc[rt][mt][i] = 0.f;
 
   const uint32_t sb = smem_u32(sbase);
-  int s = 0;
-  uint32_t ph = 0;
-  for (int i = 0; i < nst; ++i) {
-    const int k0 = kbeg + i * KS;
-    mbar_wait(&full_bar[s], ph);
-    const uint32_t wst = sb + s * STAGE_BYTES;
-    float sg[2][GS], sh[2][GS];  // this stage's scales (TMA-staged with the weights), per 64-k group
+  // Everything a consumer thread reads from one stage, in registers.
+  struct StageOps {
+    float sg[2][GS], sh[2][GS];       // the stage's scales (TMA-staged with the weights), per 64-k group
+    uint4 b[LAZY ? 1 : MT][PIECES];   // activation fragments
+    float2 sa[MT][GS], iv[MT];        // per-token corrections / inverse power-of-two scales
+    uint4 wgv[2], whv[2];             // code words of rows g / h of both row tiles
+    uint32_t scg[2][4], sch[2][4];    // per-element-scale path: splatted scale words
+  };
+  auto load_ops = [&](uint32_t wst, StageOps& o) {
     if (SACC) {
 #pragma unroll
       for (int rt = 0; rt < 2; ++rt)
 #pragma unroll
         for (int gi = 0; gi < GS; ++gi) {
-          sg[rt][gi] = lds_scale<T>(wst + SC_OFS + gi * kRowsPerCta * 2 + Rg[rt] * 2);
-          sh[rt][gi] = lds_scale<T>(wst + SC_OFS + gi * kRowsPerCta * 2 + Rh[rt] * 2);
+          o.sg[rt][gi] = lds_scale<T>(wst + SC_OFS + gi * kRowsPerCta * 2 + Rg[rt] * 2);
+          o.sh[rt][gi] = lds_scale<T>(wst + SC_OFS + gi * kRowsPerCta * 2 + Rh[rt] * 2);
         }
     }
-    if (DBG != 3 && DBG != 4) {
-      uint4 b[LAZY ? 1 : MT][PIECES];
-      if (!LAZY) {
+    if (DBG == 3 || DBG == 4) return;
+    if (!LAZY) {
 #pragma unroll
-        for (int mt = 0; mt < (LAZY ? 1 : MT); ++mt)
+      for (int mt = 0; mt < (LAZY ? 1 : MT); ++mt)
 #pragma unroll
-          for (int w16 = 0; w16 < PIECES; ++w16) b[mt][w16] = lds128(wst + aofs[mt][w16]);
-      }
-      float2 sa[MT][GS], iv[MT];
-      if (NIB) {  // {corr, 2^-e, corr_lo, corr_hi} of tokens 2t and 2t+1 (lo / hi: the 64-k halves)
+        for (int w16 = 0; w16 < PIECES; ++w16) o.b[mt][w16] = lds128(wst + aofs[mt][w16]);
+    }
+    if (NIB) {  // {corr, 2^-e, corr_lo, corr_hi} of tokens 2t and 2t+1 (lo / hi: the 64-k halves)
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-          if (GS == 1) {
-            const float2 x0 = lds64f(wst + saofs + mt * 128), x1 = lds64f(wst + saofs + mt * 128 + 16);
-            sa[mt][0] = make_float2(x0.x, x1.x);
-            iv[mt] = make_float2(x0.y, x1.y);
-          } else {
-            const uint4 x0 = lds128(wst + saofs + mt * 128), x1 = lds128(wst + saofs + mt * 128 + 16);
-            sa[mt][0] = make_float2(__uint_as_float(x0.z), __uint_as_float(x1.z));
-            sa[mt][GS - 1] = make_float2(__uint_as_float(x0.w), __uint_as_float(x1.w));
-            iv[mt] = make_float2(__uint_as_float(x0.y), __uint_as_float(x1.y));
-          }
-        }
-      } else if (OFF != 0.f) {
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) sa[mt][0] = lds64f(wst + saofs + mt * 32);
-      }
-      uint4 wgv[2], whv[2];
-#pragma unroll
-      for (int rt = 0; rt < 2; ++rt) {
+      for (int mt = 0; mt < MT; ++mt) {
         if (GS == 1) {
-          wgv[rt] = lds128(wst + wofs_g[rt]);
-          whv[rt] = lds128(wst + wofs_h[rt]);
-        } else {  // word w = 8 codes at k = 32 w + 8 t: cell w (swizzled), word t of the cell
-          uint32_t g4[4], h4[4];
-#pragma unroll
-          for (int w = 0; w < 4; ++w) {
-            g4[w] = lds32(wst + Rg[rt] * kWBytesPerRow + (swz64(w, Rg[rt]) << 4) + t * 4);
-            h4[w] = lds32(wst + Rh[rt] * kWBytesPerRow + (swz64(w, Rh[rt]) << 4) + t * 4);
-          }
-          wgv[rt] = make_uint4(g4[0], g4[1], g4[2], g4[3]);
-          whv[rt] = make_uint4(h4[0], h4[1], h4[2], h4[3]);
+          const float2 x0 = lds64f(wst + saofs + mt * 128), x1 = lds64f(wst + saofs + mt * 128 + 16);
+          o.sa[mt][0] = make_float2(x0.x, x1.x);
+          o.iv[mt] = make_float2(x0.y, x1.y);
+        } else {
+          const uint4 x0 = lds128(wst + saofs + mt * 128), x1 = lds128(wst + saofs + mt * 128 + 16);
+          o.sa[mt][0] = make_float2(__uint_as_float(x0.z), __uint_as_float(x1.z));
+          o.sa[mt][GS - 1] = make_float2(__uint_as_float(x0.w), __uint_as_float(x1.w));
+          o.iv[mt] = make_float2(__uint_as_float(x0.y), __uint_as_float(x1.y));
         }
       }
-      // per-element-scale path with TMA-staged scale rows: into registers before the stage is
-      // released (the producer may overwrite it right after the early release below)
-      uint32_t scg[2][4], sch[2][4];
-      if (!SACC && p.sc_rows) {
+    } else if (OFF != 0.f) {
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) o.sa[mt][0] = lds64f(wst + saofs + mt * 32);
+    }
+#pragma unroll
+    for (int rt = 0; rt < 2; ++rt) {
+      if (GS == 1) {
+        o.wgv[rt] = lds128(wst + wofs_g[rt]);
+        o.whv[rt] = lds128(wst + wofs_h[rt]);
+      } else {  // word w = 8 codes at k = 32 w + 8 t: cell w (swizzled), word t of the cell
+        uint32_t g4[4], h4[4];
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
-          const uint32_t so = wst + SC_OFS + (((t * SEG + w * (SEG / 4)) >> p.sc_shift) * kRowsPerCta) * 2;
+          g4[w] = lds32(wst + Rg[rt] * kWBytesPerRow + (swz64(w, Rg[rt]) << 4) + t * 4);
+          h4[w] = lds32(wst + Rh[rt] * kWBytesPerRow + (swz64(w, Rh[rt]) << 4) + t * 4);
+        }
+        o.wgv[rt] = make_uint4(g4[0], g4[1], g4[2], g4[3]);
+        o.whv[rt] = make_uint4(h4[0], h4[1], h4[2], h4[3]);
+      }
+    }
+    // per-element-scale path with TMA-staged scale rows: into registers before the stage is
+    // released (the producer may overwrite it right after the early release)
+    if (!SACC && p.sc_rows) {
 #pragma unroll
-          for (int rt = 0; rt < 2; ++rt) {
-            const uint32_t vg = lds_u16(so + Rg[rt] * 2), vh = lds_u16(so + Rh[rt] * 2);
-            scg[rt][w] = vg | (vg << 16);
-            sch[rt][w] = vh | (vh << 16);
-          }
+      for (int w = 0; w < 4; ++w) {
+        const uint32_t so = wst + SC_OFS + (((t * SEG + w * (SEG / 4)) >> p.sc_shift) * kRowsPerCta) * 2;
+#pragma unroll
+        for (int rt = 0; rt < 2; ++rt) {
+          const uint32_t vg = lds_u16(so + Rg[rt] * 2), vh = lds_u16(so + Rh[rt] * 2);
+          o.scg[rt][w] = vg | (vg << 16);
+          o.sch[rt][w] = vh | (vh << 16);
         }
       }
-      if (EARLY) {
-        // everything this warp needs from the stage is in registers: hand the slot back to the TMA
-        // producer now, so the next loads overlap this warp's dequant + MMA work
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty_bar[s]);
+    }
+  };
+  auto compute = [&](const StageOps& o, uint32_t wst, int k0) {
+    if (DBG == 3 || DBG == 4) return;
+#pragma unroll
+    for (int rt = 0; rt < 2; ++rt) {
+      const uint4 wg = o.wgv[rt];
+      const uint4 wh = o.whv[rt];
+      const uint32_t wgw[4] = {wg.x, wg.y, wg.z, wg.w};
+      const uint32_t whw[4] = {wh.x, wh.y, wh.z, wh.w};
+      float part[GS][MT][4];
+      if (SACC) {
+#pragma unroll
+        for (int gi = 0; gi < GS; ++gi)
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) part[gi][mt][q] = 0.f;
       }
 #pragma unroll
-      for (int rt = 0; rt < 2; ++rt) {
-        const uint4 wg = wgv[rt];
-        const uint4 wh = whv[rt];
-        const uint32_t wgw[4] = {wg.x, wg.y, wg.z, wg.w};
-        const uint32_t whw[4] = {wh.x, wh.y, wh.z, wh.w};
-        float part[GS][MT][4];
-        if (SACC) {
-#pragma unroll
-          for (int gi = 0; gi < GS; ++gi)
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-              for (int q = 0; q < 4; ++q) part[gi][mt][q] = 0.f;
-        }
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          uint32_t sgs = 0, shs = 0;
-          if (!SACC) {  // small / odd groups: q*s in the activation dtype before the MMA
-            if (p.sc_rows) {  // the stage's scale rows (TMA-staged, read above)
-              sgs = scg[rt][w];
-              shs = sch[rt][w];
-            } else {
-              // past the end of K (the last, partial stage) the codes and activations are TMA zero
-              // fill: clamp to the last group so the scale read stays in bounds (and finite)
-              const int kw = min(k0 + t * SEG + w * (SEG / 4), p.K - 1);
-              const size_t j = (size_t)(kw / p.group) * N;
-              sgs = splat_scale<T>(S, j + ng[rt]);
-              shs = splat_scale<T>(S, j + nh[rt]);
-            }
-          }
-          float(*dst)[4] = SACC ? part[(w * GS) >> 2] : acc[rt];
-          if (BITS == 4) {
-            uint32_t qg[4], qh[4];
-            if (DBG == 2) {
-#pragma unroll
-              for (int q = 0; q < 4; ++q) { qg[q] = wgw[w] + q; qh[q] = whw[w] + q; }
-            } else if (NIB) {
-              i4_pairs_nib<TC>(wgw[w], qg);
-              i4_pairs_nib<TC>(whw[w], qh);
-            } else if (OFF != 0.f) {
-              i4_pairs_off<T>(wgw[w], qg);
-              i4_pairs_off<T>(whw[w], qh);
-            } else {
-              i4_pairs<T>(wgw[w], qg);
-              i4_pairs<T>(whw[w], qh);
-            }
-            if (!SACC) {
-#pragma unroll
-              for (int q = 0; q < 4; ++q) { qg[q] = mul2<T>(qg[q], sgs); qh[q] = mul2<T>(qh[q], shs); }
-            }
-#pragma unroll
-            for (int pp = 0; pp < 2; ++pp) {
-              const uint32_t a[4] = {qg[2 * pp], qh[2 * pp], qg[2 * pp + 1], qh[2 * pp + 1]};
-#pragma unroll
-              for (int mt = 0; mt < MT; ++mt) {
-                const uint4 bw = LAZY ? lds128(wst + aofs[mt][w]) : b[LAZY ? 0 : mt][w];
-                const uint32_t b0 = pp ? bw.z : bw.x;
-                const uint32_t b1 = pp ? bw.w : bw.y;
-                if (DBG == 1) {
-#pragma unroll
-                  for (int q = 0; q < 4; ++q) dst[mt][q] += __uint_as_float(a[q] ^ b0);
-                } else {
-                  mma16816<TC>(dst[mt], a, b0, b1);
-                }
-              }
-            }
+      for (int w = 0; w < 4; ++w) {
+        uint32_t sgs = 0, shs = 0;
+        if (!SACC) {  // small / odd groups: q*s in the activation dtype before the MMA
+          if (p.sc_rows) {  // the stage's scale rows (TMA-staged, read with the stage)
+            sgs = o.scg[rt][w];
+            shs = o.sch[rt][w];
           } else {
-            uint32_t qg[2], qh[2];
-            if (OFF != 0.f && Dt<T>::id == FQ_FP16) {
-              i8_pairs_off_half(wgw[w], qg);
-              i8_pairs_off_half(whw[w], qh);
-            } else {
-              i8_pairs<T>(wgw[w], qg);
-              i8_pairs<T>(whw[w], qh);
-            }
-            if (!SACC) {
+            // past the end of K (the last, partial stage) the codes and activations are TMA zero
+            // fill: clamp to the last group so the scale read stays in bounds (and finite)
+            const int kw = min(k0 + t * SEG + w * (SEG / 4), p.K - 1);
+            const size_t j = (size_t)(kw / p.group) * N;
+            sgs = splat_scale<T>(S, j + ng[rt]);
+            shs = splat_scale<T>(S, j + nh[rt]);
+          }
+        }
+        float(*dst)[4] = SACC ? part[(w * GS) >> 2] : acc[rt];
+        if (BITS == 4) {
+          uint32_t qg[4], qh[4];
+          if (DBG == 2) {
 #pragma unroll
-              for (int q = 0; q < 2; ++q) { qg[q] = mul2<T>(qg[q], sgs); qh[q] = mul2<T>(qh[q], shs); }
-            }
-            const uint32_t a[4] = {qg[0], qh[0], qg[1], qh[1]};
+            for (int q = 0; q < 4; ++q) { qg[q] = wgw[w] + q; qh[q] = whw[w] + q; }
+          } else if (NIB) {
+            i4_pairs_nib<TC>(wgw[w], qg);
+            i4_pairs_nib<TC>(whw[w], qh);
+          } else if (OFF != 0.f) {
+            i4_pairs_off<T>(wgw[w], qg);
+            i4_pairs_off<T>(whw[w], qh);
+          } else {
+            i4_pairs<T>(wgw[w], qg);
+            i4_pairs<T>(whw[w], qh);
+          }
+          if (!SACC) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) { qg[q] = mul2<T>(qg[q], sgs); qh[q] = mul2<T>(qh[q], shs); }
+          }
+#pragma unroll
+          for (int pp = 0; pp < 2; ++pp) {
+            const uint32_t a[4] = {qg[2 * pp], qh[2 * pp], qg[2 * pp + 1], qh[2 * pp + 1]};
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt) {
-              const uint4 bb = LAZY ? lds128(wst + aofs[mt][w >> 1]) : b[LAZY ? 0 : mt][w >> 1];
-              mma16816<T>(dst[mt], a, (w & 1) ? bb.z : bb.x, (w & 1) ? bb.w : bb.y);
+              const uint4 bw = LAZY ? lds128(wst + aofs[mt][w]) : o.b[LAZY ? 0 : mt][w];
+              const uint32_t b0 = pp ? bw.z : bw.x;
+              const uint32_t b1 = pp ? bw.w : bw.y;
+              if (DBG == 1) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) dst[mt][q] += __uint_as_float(a[q] ^ b0);
+              } else {
+                mma16816<TC>(dst[mt], a, b0, b1);
+              }
             }
           }
-        }
-        if (SACC) {
+        } else {
+          uint32_t qg[2], qh[2];
+          if (OFF != 0.f && Dt<T>::id == FQ_FP16) {
+            i8_pairs_off_half(wgw[w], qg);
+            i8_pairs_off_half(whw[w], qh);
+          } else {
+            i8_pairs<T>(wgw[w], qg);
+            i8_pairs<T>(whw[w], qh);
+          }
+          if (!SACC) {
 #pragma unroll
-          for (int gi = 0; gi < GS; ++gi)
+            for (int q = 0; q < 2; ++q) { qg[q] = mul2<T>(qg[q], sgs); qh[q] = mul2<T>(qh[q], shs); }
+          }
+          const uint32_t a[4] = {qg[0], qh[0], qg[1], qh[1]};
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt) {
-            float(&pp)[4] = part[gi][mt];
-            if (OFF != 0.f) {  // remove OFF * sum_k a[tok, k] (tokens 2t, 2t+1 of this MMA tile)
-              pp[0] = fmaf(-OFF, sa[mt][gi].x, pp[0]);
-              pp[1] = fmaf(-OFF, sa[mt][gi].y, pp[1]);
-              pp[2] = fmaf(-OFF, sa[mt][gi].x, pp[2]);
-              pp[3] = fmaf(-OFF, sa[mt][gi].y, pp[3]);
-            }
-            if (NIB) {  // undo the chunk's power-of-two activation scale
-              acc[rt][mt][0] = fmaf(sg[rt][gi] * iv[mt].x, pp[0], acc[rt][mt][0]);
-              acc[rt][mt][1] = fmaf(sg[rt][gi] * iv[mt].y, pp[1], acc[rt][mt][1]);
-              acc[rt][mt][2] = fmaf(sh[rt][gi] * iv[mt].x, pp[2], acc[rt][mt][2]);
-              acc[rt][mt][3] = fmaf(sh[rt][gi] * iv[mt].y, pp[3], acc[rt][mt][3]);
-            } else {
-              acc[rt][mt][0] = fmaf(sg[rt][gi], pp[0], acc[rt][mt][0]);
-              acc[rt][mt][1] = fmaf(sg[rt][gi], pp[1], acc[rt][mt][1]);
-              acc[rt][mt][2] = fmaf(sh[rt][gi], pp[2], acc[rt][mt][2]);
-              acc[rt][mt][3] = fmaf(sh[rt][gi], pp[3], acc[rt][mt][3]);
-            }
+            const uint4 bb = LAZY ? lds128(wst + aofs[mt][w >> 1]) : o.b[LAZY ? 0 : mt][w >> 1];
+            mma16816<T>(dst[mt], a, (w & 1) ? bb.z : bb.x, (w & 1) ? bb.w : bb.y);
           }
         }
       }
+      if (SACC) {
+#pragma unroll
+        for (int gi = 0; gi < GS; ++gi)
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            const float(&pp)[4] = part[gi][mt];
+            float p0 = pp[0], p1 = pp[1], p2 = pp[2], p3 = pp[3];
+            if (OFF != 0.f) {  // remove OFF * sum_k a[tok, k] (tokens 2t, 2t+1 of this MMA tile)
+              p0 = fmaf(-OFF, o.sa[mt][gi].x, p0);
+              p1 = fmaf(-OFF, o.sa[mt][gi].y, p1);
+              p2 = fmaf(-OFF, o.sa[mt][gi].x, p2);
+              p3 = fmaf(-OFF, o.sa[mt][gi].y, p3);
+            }
+            if (NIB) {  // undo the chunk's power-of-two activation scale
+              acc[rt][mt][0] = fmaf(o.sg[rt][gi] * o.iv[mt].x, p0, acc[rt][mt][0]);
+              acc[rt][mt][1] = fmaf(o.sg[rt][gi] * o.iv[mt].y, p1, acc[rt][mt][1]);
+              acc[rt][mt][2] = fmaf(o.sh[rt][gi] * o.iv[mt].x, p2, acc[rt][mt][2]);
+              acc[rt][mt][3] = fmaf(o.sh[rt][gi] * o.iv[mt].y, p3, acc[rt][mt][3]);
+            } else {
+              acc[rt][mt][0] = fmaf(o.sg[rt][gi], p0, acc[rt][mt][0]);
+              acc[rt][mt][1] = fmaf(o.sg[rt][gi], p1, acc[rt][mt][1]);
+              acc[rt][mt][2] = fmaf(o.sh[rt][gi], p2, acc[rt][mt][2]);
+              acc[rt][mt][3] = fmaf(o.sh[rt][gi], p3, acc[rt][mt][3]);
+            }
+          }
+      }
     }
-    if (!EARLY || DBG == 3 || DBG == 4) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_bar[s]);
+  };
+  auto release = [&](int s_) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[s_]);
+  };
+  // (A software-pipelined variant -- stage i+1's operands read and its slot released before stage i
+  // is computed -- was measured 40% slower on OPT-175B FC1/FC2 at M <= 8: profiles/r02/decode_pf_rejected.txt.)
+  int s = 0;
+  uint32_t ph = 0;
+  {
+    for (int i = 0; i < nst; ++i) {
+      const int k0 = kbeg + i * KS;
+      mbar_wait(&full_bar[s], ph);
+      const uint32_t wst = sb + s * STAGE_BYTES;
+      StageOps o;
+      load_ops(wst, o);
+      if (EARLY && DBG != 3 && DBG != 4) release(s);  // everything is in registers: hand the slot back
+      compute(o, wst, k0);
+      if (!EARLY || DBG == 3 || DBG == 4) release(s);
+      if (++s == NSTG) { s = 0; ph ^= 1; }
     }
-    if (++s == NSTG) { s = 0; ph ^= 1; }
   }
 
   // ------------------------------------------------------------- epilogue (+ fused A5 fixup)
@@ -787,9 +798,11 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
 // (a1,a5)/16, (a2,a6), (a3,a7)/16; cell c -> (c % 4) * 4 + c / 4, XOR (tok & 1) * 4), values
 // scaled by 2^e (bf16 input: the chunk max |a| lands in [2^14, 2^15); fp16 input: e = 0).
 // S'[chunk][tok] = {1032 * sum_even(a') + 72 * sum_odd(a'), 2^-e, same sum over k < 64, over k >= 64}.
-// GS (group-split consumers, group 64): pieces stay at cell c (XOR (tok & 1) * 4): the consumers'
+// MODE 1 (group-split consumers, group 64): pieces stay at cell c (XOR (tok & 1) * 4): the consumers'
 // word w of thread t is piece 4 w + t there.
-template <typename T, bool GS>
+// MODE 2 (tcgen05 decode, fq_decode_umma.cu): pieces stay at cell c (natural order, the UMMA
+// K-major operand layout is made by the TMA swizzle) and S'[chunk][tok] = {2^-e, -corr * 2^-e, 0, 0}.
+template <typename T, int MODE>
 __global__ void __launch_bounds__(128) prep_acts_kernel(const T* __restrict__ A, int ntok, int K,
                                                         __half* __restrict__ Ap, float* __restrict__ Sp) {
   griddep_wait();  // A may be the output of the previous kernel in the stream
@@ -843,9 +856,12 @@ __global__ void __launch_bounds__(128) prep_acts_kernel(const T* __restrict__ A,
   const uint4 o = make_uint4(h2(f[0], f[4]), h2(f[1] * 0.0625f, f[5] * 0.0625f), h2(f[2], f[6]),
                              h2(f[3] * 0.0625f, f[7] * 0.0625f));
   const int kl = l * 8, tq = kl >> 5, w16 = (kl & 31) >> 3;
-  const int cell = (GS ? l : (w16 * 4 + tq)) ^ ((tok & 1) << 2);
+  const int cell = MODE == 2 ? l : ((MODE == 1 ? l : (w16 * 4 + tq)) ^ ((tok & 1) << 2));
   *reinterpret_cast<uint4*>(Ap + base + cell * 8) = o;
-  if (l == 0) *reinterpret_cast<float4*>(Sp + ((size_t)ch * ntok + tok) * 4) = make_float4(sum, inv, half_sum, other);
+  if (l == 0) {
+    const float4 rec = MODE == 2 ? make_float4(inv, -sum * inv, 0.f, 0.f) : make_float4(sum, inv, half_sum, other);
+    *reinterpret_cast<float4*>(Sp + ((size_t)ch * ntok + tok) * 4) = rec;
+  }
 }
 
 // ------------------------------------------------------------------------------------- host side
@@ -916,20 +932,23 @@ size_t gemv_workspace_bytes(const GemvPlan& p, int M, int K, int N, int bits, in
 size_t gemv_grouped_workspace_bytes(int64_t T, int K, int bits) {
   return kCounterBytes + (bits == 4 ? prep_bytes((int)T, K) : 0);
 }
-template <bool GS>
+template <int MODE>
 static cudaError_t launch_prep_g(int adt, const void* A, int ntok, int K, void* Ap, void* Sp, cudaStream_t st) {
   const int blocks = (int)(((long long)ntok * (K / 128) + 7) / 8);
   if (blocks == 0) return cudaSuccess;
   if (adt == FQ_BF16)
-    return launch_pdl(prep_acts_kernel<__nv_bfloat16, GS>, blocks, 128, 0, st,
+    return launch_pdl(prep_acts_kernel<__nv_bfloat16, MODE>, blocks, 128, 0, st,
                       reinterpret_cast<const __nv_bfloat16*>(A), ntok, K, reinterpret_cast<__half*>(Ap),
                       reinterpret_cast<float*>(Sp));
-  return launch_pdl(prep_acts_kernel<__half, GS>, blocks, 128, 0, st, reinterpret_cast<const __half*>(A), ntok, K,
-                    reinterpret_cast<__half*>(Ap), reinterpret_cast<float*>(Sp));
+  return launch_pdl(prep_acts_kernel<__half, MODE>, blocks, 128, 0, st, reinterpret_cast<const __half*>(A), ntok,
+                    K, reinterpret_cast<__half*>(Ap), reinterpret_cast<float*>(Sp));
 }
 static cudaError_t launch_prep(int adt, const void* A, int ntok, int K, void* Ap, void* Sp, cudaStream_t st,
                                bool gs = false) {
-  return gs ? launch_prep_g<true>(adt, A, ntok, K, Ap, Sp, st) : launch_prep_g<false>(adt, A, ntok, K, Ap, Sp, st);
+  return gs ? launch_prep_g<1>(adt, A, ntok, K, Ap, Sp, st) : launch_prep_g<0>(adt, A, ntok, K, Ap, Sp, st);
+}
+cudaError_t launch_prep_umma(int adt, const void* A, int ntok, int K, void* Ap, void* Sp, cudaStream_t st) {
+  return launch_prep_g<2>(adt, A, ntok, K, Ap, Sp, st);
 }
 
 template <typename T, int BITS, int MT, int SACC, int DBG, int MAXP>
