@@ -178,11 +178,8 @@ fq_status fq_gemm(const void* A, int32_t adt, int64_t M, const fq_wdesc* d, cons
 /* Routing / plan overrides (tests, measurements).  Zero-initialised = fq_gemm's own plan. */
 typedef enum {
   FQ_PATH_AUTO = 0,
-  FQ_PATH_DECODE = 1,      /* a decode kernel (A4 / A4'), whichever the plan picks for M */
-  FQ_PATH_TC = 2,          /* the tcgen05 prefill kernel A6 */
-  FQ_PATH_DECODE_MMA = 3,  /* the mma.sync decode kernel A4 (any M: token tiles of <= 16/32 re-stream W) */
-  FQ_PATH_DECODE_UMMA = 4  /* the tcgen05 decode kernel A4' (int4, group % 128 == 0, K % 128 == 0, M <= 32;
-                              FQ_ERR_UNSUPPORTED otherwise) */
+  FQ_PATH_DECODE = 1,  /* the decode kernel A4 (any M: token tiles of <= 16/32 re-stream W) */
+  FQ_PATH_TC = 2       /* the tcgen05 kernel A6 */
 } fq_path;
 typedef struct {
   int32_t path;       /* fq_path */

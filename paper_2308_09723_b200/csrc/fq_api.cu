@@ -43,7 +43,7 @@ static fq_status to_tune(const fq_gemm_opts* o, Tune& t) {
   if (!o) return FQ_OK;
   for (int i = 0; i < 4; ++i)
     if (o->reserved[i]) return FQ_ERR_INVALID_ARG;
-  if (o->path < 0 || o->path > 4 || o->splits < 0 || o->splits > 4096 || o->tc_halves < 0 || o->tc_halves > 2 ||
+  if (o->path < 0 || o->path > 2 || o->splits < 0 || o->splits > 4096 || o->tc_halves < 0 || o->tc_halves > 2 ||
       o->tc_dqg < 0 || o->tc_dqg > 2)
     return FQ_ERR_INVALID_ARG;
   t.path = o->path;
@@ -65,20 +65,11 @@ static fq_status from_cuda(cudaError_t e) { return e == cudaSuccess ? FQ_OK : FQ
 // 56-69 -> 47-48, OPT-30B attn-out 40-50 -> 32, OPT-175B FC2 146 -> 131 (M = 32); matrices with
 // >= 148 tiles (OPT-175B FC1, OPT-13B FFN1, OPT-30B QKV / FFN1) stay on the decode kernel.
 static bool use_tc_path(int64_t M, int bits, int group, int64_t N, const Tune& t) {
-  if (t.path == 1 || t.path == 3 || t.path == 4) return false;
+  if (t.path == 1) return false;
   if (t.path == 2) return true;
   const int dmax = gemv_max_m(bits, group);
   if (M > dmax) return true;
   return M > 16 && N > 0 && tc_short_of_tiles((int)M, (int)N);
-}
-
-// Decode implementation: the mma.sync kernel A4 by default.  The tcgen05 kernel A4'
-// (fq_decode_umma.cu) runs only when forced (FQ_PATH_DECODE_UMMA): a tcgen05.mma of M = 128, K = 16
-// takes 64-80 cycles whatever N <= 128 (tools/umma_probe.cu, profiles/r02/umma_probe.txt), i.e.
-// <= 32 weights per cycle per SM, which caps a tcgen05 decode at ~2.8 TB/s (measured: 111 us on
-// OPT-175B FC1 at M = 1, against 61 us for A4; profiles/r02/decode_umma_diagnostics.txt).
-static bool use_umma(int64_t M, int64_t K, int bits, int group, const Tune& t) {
-  return t.path == 4 && dumma_supported((int)M, (int)K, bits, group);
 }
 
 static int ilog2_exact(int64_t x) {  // log2 of a power of two, else -1
@@ -244,7 +235,6 @@ fq_status fq_quantize_rowshard(const void* W_shard, int32_t wdt, const fq_wdesc*
 static size_t gemm_ws_bytes(int64_t M, const fq_wdesc* d, const Tune& t) {
   if (use_tc_path(M, d->bits, d->group, d->N, t))
     return gemm_tc_workspace_bytes((int)M, (int)d->K, (int)d->N, d->bits, t);
-  if (use_umma(M, d->K, d->bits, d->group, t)) return dumma_workspace_bytes((int)M, (int)d->K, (int)d->N, t.splits);
   const GemvPlan p = plan_gemv((int)M, (int)d->K, (int)d->N, d->bits, d->group, num_sms(), t.splits);
   return gemv_workspace_bytes(p, (int)M, (int)d->K, (int)d->N, d->bits, d->group);
 }
@@ -274,13 +264,6 @@ fq_status fq_gemm_ex(const void* A, int32_t adt, int64_t M, const fq_wdesc* d, c
   if (use_tc_path(M, d->bits, d->group, d->N, t))
     return from_cuda(run_gemm_tc(adt, cdt, d->bits, A, (int)M, (int)d->K, (int)d->N, codes, scales, d->group, C,
                                  ws, ws_bytes, as_stream(stream), t));
-  if (t.path == 4 && !use_umma(M, d->K, d->bits, d->group, t)) return FQ_ERR_UNSUPPORTED;
-  if (use_umma(M, d->K, d->bits, d->group, t)) {
-    const size_t need = dumma_workspace_bytes((int)M, (int)d->K, (int)d->N, t.splits);
-    if (!ws || ws_bytes < need) return FQ_ERR_WORKSPACE;
-    return from_cuda(run_dumma(adt, cdt, A, (int)M, (int)d->K, (int)d->N, codes, scales, d->group, C, ws,
-                               as_stream(stream), t.splits));
-  }
   const GemvPlan p = plan_gemv((int)M, (int)d->K, (int)d->N, d->bits, d->group, num_sms(), t.splits);
   const size_t need = gemv_workspace_bytes(p, (int)M, (int)d->K, (int)d->N, d->bits, d->group);
   if (need > 65536 && (!ws || ws_bytes < need)) return FQ_ERR_WORKSPACE;  // counters-only: may be NULL

@@ -800,8 +800,6 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
 // S'[chunk][tok] = {1032 * sum_even(a') + 72 * sum_odd(a'), 2^-e, same sum over k < 64, over k >= 64}.
 // MODE 1 (group-split consumers, group 64): pieces stay at cell c (XOR (tok & 1) * 4): the consumers'
 // word w of thread t is piece 4 w + t there.
-// MODE 2 (tcgen05 decode, fq_decode_umma.cu): pieces stay at cell c (natural order, the UMMA
-// K-major operand layout is made by the TMA swizzle) and S'[chunk][tok] = {2^-e, -corr * 2^-e, 0, 0}.
 template <typename T, int MODE>
 __global__ void __launch_bounds__(128) prep_acts_kernel(const T* __restrict__ A, int ntok, int K,
                                                         __half* __restrict__ Ap, float* __restrict__ Sp) {
@@ -856,12 +854,9 @@ __global__ void __launch_bounds__(128) prep_acts_kernel(const T* __restrict__ A,
   const uint4 o = make_uint4(h2(f[0], f[4]), h2(f[1] * 0.0625f, f[5] * 0.0625f), h2(f[2], f[6]),
                              h2(f[3] * 0.0625f, f[7] * 0.0625f));
   const int kl = l * 8, tq = kl >> 5, w16 = (kl & 31) >> 3;
-  const int cell = MODE == 2 ? l : ((MODE == 1 ? l : (w16 * 4 + tq)) ^ ((tok & 1) << 2));
+  const int cell = (MODE == 1 ? l : (w16 * 4 + tq)) ^ ((tok & 1) << 2);
   *reinterpret_cast<uint4*>(Ap + base + cell * 8) = o;
-  if (l == 0) {
-    const float4 rec = MODE == 2 ? make_float4(inv, -sum * inv, 0.f, 0.f) : make_float4(sum, inv, half_sum, other);
-    *reinterpret_cast<float4*>(Sp + ((size_t)ch * ntok + tok) * 4) = rec;
-  }
+  if (l == 0) *reinterpret_cast<float4*>(Sp + ((size_t)ch * ntok + tok) * 4) = make_float4(sum, inv, half_sum, other);
 }
 
 // ------------------------------------------------------------------------------------- host side
@@ -947,9 +942,7 @@ static cudaError_t launch_prep(int adt, const void* A, int ntok, int K, void* Ap
                                bool gs = false) {
   return gs ? launch_prep_g<1>(adt, A, ntok, K, Ap, Sp, st) : launch_prep_g<0>(adt, A, ntok, K, Ap, Sp, st);
 }
-cudaError_t launch_prep_umma(int adt, const void* A, int ntok, int K, void* Ap, void* Sp, cudaStream_t st) {
-  return launch_prep_g<2>(adt, A, ntok, K, Ap, Sp, st);
-}
+
 
 template <typename T, int BITS, int MT, int SACC, int DBG, int MAXP>
 static cudaError_t launch_dec(const DecBatch<MAXP>& b, int ctas, cudaStream_t st) {

@@ -49,17 +49,6 @@ cudaError_t run_gemv(const GemvPlan& p, int adt, int cdt, int bits, const void* 
                      int N, const void* codes, const void* scales, int group, void* C, void* ws,
                      cudaStream_t st);
 
-// Activation pre-conversion for the tcgen05 decode kernel (fq_gemv.cu prep_acts_kernel, MODE 2):
-// A'[tok][K] fp16 (per (token, 128-k chunk) power-of-two scaled, pieces in nibble-pair order) and
-// S'[K/128][ntok] = {2^-e, -corr * 2^-e, 0, 0}.  K % 128 == 0.
-cudaError_t launch_prep_umma(int adt, const void* A, int ntok, int K, void* Ap, void* Sp, cudaStream_t st);
-
-// Decode GEMM on tcgen05 (A4', fq_decode_umma.cu): int4, group % 128 == 0, K % 128 == 0, M <= 32.
-bool dumma_supported(int M, int K, int bits, int group);
-size_t dumma_workspace_bytes(int M, int K, int N, int splits_override);
-cudaError_t run_dumma(int adt, int cdt, const void* A, int M, int K, int N, const void* codes, const void* scales,
-                      int group, void* C, void* ws, cudaStream_t st, int splits_override);
-
 // MoE batch of decode problems (experts with 1 <= M_e <= 16), one launch per kernel class.
 cudaError_t run_gemv_grouped(int adt, int cdt, int bits, const void* A, int K, int N,
                              const int64_t* offsets, const int32_t* groups, const void* const* codes,

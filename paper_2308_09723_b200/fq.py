@@ -35,7 +35,7 @@ class fq_wdesc(ctypes.Structure):
                 ("group", ctypes.c_int32), ("scale_dtype", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
-FQ_PATH_AUTO, FQ_PATH_DECODE, FQ_PATH_TC, FQ_PATH_DECODE_MMA, FQ_PATH_DECODE_UMMA = 0, 1, 2, 3, 4
+FQ_PATH_AUTO, FQ_PATH_DECODE, FQ_PATH_TC = 0, 1, 2
 
 
 class fq_gemm_opts(ctypes.Structure):
@@ -46,8 +46,7 @@ class fq_gemm_opts(ctypes.Structure):
 
 def make_opts(path: str | int = 0, splits: int = 0, tc_halves: int = 0, tc_dqg: int = 0) -> fq_gemm_opts:
     if isinstance(path, str):
-        path = {"auto": FQ_PATH_AUTO, "decode": FQ_PATH_DECODE, "tc": FQ_PATH_TC,
-                "decode_mma": FQ_PATH_DECODE_MMA, "decode_umma": FQ_PATH_DECODE_UMMA}[path]
+        path = {"auto": FQ_PATH_AUTO, "decode": FQ_PATH_DECODE, "tc": FQ_PATH_TC}[path]
     return fq_gemm_opts(path, splits, tc_halves, tc_dqg)
 
 

@@ -147,7 +147,7 @@ def test_routing_is_environment_independent(fq, monkeypatch):
 def test_gemm_opts_validation(fq):
     dummy = ctypes.c_void_p(16)
     d = fq.make_wdesc(4096, 512, 4, 128, fq.FQ_BF16)
-    for bad in (fq.make_opts(5), fq.make_opts(0, -1), fq.make_opts(0, 0, 3), fq.make_opts(0, 0, 0, 5)):
+    for bad in (fq.make_opts(3), fq.make_opts(0, -1), fq.make_opts(0, 0, 3), fq.make_opts(0, 0, 0, 5)):
         assert fq._lib.fq_gemm_ex(dummy, 0, 4, ctypes.byref(d), dummy, dummy, dummy, 0, None, 0, None,
                                   ctypes.byref(bad)) == fq.FQ_ERR_INVALID_ARG
         assert fq._lib.fq_gemm_workspace_bytes_ex(4, ctypes.byref(d), ctypes.byref(bad)) == 0

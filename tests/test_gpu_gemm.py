@@ -369,73 +369,3 @@ def test_decode_kernels(fq, env, M, K, N, bits, group, adt, splits):
         _, C = run_case(fq, Wb, Ab, bits, group, adt, env=env)
         Cr, D = oracle_ref(Wb, Ab, bits, group, adt)
         assert O.rel_err(torch_to_f64(C), Cr, D) <= TOL
-
-
-@pytest.mark.parametrize("M,K,N,adt,cdt,splits", [
-    (1, 1024, 512, "bf16", None, 0),
-    (3, 1536, 776, "bf16", None, 0),      # ragged N tail inside the second 128-row half
-    (8, 2048, 264, "fp16", None, 3),
-    (9, 4096, 512, "bf16", "fp32", 0),
-    (16, 4096, 768, "bf16", None, 5),     # split-K, last split shorter
-    (17, 1024, 1032, "fp16", None, 0),    # NT = 32 token tile
-    (32, 2048, 512, "bf16", "fp32", 2),
-    (12, 12288, 1024, "bf16", None, 0),   # OPT-175B K
-    (5, 256, 256, "bf16", None, 0),       # two stages (one group of 256)
-])
-@pytest.mark.parametrize("group", [128, 256])
-def test_decode_umma_parity(fq, env, M, K, N, adt, cdt, splits, group):
-    """tcgen05 decode kernel A4' (fq_decode_umma.cu) forced: every token-tile width, ragged N,
-    split-K (incl. a shorter last split), fp16 / bf16, fp32 output; repeated calls bit-identical."""
-    env("path", "decode_umma")
-    if splits:
-        env("splits", splits)
-    Wb, Ab = make_case(M, K, N, 4, group, adt, seed=M * 13 + K + N, outliers=1)
-    _, C0 = run_case(fq, Wb, Ab, 4, group, adt, cdt, env=env)
-    _, C1 = run_case(fq, Wb, Ab, 4, group, adt, cdt, env=env)
-    assert torch.equal(C0, C1)
-    Cr, D = oracle_ref(Wb, Ab, 4, group, adt)
-    assert O.rel_err(torch_to_f64(C0), Cr, D) <= TOL
-
-
-@pytest.mark.parametrize("adt", ["bf16", "fp16"])
-@pytest.mark.parametrize("M", [1, 13, 32])
-def test_decode_umma_dynamic_range(fq, env, M, adt):
-    """A4' with activations spanning ~2^-90..2^90 (per-(token, chunk) power-of-two re-encoding),
-    zero chunks and a zero token (D == 0 requires C == 0 exactly)."""
-    env("path", "decode_umma")
-    lo, hi, shift = (-60.0, 60.0, 30) if adt == "bf16" else (-8.0, 6.0, 4)
-    K, N = 1024, 512
-    Wb = gaussian_bits((N, K), 0.02, 1235, "bf16")
-    Ab = wide_range_activations_bits(M, K, 4322 + M, adt, lo, hi, shift)
-    _, C = run_case(fq, Wb, Ab, 4, 128, adt, "fp32", env=env)
-    Cr, D = oracle_ref(Wb, Ab, 4, 128, adt)
-    assert O.rel_err(torch_to_f64(C), Cr, D) <= TOL
-
-
-def test_decode_umma_identity_exact(fq):
-    """A = I in 16-token blocks through A4': C[k, n] = q[n,k] * s[k/g, n] exactly (fp32 output) --
-    integer-code partials, power-of-two activation scales and the fp32 fold are all exact."""
-    K = N = 256
-    Wb = gaussian_bits((N, K), 0.02, 6)
-    W = bits_to_torch(Wb, "bf16")
-    o = fq.make_opts("decode_umma")
-    for group in (128, 256):
-        qw = fq.quantize(W, 4, group)
-        r = O.quantize(O.decode_bits(Wb, "bf16"), 4, group, O.BF16)
-        ref = O.dequantize(r.q, r.s, group).T
-        eye = torch.eye(K, dtype=torch.bfloat16, device="cuda")
-        for m0 in range(0, K, 16):
-            C = fq.gemm(eye[m0:m0 + 16].contiguous(), qw, out_dtype=torch.float32, opts=o)
-            assert np.array_equal(torch_to_f64(C), ref[m0:m0 + 16])
-
-
-def test_decode_umma_unsupported(fq):
-    """Forcing A4' where it does not apply is FQ_ERR_UNSUPPORTED, not a silent fallback."""
-    W = bits_to_torch(gaussian_bits((256, 512), 0.02, 7), "bf16")
-    A = bits_to_torch(activations_bits(4, 512, 8), "bf16")
-    for bits, group, M in ((8, 128, 4), (4, 64, 4), (4, 128, 33)):
-        qw = fq.quantize(W, bits, group)
-        Am = bits_to_torch(activations_bits(M, 512, 8), "bf16")
-        with pytest.raises(fq.FQError) as ei:
-            fq.gemm(Am, qw, opts=fq.make_opts("decode_umma"))
-        assert ei.value.status == fq.FQ_ERR_UNSUPPORTED

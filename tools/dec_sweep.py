@@ -1,6 +1,6 @@
 """Time fq_gemm decode (M = 1..32) on OPT-175B FC1/FC2 int4 g128 (int8 with --bits 8), per path.
 
-    python tools/dec_sweep.py --paths decode_mma decode_umma --M 1 8 16 32 [--splits S]
+    python tools/dec_sweep.py --paths decode --M 1 8 16 32 [--splits S]
 Each GEMM is repeated back to back (weights 311 MB > L2, so no flush is needed)."""
 import argparse, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
