@@ -190,6 +190,7 @@ def main():
     ap.add_argument("--impl", default="fq", choices=["fq", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-tp-layer", action="store_true")
     # SURVEY §5 knobs: headline GEMM precision / group; adaptive parameters of the MoE extras
     ap.add_argument("--bits", type=int, default=4, choices=[4, 8])
     ap.add_argument("--group", type=int, default=128)
@@ -398,11 +399,17 @@ def main():
             "per_launch_us": {n: round(v * 1e3, 2) for n, v in per.items()},
             "allreduce_us_per_step": round(comm * 1e3, 2)}
 
+    # ---- configs[4]: the full OPT-175B layer under TP (every N, all ranks): QKV col, out row + AR,
+    # FC1 col, FC2 row + AR; 4 distinct layers rotated; layer time and all-reduce share per M.
+    del xs, ys, zs, d_x, h_x
+    q1 = q2 = None
+    torch.cuda.empty_cache()
+    tp_layer = None
+    if not args.no_tp_layer:
+        tp_layer = measure_tp_layer(fq, dev, world, rank, args)
+
     extras = {}
     if rank == 0 and world == 1 and not args.no_extras:
-        del xs, ys, zs
-        q1 = q2 = None
-        torch.cuda.empty_cache()
         extras = measure_extras(fq, dev, peaks, args)
 
     line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -416,6 +423,8 @@ def main():
             "clocks": clocks, "e2e": {"value": round(e2e_value, 4), "unit": UNIT,
                                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": LAUNCHES_PER_GEMM * 2 * len(M_SWEEP) * args.steps, "roofline": roof}
+    if tp_layer:
+        line["tp_layer"] = tp_layer
     if extras:
         line["extras"] = extras
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -427,6 +436,94 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def measure_tp_layer(fq, dev, world, rank, args, n_layers=4, Ms=(1, 16, 2048), reps=10):
+    """configs[4]: one OPT-175B decoder layer's GEMM chain under tensor parallelism (tp.TPOptLayer):
+    QKV [3h, h] column-parallel -> out-proj [h, h] row-parallel + all-reduce -> FC1 [4h, h]
+    column-parallel -> FC2 [h, 4h] row-parallel + all-reduce, int4 g128, h = 12288.  Four
+    distinct layers rotated (> L2 at every t).  layer_us = CUDA-event time per layer (max over
+    ranks); comm_us = the layer's two all-reduces timed alone on the same stream; comm_frac =
+    comm_us / layer_us; TB_s = the whole layer's effective weight bytes (all shards) / layer time."""
+    import torch
+    import torch.distributed as dist
+    from paper_2308_09723_b200.tp import ShardSpec, TPLinearFQ, TPOptLayer, shard_bounds
+    from synth import gaussian_torch
+    h = 12288
+    shapes = dict(qkv=(3 * h, h, "col"), out=(h, h, "row"), fc1=(4 * h, h, "col"), fc2=(h, 4 * h, "row"))
+    pg = dist.group.WORLD if world > 1 else None
+    layers = []
+    full_bytes = 0
+    for li in range(n_layers):
+        lin = {}
+        for j, (name, (n, k, kind)) in enumerate(shapes.items()):
+            W = gaussian_torch((n, k), 0.02, args.seed + 100 * li + j, device=dev)
+            if kind == "col":
+                lo, hi = shard_bounds(n, world, rank)
+                Ws = W[lo:hi].contiguous()
+            else:
+                lo, hi = shard_bounds(k, world, rank, 32)
+                Ws = W[:, lo:hi].contiguous()
+            del W
+            lin[name] = TPLinearFQ(Ws, ShardSpec(kind, k, n, world, rank), 4, 128, process_group=pg)
+            del Ws
+            full_bytes += eff_bytes(k, n, 4, 128) if li == 0 else 0
+        layers.append(TPOptLayer(lin["qkv"], lin["out"], lin["fc1"], lin["fc2"], process_group=pg))
+    torch.cuda.empty_cache()
+    stream = torch.cuda.current_stream()
+    out = {"layers": n_layers, "h": h, "bits": 4, "group": 128, "tp": world,
+           "weight_bytes_per_layer_all_ranks": full_bytes,
+           "weight_bytes_per_layer_per_rank": sum(l.weight_bytes for l in layers) // n_layers}
+    for M in Ms:
+        x = gaussian_torch((M, h), 1.0, 2000 + M, device=dev)
+        parts = [torch.empty((M, h), dtype=torch.float32, device=dev) for _ in range(2)]
+
+        def chain():
+            for L in layers:
+                L.forward(x)
+
+        def comms():
+            for _ in layers:
+                for t_ in parts:
+                    dist.all_reduce(t_, op=dist.ReduceOp.SUM, group=pg)
+
+        for _ in range(2):
+            chain()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            chain()
+        b.record(stream)
+        torch.cuda.synchronize()
+        lay = a.elapsed_time(b) / (reps * n_layers) * 1e3
+        com = 0.0
+        if world > 1:
+            comms()
+            torch.cuda.synchronize()
+            dist.barrier()
+            a.record(stream)
+            for _ in range(reps):
+                comms()
+            b.record(stream)
+            torch.cuda.synchronize()
+            com = a.elapsed_time(b) / (reps * n_layers) * 1e3
+        tt = torch.tensor([lay, com], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        lay, com = float(tt[0]), float(tt[1])
+        ent = {"layer_us": round(lay, 1), "comm_us": round(com, 1), "comm_frac": round(com / lay, 3),
+               "TB_s": round(full_bytes / (lay * 1e-6) / 1e12, 3)}
+        if M >= 256:
+            fl = 2.0 * M * full_bytes / (0.5 + 2 / 128)  # 2 M FLOP per weight (full layer)
+            ent["TFLOP_s"] = round(fl / (lay * 1e-6) / 1e12, 1)
+        out[f"M={M}"] = ent
+        del x, parts
+    del layers
+    torch.cuda.empty_cache()
+    return out
 
 
 def measure_extras(fq, dev, peaks, args):
