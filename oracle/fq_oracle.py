@@ -16,6 +16,12 @@ Parity status per function (see DESIGN.md §2 and tests/test_oracle_*.py):
                                                     exact round-trip construction, error-bound invariants,
                                                     exact-rational brute force)
   pack_codes / unpack_codes ....................... pinned (hand bytes 0xC2 0x86, round-trip law)
+  pack_bitstream / unpack_bitstream (int3/int2) ... pinned (hand-packed int3 bytes tests/golden/int3_hand.txt,
+                                                    equals the independent int4/int8 packers at b=4/8,
+                                                    round-trip law)
+  quantize_acts_i8 / quantize_intscale / gemm_i8 .. pinned (hand-worked tests/golden/intscale_hand.txt,
+  (int8-activation x int4-weight, integer scales)   exact round-trip construction, numpy float32 IEEE
+                                                    division, exact-rational brute force, invariants)
   adapt_ladder / adapt_group_size ................. pinned on SPEC fixtures + invariants only;
                                                     paper parity UNPINNED (the paper prints no
                                                     worked example and its inequality is ambiguous, R6)
@@ -201,7 +207,9 @@ def pack_codes(q: np.ndarray, bits: int) -> np.ndarray:
         lo = (q[:, 0::2] & 0xF).astype(np.uint8)
         hi = (q[:, 1::2] & 0xF).astype(np.uint8)
         return (lo | (hi << 4)).astype(np.uint8)
-    raise ValueError("only 4/8-bit packing has kernels (PAPER.md:360)")
+    if bits in (2, 3):
+        return pack_bitstream(q, bits)
+    raise ValueError("bits")
 
 
 def unpack_codes(codes: np.ndarray, bits: int, K: int) -> np.ndarray:
@@ -218,7 +226,42 @@ def unpack_codes(codes: np.ndarray, bits: int, K: int) -> np.ndarray:
         out[:, 0::2] = lo
         out[:, 1::2] = hi
         return out
+    if bits in (2, 3):
+        return unpack_bitstream(codes, bits, K)
     raise ValueError("bits")
+
+
+def pack_bitstream(q: np.ndarray, bits: int) -> np.ndarray:
+    """Little-endian bit stream per column: code k of column n occupies
+    bits [b*k, b*k + b) of the column's stream, least significant bit first, two's complement;
+    byte i of the column = stream bits [8i, 8i + 8).  int4 / int8 are the special cases above.
+    Used for the int3 / int2 codes of the paper's low-bit variants (PAPER.md:332-346,
+    tab:optiml-mt), for which the paper ships no kernel and no layout.
+    Requires K * bits % 8 == 0 (every column a whole number of bytes)."""
+    q = np.asarray(q).astype(np.int64)
+    N, K = q.shape
+    assert (K * bits) % 8 == 0
+    out = np.zeros((N, K * bits // 8), dtype=np.uint8)
+    mask = (1 << bits) - 1
+    for k in range(K):                      # plain loop over code positions, bit by bit
+        f = q[:, k] & mask                  # the b-bit two's-complement field
+        for b in range(bits):
+            pos = bits * k + b
+            out[:, pos // 8] |= (((f >> b) & 1) << (pos % 8)).astype(np.uint8)
+    return out
+
+
+def unpack_bitstream(codes: np.ndarray, bits: int, K: int) -> np.ndarray:
+    codes = np.asarray(codes, dtype=np.uint8)
+    N = codes.shape[0]
+    out = np.zeros((N, K), dtype=np.int64)
+    for k in range(K):
+        f = np.zeros(N, dtype=np.int64)
+        for b in range(bits):
+            pos = bits * k + b
+            f |= ((codes[:, pos // 8].astype(np.int64) >> (pos % 8)) & 1) << b
+        out[:, k] = np.where(f >= (1 << (bits - 1)), f - (1 << bits), f)
+    return out.astype(np.int8)
 
 
 # ----------------------------------------------------------------------------------------------
@@ -354,3 +397,107 @@ def gemm_grouped(A: np.ndarray, offsets: np.ndarray, experts: list, cols=None):
         if hi > lo:
             C[lo:hi], D[lo:hi] = gemm(A[lo:hi], q, s, g, cols)
     return C, D
+
+
+# ----------------------------------------------------------------------------------------------
+# int8 activations x int4 weights with INTEGER group scales -- the paper's stated future work:
+# "the proposed method does not leverage integer instructions even when they are available"
+# (§5) and "using int8 activations and int4 weights with integer scales for
+# fine-grained quantization" (§5).  Readings (R15-R19):
+#   weights: App. A's fine scale s_j = 2 amax_j / (2^b - 1) is re-expressed as
+#     sigma[n] * z[j, n]: sigma = a per-column fp32 scale, z an integer in [1, Z] (Z = 16 for
+#     int4: |q * z| <= 128 fits a signed byte, so dequantized weights are int8 and the whole
+#     K-reduction is one exact integer dot product);
+#       sigma[n] = RN_fp32( 2 * max_j amax_j / ((2^b - 1) * Z) )
+#       z[j, n]  = clamp( ceil( (2 amax_j / (2^b - 1)) / sigma[n] ), 1, Z )   (effective scale >= s_j)
+#       q[n, k]  = clamp( integer( W[n,k] / (sigma[n] z[j,n]) ), -2^(b-1), 2^(b-1) - 1 )
+#     both decisions (ceil, integer) taken in float64 (sigma * z is exact there);
+#   activations: per-token (row) symmetric int8, App. A applied to the row with b = 8 and the
+#     symmetric range [-127, 127]: s_a[m] = RN_fp32(amax_m / 127),
+#     a_q = clamp(integer(fp32(A / s_a)), -127, 127), the division in IEEE fp32 (the kernel's precision);
+#   GEMM: acc[m, n] = sum_k a_q[m,k] * q[n,k] * z[k/g, n]  (exact integer), C = acc * s_a[m] * sigma[n].
+# ----------------------------------------------------------------------------------------------
+
+INTSCALE_Z = 16
+
+
+@dataclass
+class ActQuant:
+    a_q: np.ndarray        # int8 [M, K]
+    s_a: np.ndarray        # float64 [M] (fp32 values)
+    status: int            # 0 ok; 1 non-finite input row(s) (their codes and scale are 0)
+
+
+def quantize_acts_i8(A: np.ndarray) -> ActQuant:
+    """Per-token symmetric int8 activation quantization (R17): s_a = RN_fp32(amax / 127) and
+    a_q = clamp(integer(A / s_a), -127, 127) with the quotient an IEEE fp32 division (numpy float32
+    arithmetic is IEEE: one correctly rounded division) and integer() = round half away (R1)."""
+    A = np.asarray(A, dtype=np.float64)
+    M, K = A.shape
+    fin = np.isfinite(A).all(axis=1)
+    Az = np.where(fin[:, None], A, 0.0)
+    amax = np.abs(Az).max(axis=1) if K else np.zeros(M)
+    # amax / 127 has a periodic binary expansion (period 7) unless exact, so the float64 quotient
+    # is never an fp32 rounding midpoint: one more rounding equals the fp32 division (DESIGN R17)
+    s_a = round_to_format(amax / 127.0, FP32)
+    a32 = Az.astype(np.float32)
+    s32 = s_a.astype(np.float32)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        y = np.where(s32[:, None] > 0, a32 / np.where(s32 > 0, s32, np.float32(1))[:, None], np.float32(0))
+    a_q = np.clip(round_half_away(y.astype(np.float64)), -127, 127).astype(np.int8)
+    return ActQuant(a_q=a_q, s_a=s_a, status=0 if fin.all() else 1)
+
+
+@dataclass
+class IntScaleQuant:
+    q: np.ndarray          # int8 [N, K] codes in [-2^(b-1), 2^(b-1)-1]
+    z: np.ndarray          # uint8 [G, N] integer group scales in [1, Z]
+    sigma: np.ndarray      # float64 [N] per-column scales (fp32 values)
+    status: int            # 0 ok; 1 non-finite input (column gets sigma 0, codes 0)
+
+
+def quantize_intscale(W: np.ndarray, bits: int, group: int, Z: int = INTSCALE_Z) -> IntScaleQuant:
+    """Group-wise linear absmax quantization with integer group scales (R15/R16), W[N, K]."""
+    W = np.asarray(W, dtype=np.float64)
+    N, K = W.shape
+    if bits != 4:
+        raise ValueError("integer group scales are defined for int4 weights (|q z| <= 128)")
+    if group <= 0 or K % group:
+        raise ValueError("group must divide K")
+    G = K // group
+    qmax = (1 << bits) - 1                                  # 2^b - 1 (App. A denominator)
+    fin = np.isfinite(W).all(axis=1)                         # [N]
+    Wz = np.where(fin[:, None], W, 0.0)
+    amax = group_amax(Wz, group)                             # [G, N], exact
+    amax_col = amax.max(axis=0)                              # [N]
+    # 2 amax / (15 * 16) = amax / 120: periodic expansion (1/15), never an fp32 midpoint (R16)
+    sigma = round_to_format(2.0 * amax_col / float(qmax * Z), FP32)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        ratio = np.where(sigma > 0, (2.0 * amax) / (float(qmax) * np.where(sigma > 0, sigma, 1.0)), 0.0)
+    z = np.clip(np.ceil(ratio), 1, Z).astype(np.int64)      # [G, N]
+    S = sigma[None, :] * z                                   # effective group scale, exact in float64
+    S_full = np.repeat(S.T, group, axis=1)                   # [N, K]
+    with np.errstate(divide="ignore", invalid="ignore"):
+        y = np.where(S_full > 0, Wz / np.where(S_full > 0, S_full, 1.0), 0.0)
+    lo, hi = -(1 << (bits - 1)), (1 << (bits - 1)) - 1
+    q = np.clip(round_half_away(y), lo, hi).astype(np.int8)
+    return IntScaleQuant(q=q, z=z.astype(np.uint8), sigma=sigma, status=0 if fin.all() else 1)
+
+
+def gemm_i8(a_q: np.ndarray, s_a: np.ndarray, q: np.ndarray, z: np.ndarray, sigma: np.ndarray, group: int,
+            cols=None):
+    """acc[m, n] = sum_k a_q[m,k] * q[n,k] * z[k//g, n] as an exact integer (int64), then
+    C[m, n] = acc * s_a[m] * sigma[n] in float64 and D[m, n] = sum_k |same terms| * s_a * sigma.
+    Returns (C, D, acc)."""
+    a = np.asarray(a_q, dtype=np.int64)
+    q = np.asarray(q, dtype=np.int64)
+    z = np.asarray(z, dtype=np.int64)
+    sigma = np.asarray(sigma, dtype=np.float64)
+    if cols is not None:
+        cols = np.asarray(cols)
+        q, z, sigma = q[cols], z[:, cols], sigma[cols]
+    wz = q * np.repeat(z.T, group, axis=1)                   # [n, K] integers q * z
+    acc = a @ wz.T                                           # exact int64
+    dabs = np.abs(a) @ np.abs(wz).T
+    sc = np.asarray(s_a, dtype=np.float64)[:, None] * sigma[None, :]
+    return acc.astype(np.float64) * sc, dabs.astype(np.float64) * sc, acc
