@@ -472,6 +472,7 @@ def quantize_intscale(W: np.ndarray, bits: int, group: int, Z: int = INTSCALE_Z)
     amax_col = amax.max(axis=0)                              # [N]
     # 2 amax / (15 * 16) = amax / 120: periodic expansion (1/15), never an fp32 midpoint (R16)
     sigma = round_to_format(2.0 * amax_col / float(qmax * Z), FP32)
+    sigma = np.where(fin, sigma, 0.0)                        # non-finite column: sigma 0, codes 0 (R5)
     with np.errstate(divide="ignore", invalid="ignore"):
         ratio = np.where(sigma > 0, (2.0 * amax) / (float(qmax) * np.where(sigma > 0, sigma, 1.0)), 0.0)
     z = np.clip(np.ceil(ratio), 1, Z).astype(np.int64)      # [G, N]

@@ -148,6 +148,17 @@ def test_intscale_invariants():
     assert np.all(np.abs(W - Wd)[inner] <= np.repeat(S.T, 64, axis=1)[inner] / 2 * (1 + 1e-12))
 
 
+def test_intscale_nonfinite_and_zero_columns():
+    W = O.decode_bits(gaussian_bits((4, 128), 0.02, 2), "bf16")
+    W[1, 5] = np.inf
+    W[2] = 0.0
+    r = O.quantize_intscale(W, 4, 32)
+    assert r.status == 1
+    assert r.sigma[1] == 0 and np.all(r.q[1] == 0) and np.all(r.z[:, 1] == 1)
+    assert r.sigma[2] == 0 and np.all(r.q[2] == 0) and np.all(r.z[:, 2] == 1)
+    assert r.sigma[0] > 0 and r.sigma[3] > 0
+
+
 def test_gemm_i8_brute_force():
     rng = np.random.default_rng(8)
     M, N, K, g = 3, 5, 64, 16
