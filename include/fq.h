@@ -215,6 +215,44 @@ fq_status fq_gemm_grouped(const void* A, int32_t adt, int64_t T, const int64_t* 
                           const void* const* codes_host, const void* const* scales_host, void* C,
                           int32_t cdt, void* ws, size_t ws_bytes, void* stream);
 
+/* ---------------------------------------------------------------------------------------------
+ * int8 activations x int4 weights with INTEGER group scales -- the paper's future work: "the
+ * proposed method does not leverage integer instructions even when they are available" (§5),
+ * "using int8 activations and int4 weights with integer scales for fine-grained quantization"
+ * (§5).  Readings R15-R18.  Shapes: K % 128 == 0, K <= 65536, N % 16 == 0,
+ * K % group == 0 and group in {32, 64} or group % 128 == 0 (else FQ_ERR_SHAPE).
+ *   weights (offline, fq_quantize_intscale), W [N, K] of dtype wdt:
+ *     sigma[n] = RN_fp32(2 max_k |W[n,k]| / (15 * 16))                     colscale: fp32 [N]
+ *     z[j,n]   = clamp(ceil((2 max_{k in j} |W[n,k]| / 15) / sigma[n]), 1, 16)   zscales: u8 [G, N]
+ *     q[n,k]   = clamp(round_half_away(W[n,k] / (sigma[n] z[j,n])), -8, 7)  codes: canonical int4
+ *     (z and q decided in float64, where sigma*z is exact); a non-finite column gets sigma 0,
+ *     z 1, codes 0 and sets bit 0 of status_dev (nullable).
+ *   activations (every call, fq_quantize_acts_i8), A [M, K] of dtype adt (K % 8 == 0):
+ *     s_a[m] = RN_fp32(max_k |A[m,k]| / 127)                               a_scale: fp32 [M]
+ *     a_q[m,k] = clamp(round_half_away(fp32(A[m,k] / s_a[m])), -127, 127)   a_q: int8 [M, K]
+ *     rowsum[m] = sum_k a_q[m,k]                                           a_rowsum: int32 [M]
+ *     a_q layout: row-major [M, K] with each aligned 8-element word k-interleaved, even k first:
+ *     byte 8j + i holds k = 8j + 2i and byte 8j + 4 + i holds k = 8j + 2i + 1 (i < 4) -- the
+ *     order in which the GEMM unpacks int4 codes, so its dequantization needs no byte shuffles.
+ *     (IEEE fp32 division); a non-finite row gets s_a 0, codes 0 and sets status bit 0.  The GEMM
+ *     feeds the weights to the tensor core as unsigned bytes q*z + 128 and removes 128*rowsum[m].
+ *   GEMM (fq_gemm_i8, tcgen05 kind::i8):
+ *     acc[m,n] = sum_k a_q[m,k] * q[n,k] * z[k/group, n]   (exact int32)
+ *     C[m,n]   = fp32(acc) * s_a[m] * sigma[n], rounded to cdt (BF16, FP16 or FP32)   C: [M, N]
+ *   ws: fq_gemm_i8_workspace_bytes(M, K, N) bytes, zero-filled once (64 KiB of self-resetting
+ *   split-K counters + int32 partials; same contract as fq_gemm's ws); NULL / short disables the
+ *   K split.  M == 0: nothing launched, FQ_OK.
+ * ------------------------------------------------------------------------------------------- */
+size_t fq_zscales_bytes(int64_t K, int64_t N, int32_t group);
+fq_status fq_quantize_intscale(const void* W, int32_t wdt, int64_t K, int64_t N, int32_t group, void* codes,
+                               void* zscales, float* colscale, int32_t* status_dev, void* stream);
+fq_status fq_quantize_acts_i8(const void* A, int32_t adt, int64_t M, int64_t K, void* a_q, float* a_scale,
+                              int32_t* a_rowsum, int32_t* status_dev, void* stream);
+size_t fq_gemm_i8_workspace_bytes(int64_t M, int64_t K, int64_t N);
+fq_status fq_gemm_i8(const void* a_q, const float* a_scale, const int32_t* a_rowsum, int64_t M, int64_t K,
+                     int64_t N, int32_t group, const void* codes, const void* zscales, const float* colscale,
+                     void* C, int32_t cdt, void* ws, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -426,6 +426,7 @@ class ActQuant:
     a_q: np.ndarray        # int8 [M, K]
     s_a: np.ndarray        # float64 [M] (fp32 values)
     status: int            # 0 ok; 1 non-finite input row(s) (their codes and scale are 0)
+    rowsum: np.ndarray = None  # int64 [M] = sum_k a_q[m, k] (plain definition)
 
 
 def quantize_acts_i8(A: np.ndarray) -> ActQuant:
@@ -445,7 +446,7 @@ def quantize_acts_i8(A: np.ndarray) -> ActQuant:
     with np.errstate(divide="ignore", invalid="ignore"):
         y = np.where(s32[:, None] > 0, a32 / np.where(s32 > 0, s32, np.float32(1))[:, None], np.float32(0))
     a_q = np.clip(round_half_away(y.astype(np.float64)), -127, 127).astype(np.int8)
-    return ActQuant(a_q=a_q, s_a=s_a, status=0 if fin.all() else 1)
+    return ActQuant(a_q=a_q, s_a=s_a, status=0 if fin.all() else 1, rowsum=a_q.astype(np.int64).sum(axis=1))
 
 
 @dataclass

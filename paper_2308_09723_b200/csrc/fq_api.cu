@@ -324,4 +324,56 @@ fq_status fq_gemm_grouped(const void* A, int32_t adt, int64_t T, const int64_t* 
   return FQ_OK;
 }
 
+// ------------------------------------------------------------------------------------------------
+// int8 activations x int4 weights with integer group scales (fq_i8.cu)
+static fq_status check_i8_shape(int64_t K, int64_t N, int32_t group) {
+  if (K <= 0 || N <= 0 || K % 128 || K > 65536 || N % 16 || N > ((int64_t)1 << 24)) return FQ_ERR_SHAPE;
+  if (group <= 0 || group % 32 || K % group) return FQ_ERR_SHAPE;
+  if (group % 128 && 128 % group) return FQ_ERR_SHAPE;  // 32, 64 or a multiple of 128
+  return FQ_OK;
+}
+
+size_t fq_zscales_bytes(int64_t K, int64_t N, int32_t group) {
+  if (check_i8_shape(K, N, group) != FQ_OK) return 0;
+  return (size_t)((K / group) * N);
+}
+
+fq_status fq_quantize_intscale(const void* W, int32_t wdt, int64_t K, int64_t N, int32_t group, void* codes,
+                               void* zscales, float* colscale, int32_t* status_dev, void* stream) {
+  if (!W || !codes || !zscales || !colscale || !valid_dtype(wdt)) return FQ_ERR_INVALID_ARG;
+  const fq_status s = check_i8_shape(K, N, group);
+  if (s != FQ_OK) return s;
+  return from_cuda(run_quantize_intscale(wdt, W, (int)K, (int)N, group, codes, zscales, colscale, status_dev,
+                                         as_stream(stream)));
+}
+
+fq_status fq_quantize_acts_i8(const void* A, int32_t adt, int64_t M, int64_t K, void* a_q, float* a_scale,
+                              int32_t* a_rowsum, int32_t* status_dev, void* stream) {
+  if (!valid_dtype(adt)) return FQ_ERR_INVALID_ARG;
+  if (M < 0 || M > (1 << 20) || K <= 0 || K % 8 || K > (1 << 20)) return FQ_ERR_SHAPE;
+  if (M == 0) return FQ_OK;
+  if (!A || !a_q || !a_scale || !a_rowsum) return FQ_ERR_INVALID_ARG;
+  return from_cuda(
+      run_quantize_acts_i8(adt, A, (int)M, (int)K, a_q, a_scale, a_rowsum, status_dev, as_stream(stream)));
+}
+
+size_t fq_gemm_i8_workspace_bytes(int64_t M, int64_t K, int64_t N) {
+  if (M <= 0 || M > (1 << 20) || check_i8_shape(K, N, 32) != FQ_OK) return 0;
+  return gemm_i8_workspace_bytes((int)M, (int)K, (int)N);
+}
+
+fq_status fq_gemm_i8(const void* a_q, const float* a_scale, const int32_t* a_rowsum, int64_t M, int64_t K,
+                     int64_t N, int32_t group, const void* codes, const void* zscales, const float* colscale,
+                     void* C, int32_t cdt, void* ws, size_t ws_bytes, void* stream) {
+  const fq_status s = check_i8_shape(K, N, group);
+  if (s != FQ_OK) return s;
+  if (!valid_dtype(cdt)) return FQ_ERR_INVALID_ARG;
+  if (M < 0 || M > (1 << 20)) return FQ_ERR_SHAPE;
+  if (!codes || !zscales || !colscale) return FQ_ERR_INVALID_ARG;
+  if (M == 0) return FQ_OK;
+  if (!a_q || !a_scale || !a_rowsum || !C) return FQ_ERR_INVALID_ARG;
+  return from_cuda(run_gemm_i8(a_q, a_scale, a_rowsum, (int)M, (int)K, (int)N, group, codes, zscales, colscale, C, cdt, ws,
+                               ws_bytes, as_stream(stream)));
+}
+
 }  // extern "C"

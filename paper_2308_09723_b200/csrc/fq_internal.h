@@ -67,6 +67,16 @@ cudaError_t run_gemm_tc_grouped(int adt, int cdt, int bits, const void* A, int K
                                 const int32_t* groups, const void* const* codes, const void* const* scales,
                                 void* C, const int* experts, int nexp, cudaStream_t st);
 
+// int8-activation x int4-weight path with integer group scales (fq_i8.cu).
+cudaError_t run_quantize_intscale(int wdt, const void* W, int K, int N, int group, void* codes, void* z,
+                                  float* sigma, int32_t* status, cudaStream_t st);
+cudaError_t run_quantize_acts_i8(int adt, const void* A, int M, int K, void* Aq, float* sa, int32_t* rowsum,
+                                 int32_t* status, cudaStream_t st);
+size_t gemm_i8_workspace_bytes(int M, int K, int N);
+cudaError_t run_gemm_i8(const void* Aq, const float* sa, const int32_t* rowsum, int M, int K, int N, int group,
+                        const void* codes, const void* z, const float* sigma, void* C, int cdt, void* ws,
+                        size_t ws_bytes, cudaStream_t st);
+
 int num_sms();
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is a per-device-context setting: remember, per

@@ -78,6 +78,11 @@ def _load():
         "fq_gemm_grouped_workspace_bytes": (SZ, [I64, I32, WD]),
         "fq_gemm_grouped": (c.c_int, [P, I32, I64, c.POINTER(I64), I32, WD, c.POINTER(I32),
                                       c.POINTER(P), c.POINTER(P), P, I32, P, SZ, P]),
+        "fq_zscales_bytes": (SZ, [I64, I64, I32]),
+        "fq_quantize_intscale": (c.c_int, [P, I32, I64, I64, I32, P, P, P, P, P]),
+        "fq_quantize_acts_i8": (c.c_int, [P, I32, I64, I64, P, P, P, P, P]),
+        "fq_gemm_i8_workspace_bytes": (SZ, [I64, I64, I64]),
+        "fq_gemm_i8": (c.c_int, [P, P, P, I64, I64, I64, I32, P, P, P, P, I32, P, SZ, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -90,7 +95,8 @@ EXPORTED = ("fq_version", "fq_status_str", "fq_codes_bytes", "fq_scales_bytes", 
             "fq_adapt_group_at", "fq_adapt_flags", "fq_adapt_decide", "fq_adapt_flags_rowshard",
             "fq_adapt_flags_cross", "fq_quantize", "fq_quantize_rowshard", "fq_gemm_workspace_bytes",
             "fq_gemm", "fq_gemm_workspace_bytes_ex", "fq_gemm_ex", "fq_gemm_grouped_workspace_bytes",
-            "fq_gemm_grouped")
+            "fq_gemm_grouped", "fq_zscales_bytes", "fq_quantize_intscale", "fq_quantize_acts_i8",
+            "fq_gemm_i8_workspace_bytes", "fq_gemm_i8")
 
 
 def _ptr(t):
@@ -218,6 +224,36 @@ def fq_gemm_grouped(A, T, offsets_host, E, d, groups_host, codes_ptrs, scales_pt
                                 _ptr(C), _DT[C.dtype], _ptr(ws),
                                 0 if ws is None else ws.numel() * ws.element_size(), _stream(stream)),
            "fq_gemm_grouped")
+
+
+def fq_zscales_bytes(K: int, N: int, group: int) -> int:
+    return _lib.fq_zscales_bytes(K, N, group)
+
+
+def fq_quantize_intscale(W: torch.Tensor, group: int, codes: torch.Tensor, zscales: torch.Tensor,
+                         colscale: torch.Tensor, status: torch.Tensor | None = None, stream=None) -> None:
+    N, K = W.shape
+    _check(_lib.fq_quantize_intscale(_ptr(W), _DT[W.dtype], K, N, group, _ptr(codes), _ptr(zscales),
+                                     _ptr(colscale), _ptr(status), _stream(stream)), "fq_quantize_intscale")
+
+
+def fq_quantize_acts_i8(A: torch.Tensor, a_q: torch.Tensor, a_scale: torch.Tensor, a_rowsum: torch.Tensor,
+                        status: torch.Tensor | None = None, stream=None) -> None:
+    M, K = A.shape
+    _check(_lib.fq_quantize_acts_i8(_ptr(A), _DT[A.dtype], M, K, _ptr(a_q), _ptr(a_scale), _ptr(a_rowsum),
+                                    _ptr(status), _stream(stream)), "fq_quantize_acts_i8")
+
+
+def fq_gemm_i8_workspace_bytes(M: int, K: int, N: int) -> int:
+    return _lib.fq_gemm_i8_workspace_bytes(M, K, N)
+
+
+def fq_gemm_i8(a_q: torch.Tensor, a_scale: torch.Tensor, a_rowsum: torch.Tensor, M: int, K: int, N: int,
+               group: int, codes: torch.Tensor, zscales: torch.Tensor, colscale: torch.Tensor, C: torch.Tensor,
+               ws: torch.Tensor | None, stream=None) -> None:
+    _check(_lib.fq_gemm_i8(_ptr(a_q), _ptr(a_scale), _ptr(a_rowsum), M, K, N, group, _ptr(codes), _ptr(zscales), _ptr(colscale),
+                           _ptr(C), _DT[C.dtype], _ptr(ws), 0 if ws is None else ws.numel() * ws.element_size(),
+                           _stream(stream)), "fq_gemm_i8")
 
 
 # ------------------------------------------------------------------------------ conveniences
@@ -386,3 +422,55 @@ def gemm(A: torch.Tensor, qw: QuantizedWeight, out: torch.Tensor | None = None,
 # (M, K, N, bits, group, opts) -> workspace bytes: a pure function of its key (fq.h: routing reads
 # nothing but the arguments)
 _WS_BYTES: dict = {}
+
+
+# ------------------------------------------------------------------------------ int8-activation path
+@dataclass
+class QuantizedWeightI8:
+    """int4 codes with integer group scales (fq.h fq_quantize_intscale)."""
+    codes: torch.Tensor       # uint8 [N, K/2] canonical int4
+    zscales: torch.Tensor     # uint8 [K/group, N], values 1..16
+    colscale: torch.Tensor    # float32 [N]
+    K: int
+    N: int
+    group: int
+
+    @property
+    def nbytes(self) -> int:
+        return self.codes.numel() + self.zscales.numel() + self.colscale.numel() * 4
+
+
+def quantize_intscale(W: torch.Tensor, group: int = 128, status: torch.Tensor | None = None) -> QuantizedWeightI8:
+    assert W.is_cuda and W.dim() == 2 and W.is_contiguous()
+    N, K = W.shape
+    codes = torch.empty((N, K // 2), dtype=torch.uint8, device=W.device)
+    z = torch.empty((K // group, N), dtype=torch.uint8, device=W.device)
+    sg = torch.empty((N,), dtype=torch.float32, device=W.device)
+    fq_quantize_intscale(W, group, codes, z, sg, status)
+    return QuantizedWeightI8(codes, z, sg, K, N, group)
+
+
+def quantize_acts_i8(A: torch.Tensor, status: torch.Tensor | None = None, stream=None):
+    """Per-token int8 activations: returns (a_q int8 [M, K], a_scale float32 [M], a_rowsum int32 [M])."""
+    assert A.is_cuda and A.dim() == 2 and A.is_contiguous()
+    M, K = A.shape
+    a_q = torch.empty((M, K), dtype=torch.int8, device=A.device)
+    sa = torch.empty((M,), dtype=torch.float32, device=A.device)
+    rs = torch.empty((M,), dtype=torch.int32, device=A.device)
+    fq_quantize_acts_i8(A, a_q, sa, rs, status, stream)
+    return a_q, sa, rs
+
+
+def gemm_i8(A: torch.Tensor | None, qw: QuantizedWeightI8, out: torch.Tensor | None = None, out_dtype=None,
+            stream=None, acts=None) -> torch.Tensor:
+    """C[M, N] = s_a * sigma * (a_q . (q z)^T): quantizes A per token to int8 (unless `acts` =
+    (a_q, a_scale, a_rowsum) is given), then the tcgen05 kind::i8 GEMM."""
+    a_q, sa, rs = acts if acts is not None else quantize_acts_i8(A, stream=stream)
+    M = a_q.shape[0]
+    if out is None:
+        out = torch.empty((M, qw.N), dtype=out_dtype or (A.dtype if A is not None else torch.bfloat16),
+                          device=a_q.device)
+    nb = fq_gemm_i8_workspace_bytes(M, qw.K, qw.N)
+    ws = workspace(nb, a_q.device, stream)
+    fq_gemm_i8(a_q, sa, rs, M, qw.K, qw.N, qw.group, qw.codes, qw.zscales, qw.colscale, out, ws, stream)
+    return out

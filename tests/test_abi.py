@@ -192,3 +192,34 @@ def test_rowshard_validation(fq):
     assert L.fq_quantize_rowshard(dummy, 0, ctypes.byref(d), 4, 0, None, dummy, dummy, None, None) == fq.FQ_ERR_INVALID_ARG
     d = fq.make_wdesc(12288, 256, 4, 96 * 16, fq.FQ_BF16)  # 1536 does not nest with 12288/16 = 768?  it does
     assert L.fq_quantize_rowshard(dummy, 0, ctypes.byref(d), 3, 0, None, dummy, dummy, None, None) == fq.FQ_ERR_INVALID_ARG
+
+
+def test_i8_path_sizes_and_validation(fq):
+    """int8-activation path (NEXT-4): sizes and shape / argument validation before any launch."""
+    assert fq.fq_zscales_bytes(12288, 49152, 128) == 96 * 49152
+    assert fq.fq_zscales_bytes(12288, 49152, 48) == 0      # group % 32
+    assert fq.fq_zscales_bytes(12288, 49152, 96) == 0      # neither divides nor is a multiple of 128
+    assert fq.fq_zscales_bytes(12288, 49152, 384) == 96 * 49152 // 3
+    assert fq.fq_zscales_bytes(12300, 49152, 32) == 0      # K % 128
+    assert fq.fq_zscales_bytes(12288, 49160, 128) == 0     # N % 16
+    assert fq.fq_zscales_bytes(131072, 256, 128) == 0      # K > 65536 (int32 accumulator bound)
+    assert fq.fq_gemm_i8_workspace_bytes(0, 1024, 256) == 0
+    dummy = ctypes.c_void_p(16)
+    L = fq._lib
+    assert L.fq_gemm_i8(dummy, dummy, dummy, 4, 1024, 250, 128, dummy, dummy, dummy, dummy, fq.FQ_BF16, None, 0,
+                        None) == fq.FQ_ERR_SHAPE
+    assert L.fq_gemm_i8(dummy, dummy, dummy, 4, 1024, 256, 96, dummy, dummy, dummy, dummy, fq.FQ_BF16, None, 0,
+                        None) == fq.FQ_ERR_SHAPE
+    assert L.fq_gemm_i8(dummy, dummy, dummy, 4, 1024, 256, 128, None, dummy, dummy, dummy, fq.FQ_BF16, None, 0,
+                        None) == fq.FQ_ERR_INVALID_ARG
+    assert L.fq_gemm_i8(dummy, dummy, dummy, 4, 1024, 256, 128, dummy, dummy, dummy, dummy, 7, None, 0,
+                        None) == fq.FQ_ERR_INVALID_ARG
+    # empty batch: validated, nothing launched (A and C may be NULL)
+    assert L.fq_gemm_i8(None, None, None, 0, 1024, 256, 128, dummy, dummy, dummy, None, fq.FQ_BF16, None, 0,
+                        None) == fq.FQ_OK
+    assert L.fq_quantize_acts_i8(dummy, fq.FQ_BF16, 2, 100, dummy, dummy, dummy, None, None) == fq.FQ_ERR_SHAPE
+    assert L.fq_quantize_acts_i8(None, fq.FQ_BF16, 0, 128, None, None, None, None, None) == fq.FQ_OK
+    assert L.fq_quantize_intscale(dummy, fq.FQ_BF16, 1024, 256, 48, dummy, dummy, dummy, None,
+                                  None) == fq.FQ_ERR_SHAPE
+    assert L.fq_quantize_intscale(dummy, 9, 1024, 256, 64, dummy, dummy, dummy, None,
+                                  None) == fq.FQ_ERR_INVALID_ARG
