@@ -16,6 +16,9 @@
  *    codes  [N, K*bits/8] bytes, K contiguous per column n.
  *           int4: byte (n, k/2) = (q[n,k] & 0xF) | (q[n,k+1] & 0xF) << 4  (k even; two's complement)
  *           int8: byte (n, k)   = (uint8_t) q[n,k]
+ *           int3 / int2 (the paper's low-bit variants, reading R19): the
+ *           column's little-endian bit stream, code k in bits [b k, b k + b) (two's complement),
+ *           byte i = stream bits [8i, 8i + 8) -- int4 and int8 are its b = 4 / 8 cases
  *    scales [G, N] row-major, dtype = scale_dtype (the activation dtype, §4.1).
  *  Memory.  Every tensor argument is a caller-owned DEVICE pointer unless documented as host.
  *    The library never allocates device memory; scratch is the caller's `ws`.
@@ -46,7 +49,7 @@ typedef enum {
   FQ_OK = 0,
   FQ_ERR_INVALID_ARG = 1, /* null pointer, alpha out of range, bad dtype enum */
   FQ_ERR_SHAPE = 2,       /* K/N/M/group inconsistent or misaligned */
-  FQ_ERR_UNSUPPORTED = 3, /* bits not in {4,8}; dtype combination without a kernel */
+  FQ_ERR_UNSUPPORTED = 3, /* bits not in {2,3,4,8}; dtype / path combination without a kernel */
   FQ_ERR_WORKSPACE = 4,   /* ws too small (see fq_gemm_workspace_bytes) */
   FQ_ERR_CUDA = 5         /* a CUDA launch / runtime call failed */
 } fq_status;
@@ -57,7 +60,10 @@ typedef enum { FQ_BF16 = 0, FQ_FP16 = 1, FQ_FP32 = 2 } fq_dtype;
 typedef struct {
   int64_t K;           /* reduction dim (paper rows); K % 32 == 0 */
   int64_t N;           /* outputs (paper columns); N % 8 == 0 */
-  int32_t bits;        /* 4 or 8 ("int8 or int4 weights") */
+  int32_t bits;        /* 4 or 8 ("int8 or int4 weights"); 3 or 2 (no kernel in the
+                          paper): K % 128 == 0, fq_gemm on the decode kernel only (M <= 32
+                          for group % 128 == 0, else M <= 16; larger M and fq_gemm_grouped:
+                          FQ_ERR_UNSUPPORTED) */
   int32_t group;       /* group size along K; group % 16 == 0 and K % group == 0; group == K is
                           per-column (§3.2.1, App. B) */
   int32_t scale_dtype; /* fq_dtype of the scales: FQ_BF16 or FQ_FP16 (activation dtype) */

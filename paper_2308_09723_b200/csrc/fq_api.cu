@@ -31,8 +31,9 @@ static bool valid_half(int d) { return d == FQ_BF16 || d == FQ_FP16; }
 static fq_status check_wdesc(const fq_wdesc* d) {
   if (!d) return FQ_ERR_INVALID_ARG;
   if (d->reserved != 0 || !valid_half(d->scale_dtype)) return FQ_ERR_INVALID_ARG;
-  if (d->bits != 4 && d->bits != 8) return FQ_ERR_UNSUPPORTED;
+  if (d->bits != 2 && d->bits != 3 && d->bits != 4 && d->bits != 8) return FQ_ERR_UNSUPPORTED;
   if (d->K <= 0 || d->N <= 0 || d->K % 32 || d->N % 8) return FQ_ERR_SHAPE;
+  if (d->bits < 4 && d->K % 128) return FQ_ERR_SHAPE;  // int3 / int2 rows: whole 128-k stages
   if (d->K > (int64_t)1 << 20 || d->N > (int64_t)1 << 24) return FQ_ERR_SHAPE;
   if (d->group <= 0 || d->group % 16 || d->K % d->group) return FQ_ERR_SHAPE;
   return FQ_OK;
@@ -65,7 +66,7 @@ static fq_status from_cuda(cudaError_t e) { return e == cudaSuccess ? FQ_OK : FQ
 // 56-69 -> 47-48, OPT-30B attn-out 40-50 -> 32, OPT-175B FC2 146 -> 131 (M = 32); matrices with
 // >= 148 tiles (OPT-175B FC1, OPT-13B FFN1, OPT-30B QKV / FFN1) stay on the decode kernel.
 static bool use_tc_path(int64_t M, int bits, int group, int64_t N, const Tune& t) {
-  if (t.path == 1) return false;
+  if (t.path == 1 || bits < 4) return false;  // int3 / int2: decode kernel only (callers reject larger M)
   if (t.path == 2) return true;
   const int dmax = gemv_max_m(bits, group);
   if (M > dmax) return true;
@@ -110,7 +111,7 @@ const char* fq_status_str(fq_status s) {
 }
 
 size_t fq_codes_bytes(int64_t K, int64_t N, int32_t bits) {
-  if (K <= 0 || N <= 0 || (bits != 4 && bits != 8) || (K * bits) % 8) return 0;
+  if (K <= 0 || N <= 0 || (bits != 2 && bits != 3 && bits != 4 && bits != 8) || (K * bits) % 8) return 0;
   return (size_t)(N * (K * bits / 8));
 }
 
@@ -233,6 +234,7 @@ fq_status fq_quantize_rowshard(const void* W_shard, int32_t wdt, const fq_wdesc*
 }
 
 static size_t gemm_ws_bytes(int64_t M, const fq_wdesc* d, const Tune& t) {
+  if (d->bits < 4 && (t.path == 2 || M > gemv_max_m(d->bits, d->group))) return 0;  // unsupported
   if (use_tc_path(M, d->bits, d->group, d->N, t))
     return gemm_tc_workspace_bytes((int)M, (int)d->K, (int)d->N, d->bits, t);
   const GemvPlan p = plan_gemv((int)M, (int)d->K, (int)d->N, d->bits, d->group, num_sms(), t.splits);
@@ -261,6 +263,8 @@ fq_status fq_gemm_ex(const void* A, int32_t adt, int64_t M, const fq_wdesc* d, c
   if (!codes || !scales) return FQ_ERR_INVALID_ARG;
   if (M == 0) return FQ_OK;  // empty batch (A and C may be NULL): nothing to compute, nothing launched
   if (!A || !C) return FQ_ERR_INVALID_ARG;
+  // int3 / int2 (NEXT-3): the decode kernel only (M <= 32 on groups % 128 == 0, else 16)
+  if (d->bits < 4 && (t.path == 2 || M > gemv_max_m(d->bits, d->group))) return FQ_ERR_UNSUPPORTED;
   if (use_tc_path(M, d->bits, d->group, d->N, t))
     return from_cuda(run_gemm_tc(adt, cdt, d->bits, A, (int)M, (int)d->K, (int)d->N, codes, scales, d->group, C,
                                  ws, ws_bytes, as_stream(stream), t));
@@ -293,6 +297,7 @@ fq_status fq_gemm_grouped(const void* A, int32_t adt, int64_t T, const int64_t* 
     return FQ_ERR_INVALID_ARG;
   if (T > 0 && (!A || !C)) return FQ_ERR_INVALID_ARG;  // T == 0: A and C may be NULL
   if (!valid_half(adt) || d->scale_dtype != adt || (cdt != adt && cdt != FQ_FP32)) return FQ_ERR_UNSUPPORTED;
+  if (d->bits < 4) return FQ_ERR_UNSUPPORTED;  // int3 / int2: single GEMMs on the decode kernel only
   if (offsets_host[0] != 0 || offsets_host[E] != T || T < 0) return FQ_ERR_SHAPE;
   for (int32_t e = 0; e < E; ++e) {
     fq_wdesc de = *d;

@@ -655,6 +655,7 @@ static cudaError_t launch_tc(const tc::TcBatch<MAXP>& b, cudaStream_t st) {
 // 16-warp variants only -- see the kernel).
 template <int MAXP, int BNMAX, int BK, int HM = 1>
 static cudaError_t dispatch_tc_bn(int adt, int bits, const tc::TcBatch<MAXP>& b, cudaStream_t st, int dqg = 1) {
+  if (bits != 4 && bits != 8) return cudaErrorInvalidValue;  // int4 / int8 kernels only
   if constexpr (BK == 128 && tc::dq_warps(BNMAX) == 16) {
     if (dqg == 2 && bits == 4)
       return adt == FQ_BF16 ? launch_tc<__nv_bfloat16, 4, MAXP, BNMAX, BK, HM, 2>(b, st)

@@ -50,14 +50,18 @@ constexpr int kRowsPerCta = 32 * kConsumerWarps;      // consumer warp = 2 tiles
 constexpr int kWBoxes = (kRowsPerCta + 255) / 256;    // TMA boxes are at most 256 rows
 constexpr int kWBoxRows = kRowsPerCta / kWBoxes;
 static_assert(kWBoxRows * kWBoxes == kRowsPerCta && kWBoxRows % 8 == 0, "weight box split");
-constexpr int kWBytesPerRow = 64;     // packed bytes of one column per stage (SWIZZLE_64B rows)
+constexpr int kWBytesPerRow = 64;     // packed bytes of one column per stage, int4 / int8 (SWIZZLE_64B rows)
+// int3 / int2: 128 k per stage as 48- / 32-byte rows of the canonical bit stream
+// (unswizzled: the consumers' 12- / 8-byte reads of 8 rows x 4 threads hit distinct banks)
+__host__ __device__ constexpr int wb_row(int bits) { return bits >= 4 ? kWBytesPerRow : 16 * bits; }
+template <int BITS> constexpr int stage_w() { return kRowsPerCta * wb_row(BITS); }
 constexpr int kStageW = kRowsPerCta * kWBytesPerRow;
 constexpr int kMaxDecStages = 6;
 
 template <int BITS>
 struct DecGeom {
-  static constexpr int KS = kWBytesPerRow * 8 / BITS;  // K per stage: 256 (int4) / 128 (int8)
-  static constexpr int SEG = BITS == 4 ? 32 : 16;      // K per thread per column per chunk
+  static constexpr int KS = wb_row(BITS) * 8 / BITS;  // K per stage: 128 (int2/3/4) / 64 (int8)
+  static constexpr int SEG = BITS <= 4 ? 32 : 16;      // K per thread per column per chunk
   static constexpr int KCH = 4 * SEG;                  // K per chunk (one quad): 128 / 64
   static constexpr int CHUNKS = KS / KCH;              // 2
   static constexpr int PIECES = SEG / 8;               // 16-byte activation pieces per thread/chunk
@@ -69,7 +73,7 @@ struct DecGeom {
 template <int BITS, int MT, int SACC>
 struct DecStage {
   using G = DecGeom<BITS>;
-  static constexpr int ACT_OFS = kStageW;
+  static constexpr int ACT_OFS = stage_w<BITS>();
   static constexpr int ACT_BYTES = MT * 8 * G::ROWB;
   static constexpr int SC_OFS = ACT_OFS + ACT_BYTES;  // TMA destinations: 128-byte aligned
   static constexpr int SC_BYTES = kRowsPerCta * 2 * (SACC ? SACC : 8);  // scale rows per stage (<= 8)
@@ -271,6 +275,47 @@ __device__ __forceinline__ int swz64(int c, int R) { return c ^ ((R >> 1) & 3); 
 // DBG (diagnostics build -DFQ_DIAG only, selected by FQ_DEC_DEBUG for bf16/int4/M<=8; 4 = skeleton
 // streaming codes only): 1 = no MMA (fake FADD accumulate), 2 = no dequant (raw code words as MMA
 // operands), 3 = consumers skip all compute.  The product build instantiates DBG = 0 only.
+// int3 / int2: the 32 codes k = 32t .. 32t+31 of a thread, read from the canonical
+// little-endian bit stream (12 / 8 bytes) and re-laid as four int4 words (code k + i at nibble i,
+// sign-extended to 4 bits), so everything downstream is the int4 path.  Spreading the 3-bit fields of
+// a 24-bit run x into nibbles takes three shift-and-select steps (12 / 6 / 3 bits apart); the
+// garbage each step drags along lands in bit 3 of the nibbles, which the sign extension overwrites.
+template <int BITS>
+__device__ __forceinline__ uint4 lowbit_words(uint32_t addr) {
+  uint32_t x[4];
+  if (BITS == 3) {
+    const uint32_t w0 = lds32(addr), w1 = lds32(addr + 4), w2 = lds32(addr + 8);
+    x[0] = w0;
+    x[1] = __funnelshift_r(w0, w1, 24);
+    x[2] = __funnelshift_r(w1, w2, 16);
+    x[3] = w2 >> 8;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint32_t y = x[j];
+      y = lop3_sel(y, y << 4, 0x0000FFFFu);   // fields 0-3 at bits 0-11, fields 4-7 at 16-27
+      y = lop3_sel(y, y << 2, 0x00FF00FFu);   // per half: fields (0,1) at 0-5, (2,3) at 8-13
+      y = lop3_sel(y, y << 1, 0x0F0F0F0Fu);   // per byte: even field at 0-2, odd at 4-6
+      x[j] = lop3_sel(y, y << 1, 0x77777777u);  // bit 3 of every nibble = bit 2 (sign extension)
+    }
+  } else {
+    const uint2 w = lds64(addr);
+    x[0] = w.x;
+    x[1] = w.x >> 16;
+    x[2] = w.y;
+    x[3] = w.y >> 16;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint32_t y = x[j];
+      y = lop3_sel(y, y << 8, 0x0000FFFFu);   // fields 0-3 at bits 0-7, fields 4-7 at 16-23
+      y = lop3_sel(y, y << 4, 0x00FF00FFu);   // per half: fields (0,1) at 0-3, (2,3) at 8-11
+      y = lop3_sel(y, y << 2, 0x0F0F0F0Fu);   // per byte: even field at 0-1, odd at 4-5
+      y = lop3_sel(y, y << 1, 0x33333333u);   // bit 2 = bit 1
+      x[j] = lop3_sel(y, y << 1, 0x77777777u);  // bit 3 = bit 2 (= bit 1)
+    }
+  }
+  return make_uint4(x[0], x[1], x[2], x[3]);
+}
+
 template <typename T, int BITS, int MT, int SACC, int DBG, int MAXP>
 // Register caps (two CTAs per SM fit up to 112 / 96 registers at 288 / 320 threads), set without
 // ptxas's launch_bounds heuristic.
@@ -283,7 +328,7 @@ template <typename T, int BITS, int MT, int SACC, int DBG, int MAXP>
 #ifndef FQ_DEC_NIB4_MAXREG
 #define FQ_DEC_NIB4_MAXREG 112  // four 8-token MMA tiles (17 <= M <= 32); 2 CTAs x 288 threads fit 113
 #endif
-__global__ void __maxnreg__((FQ_NIB && BITS == 4 && SACC)
+__global__ void __maxnreg__((FQ_NIB && BITS <= 4 && SACC)
                                ? (MT == 4 ? FQ_DEC_NIB4_MAXREG : MT == 2 ? FQ_DEC_NIB2_MAXREG : FQ_DEC_NIB_MAXREG)
                                : 96)
 decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
@@ -298,7 +343,7 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
   constexpr int RAW_BYTES = SG::ACT_BYTES;
   // Nibble path: activations were pre-converted by prep_acts_kernel (fp16, fragment order) and
   // arrive by TMA with their per-chunk {correction, 2^-e}; there is no stager warp.
-  constexpr bool NIB = FQ_NIB && BITS == 4 && SACC;
+  constexpr bool NIB = FQ_NIB && BITS <= 4 && SACC;
   // GS = 2 (int4, group 64, nibble path): each thread's four 8-code words come from the four 32-k
   // blocks of the stage (4 x LDS.32 instead of one LDS.128), so the MMAs of words 0-1 and 2-3 cover
   // the two 64-k groups separately; two exact partials per stage, folded with their own scales.
@@ -359,14 +404,14 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
         const int k0 = kbeg + i * KS;
         const int scb = SACC ? SACC * kRowsPerCta * 2 : p.sc_rows * kRowsPerCta * 2;
         if (DBG == 4) {  // diagnostics: codes only
-          mbar_arrive_expect_tx(&full_bar[s], kStageW);
+          mbar_arrive_expect_tx(&full_bar[s], stage_w<BITS>());
           tma_load_2d(st, &p.w, &full_bar[s], k0 * BITS / 8, n0, polw);
           return;
         }
-        mbar_arrive_expect_tx(&full_bar[s], kStageW + scb + (NIB ? RAW_BYTES + MT * 8 * 16 : 0));
+        mbar_arrive_expect_tx(&full_bar[s], stage_w<BITS>() + scb + (NIB ? RAW_BYTES + MT * 8 * 16 : 0));
 #pragma unroll
         for (int bx2 = 0; bx2 < kWBoxes; ++bx2)
-          tma_load_2d(st + bx2 * kWBoxRows * kWBytesPerRow, &p.w, &full_bar[s], k0 * BITS / 8,
+          tma_load_2d(st + bx2 * kWBoxRows * wb_row(BITS), &p.w, &full_bar[s], k0 * BITS / 8,
                       n0 + bx2 * kWBoxRows, polw);
         if (SACC) {
 #pragma unroll
@@ -462,7 +507,7 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
             for (int o = PPC / 2; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
             if ((lane % PPC) == 0) reinterpret_cast<float*>(st + SUM_OFS)[tl] = sum;
           }
-          if (BITS == 4) {
+          if (BITS <= 4) {
             v = make_uint4(prmt(v.x, v.z, 0x5410u), prmt(v.x, v.z, 0x7632u), prmt(v.y, v.w, 0x5410u),
                            prmt(v.y, v.w, 0x7632u));
           }
@@ -488,8 +533,13 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
     Rh[rt] = Rg[rt] + 8;
     ng[rt] = min(n0 + Rg[rt], N - 1);
     nh[rt] = min(n0 + Rh[rt], N - 1);
-    wofs_g[rt] = Rg[rt] * kWBytesPerRow + (swz64(t, Rg[rt]) << 4);
-    wofs_h[rt] = Rh[rt] * kWBytesPerRow + (swz64(t, Rh[rt]) << 4);
+    if (BITS < 4) {  // bytes [t * wb/4, +wb/4) of the unswizzled bit-stream row = k 32t .. 32t+31
+      wofs_g[rt] = Rg[rt] * wb_row(BITS) + t * (wb_row(BITS) / 4);
+      wofs_h[rt] = Rh[rt] * wb_row(BITS) + t * (wb_row(BITS) / 4);
+    } else {
+      wofs_g[rt] = Rg[rt] * kWBytesPerRow + (swz64(t, Rg[rt]) << 4);
+      wofs_h[rt] = Rh[rt] * kWBytesPerRow + (swz64(t, Rh[rt]) << 4);
+    }
   }
   uint32_t aofs[MT][PIECES];
 #pragma unroll
@@ -553,7 +603,10 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
     }
 #pragma unroll
     for (int rt = 0; rt < 2; ++rt) {
-      if (GS == 1) {
+      if (BITS < 4) {
+        o.wgv[rt] = lowbit_words<BITS>(wst + wofs_g[rt]);
+        o.whv[rt] = lowbit_words<BITS>(wst + wofs_h[rt]);
+      } else if (GS == 1) {
         o.wgv[rt] = lds128(wst + wofs_g[rt]);
         o.whv[rt] = lds128(wst + wofs_h[rt]);
       } else {  // word w = 8 codes at k = 32 w + 8 t: cell w (swizzled), word t of the cell
@@ -616,7 +669,7 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
           }
         }
         float(*dst)[4] = SACC ? part[(w * GS) >> 2] : acc[rt];
-        if (BITS == 4) {
+        if (BITS <= 4) {
           uint32_t qg[4], qh[4];
           if (DBG == 2) {
 #pragma unroll
@@ -870,7 +923,7 @@ static bool gs_of(int bits, int group, int K) {
   return FQ_NIB && bits == 4 && group == 64 && K % 128 == 0;
 }
 static bool nib_of(int bits, int group, int K = -1) {
-  return FQ_NIB && bits == 4 && (group % 128 == 0 || (K >= 0 && gs_of(bits, group, K)));
+  return FQ_NIB && bits <= 4 && (group % 128 == 0 || (K >= 0 && gs_of(bits, group, K)));
 }
 
 int gemv_max_m(int bits, int group) { return nib_of(bits, group) ? 32 : 16; }
@@ -878,7 +931,7 @@ int gemv_max_m(int bits, int group) { return nib_of(bits, group) ? 32 : 16; }
 GemvPlan plan_gemv(int M, int K, int N, int bits, int group, int nsm, int splits_override) {
   (void)group;
   GemvPlan p{};
-  p.kchunk = bits == 4 ? 256 : 128;  // split-K granularity (two kernel stages; one stage measured slower on small matrices)
+  p.kchunk = bits <= 4 ? 256 : 128;  // split-K granularity (two kernel stages; one stage measured slower on small matrices)
   // 8-token MMA tiles per token tile: 1 (M <= 8), 2 (<= 16), 4 (int4 nibble path, > 16 tokens:
   // every weight is streamed once per 32 tokens)
   p.mt = M <= 8 ? 1 : (M <= 16 || !nib_of(bits, group)) ? 2 : 4;  // MT = 4: group % 128 nibble path only
@@ -925,7 +978,7 @@ size_t gemv_workspace_bytes(const GemvPlan& p, int M, int K, int N, int bits, in
   return b;
 }
 size_t gemv_grouped_workspace_bytes(int64_t T, int K, int bits) {
-  return kCounterBytes + (bits == 4 ? prep_bytes((int)T, K) : 0);
+  return kCounterBytes + (bits <= 4 ? prep_bytes((int)T, K) : 0);
 }
 template <int MODE>
 static cudaError_t launch_prep_g(int adt, const void* A, int ntok, int K, void* Ap, void* Sp, cudaStream_t st) {
@@ -949,7 +1002,7 @@ static cudaError_t launch_dec(const DecBatch<MAXP>& b, int ctas, cudaStream_t st
   constexpr int smem = DecStage<BITS, MT, SACC>::SMEM;
   cudaError_t e = ensure_smem_attr<decode_kernel<T, BITS, MT, SACC, DBG, MAXP>>(smem);
   if (e != cudaSuccess) return e;
-  return launch_pdl(decode_kernel<T, BITS, MT, SACC, DBG, MAXP>, ctas, dec_threads<FQ_NIB && BITS == 4 && SACC>(),
+  return launch_pdl(decode_kernel<T, BITS, MT, SACC, DBG, MAXP>, ctas, dec_threads<FQ_NIB && BITS <= 4 && SACC>(),
                     smem, st, b);
 }
 
@@ -976,6 +1029,10 @@ static cudaError_t dispatch_dec(int adt, int bits, int mt, int sacc, int dbg, co
     FQ_DEC_CASE(__nv_bfloat16, 4, 1, 2) FQ_DEC_CASE(__nv_bfloat16, 4, 2, 2)
     FQ_DEC_CASE(__nv_bfloat16, 8, 1, 1) FQ_DEC_CASE(__nv_bfloat16, 8, 1, 0)
     FQ_DEC_CASE(__nv_bfloat16, 8, 2, 1) FQ_DEC_CASE(__nv_bfloat16, 8, 2, 0)
+    FQ_DEC_CASE(__nv_bfloat16, 3, 1, 1) FQ_DEC_CASE(__nv_bfloat16, 3, 1, 0)
+    FQ_DEC_CASE(__nv_bfloat16, 3, 2, 1) FQ_DEC_CASE(__nv_bfloat16, 3, 2, 0) FQ_DEC_CASE(__nv_bfloat16, 3, 4, 1)
+    FQ_DEC_CASE(__nv_bfloat16, 2, 1, 1) FQ_DEC_CASE(__nv_bfloat16, 2, 1, 0)
+    FQ_DEC_CASE(__nv_bfloat16, 2, 2, 1) FQ_DEC_CASE(__nv_bfloat16, 2, 2, 0) FQ_DEC_CASE(__nv_bfloat16, 2, 4, 1)
   } else {
     FQ_DEC_CASE(__half, 4, 1, 1) FQ_DEC_CASE(__half, 4, 1, 0)
     FQ_DEC_CASE(__half, 4, 2, 1) FQ_DEC_CASE(__half, 4, 2, 0)
@@ -983,6 +1040,10 @@ static cudaError_t dispatch_dec(int adt, int bits, int mt, int sacc, int dbg, co
     FQ_DEC_CASE(__half, 4, 1, 2) FQ_DEC_CASE(__half, 4, 2, 2)
     FQ_DEC_CASE(__half, 8, 1, 1) FQ_DEC_CASE(__half, 8, 1, 0)
     FQ_DEC_CASE(__half, 8, 2, 1) FQ_DEC_CASE(__half, 8, 2, 0)
+    FQ_DEC_CASE(__half, 3, 1, 1) FQ_DEC_CASE(__half, 3, 1, 0)
+    FQ_DEC_CASE(__half, 3, 2, 1) FQ_DEC_CASE(__half, 3, 2, 0) FQ_DEC_CASE(__half, 3, 4, 1)
+    FQ_DEC_CASE(__half, 2, 1, 1) FQ_DEC_CASE(__half, 2, 1, 0)
+    FQ_DEC_CASE(__half, 2, 2, 1) FQ_DEC_CASE(__half, 2, 2, 0) FQ_DEC_CASE(__half, 2, 4, 1)
   }
 #undef FQ_DEC_CASE
   return cudaErrorInvalidValue;
@@ -996,9 +1057,10 @@ static bool make_dec_prob(DecProb& d, const GemvPlan& pl, int bits, int cdt, con
                           int N, const void* codes, const void* scales, int group, void* C, void* ws,
                           const void* Sp = nullptr, int ntok_all = 0, int tok_base = 0, bool gs = false) {
   const uint64_t row_bytes = (uint64_t)K * bits / 8;
-  if (!make_tmap_2d(&d.w, codes, 1, row_bytes, (uint64_t)N, row_bytes, kWBytesPerRow, kWBoxRows, 64))
+  if (!make_tmap_2d(&d.w, codes, 1, row_bytes, (uint64_t)N, row_bytes, wb_row(bits), kWBoxRows,
+                    bits >= 4 ? 64 : 0))
     return false;
-  const int ks = kWBytesPerRow * 8 / bits;  // K per stage
+  const int ks = wb_row(bits) * 8 / bits;  // K per stage
   if (!make_tmap_2d(&d.a, A, 2, (uint64_t)K, (uint64_t)M, (uint64_t)K * 2, ks, pl.mt * 8, 0)) return false;
   d.tok_base = tok_base;
   if (Sp && !make_tmap_2d(&d.sm, reinterpret_cast<const char*>(Sp) + (size_t)tok_base * 16, 4, (uint64_t)M * 4,
@@ -1026,7 +1088,7 @@ static bool make_dec_prob(DecProb& d, const GemvPlan& pl, int bits, int cdt, con
 
 // scale path: 1 = one scale group per stage, 2 = two 64-k groups (group split), 0 = per element
 static int sacc_of(int bits, int group, int K = -1) {
-  if (group % (bits == 4 ? 128 : 64) == 0) return 1;
+  if (group % (bits <= 4 ? 128 : 64) == 0) return 1;
   return (K >= 0 && gs_of(bits, group, K)) ? 2 : 0;
 }
 

@@ -216,8 +216,16 @@ __global__ void __launch_bounds__(1024) quantize_acts_i8_kernel(const T* __restr
 constexpr int BM = 128;     // weight rows per tile (UMMA M, TMEM lanes)
 constexpr int BK = 128;     // k per stage: one 128-byte SW128 activation row, 64-byte code rows
 constexpr int ZROWS = 4;    // z rows staged per K block (groups of >= 32 k)
-constexpr int kDqWarps = 8; // two per TMEM lane quarter, 64 k each
-constexpr int kThreads = 32 * (3 + kDqWarps);  // codes TMA, MMA, 8 dequant, activation TMA
+constexpr int kGroupWarps = 8;  // dequant warps per group: two per TMEM lane quarter, 64 k each
+// DG dequant groups take alternate K blocks (one group's barrier waits and tcgen05.st round trip
+// overlap the other's loads and unpacking).  Threads: codes TMA, MMA, 8 DG dequant, activation TMA.
+__host__ __device__ constexpr int i8_threads(int dg) { return 32 * (3 + kGroupWarps * dg); }
+#ifndef FQ_I8_DG_SMALL
+#define FQ_I8_DG_SMALL 2  // token tiles <= 32
+#endif
+#ifndef FQ_I8_DG_LARGE
+#define FQ_I8_DG_LARGE 2  // measured (profiles/r02/i8_dequant_groups.txt): M = 64 -10%, M = 2048 -9%
+#endif
 constexpr int kSmemMax = 227 * 1024 - 2048;
 
 // Two rings per CTA:
@@ -300,8 +308,10 @@ __device__ __forceinline__ void i4z_bytes(uint32_t w, uint32_t z, uint32_t cz, u
   o1 = lop3_and_xor(w >> 4, 0x0F0F0F0Fu, 0x08080808u) * z + cz;  // k+1, k+3, k+5, k+7
 }
 
-template <int BNMAX>
-__global__ void __launch_bounds__(kThreads, 1) gemm_i8_kernel(const __grid_constant__ I8Prob p) {
+template <int BNMAX, int DG>
+__global__ void __launch_bounds__(i8_threads(DG), 1) gemm_i8_kernel(const __grid_constant__ I8Prob p) {
+  constexpr int kDqWarps = kGroupWarps * DG;
+  constexpr int kThreads = i8_threads(DG);
   using Gm = Geo<BNMAX>;
   constexpr int CS = Gm::CS, AS = Gm::AS;
   constexpr int kACol = BNMAX;  // A slot a at TMEM columns BNMAX + 32 a
@@ -318,11 +328,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_i8_kernel(const __grid_const
   if (threadIdx.x == 0) {
     for (int c = 0; c < CS; ++c) {
       mbar_init(&cfull[c], 1);
-      mbar_init(&cempty[c], kDqWarps);
+      mbar_init(&cempty[c], kGroupWarps);
     }
     for (int a = 0; a < AS; ++a) {
       mbar_init(&actfull[a], 1);
-      mbar_init(&slotfull[a], kDqWarps);
+      mbar_init(&slotfull[a], kGroupWarps);
       mbar_init(&aempty[a], 1);
     }
     mbar_init(&acc_full, 1);
@@ -420,12 +430,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_i8_kernel(const __grid_const
     // ------------------------------------------------------------------ dequant + epilogue
     const int dq = warp - 2;
     const int quarter = warp & 3;          // TMEM lane quarter this warp may access
-    const int kp = dq >> 2;                // which 64 k of a K block this warp dequantizes
+    const int kp = (dq >> 2) & 1;          // which 64 k of a K block this warp dequantizes
+    const int grp = dq >> 3;               // dequant group: K blocks with blk % DG == grp
     const int row = quarter * 32 + lane;   // weight row within the tile == TMEM lane
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const uint32_t sb = smem_u32(sbase);
-    int c = 0, a = 0;
-    uint32_t cph = 0, aph = 0, acc_ph = 0;
+    uint32_t acc_ph = 0;
+    int blk = 0;  // K blocks of this CTA so far (ring position of both rings)
     // groups divide the 128-k block (32 / 64) or are whole blocks (g % 128 == 0): the staged z row of
     // each of this thread's two 32-k chunks is fixed (host-validated)
     const int jr0 = p.group >= BK ? 0 : (kp * 64) / p.group;
@@ -438,8 +449,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_i8_kernel(const __grid_const
     for (int item = blockIdx.x; item < ntiles; item += gridDim.x) {
       int mt, nt, tt, ks, kb0, kb1;
       item_coords(item, mt, nt, tt, ks, kb0, kb1);
-      int prev = -1;  // A slot written but not yet published (its tcgen05.st in flight)
-      for (int kb = kb0; kb < kb1; ++kb) {
+      int prev = -1;  // (DG == 1) A slot written but not yet published (its tcgen05.st in flight)
+      for (int kb = kb0; kb < kb1; ++kb, ++blk) {
+        if (DG > 1 && (blk % DG) != grp) continue;
+        const int c = blk % CS, a = blk % AS;
+        const uint32_t cph = (blk / CS) & 1, aph = (blk / AS) & 1;
         mbar_wait(&cfull[c], cph);
         const uint32_t so = c * Gm::CODE_STAGE;
         const uint4 w0 = lds128(codes_row + so + c0ofs);
@@ -447,7 +461,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_i8_kernel(const __grid_const
         const uint32_t z0 = lds_u8(sb + so + z0ofs), z1 = lds_u8(sb + so + z1ofs);
         __syncwarp();
         if (lane == 0) mbar_arrive(&cempty[c]);  // codes in registers: the stage goes back to the TMA
-        if (++c == CS) { c = 0; cph ^= 1; }
         uint32_t out[16];
         const uint32_t cz0 = 0x80808080u - z0 * 0x08080808u, cz1 = 0x80808080u - z1 * 0x08080808u;
         i4z_bytes(w0.x, z0, cz0, out[0], out[1]);
@@ -458,9 +471,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_i8_kernel(const __grid_const
         i4z_bytes(w1.y, z1, cz1, out[10], out[11]);
         i4z_bytes(w1.z, z1, cz1, out[12], out[13]);
         i4z_bytes(w1.w, z1, cz1, out[14], out[15]);
-        // publish the previous A slot (its tcgen05.st had this block's loads and unpacking to
-        // complete), then wait until the MMAs that last read this block's slot are done
-        if (prev >= 0) {
+        // DG == 1: publish the previous A slot (its tcgen05.st had this block's loads and unpacking
+        // to complete); then wait until the MMAs that last read this block's slot are done
+        if (DG == 1 && prev >= 0) {
           tmem_wait_st();
           fence_before();
           __syncwarp();
@@ -473,31 +486,39 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_i8_kernel(const __grid_const
         } else {
           tmem_st16(tcol + a * (BK / 4), out);
         }
-        prev = a;
-        if (++a == AS) { a = 0; aph ^= 1; }
+        if (DG == 1) {
+          prev = a;
+        } else {  // the other group covers this group's tcgen05.st round trip
+          tmem_wait_st();
+          fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&slotfull[a]);
+        }
       }
-      if (prev >= 0) {
+      if (DG == 1 && prev >= 0) {
         tmem_wait_st();
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&slotfull[prev]);
       }
-      // ---- epilogue: accumulator row `row` (weight n), tokens [kp * BNMAX/2, ...)
+      // ---- epilogue: accumulator row `row` (weight n), tokens [part * TPP, +TPP), part = dq / 4
       mbar_wait(&acc_full, acc_ph);
       acc_ph ^= 1;
       fence_after();
-      constexpr int TPP = BNMAX / 2;
+      constexpr int TPP = BNMAX / (2 * DG);
+      constexpr int CH = TPP < 16 ? TPP : 16;  // accumulator columns per tcgen05.ld
+      const int part_i = dq >> 2;
       const int n = nt * BM + row;
       int32_t* part = p.splits > 1 ? p.ws + (size_t)(tt * p.splits + ks) * p.bn * BM : nullptr;
       const float sg = n < p.N ? __ldg(p.sigma + n) : 0.f;
 #pragma unroll 1
-      for (int c0 = 0; c0 < TPP && kp * TPP + c0 < p.bn; c0 += 16) {
-        uint32_t v[16];
-        tmem_ld16(tmem + lane_base + kp * TPP + c0, v);
+      for (int c0 = 0; c0 < TPP && part_i * TPP + c0 < p.bn; c0 += CH) {
+        uint32_t v[CH];
+        tmem_ldn<CH>(tmem + lane_base + part_i * TPP + c0, v);
         tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int tl = kp * TPP + c0 + i;  // token within the tile
+        for (int i = 0; i < CH; ++i) {
+          const int tl = part_i * TPP + c0 + i;  // token within the tile
           if (tl >= p.bn) continue;
           if (part) {
             __stcg(part + tl * BM + row, (int32_t)v[i]);
@@ -638,13 +659,14 @@ size_t gemm_i8_workspace_bytes(int M, int K, int N) {
   return kI8CounterBytes + tiles * s * bn * i8::BM * sizeof(int32_t);
 }
 
-template <int BNMAX>
+template <int BNMAX, int DG>
 static cudaError_t launch_i8(const i8::I8Prob& p, cudaStream_t st) {
   using Gm = i8::Geo<BNMAX>;
-  cudaError_t e = ensure_smem_attr<i8::gemm_i8_kernel<BNMAX>>(Gm::SMEM);
+  cudaError_t e = ensure_smem_attr<i8::gemm_i8_kernel<BNMAX, DG>>(Gm::SMEM);
   if (e != cudaSuccess) return e;
   const int items = p.m_tiles * p.n_tiles * p.splits;
-  return launch_pdl(i8::gemm_i8_kernel<BNMAX>, std::min(items, num_sms()), i8::kThreads, Gm::SMEM, st, p);
+  return launch_pdl(i8::gemm_i8_kernel<BNMAX, DG>, std::min(items, num_sms()), i8::i8_threads(DG), Gm::SMEM, st,
+                    p);
 }
 
 cudaError_t run_gemm_i8(const void* Aq, const float* sa, const int32_t* rowsum, int M, int K, int N, int group,
@@ -677,9 +699,9 @@ cudaError_t run_gemm_i8(const void* Aq, const float* sa, const int32_t* rowsum, 
     p.ws = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(ws) + kI8CounterBytes);
   }
   switch (i8_bnmax(p.bn)) {
-    case 32: return launch_i8<32>(p, st);
-    case 128: return launch_i8<128>(p, st);
-    default: return launch_i8<256>(p, st);
+    case 32: return launch_i8<32, FQ_I8_DG_SMALL>(p, st);
+    case 128: return launch_i8<128, FQ_I8_DG_LARGE>(p, st);
+    default: return launch_i8<256, FQ_I8_DG_LARGE>(p, st);
   }
 }
 

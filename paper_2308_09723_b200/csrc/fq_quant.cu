@@ -106,6 +106,24 @@ constexpr int kQThreads = 256;
 constexpr int kQCpt = 8;      // chunks per thread cached in registers by the quantizer
 constexpr int kQSlice = 12288;  // target K-slice per CTA (192 threads at kQCpt = 8)
 
+// int3 / int2 (reading R19): the 8 codes of chunk c (offset-binary u = q + 2^(b-1))
+// as b-bit two's-complement fields of the column's little-endian bit stream, 3 / 2 bytes per chunk.
+template <int BITS>
+__device__ __forceinline__ void store_lowbit(uint8_t* codes, int n, int K, int chunk, const uint32_t (&u)[8]) {
+  uint32_t w = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) w |= ((u[i] ^ (1u << (BITS - 1))) & ((1u << BITS) - 1)) << (BITS * i);
+  uint8_t* col = codes + (size_t)n * (K / 8 * BITS);
+  if (BITS == 2) {
+    reinterpret_cast<uint16_t*>(col)[chunk] = (uint16_t)w;
+  } else {
+    uint8_t* b = col + (size_t)chunk * 3;
+    b[0] = (uint8_t)w;
+    b[1] = (uint8_t)(w >> 8);
+    b[2] = (uint8_t)(w >> 16);
+  }
+}
+
 template <typename TIn, typename TS, int BITS, int CPT = kQCpt>
 __global__ void __launch_bounds__(sizeof(TIn) == 4 ? 512 : 1024) quantize_kernel(const TIn* __restrict__ W, int K,
                                                              int KS, int N, int group,
@@ -234,7 +252,12 @@ __global__ void __launch_bounds__(sizeof(TIn) == 4 ? 512 : 1024) quantize_kernel
         tb[i] = min(__float_as_int(t), kBase + (1 << BITS) - 1);
       }
       // pack the raw bit patterns: every field carries kBase, whose packed sum is one constant
-      if (BITS == 4) {
+      if (BITS < 4) {
+        uint32_t u[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) u[i] = (uint32_t)(tb[i] - kBase);
+        store_lowbit<BITS>(codes, n, K, sl * nchunk + c, u);
+      } else if (BITS == 4) {
         uint32_t w = (uint32_t)tb[7];
 #pragma unroll
         for (int i = 6; i >= 0; --i) w = w * 16u + (uint32_t)tb[i];
@@ -260,7 +283,9 @@ __global__ void __launch_bounds__(sizeof(TIn) == 4 ? 512 : 1024) quantize_kernel
         m = fminf(m, neg ? (float)-lo : (float)hi);
         u[i] = (uint32_t)(int)((neg ? -m : m) + (float)-lo);
       }
-      if (BITS == 4) {
+      if (BITS < 4) {
+        store_lowbit<BITS>(codes, n, K, sl * nchunk + c, u);
+      } else if (BITS == 4) {
         uint32_t w = u[7];
 #pragma unroll
         for (int i = 6; i >= 0; --i) w = w * 16u + u[i];
@@ -385,8 +410,12 @@ static cudaError_t launch_quant(const void* W, int K, int N, int group, void* co
 template <typename TIn, typename TS>
 static cudaError_t launch_quant_b(int bits, const void* W, int K, int N, int group, void* codes,
                                   void* scales, int32_t* status, cudaStream_t st, AmaxTab at) {
-  return bits == 4 ? launch_quant<TIn, TS, 4>(W, K, N, group, codes, scales, status, st, at)
-                   : launch_quant<TIn, TS, 8>(W, K, N, group, codes, scales, status, st, at);
+  switch (bits) {
+    case 2: return launch_quant<TIn, TS, 2>(W, K, N, group, codes, scales, status, st, at);
+    case 3: return launch_quant<TIn, TS, 3>(W, K, N, group, codes, scales, status, st, at);
+    case 4: return launch_quant<TIn, TS, 4>(W, K, N, group, codes, scales, status, st, at);
+    default: return launch_quant<TIn, TS, 8>(W, K, N, group, codes, scales, status, st, at);
+  }
 }
 
 template <typename TIn>

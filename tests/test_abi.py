@@ -33,7 +33,9 @@ def test_library_exports_every_declared_symbol(fq):
 def test_sizes_and_ladder(fq):
     assert fq.fq_codes_bytes(12288, 49152, 4) == 12288 * 49152 // 2
     assert fq.fq_codes_bytes(12288, 49152, 8) == 12288 * 49152
-    assert fq.fq_codes_bytes(12288, 49152, 3) == 0
+    assert fq.fq_codes_bytes(12288, 49152, 3) == 12288 * 49152 * 3 // 8   # int3 bit stream (R19)
+    assert fq.fq_codes_bytes(12288, 49152, 2) == 12288 * 49152 // 4
+    assert fq.fq_codes_bytes(12288, 49152, 5) == 0
     assert fq.fq_scales_bytes(12288, 49152, 128, fq.FQ_BF16) == 96 * 49152 * 2
     assert fq.fq_scales_bytes(12288, 49152, 100, fq.FQ_BF16) == 0
     from oracle import fq_oracle as O
@@ -55,11 +57,22 @@ def test_decide_matches_oracle_decide(fq):
 
 def test_validation_is_synchronous_and_launch_free(fq):
     """Invalid descriptors are rejected before any device work (pointers are dummies)."""
-    d = fq.make_wdesc(256, 256, 3, 64, fq.FQ_BF16)
     dummy = ctypes.c_void_p(16)
-    st = fq._lib.fq_gemm(dummy, fq.FQ_BF16, 1, ctypes.byref(d), dummy, dummy, dummy, fq.FQ_BF16,
-                         None, 0, None)
-    assert st == fq.FQ_ERR_UNSUPPORTED
+    for bits in (5, 6, 7, 1):  # no kernel
+        d = fq.make_wdesc(256, 256, bits, 64, fq.FQ_BF16)
+        st = fq._lib.fq_gemm(dummy, fq.FQ_BF16, 1, ctypes.byref(d), dummy, dummy, dummy, fq.FQ_BF16,
+                             None, 0, None)
+        assert st == fq.FQ_ERR_UNSUPPORTED
+    # int3 / int2: decode kernel only -- K % 128, and M beyond the decode kernel is refused
+    d3 = fq.make_wdesc(192, 256, 3, 64, fq.FQ_BF16)
+    assert fq._lib.fq_quantize(dummy, 0, ctypes.byref(d3), dummy, dummy, None, None) == fq.FQ_ERR_SHAPE
+    d3 = fq.make_wdesc(256, 256, 3, 64, fq.FQ_BF16)
+    assert fq._lib.fq_gemm(dummy, 0, 17, ctypes.byref(d3), dummy, dummy, dummy, 0, None, 0,
+                           None) == fq.FQ_ERR_UNSUPPORTED  # per-element-scale path: M <= 16
+    d2 = fq.make_wdesc(256, 256, 2, 128, fq.FQ_BF16)
+    assert fq._lib.fq_gemm(dummy, 0, 33, ctypes.byref(d2), dummy, dummy, dummy, 0, None, 0,
+                           None) == fq.FQ_ERR_UNSUPPORTED  # nibble path: M <= 32
+    assert fq.fq_gemm_workspace_bytes(64, d2) == 0
     for bad in (fq.make_wdesc(250, 256, 4, 64, 0), fq.make_wdesc(256, 252, 4, 64, 0),
                 fq.make_wdesc(256, 256, 4, 48, 0), fq.make_wdesc(256, 256, 4, 24, 0)):
         assert fq._lib.fq_quantize(dummy, 0, ctypes.byref(bad), dummy, dummy, None, None) == fq.FQ_ERR_SHAPE
