@@ -191,6 +191,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-tp-layer", action="store_true")
+    ap.add_argument("--xr-layer", action="store_true",
+                    help="N>1: also time the TP layer with the fused GEMM + one-shot all-reduce (NEXT-1)")
     # SURVEY §5 knobs: headline GEMM precision / group; adaptive parameters of the MoE extras
     ap.add_argument("--bits", type=int, default=4, choices=[4, 8])
     ap.add_argument("--group", type=int, default=128)
@@ -469,6 +471,13 @@ def measure_tp_layer(fq, dev, world, rank, args, n_layers=4, Ms=(1, 16, 2048), r
             del Ws
             full_bytes += eff_bytes(k, n, 4, 128) if li == 0 else 0
         layers.append(TPOptLayer(lin["qkv"], lin["out"], lin["fc1"], lin["fc2"], process_group=pg))
+    # the same layers with the row-parallel decode GEMMs fused with a one-shot all-reduce over NVLink
+    # peer memory (NEXT-1), on one-rank-per-GPU NCCL groups only
+    # Opt-in (--xr-layer): the fused path is verified on one GPU (all ranks on one device,
+    # tests/test_gpu_xr.py) but has never run on a multi-GPU box, and a failure there (a trapped wait
+    # kernel) would cost the whole scaling line.
+    fused_ok = world > 1 and args.xr_layer and os.environ.get("FQ_BENCH_ONE_GPU") != "1"
+    flayers = [TPOptLayer(L.qkv, L.out, L.fc1, L.fc2, process_group=pg, fused=True) for L in layers] if fused_ok else []
     torch.cuda.empty_cache()
     stream = torch.cuda.current_stream()
     out = {"layers": n_layers, "h": h, "bits": 4, "group": 128, "tp": world,
@@ -516,6 +525,25 @@ def measure_tp_layer(fq, dev, world, rank, args, n_layers=4, Ms=(1, 16, 2048), r
         lay, com = float(tt[0]), float(tt[1])
         ent = {"layer_us": round(lay, 1), "comm_us": round(com, 1), "comm_frac": round(com / lay, 3),
                "TB_s": round(full_bytes / (lay * 1e-6) / 1e12, 3)}
+        if flayers and M <= 16:
+            try:
+                for _ in range(2):
+                    for L in flayers:
+                        L.forward(x)
+                torch.cuda.synchronize()
+                dist.barrier()
+                a.record(stream)
+                for _ in range(reps):
+                    for L in flayers:
+                        L.forward(x)
+                b.record(stream)
+                torch.cuda.synchronize()
+                fl_us = torch.tensor([a.elapsed_time(b) / (reps * n_layers) * 1e3], device=dev, dtype=torch.float64)
+                dist.all_reduce(fl_us, op=dist.ReduceOp.MAX)
+                ent["fused_allreduce_layer_us"] = round(float(fl_us), 1)
+                ent["fused_allreduce_TB_s"] = round(full_bytes / (float(fl_us) * 1e-6) / 1e12, 3)
+            except Exception as e:  # symmetric memory unavailable on this box: report, keep the NCCL numbers
+                ent["fused_allreduce_error"] = str(e)[:200]
         if M >= 256:
             fl = 2.0 * M * full_bytes / (0.5 + 2 / 128)  # 2 M FLOP per weight (full layer)
             ent["TFLOP_s"] = round(fl / (lay * 1e-6) / 1e12, 1)

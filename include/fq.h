@@ -259,6 +259,43 @@ fq_status fq_gemm_i8(const void* a_q, const float* a_scale, const int32_t* a_row
                      int64_t N, int32_t group, const void* codes, const void* zscales, const float* colscale,
                      void* C, int32_t cdt, void* ws, size_t ws_bytes, void* stream);
 
+/* ---------------------------------------------------------------------------------------------
+ * Fused row-parallel GEMM + one-shot all-reduce.  Row-parallel layers (out-proj,
+ * FC2) end in "an all reduce after each attention and FFN block" (§2.1).  Here the decode GEMM
+ * (M <= 16, or <= 32 on the int4 nibble path) of each rank pushes its final fp32 partial of every
+ * output tile straight into the tile owner's receive slot over NVLink peer memory (tile t is owned
+ * by rank t % world); the last rank to arrive at the owner's counter sums the `world` slots in rank
+ * order (deterministic, identical on every rank) and writes the tile to EVERY rank's output.  No
+ * kernel waits on another GPU inside the GEMM; fq_xr_wait (one tiny kernel) makes the output ready
+ * on this rank's stream.  Larger M (prefill): FQ_ERR_UNSUPPORTED (use an NCCL all-reduce).
+ *   d_shard: this rank's K-shard [N, K/world] (codes/scales as fq_quantize_rowshard produces).
+ *   peers_host: the table below (host copy, validated); peers_dev: a DEVICE copy of the same bytes
+ *     (caller-owned, written once), read by the kernels.  Pointers are device addresses valid in
+ *     this process (peer memory mapped via CUDA IPC / symmetric memory, or, for one-GPU tests, plain
+ *     buffers of one device).  recv: fq_xr_recv_bytes(M, d_shard, world) bytes per rank; arrive:
+ *     fq_xr_counter_bytes(M, d_shard) bytes per rank and done: one int32 per rank, all zero-filled
+ *     once and self-resetting; out: [M, N] of dtype cdt (adt or FP32) on every rank.
+ *   ws: fq_gemm_workspace_bytes_ex(M, d_shard, {.path = FQ_PATH_DECODE}) bytes (fq_gemm's contract).
+ *   Calls of a group must be issued in the same order on every rank, each followed by fq_xr_wait on
+ *   the same stream before the outputs are read or the buffers reused.  fq_xr_wait traps (a sticky
+ *   CUDA error at the next synchronisation) if the group does not complete within 5 s.
+ * ------------------------------------------------------------------------------------------- */
+#define FQ_XR_MAX_WORLD 8
+typedef struct {
+  int32_t world;                       /* 1 .. FQ_XR_MAX_WORLD */
+  int32_t rank;                        /* 0 .. world-1 */
+  float* recv[FQ_XR_MAX_WORLD];        /* each rank's receive slots */
+  int32_t* arrive[FQ_XR_MAX_WORLD];    /* each rank's per-tile arrival counters */
+  int32_t* done[FQ_XR_MAX_WORLD];      /* each rank's completion counter */
+  void* out[FQ_XR_MAX_WORLD];          /* each rank's output C [M, N] */
+} fq_xr_peers;
+size_t fq_xr_recv_bytes(int64_t M, const fq_wdesc* d_shard, int32_t world);
+size_t fq_xr_counter_bytes(int64_t M, const fq_wdesc* d_shard);
+fq_status fq_gemm_allreduce(const void* A, int32_t adt, int64_t M, const fq_wdesc* d_shard, const void* codes,
+                            const void* scales, int32_t cdt, const fq_xr_peers* peers_host, const void* peers_dev,
+                            void* ws, size_t ws_bytes, void* stream);
+fq_status fq_xr_wait(const fq_xr_peers* peers_host, int64_t M, const fq_wdesc* d_shard, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

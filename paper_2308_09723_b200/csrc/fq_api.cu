@@ -381,4 +381,60 @@ fq_status fq_gemm_i8(const void* a_q, const float* a_scale, const int32_t* a_row
                                ws_bytes, as_stream(stream)));
 }
 
+// ------------------------------------------------------------------------------------------------
+// Fused row-parallel GEMM + one-shot all-reduce (decode kernel epilogue)
+static_assert(sizeof(fq_xr_peers) == sizeof(XRPeers) && FQ_XR_MAX_WORLD == kXRMaxWorld, "peer table layout");
+
+static fq_status xr_plan(int64_t M, const fq_wdesc* d, GemvPlan& pl) {
+  const fq_status s = check_wdesc(d);
+  if (s != FQ_OK) return s;
+  if (M <= 0 || M > gemv_max_m(d->bits, d->group)) return FQ_ERR_UNSUPPORTED;  // decode kernel only
+  pl = plan_gemv((int)M, (int)d->K, (int)d->N, d->bits, d->group, num_sms(), 0);
+  return FQ_OK;
+}
+
+static fq_status check_peers(const fq_xr_peers* x) {
+  if (!x || x->world < 1 || x->world > FQ_XR_MAX_WORLD || x->rank < 0 || x->rank >= x->world)
+    return FQ_ERR_INVALID_ARG;
+  for (int r = 0; r < x->world; ++r)
+    if (!x->recv[r] || !x->arrive[r] || !x->done[r] || !x->out[r]) return FQ_ERR_INVALID_ARG;
+  return FQ_OK;
+}
+
+size_t fq_xr_recv_bytes(int64_t M, const fq_wdesc* d, int32_t world) {
+  GemvPlan pl;
+  if (world < 1 || world > FQ_XR_MAX_WORLD || xr_plan(M, d, pl) != FQ_OK) return 0;
+  return (size_t)xr_tiles(pl, (int)d->N) * world * xr_tile_elems(pl) * sizeof(float);
+}
+
+size_t fq_xr_counter_bytes(int64_t M, const fq_wdesc* d) {
+  GemvPlan pl;
+  if (xr_plan(M, d, pl) != FQ_OK) return 0;
+  return (size_t)xr_tiles(pl, (int)d->N) * sizeof(int32_t);
+}
+
+fq_status fq_gemm_allreduce(const void* A, int32_t adt, int64_t M, const fq_wdesc* d, const void* codes,
+                            const void* scales, int32_t cdt, const fq_xr_peers* peers_host, const void* peers_dev,
+                            void* ws, size_t ws_bytes, void* stream) {
+  GemvPlan pl;
+  fq_status s = xr_plan(M, d, pl);
+  if (s != FQ_OK) return s;
+  if ((s = check_peers(peers_host)) != FQ_OK) return s;
+  if (!valid_half(adt) || d->scale_dtype != adt || (cdt != adt && cdt != FQ_FP32)) return FQ_ERR_UNSUPPORTED;
+  if (!A || !codes || !scales || !peers_dev) return FQ_ERR_INVALID_ARG;
+  const size_t need = gemv_workspace_bytes(pl, (int)M, (int)d->K, (int)d->N, d->bits, d->group);
+  if (need > 65536 && (!ws || ws_bytes < need)) return FQ_ERR_WORKSPACE;
+  return from_cuda(run_gemv(pl, adt, cdt, d->bits, A, (int)M, (int)d->K, (int)d->N, codes, scales, d->group,
+                            peers_host->out[peers_host->rank], ws, as_stream(stream),
+                            reinterpret_cast<const XRPeers*>(peers_dev)));
+}
+
+fq_status fq_xr_wait(const fq_xr_peers* peers_host, int64_t M, const fq_wdesc* d, void* stream) {
+  GemvPlan pl;
+  fq_status s = xr_plan(M, d, pl);
+  if (s != FQ_OK) return s;
+  if ((s = check_peers(peers_host)) != FQ_OK) return s;
+  return from_cuda(run_xr_wait(peers_host->done[peers_host->rank], xr_tiles(pl, (int)d->N), as_stream(stream)));
+}
+
 }  // extern "C"

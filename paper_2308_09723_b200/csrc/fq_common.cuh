@@ -183,6 +183,18 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
                : "memory");
 }
 
+// ---- system-scope accesses (peer memory over NVLink, fused all-reduce) ------------------------
+__device__ __forceinline__ float ld_relaxed_sys(const float* p) {
+  float v;
+  asm volatile("ld.relaxed.sys.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int ld_acquire_sys(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // ---- programmatic dependent launch (PDL) -----------------------------------------------------
 // griddep_wait: block until the grids this launch depends on have completed and their writes
 // are visible (no-op when launched without the PDL attribute).  griddep_launch_dependents: allow

@@ -105,6 +105,7 @@ struct DecProb {
   int sc_rows;    // per-element-scale path: scale rows per stage staged by TMA (KS / group), 0 = read
                   // from global memory (groups that do not divide the stage)
   int sc_shift;   // log2(group) when sc_rows > 0
+  const XRPeers* xr;  // fused row-parallel all-reduce (NEXT-1), device copy of the peer table; or null
 };
 template <int MAXP>
 struct DecBatch {
@@ -786,6 +787,57 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
     else reinterpret_cast<T*>(p.C)[o] = Dt<T>::from_f(v);
   };
   const int S_ = p.splits;
+  // Fused row-parallel all-reduce ("we must issue an all reduce after each attention
+  // and FFN block", §2.1): the rank's final partial of this output tile is pushed into the tile
+  // owner's receive slot (rank-indexed), and the last of the `world` ranks to arrive at the owner's
+  // counter sums the slots in rank order (deterministic) and writes the tile to every rank's output,
+  // then bumps every rank's completion counter (fq_xr_wait waits for it).  No CTA ever waits on
+  // another GPU, so the GEMMs of all ranks complete independently.
+  const XRPeers* xr = p.xr;
+  const int tile = bz * p.gx + bx;
+  const int tile_elems = MT * 8 * kRowsPerCta;
+  float* xslot = nullptr;
+  if (xr) {
+    const int owner = tile % xr->world;
+    xslot = xr->recv[owner] + ((size_t)tile * xr->world + xr->rank) * tile_elems;
+  }
+  auto emit = [&](int tok, int n, float v) {  // this rank's final value of output (tok, n)
+    if (xslot) xslot[(tok - tok0) * kRowsPerCta + (n - n0)] = v;
+    else store_out(tok, n, v);
+  };
+  auto xr_finish = [&]() {  // consumer warps only; every local value of the tile emitted
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kConsumerWarps));
+    const int owner = tile % xr->world;
+    if (threadIdx.x == 32) {
+      __threadfence_system();
+      const int last = atomicAdd_system(xr->arrive[owner] + tile, 1) == xr->world - 1;
+      if (last) __threadfence_system();
+      s_last = last;
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kConsumerWarps));
+    if (!s_last) return;
+    const int c = threadIdx.x - 32;
+    const int n = n0 + c;
+    const int ntok = min(M - tok0, MT * 8);
+    const float* slots = xr->recv[owner] + (size_t)tile * xr->world * tile_elems;
+    if (n < N) {
+      for (int j = 0; j < ntok; ++j) {
+        float v = 0.f;
+        for (int r = 0; r < xr->world; ++r) v += ld_relaxed_sys(slots + (size_t)r * tile_elems + j * kRowsPerCta + c);
+        const size_t o = (size_t)(tok0 + j) * N + n;
+        for (int d = 0; d < xr->world; ++d) {
+          if (p.cdt == FQ_FP32) reinterpret_cast<float*>(xr->out[d])[o] = v;
+          else reinterpret_cast<T*>(xr->out[d])[o] = Dt<T>::from_f(v);
+        }
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kConsumerWarps));
+    if (threadIdx.x == 32) {
+      xr->arrive[owner][tile] = 0;  // self-reset (every rank of this call has arrived)
+      __threadfence_system();
+      for (int d = 0; d < xr->world; ++d) atomicAdd_system(xr->done[d], 1);
+    }
+  };
   if (S_ == 1) {
 #pragma unroll
     for (int rt = 0; rt < 2; ++rt)
@@ -795,8 +847,9 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
         for (int i = 0; i < 4; ++i) {
           int n, tok;
           out_idx(rt, mt, i, n, tok);
-          if (n < N && tok < M) store_out(tok, n, acc[rt][mt][i]);
+          if (n < N && tok < M) emit(tok, n, acc[rt][mt][i]);
         }
+    if (xr) xr_finish();
     return;
   }
   float* part_out = p.ws + (size_t)by * M * N;
@@ -838,11 +891,31 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-          if (j0 + u < ntok) store_out(tok0 + j0 + u, n, v[u]);
+          if (j0 + u < ntok) emit(tok0 + j0 + u, n, v[u]);
       }
     }
   }
   if (threadIdx.x == 32) *ctr = 0;  // self-reset for the next call / graph replay
+  if (xr) xr_finish();
+}
+
+// Completion of a fused row-parallel GEMM on this rank (fq_xr_wait): every output tile has been
+// written by its reducing CTA (possibly on another GPU) once `done` reaches the tile count.
+// A peer that never arrives (a rank that skipped the call) traps after 5 s instead of hanging the
+// device: the error surfaces at the caller's next synchronisation.
+__global__ void xr_wait_kernel(int32_t* done, int expected) {
+  griddep_launch_dependents();
+  if (threadIdx.x == 0) {
+    uint64_t t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (ld_acquire_sys(done) < expected) {
+      __nanosleep(256);
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 5000000000ull) __trap();
+    }
+    *done = 0;  // self-reset: no rank can contribute to this rank's next call before it starts
+    __threadfence_system();
+  }
 }
 
 // ---- activation pre-conversion for the nibble path (one launch per GEMM call, M x K elements) --
@@ -1092,9 +1165,15 @@ static int sacc_of(int bits, int group, int K = -1) {
   return (K >= 0 && gs_of(bits, group, K)) ? 2 : 0;
 }
 
+int xr_tile_elems(const GemvPlan& p) { return p.mt * 8 * kRowsPerCta; }
+int xr_tiles(const GemvPlan& p, int N) { return ((N + kRowsPerCta - 1) / kRowsPerCta) * p.ktiles; }
+cudaError_t run_xr_wait(int32_t* done, int expected, cudaStream_t st) {
+  return launch_pdl(xr_wait_kernel, 1, 32, 0, st, done, expected);
+}
+
 cudaError_t run_gemv(const GemvPlan& pl, int adt, int cdt, int bits, const void* A, int M, int K,
                      int N, const void* codes, const void* scales, int group, void* C, void* ws,
-                     cudaStream_t st) {
+                     cudaStream_t st, const XRPeers* xr_dev) {
   DecBatch<1> b{};
   if (nib_of(bits, group, K)) {
     char* pre = reinterpret_cast<char*>(ws) + kCounterBytes +
@@ -1109,6 +1188,7 @@ cudaError_t run_gemv(const GemvPlan& pl, int adt, int cdt, int bits, const void*
     return cudaErrorInvalidValue;
   }
   b.p[0].cta_begin = 0;
+  b.p[0].xr = xr_dev;
   b.nprob = 1;
   const int ctas = b.p[0].gx * pl.splits * pl.ktiles;
 #ifdef FQ_DIAG

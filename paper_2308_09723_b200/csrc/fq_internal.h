@@ -30,6 +30,17 @@ cudaError_t run_adapt_flags(int wdt, const void* W, int K, int N, int nlev, int 
 cudaError_t run_adapt_cross(const float* colmax, int world, int N, int nlev_cross, uint32_t alpha,
                             int32_t* flags, cudaStream_t st);
 
+// Fused row-parallel all-reduce (NEXT-1): the peer table every rank's decode GEMM reads (a device
+// copy of fq_xr_peers, include/fq.h).
+constexpr int kXRMaxWorld = 8;
+struct XRPeers {
+  int32_t world, rank;
+  float* recv[kXRMaxWorld];     // each rank's receive slots [tiles][world][tile elems] fp32
+  int32_t* arrive[kXRMaxWorld]; // each rank's per-tile arrival counters [tiles]
+  int32_t* done[kXRMaxWorld];   // each rank's completion counter
+  void* out[kXRMaxWorld];       // each rank's output C [M, N]
+};
+
 // Decode GEMM (mma.sync, kernels A4/A5).
 struct GemvPlan {
   int rows_per_cta;   // 128 * RT
@@ -47,7 +58,11 @@ size_t gemv_workspace_bytes(const GemvPlan& p, int M, int K, int N, int bits, in
 size_t gemv_grouped_workspace_bytes(int64_t T, int K, int bits);
 cudaError_t run_gemv(const GemvPlan& p, int adt, int cdt, int bits, const void* A, int M, int K,
                      int N, const void* codes, const void* scales, int group, void* C, void* ws,
-                     cudaStream_t st);
+                     cudaStream_t st, const XRPeers* xr_dev = nullptr);
+// fused all-reduce: receive-slot elements per output tile, tile count, and the completion wait
+int xr_tile_elems(const GemvPlan& p);
+int xr_tiles(const GemvPlan& p, int N);
+cudaError_t run_xr_wait(int32_t* done, int expected, cudaStream_t st);
 
 // MoE batch of decode problems (experts with 1 <= M_e <= 16), one launch per kernel class.
 cudaError_t run_gemv_grouped(int adt, int cdt, int bits, const void* A, int K, int N,

@@ -50,6 +50,16 @@ def make_opts(path: str | int = 0, splits: int = 0, tc_halves: int = 0, tc_dqg: 
     return fq_gemm_opts(path, splits, tc_halves, tc_dqg)
 
 
+XR_MAX_WORLD = 8
+
+
+class fq_xr_peers(ctypes.Structure):
+    """Peer table of a fused row-parallel GEMM group (include/fq.h)."""
+    _fields_ = [("world", ctypes.c_int32), ("rank", ctypes.c_int32),
+                ("recv", ctypes.c_void_p * XR_MAX_WORLD), ("arrive", ctypes.c_void_p * XR_MAX_WORLD),
+                ("done", ctypes.c_void_p * XR_MAX_WORLD), ("out", ctypes.c_void_p * XR_MAX_WORLD)]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"libfq.so not built ({LIB_PATH}); run __graft_entry__.build() "
@@ -83,6 +93,10 @@ def _load():
         "fq_quantize_acts_i8": (c.c_int, [P, I32, I64, I64, P, P, P, P, P]),
         "fq_gemm_i8_workspace_bytes": (SZ, [I64, I64, I64]),
         "fq_gemm_i8": (c.c_int, [P, P, P, I64, I64, I64, I32, P, P, P, P, I32, P, SZ, P]),
+        "fq_xr_recv_bytes": (SZ, [I64, WD, I32]),
+        "fq_xr_counter_bytes": (SZ, [I64, WD]),
+        "fq_gemm_allreduce": (c.c_int, [P, I32, I64, WD, P, P, I32, c.POINTER(fq_xr_peers), P, P, SZ, P]),
+        "fq_xr_wait": (c.c_int, [c.POINTER(fq_xr_peers), I64, WD, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -96,7 +110,8 @@ EXPORTED = ("fq_version", "fq_status_str", "fq_codes_bytes", "fq_scales_bytes", 
             "fq_adapt_flags_cross", "fq_quantize", "fq_quantize_rowshard", "fq_gemm_workspace_bytes",
             "fq_gemm", "fq_gemm_workspace_bytes_ex", "fq_gemm_ex", "fq_gemm_grouped_workspace_bytes",
             "fq_gemm_grouped", "fq_zscales_bytes", "fq_quantize_intscale", "fq_quantize_acts_i8",
-            "fq_gemm_i8_workspace_bytes", "fq_gemm_i8")
+            "fq_gemm_i8_workspace_bytes", "fq_gemm_i8", "fq_xr_recv_bytes", "fq_xr_counter_bytes",
+            "fq_gemm_allreduce", "fq_xr_wait")
 
 
 def _ptr(t):
@@ -474,3 +489,113 @@ def gemm_i8(A: torch.Tensor | None, qw: QuantizedWeightI8, out: torch.Tensor | N
     ws = workspace(nb, a_q.device, stream)
     fq_gemm_i8(a_q, sa, rs, M, qw.K, qw.N, qw.group, qw.codes, qw.zscales, qw.colscale, out, ws, stream)
     return out
+
+
+# ------------------------------------------------------------------------------ fused row-parallel all-reduce
+def fq_xr_recv_bytes(M: int, d: fq_wdesc, world: int) -> int:
+    return _lib.fq_xr_recv_bytes(M, ctypes.byref(d), world)
+
+
+def fq_xr_counter_bytes(M: int, d: fq_wdesc) -> int:
+    return _lib.fq_xr_counter_bytes(M, ctypes.byref(d))
+
+
+def fq_gemm_allreduce(A: torch.Tensor, M: int, d: fq_wdesc, codes: torch.Tensor, scales: torch.Tensor, cdt: int,
+                      peers: fq_xr_peers, peers_dev: torch.Tensor, ws: torch.Tensor | None, stream=None) -> None:
+    _check(_lib.fq_gemm_allreduce(_ptr(A), _DT[A.dtype], M, ctypes.byref(d), _ptr(codes), _ptr(scales), cdt,
+                                  ctypes.byref(peers), _ptr(peers_dev), _ptr(ws),
+                                  0 if ws is None else ws.numel() * ws.element_size(), _stream(stream)),
+           "fq_gemm_allreduce")
+
+
+def fq_xr_wait(peers: fq_xr_peers, M: int, d: fq_wdesc, stream=None) -> None:
+    _check(_lib.fq_xr_wait(ctypes.byref(peers), M, ctypes.byref(d), _stream(stream)), "fq_xr_wait")
+
+
+class XRRank:
+    """One rank's view of a fused row-parallel GEMM group: its peer table (host + device copy) and
+    its output buffer.  Build with xr_group_local (all ranks on one device: tests, one-GPU
+    diagnostics) or xr_group_symmetric (one rank per GPU, peer memory from torch symmetric memory)."""
+
+    def __init__(self, peers: fq_xr_peers, out: torch.Tensor, keep: list):
+        self.peers = peers
+        self.out = out
+        raw = bytes(peers)
+        self.peers_dev = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(out.device)
+        self._keep = keep  # the buffers the table points into
+
+    def gemm(self, A: torch.Tensor, qw_shard: "QuantizedWeight", stream=None) -> torch.Tensor:
+        """out = sum over ranks of A_r . dequant(W_r)^T, on every rank; stream-ordered (fq_xr_wait)."""
+        M = A.shape[0]
+        d = qw_shard.desc
+        nb = fq_gemm_workspace_bytes_ex(M, d, make_opts("decode"))  # the decode kernel's plan
+        ws = workspace(nb, A.device, stream)
+        fq_gemm_allreduce(A, M, d, qw_shard.codes, qw_shard.scales, _DT[self.out.dtype], self.peers,
+                          self.peers_dev, ws, stream)
+        fq_xr_wait(self.peers, M, d, stream)
+        return self.out
+
+
+def gemv_max_m(bits: int, group: int) -> int:
+    """Largest M the decode kernel serves in one pass (fq.h: 32 on the nibble path, else 16); the
+    fused all-reduce GEMM needs M within it."""
+    return 32 if bits <= 4 and group % 128 == 0 else 16
+
+
+def _xr_sizes(M: int, d: fq_wdesc, world: int):
+    rb, cb = fq_xr_recv_bytes(M, d, world), fq_xr_counter_bytes(M, d)
+    if rb == 0 or cb == 0:
+        raise FQError(FQ_ERR_UNSUPPORTED, "fused all-reduce: M beyond the decode kernel or bad shard")
+    return rb, cb
+
+
+def xr_group_local(world: int, M: int, d: fq_wdesc, out_dtype=torch.bfloat16, device="cuda") -> list:
+    """Every rank of a group on ONE device (pointers are plain device addresses)."""
+    assert 1 <= world <= XR_MAX_WORLD
+    rb, cb = _xr_sizes(M, d, world)
+    recv = [torch.zeros(rb // 4, dtype=torch.float32, device=device) for _ in range(world)]
+    arrive = [torch.zeros(cb // 4, dtype=torch.int32, device=device) for _ in range(world)]
+    done = [torch.zeros(1, dtype=torch.int32, device=device) for _ in range(world)]
+    outs = [torch.zeros((M, d.N), dtype=out_dtype, device=device) for _ in range(world)]
+    keep = recv + arrive + done + outs
+    ranks = []
+    for r in range(world):
+        pt = fq_xr_peers()
+        pt.world, pt.rank = world, r
+        for q in range(world):
+            pt.recv[q], pt.arrive[q] = recv[q].data_ptr(), arrive[q].data_ptr()
+            pt.done[q], pt.out[q] = done[q].data_ptr(), outs[q].data_ptr()
+        ranks.append(XRRank(pt, outs[r], keep))
+    return ranks
+
+
+def xr_group_symmetric(process_group, M: int, d: fq_wdesc, out_dtype=torch.bfloat16) -> XRRank:
+    """This rank of a group with one rank per GPU: the receive slots, counters and outputs live in
+    torch symmetric memory, whose peer mappings (NVLink) give every rank every other rank's address."""
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm
+    world, rank = dist.get_world_size(process_group), dist.get_rank(process_group)
+    assert 1 <= world <= XR_MAX_WORLD
+    rb, cb = _xr_sizes(M, d, world)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    ob = M * d.N * torch.tensor([], dtype=out_dtype).element_size()
+    sizes = [rb, cb, 256, ob]
+    offs = [0]
+    for sz in sizes[:-1]:
+        offs.append(offs[-1] + (sz + 255) // 256 * 256)
+    try:
+        symm.enable_symm_mem_for_group(process_group.group_name)
+    except Exception:
+        pass  # newer torch: implicit
+    buf = symm.empty(offs[-1] + sizes[-1], dtype=torch.uint8, device=dev)
+    buf.zero_()
+    h = symm.rendezvous(buf, process_group)
+    torch.cuda.synchronize()
+    dist.barrier(group=process_group)
+    pt = fq_xr_peers()
+    pt.world, pt.rank = world, rank
+    for q in range(world):
+        base = int(h.buffer_ptrs[q])
+        pt.recv[q], pt.arrive[q], pt.done[q], pt.out[q] = (base + o for o in offs)
+    out = buf[offs[3]:offs[3] + ob].view(out_dtype).view(M, d.N)
+    return XRRank(pt, out, [buf, h])

@@ -143,12 +143,25 @@ class TPOptLayer:
     layer) and every weight byte are."""
 
     def __init__(self, qkv: TPLinearFQ, out: TPLinearFQ, fc1: TPLinearFQ, fc2: TPLinearFQ,
-                 process_group=None):
+                 process_group=None, fused: bool = False):
         self.qkv, self.out, self.fc1, self.fc2 = qkv, out, fc1, fc2
         self.pg = process_group
         self.world = qkv.spec.world
+        # fused=True: row-parallel GEMMs of decode size (M within the decode kernel) run the fused
+        # GEMM + one-shot all-reduce over NVLink peer memory (fq.h fq_gemm_allreduce, NEXT-1) instead of
+        # GEMM -> NCCL all-reduce.  Its output buffer is reused by the next call of the same layer and M.
+        self.fused = fused and self.world > 1
+        self._xr = {}
 
     def _row(self, lin: TPLinearFQ, h: torch.Tensor, dtype) -> torch.Tensor:
+        from . import fq
+        M = h.shape[0]
+        if self.fused and M <= fq.gemv_max_m(lin.qw.bits, lin.qw.group):
+            key = (id(lin), M, dtype)
+            xr = self._xr.get(key)
+            if xr is None:
+                xr = self._xr[key] = fq.xr_group_symmetric(self.pg, M, lin.qw.desc, dtype)
+            return xr.gemm(h.contiguous(), lin.qw)
         part = lin(h, out_dtype=torch.float32)  # fp32 partials, summed across ranks
         if self.world > 1:
             dist.all_reduce(part, op=dist.ReduceOp.SUM, group=self.pg)

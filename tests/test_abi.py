@@ -236,3 +236,26 @@ def test_i8_path_sizes_and_validation(fq):
                                   None) == fq.FQ_ERR_SHAPE
     assert L.fq_quantize_intscale(dummy, 9, 1024, 256, 64, dummy, dummy, dummy, None,
                                   None) == fq.FQ_ERR_INVALID_ARG
+
+
+def test_xr_sizes_and_validation(fq):
+    """Fused row-parallel all-reduce (NEXT-1): buffer sizes follow the decode plan (256-column tiles x
+    token tiles of 8 / 16 / 32), prefill-sized M and bad peer tables are refused before any launch."""
+    d = fq.make_wdesc(6144, 12288, 4, 128, fq.FQ_BF16)   # an OPT-175B FC2 shard at t = 8
+    for M, mt in ((1, 1), (8, 1), (16, 2), (32, 4)):
+        tiles = (12288 // 256) * 1
+        assert fq.fq_xr_counter_bytes(M, d) == tiles * 4
+        assert fq.fq_xr_recv_bytes(M, d, 8) == tiles * 8 * (mt * 8 * 256) * 4
+    assert fq.fq_xr_recv_bytes(33, d, 8) == 0 and fq.fq_xr_counter_bytes(64, d) == 0
+    assert fq.fq_xr_recv_bytes(8, d, 0) == 0 and fq.fq_xr_recv_bytes(8, d, 9) == 0
+    dummy = ctypes.c_void_p(16)
+    pt = fq.fq_xr_peers()
+    pt.world, pt.rank = 2, 0
+    pt.recv[0] = pt.arrive[0] = pt.done[0] = pt.out[0] = 16   # rank 1's entries missing
+    st = fq._lib.fq_gemm_allreduce(dummy, 0, 4, ctypes.byref(d), dummy, dummy, 0, ctypes.byref(pt), dummy,
+                                   None, 0, None)
+    assert st == fq.FQ_ERR_INVALID_ARG
+    pt.recv[1] = pt.arrive[1] = pt.done[1] = pt.out[1] = 32
+    st = fq._lib.fq_gemm_allreduce(dummy, 0, 40, ctypes.byref(d), dummy, dummy, 0, ctypes.byref(pt), dummy,
+                                   None, 0, None)
+    assert st == fq.FQ_ERR_UNSUPPORTED                    # M beyond the decode kernel
