@@ -323,11 +323,15 @@ template <typename T, int BITS, int MT, int SACC, int DBG, int MAXP>
 #ifndef FQ_DEC_NIB_MAXREG
 #define FQ_DEC_NIB_MAXREG 96  // measured: faster than 104 or 112 (which ptxas schedules worse)
 #endif
+// Two CTAs of 9 warps per SM need <= 96 registers: the register file is four 16K banks, one per SM
+// sub-partition, and 18 warps put 5 on some sub-partition (5 x 32 x 104 > 16384 would leave ONE CTA
+// per SM -- measured: FC1 M=16 99 -> 85 us, M=32 166 -> 148 us with the 96 cap;
+// profiles/r02/decode_regcap_ab.txt).
 #ifndef FQ_DEC_NIB2_MAXREG
-#define FQ_DEC_NIB2_MAXREG 104  // two 8-token MMA tiles (9 <= M <= 16); measured best of 96/104/112
+#define FQ_DEC_NIB2_MAXREG 96  // two 8-token MMA tiles (9 <= M <= 16)
 #endif
 #ifndef FQ_DEC_NIB4_MAXREG
-#define FQ_DEC_NIB4_MAXREG 112  // four 8-token MMA tiles (17 <= M <= 32); 2 CTAs x 288 threads fit 113
+#define FQ_DEC_NIB4_MAXREG 96  // four 8-token MMA tiles (17 <= M <= 32)
 #endif
 __global__ void __maxnreg__((FQ_NIB && BITS <= 4 && SACC)
                                ? (MT == 4 ? FQ_DEC_NIB4_MAXREG : MT == 2 ? FQ_DEC_NIB2_MAXREG : FQ_DEC_NIB_MAXREG)
