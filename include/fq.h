@@ -221,6 +221,20 @@ fq_status fq_gemm_grouped(const void* A, int32_t adt, int64_t T, const int64_t* 
                           const void* const* codes_host, const void* const* scales_host, void* C,
                           int32_t cdt, void* ws, size_t ws_bytes, void* stream);
 
+/* The same batch with the expert offsets on the DEVICE (SURVEY §8(b) expert_offsets_dev): MoE routing
+ * is produced on the GPU, so no D2H copy or host synchronisation is needed per MoE layer.
+ * offsets_dev: DEVICE int64 [E+1], non-decreasing, offsets[0] = 0, offsets[E] <= T (read by the
+ * kernels; it may be written by the previous kernel on the stream).  T = rows of A and C (capacity).
+ * max_tokens: a host-known bound on every expert's token count (e.g. the router's capacity); it picks
+ * the kernel (decode kernel A4 when <= 16 / 32, else tcgen05 A6) and the launch geometry.  Experts
+ * with more tokens than max_tokens, or offsets outside [0, T], are clamped (their extra rows are not
+ * computed) and set bit 2 of status_dev (nullable).  ws: fq_gemm_grouped_workspace_bytes(T, E, d).
+ * Empty experts cost one early-exiting CTA per tile of the bound. */
+fq_status fq_gemm_grouped_dev(const void* A, int32_t adt, int64_t T, const int64_t* offsets_dev, int32_t E,
+                              const fq_wdesc* d, const int32_t* groups_host, const void* const* codes_host,
+                              const void* const* scales_host, void* C, int32_t cdt, int64_t max_tokens,
+                              int32_t* status_dev, void* ws, size_t ws_bytes, void* stream);
+
 /* ---------------------------------------------------------------------------------------------
  * int8 activations x int4 weights with INTEGER group scales -- the paper's future work: "the
  * proposed method does not leverage integer instructions even when they are available" (§5),

@@ -437,4 +437,44 @@ fq_status fq_xr_wait(const fq_xr_peers* peers_host, int64_t M, const fq_wdesc* d
   return from_cuda(run_xr_wait(peers_host->done[peers_host->rank], xr_tiles(pl, (int)d->N), as_stream(stream)));
 }
 
+// ------------------------------------------------------------------------------------------------
+// MoE batch with DEVICE expert offsets (SURVEY §8(b) expert_offsets_dev): the router's output stays on
+// the device; the host supplies only the static per-expert weights and a token bound.
+fq_status fq_gemm_grouped_dev(const void* A, int32_t adt, int64_t T, const int64_t* offsets_dev, int32_t E,
+                              const fq_wdesc* d, const int32_t* groups_host, const void* const* codes_host,
+                              const void* const* scales_host, void* C, int32_t cdt, int64_t max_tokens,
+                              int32_t* status_dev, void* ws, size_t ws_bytes, void* stream) {
+  if (!d || !offsets_dev || !groups_host || !codes_host || !scales_host || E <= 0) return FQ_ERR_INVALID_ARG;
+  if (!valid_half(adt) || d->scale_dtype != adt || (cdt != adt && cdt != FQ_FP32)) return FQ_ERR_UNSUPPORTED;
+  if (d->bits < 4) return FQ_ERR_UNSUPPORTED;
+  if (T < 0 || T > (1 << 20) || max_tokens < 0 || max_tokens > (1 << 20)) return FQ_ERR_SHAPE;
+  for (int32_t e = 0; e < E; ++e) {
+    fq_wdesc de = *d;
+    de.group = groups_host[e];
+    const fq_status s = check_wdesc(&de);
+    if (s != FQ_OK) return s;
+    if (!codes_host[e] || !scales_host[e]) return FQ_ERR_INVALID_ARG;
+  }
+  if (T == 0 || max_tokens == 0) return FQ_OK;  // nothing can be routed: nothing launched
+  if (!A || !C) return FQ_ERR_INVALID_ARG;
+  const Tune t{};
+  std::vector<int> small, large;
+  for (int32_t e = 0; e < E; ++e)
+    (!use_tc_path(max_tokens, d->bits, groups_host[e], 0, t) ? small : large).push_back(e);
+  if (!small.empty() && (!ws || ws_bytes < gemv_grouped_workspace_bytes(T, (int)d->K, d->bits)))
+    return FQ_ERR_WORKSPACE;
+  const cudaStream_t st = as_stream(stream);
+  if (!large.empty()) {
+    cudaError_t r = run_gemm_tc_grouped_dev(adt, cdt, d->bits, A, T, (int)d->K, (int)d->N, offsets_dev, groups_host,
+                                            codes_host, scales_host, C, (int)max_tokens, large.data(),
+                                            (int)large.size(), status_dev, st);
+    if (r != cudaSuccess) return FQ_ERR_CUDA;
+  }
+  if (!small.empty())
+    return from_cuda(run_gemv_grouped_dev(adt, cdt, d->bits, A, T, (int)d->K, (int)d->N, offsets_dev, groups_host,
+                                          codes_host, scales_host, C, ws, (int)max_tokens, small.data(),
+                                          (int)small.size(), status_dev, st));
+  return FQ_OK;
+}
+
 }  // extern "C"

@@ -163,7 +163,23 @@ struct TcProb {
   int splits, kbs;   // split-K (few output tiles): K-block ranges of kbs blocks per work item
   float* ws;         // split-K fp32 partials [tiles * splits][bn][128]
   int* ctr;          // split-K arrival counters per output tile (self-resetting)
+  // MoE batch with DEVICE expert offsets (fq_gemm_grouped_dev): rows offs[e] .. offs[e+1]-1 of the
+  // whole A / C (the activation map spans all `rows`); M is the launch's token bound.
+  const int64_t* offs;
+  int e, rows;
+  int32_t* status;   // nullable: bit 2 = more tokens than the bound / offsets outside [0, rows]
 };
+// this problem's first row and token count (device offsets clamped to the rows and the bound)
+__device__ __forceinline__ void prob_rows(const TcProb& p, int& row0, int& Me) {
+  row0 = 0;
+  Me = p.M;
+  if (p.offs) {
+    const int64_t o0 = p.offs[p.e], o1 = p.offs[p.e + 1];
+    const int64_t lo = max((int64_t)0, min(o0, (int64_t)p.rows)), hi = max(lo, min(o1, (int64_t)p.rows));
+    row0 = (int)lo;
+    Me = (int)min(hi - lo, (int64_t)p.M);
+  }
+}
 // work item -> (token tile, weight-row tile, K-block range); work items of one output tile are
 // consecutive (its K splits run concurrently on neighbouring CTAs)
 template <int BK>
@@ -258,12 +274,15 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
         const TcProb& p = find_prob(batch, tile);
         int mt, nt, tt, ks, kb0, kb1;
         work_coords<BK>(p, tile, mt, nt, tt, ks, kb0, kb1);
+        int row0, Me;
+        prob_rows(p, row0, Me);
+        if (mt * p.bn >= Me) continue;  // device offsets: token tile beyond this expert's tokens
         // first scale row of the K block = floor(BK kb / g), division-free after the first block
         const int grp = p.group;  // hoisted out of the parameter space
         // halves entirely past the last weight row are not loaded (their TMEM rows are never stored)
         const int nh = HM == 1 ? 1 : min(HM, (p.N - nt * BMT + BM - 1) / BM);
         const uint32_t tx = p.bn * BK * 2 + nh * (Gm::CODE_HALF + Gm::SC_HALF);
-        const int arow = mt * p.bn, wrow = nt * BMT;
+        const int arow = row0 + mt * p.bn, wrow = nt * BMT;
         int j0 = (kb0 * BK) / grp, r0 = (kb0 * BK) - j0 * grp;
         for (int kb = kb0; kb < kb1; ++kb, r0 += BK) {
           while (r0 >= grp) { r0 -= grp; ++j0; }
@@ -292,6 +311,9 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
         const TcProb& pp = find_prob(batch, tile);
         int mt_, nt_, tt_, ks_, kb0, kb1;
         work_coords<BK>(pp, tile, mt_, nt_, tt_, ks_, kb0, kb1);
+        int row0_, Me_;
+        prob_rows(pp, row0_, Me_);
+        if (mt_ * pp.bn >= Me_) continue;
         const uint32_t idesc = idesc_f16<T, BM, 16>() + ((uint32_t)((pp.bn >> 3) - 2) << 17);  // N = bn
         mbar_wait(&acc_empty, acc_ph ^ 1);  // epilogue drained the accumulator
         fence_after();
@@ -334,9 +356,12 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
     uint32_t ph = 0, aph = 0, acc_ph = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const TcProb& p = find_prob(batch, tile);
-      const int N = p.N, M = p.M;
+      const int N = p.N;
       int mt, nt, tt, ks, kb0, kb1;
       work_coords<BK>(p, tile, mt, nt, tt, ks, kb0, kb1);
+      int row0, M;
+      prob_rows(p, row0, M);
+      if (mt * p.bn >= M) continue;
       const int grp = p.group;                     // hoisted: p lives in the parameter space
       const bool one_scale = grp % kKPW == 0;      // this thread's kKPW k lie in one group
       int j0 = (kb0 * BK) / grp, r0 = kb0 * BK - j0 * grp;  // first staged scale row
@@ -450,8 +475,8 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
       for (int h = 0; h < HM; ++h) {
         const int n = nt * BMT + h * BM + row;
         auto store = [&](int tok, float f) {
-          if (p.cdt == FQ_FP32) reinterpret_cast<float*>(p.C)[(size_t)tok * N + n] = f;
-          else reinterpret_cast<T*>(p.C)[(size_t)tok * N + n] = Dt<T>::from_f(f);
+          if (p.cdt == FQ_FP32) reinterpret_cast<float*>(p.C)[(size_t)(row0 + tok) * N + n] = f;
+          else reinterpret_cast<T*>(p.C)[(size_t)(row0 + tok) * N + n] = Dt<T>::from_f(f);
         };
 #pragma unroll 1
         for (int c0 = 0; c0 < TPP && half * TPP + c0 < p.bn; c0 += 32) {
@@ -508,7 +533,7 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
               for (int u = 0; u < 4; ++u) {
                 const int tl = tl0 + NPAR * u;
                 if (tl < tmax) {
-                  const size_t o = (size_t)(mt * p.bn + tl) * N + nr;
+                  const size_t o = (size_t)(row0 + mt * p.bn + tl) * N + nr;
                   if (p.cdt == FQ_FP32) reinterpret_cast<float*>(p.C)[o] = acc[u];
                   else reinterpret_cast<T*>(p.C)[o] = Dt<T>::from_f(acc[u]);
                 }
@@ -718,6 +743,38 @@ cudaError_t run_gemm_tc(int adt, int cdt, int bits, const void* A, int M, int K,
   b.nprob = 1;
   b.total_tiles = d.m_tiles * d.n_tiles * d.splits;
   return dispatch_tc<1>(adt, bits, b, st, tune.dqg);
+}
+
+// MoE with DEVICE expert offsets (fq_gemm_grouped_dev): every listed expert is laid out for `Mmax`
+// tokens; tiles beyond an expert's device token count are skipped by all warps of the CTA.
+cudaError_t run_gemm_tc_grouped_dev(int adt, int cdt, int bits, const void* A, int64_t T, int K, int N,
+                                    const int64_t* offs_dev, const int32_t* groups, const void* const* codes,
+                                    const void* const* scales, void* C, int Mmax, const int* experts, int nexp,
+                                    int32_t* status, cudaStream_t st) {
+  constexpr int MAXP = 48;
+  tc::TcBatch<MAXP> b{};
+  const int bn = tc_bn(Mmax), bk = tc_bk(bn), hm = tc_hm_batch(bn);
+  for (int ii = 0; ii < nexp; ++ii) {
+    const int e = experts[ii];
+    tc::TcProb& d = b.p[b.nprob];
+    if (!make_tc_prob(d, bits, A, Mmax, K, N, codes[e], scales[e], groups[e], C, cdt, bk, hm)) return cudaErrorInvalidValue;
+    if (!make_tmap_2d(&d.a, A, 2, (uint64_t)K, (uint64_t)T, (uint64_t)K * 2, tc::BKA, d.bn, 128))  // all T rows
+      return cudaErrorInvalidValue;
+    d.offs = offs_dev;
+    d.e = e;
+    d.rows = (int)T;
+    d.status = status;
+    d.tile_begin = b.total_tiles;
+    b.total_tiles += d.m_tiles * d.n_tiles;
+    if (++b.nprob == MAXP) {
+      cudaError_t r = dispatch_tc<MAXP>(adt, bits, b, st);
+      if (r != cudaSuccess) return r;
+      b.nprob = 0;
+      b.total_tiles = 0;
+    }
+  }
+  if (b.nprob) return dispatch_tc<MAXP>(adt, bits, b, st);
+  return cudaSuccess;
 }
 
 // MoE: every listed expert (M_e > 16) in one persistent launch per <= 48 experts.

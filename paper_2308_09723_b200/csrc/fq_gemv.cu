@@ -106,6 +106,12 @@ struct DecProb {
                   // from global memory (groups that do not divide the stage)
   int sc_shift;   // log2(group) when sc_rows > 0
   const XRPeers* xr;  // fused row-parallel all-reduce (NEXT-1), device copy of the peer table; or null
+  // MoE batch with DEVICE expert offsets (fq_gemm_grouped_dev): rows offs[e] .. offs[e+1]-1 of the
+  // whole A / A' / C; M is then an upper bound (the launch geometry) and `a`, `sm`, C span all rows.
+  const int64_t* offs;
+  int e;
+  int rows;          // rows of A / C (device offsets are clamped to them)
+  int32_t* status;   // nullable: bit 2 = some expert had more tokens than the launch bound / bad offsets
 };
 template <int MAXP>
 struct DecBatch {
@@ -373,12 +379,25 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
   const DecProb& p = batch.p[pi];
   const int local = (int)blockIdx.x - p.cta_begin;
   const int bx = local % p.gx, by = (local / p.gx) % p.splits, bz = local / (p.gx * p.splits);
-  const int N = p.N, K = p.K, M = p.M;
+  const int N = p.N, K = p.K;
   const int n0 = bx * kRowsPerCta;
   const int kbeg = by * p.klen;
   const int kend = min(K, kbeg + p.klen);
   const int nst = (kend - kbeg + KS - 1) / KS;
   const int tok0 = bz * MT * 8;
+  int M = p.M, row0 = 0;  // row0: first row of this problem in A / A' / C (device offsets only)
+  if (p.offs) {
+    griddep_wait();  // the offsets may come from the previous kernel (the router)
+    const int64_t o0 = p.offs[p.e], o1 = p.offs[p.e + 1];
+    // rows outside [0, rows) or beyond the launch's token bound are not computed (status bit 2)
+    const int64_t lo = max((int64_t)0, min(o0, (int64_t)p.rows)), hi = max(lo, min(o1, (int64_t)p.rows));
+    row0 = (int)lo;
+    M = (int)min(hi - lo, (int64_t)p.M);
+    if (threadIdx.x == 0 && blockIdx.x == p.cta_begin && p.status && (hi - lo > p.M || lo != o0 || hi != o1))
+      atomicOr(p.status, 4);
+    if (tok0 >= M) return;  // token tile beyond this expert's tokens: the whole CTA leaves
+  }
+  const int tok_base = p.offs ? row0 : p.tok_base;  // global token index of row 0 (nibble parity)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSTG; ++s) {
@@ -436,11 +455,11 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
         uint8_t* st = sbase + s * STAGE_BYTES;
         const int k0 = kbeg + i * KS;
         if (NIB) {
-          tma_load_2d(st + ACT_OFS, &p.a, &full_bar[s], k0, tok0, pola);
-          tma_load_2d(st + SUM_OFS, &p.sm, &full_bar[s], tok0 * 4, k0 / KCH, pola);
+          tma_load_2d(st + ACT_OFS, &p.a, &full_bar[s], k0, row0 + tok0, pola);
+          tma_load_2d(st + SUM_OFS, &p.sm, &full_bar[s], (row0 + tok0) * 4, k0 / KCH, pola);
         } else {
           mbar_arrive_expect_tx(&raw_bar[s], RAW_BYTES);
-          tma_load_2d(st + ACT_OFS, &p.a, &raw_bar[s], k0, tok0, pola);
+          tma_load_2d(st + ACT_OFS, &p.a, &raw_bar[s], k0, row0 + tok0, pola);
         }
       };
       // Weights are constants: the first NSTG stages are requested before waiting for the grid
@@ -552,7 +571,7 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
 #pragma unroll
     for (int w16 = 0; w16 < PIECES; ++w16)
       aofs[mt][w16] = ACT_OFS + (mt * 8 + gq) * ROWB +
-                      (((w16 * 4 + t) ^ (((NIB ? p.tok_base + tok0 + gq : gq) & 1) << 2)) << 4);
+                      (((w16 * 4 + t) ^ (((NIB ? tok_base + tok0 + gq : gq) & 1) << 2)) << 4);
   const uint32_t saofs = NIB ? SUM_OFS + 2 * t * 16 : SUM_OFS + 2 * t * 4;
   float acc[2][MT][4];
 #pragma unroll
@@ -786,7 +805,7 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
     tok = tok0 + mt * 8 + 2 * t + (i & 1);
   };
   auto store_out = [&](int tok, int n, float v) {
-    const size_t o = (size_t)tok * N + n;
+    const size_t o = (size_t)(row0 + tok) * N + n;
     if (p.cdt == FQ_FP32) reinterpret_cast<float*>(p.C)[o] = v;
     else reinterpret_cast<T*>(p.C)[o] = Dt<T>::from_f(v);
   };
@@ -1246,6 +1265,59 @@ cudaError_t run_gemv_grouped(int adt, int cdt, int bits, const void* A, int K, i
         return cudaErrorInvalidValue;
       d.cta_begin = ctas;
       ctas += d.gx * d.splits * d.ktiles;
+      if (++b.nprob == kMaxBatch) {
+        cudaError_t r = dispatch_dec<kMaxBatch>(adt, bits, mt, sacc, 0, b, ctas, st);
+        if (r != cudaSuccess) return r;
+        b.nprob = 0;
+        ctas = 0;
+      }
+    }
+    if (b.nprob) {
+      cudaError_t r = dispatch_dec<kMaxBatch>(adt, bits, mt, sacc, 0, b, ctas, st);
+      if (r != cudaSuccess) return r;
+    }
+  }
+  return cudaSuccess;
+}
+
+// ---- MoE batch with DEVICE expert offsets (fq_gemm_grouped_dev): every expert is launched with the
+// geometry of `Mmax` tokens; each CTA reads its expert's token range from the device and leaves if
+// its token tile is empty.  The activation maps span all T rows (tokens are addressed row0 + tok).
+cudaError_t run_gemv_grouped_dev(int adt, int cdt, int bits, const void* A, int64_t T, int K, int N,
+                                 const int64_t* offs_dev, const int32_t* groups, const void* const* codes,
+                                 const void* const* scales, void* C, void* ws, int Mmax, const int* experts,
+                                 int nexp, int32_t* status, cudaStream_t st) {
+  char* pre = reinterpret_cast<char*>(ws) + kCounterBytes;
+  char* Sp = pre + align256((size_t)T * K * 2);
+  bool any_nib = false;
+  for (int ii = 0; ii < nexp; ++ii) any_nib |= nib_of(bits, groups[experts[ii]]);
+  if (any_nib) {
+    cudaError_t r = launch_prep(adt, A, (int)T, K, pre, Sp, st);
+    if (r != cudaSuccess) return r;
+  }
+  for (int cls = 0; cls < 6; ++cls) {
+    const int mt = 1 << (cls >> 1);
+    const bool sacc = cls & 1;
+    DecBatch<kMaxBatch> b{};
+    int ctas = 0;
+    for (int ii = 0; ii < nexp; ++ii) {
+      const int e = experts[ii];
+      GemvPlan pl = plan_gemv(Mmax, K, N, bits, groups[e], num_sms());
+      pl.splits = 1;
+      pl.klen = ((K + pl.kchunk - 1) / pl.kchunk) * pl.kchunk;
+      if (pl.mt != mt || sacc_of(bits, groups[e]) != sacc) continue;
+      DecProb& d = b.p[b.nprob];
+      const bool nib = nib_of(bits, groups[e]);
+      if (!make_dec_prob(d, pl, bits, cdt, nib ? static_cast<const void*>(pre) : A, (int)T, K, N, codes[e],
+                         scales[e], groups[e], C, ws, nib ? Sp : nullptr, (int)T, 0))
+        return cudaErrorInvalidValue;
+      d.M = Mmax;
+      d.offs = offs_dev;
+      d.e = e;
+      d.rows = (int)T;
+      d.status = status;
+      d.cta_begin = ctas;
+      ctas += d.gx * d.ktiles;
       if (++b.nprob == kMaxBatch) {
         cudaError_t r = dispatch_dec<kMaxBatch>(adt, bits, mt, sacc, 0, b, ctas, st);
         if (r != cudaSuccess) return r;

@@ -70,6 +70,17 @@ cudaError_t run_gemv_grouped(int adt, int cdt, int bits, const void* A, int K, i
                              const void* const* scales, void* C, void* ws, int64_t T,
                              const int* experts, int nexp, cudaStream_t st);
 
+// MoE batches with DEVICE expert offsets (fq_gemm_grouped_dev): launch geometry from the token
+// bound Mmax, per-expert token ranges read on the device.
+cudaError_t run_gemv_grouped_dev(int adt, int cdt, int bits, const void* A, int64_t T, int K, int N,
+                                 const int64_t* offs_dev, const int32_t* groups, const void* const* codes,
+                                 const void* const* scales, void* C, void* ws, int Mmax, const int* experts,
+                                 int nexp, int32_t* status, cudaStream_t st);
+cudaError_t run_gemm_tc_grouped_dev(int adt, int cdt, int bits, const void* A, int64_t T, int K, int N,
+                                    const int64_t* offs_dev, const int32_t* groups, const void* const* codes,
+                                    const void* const* scales, void* C, int Mmax, const int* experts, int nexp,
+                                    int32_t* status, cudaStream_t st);
+
 // Large-M tensor-core GEMM (tcgen05 + TMEM, kernel A6).
 // Split-K when the output tiles cannot fill the SMs: workspace = 64 KiB counters (zero-filled once,
 // self-resetting) + fp32 partials; without it (ws == NULL or too small) the kernel runs unsplit.

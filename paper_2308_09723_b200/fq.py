@@ -88,6 +88,8 @@ def _load():
         "fq_gemm_grouped_workspace_bytes": (SZ, [I64, I32, WD]),
         "fq_gemm_grouped": (c.c_int, [P, I32, I64, c.POINTER(I64), I32, WD, c.POINTER(I32),
                                       c.POINTER(P), c.POINTER(P), P, I32, P, SZ, P]),
+        "fq_gemm_grouped_dev": (c.c_int, [P, I32, I64, P, I32, WD, c.POINTER(I32), c.POINTER(P), c.POINTER(P), P,
+                                          I32, I64, P, P, SZ, P]),
         "fq_zscales_bytes": (SZ, [I64, I64, I32]),
         "fq_quantize_intscale": (c.c_int, [P, I32, I64, I64, I32, P, P, P, P, P]),
         "fq_quantize_acts_i8": (c.c_int, [P, I32, I64, I64, P, P, P, P, P]),
@@ -109,7 +111,7 @@ EXPORTED = ("fq_version", "fq_status_str", "fq_codes_bytes", "fq_scales_bytes", 
             "fq_adapt_group_at", "fq_adapt_flags", "fq_adapt_decide", "fq_adapt_flags_rowshard",
             "fq_adapt_flags_cross", "fq_quantize", "fq_quantize_rowshard", "fq_gemm_workspace_bytes",
             "fq_gemm", "fq_gemm_workspace_bytes_ex", "fq_gemm_ex", "fq_gemm_grouped_workspace_bytes",
-            "fq_gemm_grouped", "fq_zscales_bytes", "fq_quantize_intscale", "fq_quantize_acts_i8",
+            "fq_gemm_grouped", "fq_gemm_grouped_dev", "fq_zscales_bytes", "fq_quantize_intscale", "fq_quantize_acts_i8",
             "fq_gemm_i8_workspace_bytes", "fq_gemm_i8", "fq_xr_recv_bytes", "fq_xr_counter_bytes",
             "fq_gemm_allreduce", "fq_xr_wait")
 
@@ -239,6 +241,17 @@ def fq_gemm_grouped(A, T, offsets_host, E, d, groups_host, codes_ptrs, scales_pt
                                 _ptr(C), _DT[C.dtype], _ptr(ws),
                                 0 if ws is None else ws.numel() * ws.element_size(), _stream(stream)),
            "fq_gemm_grouped")
+
+
+def fq_gemm_grouped_dev(A, T, offsets_dev: torch.Tensor, E, d, groups_host, codes_ptrs, scales_ptrs, C, max_tokens,
+                        ws, status: torch.Tensor | None = None, stream=None):
+    grps = (ctypes.c_int32 * E)(*[int(x) for x in groups_host])
+    cps = (ctypes.c_void_p * E)(*[int(x) for x in codes_ptrs])
+    sps = (ctypes.c_void_p * E)(*[int(x) for x in scales_ptrs])
+    _check(_lib.fq_gemm_grouped_dev(_ptr(A), _DT[A.dtype], T, _ptr(offsets_dev), E, ctypes.byref(d), grps, cps, sps,
+                                    _ptr(C), _DT[C.dtype], max_tokens, _ptr(status), _ptr(ws),
+                                    0 if ws is None else ws.numel() * ws.element_size(), _stream(stream)),
+           "fq_gemm_grouped_dev")
 
 
 def fq_zscales_bytes(K: int, N: int, group: int) -> int:
@@ -409,6 +422,25 @@ def gemm_grouped(A: torch.Tensor, offsets, experts: list, out: torch.Tensor | No
     ws = workspace(nb, A.device, stream)
     fq_gemm_grouped(A, T, offs, E, d, [q.group for q in experts], [q.codes.data_ptr() for q in experts],
                     [q.scales.data_ptr() for q in experts], out, ws, stream)
+    return out
+
+
+def gemm_grouped_dev(A: torch.Tensor, offsets_dev: torch.Tensor, experts: list, max_tokens: int,
+                     out: torch.Tensor | None = None, out_dtype=None, status: torch.Tensor | None = None,
+                     stream=None) -> torch.Tensor:
+    """MoE expert batch with the routing offsets on the device (int64 [E+1]): no host sync.
+    `max_tokens` bounds every expert's token count (rows beyond it are not computed; status bit 2)."""
+    assert A.is_cuda and A.dim() == 2 and A.is_contiguous()
+    assert offsets_dev.is_cuda and offsets_dev.dtype == torch.int64 and offsets_dev.numel() == len(experts) + 1
+    E = len(experts)
+    q0 = experts[0]
+    T = A.shape[0]
+    if out is None:
+        out = torch.empty((T, q0.N), dtype=out_dtype or A.dtype, device=A.device)
+    d = q0.desc
+    ws = workspace(fq_gemm_grouped_workspace_bytes(T, E, d), A.device, stream)
+    fq_gemm_grouped_dev(A, T, offsets_dev, E, d, [q.group for q in experts], [q.codes.data_ptr() for q in experts],
+                        [q.scales.data_ptr() for q in experts], out, max_tokens, ws, status, stream)
     return out
 
 

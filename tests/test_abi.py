@@ -259,3 +259,27 @@ def test_xr_sizes_and_validation(fq):
     st = fq._lib.fq_gemm_allreduce(dummy, 0, 40, ctypes.byref(d), dummy, dummy, 0, ctypes.byref(pt), dummy,
                                    None, 0, None)
     assert st == fq.FQ_ERR_UNSUPPORTED                    # M beyond the decode kernel
+
+
+def test_grouped_dev_validation(fq):
+    """fq_gemm_grouped_dev (device expert offsets, SURVEY §8(b)): argument checks before any launch;
+    T == 0 or a zero token bound launches nothing."""
+    d = fq.make_wdesc(256, 256, 4, 64, fq.FQ_BF16)
+    L = fq._lib
+    E = 2
+    grps = (ctypes.c_int32 * E)(64, 64)
+    ptrs = (ctypes.c_void_p * E)(16, 16)
+    dummy = ctypes.c_void_p(16)
+    ws = ctypes.c_void_p(16)
+    assert L.fq_gemm_grouped_dev(dummy, 0, 8, None, E, ctypes.byref(d), grps, ptrs, ptrs, dummy, 0, 8, None, ws,
+                                 1 << 30, None) == fq.FQ_ERR_INVALID_ARG          # offsets missing
+    bad = (ctypes.c_int32 * E)(64, 48)
+    assert L.fq_gemm_grouped_dev(dummy, 0, 8, dummy, E, ctypes.byref(d), bad, ptrs, ptrs, dummy, 0, 8, None, ws,
+                                 1 << 30, None) == fq.FQ_ERR_SHAPE                # an expert's group
+    assert L.fq_gemm_grouped_dev(dummy, 0, 8, dummy, E, ctypes.byref(d), grps, ptrs, ptrs, dummy, 0, 8, None, None,
+                                 0, None) == fq.FQ_ERR_WORKSPACE                  # decode experts need ws
+    assert L.fq_gemm_grouped_dev(None, 0, 0, dummy, E, ctypes.byref(d), grps, ptrs, ptrs, None, 0, 8, None, None,
+                                 0, None) == fq.FQ_OK                             # T == 0: nothing launched
+    d3 = fq.make_wdesc(256, 256, 3, 64, fq.FQ_BF16)
+    assert L.fq_gemm_grouped_dev(dummy, 0, 8, dummy, E, ctypes.byref(d3), grps, ptrs, ptrs, dummy, 0, 8, None, ws,
+                                 1 << 30, None) == fq.FQ_ERR_UNSUPPORTED
