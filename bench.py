@@ -413,6 +413,10 @@ def main():
     extras = {}
     if rank == 0 and world == 1 and not args.no_extras:
         extras = measure_extras(fq, dev, peaks, args)
+        try:
+            extras.update(hbm_read_probe(dev))
+        except Exception as e:  # nvcc / probe unavailable: the line still prints
+            extras["hbm_read_probe_error"] = str(e)[:200]
 
     line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
@@ -647,6 +651,24 @@ def measure_extras(fq, dev, peaks, args):
                             "frac_hbm": round(wbytes / tt / 1e9 / peaks["hbm_gbs"], 3),
                             "TFLOP_s": round(fl / tt / 1e12, 1)}
         del A
+    # Zipf(1) skewed routing with the same totals (seed 3000): host offsets and the
+    # device-offset call (fq_gemm_grouped_dev, token bound = the largest expert) next to each other
+    from synth import zipf_routing
+    for mbar in (16, 64):
+        off = zipf_routing(E, E * mbar, seed=3000)
+        cnt = np.diff(off)
+        A = gaussian_torch((int(off[-1]), K), 1.0, 3100 + mbar, device=dev)
+        tt = timeit(lambda: fq.gemm_grouped(A, [int(x) for x in off], experts), 5)
+        off_dev = torch.from_numpy(off).to(dev)
+        mx = int(cnt.max())
+        td = timeit(lambda: fq.gemm_grouped_dev(A, off_dev, experts, mx), 5)
+        fl = 2.0 * int(off[-1]) * K * N
+        moe[f"zipf_mean_M_e={mbar}"] = {"M_e_min": int(cnt.min()), "M_e_median": float(np.median(cnt)),
+                                       "M_e_max": mx, "empty_experts": int((cnt == 0).sum()),
+                                       "us": round(tt * 1e6, 1), "TB_s": round(wbytes / tt / 1e12, 3),
+                                       "TFLOP_s": round(fl / tt / 1e12, 1),
+                                       "device_offsets_us": round(td * 1e6, 1)}
+        del A
     out["moe_64x16384x4096_int4_adaptive"] = moe
     del experts
     torch.cuda.empty_cache()
@@ -664,7 +686,115 @@ def measure_extras(fq, dev, peaks, args):
     pm["baseline"] = "torch.matmul fp16 (cuBLAS), L2 flushed per GEMM; geomean of QKV/AttnOut/FFN1/FFN2 speed-ups by rows"
     pm["paper_a100"] = "up to 2.5x (int4, block 64, small row counts; figure data not in the text, P:189/P:308)"
     out["paper_microbench_opt13b_opt30b"] = pm
+    out.update(next_rows_extras(fq, dev, peaks, timeit))
     prefill_extras()
+    out.update(dequant_cublas_extras(fq, dev, peaks, timeit))
+    return out
+
+
+def hbm_read_probe(dev):
+    """Read-only HBM probe in the same run: 16-byte LDG sweep over one OPT-175B
+    FC matrix's worth of codes (302 MB) and over 2 GiB (tools/probe_stream.cu, built on demand)."""
+    import ctypes
+    import subprocess
+    import torch
+    so = os.path.join(ROOT, "tools", "libprobe_stream.so")
+    if not os.path.exists(so):
+        subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-shared", "-Xcompiler",
+                               "-fPIC", "-o", so, os.path.join(ROOT, "tools", "probe_stream.cu")])
+    L = ctypes.CDLL(so)
+    L.probe_ldg.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                            ctypes.c_void_p]
+    st = torch.cuda.current_stream().cuda_stream
+    sink = torch.zeros(4, dtype=torch.int32, device=dev)
+    big = torch.randint(0, 255, (2 * 1024 ** 3,), dtype=torch.uint8, device=dev)
+    res = {}
+    for name, nbytes in (("302MB", 12288 * 49152 // 2), ("2GiB", 2 * 1024 ** 3)):
+        best = []
+        for cps in (2, 4):
+            def fn():
+                L.probe_ldg(ctypes.c_void_p(big.data_ptr()), nbytes, 148 * cps, 512, ctypes.c_void_p(sink.data_ptr()),
+                            ctypes.c_void_p(st))
+            for _ in range(3):
+                fn()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(20):
+                fn()
+            b.record()
+            torch.cuda.synchronize()
+            best.append(nbytes / (a.elapsed_time(b) / 20 / 1e3) / 1e9)
+        res[name] = round(max(best), 1)
+    del big
+    torch.cuda.empty_cache()
+    return {"hbm_read_probe_GB_s": res}
+
+
+def next_rows_extras(fq, dev, peaks, timeit):
+    """SURVEY NEXT-3 / NEXT-4 at OPT-175B shapes: int3 / int2 decode (the canonical bit stream) and
+    the int8-activation x int4-weight path with integer group scales (tcgen05 kind::i8), next to
+    the bf16 path of the same matrices."""
+    import torch
+    from synth import gaussian_torch
+    out = {}
+    for name, (K, N) in (("FC1", FC1), ("FC2", FC2)):
+        W = gaussian_torch((N, K), 0.02, 1001, device=dev)
+        for bits in (3, 2):
+            q = fq.quantize(W, bits, 128)
+            for M in (1, 16):
+                A = gaussian_torch((M, K), 1.0, 7, device=dev)
+                tt = timeit(lambda: fq.gemm(A, q))
+                out[f"decode_int{bits}_{name}_M{M}"] = {"us": round(tt * 1e6, 1), "TB_s": round(q.nbytes / tt / 1e12, 3)}
+            del q
+        qi = fq.quantize_intscale(W, 128)
+        for M in (1, 16, 64, 256, 2048):
+            A = gaussian_torch((M, K), 1.0, 8, device=dev)
+            acts = fq.quantize_acts_i8(A)
+            C = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
+            tg = timeit(lambda: fq.gemm_i8(None, qi, out=C, acts=acts))
+            tq = timeit(lambda: fq.quantize_acts_i8(A))
+            fl = 2.0 * M * K * N
+            ent = {"gemm_us": round(tg * 1e6, 1), "act_quant_us": round(tq * 1e6, 1),
+                   "TB_s": round(qi.nbytes / tg / 1e12, 3), "TOPS": round(fl / tg / 1e12, 1)}
+            if M >= 256:  # int8 dense peak = 2 x the measured bf16 peak (B200_PROFILING.md nominal ratio)
+                ent["frac_int8_peak"] = round(fl / tg / 1e12 / (2 * peaks["bf16_tflops"]), 3)
+            out[f"int8act_int4w_{name}_M{M}"] = ent
+            del A, acts, C
+        del W, qi
+        torch.cuda.empty_cache()
+    return out
+
+
+def dequant_cublas_extras(fq, dev, peaks, timeit):
+    """The naive alternative to the fused kernel at prefill: dequantize the int4
+    codes to a bf16 matrix (torch ops) and call cuBLAS (torch.matmul); times of both steps."""
+    import torch
+    from synth import gaussian_torch
+    out = {}
+    for name, (K, N) in (("FC1", FC1), ("FC2", FC2)):
+        W = gaussian_torch((N, K), 0.02, 1001, device=dev)
+        q = fq.quantize(W, 4, 128)
+        del W
+        A = gaussian_torch((2048, K), 1.0, 8, device=dev)
+
+        def dequant():
+            c = q.codes
+            lo = (c & 0xF).to(torch.int16)
+            hi = (c >> 4).to(torch.int16)
+            qq = torch.stack((lo - ((lo & 8) << 1), hi - ((hi & 8) << 1)), dim=2).view(N, K)
+            return (qq.to(torch.bfloat16).view(N, K // 128, 128) * q.scales.t().unsqueeze(2)).view(N, K)
+
+        Wd = dequant()
+        td = timeit(dequant, 3)
+        tm = timeit(lambda: torch.matmul(A, Wd.t()), 3)
+        tf = timeit(lambda: fq.gemm(A, q), 3)
+        fl = 2.0 * 2048 * K * N
+        out[f"prefill_dequant_cublas_{name}_M2048"] = {
+            "dequant_ms": round(td * 1e3, 3), "matmul_ms": round(tm * 1e3, 3),
+            "total_ms": round((td + tm) * 1e3, 3), "fused_ms": round(tf * 1e3, 3),
+            "fused_TFLOP_s": round(fl / tf / 1e12, 1), "dequant_cublas_TFLOP_s": round(fl / (td + tm) / 1e12, 1)}
+        del A, Wd, q
+        torch.cuda.empty_cache()
     return out
 
 

@@ -457,23 +457,29 @@ fq_status fq_gemm_grouped_dev(const void* A, int32_t adt, int64_t T, const int64
   }
   if (T == 0 || max_tokens == 0) return FQ_OK;  // nothing can be routed: nothing launched
   if (!A || !C) return FQ_ERR_INVALID_ARG;
-  const Tune t{};
-  std::vector<int> small, large;
-  for (int32_t e = 0; e < E; ++e)
-    (!use_tc_path(max_tokens, d->bits, groups_host[e], 0, t) ? small : large).push_back(e);
-  if (!small.empty() && (!ws || ws_bytes < gemv_grouped_workspace_bytes(T, (int)d->K, d->bits)))
-    return FQ_ERR_WORKSPACE;
-  const cudaStream_t st = as_stream(stream);
-  if (!large.empty()) {
-    cudaError_t r = run_gemm_tc_grouped_dev(adt, cdt, d->bits, A, T, (int)d->K, (int)d->N, offsets_dev, groups_host,
-                                            codes_host, scales_host, C, (int)max_tokens, large.data(),
-                                            (int)large.size(), status_dev, st);
-    if (r != cudaSuccess) return FQ_ERR_CUDA;
+  // Every expert's first tokens (up to the decode kernel's maximum) run on the batched decode kernel,
+  // which streams each expert's weights once; when the bound exceeds that, the tcgen05 kernel takes
+  // the remaining tokens of every expert (its tiles beyond an expert's count leave at once), so a
+  // skewed routing does not push the many small experts onto tcgen05 tiles sized for the largest.
+  std::vector<int> all, large, skips;
+  for (int32_t e = 0; e < E; ++e) {
+    all.push_back(e);
+    const int dmax = gemv_max_m(d->bits, groups_host[e]);
+    if (max_tokens > dmax) {
+      large.push_back(e);
+      skips.push_back(dmax);
+    }
   }
-  if (!small.empty())
-    return from_cuda(run_gemv_grouped_dev(adt, cdt, d->bits, A, T, (int)d->K, (int)d->N, offsets_dev, groups_host,
-                                          codes_host, scales_host, C, ws, (int)max_tokens, small.data(),
-                                          (int)small.size(), status_dev, st));
+  if (!ws || ws_bytes < gemv_grouped_workspace_bytes(T, (int)d->K, d->bits)) return FQ_ERR_WORKSPACE;
+  const cudaStream_t st = as_stream(stream);
+  cudaError_t r = run_gemv_grouped_dev(adt, cdt, d->bits, A, T, (int)d->K, (int)d->N, offsets_dev, groups_host,
+                                       codes_host, scales_host, C, ws, (int)max_tokens, all.data(), (int)all.size(),
+                                       status_dev, st);
+  if (r != cudaSuccess) return FQ_ERR_CUDA;
+  if (!large.empty())
+    return from_cuda(run_gemm_tc_grouped_dev(adt, cdt, d->bits, A, T, (int)d->K, (int)d->N, offsets_dev,
+                                             groups_host, codes_host, scales_host, C, (int)max_tokens, large.data(),
+                                             (int)large.size(), skips.data(), status_dev, st));
   return FQ_OK;
 }
 

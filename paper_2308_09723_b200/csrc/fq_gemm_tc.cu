@@ -167,6 +167,7 @@ struct TcProb {
   // whole A / C (the activation map spans all `rows`); M is the launch's token bound.
   const int64_t* offs;
   int e, rows;
+  int skip;          // the expert's first `skip` tokens are served by the decode kernel (device offsets)
   int32_t* status;   // nullable: bit 2 = more tokens than the bound / offsets outside [0, rows]
 };
 // this problem's first row and token count (device offsets clamped to the rows and the bound)
@@ -176,8 +177,8 @@ __device__ __forceinline__ void prob_rows(const TcProb& p, int& row0, int& Me) {
   if (p.offs) {
     const int64_t o0 = p.offs[p.e], o1 = p.offs[p.e + 1];
     const int64_t lo = max((int64_t)0, min(o0, (int64_t)p.rows)), hi = max(lo, min(o1, (int64_t)p.rows));
-    row0 = (int)lo;
-    Me = (int)min(hi - lo, (int64_t)p.M);
+    row0 = (int)lo + p.skip;
+    Me = (int)max((int64_t)0, min(hi - lo - p.skip, (int64_t)p.M));
   }
 }
 // work item -> (token tile, weight-row tile, K-block range); work items of one output tile are
@@ -314,7 +315,10 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
         int row0_, Me_;
         prob_rows(pp, row0_, Me_);
         if (mt_ * pp.bn >= Me_) continue;
-        const uint32_t idesc = idesc_f16<T, BM, 16>() + ((uint32_t)((pp.bn >> 3) - 2) << 17);  // N = bn
+        // N = bn; with device offsets, only the tile's real tokens (rounded up to 16): a partly filled
+        // tile of a small expert costs proportionally less tensor-core time
+        const int nn = pp.offs ? min(pp.bn, (Me_ - mt_ * pp.bn + 15) / 16 * 16) : pp.bn;
+        const uint32_t idesc = idesc_f16<T, BM, 16>() + ((uint32_t)((nn >> 3) - 2) << 17);
         mbar_wait(&acc_empty, acc_ph ^ 1);  // epilogue drained the accumulator
         fence_after();
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -750,14 +754,20 @@ cudaError_t run_gemm_tc(int adt, int cdt, int bits, const void* A, int M, int K,
 cudaError_t run_gemm_tc_grouped_dev(int adt, int cdt, int bits, const void* A, int64_t T, int K, int N,
                                     const int64_t* offs_dev, const int32_t* groups, const void* const* codes,
                                     const void* const* scales, void* C, int Mmax, const int* experts, int nexp,
-                                    int32_t* status, cudaStream_t st) {
+                                    const int* skips, int32_t* status, cudaStream_t st) {
   constexpr int MAXP = 48;
   tc::TcBatch<MAXP> b{};
-  const int bn = tc_bn(Mmax), bk = tc_bk(bn), hm = tc_hm_batch(bn);
+  int mmax = 1;  // one tile geometry for the launch: the largest token range left to this kernel
+  for (int ii = 0; ii < nexp; ++ii) mmax = std::max(mmax, Mmax - skips[ii]);
+  const int bn = tc_bn(mmax), bk = tc_bk(bn), hm = tc_hm_batch(bn);
   for (int ii = 0; ii < nexp; ++ii) {
     const int e = experts[ii];
     tc::TcProb& d = b.p[b.nprob];
-    if (!make_tc_prob(d, bits, A, Mmax, K, N, codes[e], scales[e], groups[e], C, cdt, bk, hm)) return cudaErrorInvalidValue;
+    if (!make_tc_prob(d, bits, A, Mmax - skips[ii], K, N, codes[e], scales[e], groups[e], C, cdt, bk, hm))
+      return cudaErrorInvalidValue;
+    d.skip = skips[ii];
+    d.gm = 1;  // token tiles slowest: an expert's live tiles (its first ones) stay contiguous, so the
+               // persistent CTAs' strided schedule spreads them instead of collecting them on a few
     if (!make_tmap_2d(&d.a, A, 2, (uint64_t)K, (uint64_t)T, (uint64_t)K * 2, tc::BKA, d.bn, 128))  // all T rows
       return cudaErrorInvalidValue;
     d.offs = offs_dev;

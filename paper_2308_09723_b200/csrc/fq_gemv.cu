@@ -111,6 +111,8 @@ struct DecProb {
   const int64_t* offs;
   int e;
   int rows;          // rows of A / C (device offsets are clamped to them)
+  int bound;         // the call's token bound (tokens beyond it: status bit 2)
+  int tskip;         // this launch serves the expert's tokens [tskip, tskip + M)
   int32_t* status;   // nullable: bit 2 = some expert had more tokens than the launch bound / bad offsets
 };
 template <int MAXP>
@@ -391,9 +393,9 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
     const int64_t o0 = p.offs[p.e], o1 = p.offs[p.e + 1];
     // rows outside [0, rows) or beyond the launch's token bound are not computed (status bit 2)
     const int64_t lo = max((int64_t)0, min(o0, (int64_t)p.rows)), hi = max(lo, min(o1, (int64_t)p.rows));
-    row0 = (int)lo;
-    M = (int)min(hi - lo, (int64_t)p.M);
-    if (threadIdx.x == 0 && blockIdx.x == p.cta_begin && p.status && (hi - lo > p.M || lo != o0 || hi != o1))
+    row0 = (int)lo + p.tskip;
+    M = (int)max((int64_t)0, min(hi - lo - p.tskip, (int64_t)p.M));
+    if (threadIdx.x == 0 && blockIdx.x == p.cta_begin && p.status && (hi - lo > p.bound || lo != o0 || hi != o1))
       atomicOr(p.status, 4);
     if (tok0 >= M) return;  // token tile beyond this expert's tokens: the whole CTA leaves
   }
@@ -1295,39 +1297,50 @@ cudaError_t run_gemv_grouped_dev(int adt, int cdt, int bits, const void* A, int6
     cudaError_t r = launch_prep(adt, A, (int)T, K, pre, Sp, st);
     if (r != cudaSuccess) return r;
   }
-  for (int cls = 0; cls < 6; ++cls) {
-    const int mt = 1 << (cls >> 1);
-    const bool sacc = cls & 1;
-    DecBatch<kMaxBatch> b{};
-    int ctas = 0;
-    for (int ii = 0; ii < nexp; ++ii) {
-      const int e = experts[ii];
-      GemvPlan pl = plan_gemv(Mmax, K, N, bits, groups[e], num_sms());
-      pl.splits = 1;
-      pl.klen = ((K + pl.kchunk - 1) / pl.kchunk) * pl.kchunk;
-      if (pl.mt != mt || sacc_of(bits, groups[e]) != sacc) continue;
-      DecProb& d = b.p[b.nprob];
-      const bool nib = nib_of(bits, groups[e]);
-      if (!make_dec_prob(d, pl, bits, cdt, nib ? static_cast<const void*>(pre) : A, (int)T, K, N, codes[e],
-                         scales[e], groups[e], C, ws, nib ? Sp : nullptr, (int)T, 0))
-        return cudaErrorInvalidValue;
-      d.M = Mmax;
-      d.offs = offs_dev;
-      d.e = e;
-      d.rows = (int)T;
-      d.status = status;
-      d.cta_begin = ctas;
-      ctas += d.gx * d.ktiles;
-      if (++b.nprob == kMaxBatch) {
+  // Token segments of every expert: [0, 8) on the one-tile kernel class (most experts of a skewed
+  // routing are small), then [8, min(bound, decode maximum)) on the class its size needs; the
+  // tcgen05 kernel takes whatever exceeds the decode maximum.  A segment's CTAs leave at once when
+  // the expert has no tokens there.
+  for (int seg = 0; seg < 2; ++seg) {
+    for (int cls = 0; cls < 6; ++cls) {
+      const int mt = 1 << (cls >> 1);
+      const bool sacc = cls & 1;
+      DecBatch<kMaxBatch> b{};
+      int ctas = 0;
+      for (int ii = 0; ii < nexp; ++ii) {
+        const int e = experts[ii];
+        const int md = std::min(Mmax, gemv_max_m(bits, groups[e]));
+        const int t0 = seg == 0 ? 0 : 8, t1 = seg == 0 ? std::min(md, 8) : md;
+        if (t1 <= t0) continue;
+        GemvPlan pl = plan_gemv(t1 - t0, K, N, bits, groups[e], num_sms());
+        pl.splits = 1;
+        pl.klen = ((K + pl.kchunk - 1) / pl.kchunk) * pl.kchunk;
+        if (pl.mt != mt || sacc_of(bits, groups[e]) != sacc) continue;
+        DecProb& d = b.p[b.nprob];
+        const bool nib = nib_of(bits, groups[e]);
+        if (!make_dec_prob(d, pl, bits, cdt, nib ? static_cast<const void*>(pre) : A, (int)T, K, N, codes[e],
+                           scales[e], groups[e], C, ws, nib ? Sp : nullptr, (int)T, 0))
+          return cudaErrorInvalidValue;
+        d.M = t1 - t0;
+        d.tskip = t0;
+        d.offs = offs_dev;
+        d.e = e;
+        d.rows = (int)T;
+        d.bound = Mmax;
+        d.status = status;
+        d.cta_begin = ctas;
+        ctas += d.gx * d.ktiles;
+        if (++b.nprob == kMaxBatch) {
+          cudaError_t r = dispatch_dec<kMaxBatch>(adt, bits, mt, sacc, 0, b, ctas, st);
+          if (r != cudaSuccess) return r;
+          b.nprob = 0;
+          ctas = 0;
+        }
+      }
+      if (b.nprob) {
         cudaError_t r = dispatch_dec<kMaxBatch>(adt, bits, mt, sacc, 0, b, ctas, st);
         if (r != cudaSuccess) return r;
-        b.nprob = 0;
-        ctas = 0;
       }
-    }
-    if (b.nprob) {
-      cudaError_t r = dispatch_dec<kMaxBatch>(adt, bits, mt, sacc, 0, b, ctas, st);
-      if (r != cudaSuccess) return r;
     }
   }
   return cudaSuccess;

@@ -79,7 +79,7 @@ cudaError_t run_gemv_grouped_dev(int adt, int cdt, int bits, const void* A, int6
 cudaError_t run_gemm_tc_grouped_dev(int adt, int cdt, int bits, const void* A, int64_t T, int K, int N,
                                     const int64_t* offs_dev, const int32_t* groups, const void* const* codes,
                                     const void* const* scales, void* C, int Mmax, const int* experts, int nexp,
-                                    int32_t* status, cudaStream_t st);
+                                    const int* skips, int32_t* status, cudaStream_t st);
 
 // Large-M tensor-core GEMM (tcgen05 + TMEM, kernel A6).
 // Split-K when the output tiles cannot fill the SMs: workspace = 64 KiB counters (zero-filled once,
