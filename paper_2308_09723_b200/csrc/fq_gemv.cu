@@ -41,7 +41,7 @@ namespace fq {
 #define FQ_DEC_EARLY 1  // consumers release a stage as soon as its data is in registers
 #endif
 #ifndef FQ_DEC_EARLY2
-#define FQ_DEC_EARLY2 0  // two 8-token MMA tiles (9 <= M <= 16): release after the MMAs (measured 8% faster)
+#define FQ_DEC_EARLY2 1  // two 8-token MMA tiles (9 <= M <= 16): release before the MMAs (r02, 96 registers: -2%, profiles/r02/decode_early2_ab.txt)
 #endif
 constexpr int kConsumerWarps = FQ_DEC_CW;
 // TMA warp + consumers (+ one activation-stager warp unless the activations were pre-converted)
