@@ -370,6 +370,65 @@ __global__ void __launch_bounds__(kQThreads) adapt_flags_kernel(const TIn* __res
   if (threadIdx.x == 0 && s_status && status) atomicOr(status, 1);
 }
 
+// Warp-per-column variant (K <= 65536): one warp owns a column and its private shared-memory pyramid,
+// so the levels need only __syncwarp -- the block-wide version's __syncthreads per level and its
+// mostly idle threads at the coarse levels made it issue-bound (13.8 instructions per weight).
+template <typename TIn, int WPC>
+__global__ void __launch_bounds__(32 * WPC) adapt_flags_warp_kernel(const TIn* __restrict__ W, int K, int N, int nlev,
+                                                                     int gfin, uint32_t alpha_milli,
+                                                                     int32_t* __restrict__ flags, int flag_ofs,
+                                                                     float* __restrict__ colmax,
+                                                                     int32_t* __restrict__ status) {
+  extern __shared__ float smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = blockIdx.x * WPC + warp;
+  if (n >= N) return;  // whole warps leave (no block-level barrier below)
+  const int nchunk = K >> 3;
+  const int Gf = K / gfin;
+  float* pm = smem + (size_t)warp * (nchunk + 2 * Gf);  // [nchunk] chunk maxima
+  float* lev = pm + nchunk;                              // levels finest .. 0, packed
+  const TIn* row = W + (size_t)n * K;
+#pragma unroll 8
+  for (int c = lane; c < nchunk; c += 32) {
+    Chunk8<TIn> ch;
+    ch.load(row + (size_t)c * 8);
+    pm[c] = ch.amax();
+  }
+  __syncwarp();
+  const int cpg = gfin >> 3;
+  for (int j = lane; j < Gf; j += 32) {
+    float m = 0.f;
+    for (int i = 0; i < cpg; ++i) m = fmaxf(m, pm[j * cpg + i]);
+    lev[j] = m;
+  }
+  __syncwarp();
+  uint32_t fired = 0;  // bit L: level L fires (some child group below alpha x its parent)
+  int off_child = 0, cnt_child = Gf;
+  for (int L = nlev - 2; L >= 0; --L) {
+    const int off_par = off_child + cnt_child, cnt_par = cnt_child >> 1;
+    bool fire = false;
+    for (int j = lane; j < cnt_par; j += 32) {
+      const float a = lev[off_child + 2 * j], b = lev[off_child + 2 * j + 1];
+      const float pa = fmaxf(a, b);
+      lev[off_par + j] = pa;
+      const double ap = (double)alpha_milli * pa;
+      fire |= (1000.0 * (double)a < ap) | (1000.0 * (double)b < ap);
+    }
+    if (__any_sync(0xffffffffu, fire)) fired |= 1u << (L + 1);
+    __syncwarp();
+    off_child = off_par;
+    cnt_child = cnt_par;
+  }
+  if (lane == 0) {
+    const float top = lev[off_child];  // level 0: max|W[n, :]| (+inf: non-finite)
+    if (colmax) colmax[n] = top;
+    if (!isfinite(top) && status) atomicOr(status, 1);
+    if (flags)
+      for (int L = 1; L < nlev; ++L)
+        if (fired & (1u << L)) atomicOr(&flags[flag_ofs + L - 1], 1);
+  }
+}
+
 // ------------------------------------------------------------------------------------- launchers
 struct AmaxTab {
   const float* tab;
@@ -444,6 +503,18 @@ template <typename TIn>
 static cudaError_t launch_adapt(const void* W, int K, int N, int nlev, int gfin, uint32_t alpha,
                                 int32_t* flags, int flag_ofs, float* colmax, int32_t* status, cudaStream_t st) {
   const int Gf = K / gfin;
+  const size_t per_warp = (size_t)(K / 8 + 2 * Gf) * sizeof(float);
+  // warp-per-column for columns whose pyramid fits 12 KB (K <= ~16384: two 8-warp CTAs per SM);
+  // long columns (e.g. OPT FC2, K = 49152) keep the block-wide kernel, which already streams them
+  // near HBM speed
+  if (per_warp <= 12 * 1024) {
+    auto kw = adapt_flags_warp_kernel<TIn, 8>;
+    cudaError_t e = ensure_smem_attr<adapt_flags_warp_kernel<TIn, 8>>(8 * 12 * 1024);
+    if (e != cudaSuccess) return e;
+    kw<<<(N + 7) / 8, 256, 8 * per_warp, st>>>((const TIn*)W, K, N, nlev, gfin, alpha, flags, flag_ofs, colmax,
+                                               status);
+    return cudaGetLastError();
+  }
   const size_t smem = (size_t)(K / 8 + 2 * Gf) * sizeof(float);
   auto kern = adapt_flags_kernel<TIn>;
   if (smem > 48 * 1024) {  // sized for the largest K the API accepts (2^20, finest group >= 16)
