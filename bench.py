@@ -259,20 +259,20 @@ def main():
     step_bytes_rank = len(M_SWEEP) * (q1.nbytes + q2.nbytes)
     stream = torch.cuda.current_stream()
 
-    def gemm1(M):
-        fq.fq_gemm(xs[M], M, q1.desc, q1.codes, q1.scales, ys[M], ws[(q1.K, M)], stream)
+    def gemm1(M, st=None):
+        fq.fq_gemm(xs[M], M, q1.desc, q1.codes, q1.scales, ys[M], ws[(q1.K, M)], st or stream)
 
-    def gemm2(M):
-        fq.fq_gemm(ys[M], M, q2.desc, q2.codes, q2.scales, zs[M], ws[(q2.K, M)], stream)
+    def gemm2(M, st=None):
+        fq.fq_gemm(ys[M], M, q2.desc, q2.codes, q2.scales, zs[M], ws[(q2.K, M)], st or stream)
 
     def reduce(M):
         if t > 1:
             dist.all_reduce(zs[M], op=dist.ReduceOp.SUM)
 
-    def step():
+    def step(st=None):
         for M in M_SWEEP:
-            gemm1(M)
-            gemm2(M)
+            gemm1(M, st)
+            gemm2(M, st)
             reduce(M)
 
     for _ in range(max(3, args.warmup)):
@@ -331,6 +331,32 @@ def main():
     total_ms = float(tt.item())
     ms_per_step = total_ms / args.steps
     value = step_bytes_total * args.steps / (total_ms / 1e3) / 1e12
+
+    # ---- the same step captured once in a CUDA graph and replayed (the API is graph-safe: no host
+    # sync, self-resetting workspace counters, PDL edges kept): host enqueue cost leaves the step
+    graph_ms = None
+    if world == 1:
+        try:
+            g = torch.cuda.CUDAGraph()
+            cs = torch.cuda.Stream(device=dev)
+            cs.wait_stream(stream)
+            with torch.cuda.stream(cs):
+                step(cs)  # warm the TMA-descriptor cache on the capture stream
+                with torch.cuda.graph(g, stream=cs):
+                    step(cs)
+            stream.wait_stream(cs)
+            for _ in range(3):
+                g.replay()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(args.steps):
+                g.replay()
+            b.record(stream)
+            torch.cuda.synchronize()
+            graph_ms = a.elapsed_time(b) / args.steps
+        except Exception as e:  # report, keep the eager numbers
+            graph_ms = f"capture failed: {str(e)[:120]}"
 
     # ---- e2e through the public API: pinned host x -> device, FC1 -> FC2 (-> all-reduce),
     # result -> pinned host, every step.
@@ -429,6 +455,10 @@ def main():
             "clocks": clocks, "e2e": {"value": round(e2e_value, 4), "unit": UNIT,
                                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": LAUNCHES_PER_GEMM * 2 * len(M_SWEEP) * args.steps, "roofline": roof}
+    if graph_ms is not None:
+        line["cuda_graph_step"] = ({"ms_per_step": round(graph_ms, 4),
+                                    "TB_s": round(step_bytes_total / (graph_ms / 1e3) / 1e12, 4)}
+                                   if isinstance(graph_ms, float) else {"error": graph_ms})
     if tp_layer:
         line["tp_layer"] = tp_layer
     if extras:
