@@ -1,7 +1,9 @@
 """Small invocations of every kernel class, for compute-sanitizer (memcheck / racecheck / synccheck /
 initcheck): quantizer A3 + adaptive A1 (incl. row-shard TP pass), decode A4 (one / two / four
 8-token tiles, nibble, group-split, int8 and per-element-scale paths, split-K), tcgen05 A6 (one- and
-two-half tiles, split-K, 256-token tiles), MoE batch A7.  Checks results are finite."""
+two-half tiles, split-K, 256-token tiles), MoE batch A7 (host and device offsets), and the round-2
+kernels: int3 / int2 decode, the int8-activation path (quantizers + kind::i8 GEMM), the fused
+row-parallel all-reduce.  Checks results are finite."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -53,3 +55,45 @@ for r in range(2):
     q = fq.quantize_rowshard(Wf[:, r * 1024:(r + 1) * 1024].contiguous(), 2048, 2, r, 4, 2048, cm)
 torch.cuda.synchronize()
 print("ok rowshard")
+# ---- round 2 kernels ----------------------------------------------------------------------------
+# int3 / int2 decode (NEXT-3): nibble path and per-element-scale path
+for bits in (3, 2):
+    run(5, 1024, 512, bits, 128)
+    run(3, 1024, 264, bits, 64)
+    run(20, 1024, 512, bits, 128)
+# int8-activation x int4-weight path (NEXT-4): quantizers + the kind::i8 GEMM, every tile width,
+# split-K (few tiles) and a 256-token tile
+Wi = gaussian_torch((384, 2048), 0.02, 6)
+Wi[1, 2] = float("nan")
+st = torch.zeros(1, dtype=torch.int32, device="cuda")
+qi = fq.quantize_intscale(Wi, 64, status=st)
+for M in (1, 33, 200):
+    Ai = gaussian_torch((M, 2048), 1.0, 7)
+    Ci = fq.gemm_i8(Ai, qi)
+    torch.cuda.synchronize()
+    assert torch.isfinite(Ci.float()).all()
+    print(f"ok i8 M={M}", flush=True)
+# device-offset MoE (decode segments + tcgen05 remainder)
+od = torch.tensor([0, 0, 3, 20, 21, 60, 64], dtype=torch.int64, device="cuda")
+C = fq.gemm_grouped_dev(A, od, experts, 40)
+torch.cuda.synchronize()
+assert torch.isfinite(C.float()).all()
+print("ok moe device offsets")
+# fused row-parallel GEMM + one-shot all-reduce (NEXT-1), 4 ranks on one device
+world, M, K, N = 4, 5, 4096, 512
+Wx = gaussian_torch((N, K), 0.02, 8)
+Ax = gaussian_torch((M, K), 1.0, 9)
+Ks = K // world
+qs = [fq.quantize(Wx[:, r * Ks:(r + 1) * Ks].contiguous(), 4, 128) for r in range(world)]
+ranks = fq.xr_group_local(world, M, qs[0].desc, torch.bfloat16)
+d = qs[0].desc
+nb = fq.fq_gemm_workspace_bytes_ex(M, d, fq.make_opts("decode"))
+wss = [torch.zeros(max(nb, 256), dtype=torch.uint8, device="cuda") for _ in range(world)]
+for r, R in enumerate(ranks):
+    fq.fq_gemm_allreduce(Ax[:, r * Ks:(r + 1) * Ks].contiguous(), M, d, qs[r].codes, qs[r].scales, fq.FQ_BF16,
+                         R.peers, R.peers_dev, wss[r])
+for R in ranks:
+    fq.fq_xr_wait(R.peers, M, d)
+torch.cuda.synchronize()
+assert torch.isfinite(ranks[0].out.float()).all()
+print("ok fused all-reduce")
