@@ -717,6 +717,7 @@ def measure_extras(fq, dev, peaks, args):
     pm["paper_a100"] = "up to 2.5x (int4, block 64, small row counts; figure data not in the text, P:189/P:308)"
     out["paper_microbench_opt13b_opt30b"] = pm
     out.update(next_rows_extras(fq, dev, peaks, timeit))
+    out.update(xr_one_gpu_extras(fq, dev, timeit))
     prefill_extras()
     out.update(dequant_cublas_extras(fq, dev, peaks, timeit))
     return out
@@ -793,6 +794,46 @@ def next_rows_extras(fq, dev, peaks, timeit):
         del W, qi
         torch.cuda.empty_cache()
     return out
+
+
+def xr_one_gpu_extras(fq, dev, timeit):
+    """NEXT-1 on one GPU: the fused row-parallel GEMM + one-shot all-reduce with every rank of an
+    8-way group on this device (its pushes are local writes, so no NVLink latency is in these
+    numbers): per-rank time of the OPT-175B FC2 shard GEMM [12288 x 6144] plain vs with the fused
+    epilogue, and the group's completion waits."""
+    import torch
+    from synth import gaussian_torch
+    K, N, world = 49152, 12288, 8
+    Ks = K // world
+    W = gaussian_torch((N, K), 0.02, 1001, device=dev)
+    qs = [fq.quantize(W[:, r * Ks:(r + 1) * Ks].contiguous(), 4, 128) for r in range(world)]
+    del W
+    out = {"world": world, "shard": [N, Ks], "note": "all ranks on one GPU; pushes are local writes"}
+    for M in (1, 16):
+        A = gaussian_torch((M, K), 1.0, 9, device=dev)
+        As = [A[:, r * Ks:(r + 1) * Ks].contiguous() for r in range(world)]
+        d = qs[0].desc
+        ranks = fq.xr_group_local(world, M, d, torch.bfloat16, device=dev)
+        nb = fq.fq_gemm_workspace_bytes_ex(M, d, fq.make_opts("decode"))
+        wss = [torch.zeros(max(nb, 256), dtype=torch.uint8, device=dev) for _ in range(world)]
+        C = torch.empty((M, N), dtype=torch.float32, device=dev)
+
+        def plain():
+            for r in range(world):
+                fq.gemm(As[r], qs[r], out=C, opts=fq.make_opts("decode"))
+
+        def fused():
+            for r, R in enumerate(ranks):
+                fq.fq_gemm_allreduce(As[r], M, d, qs[r].codes, qs[r].scales, fq.FQ_BF16, R.peers, R.peers_dev, wss[r])
+            for R in ranks:
+                fq.fq_xr_wait(R.peers, M, d)
+
+        tp_, tf = timeit(plain, 10), timeit(fused, 10)
+        out[f"M={M}"] = {"plain_gemm_us_per_rank": round(tp_ * 1e6 / world, 2),
+                         "fused_gemm_allreduce_us_per_rank": round(tf * 1e6 / world, 2)}
+        del A, As, ranks, wss
+    torch.cuda.empty_cache()
+    return {"xr_fused_allreduce_one_gpu": out}
 
 
 def dequant_cublas_extras(fq, dev, peaks, timeit):
