@@ -223,6 +223,17 @@ __host__ __device__ constexpr int i8_threads(int dg) { return 32 * (3 + kGroupWa
 #ifndef FQ_I8_DG_SMALL
 #define FQ_I8_DG_SMALL 2  // token tiles <= 32
 #endif
+#ifndef FQ_I8_SMALL_CPS
+#define FQ_I8_SMALL_CPS 2  // CTAs per SM for token tiles <= 32 (measured: FC1 M=1 102 -> 79 us,
+                           // FC2 97 -> 67 us; profiles/r02/i8_two_ctas_per_sm.txt)
+#endif
+#ifndef FQ_I8_MID_CPS
+#define FQ_I8_MID_CPS 2    // CTAs per SM for token tiles of 33..64 (the 64-token variant; measured:
+                           // OPT-175B M=64 114 -> 87 us FC1, 111 -> 84 us FC2)
+#endif
+#ifndef FQ_I8_128_CPS
+#define FQ_I8_128_CPS 2    // CTAs per SM for token tiles of 65..128 (FC2 M=96 117 -> 95 us, M=128 124 -> 104)
+#endif
 #ifndef FQ_I8_DG_LARGE
 #define FQ_I8_DG_LARGE 2  // measured (profiles/r02/i8_dequant_groups.txt): M = 64 -10%, M = 2048 -9%
 #endif
@@ -234,18 +245,22 @@ constexpr int kSmemMax = 227 * 1024 - 2048;
 //     never the tensor core, so few bytes of smem keep many code bytes in flight (decode);
 //   activation ring (AS stages of bn x 128 B int8 activations) + one TMEM A slot (32 columns) per
 //     stage, released by the MMA commit.
-template <int BNMAX>
+// CPS CTAs per SM (2 for decode-sized token tiles: two independent pipelines per SM) split the
+// SM's tensor memory and shared memory.
+template <int BNMAX, int CPS = 1>
 struct Geo {
+  static constexpr int TMEM_COLS = 512 / CPS;
+  static constexpr int SMEM_MAX = (kSmemMax + 2048) / CPS - 2048;
   static constexpr int ACT_STAGE = BNMAX * BK;                 // int8 [bn][128] SW128 (UMMA B)
   static constexpr int CODE_BYTES = BM * BK / 2;               // int4 [128][64 B] SW64
   static constexpr int Z_OFS = CODE_BYTES;                     // z rows [ZROWS][128] after the codes
   static constexpr int CODE_STAGE = CODE_BYTES + ZROWS * BM;   // 8704 (a multiple of 512)
-  static constexpr int AS_TMEM = (512 - BNMAX) / (BK / 4);
-  static constexpr int AS_SMEM = (BNMAX >= 256 ? 160 * 1024 : 96 * 1024) / ACT_STAGE;
+  static constexpr int AS_TMEM = (TMEM_COLS - BNMAX) / (BK / 4);
+  static constexpr int AS_SMEM = (BNMAX >= 256 ? 160 * 1024 : 96 * 1024) / CPS / ACT_STAGE;
   static constexpr int AS0 = AS_TMEM < AS_SMEM ? AS_TMEM : AS_SMEM;
   static constexpr int AS = AS0 > 12 ? 12 : AS0;
   static constexpr int CODE_OFS = AS * ACT_STAGE;
-  static constexpr int CS0 = (kSmemMax - 1024 - CODE_OFS) / CODE_STAGE;
+  static constexpr int CS0 = (SMEM_MAX - 1024 - CODE_OFS) / CODE_STAGE;
   static constexpr int CS = CS0 > 20 ? 20 : CS0;
   static constexpr int SMEM = CODE_OFS + CS * CODE_STAGE + 1024;
   static_assert(AS >= 3 && CS >= 4, "stages");
@@ -308,11 +323,11 @@ __device__ __forceinline__ void i4z_bytes(uint32_t w, uint32_t z, uint32_t cz, u
   o1 = lop3_and_xor(w >> 4, 0x0F0F0F0Fu, 0x08080808u) * z + cz;  // k+1, k+3, k+5, k+7
 }
 
-template <int BNMAX, int DG>
-__global__ void __launch_bounds__(i8_threads(DG), 1) gemm_i8_kernel(const __grid_constant__ I8Prob p) {
+template <int BNMAX, int DG, int CPS>
+__global__ void __launch_bounds__(i8_threads(DG), CPS) gemm_i8_kernel(const __grid_constant__ I8Prob p) {
   constexpr int kDqWarps = kGroupWarps * DG;
   constexpr int kThreads = i8_threads(DG);
-  using Gm = Geo<BNMAX>;
+  using Gm = Geo<BNMAX, CPS>;
   constexpr int CS = Gm::CS, AS = Gm::AS;
   constexpr int kACol = BNMAX;  // A slot a at TMEM columns BNMAX + 32 a
   extern __shared__ __align__(1024) uint8_t dsmem[];
@@ -339,7 +354,7 @@ __global__ void __launch_bounds__(i8_threads(DG), 1) gemm_i8_kernel(const __grid
     mbar_init(&acc_empty, kDqWarps);
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(&tmem_base_sh, 512);
+  if (warp == 1) tmem_alloc(&tmem_base_sh, Gm::TMEM_COLS);
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&p.a);
     prefetch_tmap(&p.q);
@@ -585,7 +600,7 @@ __global__ void __launch_bounds__(i8_threads(DG), 1) gemm_i8_kernel(const __grid
   __syncthreads();
   if (warp == 1) {
     fence_after();
-    tmem_dealloc(tmem, 512);
+    tmem_dealloc(tmem, Gm::TMEM_COLS);
   }
 }
 
@@ -625,7 +640,10 @@ cudaError_t run_quantize_acts_i8(int adt, const void* A, int M, int K, void* Aq,
 }
 
 static int i8_bn(int M) { return std::min(256, (M + 15) / 16 * 16); }
-static int i8_bnmax(int bn) { return bn <= 32 ? 32 : bn <= 128 ? 128 : 256; }
+static int i8_bnmax(int bn) { return bn <= 32 ? 32 : (bn <= 64 && FQ_I8_MID_CPS == 2) ? 64 : bn <= 128 ? 128 : 256; }
+static int i8_cps(int bn) {
+  return bn <= 32 ? FQ_I8_SMALL_CPS : bn <= 64 ? FQ_I8_MID_CPS : bn <= 128 ? FQ_I8_128_CPS : 1;
+}
 constexpr size_t kI8CounterBytes = 65536;
 
 // Split-K plan: persistent CTAs walk the (tile, K range) items; pick the split count (items of
@@ -634,13 +652,14 @@ static int i8_splits(int M, int K, int N, int* kbs_out) {
   const int bn = i8_bn(M);
   const int tiles = ((M + bn - 1) / bn) * ((N + i8::BM - 1) / i8::BM);
   const int kblocks = K / i8::BK;
-  if (tiles >= num_sms()) return (kbs_out ? (*kbs_out = kblocks) : 0), 1;  // the tiles fill the GPU
+  if (tiles >= num_sms() * i8_cps(bn))  // the tiles fill the GPU
+    return (kbs_out ? (*kbs_out = kblocks) : 0), 1;
   const int smax = std::max(1, std::min(8, kblocks / 4));
   int best_s = 1;
   double best = 1e300;
   for (int s = 1; s <= smax; ++s) {
     const int kbs = (kblocks + s - 1) / s, se = (kblocks + kbs - 1) / kbs;
-    const double rounds = (double)tiles * se / num_sms();
+    const double rounds = (double)tiles * se / (num_sms() * i8_cps(bn));
     const double eff = rounds / std::ceil(rounds);
     const double cost = (1.0 + 0.03 * (se - 1)) / eff;
     if (cost < best * 0.999) { best = cost; best_s = se; }
@@ -659,14 +678,14 @@ size_t gemm_i8_workspace_bytes(int M, int K, int N) {
   return kI8CounterBytes + tiles * s * bn * i8::BM * sizeof(int32_t);
 }
 
-template <int BNMAX, int DG>
+template <int BNMAX, int DG, int CPS>
 static cudaError_t launch_i8(const i8::I8Prob& p, cudaStream_t st) {
-  using Gm = i8::Geo<BNMAX>;
-  cudaError_t e = ensure_smem_attr<i8::gemm_i8_kernel<BNMAX, DG>>(Gm::SMEM);
+  using Gm = i8::Geo<BNMAX, CPS>;
+  cudaError_t e = ensure_smem_attr<i8::gemm_i8_kernel<BNMAX, DG, CPS>>(Gm::SMEM);
   if (e != cudaSuccess) return e;
   const int items = p.m_tiles * p.n_tiles * p.splits;
-  return launch_pdl(i8::gemm_i8_kernel<BNMAX, DG>, std::min(items, num_sms()), i8::i8_threads(DG), Gm::SMEM, st,
-                    p);
+  return launch_pdl(i8::gemm_i8_kernel<BNMAX, DG, CPS>, std::min(items, CPS * num_sms()), i8::i8_threads(DG),
+                    Gm::SMEM, st, p);
 }
 
 cudaError_t run_gemm_i8(const void* Aq, const float* sa, const int32_t* rowsum, int M, int K, int N, int group,
@@ -699,9 +718,10 @@ cudaError_t run_gemm_i8(const void* Aq, const float* sa, const int32_t* rowsum, 
     p.ws = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(ws) + kI8CounterBytes);
   }
   switch (i8_bnmax(p.bn)) {
-    case 32: return launch_i8<32, FQ_I8_DG_SMALL>(p, st);
-    case 128: return launch_i8<128, FQ_I8_DG_LARGE>(p, st);
-    default: return launch_i8<256, FQ_I8_DG_LARGE>(p, st);
+    case 32: return launch_i8<32, FQ_I8_SMALL_CPS == 2 ? 1 : FQ_I8_DG_SMALL, FQ_I8_SMALL_CPS>(p, st);
+    case 64: return launch_i8<64, 1, 2>(p, st);
+    case 128: return FQ_I8_128_CPS == 2 ? launch_i8<128, 1, 2>(p, st) : launch_i8<128, FQ_I8_DG_LARGE, 1>(p, st);
+    default: return launch_i8<256, FQ_I8_DG_LARGE, 1>(p, st);
   }
 }
 
