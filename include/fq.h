@@ -158,8 +158,8 @@ fq_status fq_quantize(const void* W, int32_t wdt, const fq_wdesc* d, void* codes
                       int32_t* status_dev, void* stream);
 
 /* ---------------------------------------------------------------------------------------------
- * Fused dequantize + GEMM (kernels A4/A5 for M <= 16, and for 17 <= M <= 32 on the int4 nibble path
- * (group % 128 == 0) when the matrix has >= 148 A6 tiles; A6 otherwise), §4.1:
+ * Fused dequantize + GEMM (kernels A4/A5 for M <= 16, the tcgen05 kernel A6 for larger M;
+ * fq_gemm_opts can force either), §4.1:
  *   C[m,n] = sum_k A[m,k] * q[n,k] * s[k/group, n]
  * A: [M, K] row-major, dtype adt in {BF16, FP16}; the scales must have dtype adt.
  * C: [M, N] row-major, dtype cdt in {adt, FP32} (FP32 is a diagnostic mode).

@@ -70,7 +70,11 @@ static bool use_tc_path(int64_t M, int bits, int group, int64_t N, const Tune& t
   if (t.path == 2) return true;
   const int dmax = gemv_max_m(bits, group);
   if (M > dmax) return true;
-  return M > 16 && N > 0 && tc_short_of_tiles((int)M, (int)N);
+  // single GEMMs of 17..32 tokens: A6 (two CTAs per SM at <= 64-token tiles) beats the decode
+  // kernel's four-token-tile class on every measured shape (profiles/r02/a6_two_ctas_per_sm.txt:
+  // OPT-175B FC1 M=24 151 -> 133 us, OPT-13B FFN1 M=32 59 -> 43 us); MoE experts (N == 0 here)
+  // of <= 32 tokens stay on the batched decode kernel
+  return M > 16 && N > 0;
 }
 
 static int ilog2_exact(int64_t x) {  // log2 of a power of two, else -1

@@ -56,8 +56,13 @@ constexpr int BKA = 64;        // K per activation TMA box (one SWIZZLE_128B ato
 #ifndef FQ_TC_DQW
 #define FQ_TC_DQW 0  // diagnostics: force 8 or 16 for every variant
 #endif
-__host__ __device__ constexpr int dq_warps(int bnmax) { return FQ_TC_DQW ? FQ_TC_DQW : (bnmax == 256 ? 8 : 16); }
-__host__ __device__ constexpr int tc_threads(int bnmax) { return 32 * (2 + dq_warps(bnmax)); }
+#ifndef FQ_TC_CPS_SMALL
+#define FQ_TC_CPS_SMALL 2  // max CTAs per SM of the <= 64-token int4 one-half variants (host rule: tc_use_cps2)
+#endif
+__host__ __device__ constexpr int dq_warps(int bnmax, int cps = 1) {
+  return FQ_TC_DQW ? FQ_TC_DQW : ((bnmax == 256 || cps == 2) ? 8 : 16);
+}
+__host__ __device__ constexpr int tc_threads(int bnmax, int cps = 1) { return 32 * (2 + dq_warps(bnmax, cps)); }
 constexpr int kTmemCols = 512;
 constexpr int kAccCol = 0;                 // accumulator columns [0, BNMAX)
 __host__ __device__ constexpr int sc_rows_max(int bk) { return bk / 16 + 1; }  // >= ceil((bk-1)/g) + 1, g >= 16
@@ -67,7 +72,9 @@ constexpr int kSmemMax = 227 * 1024 - 2048;
 // has small activation tiles, so it keeps many more K blocks (codes) in flight -- at M <= 128 the
 // kernel is bound by HBM latency x bytes in flight, not by the tensor cores.
 //   TMEM: accumulator columns [0, BNMAX), A slot s at BNMAX + 32 s (one per stage).
-template <int BITS, int BNMAX, int BK, int HM>
+// CPS = CTAs per SM: 2 halves each CTA's TMEM (256 columns) and shared memory and uses 8 dequant
+// warps -- two independent pipelines per SM (<= 64-token int4 one-half tiles; see tc_use_cps2).
+template <int BITS, int BNMAX, int BK, int HM, int CPS = 1>
 struct Geo {
   static constexpr int BMT = BM * HM;                         // weight rows per tile
   static constexpr int ACT_BOX = BNMAX * BKA * 2;             // one activation box slot (SW128 atoms)
@@ -80,15 +87,16 @@ struct Geo {
   static constexpr int SC_HALF = SC_ROWS * BM * 2;            // scale rows of one half
   static constexpr int SC_BYTES = SC_HALF * HM;
   static constexpr int STAGE = ((SC_OFS + SC_BYTES + 1023) / 1024) * 1024;
-  static constexpr int S_SMEM = (kSmemMax - 1024) / STAGE;
+  static constexpr int TMEM = kTmemCols / CPS;
+  static constexpr int S_SMEM = ((kSmemMax + 2048) / CPS - 2048 - 1024) / STAGE;
   static constexpr int A_HALF = BK / 2;                       // TMEM columns of one half's A operand
   static constexpr int A_COLS = A_HALF * HM;                  // TMEM columns of one A slot
   static constexpr int ACC_COLS = BNMAX * HM;                 // accumulator columns (half h at h*BNMAX)
-  static constexpr int S_TMEM = (kTmemCols - ACC_COLS) / A_COLS;
+  static constexpr int S_TMEM = (TMEM - ACC_COLS) / A_COLS;
   // One-half tiles of >= 64 tokens: one A slot per smem stage (slot index = stage index).  Two-half
   // tiles and the 32-token variant: more smem stages than TMEM holds A slots, so the A slots form a
   // separate ring behind the stage ring.
-  static constexpr int S0 = (HM == 1 && BNMAX > 32 && S_TMEM < S_SMEM) ? S_TMEM : S_SMEM;
+  static constexpr int S0 = (HM == 1 && BNMAX > 32 && CPS == 1 && S_TMEM < S_SMEM) ? S_TMEM : S_SMEM;
   static constexpr int STAGES = S0 > 16 ? 16 : S0;
   static constexpr int ASLOTS = S_TMEM < STAGES ? S_TMEM : STAGES;
   static constexpr bool SEP_A = ASLOTS < STAGES;
@@ -213,9 +221,10 @@ __device__ __forceinline__ int swz_chunk(int c, int r) {
   return ROWB == 32 ? c ^ ((r >> 2) & 1) : ROWB == 64 ? c ^ ((r >> 1) & 3) : c ^ (r & 7);
 }
 
-template <typename T, int BITS, int MAXP, int BNMAX, int BK, int HM, int DQG>
-__global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __grid_constant__ TcBatch<MAXP> batch) {
-  constexpr int kDqWarps = dq_warps(BNMAX);
+template <typename T, int BITS, int MAXP, int BNMAX, int BK, int HM, int DQG, int CPS>
+__global__ void __launch_bounds__(tc_threads(BNMAX, CPS), CPS)
+    gemm_tc_kernel(const __grid_constant__ TcBatch<MAXP> batch) {
+  constexpr int kDqWarps = dq_warps(BNMAX, CPS);
   constexpr int kParts = kDqWarps / 4;
   // With 16 dequant warps, two groups of 8 take alternate K blocks, so one group's tcgen05.st /
   // wait::st / arrive latency overlaps the other's loads and unpacking (each group covers a whole
@@ -223,7 +232,7 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
   constexpr int kDqGroups = kDqWarps == 16 ? DQG : 1;
   constexpr int kPartsG = kParts / kDqGroups;
   constexpr int kKPW = BK / kPartsG;  // k per dequant thread per K block (16 / 32 / 64)
-  using Gm = Geo<BITS, BNMAX, BK, HM>;
+  using Gm = Geo<BITS, BNMAX, BK, HM, CPS>;
   constexpr int STAGES = Gm::STAGES;
   constexpr int ASLOTS = Gm::ASLOTS;
   constexpr bool kSepA = Gm::SEP_A;  // A slots in their own ring (see Geo)
@@ -251,7 +260,7 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
     mbar_init(&acc_empty, kDqWarps);
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(&tmem_base_sh, kTmemCols);
+  if (warp == 1) tmem_alloc(&tmem_base_sh, Gm::TMEM);
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < batch.nprob; ++i) {
       prefetch_tmap(&batch.p[i].a);
@@ -552,7 +561,7 @@ __global__ void __launch_bounds__(tc_threads(BNMAX), 1) gemm_tc_kernel(const __g
   __syncthreads();
   if (warp == 1) {
     fence_after();
-    tmem_dealloc(tmem, kTmemCols);
+    tmem_dealloc(tmem, Gm::TMEM);
   }
 }
 
@@ -575,16 +584,27 @@ static int tc_bk(int bnmax) { return bnmax > 128 ? 64 : 128; }
 // two-half split plan keeps >= 64 K blocks (8192 k) per item.  Tune::hm = 1 | 2 overrides.
 static int tc_bn(int M);
 static int tc_splits_hm(int M, int K, int N, int bits, int hm, int* kbs_out, int forced_splits);
-static bool tc_hm_ok(int bnmax) { return bnmax <= 128 && tc_bk(bnmax) == 128; }
-static int tc_hm_batch(int bnmax) {  // MoE batch
-  return tc_hm_ok(bnmax) ? 2 : 1;
+static int tc_bnmax(int bn) { return bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : 256; }
+// persistent CTA slots of the variant serving token tiles of bn tokens
+static int tc_slots(int bn, int bits, int hm) { (void)bn; (void)bits; (void)hm; return num_sms(); }
+static bool tc_hm_ok(int bn, int bits) { (void)bits; return bn <= 128 && tc_bk(bn) == 128; }
+// Two CTAs per SM (tc::Geo CPS = 2) for int4 one-half tiles of <= 64 tokens when the tiles fill the
+// GPU without a K split: measured (profiles/r02/a6_two_ctas_per_sm.txt) OPT-175B FC1 M = 48 / 64
+// 179 -> 140 us, OPT-30B QKV 78 -> 59 us, MoE g128 M_e = 64 1184 -> 1011 us; with a K split (few
+// tiles: OPT-13B FFN2) the 16-warp single CTA stays faster.
+static bool tc_use_cps2(int bn, int bits, int hm, long long items) {
+  return FQ_TC_CPS_SMALL == 2 && bn <= 64 && bits == 4 && hm == 1 && items >= num_sms();
+}
+static int tc_hm_batch(int bnmax, int bits) {  // MoE batch: two CTAs per SM beat two halves at <= 64 tokens
+  if (FQ_TC_CPS_SMALL == 2 && bnmax <= 64 && bits == 4) return 1;
+  return tc_hm_ok(bnmax, bits) ? 2 : 1;
 }
 static int tc_hm_gemm(int M, int K, int N, int bits, const Tune& tune) {
   const int bn = tc_bn(M);
-  if (!tc_hm_ok(bn)) return 1;
+  if (!tc_hm_ok(bn, bits)) return 1;
   if (tune.hm == 1 || tune.hm == 2) return tune.hm;
   const long long tiles1 = (long long)((M + bn - 1) / bn) * ((N + tc::BM - 1) / tc::BM);
-  if (tiles1 >= num_sms()) return 1;
+  if (tiles1 >= tc_slots(bn, bits, 1)) return 1;
   int kbs2 = 0;
   tc_splits_hm(M, K, N, bits, 2, &kbs2, 0);
   return kbs2 >= 64 ? 2 : 1;
@@ -632,14 +652,14 @@ static int tc_splits_hm(int M, int K, int N, int bits, int hm, int* kbs_out, int
   if (forced_splits > 0) {
     s = forced_splits;
   } else if (hm == 1) {
-    s = num_sms() / std::max(1, tiles);
+    s = tc_slots(bn, bits, hm) / std::max(1, tiles);
   } else {
     const double code = (double)N * K * bits / 8;
     double best = 1e300;
     s = 1;
     for (int c = 1; c <= std::min(8, smax); ++c) {
       const int kbs = (kblocks + c - 1) / c, ce = (kblocks + kbs - 1) / kbs;
-      const double items = (double)tiles * ce, rounds = items / num_sms();
+      const double items = (double)tiles * ce, rounds = items / tc_slots(bn, bits, hm);
       const double eff = rounds / std::ceil(rounds);
       const double part = ce > 1 ? 2.0 * items * bn * tc::BM * hm * sizeof(float) : 0.0;
       const double cost = (code + part) / eff;
@@ -651,11 +671,6 @@ static int tc_splits_hm(int M, int K, int N, int bits, int hm, int* kbs_out, int
   const int kbs = (kblocks + s - 1) / s;
   if (kbs_out) *kbs_out = kbs;
   return (kblocks + kbs - 1) / kbs;
-}
-// Do the 128-row tiles of a single GEMM leave SMs idle (so A6 splits K to fill them)?
-bool tc_short_of_tiles(int M, int N) {
-  const int bn = tc_bn(M);
-  return (long long)((M + bn - 1) / bn) * ((N + tc::BM - 1) / tc::BM) < num_sms();
 }
 static int tc_splits(int M, int K, int N, int bits, const Tune& tune, int* kbs_out = nullptr) {
   return tc_splits_hm(M, K, N, bits, tc_hm_gemm(M, K, N, bits, tune), kbs_out, tune.splits);
@@ -669,14 +684,14 @@ size_t gemm_tc_workspace_bytes(int M, int K, int N, int bits, const Tune& tune) 
   return kTcCounterBytes + tiles * s * bn * bmt * sizeof(float);
 }
 
-template <typename T, int BITS, int MAXP, int BNMAX, int BK, int HM, int DQG>
+template <typename T, int BITS, int MAXP, int BNMAX, int BK, int HM, int DQG, int CPS = 1>
 static cudaError_t launch_tc(const tc::TcBatch<MAXP>& b, cudaStream_t st) {
-  using Gm = tc::Geo<BITS, BNMAX, BK, HM>;
-  auto kern = tc::gemm_tc_kernel<T, BITS, MAXP, BNMAX, BK, HM, DQG>;
-  cudaError_t e = ensure_smem_attr<tc::gemm_tc_kernel<T, BITS, MAXP, BNMAX, BK, HM, DQG>>(Gm::SMEM);
+  using Gm = tc::Geo<BITS, BNMAX, BK, HM, CPS>;
+  auto kern = tc::gemm_tc_kernel<T, BITS, MAXP, BNMAX, BK, HM, DQG, CPS>;
+  cudaError_t e = ensure_smem_attr<tc::gemm_tc_kernel<T, BITS, MAXP, BNMAX, BK, HM, DQG, CPS>>(Gm::SMEM);
   if (e != cudaSuccess) return e;
-  const int grid = std::min(b.total_tiles, num_sms());
-  kern<<<grid, tc::tc_threads(BNMAX), Gm::SMEM, st>>>(b);
+  const int grid = std::min(b.total_tiles, num_sms() * CPS);
+  kern<<<grid, tc::tc_threads(BNMAX, CPS), Gm::SMEM, st>>>(b);
   return cudaGetLastError();
 }
 
@@ -701,6 +716,15 @@ template <int MAXP>
 static cudaError_t dispatch_tc(int adt, int bits, const tc::TcBatch<MAXP>& b, cudaStream_t st, int forced_dqg = 0) {
   int bn = 0;
   for (int i = 0; i < b.nprob; ++i) bn = std::max(bn, b.p[i].bn);
+  bool split = false;
+  for (int i = 0; i < b.nprob; ++i) split |= b.p[i].splits > 1;
+  if (!split && tc_use_cps2(bn, bits, b.p[0].hm, b.total_tiles) && b.p[0].bk == 128) {  // int4, one-half, <= 64 tokens
+    const bool v32 = bn <= 32;
+    if (adt == FQ_BF16)
+      return v32 ? launch_tc<__nv_bfloat16, 4, MAXP, 32, 128, 1, 1, 2>(b, st)
+                 : launch_tc<__nv_bfloat16, 4, MAXP, 64, 128, 1, 1, 2>(b, st);
+    return v32 ? launch_tc<__half, 4, MAXP, 32, 128, 1, 1, 2>(b, st) : launch_tc<__half, 4, MAXP, 64, 128, 1, 1, 2>(b, st);
+  }
   const int bk = b.p[0].bk, hm = b.p[0].hm;
   for (int i = 1; i < b.nprob; ++i)
     if (b.p[i].bk != bk || b.p[i].hm != hm) return cudaErrorInvalidValue;
@@ -759,7 +783,7 @@ cudaError_t run_gemm_tc_grouped_dev(int adt, int cdt, int bits, const void* A, i
   tc::TcBatch<MAXP> b{};
   int mmax = 1;  // one tile geometry for the launch: the largest token range left to this kernel
   for (int ii = 0; ii < nexp; ++ii) mmax = std::max(mmax, Mmax - skips[ii]);
-  const int bn = tc_bn(mmax), bk = tc_bk(bn), hm = tc_hm_batch(bn);
+  const int bn = tc_bn(mmax), bk = tc_bk(bn), hm = tc_hm_batch(bn, bits);
   for (int ii = 0; ii < nexp; ++ii) {
     const int e = experts[ii];
     tc::TcProb& d = b.p[b.nprob];
@@ -797,7 +821,7 @@ cudaError_t run_gemm_tc_grouped(int adt, int cdt, int bits, const void* A, int K
   int bnmax = 0;  // one stage K for every launch of the call (all chunks fit its variant)
   for (int ii = 0; ii < nexp; ++ii)
     bnmax = std::max(bnmax, tc_bn((int)(offsets[experts[ii] + 1] - offsets[experts[ii]])));
-  const int bk = tc_bk(bnmax), hm = tc_hm_batch(bnmax);
+  const int bk = tc_bk(bnmax), hm = tc_hm_batch(bnmax, bits);
   for (int ii = 0; ii < nexp; ++ii) {
     const int e = experts[ii];
     const int Me = (int)(offsets[e + 1] - offsets[e]);

@@ -85,7 +85,6 @@ cudaError_t run_gemm_tc_grouped_dev(int adt, int cdt, int bits, const void* A, i
 // Split-K when the output tiles cannot fill the SMs: workspace = 64 KiB counters (zero-filled once,
 // self-resetting) + fp32 partials; without it (ws == NULL or too small) the kernel runs unsplit.
 size_t gemm_tc_workspace_bytes(int M, int K, int N, int bits, const Tune& tune);
-bool tc_short_of_tiles(int M, int N);  // A6's 128-row tiles of this GEMM do not fill the SMs
 cudaError_t run_gemm_tc(int adt, int cdt, int bits, const void* A, int M, int K, int N, const void* codes,
                         const void* scales, int group, void* C, void* ws, size_t ws_bytes, cudaStream_t st,
                         const Tune& tune);

@@ -119,8 +119,12 @@ def test_gemm_workspace_sizes(fq):
     pre-converted activations; the tensor-core path adds split-K partials only when its output
     tiles cannot fill the GPU.  Pure host logic (no device calls)."""
     d = fq.make_wdesc(12288, 49152, 4, 128, fq.FQ_BF16)
-    for M in (1, 8, 16, 32):  # decode path (int4 g128 serves M <= 32)
+    for M in (1, 8, 16):  # decode path
         assert fq.fq_gemm_workspace_bytes(M, d) >= 65536 + M * 12288 * 2
+    # 17..32 tokens: the tensor-core path by default (384 tiles, no split), the decode kernel's
+    # four-token-tile class when forced
+    assert fq.fq_gemm_workspace_bytes(32, d) == 256
+    assert fq.fq_gemm_workspace_bytes_ex(32, d, fq.make_opts("decode")) >= 65536 + 32 * 12288 * 2
     big = fq.make_wdesc(12288, 49152, 4, 128, fq.FQ_BF16)
     assert fq.fq_gemm_workspace_bytes(2048, big) == 256           # 384 x 8 tiles fill the GPU: no split
     small = fq.make_wdesc(4096, 512, 4, 128, fq.FQ_BF16)
@@ -139,8 +143,8 @@ def test_gemm_workspace_sizes(fq):
     dec = fq.fq_gemm_workspace_bytes_ex(32, fc2, fq.make_opts("decode"))
     assert forced != dec and fq.fq_gemm_workspace_bytes(32, fc2) == forced
     assert fq.fq_gemm_workspace_bytes_ex(32, fc2, None) == forced
-    # ... while FC1 (384 one-half tiles) keeps 17..32 tokens on the decode kernel
-    assert fq.fq_gemm_workspace_bytes(32, d) >= 65536 + 32 * 12288 * 2
+    # ... and so does FC1 (384 one-half tiles, two CTAs per SM: no split, no partials)
+    assert fq.fq_gemm_workspace_bytes(32, d) == fq.fq_gemm_workspace_bytes_ex(32, d, fq.make_opts("tc")) == 256
 
 
 def test_routing_is_environment_independent(fq, monkeypatch):

@@ -97,3 +97,6 @@ for R in ranks:
 torch.cuda.synchronize()
 assert torch.isfinite(ranks[0].out.float()).all()
 print("ok fused all-reduce")
+# A6 with two CTAs per SM (int4 one-half tiles of <= 64 tokens that fill the GPU without a K split)
+run(40, 1024, 19200, 4, 128)
+run(20, 1024, 19200, 4, 64)
