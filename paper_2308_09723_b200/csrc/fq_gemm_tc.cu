@@ -599,10 +599,26 @@ static int tc_hm_batch(int bnmax, int bits) {  // MoE batch: two CTAs per SM bea
   if (FQ_TC_CPS_SMALL == 2 && bnmax <= 64 && bits == 4) return 1;
   return tc_hm_ok(bnmax, bits) ? 2 : 1;
 }
+// Two CTAs per SM with a K split (one-half tiles that do not fill the GPU): only when every item
+// keeps >= 64 K blocks, so the split fixup stays rare (OPT-175B FC2 M = 64: 141 -> 132 us; short
+// items, e.g. OPT-13B FFN2, lose).  Returns the split count, 0 if the plan does not apply.
+static int tc_cps2_split(int M, int K, int N, int bits, int* kbs_out) {
+  const int bn = tc_bn(M);
+  if (FQ_TC_CPS_SMALL != 2 || bn > 64 || bits != 4) return 0;
+  const int tiles = ((M + bn - 1) / bn) * ((N + tc::BM - 1) / tc::BM);
+  if (tiles >= num_sms()) return 0;  // no split needed: the plain two-CTA rule applies
+  const int kblocks = (K + 127) / 128;
+  const int s = std::max(1, std::min(kblocks, 2 * num_sms() / std::max(1, tiles)));
+  const int kbs = (kblocks + s - 1) / s;
+  if (kbs < 64) return 0;
+  if (kbs_out) *kbs_out = kbs;
+  return (kblocks + kbs - 1) / kbs;
+}
 static int tc_hm_gemm(int M, int K, int N, int bits, const Tune& tune) {
   const int bn = tc_bn(M);
   if (!tc_hm_ok(bn, bits)) return 1;
   if (tune.hm == 1 || tune.hm == 2) return tune.hm;
+  if (tune.splits == 0 && tc_cps2_split(M, K, N, bits, nullptr) > 1) return 1;
   const long long tiles1 = (long long)((M + bn - 1) / bn) * ((N + tc::BM - 1) / tc::BM);
   if (tiles1 >= tc_slots(bn, bits, 1)) return 1;
   int kbs2 = 0;
@@ -673,7 +689,12 @@ static int tc_splits_hm(int M, int K, int N, int bits, int hm, int* kbs_out, int
   return (kblocks + kbs - 1) / kbs;
 }
 static int tc_splits(int M, int K, int N, int bits, const Tune& tune, int* kbs_out = nullptr) {
-  return tc_splits_hm(M, K, N, bits, tc_hm_gemm(M, K, N, bits, tune), kbs_out, tune.splits);
+  const int hm = tc_hm_gemm(M, K, N, bits, tune);
+  if (hm == 1 && tune.splits == 0) {
+    const int s2 = tc_cps2_split(M, K, N, bits, kbs_out);
+    if (s2 > 1) return s2;
+  }
+  return tc_splits_hm(M, K, N, bits, hm, kbs_out, tune.splits);
 }
 size_t gemm_tc_workspace_bytes(int M, int K, int N, int bits, const Tune& tune) {
   const int s = tc_splits(M, K, N, bits, tune);
@@ -716,9 +737,14 @@ template <int MAXP>
 static cudaError_t dispatch_tc(int adt, int bits, const tc::TcBatch<MAXP>& b, cudaStream_t st, int forced_dqg = 0) {
   int bn = 0;
   for (int i = 0; i < b.nprob; ++i) bn = std::max(bn, b.p[i].bn);
-  bool split = false;
-  for (int i = 0; i < b.nprob; ++i) split |= b.p[i].splits > 1;
-  if (!split && tc_use_cps2(bn, bits, b.p[0].hm, b.total_tiles) && b.p[0].bk == 128) {  // int4, one-half, <= 64 tokens
+  bool split = false, short_items = false;
+  for (int i = 0; i < b.nprob; ++i) {
+    split |= b.p[i].splits > 1;
+    short_items |= b.p[i].splits > 1 && b.p[i].kbs < 64;
+  }
+  const bool cps2 = split ? (FQ_TC_CPS_SMALL == 2 && bn <= 64 && bits == 4 && b.p[0].hm == 1 && !short_items)
+                          : tc_use_cps2(bn, bits, b.p[0].hm, b.total_tiles);
+  if (cps2 && b.p[0].bk == 128) {  // int4, one-half, <= 64 tokens
     const bool v32 = bn <= 32;
     if (adt == FQ_BF16)
       return v32 ? launch_tc<__nv_bfloat16, 4, MAXP, 32, 128, 1, 1, 2>(b, st)
