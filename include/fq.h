@@ -145,9 +145,10 @@ fq_status fq_quantize_rowshard(const void* W_shard, int32_t wdt, const fq_wdesc*
                                void* stream);
 
 /* ---------------------------------------------------------------------------------------------
- * Quantize + pack (kernel A3), App. A with groups.  One CTA holds a K-slice
- * of whole groups of one column in registers, so group <= 65536 for 16-bit W and <= 32768 for
- * fp32 W (any K otherwise), else FQ_ERR_SHAPE.
+ * Quantize + pack (kernel A3), App. A with groups.  A CTA streams K-slices
+ * of whole groups of one column (<= 24 KB each) through shared memory; a group longer than that is
+ * held by one CTA in registers, so group <= 65536 for 16-bit W and <= 32768 for fp32 W (any K
+ * otherwise), else FQ_ERR_SHAPE.  W and codes must be 16-byte aligned, else FQ_ERR_INVALID_ARG.
  *   s[j,n] = RNE_scale_dtype( 2 * max_{k in group j} |W[n,k]| / (2^bits - 1) )   (one rounding)
  *   q[n,k] = clamp( round_half_away( W[n,k] / s[k/group, n] ), -2^(bits-1), 2^(bits-1)-1 ),
  *            q = 0 where s == 0.

@@ -27,6 +27,7 @@ int num_sms() {
 
 static bool valid_dtype(int d) { return d == FQ_BF16 || d == FQ_FP16 || d == FQ_FP32; }
 static bool valid_half(int d) { return d == FQ_BF16 || d == FQ_FP16; }
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 static fq_status check_wdesc(const fq_wdesc* d) {
   if (!d) return FQ_ERR_INVALID_ARG;
@@ -203,6 +204,7 @@ fq_status fq_quantize(const void* W, int32_t wdt, const fq_wdesc* d, void* codes
   fq_status s = check_wdesc(d);
   if (s != FQ_OK) return s;
   if (!W || !codes || !scales || !valid_dtype(wdt)) return FQ_ERR_INVALID_ARG;
+  if (!aligned16(W) || !aligned16(codes)) return FQ_ERR_INVALID_ARG;  // 16-byte loads / bulk copies
   // one CTA holds a K-slice of whole groups in registers (slices of <= 12288 elements where the
   // group allows, else one group): group <= 65536 (16-bit W), 32768 (fp32 W)
   if (d->group > (wdt == FQ_FP32 ? 32768 : 65536)) return FQ_ERR_SHAPE;
@@ -216,6 +218,7 @@ fq_status fq_quantize_rowshard(const void* W_shard, int32_t wdt, const fq_wdesc*
   fq_status s = check_wdesc(d);
   if (s != FQ_OK) return s;
   if (!W_shard || !codes || !scales || !valid_dtype(wdt)) return FQ_ERR_INVALID_ARG;
+  if (!aligned16(W_shard) || !aligned16(codes)) return FQ_ERR_INVALID_ARG;
   if (rank < 0 || world <= 0 || rank >= world || world > 64 || ilog2_exact(world) < 0) return FQ_ERR_INVALID_ARG;
   if (d->K % world) return FQ_ERR_SHAPE;
   const int64_t Ks = d->K / world;

@@ -5,18 +5,19 @@
 // activation dtype.  Arithmetic contract (bit-exact with the oracle):
 //   * amax is exact;  s = RNE_dtype((double)(2*amax) / (2^b-1)) — the double quotient can never sit
 //     on a bf16/fp16 tie, so this equals one rounding of the exact rational (R4);
-//   * q = clamp(round_half_away(x / s)): for 16-bit W, x * rcp(s) nudged 2^-15 away from zero and
-//     rounded to nearest (exact: the estimate is within 2^-20 of x / s, off-tie quotients are
-//     >= 2^-14 from a half-integer); fp32 W and tiny scales: IEEE division; clamp to
-//     [-2^(b-1), 2^(b-1)-1].
+//   * q = clamp(round_half_away(x / s)): for 16-bit W under a normal scale, x * rcp(s) nudged 2^-15
+//     away from zero and rounded to nearest (exact: the estimate is within 2^-20 of x / s, off-tie
+//     quotients are >= 2^-14 from a half-integer); fp32 W and subnormal scales: the half-integer
+//     test |x| - (floor(y) + 1/2) s >= 0 evaluated exactly by one fma; clamp to [-2^(b-1), 2^(b-1)-1].
 // A1 follows P:147-149 §3.3 under reading R6: level L fires iff some child group range is below
 // alpha * its parent's range, compared exactly as 1000*child < alpha_milli*parent in fp64.
 //
-// Layout: one CTA per paper column n (= row n of the stored [N, K] matrix), sized so each thread
-// holds <= 8 chunks of 8 elements.  Pass 1 streams the row once from HBM with 16-byte loads, keeps
-// the raw chunks in registers and writes one max|.| per chunk to shared memory; pass 2 reduces
-// chunks to groups and writes the scales; pass 3 turns the register-resident chunks into codes,
-// written coalesced.  HBM traffic = read W once + write codes/scales (the algorithmic minimum).
+// Layout: power-of-two groups of 32 .. 1024 run quantize_warp_kernel -- one warp per 1024-element
+// unit of a column, a group = a run of lanes, no shared memory or block barrier.  Other groups run
+// quantize_kernel: one CTA per K-slice of a column, each thread holding <= 8 chunks of 8 elements
+// in registers; pass 1 writes one max|.| per chunk to shared memory, pass 2 reduces chunks to
+// groups and writes the scales, pass 3 turns the register-resident chunks into codes.  Both read W
+// from HBM once and write codes/scales once (the algorithmic minimum).
 #include <algorithm>
 
 #include "fq_common.cuh"
@@ -32,6 +33,10 @@ struct Chunk8 {
   __device__ __forceinline__ void load(const TIn* p) {
 #pragma unroll
     for (int i = 0; i < NV; ++i) r[i] = __ldg(reinterpret_cast<const uint4*>(p) + i);
+  }
+  __device__ __forceinline__ void lds(uint32_t addr) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) r[i] = lds128(addr + 16 * i);
   }
   __device__ __forceinline__ void decode(float (&v)[8]) const;
   __device__ __forceinline__ float amax() const;
@@ -107,21 +112,135 @@ constexpr int kQThreads = 256;
 constexpr int kQCpt = 8;      // chunks per thread cached in registers by the quantizer
 constexpr int kQSlice = 12288;  // target K-slice per CTA (192 threads at kQCpt = 8)
 
-// int3 / int2 (reading R19): the 8 codes of chunk c (offset-binary u = q + 2^(b-1))
-// as b-bit two's-complement fields of the column's little-endian bit stream, 3 / 2 bytes per chunk.
-template <int BITS>
-__device__ __forceinline__ void store_lowbit(uint8_t* codes, int n, int K, int chunk, const uint32_t (&u)[8]) {
+// Pass 2 of A3 for one group: the scale from the group's max|x| (App. A; R4).  Returns
+// the status bits (1: non-finite weights, 2: scale overflows the scale dtype); s = 0 zeroes the codes.
+template <typename TS, int BITS>
+__device__ __forceinline__ int group_scale(float amax, float& s, TS& s_t) {
+  s = 0.f;
+  if (!isfinite(amax)) {
+    s_t = Dt<TS>::from_f(0.f);
+    return 1;
+  }
+  s_t = Dt<TS>::from_d(2.0 * (double)amax / (double)((1 << BITS) - 1));
+  s = Dt<TS>::to_f(s_t);
+  if (!isfinite(s)) {
+    s = 0.f;
+    s_t = Dt<TS>::from_f(0.f);
+    return 2;
+  }
+  return 0;
+}
+
+// Smallest normal value of the scale dtype: below it the scale carries fewer significant bits, so
+// |x| / s may leave [-2^(b-1) - 1/2, 2^(b-1) + 1/2] and the fast path's one-sided clamp no longer
+// suffices (fp16 scales of groups with amax < ~2^-14 (2^b - 1) / 2).
+template <typename TS>
+__device__ __forceinline__ float scale_min_normal() {
+  return Dt<TS>::id == FQ_FP16 ? 6.103515625e-05f /* 2^-14 */ : 1.17549435e-38f /* 2^-126 */;
+}
+
+// Pass 3 of A3 for one 8-element chunk: the codes of v[0..8) under scale s (rs = rcp(s), 0 when
+// s == 0), packed as stored -- int4: 32 bits (.x), int8: 64 bits, int3: 24 bits, int2: 16 bits.
+// fast: 16-bit W under a normal scale (the caller's per-group choice); else the exact test below.
+template <typename TIn, int BITS>
+__device__ __forceinline__ uint2 pack_chunk(const float (&v)[8], float s, float rs, bool fast) {
+  constexpr int lo = -(1 << (BITS - 1)), hi = (1 << (BITS - 1)) - 1;
+  // offset-binary code u = q + 2^(b-1) in [0, 2^b - 1]; the stored two's complement field is
+  // u ^ 2^(b-1).
+  uint32_t u[8];
+  if (Dt<TIn>::id != FQ_FP32 && fast) {
+    // 16-bit W, signed magic-number rounding: t = fma(x, rcp(s), 1.5 * 2^23 + 2^(b-1)) holds
+    // u' = rn_even(x / s) + 2^(b-1) in its low mantissa bits (the magic is even, the sum stays in
+    // [2^23, 2^24)), so the raw bits ARE 0x4B400000 + u'.  |x| <= amax keeps x / s within
+    // (-2^(b-1) - 1/2, 2^(b-1) + 1/2), so only the top needs a clamp.
+    constexpr float kMagic = 12582912.f + (float)(1 << (BITS - 1));
+    constexpr int32_t kBase = 0x4B400000;
+    int32_t tb[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      // y = x * rcp(s) nudged 2^-15 away from zero: |x * rcp(s) - x / s| <= 8.5 * 2^-23 < 2^-20, and
+      // an off-tie quotient is >= 2^-14 from every half-integer (x, s with <= 11 significant bits),
+      // so the nudge carries exact ties past the half-integer (round half AWAY) and leaves every other
+      // quotient on its side; the magic add then rounds to the nearest integer.  Exhaustively checked
+      // against the exact rational rounding on every finite bf16 pattern (tests/test_gpu_quant.py).
+      const float nudge = __uint_as_float((__float_as_uint(v[i]) & 0x80000000u) | 0x38000000u);  // +-2^-15
+      const float t = fmaf(v[i], rs, nudge) + kMagic;
+      tb[i] = min(__float_as_int(t), kBase + (1 << BITS) - 1);
+    }
+    // pack the raw bit patterns: every field carries kBase, whose packed sum is one constant
+    if (BITS == 4) {
+      uint32_t w = (uint32_t)tb[7];
+#pragma unroll
+      for (int i = 6; i >= 0; --i) w = w * 16u + (uint32_t)tb[i];
+      constexpr uint32_t kBias = (uint32_t)kBase * 0x11111111u;
+      return make_uint2((w - kBias) ^ 0x88888888u, 0u);
+    }
+    if (BITS == 8) {
+      constexpr uint32_t kBias = (uint32_t)kBase * 0x01010101u;
+      uint2 w;
+      w.x = ((uint32_t)tb[3] * 256u + (uint32_t)tb[2]) * 256u * 256u + (uint32_t)tb[1] * 256u + (uint32_t)tb[0];
+      w.y = ((uint32_t)tb[7] * 256u + (uint32_t)tb[6]) * 256u * 256u + (uint32_t)tb[5] * 256u + (uint32_t)tb[4];
+      w.x = (w.x - kBias) ^ 0x80808080u;
+      w.y = (w.y - kBias) ^ 0x80808080u;
+      return w;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) u[i] = (uint32_t)(tb[i] - kBase);
+  } else {
+    // fp32 W (24-bit x: no tie-distance guarantee) and subnormal scales: round_half_away(|x| / s)
+    // decided exactly.  c = floor(y) for an estimate y within 1/2 of |x| / s; |x| / s >= c + 1/2
+    // iff |x| - (c + 1/2) s >= 0, and fma evaluates that difference exactly before its one rounding,
+    // which keeps the sign (its exact value is a multiple of 2^-149, so it never rounds to 0).
+    // Scales below 2^-100 are first rescaled with x by 2^64 (exact) so rcp(s) stays finite.
+    const float k2 = s < 7.88860905e-31f /* 2^-100 */ ? 1.8446744e19f /* 2^64 */ : 1.f;
+    const float ss = s * k2, rr = s == 0.f ? 0.f : __frcp_rn(ss);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float a = fabsf(v[i]) * k2;
+      const float c = floorf(a * rr);
+      float m = fmaf(-(c + 0.5f), ss, a) >= 0.f ? c + 1.f : c;
+      if (s == 0.f) m = 0.f;
+      const bool neg = v[i] < 0.f;
+      m = fminf(m, neg ? (float)-lo : (float)hi);
+      u[i] = (uint32_t)(int)((neg ? -m : m) + (float)-lo);
+    }
+    if (BITS == 4) {
+      uint32_t w = u[7];
+#pragma unroll
+      for (int i = 6; i >= 0; --i) w = w * 16u + u[i];
+      return make_uint2(w ^ 0x88888888u, 0u);
+    }
+    if (BITS == 8) {
+      uint2 w;
+      w.x = ((u[3] * 256u + u[2]) * 256u + u[1]) * 256u + u[0];
+      w.y = ((u[7] * 256u + u[6]) * 256u + u[5]) * 256u + u[4];
+      return make_uint2(w.x ^ 0x80808080u, w.y ^ 0x80808080u);
+    }
+  }
+  // int3 / int2 (reading R19): the chunk's b-bit two's-complement fields of the
+  // column's little-endian bit stream
   uint32_t w = 0;
 #pragma unroll
   for (int i = 0; i < 8; ++i) w |= ((u[i] ^ (1u << (BITS - 1))) & ((1u << BITS) - 1)) << (BITS * i);
-  uint8_t* col = codes + (size_t)n * (K / 8 * BITS);
-  if (BITS == 2) {
-    reinterpret_cast<uint16_t*>(col)[chunk] = (uint16_t)w;
+  return make_uint2(w, 0u);
+}
+
+// Pass 3 of A3 for one chunk, stored as chunk `chunk` of column n's packed codes.
+template <typename TIn, int BITS>
+__device__ __forceinline__ void emit_chunk(const float (&v)[8], float s, float rs, bool fast,
+                                           uint8_t* __restrict__ codes, int n, int K, int chunk) {
+  const uint2 w = pack_chunk<TIn, BITS>(v, s, rs, fast);
+  if (BITS == 4) {
+    reinterpret_cast<uint32_t*>(codes + (size_t)n * (K / 2))[chunk] = w.x;
+  } else if (BITS == 8) {
+    reinterpret_cast<uint2*>(codes + (size_t)n * K)[chunk] = w;
+  } else if (BITS == 2) {
+    reinterpret_cast<uint16_t*>(codes + (size_t)n * (K / 4))[chunk] = (uint16_t)w.x;
   } else {
-    uint8_t* b = col + (size_t)chunk * 3;
-    b[0] = (uint8_t)w;
-    b[1] = (uint8_t)(w >> 8);
-    b[2] = (uint8_t)(w >> 16);
+    uint8_t* b = codes + (size_t)n * (K / 8 * 3) + (size_t)chunk * 3;
+    b[0] = (uint8_t)w.x;
+    b[1] = (uint8_t)(w.x >> 8);
+    b[2] = (uint8_t)(w.x >> 16);
   }
 }
 
@@ -168,21 +287,9 @@ __global__ void __launch_bounds__(sizeof(TIn) == 4 ? 512 : 1024) quantize_kernel
   // pass 2: group maxima -> scales
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   auto finish_group = [&](int j, float amax) {
-    int st = 0;
-    float s = 0.f;
+    float s;
     TS s_t;
-    if (!isfinite(amax)) {
-      st |= 1;
-      s_t = Dt<TS>::from_f(0.f);
-    } else {
-      s_t = Dt<TS>::from_d(2.0 * (double)amax / (double)((1 << BITS) - 1));
-      s = Dt<TS>::to_f(s_t);
-      if (!isfinite(s)) {
-        st |= 2;
-        s = 0.f;
-        s_t = Dt<TS>::from_f(0.f);
-      }
-    }
+    const int st = group_scale<TS, BITS>(amax, s, s_t);
     sc[j] = s;
     sr[j] = s == 0.f ? 0.f : __frcp_rn(s);
     scales[(size_t)(sl * G + j) * N + n] = s_t;
@@ -216,7 +323,6 @@ __global__ void __launch_bounds__(sizeof(TIn) == 4 ? 512 : 1024) quantize_kernel
 
   // pass 3: codes
   const uint32_t cpg_magic = 0xFFFFFFFFu / (uint32_t)cpg + 1u;  // ceil(2^32 / cpg), cpg >= 2
-  constexpr int lo = -(1 << (BITS - 1)), hi = (1 << (BITS - 1)) - 1;
 #pragma unroll
   for (int ci = 0; ci < CPT; ++ci) {
     const int c = threadIdx.x + ci * T;
@@ -224,87 +330,91 @@ __global__ void __launch_bounds__(sizeof(TIn) == 4 ? 512 : 1024) quantize_kernel
     float v[8];
     raw[ci].decode(v);
     const int j = (int)__umulhi((uint32_t)c, cpg_magic);  // c / cpg, exact for c < 2^32 / cpg
-    const float s = sc[j];
-    const float rs = sr[j];  // rcp(s), 0 when s == 0
-    const float hs = 0.5f * s;     // exact
-    // offset-binary code u = q + 2^(b-1) in [0, 2^b - 1]; the stored two's complement field is
-    // u ^ 2^(b-1).
-    if (Dt<TIn>::id != FQ_FP32 && s >= 1e-30f) {
-      // 16-bit W, signed magic-number rounding: t = fma(x, rcp(s), 1.5 * 2^23 + 2^(b-1)) holds
-      // u' = rn_even(x / s) + 2^(b-1) in its low mantissa bits (the magic is even, the sum stays in
-      // [2^23, 2^24)), so the raw bits ARE 0x4B400000 + u'.  rn_even(x * rcp(s)) is the correctly
-      // rounded quotient except possibly at an exact tie |x| = (|m| + 1/2) s, where round-half-away
-      // needs one more step away from zero; the tie is detected exactly because
-      // m s + sign(x) s/2 = fma(m, s, +-s/2) is an exact fp32 value (<= 20 significant bits).
-      // Off-tie quotients are >= 2^-13 (absolute) away from a half-integer (x, s have <= 11
-      // significant bits), far beyond the ~2^-16 error of the estimate.  |x| <= amax
-      // keeps x / s within (-2^(b-1) - 1/2, 2^(b-1) + 1/2), so only the top needs a clamp.
-      constexpr float kMagic = 12582912.f + (float)(1 << (BITS - 1));
-      constexpr int32_t kBase = 0x4B400000;
-      (void)hs;
-      int32_t tb[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        // y = x * rcp(s) nudged 2^-15 away from zero: |x * rcp(s) - x / s| <= 8.5 * 2^-23 < 2^-20, and
-        // an off-tie quotient is >= 2^-14 from every half-integer (x, s with <= 11 significant bits),
-        // so the nudge carries exact ties past the half-integer (round half AWAY) and leaves every other
-        // quotient on its side; the magic add then rounds to the nearest integer.  Exhaustively checked
-        // against the exact rational rounding on every finite bf16 pattern (tests/test_gpu_quant.py).
-        const float nudge = __uint_as_float((__float_as_uint(v[i]) & 0x80000000u) | 0x38000000u);  // +-2^-15
-        const float t = fmaf(v[i], rs, nudge) + kMagic;
-        tb[i] = min(__float_as_int(t), kBase + (1 << BITS) - 1);
-      }
-      // pack the raw bit patterns: every field carries kBase, whose packed sum is one constant
-      if (BITS < 4) {
-        uint32_t u[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) u[i] = (uint32_t)(tb[i] - kBase);
-        store_lowbit<BITS>(codes, n, K, sl * nchunk + c, u);
-      } else if (BITS == 4) {
-        uint32_t w = (uint32_t)tb[7];
-#pragma unroll
-        for (int i = 6; i >= 0; --i) w = w * 16u + (uint32_t)tb[i];
-        constexpr uint32_t kBias = (uint32_t)kBase * 0x11111111u;
-        reinterpret_cast<uint32_t*>(codes + (size_t)n * (K / 2))[sl * nchunk + c] = (w - kBias) ^ 0x88888888u;
-      } else {
-        constexpr uint32_t kBias = (uint32_t)kBase * 0x01010101u;
-        uint2 w;
-        w.x = ((uint32_t)tb[3] * 256u + (uint32_t)tb[2]) * 256u * 256u + (uint32_t)tb[1] * 256u + (uint32_t)tb[0];
-        w.y = ((uint32_t)tb[7] * 256u + (uint32_t)tb[6]) * 256u * 256u + (uint32_t)tb[5] * 256u + (uint32_t)tb[4];
-        w.x = (w.x - kBias) ^ 0x80808080u;
-        w.y = (w.y - kBias) ^ 0x80808080u;
-        reinterpret_cast<uint2*>(codes + (size_t)n * K)[sl * nchunk + c] = w;
-      }
-    } else {
-      // fp32 W (no tie-distance guarantee) and tiny/subnormal scales: IEEE division decides.
-      uint32_t u[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        float m = 0.f;
-        if (s != 0.f) m = fminf(roundf(__fdiv_rn(fabsf(v[i]), s)), 256.f);
-        const bool neg = v[i] < 0.f;
-        m = fminf(m, neg ? (float)-lo : (float)hi);
-        u[i] = (uint32_t)(int)((neg ? -m : m) + (float)-lo);
-      }
-      if (BITS < 4) {
-        store_lowbit<BITS>(codes, n, K, sl * nchunk + c, u);
-      } else if (BITS == 4) {
-        uint32_t w = u[7];
-#pragma unroll
-        for (int i = 6; i >= 0; --i) w = w * 16u + u[i];
-        reinterpret_cast<uint32_t*>(codes + (size_t)n * (K / 2))[sl * nchunk + c] = w ^ 0x88888888u;
-      } else {
-        uint2 w;
-        w.x = ((u[3] * 256u + u[2]) * 256u + u[1]) * 256u + u[0];
-        w.y = ((u[7] * 256u + u[6]) * 256u + u[5]) * 256u + u[4];
-        w.x ^= 0x80808080u;
-        w.y ^= 0x80808080u;
-        reinterpret_cast<uint2*>(codes + (size_t)n * K)[sl * nchunk + c] = w;
-      }
-    }
+    emit_chunk<TIn, BITS>(v, sc[j], sr[j], sc[j] >= scale_min_normal<TS>(), codes, n, K, sl * nchunk + c);
   }
   __syncthreads();
   if (threadIdx.x == 0 && s_status && status) atomicOr(status, s_status);
+}
+
+// A3, one warp per 1024-element unit of a column (the product kernel for power-of-two groups of
+// 32 .. 1024): lane l holds elements [32 l, 32 l + 32) of the unit -- four chunks of ONE group --
+// so a group is a run of group/32 lanes and its max a butterfly of log2(group/32) shuffles.  Every
+// lane then derives its group's scale (the same instructions warp-wide), quantizes its 32 elements
+// from registers and writes them with one (int4) / two (int8) 16-byte stores.  No shared memory and
+// no block barrier: each warp keeps kQwUnits units (kQwUnits x 64 B per lane) of loads in flight.
+// The per-column kernel above serialises load -> reduce -> emit inside each CTA (0.54 of HBM on
+// OPT-175B FC1, profiles/r02/quantize_adapt_ncu.txt).
+constexpr int kQwThreads = 256;
+
+template <typename TIn, typename TS, int BITS>
+__global__ void __launch_bounds__(kQwThreads) quantize_warp_kernel(const TIn* __restrict__ W, int K, int N,
+                                                                   int glog, uint8_t* __restrict__ codes,
+                                                                   TS* __restrict__ scales,
+                                                                   int32_t* __restrict__ status) {
+  constexpr int R = sizeof(TIn) == 4 ? 1 : 2;  // units in flight per warp (64 B of W per lane each)
+  const int lane = threadIdx.x & 31;
+  const int lpg = 1 << (glog - 5);  // lanes per group
+  const int upc = (K + 1023) >> 10;  // units per column (the last may be partial: whole groups)
+  const long units = (long)N * upc;
+  const long nw = (long)gridDim.x * (kQwThreads / 32);
+  int st = 0;
+  for (long u0 = (long)blockIdx.x * (kQwThreads / 32) + (threadIdx.x >> 5); u0 < units; u0 += nw * R) {
+    Chunk8<TIn> raw[R][4];
+    int nn[R], kk[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const long u = u0 + r * nw;
+      nn[r] = (int)(u / upc);
+      kk[r] = (int)(u - (long)nn[r] * upc) * 1024 + lane * 32;
+      if (u < units && kk[r] < K) {
+        const TIn* p = W + (size_t)nn[r] * K + kk[r];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) raw[r][c].load(p + 8 * c);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (u0 + r * nw >= units) break;  // warp-uniform
+      const bool ok = kk[r] < K;        // a group lies wholly inside or outside K
+      float m = 0.f;
+      if (ok) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) m = fmaxf(m, raw[r][c].amax());  // +inf marks a non-finite element
+      }
+      for (int o = 1; o < lpg; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (!ok) continue;
+      float s;
+      TS s_t;
+      st |= group_scale<TS, BITS>(m, s, s_t);
+      const float rs = s == 0.f ? 0.f : __frcp_rn(s);
+      const bool fast = s >= scale_min_normal<TS>();
+      const int n = nn[r], k = kk[r];
+      if ((lane & (lpg - 1)) == 0) scales[(size_t)(k >> glog) * N + n] = s_t;
+      uint2 w[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float v[8];
+        raw[r][c].decode(v);
+        w[c] = pack_chunk<TIn, BITS>(v, s, rs, fast);
+      }
+      if (BITS == 4) {
+        *reinterpret_cast<uint4*>(codes + (size_t)n * (K / 2) + k / 2) = make_uint4(w[0].x, w[1].x, w[2].x, w[3].x);
+      } else if (BITS == 8) {
+        uint4* d = reinterpret_cast<uint4*>(codes + (size_t)n * K + k);
+        d[0] = make_uint4(w[0].x, w[0].y, w[1].x, w[1].y);
+        d[1] = make_uint4(w[2].x, w[2].y, w[3].x, w[3].y);
+      } else if (BITS == 2) {
+        *reinterpret_cast<uint2*>(codes + (size_t)n * (K / 4) + k / 4) =
+            make_uint2(w[0].x | (w[1].x << 16), w[2].x | (w[3].x << 16));
+      } else {  // four 24-bit fields = three words
+        uint32_t* d = reinterpret_cast<uint32_t*>(codes + (size_t)n * (K / 8 * 3) + k / 8 * 3);
+        d[0] = w[0].x | (w[1].x << 24);
+        d[1] = (w[1].x >> 8) | (w[2].x << 16);
+        d[2] = (w[2].x >> 16) | (w[3].x << 8);
+      }
+    }
+  }
+  if (st && status) atomicOr(status, st);
 }
 
 // ------------------------------------------------------------------------------------- A1
@@ -464,8 +574,26 @@ static cudaError_t launch_quant_c(const void* W, int K, int N, int group, void* 
 template <typename TIn, typename TS, int BITS>
 static cudaError_t launch_quant(const void* W, int K, int N, int group, void* codes, void* scales,
                                 int32_t* status, cudaStream_t st, AmaxTab at) {
-  // measured on B200 (OPT FC1/FC2): 8 chunks per thread and 12288-element slices beat 4 chunks
-  // and 4096 / 6144 / 24576-element slices
+#ifndef FQ_QUANT_WARP
+#define FQ_QUANT_WARP 1
+#endif
+  if (FQ_QUANT_WARP && !at.tab && group >= 32 && group <= 1024 && (group & (group - 1)) == 0) {
+    auto kern = quantize_warp_kernel<TIn, TS, BITS>;
+    static int bps = 0;  // resident CTAs per SM (per instantiation)
+    if (!bps) {
+      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kQwThreads, 0);
+      if (e != cudaSuccess) return e;
+      bps = std::max(bps, 1);
+    }
+    const long units = (long)N * ((K + 1023) / 1024);
+    const long grid = std::min<long>((units + kQwThreads / 32 - 1) / (kQwThreads / 32), (long)bps * num_sms());
+    kern<<<(unsigned)grid, kQwThreads, 0, st>>>((const TIn*)W, K, N, __builtin_ctz(group), (uint8_t*)codes,
+                                                (TS*)scales, status);
+    return cudaGetLastError();
+  }
+  // per-column kernel: row-parallel shards of groups spanning several shards (amax table), groups
+  // of 16, above 1024 or not a power of two.  Measured on B200 (OPT FC1/FC2): 8 chunks per thread and
+  // 12288-element slices beat 4 chunks and 4096 / 6144 / 24576-element slices
   return launch_quant_c<TIn, TS, BITS, kQCpt>(W, K, N, group, codes, scales, status, st, kQSlice, at);
 }
 

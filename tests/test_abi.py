@@ -88,6 +88,12 @@ def test_validation_is_synchronous_and_launch_free(fq):
     assert fq._lib.fq_quantize(dummy, 0, ctypes.byref(per_col), dummy, dummy, None, None) == fq.FQ_ERR_SHAPE
     g32k = fq.make_wdesc(65536, 256, 4, 65536, fq.FQ_BF16)
     assert fq._lib.fq_quantize(dummy, fq.FQ_FP32, ctypes.byref(g32k), dummy, dummy, None, None) == fq.FQ_ERR_SHAPE
+    # W and codes feed 16-byte loads / bulk copies: misaligned pointers are refused before any launch
+    odd = ctypes.c_void_p(16 + 8)
+    assert fq._lib.fq_quantize(odd, 0, ctypes.byref(d), dummy, dummy, None, None) == fq.FQ_ERR_INVALID_ARG
+    assert fq._lib.fq_quantize(dummy, 0, ctypes.byref(d), odd, dummy, None, None) == fq.FQ_ERR_INVALID_ARG
+    assert fq._lib.fq_quantize_rowshard(odd, 0, ctypes.byref(d), 2, 0, None, dummy, dummy, None,
+                                        None) == fq.FQ_ERR_INVALID_ARG
 
 
 def test_empty_batches_are_launch_free_noops(fq):

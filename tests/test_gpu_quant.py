@@ -95,19 +95,25 @@ def test_quantize_exact_tiny_config(fq):
     check_exact(fq, W, "bf16", 4, 64, "bf16")
 
 
-def test_quantize_ties_all_bf16_patterns(fq):
-    """Every finite bf16 value appears in a group whose scale is fixed by a planted anchor; codes
-    must match the oracle bit for bit (covers the +-7.5 / 127.5 tie cases)."""
+@pytest.mark.parametrize("wdt", ["bf16", "fp16"])
+@pytest.mark.parametrize("group", [16, 32, 256])
+@pytest.mark.parametrize("order", ["sorted", "shuffled"])
+def test_quantize_all_16bit_patterns(fq, wdt, group, order):
+    """Every finite bf16 / fp16 value, in pattern order (groups of neighbouring magnitudes: the
+    +-7.5 / 127.5 tie cases) and in a seeded shuffle (each value under many unrelated scales); codes
+    and scales must match the oracle bit for bit at every bit width.  group 16 runs the per-column
+    kernel, 32 / 256 the warp-per-unit kernel."""
     allb = np.arange(65536, dtype=np.uint32).astype(np.uint16)
-    vals = O.decode_bits(allb, "bf16")
-    allb = allb[np.isfinite(vals)]
-    K = 256
+    allb = allb[np.isfinite(O.decode_bits(allb, wdt))]
+    if order == "shuffled":
+        allb = np.random.default_rng(group).permutation(allb)
+    K = 1024 + 512  # one full and one partial 1024-element unit per column
     n = ((allb.size + K - 1) // K + 7) // 8 * 8
     buf = np.zeros(n * K, dtype=np.uint16)
     buf[: allb.size] = allb
     W = buf.reshape(n, K)
-    for bits in (4, 8):
-        check_exact(fq, W, "bf16", bits, 32, "bf16")
+    for bits in (4, 8, 3, 2):
+        check_exact(fq, W, wdt, bits, group, wdt)
 
 
 @pytest.mark.parametrize("wdt", ["bf16", "fp16"])
@@ -137,6 +143,55 @@ def test_quantize_exact_ties_both_signs(fq, wdt):
         else:
             bitsW = W.astype(np.float16).view(np.uint16)
         check_exact(fq, bitsW, wdt, bits, group, wdt)
+
+
+@pytest.mark.parametrize("group", [16, 64])
+def test_quantize_fp32_near_ties(fq, group):
+    """fp32 W (24 significant bits) one ulp either side of every half-integer multiple (k + 1/2) s
+    under non-power-of-two scales s: |x| / s sits within ~2^-23 of a tie, so round_half_away must be
+    decided exactly (the oracle divides in float64).  Both kernels: group 16 / 64."""
+    rows = []
+    for bits in (4, 8):
+        qmax = 1 << (bits - 1)
+        for m in (3.0, 5.0, 1.96875 * 64, 1.5 * 128, 127.0):  # bf16-exact scale mantissas
+            s = m * 2.0 ** -12
+            vals = []
+            for k in range(-qmax, qmax):
+                t = np.float32((k + 0.5) * s)
+                vals += [np.nextafter(t, np.float32(np.inf)), np.nextafter(t, np.float32(-np.inf)), t]
+            vals = np.array(vals, dtype=np.float32)
+            K = ((vals.size + group - 2) // (group - 1)) * group
+            K = (K + 1023) // 1024 * 1024
+            row = np.zeros(K, dtype=np.float32)
+            per = group - 1
+            for g0, v0 in zip(range(0, K, group), range(0, vals.size, per)):
+                chunk = vals[v0:v0 + per]
+                row[g0:g0 + chunk.size] = chunk
+                row[g0 + group - 1] = np.float32((qmax - 0.5) * s)  # anchor: amax -> this s
+            rows.append((bits, row))
+    for bits in (4, 8):
+        W = np.stack([r for b, r in rows if b == bits])
+        W = np.concatenate([W, np.zeros(((8 - W.shape[0] % 8) % 8, W.shape[1]), np.float32)])
+        check_exact(fq, W.view(np.uint32), "fp32", bits, group, "bf16")
+
+
+@pytest.mark.parametrize("wdt", ["bf16", "fp16"])
+@pytest.mark.parametrize("group", [16, 64, 1024])
+def test_quantize_subnormal_fp16_scales(fq, wdt, group):
+    """Groups with amax from 1e-9 to 1e-3 under fp16 scales: below amax ~ 2^-14 (2^b - 1) / 2 the
+    scale is an fp16 subnormal with few significant bits, so |x| / s can leave the code range on
+    either side and must be clamped at both ends (and ties still decided exactly)."""
+    rng = np.random.default_rng(group)
+    N, K = 64, 2048
+    amax = 10.0 ** rng.uniform(-9, -3, size=(N, K // group))
+    W = rng.uniform(-1, 1, size=(N, K)) * np.repeat(amax, group, axis=1)
+    if wdt == "bf16":
+        from synth import f32_to_bf16_bits
+        bitsW = f32_to_bf16_bits(W.astype(np.float32))
+    else:
+        bitsW = W.astype(np.float16).view(np.uint16)
+    for bits in (4, 8, 3, 2):
+        check_exact(fq, bitsW, wdt, bits, group, "fp16")
 
 
 def test_zero_and_nonfinite_status(fq):
