@@ -469,6 +469,14 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
       // flight from the previous kernel in the stream).
       const int npre = min(nst, NSTG);
       for (int i = 0; i < npre; ++i) issue_w(i, i);
+#ifndef FQ_DEC_EARLY_TRIGGER
+#define FQ_DEC_EARLY_TRIGGER 1
+#endif
+      // The next kernel in the stream (the next GEMM's prep, which triggers its decode kernel at once)
+      // may launch as soon as every CTA of this grid has started: its CTAs take the SM slots this
+      // grid's early finishers leave and pre-stream their weights; everything they read or write that
+      // this grid touches is ordered behind their griddep_wait.
+      if (FQ_DEC_EARLY_TRIGGER) griddep_launch_dependents();
       griddep_wait();
       for (int i = 0; i < npre; ++i) issue_a(i, i);
       int s = npre % NSTG;
@@ -479,7 +487,7 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
         issue_a(i, s);
         if (++s == NSTG) { s = 0; ph ^= 1; }
       }
-      griddep_launch_dependents();
+      if (!FQ_DEC_EARLY_TRIGGER) griddep_launch_dependents();
     }
     return;
   }
@@ -954,8 +962,19 @@ __global__ void xr_wait_kernel(int32_t* done, int expected) {
 template <typename T, int MODE>
 __global__ void __launch_bounds__(128) prep_acts_kernel(const T* __restrict__ A, int ntok, int K,
                                                         __half* __restrict__ Ap, float* __restrict__ Sp) {
+#ifndef FQ_PREP_EARLY_TRIGGER
+#define FQ_PREP_EARLY_TRIGGER 1
+#endif
+#if FQ_PREP_EARLY_TRIGGER
+  // Trigger first: the decode kernel that follows may launch into SM slots the previous GEMM's tail
+  // leaves free and start streaming its (constant) weights; it reads A' / S' and writes anything only
+  // after its own griddep_wait, i.e. after this grid -- which waits for the previous kernel -- completed.
+  griddep_launch_dependents();
+  griddep_wait();  // A may be the output of the previous kernel in the stream
+#else
   griddep_wait();  // A may be the output of the previous kernel in the stream
   griddep_launch_dependents();
+#endif
   const int chunks = K >> 7;
   const int hw = blockIdx.x * 8 + (threadIdx.x >> 4);
   const int l = threadIdx.x & 15;
