@@ -325,6 +325,19 @@ __device__ __forceinline__ uint4 lowbit_words(uint32_t addr) {
   return make_uint4(x[0], x[1], x[2], x[3]);
 }
 
+#ifdef FQ_DIAG
+// Diagnostics build only: per-CTA timeline of the last decode launch (globaltimer ns):
+// {smid, start, first stage landed, main loop done, exit, producer past griddep_wait} --
+// read with fq_diag_timeline() (tools/dec_timeline.py).
+constexpr int kDiagCtas = 4096;
+__device__ unsigned long long g_diag_tl[kDiagCtas][6];
+__device__ __forceinline__ unsigned long long diag_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define FQ_TL(slot, v) do { if (threadIdx.x == 32 && blockIdx.x < kDiagCtas) g_diag_tl[blockIdx.x][slot] = (v); } while (0)
+#endif
 template <typename T, int BITS, int MT, int SACC, int DBG, int MAXP>
 // Register caps (two CTAs per SM fit up to 112 / 96 registers at 288 / 320 threads), set without
 // ptxas's launch_bounds heuristic.
@@ -376,6 +389,9 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
   uint8_t* sbase = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsmem) + 1023) & ~uintptr_t(1023));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef FQ_DIAG
+  { unsigned sm; asm("mov.u32 %0, %%smid;" : "=r"(sm)); FQ_TL(0, sm); FQ_TL(1, diag_now()); }
+#endif
   int pi = 0;
   while (pi + 1 < batch.nprob && (int)blockIdx.x >= batch.p[pi + 1].cta_begin) ++pi;
   const DecProb& p = batch.p[pi];
@@ -478,6 +494,9 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
       // this grid touches is ordered behind their griddep_wait.
       if (FQ_DEC_EARLY_TRIGGER) griddep_launch_dependents();
       griddep_wait();
+#ifdef FQ_DIAG
+      if (blockIdx.x < kDiagCtas) g_diag_tl[blockIdx.x][5] = diag_now();
+#endif
       for (int i = 0; i < npre; ++i) issue_a(i, i);
       int s = npre % NSTG;
       uint32_t ph = npre == NSTG ? 1u : 0u;
@@ -799,6 +818,9 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
     for (int i = 0; i < nst; ++i) {
       const int k0 = kbeg + i * KS;
       mbar_wait(&full_bar[s], ph);
+#ifdef FQ_DIAG
+      if (i == 0) FQ_TL(2, diag_now());
+#endif
       const uint32_t wst = sb + s * STAGE_BYTES;
       StageOps o;
       load_ops(wst, o);
@@ -810,6 +832,11 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
   }
 
   // ------------------------------------------------------------- epilogue (+ fused A5 fixup)
+#ifdef FQ_DIAG
+  FQ_TL(3, diag_now());
+  FQ_TL(4, 0ull);
+  struct DiagExit { __device__ ~DiagExit() { FQ_TL(4, diag_now()); } } diag_exit;
+#endif
   auto out_idx = [&](int rt, int mt, int i, int& n, int& tok) {
     n = n0 + ((i >> 1) ? Rh[rt] : Rg[rt]);
     tok = tok0 + mt * 8 + 2 * t + (i & 1);
@@ -1030,6 +1057,13 @@ __global__ void __launch_bounds__(128) prep_acts_kernel(const T* __restrict__ A,
 }
 
 // ------------------------------------------------------------------------------------- host side
+#ifdef FQ_DIAG
+extern "C" int fq_diag_timeline(unsigned long long* host, int nctas, int reset) {
+  const int n = nctas < kDiagCtas ? nctas : kDiagCtas;
+  if (reset) return (int)cudaMemcpyToSymbol(g_diag_tl, host, (size_t)n * 6 * sizeof(unsigned long long));
+  return (int)cudaMemcpyFromSymbol(host, g_diag_tl, (size_t)n * 6 * sizeof(unsigned long long));
+}
+#endif
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 constexpr int kMaxCounters = 16384;
 constexpr size_t kCounterBytes = kMaxCounters * sizeof(int);
