@@ -1257,7 +1257,15 @@ cudaError_t run_gemv(const GemvPlan& pl, int adt, int cdt, int bits, const void*
     char* pre = reinterpret_cast<char*>(ws) + kCounterBytes +
                 (pl.splits > 1 ? align256((size_t)pl.splits * M * N * sizeof(float)) : 0);
     char* Sp = pre + align256((size_t)M * K * 2);
+#ifdef FQ_DIAG
+    // diagnostics only (FQ_DEC_NOPREP=1): skip the activation pre-conversion (stale A' / S' -- valid
+    // only when the same activations were converted by an earlier call): the prep kernel's share of
+    // the critical path between back-to-back GEMMs
+    static const bool noprep = std::getenv("FQ_DEC_NOPREP") && std::atoi(std::getenv("FQ_DEC_NOPREP"));
+    cudaError_t r = noprep ? cudaSuccess : launch_prep(adt, A, M, K, pre, Sp, st, sacc_of(bits, group, K) == 2);
+#else
     cudaError_t r = launch_prep(adt, A, M, K, pre, Sp, st, sacc_of(bits, group, K) == 2);
+#endif
     if (r != cudaSuccess) return r;
     if (!make_dec_prob(b.p[0], pl, bits, cdt, pre, M, K, N, codes, scales, group, C, ws, Sp, M, 0,
                        sacc_of(bits, group, K) == 2))
