@@ -70,20 +70,33 @@ struct DecGeom {
 
 // Stage = [packed weights 256 x 64 B][activations MT*8 x KS (TMA, then permuted in place by the
 // stager)][256 scales][per-token activation sums].  As many stages as fit two CTAs per SM.
+// SACC == 3 ("double stage", int4 nibble path, <= 8 tokens, groups % 128 == 0): TWO 128-k chunks per
+// stage -- two code boxes, one activation / sum / scale TMA each covering both chunks -- so the TMA
+// operations, barrier round trips and loop overhead per weight byte halve.  Its stages do not fit
+// the 1024-byte-rounded layout three times, so the code tiles of all stages form one ring (512-byte
+// aligned for SWIZZLE_64B) and the small operands a second one behind it.  Small-operand offsets are
+// relative to the stage's small-operand base: code(s) = s * CS, small(s) = SB + s * SS.
 template <int BITS, int MT, int SACC>
 struct DecStage {
   using G = DecGeom<BITS>;
-  static constexpr int ACT_OFS = stage_w<BITS>();
-  static constexpr int ACT_BYTES = MT * 8 * G::ROWB;
+  static constexpr bool DS = SACC == 3;
+  static constexpr int NCH = DS ? 2 : 1;  // 128-k chunks per stage
+  static constexpr int CODE = stage_w<BITS>() * NCH;
+  static constexpr int ACT_BYTES = MT * 8 * G::ROWB * NCH;
+  static constexpr int SC_BYTES = kRowsPerCta * 2 * (DS ? 2 : (SACC ? SACC : 8));  // scale rows (<= 8)
+  static constexpr int SUM_BYTES = MT * 8 * 16 * NCH;  // per token and chunk: correction, 2^-e (+pad)
+  static constexpr int ACT_OFS = 0;
   static constexpr int SC_OFS = ACT_OFS + ACT_BYTES;  // TMA destinations: 128-byte aligned
-  static constexpr int SC_BYTES = kRowsPerCta * 2 * (SACC ? SACC : 8);  // scale rows per stage (<= 8)
   static constexpr int SUM_OFS = SC_OFS + SC_BYTES;
-  static constexpr int SUM_BYTES = MT * 8 * 16;  // per token: offset correction, inverse scale (+pad)
-  static constexpr int BYTES = ((SUM_OFS + SUM_BYTES + 1023) / 1024) * 1024;
-  static_assert(ACT_OFS % 128 == 0 && SC_OFS % 128 == 0, "TMA smem alignment");
-  static constexpr int kBudget = 115712 - 1024 - 256;  // per CTA at 2 CTAs/SM, minus alignment + static
-  static constexpr int N = kBudget / BYTES < kMaxDecStages ? kBudget / BYTES : kMaxDecStages;
-  static constexpr int SMEM = N * BYTES + 1024;
+  static constexpr int SMALL = SUM_OFS + SUM_BYTES;
+  static_assert(CODE % 512 == 0 && ACT_BYTES % 128 == 0 && SC_BYTES % 128 == 0, "TMA smem alignment");
+  // per CTA at 2 CTAs/SM: 115712 B of static (1024: the barriers, padded by the aligned extern
+  // declaration) + dynamic shared memory
+  static constexpr int PER = DS ? CODE + SMALL : ((CODE + SMALL + 1023) / 1024) * 1024;
+  static constexpr int kBudget = DS ? 115712 - 1024 : 115712 - 1024 - 256;
+  static constexpr int N = kBudget / PER < kMaxDecStages ? kBudget / PER : kMaxDecStages;
+  static constexpr int CS = DS ? CODE : PER, SS = DS ? SMALL : PER, SB = DS ? N * CODE : CODE;
+  static constexpr int SMEM = DS ? N * PER : N * PER + 1024;
 };
 
 // One decode problem (a matrix, its activation slice and output slice) of a batch.  A single
@@ -364,12 +377,15 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
   constexpr int ROWB = G::ROWB;
   constexpr int NSTG = SG::N;
   constexpr int ACT_OFS = SG::ACT_OFS, SUM_OFS = SG::SUM_OFS, SC_OFS = SG::SC_OFS;
-  constexpr int STAGE_BYTES = SG::BYTES;
+  constexpr bool DS = SG::DS;
+  constexpr int KSS = KS * SG::NCH;  // K per stage
+  constexpr int CS = SG::CS, SS = SG::SS, SB = SG::SB;  // code(s) = s * CS, small operands: SB + s * SS
   constexpr int SC_BYTES = SG::SC_BYTES;
   constexpr int RAW_BYTES = SG::ACT_BYTES;
   // Nibble path: activations were pre-converted by prep_acts_kernel (fp16, fragment order) and
   // arrive by TMA with their per-chunk {correction, 2^-e}; there is no stager warp.
   constexpr bool NIB = FQ_NIB && BITS <= 4 && SACC;
+  static_assert(!DS || (NIB && BITS == 4 && MT == 1), "double stages: int4 nibble path, <= 8 tokens");
   // GS = 2 (int4, group 64, nibble path): each thread's four 8-code words come from the four 32-k
   // blocks of the stage (4 x LDS.32 instead of one LDS.128), so the MMAs of words 0-1 and 2-3 cover
   // the two 64-k groups separately; two exact partials per stage, folded with their own scales.
@@ -387,6 +403,7 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
   __shared__ __align__(8) uint64_t full_bar[kMaxDecStages], empty_bar[kMaxDecStages], raw_bar[kMaxDecStages];
   __shared__ int s_last;
   uint8_t* sbase = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsmem) + 1023) & ~uintptr_t(1023));
+  if (DS && sbase != dsmem) __trap();  // exact-size layout: the dynamic base must be 1024-byte aligned
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef FQ_DIAG
@@ -401,7 +418,7 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
   const int n0 = bx * kRowsPerCta;
   const int kbeg = by * p.klen;
   const int kend = min(K, kbeg + p.klen);
-  const int nst = (kend - kbeg + KS - 1) / KS;
+  const int nst = (kend - kbeg + KSS - 1) / KSS;
   const int tok0 = bz * MT * 8;
   int M = p.M, row0 = 0;  // row0: first row of this problem in A / A' / C (device offsets only)
   if (p.offs) {
@@ -442,36 +459,44 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
       const int gm = SACC == 1 ? p.group / KCH : 1;
       int grem = SACC == 1 ? (kbeg / KCH) % gm : 0, gj = SACC == 1 ? (kbeg / KCH) / gm : 0;
       auto issue_w = [&](int i, int s) {  // the stage's packed weights + scales (+ expect_tx)
-        uint8_t* st = sbase + s * STAGE_BYTES;
-        const int k0 = kbeg + i * KS;
-        const int scb = SACC ? SACC * kRowsPerCta * 2 : p.sc_rows * kRowsPerCta * 2;
+        uint8_t* st = sbase + s * CS;
+        uint8_t* xs = sbase + SB + s * SS;
+        const int k0 = kbeg + i * KSS;
+        const int scb = DS ? SG::SC_BYTES : SACC ? SACC * kRowsPerCta * 2 : p.sc_rows * kRowsPerCta * 2;
         if (DBG == 4) {  // diagnostics: codes only
           mbar_arrive_expect_tx(&full_bar[s], stage_w<BITS>());
           tma_load_2d(st, &p.w, &full_bar[s], k0 * BITS / 8, n0, polw);
           return;
         }
-        mbar_arrive_expect_tx(&full_bar[s], stage_w<BITS>() + scb + (NIB ? RAW_BYTES + MT * 8 * 16 : 0));
+        mbar_arrive_expect_tx(&full_bar[s], SG::CODE + scb + (NIB ? SG::ACT_BYTES + SG::SUM_BYTES : 0));
 #pragma unroll
-        for (int bx2 = 0; bx2 < kWBoxes; ++bx2)
-          tma_load_2d(st + bx2 * kWBoxRows * wb_row(BITS), &p.w, &full_bar[s], k0 * BITS / 8,
-                      n0 + bx2 * kWBoxRows, polw);
-        if (SACC) {
+        for (int ch = 0; ch < SG::NCH; ++ch)
 #pragma unroll
           for (int bx2 = 0; bx2 < kWBoxes; ++bx2)
-            tma_load_2d(st + SC_OFS + bx2 * kWBoxRows * 2, &p.s, &full_bar[s], n0 + bx2 * kWBoxRows,
+            tma_load_2d(st + ch * stage_w<BITS>() + bx2 * kWBoxRows * wb_row(BITS), &p.w, &full_bar[s],
+                        (k0 + ch * KS) * BITS / 8, n0 + bx2 * kWBoxRows, polw);
+        if (DS) {  // scale rows k0 / g and the next (box of 2): chunk 1 uses the second iff it starts a group
+#pragma unroll
+          for (int bx2 = 0; bx2 < kWBoxes; ++bx2)
+            tma_load_2d(xs + SC_OFS + bx2 * kWBoxRows * 2, &p.s, &full_bar[s], n0 + bx2 * kWBoxRows,
+                        k0 / p.group, polw);
+        } else if (SACC) {
+#pragma unroll
+          for (int bx2 = 0; bx2 < kWBoxes; ++bx2)
+            tma_load_2d(xs + SC_OFS + bx2 * kWBoxRows * 2, &p.s, &full_bar[s], n0 + bx2 * kWBoxRows,
                         GS == 2 ? (k0 >> 6) : gj, polw);  // GS: the stage's two 64-k rows (box of 2)
           if (++grem == gm) { grem = 0; ++gj; }
         } else if (p.sc_rows) {
 #pragma unroll
           for (int bx2 = 0; bx2 < kWBoxes; ++bx2)
-            tma_load_2d(st + SC_OFS + bx2 * kWBoxRows * 2, &p.s, &full_bar[s], n0 + bx2 * kWBoxRows,
+            tma_load_2d(xs + SC_OFS + bx2 * kWBoxRows * 2, &p.s, &full_bar[s], n0 + bx2 * kWBoxRows,
                         k0 >> p.sc_shift, polw);
         }
       };
       auto issue_a = [&](int i, int s) {  // the stage's activations (+ per-chunk sums)
         if (DBG == 4) return;
-        uint8_t* st = sbase + s * STAGE_BYTES;
-        const int k0 = kbeg + i * KS;
+        uint8_t* st = sbase + SB + s * SS;  // the stage's small operands
+        const int k0 = kbeg + i * KSS;
         if (NIB) {
           tma_load_2d(st + ACT_OFS, &p.a, &full_bar[s], k0, row0 + tok0, pola);
           tma_load_2d(st + SUM_OFS, &p.sm, &full_bar[s], (row0 + tok0) * 4, k0 / KCH, pola);
@@ -526,7 +551,7 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
     uint32_t ph = 0;
     for (int i = 0; i < nst; ++i) {
       mbar_wait(&raw_bar[s], ph);
-      uint8_t* st = sbase + s * STAGE_BYTES;
+      uint8_t* st = sbase + SB + s * SS;  // the stage's small operands
       const uint32_t stu = smem_u32(st);
       uint4 vj[NPW];
 #pragma unroll
@@ -599,7 +624,7 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
   for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
     for (int w16 = 0; w16 < PIECES; ++w16)
-      aofs[mt][w16] = ACT_OFS + (mt * 8 + gq) * ROWB +
+      aofs[mt][w16] = ACT_OFS + (mt * 8 + gq) * ROWB * SG::NCH +
                       (((w16 * 4 + t) ^ (((NIB ? tok_base + tok0 + gq : gq) & 1) << 2)) << 4);
   const uint32_t saofs = NIB ? SUM_OFS + 2 * t * 16 : SUM_OFS + 2 * t * 4;
   float acc[2][MT][4];
@@ -619,14 +644,16 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
     uint4 wgv[2], whv[2];             // code words of rows g / h of both row tiles
     uint32_t scg[2][4], sch[2][4];    // per-element-scale path: splatted scale words
   };
-  auto load_ops = [&](uint32_t wst, StageOps& o) {
+  // wst: the chunk's codes; xst: the stage's small operands; DS chunk 1: ach / sch = activation / sum
+  // offsets of the chunk, srow = byte offset of its scale row
+  auto load_ops = [&](uint32_t wst, uint32_t xst, StageOps& o, int ach = 0, int sch = 0, int srow = 0) {
     if (SACC) {
 #pragma unroll
       for (int rt = 0; rt < 2; ++rt)
 #pragma unroll
         for (int gi = 0; gi < GS; ++gi) {
-          o.sg[rt][gi] = lds_scale<T>(wst + SC_OFS + gi * kRowsPerCta * 2 + Rg[rt] * 2);
-          o.sh[rt][gi] = lds_scale<T>(wst + SC_OFS + gi * kRowsPerCta * 2 + Rh[rt] * 2);
+          o.sg[rt][gi] = lds_scale<T>(xst + SC_OFS + srow + gi * kRowsPerCta * 2 + Rg[rt] * 2);
+          o.sh[rt][gi] = lds_scale<T>(xst + SC_OFS + srow + gi * kRowsPerCta * 2 + Rh[rt] * 2);
         }
     }
     if (DBG == 3 || DBG == 4) return;
@@ -634,17 +661,17 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
 #pragma unroll
       for (int mt = 0; mt < (LAZY ? 1 : MT); ++mt)
 #pragma unroll
-        for (int w16 = 0; w16 < PIECES; ++w16) o.b[mt][w16] = lds128(wst + aofs[mt][w16]);
+        for (int w16 = 0; w16 < PIECES; ++w16) o.b[mt][w16] = lds128(xst + ach + aofs[mt][w16]);
     }
     if (NIB) {  // {corr, 2^-e, corr_lo, corr_hi} of tokens 2t and 2t+1 (lo / hi: the 64-k halves)
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
         if (GS == 1) {
-          const float2 x0 = lds64f(wst + saofs + mt * 128), x1 = lds64f(wst + saofs + mt * 128 + 16);
+          const float2 x0 = lds64f(xst + sch + saofs + mt * 128), x1 = lds64f(xst + sch + saofs + mt * 128 + 16);
           o.sa[mt][0] = make_float2(x0.x, x1.x);
           o.iv[mt] = make_float2(x0.y, x1.y);
         } else {
-          const uint4 x0 = lds128(wst + saofs + mt * 128), x1 = lds128(wst + saofs + mt * 128 + 16);
+          const uint4 x0 = lds128(xst + sch + saofs + mt * 128), x1 = lds128(xst + sch + saofs + mt * 128 + 16);
           o.sa[mt][0] = make_float2(__uint_as_float(x0.z), __uint_as_float(x1.z));
           o.sa[mt][GS - 1] = make_float2(__uint_as_float(x0.w), __uint_as_float(x1.w));
           o.iv[mt] = make_float2(__uint_as_float(x0.y), __uint_as_float(x1.y));
@@ -652,7 +679,7 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
       }
     } else if (OFF != 0.f) {
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) o.sa[mt][0] = lds64f(wst + saofs + mt * 32);
+      for (int mt = 0; mt < MT; ++mt) o.sa[mt][0] = lds64f(xst + sch + saofs + mt * 32);
     }
 #pragma unroll
     for (int rt = 0; rt < 2; ++rt) {
@@ -678,7 +705,7 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
     if (!SACC && p.sc_rows) {
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
-        const uint32_t so = wst + SC_OFS + (((t * SEG + w * (SEG / 4)) >> p.sc_shift) * kRowsPerCta) * 2;
+        const uint32_t so = xst + SC_OFS + (((t * SEG + w * (SEG / 4)) >> p.sc_shift) * kRowsPerCta) * 2;
 #pragma unroll
         for (int rt = 0; rt < 2; ++rt) {
           const uint32_t vg = lds_u16(so + Rg[rt] * 2), vh = lds_u16(so + Rh[rt] * 2);
@@ -688,7 +715,7 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
       }
     }
   };
-  auto compute = [&](const StageOps& o, uint32_t wst, int k0) {
+  auto compute = [&](const StageOps& o, uint32_t xst, int k0) {
     if (DBG == 3 || DBG == 4) return;
 #pragma unroll
     for (int rt = 0; rt < 2; ++rt) {
@@ -746,7 +773,7 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
             const uint32_t a[4] = {qg[2 * pp], qh[2 * pp], qg[2 * pp + 1], qh[2 * pp + 1]};
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt) {
-              const uint4 bw = LAZY ? lds128(wst + aofs[mt][w]) : o.b[LAZY ? 0 : mt][w];
+              const uint4 bw = LAZY ? lds128(xst + aofs[mt][w]) : o.b[LAZY ? 0 : mt][w];
               const uint32_t b0 = pp ? bw.z : bw.x;
               const uint32_t b1 = pp ? bw.w : bw.y;
               if (DBG == 1) {
@@ -773,7 +800,7 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
           const uint32_t a[4] = {qg[0], qh[0], qg[1], qh[1]};
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt) {
-            const uint4 bb = LAZY ? lds128(wst + aofs[mt][w >> 1]) : o.b[LAZY ? 0 : mt][w >> 1];
+            const uint4 bb = LAZY ? lds128(xst + aofs[mt][w >> 1]) : o.b[LAZY ? 0 : mt][w >> 1];
             mma16816<T>(dst[mt], a, (w & 1) ? bb.z : bb.x, (w & 1) ? bb.w : bb.y);
           }
         }
@@ -814,18 +841,41 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
   // is computed -- was measured 40% slower on OPT-175B FC1/FC2 at M <= 8: profiles/r02/decode_pf_rejected.txt.)
   int s = 0;
   uint32_t ph = 0;
-  {
+  // DS: chunk 1 of a stage uses the second staged scale row iff it starts a new group (groups % 128)
+  const int gch = DS ? p.group / KCH : 1;
+  int gpos = DS ? (kbeg / KCH) % gch : 0;  // position of the stage's chunk 0 inside its group
+  if (DS) {
+    for (int i = 0; i < nst; ++i) {
+      const int k0 = kbeg + i * KSS;
+      mbar_wait(&full_bar[s], ph);
+#ifdef FQ_DIAG
+      if (i == 0) FQ_TL(2, diag_now());
+#endif
+      const uint32_t wst = sb + s * CS, xst = sb + SB + s * SS;
+      const int r1 = gpos + 1 == gch ? kRowsPerCta * 2 : 0;
+      gpos += 2;
+      if (gpos >= gch) gpos -= gch;
+      if (gpos >= gch) gpos -= gch;
+      StageOps o;
+      load_ops(wst, xst, o);
+      compute(o, xst, k0);
+      load_ops(wst + stage_w<BITS>(), xst, o, ROWB, MT * 8 * 16, r1);
+      release(s);  // the stage's operands are in registers
+      compute(o, xst, k0 + KS);
+      if (++s == NSTG) { s = 0; ph ^= 1; }
+    }
+  } else {
     for (int i = 0; i < nst; ++i) {
       const int k0 = kbeg + i * KS;
       mbar_wait(&full_bar[s], ph);
 #ifdef FQ_DIAG
       if (i == 0) FQ_TL(2, diag_now());
 #endif
-      const uint32_t wst = sb + s * STAGE_BYTES;
+      const uint32_t wst = sb + s * CS, xst = sb + SB + s * SS;
       StageOps o;
-      load_ops(wst, o);
+      load_ops(wst, xst, o);
       if (EARLY && DBG != 3 && DBG != 4) release(s);  // everything is in registers: hand the slot back
-      compute(o, wst, k0);
+      compute(o, xst, k0);
       if (!EARLY || DBG == 3 || DBG == 4) release(s);
       if (++s == NSTG) { s = 0; ph ^= 1; }
     }
@@ -1175,6 +1225,7 @@ static cudaError_t dispatch_dec(int adt, int bits, int mt, int sacc, int dbg, co
   if (bits == BB && mt == MM && sacc == SS) return launch_dec<TT, BB, MM, SS, 0, MAXP>(b, ctas, st);
   if (adt == FQ_BF16) {
     FQ_DEC_CASE(__nv_bfloat16, 4, 1, 1) FQ_DEC_CASE(__nv_bfloat16, 4, 1, 0)
+    if constexpr (MAXP == 1) { FQ_DEC_CASE(__nv_bfloat16, 4, 1, 3) }
     FQ_DEC_CASE(__nv_bfloat16, 4, 2, 1) FQ_DEC_CASE(__nv_bfloat16, 4, 2, 0)
     FQ_DEC_CASE(__nv_bfloat16, 4, 4, 1)
     FQ_DEC_CASE(__nv_bfloat16, 4, 1, 2) FQ_DEC_CASE(__nv_bfloat16, 4, 2, 2)
@@ -1186,6 +1237,7 @@ static cudaError_t dispatch_dec(int adt, int bits, int mt, int sacc, int dbg, co
     FQ_DEC_CASE(__nv_bfloat16, 2, 2, 1) FQ_DEC_CASE(__nv_bfloat16, 2, 2, 0) FQ_DEC_CASE(__nv_bfloat16, 2, 4, 1)
   } else {
     FQ_DEC_CASE(__half, 4, 1, 1) FQ_DEC_CASE(__half, 4, 1, 0)
+    if constexpr (MAXP == 1) { FQ_DEC_CASE(__half, 4, 1, 3) }
     FQ_DEC_CASE(__half, 4, 2, 1) FQ_DEC_CASE(__half, 4, 2, 0)
     FQ_DEC_CASE(__half, 4, 4, 1)
     FQ_DEC_CASE(__half, 4, 1, 2) FQ_DEC_CASE(__half, 4, 2, 2)
@@ -1206,16 +1258,18 @@ static cudaError_t dispatch_dec(int adt, int bits, int mt, int sacc, int dbg, co
 // [K/128][ntok_all][4] array.
 static bool make_dec_prob(DecProb& d, const GemvPlan& pl, int bits, int cdt, const void* A, int M, int K,
                           int N, const void* codes, const void* scales, int group, void* C, void* ws,
-                          const void* Sp = nullptr, int ntok_all = 0, int tok_base = 0, bool gs = false) {
+                          const void* Sp = nullptr, int ntok_all = 0, int tok_base = 0, bool gs = false,
+                          bool ds = false) {
   const uint64_t row_bytes = (uint64_t)K * bits / 8;
   if (!make_tmap_2d(&d.w, codes, 1, row_bytes, (uint64_t)N, row_bytes, wb_row(bits), kWBoxRows,
                     bits >= 4 ? 64 : 0))
     return false;
-  const int ks = wb_row(bits) * 8 / bits;  // K per stage
-  if (!make_tmap_2d(&d.a, A, 2, (uint64_t)K, (uint64_t)M, (uint64_t)K * 2, ks, pl.mt * 8, 0)) return false;
+  const int ks = wb_row(bits) * 8 / bits;  // K per 128-k chunk (one stage unless ds: two)
+  if (!make_tmap_2d(&d.a, A, 2, (uint64_t)K, (uint64_t)M, (uint64_t)K * 2, ks * (ds ? 2 : 1), pl.mt * 8, 0))
+    return false;
   d.tok_base = tok_base;
   if (Sp && !make_tmap_2d(&d.sm, reinterpret_cast<const char*>(Sp) + (size_t)tok_base * 16, 4, (uint64_t)M * 4,
-                          (uint64_t)(K / 128), (uint64_t)ntok_all * 16, pl.mt * 8 * 4, 1, 0))
+                          (uint64_t)(K / 128), (uint64_t)ntok_all * 16, pl.mt * 8 * 4, ds ? 2 : 1, 0))
     return false;
   // per-element-scale path (group does not cover a stage): stage the KS / group scale rows by TMA
   // when the group divides the stage (then a power of two >= 16), else read them from global memory
@@ -1223,7 +1277,7 @@ static bool make_dec_prob(DecProb& d, const GemvPlan& pl, int bits, int cdt, con
   d.sc_rows = (!sacc && ks % group == 0) ? ks / group : 0;
   d.sc_shift = d.sc_rows ? __builtin_ctz((unsigned)group) : 0;
   if (!make_tmap_2d(&d.s, scales, 2, (uint64_t)N, (uint64_t)(K / group), (uint64_t)N * 2, kWBoxRows,
-                    d.sc_rows ? d.sc_rows : (sacc == 2 ? 2 : 1), 0))
+                    d.sc_rows ? d.sc_rows : (sacc == 2 || ds ? 2 : 1), 0))
     return false;
   d.scales = scales;
   d.C = C;
@@ -1253,6 +1307,11 @@ cudaError_t run_gemv(const GemvPlan& pl, int adt, int cdt, int bits, const void*
                      int N, const void* codes, const void* scales, int group, void* C, void* ws,
                      cudaStream_t st, const XRPeers* xr_dev) {
   DecBatch<1> b{};
+#ifndef FQ_DEC_DS
+#define FQ_DEC_DS 1
+#endif
+  // double stages (two 128-k chunks per stage): int4 nibble path, one 8-token MMA tile, groups % 128
+  const bool ds = FQ_DEC_DS && bits == 4 && pl.mt == 1 && nib_of(bits, group, K) && sacc_of(bits, group, K) == 1;
   if (nib_of(bits, group, K)) {
     char* pre = reinterpret_cast<char*>(ws) + kCounterBytes +
                 (pl.splits > 1 ? align256((size_t)pl.splits * M * N * sizeof(float)) : 0);
@@ -1268,7 +1327,7 @@ cudaError_t run_gemv(const GemvPlan& pl, int adt, int cdt, int bits, const void*
 #endif
     if (r != cudaSuccess) return r;
     if (!make_dec_prob(b.p[0], pl, bits, cdt, pre, M, K, N, codes, scales, group, C, ws, Sp, M, 0,
-                       sacc_of(bits, group, K) == 2))
+                       sacc_of(bits, group, K) == 2, ds))
       return cudaErrorInvalidValue;
   } else if (!make_dec_prob(b.p[0], pl, bits, cdt, A, M, K, N, codes, scales, group, C, ws)) {
     return cudaErrorInvalidValue;
@@ -1283,7 +1342,7 @@ cudaError_t run_gemv(const GemvPlan& pl, int adt, int cdt, int bits, const void*
 #else
   const int dbg = 0;
 #endif
-  return dispatch_dec<1>(adt, bits, pl.mt, sacc_of(bits, group, K), dbg, b, ctas, st);
+  return dispatch_dec<1>(adt, bits, pl.mt, ds ? 3 : sacc_of(bits, group, K), dbg, b, ctas, st);
 }
 
 // ---- MoE batch (kernel A7, decode side): experts listed in `experts` (each with 1 <= M_e <= 16)
