@@ -343,7 +343,7 @@ __device__ __forceinline__ uint4 lowbit_words(uint32_t addr) {
 // {smid, start, first stage landed, main loop done, exit, producer past griddep_wait} --
 // read with fq_diag_timeline() (tools/dec_timeline.py).
 constexpr int kDiagCtas = 4096;
-__device__ unsigned long long g_diag_tl[kDiagCtas][6];
+__device__ unsigned long long g_diag_tl[kDiagCtas][8];
 __device__ __forceinline__ unsigned long long diag_now() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -509,7 +509,13 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
       // this launch depends on (programmatic dependent launch: the activations may still be in
       // flight from the previous kernel in the stream).
       const int npre = min(nst, NSTG);
+#ifdef FQ_DIAG
+      if (blockIdx.x < kDiagCtas) g_diag_tl[blockIdx.x][6] = diag_now();
+#endif
       for (int i = 0; i < npre; ++i) issue_w(i, i);
+#ifdef FQ_DIAG
+      if (blockIdx.x < kDiagCtas) g_diag_tl[blockIdx.x][7] = diag_now();
+#endif
 #ifndef FQ_DEC_EARLY_TRIGGER
 #define FQ_DEC_EARLY_TRIGGER 1
 #endif
@@ -1110,8 +1116,8 @@ __global__ void __launch_bounds__(128) prep_acts_kernel(const T* __restrict__ A,
 #ifdef FQ_DIAG
 extern "C" int fq_diag_timeline(unsigned long long* host, int nctas, int reset) {
   const int n = nctas < kDiagCtas ? nctas : kDiagCtas;
-  if (reset) return (int)cudaMemcpyToSymbol(g_diag_tl, host, (size_t)n * 6 * sizeof(unsigned long long));
-  return (int)cudaMemcpyFromSymbol(host, g_diag_tl, (size_t)n * 6 * sizeof(unsigned long long));
+  if (reset) return (int)cudaMemcpyToSymbol(g_diag_tl, host, (size_t)n * 8 * sizeof(unsigned long long));
+  return (int)cudaMemcpyFromSymbol(host, g_diag_tl, (size_t)n * 8 * sizeof(unsigned long long));
 }
 #endif
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }

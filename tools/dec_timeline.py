@@ -42,7 +42,7 @@ for name in a.shapes:
         for _ in range(20):
             fq.gemm(A, q, out=C, opts=o)
         torch.cuda.synchronize()
-        buf = np.zeros((4096, 6), dtype=np.uint64)
+        buf = np.zeros((4096, 8), dtype=np.uint64)
         assert lib.fq_diag_timeline(buf.ctypes.data, 4096, 1) == 0
         for _ in range(3):  # the last of three back-to-back launches (PDL overlap as in a real step)
             fq.gemm(A, q, out=C, opts=o)
@@ -50,12 +50,15 @@ for name in a.shapes:
         assert lib.fq_diag_timeline(buf.ctypes.data, 4096, 0) == 0
         n = int((buf[:, 1] > 0).sum())
         t = buf[:n].astype(np.int64)
-        sm, t0, tf, tl, te, tg = t[:, 0], t[:, 1], t[:, 2], t[:, 3], t[:, 4], t[:, 5]
+        sm, t0, tf, tl, te, tg, tp0, tp1 = (t[:, j] for j in range(8))
         base = t0.min()
+        nst_pre = 3
         w1 = (t0 - base) < 1000
         for lab, msk in (("wave1", w1), ("later", ~w1)):
             if msk.sum() == 0:
                 continue
+            print(f"  {lab}: producer start {pct((tp0 - t0)[msk], 50):.2f} us after CTA start, first {min(nst_pre, 9)} issues"
+                  f" {pct((tp1 - tp0)[msk], 50):.2f} us (p90 {pct((tp1 - tp0)[msk], 90):.2f}), griddep_wait {pct((tg - tp1)[msk], 50):.2f} us")
             print(f"  {lab}: {int(msk.sum())} CTAs; start->griddep {pct((tg - t0)[msk], 50):.2f} us,"
                   f" griddep->first stage {pct((tf - tg)[msk], 50):.2f} (p90 {pct((tf - tg)[msk], 90):.2f}) us,"
                   f" loop {pct((tl - tf)[msk], 50):.1f} us, epilogue {pct((te - tl)[msk], 50):.2f} us")
