@@ -70,7 +70,7 @@ struct DecGeom {
 
 // Stage = [packed weights 256 x 64 B][activations MT*8 x KS (TMA, then permuted in place by the
 // stager)][256 scales][per-token activation sums].  As many stages as fit two CTAs per SM.
-// SACC == 3 ("double stage", int4 nibble path, <= 8 tokens, groups % 128 == 0): TWO 128-k chunks per
+// SACC == 3 ("double stage", int4 nibble path, <= 16 tokens, groups % 128 == 0): TWO 128-k chunks per
 // stage -- two code boxes, one activation / sum / scale TMA each covering both chunks -- so the TMA
 // operations, barrier round trips and loop overhead per weight byte halve.  Its stages do not fit
 // the 1024-byte-rounded layout three times, so the code tiles of all stages form one ring (512-byte
@@ -385,7 +385,7 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
   // Nibble path: activations were pre-converted by prep_acts_kernel (fp16, fragment order) and
   // arrive by TMA with their per-chunk {correction, 2^-e}; there is no stager warp.
   constexpr bool NIB = FQ_NIB && BITS <= 4 && SACC;
-  static_assert(!DS || (NIB && BITS == 4 && MT == 1), "double stages: int4 nibble path, <= 8 tokens");
+  static_assert(!DS || (NIB && BITS == 4 && MT <= 2), "double stages: int4 nibble path, <= 16 tokens");
   // GS = 2 (int4, group 64, nibble path): each thread's four 8-code words come from the four 32-k
   // blocks of the stage (4 x LDS.32 instead of one LDS.128), so the MMAs of words 0-1 and 2-3 cover
   // the two 64-k groups separately; two exact partials per stage, folded with their own scales.
@@ -1231,7 +1231,7 @@ static cudaError_t dispatch_dec(int adt, int bits, int mt, int sacc, int dbg, co
   if (bits == BB && mt == MM && sacc == SS) return launch_dec<TT, BB, MM, SS, 0, MAXP>(b, ctas, st);
   if (adt == FQ_BF16) {
     FQ_DEC_CASE(__nv_bfloat16, 4, 1, 1) FQ_DEC_CASE(__nv_bfloat16, 4, 1, 0)
-    if constexpr (MAXP == 1) { FQ_DEC_CASE(__nv_bfloat16, 4, 1, 3) }
+    if constexpr (MAXP == 1) { FQ_DEC_CASE(__nv_bfloat16, 4, 1, 3) FQ_DEC_CASE(__nv_bfloat16, 4, 2, 3) }
     FQ_DEC_CASE(__nv_bfloat16, 4, 2, 1) FQ_DEC_CASE(__nv_bfloat16, 4, 2, 0)
     FQ_DEC_CASE(__nv_bfloat16, 4, 4, 1)
     FQ_DEC_CASE(__nv_bfloat16, 4, 1, 2) FQ_DEC_CASE(__nv_bfloat16, 4, 2, 2)
@@ -1243,7 +1243,7 @@ static cudaError_t dispatch_dec(int adt, int bits, int mt, int sacc, int dbg, co
     FQ_DEC_CASE(__nv_bfloat16, 2, 2, 1) FQ_DEC_CASE(__nv_bfloat16, 2, 2, 0) FQ_DEC_CASE(__nv_bfloat16, 2, 4, 1)
   } else {
     FQ_DEC_CASE(__half, 4, 1, 1) FQ_DEC_CASE(__half, 4, 1, 0)
-    if constexpr (MAXP == 1) { FQ_DEC_CASE(__half, 4, 1, 3) }
+    if constexpr (MAXP == 1) { FQ_DEC_CASE(__half, 4, 1, 3) FQ_DEC_CASE(__half, 4, 2, 3) }
     FQ_DEC_CASE(__half, 4, 2, 1) FQ_DEC_CASE(__half, 4, 2, 0)
     FQ_DEC_CASE(__half, 4, 4, 1)
     FQ_DEC_CASE(__half, 4, 1, 2) FQ_DEC_CASE(__half, 4, 2, 2)
@@ -1317,7 +1317,11 @@ cudaError_t run_gemv(const GemvPlan& pl, int adt, int cdt, int bits, const void*
 #define FQ_DEC_DS 1
 #endif
   // double stages (two 128-k chunks per stage): int4 nibble path, one 8-token MMA tile, groups % 128
-  const bool ds = FQ_DEC_DS && bits == 4 && pl.mt == 1 && nib_of(bits, group, K) && sacc_of(bits, group, K) == 1;
+#ifndef FQ_DEC_DS_MT
+#define FQ_DEC_DS_MT 2  // double stages up to two 8-token MMA tiles (MT = 2: 2 stages of 42 KB; -1.5 us at M = 9..16)
+#endif
+  const bool ds = FQ_DEC_DS && bits == 4 && pl.mt <= FQ_DEC_DS_MT && nib_of(bits, group, K) &&
+                  sacc_of(bits, group, K) == 1;
   if (nib_of(bits, group, K)) {
     char* pre = reinterpret_cast<char*>(ws) + kCounterBytes +
                 (pl.splits > 1 ? align256((size_t)pl.splits * M * N * sizeof(float)) : 0);
