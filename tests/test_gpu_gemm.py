@@ -94,6 +94,8 @@ def test_group_sizes_multi_tile_ragged(fq, bits, group):
     (5, 352, 256, 8, 32),      # int8 per-element path (128-k stages), K tail of 96
     (1, 96, 256, 4, 96),       # K shorter than one stage, one group per column
     (24, 1152, 392, 4, 128),   # four token tiles (nibble path), K = 4.5 stages
+    (1, 1152, 264, 4, 128),    # double stages (two 128-k chunks): K = 4.5 stages, chunk 1 of the last is past K
+    (12, 1152, 520, 4, 128),   # double stages, two MMA token tiles, ragged N
     (40, 1088, 264, 4, 64),    # tcgen05 path, K = 17 blocks of 64
     (200, 800, 136, 8, 32),    # tcgen05 path, K = 12.5 blocks
 ])
@@ -347,6 +349,25 @@ def test_opt175b_prefill_sampled(fq, shape, bits):
     r = O.quantize(Wc, bits, 128, O.BF16)
     Cr, D = O.gemm(A[torch.from_numpy(rows).cuda()].float().cpu().double().numpy(), r.q, r.s, 128)
     assert O.rel_err(torch_to_f64(C)[np.ix_(rows, cols)], Cr, D) <= TOL
+
+
+@pytest.mark.parametrize("M,K,N,group,splits", [
+    (1, 1152, 264, 384, None),   # groups of 3 chunks: chunk 1 of every other stage starts a group
+    (5, 1152, 264, 384, 3),      # splits start at k = 512 / 1024: chunk 1 / 2 of a group
+    (12, 2304, 520, 768, 2),     # two MMA token tiles, 6-chunk groups, second split starts at chunk 4
+    (8, 3840, 256, 640, 4),      # 5-chunk groups (not a power of two), splits start at chunks 8 / 16 / 24
+    (16, 2048, 296, 1024, 3),    # 8-chunk groups, splits start at chunks 6 / 12
+])
+def test_double_stage_group_phase(fq, env, M, K, N, group, splits):
+    """Double-stage decode (two 128-k chunks per stage, int4, groups % 128): the scale row of each
+    chunk follows the group boundaries whatever the split's first k (P:149 group-wise scales)."""
+    env("path", "decode")
+    if splits:
+        env("splits", splits)
+    Wb, Ab = make_case(M, K, N, 4, group, "bf16", seed=M + K + group, outliers=1)
+    _, C = run_case(fq, Wb, Ab, 4, group, "bf16", env=env)
+    Cr, D = oracle_ref(Wb, Ab, 4, group, "bf16")
+    assert O.rel_err(torch_to_f64(C), Cr, D) <= TOL
 
 
 @pytest.mark.parametrize("M,K,N,bits,group,adt,splits", [

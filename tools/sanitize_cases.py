@@ -26,6 +26,8 @@ print("adaptive g", g)
 for M in (1, 9, 24):
     run(M, 2048, 512, 4, 128)
 run(5, 2048, 512, 4, 64)                      # group-split nibble path
+run(2, 1152, 264, 4, 384, fq.make_opts("decode", 3))  # double stages: ragged K, mid-group split starts
+run(12, 1152, 264, 4, 128)                    # double stages, two MMA token tiles, K = 4.5 stages
 run(5, 2048, 512, 8, 128)                     # int8
 run(5, 2048, 520, 4, 32)                      # per-element-scale path, ragged N
 run(3, 4096, 512, 4, 128, fq.make_opts("decode", 3))  # split-K
