@@ -1231,7 +1231,7 @@ static cudaError_t dispatch_dec(int adt, int bits, int mt, int sacc, int dbg, co
   if (bits == BB && mt == MM && sacc == SS) return launch_dec<TT, BB, MM, SS, 0, MAXP>(b, ctas, st);
   if (adt == FQ_BF16) {
     FQ_DEC_CASE(__nv_bfloat16, 4, 1, 1) FQ_DEC_CASE(__nv_bfloat16, 4, 1, 0)
-    if constexpr (MAXP == 1) { FQ_DEC_CASE(__nv_bfloat16, 4, 1, 3) FQ_DEC_CASE(__nv_bfloat16, 4, 2, 3) }
+    FQ_DEC_CASE(__nv_bfloat16, 4, 1, 3) FQ_DEC_CASE(__nv_bfloat16, 4, 2, 3)
     FQ_DEC_CASE(__nv_bfloat16, 4, 2, 1) FQ_DEC_CASE(__nv_bfloat16, 4, 2, 0)
     FQ_DEC_CASE(__nv_bfloat16, 4, 4, 1)
     FQ_DEC_CASE(__nv_bfloat16, 4, 1, 2) FQ_DEC_CASE(__nv_bfloat16, 4, 2, 2)
@@ -1243,7 +1243,7 @@ static cudaError_t dispatch_dec(int adt, int bits, int mt, int sacc, int dbg, co
     FQ_DEC_CASE(__nv_bfloat16, 2, 2, 1) FQ_DEC_CASE(__nv_bfloat16, 2, 2, 0) FQ_DEC_CASE(__nv_bfloat16, 2, 4, 1)
   } else {
     FQ_DEC_CASE(__half, 4, 1, 1) FQ_DEC_CASE(__half, 4, 1, 0)
-    if constexpr (MAXP == 1) { FQ_DEC_CASE(__half, 4, 1, 3) FQ_DEC_CASE(__half, 4, 2, 3) }
+    FQ_DEC_CASE(__half, 4, 1, 3) FQ_DEC_CASE(__half, 4, 2, 3)
     FQ_DEC_CASE(__half, 4, 2, 1) FQ_DEC_CASE(__half, 4, 2, 0)
     FQ_DEC_CASE(__half, 4, 4, 1)
     FQ_DEC_CASE(__half, 4, 1, 2) FQ_DEC_CASE(__half, 4, 2, 2)
@@ -1297,6 +1297,16 @@ static bool make_dec_prob(DecProb& d, const GemvPlan& pl, int bits, int cdt, con
   return true;
 }
 
+#ifndef FQ_DEC_DS
+#define FQ_DEC_DS 1
+#endif
+#ifndef FQ_DEC_DS_MT
+#define FQ_DEC_DS_MT 2  // double stages up to two 8-token MMA tiles (MT = 2: 2 stages of 42 KB; -1.5 us at M = 9..16)
+#endif
+// double stages (kernel SACC == 3): int4 nibble path with one scale group per 128-k chunk, up to
+// FQ_DEC_DS_MT 8-token MMA tiles
+static bool ds_of(int bits, int mt, int sacc) { return FQ_DEC_DS && bits == 4 && sacc == 1 && mt <= FQ_DEC_DS_MT; }
+
 // scale path: 1 = one scale group per stage, 2 = two 64-k groups (group split), 0 = per element
 static int sacc_of(int bits, int group, int K = -1) {
   if (group % (bits <= 4 ? 128 : 64) == 0) return 1;
@@ -1313,15 +1323,8 @@ cudaError_t run_gemv(const GemvPlan& pl, int adt, int cdt, int bits, const void*
                      int N, const void* codes, const void* scales, int group, void* C, void* ws,
                      cudaStream_t st, const XRPeers* xr_dev) {
   DecBatch<1> b{};
-#ifndef FQ_DEC_DS
-#define FQ_DEC_DS 1
-#endif
   // double stages (two 128-k chunks per stage): int4 nibble path, one 8-token MMA tile, groups % 128
-#ifndef FQ_DEC_DS_MT
-#define FQ_DEC_DS_MT 2  // double stages up to two 8-token MMA tiles (MT = 2: 2 stages of 42 KB; -1.5 us at M = 9..16)
-#endif
-  const bool ds = FQ_DEC_DS && bits == 4 && pl.mt <= FQ_DEC_DS_MT && nib_of(bits, group, K) &&
-                  sacc_of(bits, group, K) == 1;
+  const bool ds = nib_of(bits, group, K) && ds_of(bits, pl.mt, sacc_of(bits, group, K));
   if (nib_of(bits, group, K)) {
     char* pre = reinterpret_cast<char*>(ws) + kCounterBytes +
                 (pl.splits > 1 ? align256((size_t)pl.splits * M * N * sizeof(float)) : 0);
@@ -1393,19 +1396,19 @@ cudaError_t run_gemv_grouped(int adt, int cdt, int bits, const void* A, int K, i
       const bool nib = nib_of(bits, groups[e]);
       const void* Ause = nib ? static_cast<const void*>(pre + (size_t)offsets[e] * K * 2) : static_cast<const void*>(Ae);
       if (!make_dec_prob(d, pl, bits, cdt, Ause, Me, K, N, codes[e], scales[e], groups[e], Ce, ws,
-                         nib ? Sp : nullptr, (int)T, (int)offsets[e]))
+                         nib ? Sp : nullptr, (int)T, (int)offsets[e], false, nib && ds_of(bits, mt, sacc)))
         return cudaErrorInvalidValue;
       d.cta_begin = ctas;
       ctas += d.gx * d.splits * d.ktiles;
       if (++b.nprob == kMaxBatch) {
-        cudaError_t r = dispatch_dec<kMaxBatch>(adt, bits, mt, sacc, 0, b, ctas, st);
+        cudaError_t r = dispatch_dec<kMaxBatch>(adt, bits, mt, ds_of(bits, mt, sacc) ? 3 : sacc, 0, b, ctas, st);
         if (r != cudaSuccess) return r;
         b.nprob = 0;
         ctas = 0;
       }
     }
     if (b.nprob) {
-      cudaError_t r = dispatch_dec<kMaxBatch>(adt, bits, mt, sacc, 0, b, ctas, st);
+      cudaError_t r = dispatch_dec<kMaxBatch>(adt, bits, mt, ds_of(bits, mt, sacc) ? 3 : sacc, 0, b, ctas, st);
       if (r != cudaSuccess) return r;
     }
   }
@@ -1449,7 +1452,8 @@ cudaError_t run_gemv_grouped_dev(int adt, int cdt, int bits, const void* A, int6
         DecProb& d = b.p[b.nprob];
         const bool nib = nib_of(bits, groups[e]);
         if (!make_dec_prob(d, pl, bits, cdt, nib ? static_cast<const void*>(pre) : A, (int)T, K, N, codes[e],
-                           scales[e], groups[e], C, ws, nib ? Sp : nullptr, (int)T, 0))
+                           scales[e], groups[e], C, ws, nib ? Sp : nullptr, (int)T, 0, false,
+                           nib && ds_of(bits, mt, sacc)))
           return cudaErrorInvalidValue;
         d.M = t1 - t0;
         d.tskip = t0;
@@ -1461,14 +1465,14 @@ cudaError_t run_gemv_grouped_dev(int adt, int cdt, int bits, const void* A, int6
         d.cta_begin = ctas;
         ctas += d.gx * d.ktiles;
         if (++b.nprob == kMaxBatch) {
-          cudaError_t r = dispatch_dec<kMaxBatch>(adt, bits, mt, sacc, 0, b, ctas, st);
+          cudaError_t r = dispatch_dec<kMaxBatch>(adt, bits, mt, ds_of(bits, mt, sacc) ? 3 : sacc, 0, b, ctas, st);
           if (r != cudaSuccess) return r;
           b.nprob = 0;
           ctas = 0;
         }
       }
       if (b.nprob) {
-        cudaError_t r = dispatch_dec<kMaxBatch>(adt, bits, mt, sacc, 0, b, ctas, st);
+        cudaError_t r = dispatch_dec<kMaxBatch>(adt, bits, mt, ds_of(bits, mt, sacc) ? 3 : sacc, 0, b, ctas, st);
         if (r != cudaSuccess) return r;
       }
     }
