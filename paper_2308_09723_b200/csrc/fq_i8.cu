@@ -604,6 +604,252 @@ __global__ void __launch_bounds__(i8_threads(DG), CPS) gemm_i8_kernel(const __gr
   }
 }
 
+
+// ---------------------------------------------------------------- decode (M <= 16): legacy IMMA
+// Decode sizes stream every weight once per call and are bound by HBM, not by the tensor core, so
+// the tcgen05 kernel above (one 128-row UMMA per 64 weights x 16 k, N padded to 32) is not needed
+// there.  This kernel is the bf16 decode kernel's structure (fq_gemv.cu: TMA producer warp, 8
+// consumer warps x 32 weight rows, 256-row CTA tiles, 128-k stages, split-K with a deterministic
+// last-arriver fixup) on the integer path: each code word becomes the biased u8 weights q z + 128
+// with one LOP3 + one IMAD per 4 codes (as above), and mma.sync m16n8k32 u8 x s8 -> s32 takes 32 k
+// per instruction (twice bf16's m16n8k16).  The whole K accumulates exactly in int32 (no per-group
+// fold: z is inside the weights); the epilogue removes 128 * rowsum and applies s_a * sigma once.
+// MMA k-slot mapping (k-step j of a 128-k stage): thread t's slots 4t..4t+3 hold the even k of the
+// 8-k block 4t + j and slots 16+4t..16+4t+3 its odd k -- exactly the k-interleaved words of both the
+// code nibbles (low / high nibbles) and fq_quantize_acts_i8's a_q layout.
+constexpr int kDecRows = 256;
+constexpr int kDecWarps = 8;
+constexpr int kDecThreads = 32 * (1 + kDecWarps);
+template <int MT>
+struct DecI8Geo {
+  static constexpr int CODE = kDecRows * 64;  // [256 rows][64 B] int4, SWIZZLE_64B
+  static constexpr int ACT = MT * 8 * 128;    // [MT*8 tokens][128 B] int8, SWIZZLE_128B
+  static constexpr int ZB = 4 * kDecRows;     // up to 4 z rows [4][256] u8 (groups of 32)
+  static constexpr int PER = ((CODE + ACT + ZB + 1023) / 1024) * 1024;
+  static constexpr int N0 = (115712 - 2048) / PER;
+  static constexpr int N = N0 > 8 ? 8 : N0;
+  static constexpr int SMEM = N * PER + 1024;
+};
+struct DecI8Prob {
+  CUtensorMap a;  // a_q [M][K] int8, box [128 B][MT*8 rows], SWIZZLE_128B
+  CUtensorMap q;  // codes [N][K/2], box [64 B][256 rows], SWIZZLE_64B
+  CUtensorMap z;  // z [G][N] u8, box [256 cols][zr rows]
+  const float* sa;
+  const int32_t* rowsum;
+  const float* sigma;
+  void* C;
+  int32_t* ws;    // split-K int32 partials [splits][M][N]
+  int* ctr;       // per column tile, self-resetting
+  int M, K, N, group, cdt, zr, gx, splits, klen;
+};
+
+__device__ __forceinline__ void imma16832(int (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int MT>
+__global__ void __launch_bounds__(kDecThreads, 2) decode_i8_kernel(const __grid_constant__ DecI8Prob p) {
+  using G = DecI8Geo<MT>;
+  constexpr int NSTG = G::N;
+  extern __shared__ __align__(1024) uint8_t dsmem[];
+  __shared__ __align__(8) uint64_t full_bar[8], empty_bar[8];
+  __shared__ int s_last;
+  uint8_t* sbase = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsmem) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bx = (int)blockIdx.x % p.gx, by = (int)blockIdx.x / p.gx;
+  const int n0 = bx * kDecRows;
+  const int kbeg = by * p.klen, kend = min(p.K, kbeg + p.klen);
+  const int nst = (kend - kbeg) / 128;  // K % 128 == 0 (ABI)
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSTG; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], kDecWarps);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&p.q);
+    prefetch_tmap(&p.z);
+    prefetch_tmap(&p.a);
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (one lane)
+    if (lane == 0) {
+      const uint64_t polw = policy_evict_first(), pola = policy_evict_last();
+      auto issue_w = [&](int i, int s) {
+        uint8_t* st = sbase + s * G::PER;
+        const int k0 = kbeg + i * 128;
+        mbar_arrive_expect_tx(&full_bar[s], G::CODE + G::ACT + p.zr * kDecRows);
+        tma_load_2d(st, &p.q, &full_bar[s], k0 / 2, n0, polw);
+        tma_load_2d(st + G::CODE + G::ACT, &p.z, &full_bar[s], n0, k0 / p.group, polw);
+      };
+      auto issue_a = [&](int i, int s) {
+        tma_load_2d(sbase + s * G::PER + G::CODE, &p.a, &full_bar[s], kbeg + i * 128, 0, pola);
+      };
+      // weights and z are constants: requested before the wait for the activation quantizer
+      const int npre = min(nst, NSTG);
+      for (int i = 0; i < npre; ++i) issue_w(i, i);
+      griddep_launch_dependents();
+      griddep_wait();
+      for (int i = 0; i < npre; ++i) issue_a(i, i);
+      int s = npre % NSTG;
+      uint32_t ph = npre == NSTG ? 1u : 0u;
+      for (int i = npre; i < nst; ++i) {
+        mbar_wait(&empty_bar[s], ph ^ 1);
+        issue_w(i, s);
+        issue_a(i, s);
+        if (++s == NSTG) { s = 0; ph ^= 1; }
+      }
+    }
+    return;
+  }
+
+  // --------------------------------------------------------------------------- consumers
+  const int cw = warp - 1, gq = lane >> 2, t = lane & 3;
+  uint32_t wofs[2][2], zofs[2][2];  // [row tile][g / h]: byte offsets in a stage
+  const int zrow = p.group < 128 ? (32 * t) / p.group : 0;  // staged z row of this thread's 32-k block
+#pragma unroll
+  for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int R = cw * 32 + rt * 16 + gq + 8 * h;
+      wofs[rt][h] = R * 64 + ((t ^ ((R >> 1) & 3)) << 4);  // SWIZZLE_64B: cell t of row R
+      zofs[rt][h] = G::CODE + G::ACT + zrow * kDecRows + R;
+    }
+  uint32_t aofs[MT][2];  // the thread's 32 B (cells 2t, 2t+1) of token mt*8+gq, SWIZZLE_128B
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int tok = mt * 8 + gq;
+      aofs[mt][c] = G::CODE + tok * 128 + (((2 * t + c) ^ (tok & 7)) << 4);
+    }
+  int acc[2][MT][4];
+#pragma unroll
+  for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[rt][mt][i] = 0;
+
+  const uint32_t sb = smem_u32(sbase);
+  int s = 0;
+  uint32_t ph = 0;
+  for (int i = 0; i < nst; ++i) {
+    mbar_wait(&full_bar[s], ph);
+    const uint32_t st = sb + s * G::PER;
+    uint4 w[2][2];
+    uint32_t zz[2][2];
+    uint4 b[MT][2];
+#pragma unroll
+    for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        w[rt][h] = lds128(st + wofs[rt][h]);
+        zz[rt][h] = lds_u8(st + zofs[rt][h]);
+      }
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) b[mt][c] = lds128(st + aofs[mt][c]);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[s]);  // operands in registers: hand the slot back
+#pragma unroll
+    for (int rt = 0; rt < 2; ++rt) {
+      uint32_t zm[2], bias[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        zm[h] = zz[rt][h];
+        bias[h] = (128u - 8u * zm[h]) * 0x01010101u;  // u z + 128 - 8 z = q z + 128 per byte
+      }
+      const uint32_t wg[4] = {w[rt][0].x, w[rt][0].y, w[rt][0].z, w[rt][0].w};
+      const uint32_t wh[4] = {w[rt][1].x, w[rt][1].y, w[rt][1].z, w[rt][1].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        // u = q + 8 per nibble: even k in the low nibbles, odd k in the high nibbles
+        const uint32_t elo_g = lop3_and_xor(wg[j], 0x0F0F0F0Fu, 0x08080808u);
+        const uint32_t ehi_g = lop3_and_xor(wg[j] >> 4, 0x0F0F0F0Fu, 0x08080808u);
+        const uint32_t elo_h = lop3_and_xor(wh[j], 0x0F0F0F0Fu, 0x08080808u);
+        const uint32_t ehi_h = lop3_and_xor(wh[j] >> 4, 0x0F0F0F0Fu, 0x08080808u);
+        const uint32_t a[4] = {elo_g * zm[0] + bias[0], elo_h * zm[1] + bias[1], ehi_g * zm[0] + bias[0],
+                               ehi_h * zm[1] + bias[1]};
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          // block 4t + j of token mt*8 + gq: even-k word 2j, odd-k word 2j + 1 of the thread's 32 B
+          const uint4 v = b[mt][j >> 1];
+          const uint32_t b0 = (j & 1) ? v.z : v.x, b1 = (j & 1) ? v.w : v.y;
+          imma16832(acc[rt][mt], a, b0, b1);
+        }
+      }
+    }
+    if (++s == NSTG) { s = 0; ph ^= 1; }
+  }
+
+  // ------------------------------------------------------------- epilogue (+ split-K fixup)
+  auto store = [&](int tok, int n, int32_t v) {
+    const float f = (float)(v - 128 * __ldg(p.rowsum + tok)) * __ldg(p.sa + tok) * __ldg(p.sigma + n);
+    const size_t o = (size_t)tok * p.N + n;
+    if (p.cdt == FQ_FP32) reinterpret_cast<float*>(p.C)[o] = f;
+    else if (p.cdt == FQ_BF16) reinterpret_cast<__nv_bfloat16*>(p.C)[o] = __float2bfloat16_rn(f);
+    else reinterpret_cast<__half*>(p.C)[o] = __float2half_rn(f);
+  };
+  auto out_idx = [&](int rt, int mt, int i, int& n, int& tok) {
+    n = n0 + cw * 32 + rt * 16 + gq + ((i >> 1) ? 8 : 0);
+    tok = mt * 8 + 2 * t + (i & 1);
+  };
+  if (p.splits == 1) {
+#pragma unroll
+    for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          int n, tok;
+          out_idx(rt, mt, i, n, tok);
+          if (n < p.N && tok < p.M) store(tok, n, acc[rt][mt][i]);
+        }
+    return;
+  }
+  int32_t* part = p.ws + (size_t)by * p.M * p.N;
+#pragma unroll
+  for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        int n, tok;
+        out_idx(rt, mt, i, n, tok);
+        if (n < p.N && tok < p.M) __stcg(part + (size_t)tok * p.N + n, acc[rt][mt][i]);
+      }
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * kDecWarps));
+  int* ctr = p.ctr + bx;
+  if (threadIdx.x == 32) {
+    __threadfence();
+    const int last = atomicAdd(ctr, 1) == p.splits - 1;
+    if (last) __threadfence();
+    s_last = last;
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * kDecWarps));
+  if (!s_last) return;
+  {
+    const int n = n0 + (int)threadIdx.x - 32;  // consumer thread = column (coalesced)
+    if (n < p.N) {
+      for (int tok = 0; tok < min(p.M, MT * 8); ++tok) {
+        int32_t v = 0;
+        for (int sp = 0; sp < p.splits; ++sp) v += __ldcg(p.ws + ((size_t)sp * p.M + tok) * p.N + n);
+        store(tok, n, v);
+      }
+    }
+  }
+  if (threadIdx.x == 32) *ctr = 0;  // self-reset for the next call / graph replay
+}
+
 }  // namespace i8
 
 // ------------------------------------------------------------------------------------- host side
@@ -670,7 +916,19 @@ static int i8_splits(int M, int K, int N, int* kbs_out) {
   return (kblocks + kbs - 1) / kbs;
 }
 
+#ifndef FQ_I8_IMMA
+#define FQ_I8_IMMA 1  // decode sizes (M <= 16) on the mma.sync m16n8k32 u8 x s8 kernel
+#endif
+static bool i8_imma(int M) { return FQ_I8_IMMA && M <= 16; }
+static GemvPlan i8_dec_plan(int M, int K, int N, int group) {
+  return plan_gemv(M, K, N, 4, group, num_sms());  // same split plan as the bf16 decode kernel
+}
+
 size_t gemm_i8_workspace_bytes(int M, int K, int N) {
+  if (i8_imma(M)) {
+    const GemvPlan pl = i8_dec_plan(M, K, N, 128);
+    return pl.splits > 1 ? kI8CounterBytes + (size_t)pl.splits * M * N * sizeof(int32_t) : 256;
+  }
   const int s = i8_splits(M, K, N, nullptr);
   if (s == 1) return 256;
   const int bn = i8_bn(M);
@@ -688,10 +946,50 @@ static cudaError_t launch_i8(const i8::I8Prob& p, cudaStream_t st) {
                     Gm::SMEM, st, p);
 }
 
+template <int MT>
+static cudaError_t launch_dec_i8(const i8::DecI8Prob& d, int ctas, cudaStream_t st) {
+  constexpr int smem = i8::DecI8Geo<MT>::SMEM;
+  cudaError_t e = ensure_smem_attr<i8::decode_i8_kernel<MT>>(smem);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(i8::decode_i8_kernel<MT>, ctas, i8::kDecThreads, smem, st, d);
+}
+
+static cudaError_t run_dec_i8(const void* Aq, const float* sa, const int32_t* rowsum, int M, int K, int N,
+                              int group, const void* codes, const void* z, const float* sigma, void* C, int cdt,
+                              void* ws, size_t ws_bytes, cudaStream_t st) {
+  i8::DecI8Prob d{};
+  const int mt = M <= 8 ? 1 : 2;
+  d.zr = group < 128 ? 128 / group : 1;
+  if (!make_tmap_2d(&d.a, Aq, 1, (uint64_t)K, (uint64_t)M, (uint64_t)K, 128, mt * 8, 128)) return cudaErrorInvalidValue;
+  if (!make_tmap_2d(&d.q, codes, 1, (uint64_t)K / 2, (uint64_t)N, (uint64_t)K / 2, 64, i8::kDecRows, 64))
+    return cudaErrorInvalidValue;
+  if (!make_tmap_2d(&d.z, z, 1, (uint64_t)N, (uint64_t)(K / group), (uint64_t)N, i8::kDecRows, d.zr, 0))
+    return cudaErrorInvalidValue;
+  d.sa = sa;
+  d.rowsum = rowsum;
+  d.sigma = sigma;
+  d.C = C;
+  d.M = M; d.K = K; d.N = N; d.group = group; d.cdt = cdt;
+  d.gx = (N + i8::kDecRows - 1) / i8::kDecRows;
+  const GemvPlan pl = i8_dec_plan(M, K, N, group);
+  d.splits = 1;
+  d.klen = K;
+  const size_t need = kI8CounterBytes + (size_t)pl.splits * M * N * sizeof(int32_t);
+  if (pl.splits > 1 && ws && ws_bytes >= need && d.gx <= (int)(kI8CounterBytes / sizeof(int))) {
+    d.splits = pl.splits;
+    d.klen = pl.klen;
+    d.ctr = reinterpret_cast<int*>(ws);
+    d.ws = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(ws) + kI8CounterBytes);
+  }
+  const int ctas = d.gx * d.splits;
+  return mt == 1 ? launch_dec_i8<1>(d, ctas, st) : launch_dec_i8<2>(d, ctas, st);
+}
+
 cudaError_t run_gemm_i8(const void* Aq, const float* sa, const int32_t* rowsum, int M, int K, int N, int group,
                         const void* codes,
                         const void* z, const float* sigma, void* C, int cdt, void* ws, size_t ws_bytes,
                         cudaStream_t st) {
+  if (i8_imma(M)) return run_dec_i8(Aq, sa, rowsum, M, K, N, group, codes, z, sigma, C, cdt, ws, ws_bytes, st);
   i8::I8Prob p{};
   p.bn = i8_bn(M);
   if (!make_tmap_2d(&p.a, Aq, 1, (uint64_t)K, (uint64_t)M, (uint64_t)K, i8::BK, p.bn, 128)) return cudaErrorInvalidValue;

@@ -109,6 +109,9 @@ CASES = [
     (33, 1024, 272, 256), (64, 2048, 384, 64), (100, 4096, 128, 4096), (128, 1024, 1024, 128),
     (129, 512, 256, 32), (200, 6144, 512, 128), (256, 2048, 640, 64), (300, 1024, 384, 128),
     (640, 4096, 256, 128), (1000, 512, 1152, 512),
+    # decode sizes on the mma.sync m16n8k32 u8 x s8 kernel: two token tiles, ragged column tile,
+    # 32- / 64-k groups (4 / 2 staged z rows), split-K with long K, groups of 3 stages
+    (9, 2048, 784, 32), (12, 12288, 1024, 64), (2, 4096, 4096, 256), (8, 3072, 400, 384), (13, 1024, 16, 128),
 ]
 
 
