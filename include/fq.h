@@ -257,7 +257,7 @@ fq_status fq_gemm_grouped_dev(const void* A, int32_t adt, int64_t T, const int64
  *     order in which the GEMM unpacks int4 codes, so its dequantization needs no byte shuffles.
  *     (IEEE fp32 division); a non-finite row gets s_a 0, codes 0 and sets status bit 0.  The GEMM
  *     feeds the weights to the tensor core as unsigned bytes q*z + 128 and removes 128*rowsum[m].
- *   GEMM (fq_gemm_i8, tcgen05 kind::i8):
+ *   GEMM (fq_gemm_i8; M <= 16: mma.sync m16n8k32 u8 x s8 decode kernel, else tcgen05 kind::i8):
  *     acc[m,n] = sum_k a_q[m,k] * q[n,k] * z[k/group, n]   (exact int32)
  *     C[m,n]   = fp32(acc) * s_a[m] * sigma[n], rounded to cdt (BF16, FP16 or FP32)   C: [M, N]
  *   ws: fq_gemm_i8_workspace_bytes(M, K, N) bytes, zero-filled once (64 KiB of self-resetting
