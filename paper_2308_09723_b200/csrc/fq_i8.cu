@@ -839,12 +839,25 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode_i8_kernel(const __grid_
   if (!s_last) return;
   {
     const int n = n0 + (int)threadIdx.x - 32;  // consumer thread = column (coalesced)
-    if (n < p.N) {
-      for (int tok = 0; tok < min(p.M, MT * 8); ++tok) {
+    if (n < p.N && p.M <= 4) {  // few tokens: one token at a time (measured faster at M = 1)
+      for (int tok = 0; tok < p.M; ++tok) {
         int32_t v = 0;
         for (int sp = 0; sp < p.splits; ++sp) v += __ldcg(p.ws + ((size_t)sp * p.M + tok) * p.N + n);
         store(tok, n, v);
       }
+    } else if (n < p.N) {
+      // all tokens of one split in flight per round (integer sums: exact in any order)
+      int32_t v[MT * 8];
+#pragma unroll
+      for (int tok = 0; tok < MT * 8; ++tok) v[tok] = 0;
+      for (int sp = 0; sp < p.splits; ++sp) {
+#pragma unroll
+        for (int tok = 0; tok < MT * 8; ++tok)
+          if (tok < p.M) v[tok] += __ldcg(p.ws + ((size_t)sp * p.M + tok) * p.N + n);
+      }
+#pragma unroll
+      for (int tok = 0; tok < MT * 8; ++tok)
+        if (tok < p.M) store(tok, n, v[tok]);
     }
   }
   if (threadIdx.x == 32) *ctr = 0;  // self-reset for the next call / graph replay
