@@ -160,6 +160,12 @@ __global__ void __launch_bounds__(1024) quantize_acts_i8_kernel(const T* __restr
                                                                int32_t* status) {
   __shared__ float red[32];
   __shared__ int redi[32];
+#ifndef FQ_I8_EARLY_TRIGGER
+#define FQ_I8_EARLY_TRIGGER 1
+#endif
+  // The GEMM that follows may launch at once and stream its (constant) weights while this runs; it
+  // reads a_q / s_a / rowsum only after its own griddep_wait (this grid complete).
+  if (FQ_I8_EARLY_TRIGGER) griddep_launch_dependents();
   griddep_wait();  // A may be the previous kernel's output
   const int m = blockIdx.x;
   const T* row = A + (size_t)m * K;
@@ -209,7 +215,7 @@ __global__ void __launch_bounds__(1024) quantize_acts_i8_kernel(const T* __restr
     for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += redi[i];
     rowsum[m] = t;
   }
-  griddep_launch_dependents();
+  if (!FQ_I8_EARLY_TRIGGER) griddep_launch_dependents();
 }
 
 // ---------------------------------------------------------------- tcgen05 kind::i8 GEMM
