@@ -221,6 +221,9 @@ __device__ __forceinline__ void i4_pairs_off(uint32_t w, uint32_t (&q)[4]) {
 #ifndef FQ_NIB
 #define FQ_NIB 1
 #endif
+#ifndef FQ_FOLD2
+#define FQ_FOLD2 1  // the prep kernel stores -2^-e * correction; the fold is two FFMAs per output
+#endif
 template <typename T> struct Nib;
 template <> struct Nib<__nv_bfloat16> {
   static constexpr uint32_t lo = 0x43084308u, hi = 0x43804380u, sixteenth = 0x3D803D80u;
@@ -818,6 +821,16 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
           for (int mt = 0; mt < MT; ++mt) {
             const float(&pp)[4] = part[gi][mt];
             float p0 = pp[0], p1 = pp[1], p2 = pp[2], p3 = pp[3];
+            if (NIB && FQ_FOLD2) {
+              // S' holds -2^-e * correction: t = 2^-e p - 2^-e corr = 2^-e (p - corr) exactly (power
+              // of two), then acc += s * t -- the same two roundings as (s 2^-e) (p - corr), two
+              // instructions per output instead of three
+              acc[rt][mt][0] = fmaf(o.sg[rt][gi], fmaf(o.iv[mt].x, p0, o.sa[mt][gi].x), acc[rt][mt][0]);
+              acc[rt][mt][1] = fmaf(o.sg[rt][gi], fmaf(o.iv[mt].y, p1, o.sa[mt][gi].y), acc[rt][mt][1]);
+              acc[rt][mt][2] = fmaf(o.sh[rt][gi], fmaf(o.iv[mt].x, p2, o.sa[mt][gi].x), acc[rt][mt][2]);
+              acc[rt][mt][3] = fmaf(o.sh[rt][gi], fmaf(o.iv[mt].y, p3, o.sa[mt][gi].y), acc[rt][mt][3]);
+              continue;
+            }
             if (OFF != 0.f) {  // remove OFF * sum_k a[tok, k] (tokens 2t, 2t+1 of this MMA tile)
               p0 = fmaf(-OFF, o.sa[mt][gi].x, p0);
               p1 = fmaf(-OFF, o.sa[mt][gi].y, p1);
@@ -1109,7 +1122,13 @@ __global__ void __launch_bounds__(128) prep_acts_kernel(const T* __restrict__ A,
   const int kl = l * 8, tq = kl >> 5, w16 = (kl & 31) >> 3;
   const int cell = (MODE == 1 ? l : (w16 * 4 + tq)) ^ ((tok & 1) << 2);
   *reinterpret_cast<uint4*>(Ap + base + cell * 8) = o;
-  if (l == 0) *reinterpret_cast<float4*>(Sp + ((size_t)ch * ntok + tok) * 4) = make_float4(sum, inv, half_sum, other);
+  if (l == 0) {
+    if (FQ_FOLD2)  // corrections pre-multiplied by -2^-e (exact: power of two)
+      *reinterpret_cast<float4*>(Sp + ((size_t)ch * ntok + tok) * 4) =
+          make_float4(-sum * inv, inv, -half_sum * inv, -other * inv);
+    else
+      *reinterpret_cast<float4*>(Sp + ((size_t)ch * ntok + tok) * 4) = make_float4(sum, inv, half_sum, other);
+  }
 }
 
 // ------------------------------------------------------------------------------------- host side
