@@ -745,7 +745,10 @@ __device__ __forceinline__ void imma16832(int (&d)[4], const uint32_t (&a)[4], u
 }
 
 template <int MT>
-__global__ void __launch_bounds__(kDecThreads, 2) decode_i8_kernel(const __grid_constant__ DecI8Prob p) {
+// two 9-warp CTAs per SM: <= 96 registers (18 warps put 5 on some sub-partition's 16K register bank).
+// (Four 8-token tiles for 17..32 tokens were measured: FC2 M = 17..32 82-86 us vs 73-78 us on the
+// tcgen05 kernel, FC1 equal -- so the IMMA kernel stops at 16 tokens.)
+__global__ void __maxnreg__(96) decode_i8_kernel(const __grid_constant__ DecI8Prob p) {
   using G = DecI8Geo<MT>;
   constexpr int NSTG = G::N;
   extern __shared__ __align__(1024) uint8_t dsmem[];
