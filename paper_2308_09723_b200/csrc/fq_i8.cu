@@ -713,11 +713,15 @@ __global__ void __launch_bounds__(i8_threads(DG), CPS) gemm_i8_kernel(const __gr
 constexpr int kDecRows = 256;
 constexpr int kDecWarps = 8;
 constexpr int kDecThreads = 32 * (1 + kDecWarps);
-template <int MT>
+// NC 128-k chunks per stage (2: the code, activation and z TMAs of two chunks share one barrier
+// round trip, as in the bf16 kernel's double stages)
+template <int MT, int NC>
 struct DecI8Geo {
-  static constexpr int CODE = kDecRows * 64;  // [256 rows][64 B] int4, SWIZZLE_64B
-  static constexpr int ACT = MT * 8 * 128;    // [MT*8 tokens][128 B] int8, SWIZZLE_128B
-  static constexpr int ZB = 4 * kDecRows;     // up to 4 z rows [4][256] u8 (groups of 32)
+  static constexpr int CODE1 = kDecRows * 64;  // one chunk: [256 rows][64 B] int4, SWIZZLE_64B
+  static constexpr int ACT1 = MT * 8 * 128;    // one chunk: [MT*8 tokens][128 B] int8, SWIZZLE_128B
+  static constexpr int CODE = NC * CODE1;
+  static constexpr int ACT = NC * ACT1;
+  static constexpr int ZB = 4 * NC * kDecRows;  // up to 4 NC z rows [.][256] u8 (groups of 32)
   static constexpr int PER = ((CODE + ACT + ZB + 1023) / 1024) * 1024;
   static constexpr int N0 = (115712 - 2048) / PER;
   static constexpr int N = N0 > 8 ? 8 : N0;
@@ -744,13 +748,14 @@ __device__ __forceinline__ void imma16832(int (&d)[4], const uint32_t (&a)[4], u
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-template <int MT>
+template <int MT, int NC>
 // two 9-warp CTAs per SM: <= 96 registers (18 warps put 5 on some sub-partition's 16K register bank).
 // (Four 8-token tiles for 17..32 tokens were measured: FC2 M = 17..32 82-86 us vs 73-78 us on the
 // tcgen05 kernel, FC1 equal -- so the IMMA kernel stops at 16 tokens.)
 __global__ void __maxnreg__(96) decode_i8_kernel(const __grid_constant__ DecI8Prob p) {
-  using G = DecI8Geo<MT>;
+  using G = DecI8Geo<MT, NC>;
   constexpr int NSTG = G::N;
+  constexpr int KST = 128 * NC;  // K per stage
   extern __shared__ __align__(1024) uint8_t dsmem[];
   __shared__ __align__(8) uint64_t full_bar[8], empty_bar[8];
   __shared__ int s_last;
@@ -759,7 +764,7 @@ __global__ void __maxnreg__(96) decode_i8_kernel(const __grid_constant__ DecI8Pr
   const int bx = (int)blockIdx.x % p.gx, by = (int)blockIdx.x / p.gx;
   const int n0 = bx * kDecRows;
   const int kbeg = by * p.klen, kend = min(p.K, kbeg + p.klen);
-  const int nst = (kend - kbeg) / 128;  // K % 128 == 0 (ABI)
+  const int nst = (kend - kbeg + KST - 1) / KST;  // K % 128 == 0 (ABI); a past-K chunk is TMA zero fill
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSTG; ++s) {
       mbar_init(&full_bar[s], 1);
@@ -780,13 +785,17 @@ __global__ void __maxnreg__(96) decode_i8_kernel(const __grid_constant__ DecI8Pr
       const uint64_t polw = policy_evict_first(), pola = policy_evict_last();
       auto issue_w = [&](int i, int s) {
         uint8_t* st = sbase + s * G::PER;
-        const int k0 = kbeg + i * 128;
+        const int k0 = kbeg + i * KST;
         mbar_arrive_expect_tx(&full_bar[s], G::CODE + G::ACT + p.zr * kDecRows);
-        tma_load_2d(st, &p.q, &full_bar[s], k0 / 2, n0, polw);
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+          tma_load_2d(st + c * G::CODE1, &p.q, &full_bar[s], (k0 + 128 * c) / 2, n0, polw);
         tma_load_2d(st + G::CODE + G::ACT, &p.z, &full_bar[s], n0, k0 / p.group, polw);
       };
       auto issue_a = [&](int i, int s) {
-        tma_load_2d(sbase + s * G::PER + G::CODE, &p.a, &full_bar[s], kbeg + i * 128, 0, pola);
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+          tma_load_2d(sbase + s * G::PER + G::CODE + c * G::ACT1, &p.a, &full_bar[s], kbeg + i * KST + 128 * c, 0, pola);
       };
       // weights and z are constants: requested before the wait for the activation quantizer
       const int npre = min(nst, NSTG);
@@ -808,15 +817,14 @@ __global__ void __maxnreg__(96) decode_i8_kernel(const __grid_constant__ DecI8Pr
 
   // --------------------------------------------------------------------------- consumers
   const int cw = warp - 1, gq = lane >> 2, t = lane & 3;
-  uint32_t wofs[2][2], zofs[2][2];  // [row tile][g / h]: byte offsets in a stage
-  const int zrow = p.group < 128 ? (32 * t) / p.group : 0;  // staged z row of this thread's 32-k block
+  uint32_t wofs[2][2], zofs[2][2];  // [row tile][g / h]: byte offsets in a stage (z: row 0)
 #pragma unroll
   for (int rt = 0; rt < 2; ++rt)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int R = cw * 32 + rt * 16 + gq + 8 * h;
       wofs[rt][h] = R * 64 + ((t ^ ((R >> 1) & 3)) << 4);  // SWIZZLE_64B: cell t of row R
-      zofs[rt][h] = G::CODE + G::ACT + zrow * kDecRows + R;
+      zofs[rt][h] = G::CODE + G::ACT + R;
     }
   uint32_t aofs[MT][2];  // the thread's 32 B (cells 2t, 2t+1) of token mt*8+gq, SWIZZLE_128B
 #pragma unroll
@@ -837,9 +845,16 @@ __global__ void __maxnreg__(96) decode_i8_kernel(const __grid_constant__ DecI8Pr
   const uint32_t sb = smem_u32(sbase);
   int s = 0;
   uint32_t ph = 0;
+  // staged z row of this thread's 32-k block in chunk c: (k0 + 128 c + 32 t) / g - k0 / g; for groups
+  // >= 128 that needs k0 mod g, tracked per stage (kmod)
+  const int g = p.group;
+  int kmod = kbeg % g;
   for (int i = 0; i < nst; ++i) {
     mbar_wait(&full_bar[s], ph);
     const uint32_t st = sb + s * G::PER;
+#pragma unroll
+    for (int ch = 0; ch < NC; ++ch) {
+    const int zrow = g <= 128 ? (128 * ch + 32 * t) / g : (kmod + 128 * ch + 32 * t) / g;
     uint4 w[2][2];
     uint32_t zz[2][2];
     uint4 b[MT][2];
@@ -847,15 +862,17 @@ __global__ void __maxnreg__(96) decode_i8_kernel(const __grid_constant__ DecI8Pr
     for (int rt = 0; rt < 2; ++rt)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        w[rt][h] = lds128(st + wofs[rt][h]);
-        zz[rt][h] = lds_u8(st + zofs[rt][h]);
+        w[rt][h] = lds128(st + ch * G::CODE1 + wofs[rt][h]);
+        zz[rt][h] = lds_u8(st + zofs[rt][h] + zrow * kDecRows);
       }
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-      for (int c = 0; c < 2; ++c) b[mt][c] = lds128(st + aofs[mt][c]);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_bar[s]);  // operands in registers: hand the slot back
+      for (int c = 0; c < 2; ++c) b[mt][c] = lds128(st + ch * G::ACT1 + aofs[mt][c]);
+    if (ch == NC - 1) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[s]);  // operands in registers: hand the slot back
+    }
 #pragma unroll
     for (int rt = 0; rt < 2; ++rt) {
       uint32_t zm[2], bias[2];
@@ -884,6 +901,8 @@ __global__ void __maxnreg__(96) decode_i8_kernel(const __grid_constant__ DecI8Pr
         }
       }
     }
+    }  // chunk
+    if (g > 128) { kmod += KST; while (kmod >= g) kmod -= g; }
     if (++s == NSTG) { s = 0; ph ^= 1; }
   }
 
@@ -1070,12 +1089,16 @@ static cudaError_t launch_i8(const i8::I8Prob& p, cudaStream_t st) {
                     Gm::SMEM, st, p);
 }
 
+#ifndef FQ_I8_DEC_NC
+#define FQ_I8_DEC_NC 2  // 128-k chunks per stage of the IMMA decode kernel
+#endif
 template <int MT>
 static cudaError_t launch_dec_i8(const i8::DecI8Prob& d, int ctas, cudaStream_t st) {
-  constexpr int smem = i8::DecI8Geo<MT>::SMEM;
-  cudaError_t e = ensure_smem_attr<i8::decode_i8_kernel<MT>>(smem);
+  constexpr int NC = FQ_I8_DEC_NC;
+  constexpr int smem = i8::DecI8Geo<MT, NC>::SMEM;
+  cudaError_t e = ensure_smem_attr<i8::decode_i8_kernel<MT, NC>>(smem);
   if (e != cudaSuccess) return e;
-  return launch_pdl(i8::decode_i8_kernel<MT>, ctas, i8::kDecThreads, smem, st, d);
+  return launch_pdl(i8::decode_i8_kernel<MT, NC>, ctas, i8::kDecThreads, smem, st, d);
 }
 
 static cudaError_t run_dec_i8(const void* Aq, const float* sa, const int32_t* rowsum, int M, int K, int N,
@@ -1083,7 +1106,8 @@ static cudaError_t run_dec_i8(const void* Aq, const float* sa, const int32_t* ro
                               void* ws, size_t ws_bytes, cudaStream_t st) {
   i8::DecI8Prob d{};
   const int mt = M <= 8 ? 1 : 2;
-  d.zr = group < 128 ? 128 / group : 1;
+  // z rows staged per stage: every group a stage touches (groups >= the stage: the first two)
+  d.zr = group < 128 * FQ_I8_DEC_NC ? 128 * FQ_I8_DEC_NC / group : (FQ_I8_DEC_NC > 1 ? 2 : 1);
   if (!make_tmap_2d(&d.a, Aq, 1, (uint64_t)K, (uint64_t)M, (uint64_t)K, 128, mt * 8, 128)) return cudaErrorInvalidValue;
   if (!make_tmap_2d(&d.q, codes, 1, (uint64_t)K / 2, (uint64_t)N, (uint64_t)K / 2, 64, i8::kDecRows, 64))
     return cudaErrorInvalidValue;

@@ -112,6 +112,8 @@ CASES = [
     # decode sizes on the mma.sync m16n8k32 u8 x s8 kernel: two token tiles, ragged column tile,
     # 32- / 64-k groups (4 / 2 staged z rows), split-K with long K, groups of 3 stages
     (9, 2048, 784, 32), (12, 12288, 1024, 64), (2, 4096, 4096, 256), (8, 3072, 400, 384), (13, 1024, 16, 128),
+    # two-chunk stages: K % 256 == 128 (the last stage's second chunk is past K), groups straddling stages
+    (4, 1152, 272, 128), (11, 1920, 400, 384), (1, 2432, 512, 32),
 ]
 
 
