@@ -388,7 +388,7 @@ decode_kernel(const __grid_constant__ DecBatch<MAXP> batch) {
   // Nibble path: activations were pre-converted by prep_acts_kernel (fp16, fragment order) and
   // arrive by TMA with their per-chunk {correction, 2^-e}; there is no stager warp.
   constexpr bool NIB = FQ_NIB && BITS <= 4 && SACC;
-  static_assert(!DS || (NIB && BITS == 4 && MT <= 2), "double stages: int4 nibble path, <= 16 tokens");
+  static_assert(!DS || (NIB && BITS >= 2 && BITS <= 4 && MT <= 2), "double stages: int4/3/2 nibble path, <= 16 tokens");
   // GS = 2 (int4, group 64, nibble path): each thread's four 8-code words come from the four 32-k
   // blocks of the stage (4 x LDS.32 instead of one LDS.128), so the MMAs of words 0-1 and 2-3 cover
   // the two 64-k groups separately; two exact partials per stage, folded with their own scales.
@@ -1260,6 +1260,7 @@ static cudaError_t dispatch_dec(int adt, int bits, int mt, int sacc, int dbg, co
     FQ_DEC_CASE(__nv_bfloat16, 3, 2, 1) FQ_DEC_CASE(__nv_bfloat16, 3, 2, 0) FQ_DEC_CASE(__nv_bfloat16, 3, 4, 1)
     FQ_DEC_CASE(__nv_bfloat16, 2, 1, 1) FQ_DEC_CASE(__nv_bfloat16, 2, 1, 0)
     FQ_DEC_CASE(__nv_bfloat16, 2, 2, 1) FQ_DEC_CASE(__nv_bfloat16, 2, 2, 0) FQ_DEC_CASE(__nv_bfloat16, 2, 4, 1)
+    FQ_DEC_CASE(__nv_bfloat16, 3, 2, 3) FQ_DEC_CASE(__nv_bfloat16, 2, 2, 3)
   } else {
     FQ_DEC_CASE(__half, 4, 1, 1) FQ_DEC_CASE(__half, 4, 1, 0)
     FQ_DEC_CASE(__half, 4, 1, 3) FQ_DEC_CASE(__half, 4, 2, 3)
@@ -1272,6 +1273,7 @@ static cudaError_t dispatch_dec(int adt, int bits, int mt, int sacc, int dbg, co
     FQ_DEC_CASE(__half, 3, 2, 1) FQ_DEC_CASE(__half, 3, 2, 0) FQ_DEC_CASE(__half, 3, 4, 1)
     FQ_DEC_CASE(__half, 2, 1, 1) FQ_DEC_CASE(__half, 2, 1, 0)
     FQ_DEC_CASE(__half, 2, 2, 1) FQ_DEC_CASE(__half, 2, 2, 0) FQ_DEC_CASE(__half, 2, 4, 1)
+    FQ_DEC_CASE(__half, 3, 2, 3) FQ_DEC_CASE(__half, 2, 2, 3)
   }
 #undef FQ_DEC_CASE
   return cudaErrorInvalidValue;
@@ -1324,7 +1326,13 @@ static bool make_dec_prob(DecProb& d, const GemvPlan& pl, int bits, int cdt, con
 #endif
 // double stages (kernel SACC == 3): int4 nibble path with one scale group per 128-k chunk, up to
 // FQ_DEC_DS_MT 8-token MMA tiles
-static bool ds_of(int bits, int mt, int sacc) { return FQ_DEC_DS && bits == 4 && sacc == 1 && mt <= FQ_DEC_DS_MT; }
+#ifndef FQ_DEC_DS_LOWBIT
+#define FQ_DEC_DS_LOWBIT 1  // int3 / int2 bit streams at 9..16 tokens (measured: -4 / -5 us at M = 16,
+#endif                      // +0.5..2 us at M <= 8, where they keep single stages)
+static bool ds_of(int bits, int mt, int sacc) {
+  const bool lowbit = FQ_DEC_DS_LOWBIT && (bits == 3 || bits == 2) && mt == 2;
+  return FQ_DEC_DS && (bits == 4 || lowbit) && sacc == 1 && mt <= FQ_DEC_DS_MT;
+}
 
 // scale path: 1 = one scale group per stage, 2 = two 64-k groups (group split), 0 = per element
 static int sacc_of(int bits, int group, int K = -1) {
