@@ -77,7 +77,7 @@ def test_quantize_intscale_nonfinite_and_zero_columns(fq):
 
 
 @pytest.mark.parametrize("adt", ["bf16", "fp16", "fp32"])
-@pytest.mark.parametrize("M,K", [(1, 128), (7, 4096), (64, 12288)])
+@pytest.mark.parametrize("M,K", [(1, 128), (7, 4096), (64, 12288), (3, 1000), (65, 256), (16, 49152)])
 def test_quantize_acts_bit_exact(fq, adt, M, K):
     Ab = activations_bits(M, K, 40 + M, dtype=adt)
     A = bits_to_torch(Ab, adt)
